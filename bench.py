@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""Frames/s of the online per-frame MM reconstruction loop on B200.
+
+Default workload = BASELINE.json configs[1] ("c2"): one 256x256 complex64
+cine phantom slice, T=200 frames, R=20, lambda=0.05, Fixed mu=0.01,
+informative row sampling at 4x (K=64 trials incl. 16 forced centre lines,
+beta=0.1, Philox draws). One bench *step* = the whole T-frame online
+sequence from the same initial state: per frame [row scores -> Philox draw
+-> gather y -> Gram/ridge -> k-space factor update] in one persistent
+cluster-kernel launch, then the inverse column FFTs of the per-frame factors
+and the reconstruction of all T image frames (4 launches of our kernels).
+
+`value`  = frames reconstructed per second over all ranks (device time,
+           inputs resident, L2 flushed between steps).
+`e2e`    = the same through the public call `run_online` with the truth
+           k-space in pinned host memory (H2D) and the reconstructions +
+           per-frame reports read back (D2H) inside the timed region.
+`--impl reference` times the CPU oracle port of the reference algorithm
+(numpy SVD ridge etc.) on the host cores for a bounded sample.
+Multi-GPU (torchrun): one independent C2 replica per rank (the single-slice
+config does not shard), `scaling: weak`. `--config c3` runs
+the 64-slice config sharded over ranks (no collective, `scaling: strong`).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+METRIC = "frames/sec reconstructed (online per-frame update) and % HBM roofline, 1–8 B200"
+
+
+def center_lines(n, m):
+    return tuple(list(range(m // 2)) + list(range(n - m // 2, n)))
+
+
+CONFIGS = {
+    "c2": dict(n=256, R=20, T=200, lam=0.05, period=20.0, K=64, forced=center_lines(256, 16), beta=0.1, mu=0.01,
+               slices=1, desc="config 2: 256x256 complex64 cine phantom, T=200, R=20, lambda=0.05, informative "
+                              "rows K=64 (4x) incl. 16 centre lines, beta=0.1, Philox draws, Fixed mu=0.01"),
+    "c3": dict(n=256, R=16, T=100, lam=0.05, period=16.0, K=52, forced=(0,), beta=0.1, mu=0.01, slices=64,
+               desc="config 3: 64 independent 256x256 slices, T=100, R=16, 20% informative rows (K=52, forced DC)"),
+}
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ data
+def make_data(cfg, slice_ids, seed=2024):
+    from paper_1609_04104_b200.phantom import cine_phantom
+
+    ks, cl = [], []
+    for s in slice_ids:
+        ph = cine_phantom(cfg["n"], cfg["n"], cfg["T"], period=cfg["period"], seed=seed, slice_index=s)
+        ks.append(ph.kspace)
+        cl.append(ph.clean)
+    return np.stack(ks, axis=1), np.stack(cl, axis=1)  # (T, ns, n, n)
+
+
+def init_factors(cfg, slice_ids, seed=7):
+    A, B = [], []
+    for s in slice_ids:
+        rng = np.random.default_rng([seed, s])
+        a = (rng.standard_normal((cfg["n"], cfg["R"])) + 1j * rng.standard_normal((cfg["n"], cfg["R"]))) / np.sqrt(2 * cfg["n"])
+        b = (rng.standard_normal((cfg["n"], cfg["R"])) + 1j * rng.standard_normal((cfg["n"], cfg["R"]))) / np.sqrt(2 * cfg["n"])
+        A.append(a)
+        B.append(b)
+    return np.stack(A), np.stack(B)
+
+
+def measured_peaks():
+    p = os.path.join(HERE, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), float(d.get("sm_max_mhz", 1965.0)), "measured"
+    return 6650.0, 1965.0, "fallback"
+
+
+# ------------------------------------------------------------------ CPU oracle (reference arm / cpu_baseline)
+def cpu_oracle_fps(cfg, frames, ks, A0, B0):
+    from oracle import tt_oracle as O
+
+    pol = {"kind": "informative", "k": cfg["K"], "forced": list(cfg["forced"]), "beta": cfg["beta"], "key": (2024, 0)}
+    t0 = time.perf_counter()
+    O.online_run(ks[:frames, 0], A0[0], B0[0], cfg["lam"], ("fixed", cfg["mu"]), pol)
+    dt = time.perf_counter() - t0
+    return frames / dt, dt
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    frames = args.ref_frames
+    ks, _ = make_data(dict(cfg, T=frames), [0])
+    A0, B0 = init_factors(cfg, [0])
+    for _ in range(args.warmup):
+        cpu_oracle_fps(cfg, max(1, frames // 4), ks, A0, B0)
+    times = []
+    for _ in range(args.steps):
+        fps, dt = cpu_oracle_fps(cfg, frames, ks, A0, B0)
+        times.append(dt)
+    total = sum(times)
+    value = frames * args.steps / total
+    cores = os.cpu_count()
+    line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "config": {"workload": cfg["desc"], "frames_per_step": frames, "parallelism": "cpu"},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "frames/s", "cores": cores, "kind": "port",
+                             "sample": f"first {frames} frames of the {args.config} sequence per step, oracle port "
+                                       "of the reference algorithm (numpy/OpenBLAS, all host threads)"},
+            "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1609_04104_b200 as tt
+    from paper_1609_04104_b200 import _lib as L
+    from paper_1609_04104_b200 import _ops as K
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    L.load()
+
+    # slices of this rank: replicas for c2 (weak), shards for c3 (strong)
+    if cfg["slices"] == 1:
+        slice_ids = [rank]
+        scaling = "weak"
+    else:
+        per = cfg["slices"] // world
+        slice_ids = list(range(rank * per, (rank + 1) * per))
+        scaling = "strong"
+    ns = len(slice_ids)
+    n, R, T = cfg["n"], cfg["R"], cfg["T"]
+    ks_np, clean_np = make_data(cfg, slice_ids)
+    A0, B0 = init_factors(cfg, slice_ids)
+
+    pol = tt.Informative(k=cfg["K"], forced=cfg["forced"], beta=cfg["beta"], key0=2024, key1=slice_ids[0])
+    eng = tt.OnlineEngine(n, n, R, ns, cfg["lam"], tt.Fixed(cfg["mu"]), pol, cluster=args.cluster)
+    eng.set_image_factors(A0, B0)
+    ah0, bh0 = eng.ah.clone(), eng.bh.clone()
+    ahf, bhf = torch.empty_like(ah0), torch.empty_like(bh0)
+    ks = torch.from_numpy(ks_np).to(dev)
+    out = eng.make_outputs(T, history=True)
+    X = torch.empty(T * ns, n, n, dtype=torch.complex64, device=dev)
+    rows_args = eng.args(ks, T, out, ah_in=ah0, bh_in=bh0, ah_out=ahf, bh_out=bhf, frame0=0, t0=1)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    lib = L.lib()
+    stream = torch.cuda.current_stream()
+
+    def reset():
+        eng.philox_pos.zero_()
+        eng.alpha_bar.zero_()
+
+    def step_kernels():
+        K.track_rows(rows_args)                                   # 1: fused online loop, T frames
+        K.fft_cols_(out["ah"], inverse=True)                      # 2: A_t = F^-1 Ah_t (all frames)
+        K.fft_cols_(out["bh"], inverse=True)                      # 3: B_t = F^-1 Bh_t
+        L.check(lib.tt_reconstruct(stream.cuda_stream, T * ns, n, n, R, out["ah"].data_ptr(),
+                                   out["bh"].data_ptr(), out["gamma"].data_ptr(), X.data_ptr()), "reconstruct")  # 4
+    launches_per_step = 4
+
+    for _ in range(args.warmup):
+        reset()
+        step_kernels()
+    torch.cuda.synchronize()
+    eng.check_status()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()          # L2 flush (256 MB write), outside the timed events
+            reset()
+            e0, e1, e2 = ev[i]
+            e0.record(stream)
+            K.track_rows(rows_args)
+            e1.record(stream)
+            K.fft_cols_(out["ah"], inverse=True)
+            K.fft_cols_(out["bh"], inverse=True)
+            L.check(lib.tt_reconstruct(stream.cuda_stream, T * ns, n, n, R, out["ah"].data_ptr(),
+                                       out["bh"].data_ptr(), out["gamma"].data_ptr(), X.data_ptr()), "reconstruct")
+            e2.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(c) for a, b, c in ev]
+    track_ms = [a.elapsed_time(b) for a, b, c in ev]
+    total_ms = sum(step_ms)
+    tot = torch.tensor([total_ms, sum(track_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    total_ms, track_total = float(tot[0]), float(tot[1])
+    eng.check_status()
+    frames_all = T * cfg["slices"] * (world if cfg["slices"] == 1 else 1) * args.steps
+    value = frames_all / (total_ms / 1e3)
+
+    # ---- quality (outside timing): NRMSE of the last step's reconstructions
+    Xr = X.reshape(T, ns, n, n)
+    cl = torch.from_numpy(clean_np).to(dev)
+    nmse = ((cl - Xr).abs().pow(2).sum((-1, -2)) / cl.abs().pow(2).sum((-1, -2))).double()
+    cnt = out["cnt"].double()
+
+    # ---- roofline of the dominant kernel (tt_rows_kernel) from the BASELINE byte model
+    S_avg = float(cnt.mean())
+    b_upd = 8 * S_avg * n + 4 * S_avg + 16 * R * (2 * n) + 8 * R + 8 * n       # per slice-frame
+    b_rec = 8 * n * n
+    f_sep = 16 * S_avg * n * R + 16 * (S_avg + n) * R * R + 10 * R * 2 * n * math.log2(n) + 16 * R * 2 * n
+    hbm_peak, sm_max, peak_kind = measured_peaks()
+    track_s = track_total / 1e3 / args.steps
+    achieved = b_upd * T * ns / track_s / 1e9
+    fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12
+    traffic = None
+    prof = os.path.join(HERE, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+
+    # ---- e2e through the public API with pinned host buffers
+    e2e = None
+    h2d = d2h = 0
+    if not args.no_e2e:
+        ks_pin = torch.from_numpy(ks_np).pin_memory()
+        for _ in range(1):
+            tt.run_online(ks_pin, A0, B0, cfg["lam"], tt.Fixed(cfg["mu"]), pol, cluster=args.cluster)
+        torch.cuda.synchronize()
+        t_e2e = []
+        for _ in range(max(1, args.steps)):
+            t0 = time.perf_counter()
+            res = tt.run_online(ks_pin, A0, B0, cfg["lam"], tt.Fixed(cfg["mu"]), pol, cluster=args.cluster)
+            torch.cuda.synchronize()
+            t_e2e.append(time.perf_counter() - t0)
+        h2d = ks_np.nbytes
+        d2h = res.recon.nbytes + res.gamma.nbytes + res.cost.nbytes + res.mu.nbytes + 4 * (T * ns * (eng.max_rows + 1))
+        et = torch.tensor([sum(t_e2e)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": T * ns * (world if cfg["slices"] == 1 else 1) * len(t_e2e) / float(et[0]), "unit": "frames/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "call": "paper_1609_04104_b200.run_online(pinned host kspace) -> host recon/reports"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        fr = args.cpu_frames
+        fps, dt = cpu_oracle_fps(cfg, fr, ks_np, A0, B0)
+        cpu = {"value": fps, "unit": "frames/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"first {fr} frames of slice 0 ({dt:.1f} s), oracle port of the reference algorithm "
+                         "(numpy SVD ridge, pocketfft), all host threads"}
+
+    if world > 1:
+        dist.destroy_process_group()
+    if rank != 0:
+        return 0
+    line = {
+        "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": scaling,
+        "vs_baseline": None, "dtype": "c64", "data": "synthetic",
+        "config": {"workload": cfg["desc"], "frames_per_step": T, "slices_per_gpu": ns, "rank": R,
+                   "nx": n, "ny": n, "cluster_ctas_per_slice": eng.cluster, "l2": "flushed between steps (256 MB write)",
+                   "parallelism": f"{'replicas' if cfg['slices'] == 1 else 'slice-shard'} x{world}"},
+        "gpu_launches": launches_per_step * args.steps,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": traffic, "kernel": "tt_rows_kernel",
+                     "bytes_per_slice_frame": b_upd, "peak_kind": peak_kind},
+        "extra": {"track_ms_per_step": track_total / args.steps,
+                  "us_per_frame_tracking": 1e6 * track_s / T,
+                  "step_hbm_frac": (b_upd + b_rec) * value / 1e9 / hbm_peak / (1 if cfg["slices"] == 1 else 1),
+                  "fp32_frac_tracking": f_sep * T * ns / track_s / 1e12 / fp32_peak,
+                  "mean_nrmse": float(nmse.sqrt().mean()), "last_nrmse": float(nmse[-1].sqrt().mean()),
+                  "rows_per_frame_avg": S_avg},
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--cluster", type=int, default=0)
+    ap.add_argument("--cpu-frames", type=int, default=100)
+    ap.add_argument("--ref-frames", type=int, default=8)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

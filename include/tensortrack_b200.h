@@ -1,0 +1,184 @@
+/*
+ * tensortrack_b200 — C ABI of the B200-native online tensor-subspace tracker.
+ *
+ * Drop-in boundary for the hot path of the reference package `tensortrack`
+ * (arXiv 1609.04104 reference, /root/reference/pkg/src/tensortrack). The
+ * reference has no FFI of its own: its boundary is the Python function API
+ * (`__init__.py:3-62`). These entry points are what that API binds to; the
+ * Python mirror lives in `paper_1609_04104_b200/` and the ctypes binding a
+ * maintainer would add is shown in INTEGRATION.md.
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers unless stated otherwise.
+ *  - complex64 arrays are interleaved (re, im) float pairs; complex128 are
+ *    interleaved doubles.
+ *  - Factor matrices are row-major (N, R) per slice: [nslices][N][R].
+ *  - "k-space factors" Ah = F_x A, Bh = F_y B (ortho, unshifted DFT down the
+ *    columns, observation.py:225-226). The row-mask step runs on them; the
+ *    image-domain factors are A = F_x^-1 Ah (tt_fft_cols, inverse=1).
+ *  - Every call is asynchronous on `stream` (a cudaStream_t passed as void*),
+ *    takes no locks, never aborts, and returns a status code:
+ *      TT_OK          0  success
+ *      TT_EINVAL      1  invalid argument  -> ValueError   (observation.py:41-55)
+ *      TT_EUNSUPPORTED 2 unsupported shape/descriptor -> TypeError (tracker.py:238)
+ *      TT_ENONFINITE  3  non-finite result -> NumericalError (experiment.py:66)
+ *      TT_ECUDA       4  CUDA error        -> RuntimeError
+ *    Device-side problems (bad row ids in a table, non-finite gamma) are
+ *    OR-ed into the caller's `status` array (TT_ST_* bits) for a later read.
+ *  - tt_last_error() returns a thread-local message for the last failure.
+ */
+#ifndef TENSORTRACK_B200_H
+#define TENSORTRACK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { TT_OK = 0, TT_EINVAL = 1, TT_EUNSUPPORTED = 2, TT_ENONFINITE = 3, TT_ECUDA = 4 };
+
+/* device status bits */
+enum { TT_ST_BADROW = 1, TT_ST_DUPROW = 2, TT_ST_NONFINITE = 4, TT_ST_ZEROCOL = 8, TT_ST_OVERFLOW = 16 };
+
+enum { TT_POLICY_STATIC = 0, TT_POLICY_INFORMATIVE = 1 };
+enum { TT_Y_GATHER = 0, TT_Y_PACKED = 1 };
+enum { TT_STEP_FIXED = 0, TT_STEP_HESSIAN = 1 };
+
+const char* tt_version(void);
+const char* tt_last_error(void);
+
+/* ------------------------------------------------------------------ FFT
+ * Batched ortho 1-D DFT down the columns of `batch` row-major (n x ncols)
+ * complex64 matrices, in place. inverse=0: F (np.fft.fft(.., axis=0,
+ * norm="ortho")); inverse=1: F^-1. Replaces observation.py:225-226 (build_phi
+ * Fourier branch) and the x/y inverse transforms inside _scatter_theta
+ * (tracker.py:186-188) by the separable identity F(a b^T) = (F a)(F b)^T.
+ * Power-of-two n <= 4096 use shared-memory radix-2 Stockham passes; other n
+ * use a direct DFT (exact same convention). */
+int tt_fft_cols(void* stream, float* data, int n, int ncols, int batch, int inverse);
+
+/* ------------------------------------------------------------------ row-mask step
+ * Persistent fused online step for Cartesian row masks (the path of
+ * tracker.track_step with a FourierMask whose indices are full phase-encode
+ * lines, tracker.py:367-411, and of experiment.run_adaptive's per-frame body,
+ * experiment.py:482-530). One thread-block cluster of `cluster` CTAs per
+ * slice runs `frames` consecutive frames: [informative draw] -> gather y ->
+ * separable Gram/rhs -> fp64 LDL^H ridge solve -> Lipschitz/fixed step ->
+ * k-space factor update. State stays resident in shared memory across frames.
+ */
+typedef struct tt_rows_args {
+  int32_t nslices, nx, ny, rank, frames, max_rows, cluster;
+  int64_t t0;                 /* tracker time of frame 0 (same for every slice) */
+  const float* ah_in;         /* [nslices][nx][rank] complex64 k-space factors */
+  const float* bh_in;         /* [nslices][ny][rank] */
+  float* ah_out;              /* may alias ah_in */
+  float* bh_out;              /* may alias bh_in */
+  double* alpha_bar;          /* [nslices] in/out (HessianBound running sum) */
+  int32_t policy;             /* TT_POLICY_* */
+  const int32_t* rows_tab;    /* static: [frames][nslices][max_rows] */
+  const int32_t* rows_cnt;    /* static: [frames][nslices] */
+  int32_t k_draws;            /* informative: trials K (forced lines count) */
+  const int32_t* forced;      /* informative: sorted unique forced rows */
+  int32_t nforced;
+  double beta;                /* uniform blend weight (sampler.py:32) */
+  uint64_t key0, key1;        /* Philox key; slice s draws with (key0, key1 + s) */
+  uint64_t* philox_pos;       /* [nslices] stream positions, in/out */
+  int32_t y_mode;             /* TT_Y_* */
+  const float* ysrc;          /* GATHER: truth k-space, frame f slice s row i at
+                                 ysrc + (f*y_frame_stride + s*y_slice_stride + i*ny)*2
+                                 PACKED: [frames][nslices][max_rows][ny] */
+  int64_t y_frame_stride, y_slice_stride; /* complex elements (GATHER) */
+  double lam;
+  int32_t step_mode;          /* TT_STEP_* */
+  double mu, c_floor, c_cap;
+  float* gamma_out;           /* [frames][nslices][rank] complex64 or NULL */
+  double* cost_out;           /* [frames][nslices] or NULL */
+  double* mu_out;             /* [frames][nslices] or NULL */
+  double* alpha_out;          /* [frames][nslices] or NULL */
+  int32_t* rows_out;          /* [frames][nslices][max_rows] or NULL */
+  int32_t* cnt_out;           /* [frames][nslices] or NULL */
+  float* resid_out;           /* [frames][nslices][max_rows][ny] complex64 or NULL */
+  float* ah_hist;             /* [frames][nslices][nx][rank] post-update or NULL */
+  float* bh_hist;             /* [frames][nslices][ny][rank] or NULL */
+  int32_t* status;            /* [nslices] OR-ed TT_ST_* bits */
+  void* scratch;              /* tt_rows_scratch_bytes() bytes */
+} tt_rows_args;
+
+/* Choose the cluster size (if *cluster <= 0) and report the dynamic shared
+ * memory per CTA; TT_EUNSUPPORTED if no cluster size fits. */
+int tt_rows_plan(int nx, int ny, int rank, int max_rows, int policy, int* cluster, size_t* smem_bytes);
+size_t tt_rows_scratch_bytes(int nslices, int nx, int ny, int rank, int max_rows, int cluster);
+int tt_track_rows(void* stream, const tt_rows_args* a);
+
+/* ------------------------------------------------------------------ generic index step
+ * One frame of tracker.track_step for an arbitrary (i, j) index list
+ * (FourierMask / EntryMask, observation.py:58-90) on measurement-domain
+ * factors: Gram over |Omega| samples (fp64), ridge solve, residual, dense
+ * back-projection P = Xi conj(Bh), Q = Xi^T conj(Ah) (the collapsed form of
+ * tracker.py:176-228), closed-form Lipschitz bound, update. */
+typedef struct tt_entries_args {
+  int32_t nx, ny, rank, nmeas;
+  int64_t t;
+  const float* ah_in;
+  const float* bh_in;
+  float* ah_out;
+  float* bh_out;
+  double* alpha_bar;          /* [1] */
+  const int32_t* idx;         /* [nmeas][2] (i, j) */
+  const float* y;             /* [nmeas] complex64 */
+  double lam;
+  int32_t step_mode;
+  double mu, c_floor, c_cap;
+  float* gamma_out;           /* [rank] */
+  double* cost_out;           /* [1] */
+  double* mu_out;             /* [1] */
+  double* alpha_out;          /* [1] */
+  float* resid_out;           /* [nmeas] or NULL */
+  int32_t* status;            /* [1] */
+  void* scratch;
+} tt_entries_args;
+size_t tt_entries_scratch_bytes(int nx, int ny, int rank, int nmeas);
+int tt_track_entries(void* stream, const tt_entries_args* a);
+
+/* ------------------------------------------------------------------ sampling
+ * row_scores (sampler.py:115-128) on the factor `a` ([nslices][nx][rank]):
+ * s(i) = (ny e_i + R)/(R (nx + ny)), e_i = sum_r |a_ir|^2/||a_r||^2,
+ * normalised, blended with beta/nx, renormalised; fp64 out [nslices][nx]. */
+int tt_row_scores(void* stream, int nslices, int nx, int ny, int rank, const float* a, double beta,
+                  double* probs_out, int32_t* status);
+/* entry_scores (sampler.py:95-112): [nx][ny] fp64 */
+int tt_entry_scores(void* stream, int nx, int ny, int rank, const float* a, const float* b, double beta,
+                    double* probs_out, int32_t* status);
+/* draw_samples(replacement=True) (sampler.py:146-162): k - nforced draws of
+ * Generator(Philox(key)).choice(n, p=probs) at stream positions pos[s]..,
+ * union with forced -> sorted unique rows. Bit-exact with numpy for the
+ * same probabilities (sequential fp64 cumsum semantics). */
+int tt_draw_with_replacement(void* stream, int nslices, int n, const double* probs, int k,
+                             const int32_t* forced, int nforced, uint64_t key0, uint64_t key1,
+                             uint64_t* pos, int32_t* omega_out, int32_t* count_out);
+/* weighted_draw_without_replacement (observation.py:279-297): k sequential
+ * renormalised draws, draw order; consumes k uniforms from pos[0]. */
+int tt_draw_without_replacement(void* stream, int n, const double* weights, int k, uint64_t key0,
+                                uint64_t key1, uint64_t* pos, int32_t* out, int32_t* status);
+
+/* ------------------------------------------------------------------ values
+ * Reconstruction X_f = A_f diag(gamma_f) B_f^T (core.py:91-104,
+ * mri.py:107-121), batched over frames: a [frames][nx][rank],
+ * b [frames][ny][rank], gamma [frames][rank] -> x [frames][nx][ny]. */
+int tt_reconstruct(void* stream, int frames, int nx, int ny, int rank, const float* a, const float* b,
+                   const float* gamma, float* x_out);
+/* rebalance (core.py:138-166) in place on [nslices][n][rank] factor pairs. */
+int tt_rebalance(void* stream, int nslices, int nx, int ny, int rank, float* a, float* b, int32_t* status);
+/* solve_gamma (tracker.py:139-156) for a dense complex128 Phi [L][R]:
+ * (Phi^H Phi + lam I)^-1 Phi^H y in fp64 (LDL^H); gamma_out complex128 [R].
+ * scratch: tt_solve_scratch_bytes(R). */
+size_t tt_solve_scratch_bytes(int L, int R);
+int tt_solve_gamma(void* stream, int L, int R, const double* phi, const double* y, double lam, double* gamma_out,
+                   void* scratch);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TENSORTRACK_B200_H */

@@ -1,0 +1,60 @@
+"""tensortrack_b200 — B200-native online tensor-subspace tracking for
+dynamic MRI (arXiv 1609.04104), a drop-in for the hot path of the reference
+package ``tensortrack`` (`pkg/src/tensortrack/__init__.py:3-62`).
+
+The public names mirror the reference modules; the arithmetic runs in the
+sm_100a CUDA library ``libtensortrack_b200.so`` (C ABI in
+``include/tensortrack_b200.h``). There is no CPU fallback: importing works
+anywhere, but every compute call needs a CUDA device and the built library.
+"""
+
+from .core import TensorSubspace, rebalance, synthesize_slice
+from .engine import Informative, OnlineEngine, OnlineResult, StaticRows, run_online
+from .mri import FrameEstimate, interp_track_step, reconstruct_frame
+from .observation import (
+    EntryMask,
+    FourierMask,
+    MeasurementBatch,
+    build_phi,
+    row_distances,
+    rows_to_entries,
+    unitary_dft2,
+    unitary_dft_matrix,
+    variable_density_rows,
+    weighted_draw_without_replacement,
+)
+from .sampler import (
+    SamplePlan,
+    SamplingDistribution,
+    adaptive_step,
+    draw_samples,
+    entry_scores,
+    expected_count_trace,
+    expected_sample_count,
+    row_scores,
+)
+from .tracker import (
+    Fixed,
+    HessianBound,
+    StepConfig,
+    StepReport,
+    TrackerState,
+    init_state,
+    random_subspace,
+    run,
+    solve_gamma,
+    track_step,
+)
+from ._lib import NumericalError
+
+__all__ = [
+    "TensorSubspace", "rebalance", "synthesize_slice",
+    "EntryMask", "FourierMask", "MeasurementBatch", "build_phi", "row_distances", "rows_to_entries",
+    "unitary_dft2", "unitary_dft_matrix", "variable_density_rows", "weighted_draw_without_replacement",
+    "Fixed", "HessianBound", "StepConfig", "StepReport", "TrackerState", "init_state", "random_subspace",
+    "run", "solve_gamma", "track_step",
+    "SamplePlan", "SamplingDistribution", "adaptive_step", "draw_samples", "entry_scores",
+    "expected_count_trace", "expected_sample_count", "row_scores",
+    "FrameEstimate", "interp_track_step", "reconstruct_frame",
+    "OnlineEngine", "OnlineResult", "StaticRows", "Informative", "run_online", "NumericalError",
+]

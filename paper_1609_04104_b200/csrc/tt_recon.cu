@@ -1,0 +1,86 @@
+// Frame reconstruction X_f = A_f diag(gamma_f) B_f^T, batched over frames.
+//
+// Reference: core.synthesize_slice (core.py:91-104, einsum over the rank) and
+// mri.reconstruct_frame (mri.py:107-121, (A1 * gamma) @ A2.T, plain
+// transpose). In run_adaptive it is called once per frame with the
+// post-update factors and that frame's gamma (experiment.py:525).
+//
+// Each CTA produces a 64 x 64 output tile: the gamma-scaled A tile and the B
+// tile are staged transposed ([r][64]) in shared memory and every thread
+// accumulates a 4 x 4 register block over r (complex fp32 FMAs), then writes
+// rows of 16 consecutive complex64 values (128 B segments).
+
+#include "tt_common.cuh"
+
+#define RC_T 64
+#define RC_NT 256
+#define RC_RMAX 64
+
+__global__ void __launch_bounds__(RC_NT) recon_kernel(int nx, int ny, int R, const float2* __restrict__ A,
+                                                      const float2* __restrict__ B, const float2* __restrict__ gamma,
+                                                      float2* __restrict__ X) {
+  extern __shared__ __align__(16) float2 rsm[];
+  float2* as = rsm;               // [R][64]
+  float2* bs = rsm + R * RC_T;    // [R][64]
+  const int tid = threadIdx.x;
+  const int f = blockIdx.z;
+  const int i0 = blockIdx.y * RC_T, j0 = blockIdx.x * RC_T;
+  const float2* Af = A + (size_t)f * nx * R;
+  const float2* Bf = B + (size_t)f * ny * R;
+  const float2* gf = gamma + (size_t)f * R;
+  for (int o = tid; o < RC_T * R; o += RC_NT) {
+    const int ii = o / R, r = o - ii * R;
+    const int i = i0 + ii, j = j0 + ii;
+    as[r * RC_T + ii] = i < nx ? cmul(Af[(size_t)i * R + r], gf[r]) : make_float2(0.f, 0.f);
+    bs[r * RC_T + ii] = j < ny ? Bf[(size_t)j * R + r] : make_float2(0.f, 0.f);
+  }
+  __syncthreads();
+  const int tj = tid & 15, ti = tid >> 4;  // 16 x 16 threads, 4 x 4 outputs each
+  float2 acc[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = make_float2(0.f, 0.f);
+  for (int r = 0; r < R; ++r) {
+    float2 av[4], bv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) av[u] = as[r * RC_T + ti + 16 * u];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) bv[v] = bs[r * RC_T + tj + 16 * v];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[u][v] = cfma(av[u], bv[v], acc[u][v]);
+  }
+  float2* Xf = X + (size_t)f * nx * ny;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int i = i0 + ti + 16 * u;
+    if (i >= nx) continue;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int j = j0 + tj + 16 * v;
+      if (j < ny) Xf[(size_t)i * ny + j] = acc[u][v];
+    }
+  }
+}
+
+extern "C" int tt_reconstruct(void* stream, int frames, int nx, int ny, int rank, const float* a, const float* b,
+                              const float* gamma, float* x_out) {
+  if (frames < 0 || nx < 1 || ny < 1 || rank < 1 || !a || !b || !gamma || !x_out)
+    return tt_fail(TT_EINVAL, "tt_reconstruct: bad arguments");
+  if (rank > RC_RMAX) return tt_fail(TT_EUNSUPPORTED, "tt_reconstruct: rank > %d", RC_RMAX);
+  if (frames == 0) return TT_OK;
+  if (frames > 65535) return tt_fail(TT_EINVAL, "tt_reconstruct: frames > 65535 per call");
+  const size_t sm = sizeof(float2) * 2 * RC_T * (size_t)rank;
+  static size_t cfg = 0;
+  if (sm > cfg) {
+    TT_CUDA_TRY(cudaFuncSetAttribute(recon_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    cfg = sm;
+  }
+  dim3 grid((ny + RC_T - 1) / RC_T, (nx + RC_T - 1) / RC_T, frames);
+  recon_kernel<<<grid, RC_NT, sm, (cudaStream_t)stream>>>(nx, ny, rank, (const float2*)a, (const float2*)b,
+                                                          (const float2*)gamma, (float2*)x_out);
+  TT_CUDA_TRY(cudaGetLastError());
+  return TT_OK;
+}

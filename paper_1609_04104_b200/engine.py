@@ -1,0 +1,255 @@
+"""Device-resident online reconstruction loop (the B200 form of the
+per-frame body of ``experiment.run_adaptive``, experiment.py:482-530, and of
+``run_tracking``'s streaming pass, :284-296).
+
+One ``tt_track_rows`` launch runs a whole block of frames for a batch of
+independent slices: per frame [informative row draw from the current
+k-space factor | static row table] -> gather y from the resident truth
+k-space -> ridge gamma -> k-space factor update, with the state resident in
+shared memory. The post-update factors of every frame are written to a
+history buffer; ``reconstruct`` then turns them into image frames
+X_t = A_t diag(gamma_t) B_t^T with the inverse column FFT and outer-product
+kernels (the online reconstruction with post-update factors and the same
+frame's gamma, experiment.py:525).
+
+Semantics kept from the reference loop:
+  * t starts at ``t0`` and advances by one per frame (tracker.py:411);
+  * informative draws: k trials with replacement from row_scores of the
+    pre-step k-space factor, forced lines count toward k, result sorted
+    unique (sampler.py:146-162; experiment.py:499-505), Philox stream
+    ``(key0, key1 + slice)`` shared across frames;
+  * static masks keep the given (draw) order (experiment.py:166-167).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from . import _ops as K
+from .tracker import Fixed, HessianBound
+
+__all__ = ["StaticRows", "Informative", "OnlineEngine", "run_online", "OnlineResult"]
+
+
+@dataclass(frozen=True)
+class StaticRows:
+    """Pre-drawn row masks: ``rows[f, s, :cnt[f, s]]`` for frame f, slice s."""
+
+    rows: np.ndarray  # (T, nslices, Smax) int
+    counts: np.ndarray  # (T, nslices) int
+
+
+@dataclass(frozen=True)
+class Informative:
+    """Subspace-driven row sampling (sampler.row_scores + draw_samples)."""
+
+    k: int
+    forced: tuple = (0,)
+    beta: float = 0.1
+    key0: int = 0
+    key1: int = 0
+
+
+def _step_params(step):
+    if isinstance(step, HessianBound):
+        return L.TT_STEP_HESSIAN, 0.0, float(step.c_floor), float(step.c_cap)
+    if isinstance(step, Fixed):
+        return L.TT_STEP_FIXED, float(step.mu), 0.0, 0.0
+    raise TypeError("step must be Fixed or HessianBound")
+
+
+class OnlineEngine:
+    def __init__(self, nx, ny, rank, nslices=1, lam=0.1, step=Fixed(0.01), policy=None, cluster=0, t0=1):
+        if policy is None:
+            raise ValueError("policy is required (StaticRows or Informative)")
+        self.nx, self.ny, self.rank, self.nslices = int(nx), int(ny), int(rank), int(nslices)
+        self.lam = float(lam)
+        self.step = step
+        self.policy = policy
+        self.dev = L.device()
+        if isinstance(policy, Informative):
+            if not 1 <= policy.k <= nx:
+                raise ValueError("informative k must be in [1, nx]")
+            forced = np.unique(np.asarray(policy.forced, dtype=np.int64))
+            if forced.size and (forced.min() < 0 or forced.max() >= nx):
+                raise ValueError("forced index out of range")
+            if forced.size > policy.k:
+                raise ValueError("more forced indices than trials")
+            self.max_rows = int(policy.k)
+            self.forced = torch.from_numpy(forced.astype(np.int32)).to(self.dev)
+            self.rows_tab = self.rows_cnt = None
+        elif isinstance(policy, StaticRows):
+            rows = np.asarray(policy.rows)
+            if rows.ndim == 2:
+                rows = rows[:, None, :]
+            cnt = np.asarray(policy.counts).reshape(rows.shape[0], -1)
+            if rows.shape[1] != nslices or cnt.shape != rows.shape[:2]:
+                raise ValueError("static row table must be (T, nslices, Smax) with counts (T, nslices)")
+            self.max_rows = int(rows.shape[2])
+            self.rows_tab = torch.from_numpy(np.ascontiguousarray(rows, dtype=np.int32)).to(self.dev)
+            self.rows_cnt = torch.from_numpy(np.ascontiguousarray(cnt, dtype=np.int32)).to(self.dev)
+            self.forced = None
+        else:
+            raise TypeError("policy must be StaticRows or Informative")
+        self.scr = K.RowsScratch(nslices, nx, ny, rank, self.max_rows, cluster)
+        self.cluster = self.scr.cluster
+        z = lambda *s: torch.zeros(*s, dtype=torch.complex64, device=self.dev)  # noqa: E731
+        self.ah = z(nslices, nx, rank)
+        self.bh = z(nslices, ny, rank)
+        self.alpha_bar = torch.zeros(nslices, dtype=torch.float64, device=self.dev)
+        self.philox_pos = torch.zeros(nslices, dtype=torch.int64, device=self.dev)
+        self.status = torch.zeros(nslices, dtype=torch.int32, device=self.dev)
+        self.t = int(t0)
+        self.frame = 0
+
+    # ------------------------------------------------------------------ state
+    def set_image_factors(self, A, B):
+        """Image-domain factors (nslices, N, R) -> resident k-space factors."""
+        a = torch.as_tensor(np.asarray(A) if not isinstance(A, torch.Tensor) else A)
+        b = torch.as_tensor(np.asarray(B) if not isinstance(B, torch.Tensor) else B)
+        a = a.to(self.dev, torch.complex64).reshape(self.nslices, self.nx, self.rank).contiguous()
+        b = b.to(self.dev, torch.complex64).reshape(self.nslices, self.ny, self.rank).contiguous()
+        self.ah = K.fft_cols_(a)
+        self.bh = K.fft_cols_(b)
+
+    def image_factors(self):
+        return K.fft_cols(self.ah, inverse=True), K.fft_cols(self.bh, inverse=True)
+
+    # ------------------------------------------------------------------ frames
+    def make_outputs(self, frames: int, history: bool = True):
+        d, ns, R = self.dev, self.nslices, self.rank
+        out = dict(
+            gamma=torch.empty(frames, ns, R, dtype=torch.complex64, device=d),
+            cost=torch.empty(frames, ns, dtype=torch.float64, device=d),
+            mu=torch.empty(frames, ns, dtype=torch.float64, device=d),
+            alpha=torch.empty(frames, ns, dtype=torch.float64, device=d),
+            rows=torch.empty(frames, ns, self.max_rows, dtype=torch.int32, device=d),
+            cnt=torch.empty(frames, ns, dtype=torch.int32, device=d),
+        )
+        if history:
+            out["ah"] = torch.empty(frames, ns, self.nx, R, dtype=torch.complex64, device=d)
+            out["bh"] = torch.empty(frames, ns, self.ny, R, dtype=torch.complex64, device=d)
+        return out
+
+    def args(self, kspace: torch.Tensor, frames: int, out: dict, ah_in=None, bh_in=None, ah_out=None,
+             bh_out=None, frame0=None, t0=None) -> L.RowsArgs:
+        """Build the C argument block. ``kspace`` is the resident truth,
+        (T, nslices, nx, ny) complex64; frames [frame0, frame0+frames)."""
+        if kspace.dtype != torch.complex64 or not kspace.is_cuda or not kspace.is_contiguous():
+            raise TypeError("kspace must be a contiguous complex64 CUDA tensor (T, nslices, nx, ny)")
+        f0 = self.frame if frame0 is None else int(frame0)
+        ks = kspace.reshape(kspace.shape[0], self.nslices, self.nx, self.ny)
+        if f0 + frames > ks.shape[0]:
+            raise ValueError("not enough truth frames")
+        mode, mu, cf, cc = _step_params(self.step)
+        a = L.RowsArgs()
+        a.nslices, a.nx, a.ny, a.rank, a.frames = self.nslices, self.nx, self.ny, self.rank, int(frames)
+        a.max_rows, a.cluster = self.max_rows, self.cluster
+        a.t0 = self.t if t0 is None else int(t0)
+        a.ah_in = (self.ah if ah_in is None else ah_in).data_ptr()
+        a.bh_in = (self.bh if bh_in is None else bh_in).data_ptr()
+        a.ah_out = (self.ah if ah_out is None else ah_out).data_ptr()
+        a.bh_out = (self.bh if bh_out is None else bh_out).data_ptr()
+        a.alpha_bar = self.alpha_bar.data_ptr()
+        if isinstance(self.policy, Informative):
+            a.policy = L.TT_POLICY_INFORMATIVE
+            a.k_draws = int(self.policy.k)
+            a.forced = self.forced.data_ptr() if self.forced.numel() else None
+            a.nforced = int(self.forced.numel())
+            a.beta = float(self.policy.beta)
+            a.key0, a.key1 = int(self.policy.key0), int(self.policy.key1)
+            a.philox_pos = self.philox_pos.data_ptr()
+        else:
+            a.policy = L.TT_POLICY_STATIC
+            rs = self.nslices * self.max_rows
+            a.rows_tab = self.rows_tab.data_ptr() + 4 * f0 * rs
+            a.rows_cnt = self.rows_cnt.data_ptr() + 4 * f0 * self.nslices
+        a.y_mode = L.TT_Y_GATHER
+        a.ysrc = ks[f0].data_ptr()
+        a.y_frame_stride = self.nslices * self.nx * self.ny
+        a.y_slice_stride = self.nx * self.ny
+        a.lam, a.step_mode, a.mu, a.c_floor, a.c_cap = self.lam, mode, mu, cf, cc
+        a.gamma_out = out["gamma"].data_ptr()
+        a.cost_out = out["cost"].data_ptr()
+        a.mu_out = out["mu"].data_ptr()
+        a.alpha_out = out["alpha"].data_ptr()
+        a.rows_out = out["rows"].data_ptr()
+        a.cnt_out = out["cnt"].data_ptr()
+        a.ah_hist = out["ah"].data_ptr() if "ah" in out else None
+        a.bh_hist = out["bh"].data_ptr() if "bh" in out else None
+        a.status = self.status.data_ptr()
+        a.scratch = self.scr.buf.data_ptr()
+        return a
+
+    def run(self, kspace: torch.Tensor, frames: int, history: bool = True, out: dict | None = None) -> dict:
+        """Advance ``frames`` frames from the current frame index."""
+        if out is None:
+            out = self.make_outputs(frames, history)
+        K.track_rows(self.args(kspace, frames, out))
+        self.frame += frames
+        self.t += frames
+        return out
+
+    def check_status(self):
+        L.raise_status(int(self.status.max().item()), "online engine")
+
+    def reconstruct(self, out: dict) -> torch.Tensor:
+        """Image frames (F, nslices, nx, ny) from the recorded k-space factor
+        history: inverse column FFT of each frame's factors, then the
+        gamma-weighted outer product."""
+        F, ns = out["gamma"].shape[:2]
+        A = K.fft_cols(out["ah"], inverse=True).reshape(F * ns, self.nx, self.rank)
+        B = K.fft_cols(out["bh"], inverse=True).reshape(F * ns, self.ny, self.rank)
+        X = K.reconstruct(A, B, out["gamma"].reshape(F * ns, self.rank))
+        return X.reshape(F, ns, self.nx, self.ny)
+
+
+@dataclass
+class OnlineResult:
+    recon: np.ndarray     # (T, nslices, nx, ny) complex64 image frames
+    gamma: np.ndarray     # (T, nslices, R)
+    cost: np.ndarray      # (T, nslices)
+    mu: np.ndarray
+    rows: list            # per frame per slice row arrays
+    nmse: np.ndarray | None
+    final_A: np.ndarray
+    final_B: np.ndarray
+
+
+def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1) -> OnlineResult:
+    """Public end-to-end call (host in, host out): the online loop over all
+    frames of ``kspace`` (T, [nslices,] nx, ny) from image-domain initial
+    factors, returning reconstructions and per-frame reports. The analogue of
+    ``experiment.run_adaptive`` for pre-noised truth without warm-up."""
+    ks = np.asarray(kspace) if not isinstance(kspace, torch.Tensor) else kspace
+    if ks.ndim == 3:
+        ks = ks[:, None]
+    T, ns, nx, ny = ks.shape
+    A0 = np.asarray(A0).reshape(ns, nx, -1)
+    R = A0.shape[-1]
+    eng = OnlineEngine(nx, ny, R, ns, lam, step, policy, cluster, t0)
+    eng.set_image_factors(A0, np.asarray(B0).reshape(ns, ny, R))
+    if isinstance(ks, torch.Tensor):
+        kd = ks.to(eng.dev, torch.complex64).contiguous()
+    else:
+        kd = torch.from_numpy(np.ascontiguousarray(ks, dtype=np.complex64)).to(eng.dev)
+    out = eng.run(kd, T)
+    X = eng.reconstruct(out)
+    eng.check_status()
+    nm = None
+    if clean is not None:
+        cl = torch.as_tensor(np.asarray(clean, dtype=np.complex64)).to(eng.dev).reshape(T, ns, nx, ny)
+        num = (cl - X).abs().pow(2).sum(dim=(-1, -2)).double()
+        den = cl.abs().pow(2).sum(dim=(-1, -2)).double()
+        nm = (num / den).cpu().numpy()
+    cnt = out["cnt"].cpu().numpy()
+    rows_np = out["rows"].cpu().numpy()
+    rows = [[rows_np[f, s, :cnt[f, s]].astype(np.int64) for s in range(ns)] for f in range(T)]
+    A, B = eng.image_factors()
+    return OnlineResult(recon=X.cpu().numpy(), gamma=out["gamma"].cpu().numpy(), cost=out["cost"].cpu().numpy(),
+                        mu=out["mu"].cpu().numpy(), rows=rows, nmse=nm, final_A=A.cpu().numpy(),
+                        final_B=B.cpu().numpy())

@@ -1,0 +1,69 @@
+"""GPU parity of the value kernels: column FFT (ortho convention), 2-D DFT by
+two column passes, reconstruction, rebalance."""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, rel
+from oracle import tt_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 7, 64, 100, 128, 256, 1000, 1024, 4096])
+@pytest.mark.parametrize("inverse", [False, True])
+def test_fft_cols_matches_numpy(n, inverse):
+    import torch
+
+    from paper_1609_04104_b200 import _ops as K
+
+    rng = np.random.default_rng(n)
+    x = (rng.standard_normal((3, n, 11)) + 1j * rng.standard_normal((3, n, 11))).astype(np.complex64)
+    got = K.fft_cols(torch.from_numpy(x).cuda(), inverse).cpu().numpy()
+    want = np.stack([O.fft_cols(x[b], inverse) for b in range(3)])
+    assert rel(got, want) < 2e-6
+
+
+def test_dft2_delta_roundtrip_and_golden():
+    import paper_1609_04104_b200 as tt
+
+    x = np.zeros((4, 6), complex)
+    x[0, 0] = 1.0
+    np.testing.assert_allclose(tt.unitary_dft2(x), np.full((4, 6), 1 / np.sqrt(24)), atol=1e-7)
+    g = load_golden("value_cases")
+    assert rel(tt.unitary_dft2(g["dft_in"]), g["dft_out"]) < 1e-6
+    assert rel(tt.unitary_dft2(g["dft_in"], inverse=True), g["idft_out"]) < 1e-6
+    F = tt.unitary_dft_matrix(6)
+    np.testing.assert_allclose(F, F.T, atol=1e-7)
+
+
+def test_synthesis_reconstruction_rebalance_golden():
+    import paper_1609_04104_b200 as tt
+
+    g = load_golden("value_cases")
+    A, B, gm = g["A"], g["B"], g["gamma"]
+    sub = tt.TensorSubspace((A, B))
+    assert rel(tt.synthesize_slice(sub, gm), g["synth"]) < 1e-6
+    est = tt.reconstruct_frame(sub, gm)
+    assert rel(est.kspace, g["synth"]) < 1e-6
+    assert rel(est.image, g["image"]) < 1e-5
+    rb = tt.rebalance(sub)
+    assert rel(rb.factors[0], g["rebal_A"]) < 1e-6 and rel(rb.factors[1], g["rebal_B"]) < 1e-6
+    with pytest.raises(ValueError):
+        tt.synthesize_slice(sub, np.zeros(3))
+
+
+@pytest.mark.parametrize("shape", [(256, 256, 20, 7), (128, 96, 10, 3), (1024, 1024, 32, 2), (50, 70, 64, 2)])
+def test_batched_reconstruct_matches_outer_product(shape):
+    import torch
+
+    from paper_1609_04104_b200 import _ops as K
+
+    nx, ny, R, F = shape
+    rng = np.random.default_rng(nx + R)
+    A = (rng.standard_normal((F, nx, R)) + 1j * rng.standard_normal((F, nx, R))).astype(np.complex64)
+    B = (rng.standard_normal((F, ny, R)) + 1j * rng.standard_normal((F, ny, R))).astype(np.complex64)
+    gm = (rng.standard_normal((F, R)) + 1j * rng.standard_normal((F, R))).astype(np.complex64)
+    X = K.reconstruct(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), torch.from_numpy(gm).cuda()).cpu().numpy()
+    for f in range(F):
+        assert rel(X[f], O.synth(A[f], B[f], gm[f])) < 1e-5
