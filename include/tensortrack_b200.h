@@ -104,6 +104,7 @@ typedef struct tt_rows_args {
   float* bh_hist;             /* [frames][nslices][ny][rank] or NULL */
   int32_t* status;            /* [nslices] OR-ed TT_ST_* bits */
   void* scratch;              /* tt_rows_scratch_bytes() bytes */
+  int64_t* phase_clock;       /* optional profiling: [frames][16] SM clock64 stamps of CTA 0, or NULL */
 } tt_rows_args;
 
 /* Choose the cluster size (if *cluster <= 0) and report the dynamic shared

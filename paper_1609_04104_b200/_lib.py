@@ -46,6 +46,7 @@ class RowsArgs(C.Structure):
         ("lam", _f64), ("step_mode", _i32), ("mu", _f64), ("c_floor", _f64), ("c_cap", _f64),
         ("gamma_out", _p), ("cost_out", _p), ("mu_out", _p), ("alpha_out", _p), ("rows_out", _p),
         ("cnt_out", _p), ("resid_out", _p), ("ah_hist", _p), ("bh_hist", _p), ("status", _p), ("scratch", _p),
+        ("phase_clock", _p),
     ]
 
 

@@ -28,6 +28,16 @@ TT_DEV void tri_decode(int e, int& r, int& q) {
 }
 TT_DEV int tri_idx(int r, int q) { return r * (r + 1) / 2 + q; }
 
+// fp64 reciprocal without the IEEE division sequence on the critical path:
+// MUFU approximation + two Newton steps (error ~ 1 ulp), for LDL pivots.
+TT_DEV double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = r * fma(-x, r, 2.0);
+  r = r * fma(-x, r, 2.0);
+  return r;
+}
+
 // ---------------------------------------------------------------- scans
 // Block-wide exclusive scan of per-thread integer counts (deterministic).
 TT_DEV int block_excl_scan_int(int v, int* red, int& total) {
@@ -119,6 +129,7 @@ TT_DEV void block_cumsum(const double* p, double* cdf, int n, bool exact, double
 // the result is bit-identical to numpy for identical probabilities.
 // Marks flags[idx] = 1 (flags cleared here), then adds forced indices and
 // compacts the flags into sorted unique rows (np.union1d semantics).
+template <bool EXACT_DIV = true>
 TT_DEV void draw_with_replacement_block(const double* p, double* cdf, int* flags, int* rows, int& S, int n,
                                         int ndraw, const int* forced, int nforced, uint64_t k0, uint64_t k1,
                                         uint64_t pos, double* red, int* sh_flag) {
@@ -129,7 +140,12 @@ TT_DEV void draw_with_replacement_block(const double* p, double* cdf, int* flags
     block_cumsum(p, cdf, n, exact != 0, red);
     const double last = cdf[n - 1];
     __syncthreads();
-    for (int i = tid; i < n; i += NT) cdf[i] = cdf[i] / last;
+    if (EXACT_DIV || exact) {
+      for (int i = tid; i < n; i += NT) cdf[i] = cdf[i] / last;
+    } else {
+      const double il = fast_rcp(last);
+      for (int i = tid; i < n; i += NT) cdf[i] = cdf[i] * il;
+    }
     __syncthreads();
     for (int m = tid; m < ndraw; m += NT) {
       const double u = philox_uniform(k0, k1, pos + (uint64_t)m);
@@ -209,6 +225,332 @@ TT_DEV void block_ldl_solve(double2* G, double2* hv, double2* gam, int R) {
       acc.y = warp_sum(acc.y);
       if (lane == 0) gam[k] = make_double2((hv[k].x - acc.x) * inv, (hv[k].y - acc.y) * inv);
       __syncwarp();
+    }
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- cluster-part sums
+// Sum of CL (<= 16) values at p, p+stride, ... read with ld.global.cg. All
+// loads are issued before the adds (one L2 round trip, not CL dependent ones);
+// the fixed 0..CL-1 order keeps every CTA bit-identical.
+TT_DEV double sum_parts(const double* p, size_t stride, int CL) {
+  double v[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) v[c] = c < CL ? __ldcg(p + c * stride) : 0.0;
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < 16; ++c) s += v[c];
+  return s;
+}
+TT_DEV double2 sum_parts2(const double2* p, size_t stride, int CL) {
+  double2 v[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    v[c].x = c < CL ? __ldcg(&p[c * stride].x) : 0.0;
+    v[c].y = c < CL ? __ldcg(&p[c * stride].y) : 0.0;
+  }
+  double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int c = 0; c < 16; ++c) s = zadd(s, v[c]);
+  return s;
+}
+TT_DEV float2 sum_parts_f2(const float2* p, size_t stride, int CL) {
+  float2 v[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    v[c].x = c < CL ? __ldcg(&p[c * stride].x) : 0.f;
+    v[c].y = c < CL ? __ldcg(&p[c * stride].y) : 0.f;
+  }
+  float2 s = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int c = 0; c < 16; ++c) s = cadd(s, v[c]);
+  return s;
+}
+
+// ---------------------------------------------------------------- fast fp64 LDL^H solve
+// Same factorisation as block_ldl_solve, organised for latency: `tab[e]`
+// holds the pre-decoded (i << 8 | j) of packed entry e, the owner of the next
+// diagonal publishes its reciprocal pivot inside the step (one barrier per
+// column), and the back substitution is column-oriented in warp 0 (one
+// shuffle broadcast per step). R <= 64.
+TT_DEV void ldl_table_init(unsigned short* tab, int R) {
+  const int Rp = R * (R + 1) / 2;
+  for (int e = threadIdx.x; e < Rp; e += blockDim.x) {
+    int r, q;
+    tri_decode(e, r, q);
+    tab[e] = (unsigned short)((r << 8) | q);
+  }
+}
+
+TT_DEV void block_ldl_solve_fast(double2* G, double2* hv, double2* gam, double* inv, const unsigned short* tab,
+                                 int R) {
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int Rp = R * (R + 1) / 2;
+  if (tid == 0) {
+    const double d = G[0].x;
+    inv[0] = d > 0.0 ? fast_rcp(d) : 0.0;
+  }
+  __syncthreads();
+  for (int k = 0; k < R - 1; ++k) {
+    const double ik = inv[k];
+    const int e0 = (k + 1) * (k + 2) / 2;  // first entry of row k+1; rows <= k never change
+    for (int e = e0 + tid; e < Rp; e += NT) {
+      const int ij = tab[e];
+      const int i = ij >> 8, j = ij & 255;
+      if (j > k) {
+        const double2 lik = G[i * (i + 1) / 2 + k], ljk = G[j * (j + 1) / 2 + k];
+        double2 g = G[e];
+        g.x -= (lik.x * ljk.x + lik.y * ljk.y) * ik;
+        g.y -= (lik.y * ljk.x - lik.x * ljk.y) * ik;
+        G[e] = g;
+        if (i == k + 1 && j == k + 1) inv[k + 1] = g.x > 0.0 ? fast_rcp(g.x) : 0.0;
+      }
+    }
+    if (tid > k && tid < R) {
+      const double2 lik = G[tid * (tid + 1) / 2 + k], hk = hv[k];
+      hv[tid].x -= (lik.x * hk.x - lik.y * hk.y) * ik;
+      hv[tid].y -= (lik.x * hk.y + lik.y * hk.x) * ik;
+    }
+    __syncthreads();
+  }
+  if (tid < 32) {
+    double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+    for (int k = R - 1; k >= 0; --k) {
+      const int own = k & 31;
+      double gx = 0.0, gy = 0.0;
+      if (tid == own) {
+        const double2 a = k < 32 ? a0 : a1;
+        gx = (hv[k].x - a.x) * inv[k];
+        gy = (hv[k].y - a.y) * inv[k];
+        gam[k] = make_double2(gx, gy);
+      }
+      gx = __shfl_sync(0xffffffffu, gx, own);
+      gy = __shfl_sync(0xffffffffu, gy, own);
+      const int kb = k * (k + 1) / 2;
+      if (tid < k) {
+        const double2 g = G[kb + tid];
+        a0.x += g.x * gx + g.y * gy;
+        a0.y += g.x * gy - g.y * gx;
+      }
+      if (tid + 32 < k) {
+        const double2 g = G[kb + tid + 32];
+        a1.x += g.x * gx + g.y * gy;
+        a1.y += g.x * gy - g.y * gx;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Warp-synchronous variant for the fused per-frame kernel: warp 0 alone runs
+// the factorisation (no CTA barriers between columns, only __syncwarp), every
+// lane recomputing the reciprocal pivot itself. Other warps only meet the
+// closing __syncthreads. Same arithmetic as block_ldl_solve_fast.
+TT_DEV void warp_ldl_solve(double2* G, double2* hv, double2* gam, const unsigned short* tab, int R) {
+  const int tid = threadIdx.x;
+  if (tid < 32) {
+    const int lane = tid;
+    const int Rp = R * (R + 1) / 2;
+    for (int k = 0; k < R - 1; ++k) {
+      const double d = G[k * (k + 1) / 2 + k].x;
+      const double ik = d > 0.0 ? fast_rcp(d) : 0.0;
+      const int e0 = (k + 1) * (k + 2) / 2;
+#pragma unroll 2
+      for (int e = e0 + lane; e < Rp; e += 32) {
+        const int ij = tab[e];
+        const int i = ij >> 8, j = ij & 255;
+        if (j > k) {
+          const double2 lik = G[i * (i + 1) / 2 + k], ljk = G[j * (j + 1) / 2 + k];
+          double2 g = G[e];
+          g.x -= (lik.x * ljk.x + lik.y * ljk.y) * ik;
+          g.y -= (lik.y * ljk.x - lik.x * ljk.y) * ik;
+          G[e] = g;
+        }
+      }
+      for (int i = k + 1 + lane; i < R; i += 32) {
+        const double2 lik = G[i * (i + 1) / 2 + k], hk = hv[k];
+        hv[i].x -= (lik.x * hk.x - lik.y * hk.y) * ik;
+        hv[i].y -= (lik.x * hk.y + lik.y * hk.x) * ik;
+      }
+      __syncwarp();
+    }
+    double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+    for (int k = R - 1; k >= 0; --k) {
+      const int own = k & 31;
+      const double d = G[k * (k + 1) / 2 + k].x;
+      const double ik = d > 0.0 ? fast_rcp(d) : 0.0;
+      double gx = 0.0, gy = 0.0;
+      if (lane == own) {
+        const double2 a = k < 32 ? a0 : a1;
+        gx = (hv[k].x - a.x) * ik;
+        gy = (hv[k].y - a.y) * ik;
+        gam[k] = make_double2(gx, gy);
+      }
+      gx = __shfl_sync(0xffffffffu, gx, own);
+      gy = __shfl_sync(0xffffffffu, gy, own);
+      const int kb = k * (k + 1) / 2;
+      if (lane < k) {
+        const double2 g = G[kb + lane];
+        a0.x += g.x * gx + g.y * gy;
+        a0.y += g.x * gy - g.y * gx;
+      }
+      if (lane + 32 < k) {
+        const double2 g = G[kb + lane + 32];
+        a1.x += g.x * gx + g.y * gy;
+        a1.y += g.x * gy - g.y * gx;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// value of row `row` held by lane row % 32 in (a0: rows < 32, a1: rows >= 32), broadcast to the warp
+TT_DEV double2 shfl_d2_sel(double2 a0, double2 a1, int row) {
+  const double2 v = row < 32 ? a0 : a1;
+  double2 o;
+  o.x = __shfl_sync(0xffffffffu, v.x, row & 31);
+  o.y = __shfl_sync(0xffffffffu, v.y, row & 31);
+  return o;
+}
+
+// ---------------------------------------------------------------- 2x2-blocked register LDL^H
+// Solves (G) gamma = h for Hermitian positive (semi)definite G given as a
+// packed lower triangle, with 2x2 pivot blocks: R/2 elimination steps and
+// R/2 back-substitution steps instead of R each (the per-step latency of a
+// barrier-synchronised chain dominates at R <= 64). Thread t owns entries
+// e = t + m*NT of the augmented system (packed lower entries 0..Rp-1, then the
+// rhs "column" R as entries Rp + i) in registers. The two pivot columns of
+// each step are final after the previous step; their owners publish them to a
+// double-buffered column buffer (slot R holds conj(h)). Singular pivot blocks
+// (det <= 0) drop their components, mirroring the s > 0 filter of the
+// reference SVD ridge (tracker.py:154-155).
+//   scratch: colb 2*2*(R+1) double2 | blk (R/2+1)*4 double | zf R double2
+//   Gio: packed lower in / final factor out. Ends with __syncthreads.
+template <int EPT>
+TT_DEV void block_ldl2_solve(double2* Gio, const double2* hin, double2* gam, double2* colb, double* blk, double2* zf,
+                             int R) {
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int Rp = R * (R + 1) / 2, E = Rp + R, W = R + 1;
+  int ri[EPT], rj[EPT];
+  double2 g[EPT];
+#pragma unroll
+  for (int m = 0; m < EPT; ++m) {
+    const int e = tid + m * NT;
+    ri[m] = -1;
+    rj[m] = -1;
+    g[m] = make_double2(0.0, 0.0);
+    if (e < Rp) {
+      int r, q;
+      tri_decode(e, r, q);
+      ri[m] = r;
+      rj[m] = q;
+      g[m] = Gio[e];
+    } else if (e < E) {
+      ri[m] = e - Rp;
+      rj[m] = R;
+      g[m] = hin[e - Rp];
+    }
+    // publish block 0 columns (0, 1) into buffer 0
+    if (rj[m] == 0 || rj[m] == 1) colb[rj[m] * W + ri[m]] = g[m];
+    if (rj[m] == R && ri[m] < 2) colb[ri[m] * W + R] = zconj(g[m]);
+  }
+  __syncthreads();
+  const int nb = (R + 1) / 2;
+  for (int b = 0; b < nb; ++b) {
+    const int k = 2 * b;
+    const bool pair = k + 1 < R;
+    const double2* c0 = colb + (b & 1) * 2 * W;
+    const double2* c1 = c0 + W;
+    double2* n0 = colb + ((b + 1) & 1) * 2 * W;
+    double2* n1 = n0 + W;
+    const double a = c0[k].x;
+    const double2 c = pair ? c0[k + 1] : make_double2(0.0, 0.0);
+    const double bb = pair ? c1[k + 1].x : 0.0;
+    double id;  // 1 / det (pair) or 1 / a (single)
+    if (pair) {
+      const double det = a * bb - (c.x * c.x + c.y * c.y);
+      id = det > 0.0 ? fast_rcp(det) : 0.0;
+    } else {
+      id = a > 0.0 ? fast_rcp(a) : 0.0;
+    }
+    if (tid == 0) {
+      blk[4 * b + 0] = a;
+      blk[4 * b + 1] = bb;
+      blk[4 * b + 2] = id;
+      zf[k] = zconj(c0[R]);
+      if (pair) zf[k + 1] = zconj(c1[R]);
+    }
+#pragma unroll
+    for (int m = 0; m < EPT; ++m) {
+      const int i = ri[m], j = rj[m];
+      if ((j >= k + 2 && j < R && i >= j) || (j == R && i >= k + 2)) {  // trailing lower entry or rhs row
+        // u = (G_ik, G_i,k+1), v = (G_jk, G_j,k+1) [slot R: conj(h_k), conj(h_k+1)]
+        const double2 u0 = c0[i], v0 = c0[j];
+        double2 upd;
+        if (pair) {
+          const double2 u1 = c1[i], v1 = c1[j];
+          // t = B^-1 v^H * det : t0 = bb conj(v0) - conj(c) conj(v1); t1 = -c conj(v0) + a conj(v1)
+          const double2 cv0 = zconj(v0), cv1 = zconj(v1);
+          const double2 cc = zconj(c);
+          double2 t0 = zscale(cv0, bb);
+          t0 = zsub(t0, zmul(cc, cv1));
+          double2 t1 = zscale(cv1, a);
+          t1 = zsub(t1, zmul(c, cv0));
+          upd = zadd(zmul(u0, t0), zmul(u1, t1));
+        } else {
+          upd = zmul(u0, zconj(v0));
+        }
+        g[m].x -= upd.x * id;
+        g[m].y -= upd.y * id;
+        if (j == k + 2 || j == k + 3) n0[(j - k - 2) * W + i] = g[m];  // next pivot columns
+        if (j == R && (i == k + 2 || i == k + 3)) n0[(i - k - 2) * W + R] = zconj(g[m]);
+      }
+      // entries of the two pivot columns are final now: keep them for the back substitution
+      if (j == k || (pair && j == k + 1)) Gio[tid + m * NT] = g[m];
+    }
+    (void)n1;
+    __syncthreads();
+  }
+  // back substitution (warp 0): blocks from last to first
+  //   [gk, gk1] = Bk^-1 ([zk, zk1] - [acc_k, acc_k1]),  acc_i = sum_{j > block} conj(G_ji) gamma_j
+  if (tid < 32) {
+    const int lane = tid;
+    double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);  // acc for rows lane, lane+32
+    for (int b = nb - 1; b >= 0; --b) {
+      const int k = 2 * b;
+      const bool pair = k + 1 < R;
+      const double2 acck = shfl_d2_sel(a0, a1, k);
+      const double2 acck1 = pair ? shfl_d2_sel(a0, a1, k + 1) : make_double2(0.0, 0.0);
+      const double a = blk[4 * b + 0], bb = blk[4 * b + 1], id = blk[4 * b + 2];
+      const double2 r0 = zsub(zf[k], acck);
+      double2 gk, gk1 = make_double2(0.0, 0.0);
+      if (pair) {
+        const double2 c = Gio[(k + 1) * (k + 2) / 2 + k];  // G_k+1,k
+        // B^-1 r = (1/det) [bb r0 - conj(c) r1 ; -c r0 + a r1]
+        const double2 r1 = zsub(zf[k + 1], acck1);
+        gk = zscale(zsub(zscale(r0, bb), zmul(zconj(c), r1)), id);
+        gk1 = zscale(zsub(zscale(r1, a), zmul(c, r0)), id);
+      } else {
+        gk = zscale(r0, id);
+      }
+      if (lane == 0) {
+        gam[k] = gk;
+        if (pair) gam[k + 1] = gk1;
+      }
+      // rows i < k: acc_i += conj(G_k,i) gk + conj(G_k+1,i) gk1 (rows k, k+1 of the factor, contiguous)
+      const double2* rk = Gio + k * (k + 1) / 2;
+      const double2* rk1 = Gio + (k + 1) * (k + 2) / 2;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = lane + 32 * h;
+        if (i < k) {
+          double2 acc = h ? a1 : a0;
+          acc = zfma_cj(rk[i], gk, acc);
+          if (pair) acc = zfma_cj(rk1[i], gk1, acc);
+          if (h) a1 = acc; else a0 = acc;
+        }
+      }
     }
   }
   __syncthreads();

@@ -42,11 +42,10 @@
 namespace cg = cooperative_groups;
 
 #define ROWS_NT 256
-#define ROWS_WPT 16
 
 struct RowsPlan {
   int CL, KT, nIm, nJm, Rp;
-  int o_ahl, o_bhl, o_u1, o_ga32, o_gb32, o_vec, o_flags, o_rows, o_u2, o_red;
+  int o_ahl, o_bhl, o_u1, o_ga32, o_gb32, o_vec, o_tab, o_flags, o_rows, o_forced, o_wacc, o_u2, o_red;
   int smem;
 };
 
@@ -76,30 +75,36 @@ __host__ __device__ inline RowsScratch rows_scratch_layout(int nx, int ny, int R
 
 static bool rows_make_plan(int nx, int ny, int R, int Smax, int CL, RowsPlan* p) {
   const int maxsmem = 227 * 1024;
+  if (R > 64) return false;
   p->CL = CL;
   p->nIm = (nx + CL - 1) / CL;
   p->nJm = (ny + CL - 1) / CL;
   p->Rp = R * (R + 1) / 2;
-  if (p->nJm * R > ROWS_WPT * ROWS_NT) return false;
   size_t o = 0;
-  p->o_ahl = (int)o;   o = al16(o + sizeof(float2) * p->nIm * R);
-  p->o_bhl = (int)o;   o = al16(o + sizeof(float2) * p->nJm * R);
-  p->o_u1 = (int)o;    // packed fp64 Gram / LDL workspace  |  p + cdf (draw phase)
+  p->o_ahl = (int)o;    o = al16(o + sizeof(float2) * p->nIm * R);
+  p->o_bhl = (int)o;    o = al16(o + sizeof(float2) * p->nJm * R);
+  p->o_u1 = (int)o;     // packed fp64 Gram / LDL workspace  |  p + cdf (draw phase)
   {
     size_t g = sizeof(double2) * (size_t)p->Rp;
     size_t d = sizeof(double) * 2 * (size_t)nx;
     o = al16(o + (g > d ? g : d));
   }
-  p->o_ga32 = (int)o;  o = al16(o + sizeof(float2) * R * R);
-  p->o_gb32 = (int)o;  o = al16(o + sizeof(float2) * R * R);
-  p->o_vec = (int)o;   o = al16(o + sizeof(double2) * R * 2 + sizeof(double) * R + sizeof(float2) * R + 64);
-  p->o_flags = (int)o; o = al16(o + sizeof(int) * (nx > p->nIm ? nx : p->nIm));
-  p->o_rows = (int)o;  o = al16(o + sizeof(int) * (Smax > 0 ? Smax : 1));
+  p->o_ga32 = (int)o;   o = al16(o + sizeof(float2) * p->Rp);  // packed lower, fp32
+  p->o_gb32 = (int)o;   o = al16(o + sizeof(float2) * p->Rp);
+  // vec: gam, hv, hsave (double2 R); nrm, inrm, inv, gda, gdb (double R); gamf (float2 R); 16 scalars
+  // + LDL scratch: colb 4 (R+1) double2, blk 4 (R/2+1) double, zf R double2
+  p->o_vec = (int)o;    o = al16(o + sizeof(double2) * R * 3 + sizeof(double) * R * 5 + sizeof(float2) * R + 128 +
+                                 sizeof(double2) * 4 * (R + 1) + sizeof(double) * 4 * (R / 2 + 1) + sizeof(double2) * R);
+  p->o_tab = (int)o;    o = al16(o + sizeof(unsigned short) * p->Rp);
+  p->o_flags = (int)o;  o = al16(o + sizeof(int) * (nx > p->nIm ? nx : p->nIm));
+  p->o_rows = (int)o;   o = al16(o + sizeof(int) * Smax);
+  p->o_forced = (int)o; o = al16(o + sizeof(int) * Smax);
+  p->o_wacc = (int)o;   o = al16(o + sizeof(float2) * p->nJm * R);
   p->o_u2 = (int)o;
   size_t fixed = o + sizeof(double) * 64;
   if (fixed > (size_t)maxsmem) return false;
-  // U2: k-tiles (ys KT x nJm, ahs KT x R)  |  W buffer nJm x R  |  P rows nIm x R
-  size_t other = sizeof(float2) * (size_t)R * (p->nJm > p->nIm ? p->nJm : p->nIm);
+  // U2: k-tiles (ys KT x nJm, ahs KT x R)  |  P rows nIm x R
+  size_t other = sizeof(float2) * (size_t)R * p->nIm;
   size_t avail = maxsmem - fixed;
   int KT = (int)(avail / (sizeof(float2) * (size_t)(p->nJm + R)));
   if (KT > Smax) KT = Smax;
@@ -116,6 +121,72 @@ static bool rows_make_plan(int nx, int ny, int R, int Smax, int CL, RowsPlan* p)
   return true;
 }
 
+// Hermitian R x R from a packed lower triangle: M[r][q]
+TT_DEV float2 herm_at(const float2* P, int r, int q) {
+  return r >= q ? P[r * (r + 1) / 2 + q] : cconj(P[q * (q + 1) / 2 + r]);
+}
+
+// ---------------------------------------------------------------- cold paths (kept out of line)
+// Static row table validation: range and duplicates (observation.py:41-55).
+static __device__ __noinline__ int load_static_rows(const tt_rows_args& a, int f, int s, int* rows, int* flags,
+                                                    int* sh_err) {
+  const int tid = threadIdx.x, NT = blockDim.x, nx = a.nx, Smax = a.max_rows;
+  const int* tab_rows = a.rows_tab + ((size_t)f * a.nslices + s) * Smax;
+  const int cnt = a.rows_cnt[(size_t)f * a.nslices + s];
+  for (int i = tid; i < nx; i += NT) flags[i] = 0;
+  __syncthreads();
+  int S = 0;
+  if (cnt < 0 || cnt > Smax) {
+    if (tid == 0) atomicOr(sh_err, TT_ST_OVERFLOW);
+  } else {
+    for (int k = tid; k < cnt; k += NT) {
+      const int i = tab_rows[k];
+      rows[k] = i;
+      if (i < 0 || i >= nx) atomicOr(sh_err, TT_ST_BADROW);
+      else if (atomicAdd(&flags[i], 1) > 0) atomicOr(sh_err, TT_ST_DUPROW);
+    }
+    S = cnt;
+  }
+  __syncthreads();
+  if (*sh_err & (TT_ST_BADROW | TT_ST_DUPROW | TT_ST_OVERFLOW)) S = 0;
+  return S;
+}
+
+// Residual e = Y - Ah_S diag(gamma) Bh^T on this CTA's columns (pre-update),
+// in measurement order (tracker.py:388, StepReport.residual).
+static __device__ __noinline__ void write_residual(const tt_rows_args& a, const RowsPlan& pl, int f, int s, int S,
+                                                   int j0, int nJ, const int* rows, const float2* g_ahs,
+                                                   const float2* gamf, const float2* bhl, float2* ys, float2* ahs) {
+  const int tid = threadIdx.x, NT = blockDim.x, R = a.rank, ny = a.ny, Smax = a.max_rows, KT = pl.KT;
+  for (int k0 = 0; k0 < S; k0 += KT) {
+    const int kt = min(KT, S - k0);
+    for (int o = tid; o < kt * nJ; o += NT) {
+      const int kk = o / nJ, jj = o - kk * nJ;
+      const float2* src = a.y_mode == TT_Y_GATHER
+                              ? (const float2*)a.ysrc + (size_t)f * a.y_frame_stride + (size_t)s * a.y_slice_stride +
+                                    (size_t)rows[k0 + kk] * ny + j0
+                              : (const float2*)a.ysrc + (((size_t)f * a.nslices + s) * Smax + k0 + kk) * ny + j0;
+      ys[kk * pl.nJm + jj] = src[jj];
+    }
+    for (int o = tid; o < kt * R; o += NT) {
+      float2 v;
+      v.x = __ldcg(&g_ahs[(size_t)k0 * R + o].x);
+      v.y = __ldcg(&g_ahs[(size_t)k0 * R + o].y);
+      ahs[o] = cmul(v, gamf[o % R]);
+    }
+    __syncthreads();
+    for (int o = tid; o < kt * nJ; o += NT) {
+      const int kk = o / nJ, jj = o - kk * nJ;
+      float2 e = ys[kk * pl.nJm + jj];
+      float2 sacc = make_float2(0.f, 0.f);
+      for (int r = 0; r < R; ++r) sacc = cfma(ahs[kk * R + r], bhl[jj * R + r], sacc);
+      float2* dst = (float2*)a.resid_out + (((size_t)f * a.nslices + s) * Smax + k0 + kk) * ny + j0 + jj;
+      *dst = csub(e, sacc);
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------- the kernel
 __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_constant__ tt_rows_args a,
                                                              const __grid_constant__ RowsPlan pl) {
@@ -128,6 +199,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
   const int nx = a.nx, ny = a.ny, R = a.rank, Smax = a.max_rows, Rp = pl.Rp;
   const int i0 = part_begin(nx, CL, c), nI = part_begin(nx, CL, c + 1) - i0;
   const int j0 = part_begin(ny, CL, c), nJ = part_begin(ny, CL, c + 1) - j0;
+  const int KT = pl.KT;
 
   float2* ahl = (float2*)(smem + pl.o_ahl);
   float2* bhl = (float2*)(smem + pl.o_bhl);
@@ -138,18 +210,32 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
   float2* gb32 = (float2*)(smem + pl.o_gb32);
   double2* gam = (double2*)(smem + pl.o_vec);
   double2* hv = gam + R;
-  double* nrm = (double*)(hv + R);
-  float2* gamf = (float2*)(nrm + R);
-  double* scal = (double*)(gamf + R);  // 8 scalars
+  double2* hsave = hv + R;
+  double* nrm = (double*)(hsave + R);
+  double* inrm = nrm + R;
+  double* inv = inrm + R;
+  double* gda = inv + R;
+  double* gdb = gda + R;
+  float2* gamf = (float2*)(gdb + R);
+  double* scal = (double*)(gamf + R);  // 16 scalars
+  double2* colb = (double2*)(scal + 16);
+  double* blk = (double*)(colb + 4 * (R + 1));
+  double2* zf = (double2*)(blk + 4 * (R / 2 + 1));
+  unsigned short* tab = (unsigned short*)(smem + pl.o_tab);
   int* flags = (int*)(smem + pl.o_flags);
   int* rows = (int*)(smem + pl.o_rows);
+  int* forced = (int*)(smem + pl.o_forced);
+  float2* wacc = (float2*)(smem + pl.o_wacc);
   float2* ys = (float2*)(smem + pl.o_u2);
-  float2* ahs = ys + (size_t)pl.KT * pl.nJm;
-  float2* wbuf = (float2*)(smem + pl.o_u2);
+  float2* ahs = ys + (size_t)KT * pl.nJm;
   float2* prow = (float2*)(smem + pl.o_u2);
   double* red = (double*)(smem + pl.o_red);
-  int* ired = (int*)red;
   __shared__ int sh_S, sh_flag, sh_err;
+  long long* pclk = (a.phase_clock != nullptr && blockIdx.x == 0) ? (long long*)a.phase_clock : nullptr;
+#define STAMP(k)                                                             \
+  do {                                                                       \
+    if (pclk != nullptr && tid == 0) pclk[(size_t)f * 32 + (k)] = clock64(); \
+  } while (0)
 
   // global scratch for this slice
   const RowsScratch L = rows_scratch_layout(nx, ny, R, Smax, CL);
@@ -164,13 +250,16 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
   double2* g_hp = (double2*)(sb + L.hp);
   double* g_yn = (double*)(sb + L.yn);
 
-  // ---- load resident state
+  // ---- load resident state and constants once
   {
     const float2* src = (const float2*)a.ah_in + ((size_t)s * nx + i0) * R;
     for (int o = tid; o < nI * R; o += NT) ahl[o] = src[o];
     const float2* srb = (const float2*)a.bh_in + ((size_t)s * ny + j0) * R;
     for (int o = tid; o < nJ * R; o += NT) bhl[o] = srb[o];
+    if (a.policy == TT_POLICY_INFORMATIVE)
+      for (int m = tid; m < a.nforced; m += NT) forced[m] = a.forced[m];
   }
+  ldl_table_init(tab, R);
   double alpha_bar = a.alpha_bar ? a.alpha_bar[s] : 0.0;
   uint64_t ppos = (a.policy == TT_POLICY_INFORMATIVE && a.philox_pos) ? a.philox_pos[s] : 0ull;
   int status = 0;
@@ -180,7 +269,8 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
   for (int f = 0; f < a.frames; ++f) {
     const long long t = a.t0 + f;
     const double lt = a.lam / (double)t;
-    // ======== (a) column norms of Ah (own rows) and packed GB partials
+    STAMP(0);
+    // ======== (a) column-norm partials of Ah (own rows) and packed GB partials
     for (int r = warp; r < R; r += nwarps) {
       double acc = 0.0;
       for (int i = lane; i < nI; i += 32) {
@@ -191,97 +281,84 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       if (lane == 0) __stcg(&g_cn[c * R + r], acc);
     }
     for (int e = tid; e < Rp; e += NT) {
-      int r, q;
-      tri_decode(e, r, q);
-      double2 acc = make_double2(0.0, 0.0);
-      for (int jj = 0; jj < nJ; ++jj) acc = zfma_cj(bhl[jj * R + r], bhl[jj * R + q], acc);
+      const int ij = tab[e];
+      const int r = ij >> 8, q = ij & 255;
+      double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
+      int jj = 0;
+      for (; jj + 1 < nJ; jj += 2) {
+        acc = zfma_cj(bhl[jj * R + r], bhl[jj * R + q], acc);
+        acc2 = zfma_cj(bhl[(jj + 1) * R + r], bhl[(jj + 1) * R + q], acc2);
+      }
+      if (jj < nJ) acc = zfma_cj(bhl[jj * R + r], bhl[jj * R + q], acc);
+      acc = zadd(acc, acc2);
       __stcg(&g_gbp[(size_t)c * Rp + e].x, acc.x);
       __stcg(&g_gbp[(size_t)c * Rp + e].y, acc.y);
     }
+    STAMP(1);
     cluster_barrier();  // ---------------------------------------------- B1
-    for (int e = eb + tid; e < ee; e += NT) {
-      double2 acc = make_double2(0.0, 0.0);
-      for (int cc = 0; cc < CL; ++cc) {
-        acc.x += __ldcg(&g_gbp[(size_t)cc * Rp + e].x);
-        acc.y += __ldcg(&g_gbp[(size_t)cc * Rp + e].y);
-      }
-      __stcg(&g_gb[e].x, acc.x);
-      __stcg(&g_gb[e].y, acc.y);
+    STAMP(2);
+    for (int e = eb + tid - 32; tid >= 32 && e < ee; e += NT - 32) {
+      const double2 g = sum_parts2(g_gbp + e, (size_t)Rp, CL);
+      __stcg(&g_gb[e].x, g.x);
+      __stcg(&g_gb[e].y, g.y);
     }
-    if (tid < R) {
-      double acc = 0.0;
-      for (int cc = 0; cc < CL; ++cc) acc += __ldcg(&g_cn[cc * R + tid]);
-      nrm[tid] = acc;
+    for (int r = tid; r < R && tid < 32; r += 32) {
+      const double n2 = sum_parts(g_cn + r, (size_t)R, CL);
+      nrm[r] = n2;
+      inrm[r] = n2 > 0.0 ? fast_rcp(n2) : 0.0;
     }
     if (tid == 0) sh_err = 0;
     __syncthreads();
-    double anorm2 = 0.0;
-    for (int r = 0; r < R; ++r) anorm2 += nrm[r];
+    if (warp == 0) {  // ||Ah||^2, fixed order
+      double v = 0.0;
+      for (int r = lane; r < R; r += 32) v += nrm[r];
+      v = warp_sum(v);
+      if (lane == 0) scal[1] = v;
+    }
 
     int S = 0;
     if (a.policy == TT_POLICY_INFORMATIVE) {
       // raw row scores for own rows (sampler.py:77-85, :126)
+      const double cs = (double)ny, cr = (double)R, cd = 1.0 / ((double)R * (double)(nx + ny));
       for (int i = tid; i < nI; i += NT) {
         double e = 0.0;
         for (int r = 0; r < R; ++r) {
           const float2 v = ahl[i * R + r];
-          const double n2 = nrm[r];
-          if (n2 > 0.0) e += ((double)v.x * v.x + (double)v.y * v.y) / n2;
+          e = fma((double)v.x * v.x + (double)v.y * v.y, inrm[r], e);
         }
-        const double sc = ((double)ny * e + (double)R) / ((double)R * (double)(nx + ny));
-        __stcg(&g_sraw[i0 + i], sc);
+        __stcg(&g_sraw[i0 + i], (cs * e + cr) * cd);
       }
-      if (tid < R && nrm[tid] == 0.0) sh_err = TT_ST_ZEROCOL;
+      if (tid < R && nrm[tid] == 0.0) atomicOr(&sh_err, TT_ST_ZEROCOL);
+      STAMP(3);
       cluster_barrier();  // -------------------------------------------- B2
-      double loc = 0.0;
-      for (int i = tid; i < nx; i += NT) {
-        const double v = __ldcg(&g_sraw[i]);
-        pbuf[i] = v;
-      }
-      __syncthreads();
-      // deterministic sums over contiguous chunks
+      STAMP(4);
+      // probabilities: normalise, blend with the uniform law (sampler.py:88-92);
+      // the final renormalisation is folded into cdf /= cdf[-1] of the draw.
       const int chunk = (nx + NT - 1) / NT;
       const int q0 = min(nx, tid * chunk), q1 = min(nx, q0 + chunk);
-      loc = 0.0;
-      for (int i = q0; i < q1; ++i) loc += pbuf[i];
-      const double S1 = block_sum(loc, red);
-      loc = 0.0;
+      double loc = 0.0;
       for (int i = q0; i < q1; ++i) {
-        const double v = (1.0 - a.beta) * (pbuf[i] / S1) + a.beta / (double)nx;  // sampler.py:88-92
+        const double v = __ldcg(&g_sraw[i]);
         pbuf[i] = v;
         loc += v;
       }
-      const double S2 = block_sum(loc, red);
-      for (int i = q0; i < q1; ++i) pbuf[i] = pbuf[i] / S2;
+      const double S1 = block_sum(loc, red);
+      const double w1 = (1.0 - a.beta) / S1, w0 = a.beta / (double)nx;
+      for (int i = q0; i < q1; ++i) pbuf[i] = fma(pbuf[i], w1, w0);
       __syncthreads();
+      STAMP(20);
       const int ndraw = a.k_draws - a.nforced;
       int Sd;
-      draw_with_replacement_block(pbuf, cdf, flags, rows, Sd, nx, ndraw > 0 ? ndraw : 0, a.forced, a.nforced,
+      draw_with_replacement_block<false>(pbuf, cdf, flags, rows, Sd, nx, ndraw > 0 ? ndraw : 0, forced, a.nforced,
                                   a.key0, a.key1 + (uint64_t)s, ppos, red, &sh_flag);
       ppos += (uint64_t)(ndraw > 0 ? ndraw : 0);
       S = Sd;
     } else {
-      const int* tab = a.rows_tab + ((size_t)f * a.nslices + s) * Smax;
-      const int cnt = a.rows_cnt[(size_t)f * a.nslices + s];
-      for (int i = tid; i < nx; i += NT) flags[i] = 0;
-      __syncthreads();
-      if (cnt < 0 || cnt > Smax) {
-        if (tid == 0) sh_err |= TT_ST_OVERFLOW;
-        S = 0;
-      } else {
-        for (int k = tid; k < cnt; k += NT) {
-          const int i = tab[k];
-          rows[k] = i;
-          if (i < 0 || i >= nx) atomicOr(&sh_err, TT_ST_BADROW);
-          else if (atomicAdd(&flags[i], 1) > 0) atomicOr(&sh_err, TT_ST_DUPROW);
-        }
-        S = cnt;
-      }
-      __syncthreads();
-      if (sh_err & (TT_ST_BADROW | TT_ST_DUPROW | TT_ST_OVERFLOW)) S = 0;
+      S = load_static_rows(a, f, s, rows, flags, &sh_err);
     }
     if (tid == 0) sh_S = S;
     __syncthreads();
+    STAMP(5);
     S = sh_S;
     status |= sh_err;
 
@@ -295,90 +372,116 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         __stcg(&g_ahs[(size_t)k * R + r].y, v.y);
       }
     }
+    STAMP(6);
     cluster_arrive();  // ------------------------------------------------ B3 (split)
-    auto yptr = [&](int k) -> const float2* {
-      if (a.y_mode == TT_Y_GATHER)
-        return (const float2*)a.ysrc + (size_t)f * a.y_frame_stride + (size_t)s * a.y_slice_stride +
-               (size_t)rows[k] * ny + j0;
-      return (const float2*)a.ysrc + (((size_t)f * a.nslices + s) * Smax + k) * ny + j0;
-    };
-    const int KT = pl.KT;
+    const float2* ybase = a.y_mode == TT_Y_GATHER
+                              ? (const float2*)a.ysrc + (size_t)f * a.y_frame_stride + (size_t)s * a.y_slice_stride + j0
+                              : (const float2*)a.ysrc + ((size_t)f * a.nslices + s) * Smax * ny + j0;
+    const bool gather = a.y_mode == TT_Y_GATHER;
     {
       const int kt = min(KT, S);
       for (int o = tid; o < kt * nJ; o += NT) {
         const int kk = o / nJ, jj = o - kk * nJ;
-        cp_async8(&ys[kk * pl.nJm + jj], yptr(kk) + jj);
+        cp_async8(&ys[kk * pl.nJm + jj], ybase + (size_t)(gather ? rows[kk] : kk) * ny + jj);
       }
     }
+    for (int o = tid; o < nJ * R; o += NT) wacc[o] = make_float2(0.f, 0.f);
+    for (int e = eb + tid; e < ee; e += NT) G[e - eb] = make_double2(0.0, 0.0);
     cluster_wait();
+    STAMP(7);
 
     // ======== (c) heavy phase over k tiles: W, Z partials, GA (own entries), ||Y||^2
-    float2 acc[ROWS_WPT];
-#pragma unroll
-    for (int m = 0; m < ROWS_WPT; ++m) acc[m] = make_float2(0.f, 0.f);
-    for (int e = eb + tid; e < ee; e += NT) G[e - eb] = make_double2(0.0, 0.0);
     double ysq = 0.0;
     for (int k0 = 0; k0 < S; k0 += KT) {
       const int kt = min(KT, S - k0);
       if (k0 > 0) {
         for (int o = tid; o < kt * nJ; o += NT) {
           const int kk = o / nJ, jj = o - kk * nJ;
-          cp_async8(&ys[kk * pl.nJm + jj], yptr(k0 + kk) + jj);
+          cp_async8(&ys[kk * pl.nJm + jj], ybase + (size_t)(gather ? rows[k0 + kk] : k0 + kk) * ny + jj);
         }
       }
       for (int o = tid; o < kt * R; o += NT) {
         float2 v;
-        v.x = __ldcg(&g_ahs[(size_t)(k0) * R + o].x);
-        v.y = __ldcg(&g_ahs[(size_t)(k0) * R + o].y);
+        v.x = __ldcg(&g_ahs[(size_t)k0 * R + o].x);
+        v.y = __ldcg(&g_ahs[(size_t)k0 * R + o].y);
         ahs[o] = v;
       }
       cp_async_wait_all();
       __syncthreads();
+      if (k0 == 0) STAMP(16);
       for (int o = tid; o < kt * nJ; o += NT) {
         const int kk = o / nJ, jj = o - kk * nJ;
         const float2 v = ys[kk * pl.nJm + jj];
         ysq += (double)v.x * v.x + (double)v.y * v.y;
       }
-      // W[jj][r] += sum_k Y[k][jj] conj(Ah_S[k][r])
+      // W[jj][r] += sum_k Y[k][jj] conj(Ah_S[k][r])   (thread-owned smem accumulators)
+      for (int o = tid; o < nJ * R; o += 2 * NT) {
+        const int o2 = o + NT;
+        const bool two = o2 < nJ * R;
+        const int jj = o / R, r = o - jj * R;
+        const int jj2 = two ? o2 / R : jj, r2 = two ? o2 - jj2 * R : r;
+        float2 w = wacc[o], w2 = two ? wacc[o2] : make_float2(0.f, 0.f);
+#pragma unroll 4
+        for (int kk = 0; kk < kt; ++kk) {
+          w = cfma_conj(ys[kk * pl.nJm + jj], ahs[kk * R + r], w);
+          w2 = cfma_conj(ys[kk * pl.nJm + jj2], ahs[kk * R + r2], w2);
+        }
+        wacc[o] = w;
+        if (two) wacc[o2] = w2;
+      }
+      if (k0 == 0) STAMP(17);
+      // Z partial over own columns
+      for (int ob = tid; ob < kt * R; ob += 4 * NT) {
+        int kq[4], rq[4];
+        float2 z[4];
 #pragma unroll
-      for (int m = 0; m < ROWS_WPT; ++m) {
-        const int o = tid + m * NT;
-        if (o < nJ * R) {
-          const int jj = o / R, r = o - jj * R;
-          float2 w = acc[m];
-          for (int kk = 0; kk < kt; ++kk) w = cfma_conj(ys[kk * pl.nJm + jj], ahs[kk * R + r], w);
-          acc[m] = w;
+        for (int u = 0; u < 4; ++u) {
+          const int o = min(ob + u * NT, kt * R - 1);
+          kq[u] = o / R;
+          rq[u] = o - kq[u] * R;
+          z[u] = make_float2(0.f, 0.f);
+        }
+#pragma unroll 2
+        for (int jj = 0; jj < nJ; ++jj) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) z[u] = cfma_conj(ys[kq[u] * pl.nJm + jj], bhl[jj * R + rq[u]], z[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (ob + u * NT < kt * R) {
+            float2* dst = &g_zp[((size_t)c * Smax + k0 + kq[u]) * R + rq[u]];
+            __stcg(&dst->x, z[u].x);
+            __stcg(&dst->y, z[u].y);
+          }
         }
       }
-      // Z partial over own columns
-      for (int o = tid; o < kt * R; o += NT) {
-        const int kk = o / R, r = o - kk * R;
-        float2 z = make_float2(0.f, 0.f);
-        for (int jj = 0; jj < nJ; ++jj) z = cfma_conj(ys[kk * pl.nJm + jj], bhl[jj * R + r], z);
-        float2* dst = &g_zp[((size_t)c * Smax + k0 + kk) * R + r];
-        __stcg(&dst->x, z.x);
-        __stcg(&dst->y, z.y);
-      }
+      if (k0 == 0) STAMP(18);
       // GA own packed entries
-      for (int e = eb + tid; e < ee; e += NT) {
-        int r, q;
-        tri_decode(e, r, q);
-        double2 g = G[e - eb];
-        for (int kk = 0; kk < kt; ++kk) g = zfma_cj(ahs[kk * R + r], ahs[kk * R + q], g);
-        G[e - eb] = g;
+      const int nq = 4 * (ee - eb);
+      for (int base = tid & ~31; base < nq; base += NT) {  // warp-uniform trip count
+        const int eq = base + lane;
+        const int e = eb + (eq >> 2), part = eq & 3;
+        double2 g = make_double2(0.0, 0.0);
+        if (eq < nq) {
+          const int ij = tab[e];
+          const int r = ij >> 8, q = ij & 255;
+          for (int kk = part; kk < kt; kk += 4) g = zfma_cj(ahs[kk * R + r], ahs[kk * R + q], g);
+        }
+        // lanes 4m..4m+3 hold the parts of one entry: (p0 + p1) + (p2 + p3)
+        g.x += __shfl_xor_sync(0xffffffffu, g.x, 1);
+        g.y += __shfl_xor_sync(0xffffffffu, g.y, 1);
+        g.x += __shfl_xor_sync(0xffffffffu, g.x, 2);
+        g.y += __shfl_xor_sync(0xffffffffu, g.y, 2);
+        if (part == 0 && eq < nq) G[e - eb] = zadd(G[e - eb], g);
       }
+      if (k0 == 0) STAMP(19);
       __syncthreads();
     }
+    STAMP(8);
     // h partial: sum_jj conj(Bh[jj][r]) W[jj][r]
-#pragma unroll
-    for (int m = 0; m < ROWS_WPT; ++m) {
-      const int o = tid + m * NT;
-      if (o < nJ * R) wbuf[o] = acc[m];
-    }
-    __syncthreads();
     if (tid < R) {
       double2 h = make_double2(0.0, 0.0);
-      for (int jj = 0; jj < nJ; ++jj) h = zfma_cj(bhl[jj * R + tid], wbuf[jj * R + tid], h);
+      for (int jj = 0; jj < nJ; ++jj) h = zfma_cj(bhl[jj * R + tid], wacc[jj * R + tid], h);
       __stcg(&g_hp[c * R + tid].x, h.x);
       __stcg(&g_hp[c * R + tid].y, h.y);
     }
@@ -390,113 +493,96 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       const double yt = block_sum(ysq, red);
       if (tid == 0) __stcg(&g_yn[c], yt);
     }
+    STAMP(9);
     cluster_barrier();  // ---------------------------------------------- B4
+    STAMP(10);
 
-    // ======== (d) redundant fp64 solve
+    // ======== (d) redundant fp64 solve (every cross-CTA read is one parallel round trip)
     for (int e = tid; e < Rp; e += NT) {
-      int r, q;
-      tri_decode(e, r, q);
+      const int ij = tab[e];
+      const int r = ij >> 8, q = ij & 255;
       double2 gae, gbe;
       gae.x = __ldcg(&g_ga[e].x);
       gae.y = __ldcg(&g_ga[e].y);
       gbe.x = __ldcg(&g_gb[e].x);
       gbe.y = __ldcg(&g_gb[e].y);
       double2 gg = zmul(gae, gbe);
-      if (r == q) gg.x += a.lam;
+      if (r == q) {
+        gg.x += a.lam;
+        gda[r] = gae.x;
+        gdb[r] = gbe.x;
+      }
       G[e] = gg;
-      ga32[r * R + q] = to_f2(gae);
-      ga32[q * R + r] = to_f2(zconj(gae));
-      gb32[r * R + q] = to_f2(gbe);
-      gb32[q * R + r] = to_f2(zconj(gbe));
+      ga32[e] = to_f2(gae);
+      gb32[e] = to_f2(gbe);
     }
     if (tid < R) {
-      double2 h = make_double2(0.0, 0.0);
-      for (int cc = 0; cc < CL; ++cc) {
-        h.x += __ldcg(&g_hp[cc * R + tid].x);
-        h.y += __ldcg(&g_hp[cc * R + tid].y);
-      }
+      const double2 h = sum_parts2(g_hp + tid, (size_t)R, CL);
       hv[tid] = h;
+      hsave[tid] = h;
     }
-    if (tid == 0) {
-      double yn = 0.0;
-      for (int cc = 0; cc < CL; ++cc) yn += __ldcg(&g_yn[cc]);
-      scal[0] = yn;
-    }
+    if (tid == 32) scal[0] = sum_parts(g_yn, 1, CL);
     __syncthreads();
-    double bnorm2 = 0.0;  // ||Bh||^2 = trace(GB)
-    for (int r = 0; r < R; ++r) bnorm2 += __ldcg(&g_gb[tri_idx(r, r)].x);
-    const double energy = anorm2 + bnorm2;
+    if (warp == 0) {  // ||Bh||^2 = trace(GB)
+      double v = 0.0;
+      for (int r = lane; r < R; r += 32) v += gdb[r];
+      v = warp_sum(v);
+      if (lane == 0) scal[2] = v;
+    }
+    STAMP(11);
 
     double mu_used = 0.0, alpha = 0.0, cost;
-    bool update = S > 0;
+    const bool update = S > 0;
     if (update) {
-      block_ldl_solve(G, hv, gam, R);
-      // h was overwritten by the elimination: reload it for the cost
-      if (tid < R) {
-        double2 h = make_double2(0.0, 0.0);
-        for (int cc = 0; cc < CL; ++cc) {
-          h.x += __ldcg(&g_hp[cc * R + tid].x);
-          h.y += __ldcg(&g_hp[cc * R + tid].y);
+      {
+        const int E = Rp + R;  // augmented entries; registers per thread
+        if (E <= 2 * ROWS_NT) block_ldl2_solve<2>(G, hv, gam, colb, blk, zf, R);
+        else if (E <= 4 * ROWS_NT) block_ldl2_solve<4>(G, hv, gam, colb, blk, zf, R);
+        else block_ldl2_solve<9>(G, hv, gam, colb, blk, zf, R);
+      }
+      STAMP(12);
+      if (warp == 0) {
+        double gh = 0.0, gg = 0.0, top = 0.0;
+        for (int r = lane; r < R; r += 32) {
+          const double2 g = gam[r], h = hsave[r];
+          gh += g.x * h.x + g.y * h.y;  // Re(conj(g) h)
+          const double g2 = g.x * g.x + g.y * g.y;
+          gg += g2;
+          top = fmax(top, g2 * fmax(gda[r], gdb[r]));
+          gamf[r] = to_f2(g);
         }
-        hv[tid] = h;
-        gamf[tid] = to_f2(gam[tid]);
+        gh = warp_sum(gh);
+        gg = warp_sum(gg);
+        top = warp_max(top);
+        if (lane == 0) {
+          scal[3] = gh;
+          scal[4] = gg;
+          scal[5] = top;
+        }
       }
       __syncthreads();
-      double gh = 0.0, gg = 0.0, top = 0.0;
-      for (int r = 0; r < R; ++r) {
-        const double2 g = gam[r], h = hv[r];
-        gh += g.x * h.x + g.y * h.y;  // Re(conj(g) h)
-        const double g2 = g.x * g.x + g.y * g.y;
-        gg += g2;
-        const double da = __ldcg(&g_ga[tri_idx(r, r)].x), db = __ldcg(&g_gb[tri_idx(r, r)].x);
-        top = fmax(top, g2 * fmax(da, db));
-      }
-      const double e2 = scal[0] - gh - a.lam * gg;
+      const double energy = scal[1] + scal[2];
+      const double e2 = scal[0] - scal[3] - a.lam * scal[4];
       cost = 0.5 * e2 + 0.5 * lt * energy;
       if (a.step_mode == TT_STEP_HESSIAN) {
-        alpha = fmin(fmax(lt + top, a.c_floor), a.c_cap);  // tracker.py:364
+        alpha = fmin(fmax(lt + scal[5], a.c_floor), a.c_cap);  // tracker.py:364
         alpha_bar += alpha;
         mu_used = 1.0 / alpha_bar;
       } else {
         mu_used = a.mu;
       }
-      if (!isfinite(cost) || !isfinite(gh)) status |= TT_ST_NONFINITE;
+      if (!isfinite(cost) || !isfinite(scal[3])) status |= TT_ST_NONFINITE;
     } else {
+      __syncthreads();
       if (tid < R) {
         gam[tid] = make_double2(0.0, 0.0);
         gamf[tid] = make_float2(0.f, 0.f);
       }
-      cost = 0.5 * lt * energy;
+      cost = 0.5 * lt * (scal[1] + scal[2]);
       __syncthreads();
     }
-
-    // optional residual e = Y - Ah_S diag(gamma) Bh^T on own columns (pre-update)
-    if (a.resid_out != nullptr) {
-      for (int k0 = 0; k0 < S; k0 += KT) {
-        const int kt = min(KT, S - k0);
-        for (int o = tid; o < kt * nJ; o += NT) {
-          const int kk = o / nJ, jj = o - kk * nJ;
-          ys[kk * pl.nJm + jj] = yptr(k0 + kk)[jj];
-        }
-        for (int o = tid; o < kt * R; o += NT) {
-          float2 v;
-          v.x = __ldcg(&g_ahs[(size_t)k0 * R + o].x);
-          v.y = __ldcg(&g_ahs[(size_t)k0 * R + o].y);
-          ahs[o] = cmul(v, gamf[o % R]);
-        }
-        __syncthreads();
-        for (int o = tid; o < kt * nJ; o += NT) {
-          const int kk = o / nJ, jj = o - kk * nJ;
-          float2 e = ys[kk * pl.nJm + jj];
-          float2 sacc = make_float2(0.f, 0.f);
-          for (int r = 0; r < R; ++r) sacc = cfma(ahs[kk * R + r], bhl[jj * R + r], sacc);
-          e = csub(e, sacc);
-          float2* dst = (float2*)a.resid_out + (((size_t)f * a.nslices + s) * Smax + k0 + kk) * ny + j0 + jj;
-          *dst = e;
-        }
-        __syncthreads();
-      }
-    }
+    if (a.resid_out != nullptr) write_residual(a, pl, f, s, S, j0, nJ, rows, g_ahs, gamf, bhl, ys, ahs);
+    STAMP(13);
 
     // ======== (e) updates (k-space): Ah <- cfac Ah + mu conj(g) P_S ; Bh <- cfac Bh + mu conj(g) Q
     if (update) {
@@ -509,34 +595,24 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         if (i >= i0 && i < i0 + nI) flags[i - i0] = k;
       }
       __syncthreads();
+      // P_S rows owned here: Z (summed over the cluster) - Ah_S diag(gamma) GB^T
       for (int o = tid; o < nI * R; o += NT) {
         const int li = o / R, r = o - li * R;
         const int k = flags[li];
         if (k >= 0) {
-          float2 z = make_float2(0.f, 0.f);
-          for (int cc = 0; cc < CL; ++cc) {
-            const float2* src = &g_zp[((size_t)cc * Smax + k) * R + r];
-            z.x += __ldcg(&src->x);
-            z.y += __ldcg(&src->y);
-          }
+          const float2 z = sum_parts_f2(g_zp + (size_t)k * R + r, (size_t)Smax * R, CL);
           float2 corr = make_float2(0.f, 0.f);
-          for (int q = 0; q < R; ++q) corr = cfma(cmul(ahl[li * R + q], gamf[q]), gb32[r * R + q], corr);
+          for (int q = 0; q < R; ++q) corr = cfma(cmul(ahl[li * R + q], gamf[q]), herm_at(gb32, r, q), corr);
           prow[o] = csub(z, corr);
         }
       }
-      // new Bh values (need old Bh everywhere) into registers
-      float2 nb[ROWS_WPT];
-#pragma unroll
-      for (int m = 0; m < ROWS_WPT; ++m) {
-        const int o = tid + m * NT;
-        nb[m] = make_float2(0.f, 0.f);
-        if (o < nJ * R) {
-          const int jj = o / R, r = o - jj * R;
-          float2 corr = make_float2(0.f, 0.f);
-          for (int q = 0; q < R; ++q) corr = cfma(cmul(bhl[jj * R + q], gamf[q]), ga32[r * R + q], corr);
-          const float2 qv = csub(acc[m], corr);
-          nb[m] = cadd(cscale(bhl[o], cfac), cscale(cmul(cconj(gamf[r]), qv), muf));
-        }
+      // Q = W - Bh diag(gamma) GA^T ; new Bh into wacc (W is consumed in place)
+      for (int o = tid; o < nJ * R; o += NT) {
+        const int jj = o / R, r = o - jj * R;
+        float2 corr = make_float2(0.f, 0.f);
+        for (int q = 0; q < R; ++q) corr = cfma(cmul(bhl[jj * R + q], gamf[q]), herm_at(ga32, r, q), corr);
+        const float2 qv = csub(wacc[o], corr);
+        wacc[o] = cadd(cscale(bhl[o], cfac), cscale(cmul(cconj(gamf[r]), qv), muf));
       }
       __syncthreads();
       for (int o = tid; o < nI * R; o += NT) {
@@ -545,13 +621,10 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         if (flags[li] >= 0) v = cadd(v, cscale(cmul(cconj(gamf[r]), prow[o]), muf));
         ahl[o] = v;
       }
-#pragma unroll
-      for (int m = 0; m < ROWS_WPT; ++m) {
-        const int o = tid + m * NT;
-        if (o < nJ * R) bhl[o] = nb[m];
-      }
+      for (int o = tid; o < nJ * R; o += NT) bhl[o] = wacc[o];
       __syncthreads();
     }
+    STAMP(14);
 
     // ======== outputs
     const size_t fs = (size_t)f * a.nslices + s;
@@ -575,7 +648,9 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       for (int o = tid; o < nJ * R; o += NT) dst[o] = bhl[o];
     }
     __syncthreads();
+    STAMP(15);
   }
+#undef STAMP
 
   // ---- write back resident state
   {
