@@ -47,41 +47,91 @@ def center_lines(n, m):
 
 
 CONFIGS = {
+    "c1": dict(n=128, R=10, T=64, lam=0.1, period=16.0, vd=0.25, mu=0.01, slices=1,
+               desc="config 1: 128x128 complex64 cine phantom, T=64, R=10, lambda=0.1, variable-density rows "
+                    "25% (32 rows/frame, alpha=-1, Philox), Fixed mu=0.01"),
     "c2": dict(n=256, R=20, T=200, lam=0.05, period=20.0, K=64, forced=center_lines(256, 16), beta=0.1, mu=0.01,
                slices=1, desc="config 2: 256x256 complex64 cine phantom, T=200, R=20, lambda=0.05, informative "
                               "rows K=64 (4x) incl. 16 centre lines, beta=0.1, Philox draws, Fixed mu=0.01"),
     "c3": dict(n=256, R=16, T=100, lam=0.05, period=16.0, K=52, forced=(0,), beta=0.1, mu=0.01, slices=64,
                desc="config 3: 64 independent 256x256 slices, T=100, R=16, 20% informative rows (K=52, forced DC)"),
+    "c4": dict(n=1024, R=32, T=256, lam=0.1, period=16.0, vd=0.125, mu=0.01, slices=1,
+               desc="config 4: 1024x1024 complex64 cine phantom, T=256, R=32, lambda=0.1, variable-density rows "
+                    "12.5% (128 rows/frame), Fixed mu=0.01 (single GPU, unsharded)"),
 }
 
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clock and throttle reasons sampled during the timed region: NVML polled
+    every ~1 ms from a thread (the timed region is tens of ms), falling back to
+    `nvidia-smi -lms 100` when NVML is unavailable."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown"}
 
     def __init__(self, index):
         self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
         self.proc = None
         self.lines = []
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            get_r = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+
+            def poll():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                        r = int(get_r(h))
+                        for bit, name in self.REASONS.items():
+                            if r & bit:
+                                self.reasons.add(name)
+                    except Exception:
+                        pass
+                    time.sleep(0.001)
+
+            self.thread = threading.Thread(target=poll, daemon=True)
             self.thread.start()
-        except FileNotFoundError:
-            self.proc = None
+        except Exception:
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                     "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                     "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self.thread = threading.Thread(target=self._read, daemon=True)
+                self.thread.start()
+            except FileNotFoundError:
+                self.proc = None
         return self
 
     def _read(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                self.samples.append(float(parts[0]))
+                self.max_mhz = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    self.reasons.add(nm)
 
     def __exit__(self, *exc):
+        self._stop.set()
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -90,24 +140,10 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[4:8]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
 # ------------------------------------------------------------------ data
@@ -146,7 +182,12 @@ def measured_peaks():
 def cpu_oracle_fps(cfg, frames, ks, A0, B0):
     from oracle import tt_oracle as O
 
-    pol = {"kind": "informative", "k": cfg["K"], "forced": list(cfg["forced"]), "beta": cfg["beta"], "key": (2024, 0)}
+    if "vd" in cfg:
+        gen = np.random.Generator(np.random.Philox(key=2024))
+        pol = {"kind": "static", "rows": [O.vd_rows(cfg["n"], -1.0, cfg["vd"], gen.random) for _ in range(frames)]}
+    else:
+        pol = {"kind": "informative", "k": cfg["K"], "forced": list(cfg["forced"]), "beta": cfg["beta"],
+               "key": (2024, 0)}
     t0 = time.perf_counter()
     O.online_run(ks[:frames, 0], A0[0], B0[0], cfg["lam"], ("fixed", cfg["mu"]), pol)
     dt = time.perf_counter() - t0
@@ -201,19 +242,30 @@ def run_ours(args, cfg):
     L.load()
 
     # slices of this rank: replicas for c2 (weak), shards for c3 (strong)
+    from paper_1609_04104_b200.sharding import slice_partition
+
     if cfg["slices"] == 1:
         slice_ids = [rank]
         scaling = "weak"
     else:
-        per = cfg["slices"] // world
-        slice_ids = list(range(rank * per, (rank + 1) * per))
+        slice_ids = slice_partition(cfg["slices"], world, rank)
         scaling = "strong"
     ns = len(slice_ids)
     n, R, T = cfg["n"], cfg["R"], cfg["T"]
     ks_np, clean_np = make_data(cfg, slice_ids)
     A0, B0 = init_factors(cfg, slice_ids)
 
-    pol = tt.Informative(k=cfg["K"], forced=cfg["forced"], beta=cfg["beta"], key0=2024, key1=slice_ids[0])
+    if "vd" in cfg:
+        # static variable-density masks per frame and slice (observation.py:300-323), drawn on device
+        Smax = int(np.ceil(cfg["vd"] * n))
+        tab = np.zeros((T, ns, Smax), np.int64)
+        for si, s_id in enumerate(slice_ids):
+            gen = np.random.Generator(np.random.Philox(key=2024 + (s_id << 64)))
+            for f in range(T):
+                tab[f, si] = tt.variable_density_rows(n, -1.0, cfg["vd"], gen)
+        pol = tt.StaticRows(tab, np.full((T, ns), Smax))
+    else:
+        pol = tt.Informative(k=cfg["K"], forced=cfg["forced"], beta=cfg["beta"], key0=2024, key1=slice_ids[0])
     eng = tt.OnlineEngine(n, n, R, ns, cfg["lam"], tt.Fixed(cfg["mu"]), pol, cluster=args.cluster)
     eng.set_image_factors(A0, B0)
     ah0, bh0 = eng.ah.clone(), eng.bh.clone()
@@ -284,7 +336,7 @@ def run_ours(args, cfg):
 
     # ---- roofline of the dominant kernel (tt_rows_kernel) from the BASELINE byte model
     S_avg = float(cnt.mean())
-    b_upd = 8 * S_avg * n + 4 * S_avg + 16 * R * (2 * n) + 8 * R + 8 * n       # per slice-frame
+    b_upd = 8 * S_avg * n + 4 * S_avg + 16 * R * (2 * n) + 8 * R + (8 * n if "K" in cfg else 0)
     b_rec = 8 * n * n
     f_sep = 16 * S_avg * n * R + 16 * (S_avg + n) * R * R + 10 * R * 2 * n * math.log2(n) + 16 * R * 2 * n
     hbm_peak, sm_max, peak_kind = measured_peaks()

@@ -454,3 +454,46 @@ def online_run(kspace, A, B, lam, step, policy, clean=None, t0=1, alpha_bar=0.0,
         out["recon"].append(X)
     out["final"] = (A, B, t, alpha_bar, pos)
     return out
+
+
+# ---------------------------------------------------------------------------
+# row-sharded step — decomposition check, k-space form
+# ---------------------------------------------------------------------------
+def row_shard_partials(Ah, Bh, rows, Y, r0, r1):
+    """Partials of one rank owning k-space rows [r0, r1) of Ah (full Ah given
+    for convenience; only the owned rows are read). Returns the payload that
+    is summed across ranks: W (Ny x R), GA (R x R), ||Y_own||^2, ||Ah_own||^2."""
+    rows = np.asarray(rows)
+    own = np.flatnonzero((rows >= r0) & (rows < r1))
+    As = np.asarray(Ah, np.complex128)[rows[own]]
+    Yo = np.asarray(Y, np.complex128)[own]
+    W = Yo.T @ np.conj(As)
+    GA = As.conj().T @ As
+    return dict(W=W, GA=GA, yn=float(np.sum(np.abs(Yo) ** 2)),
+                an=float(np.sum(np.abs(np.asarray(Ah, np.complex128)[r0:r1]) ** 2)), own=own)
+
+
+def row_shard_finish(Ah, Bh, rows, Y, r0, r1, red, lam, t, mu):
+    """Given the all-reduced payload `red`, solve redundantly and update the
+    owned rows of Ah and the replicated Bh (fixed step). Returns
+    (Ah_own_new, Bh_new, gamma, cost)."""
+    Ah = np.asarray(Ah, np.complex128)
+    Bh = np.asarray(Bh, np.complex128)
+    rows = np.asarray(rows)
+    own = np.flatnonzero((rows >= r0) & (rows < r1))
+    GB = Bh.conj().T @ Bh
+    W, GA = red["W"], red["GA"]
+    h = np.sum(np.conj(Bh) * W, axis=0)
+    R = Ah.shape[1]
+    gamma = np.linalg.solve(GA * GB + lam * np.eye(R), h)
+    cost = 0.5 * (red["yn"] - float(np.real(np.vdot(gamma, h))) - lam * float(np.vdot(gamma, gamma).real)) \
+        + 0.5 * (lam / t) * (red["an"] + float(np.real(np.trace(GB))))
+    As = Ah[rows[own]]
+    Z = np.asarray(Y, np.complex128)[own] @ np.conj(Bh)
+    P = Z - (As * gamma[None, :]) @ GB.T
+    Q = W - (Bh * gamma[None, :]) @ GA.T
+    c = 1.0 - mu * lam / t
+    A_own = c * Ah[r0:r1].copy()
+    A_own[rows[own] - r0] += mu * np.conj(gamma)[None, :] * P
+    B_new = c * Bh + mu * np.conj(gamma)[None, :] * Q
+    return A_own, B_new, gamma, cost

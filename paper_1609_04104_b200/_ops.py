@@ -73,6 +73,12 @@ class RowsScratch:
         self.key = (nslices, nx, ny, rank, max_rows, self.cluster)
 
 
+def rows_plan_fits(nx, ny, rank, max_rows) -> bool:
+    cl = C.c_int(0)
+    sm = C.c_size_t(0)
+    return L.lib().tt_rows_plan(nx, ny, rank, max_rows, 0, C.byref(cl), C.byref(sm)) == 0
+
+
 _scratch_cache: dict = {}
 
 

@@ -555,3 +555,154 @@ TT_DEV void block_ldl2_solve(double2* Gio, const double2* hin, double2* gam, dou
   }
   __syncthreads();
 }
+
+// ---------------------------------------------------------------- register-tiled complex GEMM
+// C(m, n) = sum_{k<K} opA(A[m*a_m + k*a_k]) * opB(B[k*b_k + n*b_n]) over shared
+// memory operands (complex fp32). Work item = (TM x TN output tile, k part);
+// with KS > 1 the parts are summed in fixed order through `red`
+// (KS * M * N float2) after a barrier, so results are deterministic. Every
+// (m, n) is delivered once to out(m, n, value). Callers synchronise after.
+template <int TM, int TN, bool CA, bool CB, typename Out>
+TT_DEV void cgemm_tile(int M, int N, int K, const float2* A, int a_m, int a_k, const float2* B, int b_k, int b_n,
+                       int KS, float2* red, Out out) {
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int tn = (N + TN - 1) / TN, tiles = ((M + TM - 1) / TM) * tn;
+  const int items = tiles * KS;
+  for (int it = tid; it < items; it += NT) {
+    const int tile = it % tiles, ks = it / tiles;
+    const int m0 = (tile / tn) * TM, n0 = (tile % tn) * TN;
+    const int k0 = (K * ks) / KS, k1 = (K * (ks + 1)) / KS;
+    float2 acc[TM][TN];
+#pragma unroll
+    for (int u = 0; u < TM; ++u)
+#pragma unroll
+      for (int v = 0; v < TN; ++v) acc[u][v] = make_float2(0.f, 0.f);
+    const float2* Ap[TM];
+    const float2* Bp[TN];
+#pragma unroll
+    for (int u = 0; u < TM; ++u) Ap[u] = A + (size_t)min(m0 + u, M - 1) * a_m;
+#pragma unroll
+    for (int v = 0; v < TN; ++v) Bp[v] = B + (size_t)min(n0 + v, N - 1) * b_n;
+#pragma unroll 2
+    for (int k = k0; k < k1; ++k) {
+      float2 a[TM], b[TN];
+#pragma unroll
+      for (int u = 0; u < TM; ++u) {
+        a[u] = Ap[u][(size_t)k * a_k];
+        if (CA) a[u].y = -a[u].y;
+      }
+#pragma unroll
+      for (int v = 0; v < TN; ++v) {
+        b[v] = Bp[v][(size_t)k * b_k];
+        if (CB) b[v].y = -b[v].y;
+      }
+#pragma unroll
+      for (int u = 0; u < TM; ++u)
+#pragma unroll
+        for (int v = 0; v < TN; ++v) acc[u][v] = cfma(a[u], b[v], acc[u][v]);
+    }
+#pragma unroll
+    for (int u = 0; u < TM; ++u)
+#pragma unroll
+      for (int v = 0; v < TN; ++v) {
+        const int m = m0 + u, n = n0 + v;
+        if (m < M && n < N) {
+          if (KS == 1) out(m, n, acc[u][v]);
+          else red[((size_t)ks * M + m) * N + n] = acc[u][v];
+        }
+      }
+  }
+  if (KS > 1) {
+    __syncthreads();
+    for (int o = tid; o < M * N; o += NT) {
+      float2 s = red[o];
+      for (int ks = 1; ks < KS; ++ks) s = cadd(s, red[(size_t)ks * M * N + o]);
+      out(o / N, o % N, s);
+    }
+  }
+}
+
+// K-split factor that fills the block without exceeding the reduction buffer
+TT_DEV int gemm_split(int M, int N, int K, int TM, int TN, int red_cap) {
+  const int tiles = ((M + TM - 1) / TM) * ((N + TN - 1) / TN);
+  int ks = (int)blockDim.x / (tiles > 0 ? tiles : 1);
+  if (ks > K / 4) ks = K / 4;
+  if (ks > 8) ks = 8;
+  while (ks > 1 && ks * M * N > red_cap) --ks;
+  return ks < 1 ? 1 : ks;
+}
+
+// ---------------------------------------------------------------- warp-level draw (fused kernel)
+// Same semantics as draw_with_replacement_block<false> but executed by one
+// warp only (no CTA barriers): chunked warp scan, parallel Philox draws with
+// the 1e-12 ambiguity check and exact sequential fallback, flag compaction.
+// `p` may be unnormalised (the CDF is normalised by its last element).
+TT_DEV void warp_draw_with_replacement(const double* p, double* cdf, int* flags, int* rows, int* S_out, int n,
+                                       int ndraw, const int* forced, int nforced, uint64_t k0, uint64_t k1,
+                                       uint64_t pos) {
+  const int lane = threadIdx.x & 31;
+  const int chunk = (n + 31) / 32;
+  const int c0 = min(n, lane * chunk), c1 = min(n, c0 + chunk);
+  for (int exact = 0; exact < 2; ++exact) {
+    if (!exact) {
+      double loc = 0.0;
+      for (int i = c0; i < c1; ++i) loc += p[i];
+      double x = loc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      const double total = __shfl_sync(0xffffffffu, x, 31);
+      const double il = fast_rcp(total);
+      double run = x - loc;
+      for (int i = c0; i < c1; ++i) {
+        run += p[i];
+        cdf[i] = run * il;
+      }
+    } else {
+      if (lane == 0) {
+        double cacc = 0.0;
+        for (int i = 0; i < n; ++i) {
+          cacc += p[i];
+          cdf[i] = cacc;
+        }
+        const double last = cdf[n - 1];
+        for (int i = 0; i < n; ++i) cdf[i] = cdf[i] / last;
+      }
+    }
+    for (int i = c0; i < c1; ++i) flags[i] = 0;
+    __syncwarp();
+    int amb = 0;
+    for (int m = lane; m < ndraw; m += 32) {
+      const double u = philox_uniform(k0, k1, pos + (uint64_t)m);
+      const int idx = upper_bound_d(cdf, n, u);
+      if (!exact) {
+        const double lo = idx > 0 ? cdf[idx - 1] : -1.0;
+        const double hi = idx < n ? cdf[idx] : 2.0;
+        if (u - lo <= 1e-12 || hi - u <= 1e-12) amb = 1;
+      }
+      flags[idx < n ? idx : n - 1] = 1;
+    }
+    __syncwarp();
+    if (exact || !__any_sync(0xffffffffu, amb)) break;
+  }
+  for (int m = lane; m < nforced; m += 32) {
+    const int f = forced[m];
+    if (f >= 0 && f < n) flags[f] = 1;
+  }
+  __syncwarp();
+  int cnt = 0;
+  for (int i = c0; i < c1; ++i) cnt += flags[i];
+  int x = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  int o = x - cnt;
+  for (int i = c0; i < c1; ++i)
+    if (flags[i]) rows[o++] = i;
+  if (lane == 31) *S_out = x;
+  __syncwarp();
+}

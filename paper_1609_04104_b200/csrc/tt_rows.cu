@@ -44,8 +44,9 @@ namespace cg = cooperative_groups;
 #define ROWS_NT 256
 
 struct RowsPlan {
-  int CL, KT, nIm, nJm, Rp;
-  int o_ahl, o_bhl, o_u1, o_ga32, o_gb32, o_vec, o_tab, o_flags, o_rows, o_forced, o_wacc, o_u2, o_red;
+  int CL, KT, nIm, nJm, Rp, red_cap;
+  int o_ahl, o_bhl, o_u1, o_gaf, o_gbf, o_vec, o_tab, o_flags, o_rows, o_forced, o_own, o_wacc, o_zs, o_red2, o_u2,
+      o_red;
   int smem;
 };
 
@@ -73,13 +74,21 @@ __host__ __device__ inline RowsScratch rows_scratch_layout(int nx, int ny, int R
   return s;
 }
 
+static bool rows_make_plan_cap(int nx, int ny, int R, int Smax, int CL, int red_cap, RowsPlan* p);
+// The K-split reduction buffer of the small GEMMs is optional: when shared
+// memory is tight (R = 64 at large N) the plan drops it and every GEMM runs
+// with KS = 1.
 static bool rows_make_plan(int nx, int ny, int R, int Smax, int CL, RowsPlan* p) {
+  return rows_make_plan_cap(nx, ny, R, Smax, CL, 2048, p) || rows_make_plan_cap(nx, ny, R, Smax, CL, 0, p);
+}
+static bool rows_make_plan_cap(int nx, int ny, int R, int Smax, int CL, int red_cap, RowsPlan* p) {
   const int maxsmem = 227 * 1024;
   if (R > 64) return false;
   p->CL = CL;
   p->nIm = (nx + CL - 1) / CL;
   p->nJm = (ny + CL - 1) / CL;
   p->Rp = R * (R + 1) / 2;
+  p->red_cap = red_cap;
   size_t o = 0;
   p->o_ahl = (int)o;    o = al16(o + sizeof(float2) * p->nIm * R);
   p->o_bhl = (int)o;    o = al16(o + sizeof(float2) * p->nJm * R);
@@ -89,22 +98,27 @@ static bool rows_make_plan(int nx, int ny, int R, int Smax, int CL, RowsPlan* p)
     size_t d = sizeof(double) * 2 * (size_t)nx;
     o = al16(o + (g > d ? g : d));
   }
-  p->o_ga32 = (int)o;   o = al16(o + sizeof(float2) * p->Rp);  // packed lower, fp32
-  p->o_gb32 = (int)o;   o = al16(o + sizeof(float2) * p->Rp);
+  p->o_gaf = (int)o;    o = al16(o + sizeof(float2) * R * R);  // full Hermitian fp32 GA, GB
+  p->o_gbf = (int)o;    o = al16(o + sizeof(float2) * R * R);
   // vec: gam, hv, hsave (double2 R); nrm, inrm, inv, gda, gdb (double R); gamf (float2 R); 16 scalars
-  // + LDL scratch: colb 4 (R+1) double2, blk 4 (R/2+1) double, zf R double2
+  //      + LDL scratch: colb 4 (R+1) double2, blk 4 (R/2+1) double, zf R double2
   p->o_vec = (int)o;    o = al16(o + sizeof(double2) * R * 3 + sizeof(double) * R * 5 + sizeof(float2) * R + 128 +
                                  sizeof(double2) * 4 * (R + 1) + sizeof(double) * 4 * (R / 2 + 1) + sizeof(double2) * R);
   p->o_tab = (int)o;    o = al16(o + sizeof(unsigned short) * p->Rp);
   p->o_flags = (int)o;  o = al16(o + sizeof(int) * (nx > p->nIm ? nx : p->nIm));
   p->o_rows = (int)o;   o = al16(o + sizeof(int) * Smax);
   p->o_forced = (int)o; o = al16(o + sizeof(int) * Smax);
+  p->o_own = (int)o;    o = al16(o + sizeof(int) * 2 * p->nIm);
   p->o_wacc = (int)o;   o = al16(o + sizeof(float2) * p->nJm * R);
+  p->o_zs = (int)o;     o = al16(o + sizeof(float2) * p->nIm * R);
+  p->o_red2 = (int)o;   o = al16(o + sizeof(float2) * p->red_cap);
   p->o_u2 = (int)o;
   size_t fixed = o + sizeof(double) * 64;
   if (fixed > (size_t)maxsmem) return false;
-  // U2: k-tiles (ys KT x nJm, ahs KT x R)  |  P rows nIm x R
-  size_t other = sizeof(float2) * (size_t)R * p->nIm;
+  // U2: k-tiles (ys KT x nJm, ahs KT x R) | Bh in fp64 + colnorm partials (phase a) | gamma-scaled GEMM operands
+  size_t other = sizeof(double2) * (size_t)p->nJm * R + sizeof(double) * 256;
+  const size_t v2 = sizeof(float2) * (size_t)R * (p->nJm > p->nIm ? p->nJm : p->nIm);
+  if (v2 > other) other = v2;
   size_t avail = maxsmem - fixed;
   int KT = (int)(avail / (sizeof(float2) * (size_t)(p->nJm + R)));
   if (KT > Smax) KT = Smax;
@@ -119,11 +133,6 @@ static bool rows_make_plan(int nx, int ny, int R, int Smax, int CL, RowsPlan* p)
   o += sizeof(double) * 64;
   p->smem = (int)o;
   return true;
-}
-
-// Hermitian R x R from a packed lower triangle: M[r][q]
-TT_DEV float2 herm_at(const float2* P, int r, int q) {
-  return r >= q ? P[r * (r + 1) / 2 + q] : cconj(P[q * (q + 1) / 2 + r]);
 }
 
 // ---------------------------------------------------------------- cold paths (kept out of line)
@@ -192,7 +201,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
                                                              const __grid_constant__ RowsPlan pl) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, NT = blockDim.x;
-  const int lane = tid & 31, warp = tid >> 5, nwarps = NT >> 5;
+  const int lane = tid & 31, warp = tid >> 5;
   const int CL = pl.CL;
   const int c = (int)(blockIdx.x % CL);
   const int s = (int)(blockIdx.x / CL);
@@ -206,8 +215,8 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
   double2* G = (double2*)(smem + pl.o_u1);
   double* pbuf = (double*)(smem + pl.o_u1);
   double* cdf = pbuf + nx;
-  float2* ga32 = (float2*)(smem + pl.o_ga32);
-  float2* gb32 = (float2*)(smem + pl.o_gb32);
+  float2* gaf = (float2*)(smem + pl.o_gaf);  // full Hermitian GA, GB (fp32, row-major)
+  float2* gbf = (float2*)(smem + pl.o_gbf);
   double2* gam = (double2*)(smem + pl.o_vec);
   double2* hv = gam + R;
   double2* hsave = hv + R;
@@ -225,12 +234,19 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
   int* flags = (int*)(smem + pl.o_flags);
   int* rows = (int*)(smem + pl.o_rows);
   int* forced = (int*)(smem + pl.o_forced);
+  int* own_k = (int*)(smem + pl.o_own);  // sampled rows owned by this CTA: measurement index
+  int* own_li = own_k + pl.nIm;          // and local row
   float2* wacc = (float2*)(smem + pl.o_wacc);
+  float2* zs = (float2*)(smem + pl.o_zs);
+  float2* red2 = (float2*)(smem + pl.o_red2);
   float2* ys = (float2*)(smem + pl.o_u2);
   float2* ahs = ys + (size_t)KT * pl.nJm;
-  float2* prow = (float2*)(smem + pl.o_u2);
+  double2* bh64 = (double2*)(smem + pl.o_u2);          // phase (a) only
+  double* cnp = (double*)(bh64 + (size_t)pl.nJm * R);   // phase (a) only: colnorm partials [parts][R]
+  float2* vop = (float2*)(smem + pl.o_u2);              // update only: gamma-scaled GEMM operand
   double* red = (double*)(smem + pl.o_red);
-  __shared__ int sh_S, sh_flag, sh_err;
+  (void)inv;
+  __shared__ int sh_S, sh_err, sh_own, sh_amb;
   long long* pclk = (a.phase_clock != nullptr && blockIdx.x == 0) ? (long long*)a.phase_clock : nullptr;
 #define STAMP(k)                                                             \
   do {                                                                       \
@@ -264,32 +280,41 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
   uint64_t ppos = (a.policy == TT_POLICY_INFORMATIVE && a.philox_pos) ? a.philox_pos[s] : 0ull;
   int status = 0;
   const int eb = part_begin(Rp, CL, c), ee = part_begin(Rp, CL, c + 1);
+  const int cparts = NT / R;  // column-norm partial sums per column
   __syncthreads();
 
   for (int f = 0; f < a.frames; ++f) {
     const long long t = a.t0 + f;
     const double lt = a.lam / (double)t;
     STAMP(0);
-    // ======== (a) column-norm partials of Ah (own rows) and packed GB partials
-    for (int r = warp; r < R; r += nwarps) {
+    // ======== (a) column-norm partials of Ah (own rows), Bh staged in fp64, packed GB partials
+    if (tid < cparts * R) {
+      const int r = tid % R, part = tid / R;
       double acc = 0.0;
-      for (int i = lane; i < nI; i += 32) {
-        const float2 v = ahl[i * R + r];
+      for (int li = part; li < nI; li += cparts) {
+        const float2 v = ahl[li * R + r];
         acc += (double)v.x * v.x + (double)v.y * v.y;
       }
-      acc = warp_sum(acc);
-      if (lane == 0) __stcg(&g_cn[c * R + r], acc);
+      cnp[part * R + r] = acc;
     }
+    for (int o = tid; o < nJ * R; o += NT) bh64[o] = to_d2(bhl[o]);
+    __syncthreads();
+    if (tid < R) {
+      double acc = 0.0;
+      for (int part = 0; part < cparts; ++part) acc += cnp[part * R + tid];
+      __stcg(&g_cn[c * R + tid], acc);
+    }
+    STAMP(26);
     for (int e = tid; e < Rp; e += NT) {
       const int ij = tab[e];
       const int r = ij >> 8, q = ij & 255;
       double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
       int jj = 0;
       for (; jj + 1 < nJ; jj += 2) {
-        acc = zfma_cj(bhl[jj * R + r], bhl[jj * R + q], acc);
-        acc2 = zfma_cj(bhl[(jj + 1) * R + r], bhl[(jj + 1) * R + q], acc2);
+        acc = zfma_cj(bh64[jj * R + r], bh64[jj * R + q], acc);
+        acc2 = zfma_cj(bh64[(jj + 1) * R + r], bh64[(jj + 1) * R + q], acc2);
       }
-      if (jj < nJ) acc = zfma_cj(bhl[jj * R + r], bhl[jj * R + q], acc);
+      if (jj < nJ) acc = zfma_cj(bh64[jj * R + r], bh64[jj * R + q], acc);
       acc = zadd(acc, acc2);
       __stcg(&g_gbp[(size_t)c * Rp + e].x, acc.x);
       __stcg(&g_gbp[(size_t)c * Rp + e].y, acc.y);
@@ -332,37 +357,113 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       STAMP(3);
       cluster_barrier();  // -------------------------------------------- B2
       STAMP(4);
-      // probabilities: normalise, blend with the uniform law (sampler.py:88-92);
-      // the final renormalisation is folded into cdf /= cdf[-1] of the draw.
-      const int chunk = (nx + NT - 1) / NT;
-      const int q0 = min(nx, tid * chunk), q1 = min(nx, q0 + chunk);
-      double loc = 0.0;
-      for (int i = q0; i < q1; ++i) {
-        const double v = __ldcg(&g_sraw[i]);
-        pbuf[i] = v;
-        loc += v;
-      }
-      const double S1 = block_sum(loc, red);
-      const double w1 = (1.0 - a.beta) / S1, w0 = a.beta / (double)nx;
-      for (int i = q0; i < q1; ++i) pbuf[i] = fma(pbuf[i], w1, w0);
+      for (int i = tid; i < nx; i += NT) pbuf[i] = __ldcg(&g_sraw[i]);  // one parallel round trip
+      if (tid == 0) sh_amb = 0;
       __syncthreads();
+      const int ndraw = max(a.k_draws - a.nforced, 0);
+      const uint64_t k1s = a.key1 + (uint64_t)s;
+      if (warp == 0) {
+        // probabilities: normalise, blend with the uniform law (sampler.py:88-92); the final
+        // renormalisation is folded into cdf /= cdf[-1]. Chunked warp scan -> normalised CDF.
+        const int chunk = (nx + 31) / 32;
+        const int q0 = min(nx, lane * chunk), q1 = min(nx, q0 + chunk);
+        double loc = 0.0;
+        for (int i = q0; i < q1; ++i) loc += pbuf[i];
+        const double S1 = warp_sum(loc);
+        const double w1 = (1.0 - a.beta) / S1, w0 = a.beta / (double)nx;
+        loc = 0.0;
+        for (int i = q0; i < q1; ++i) {
+          const double v = fma(pbuf[i], w1, w0);
+          pbuf[i] = v;
+          loc += v;
+        }
+        double x = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        const double il = fast_rcp(__shfl_sync(0xffffffffu, x, 31));
+        double run = x - loc;
+        for (int i = q0; i < q1; ++i) {
+          run += pbuf[i];
+          cdf[i] = run * il;
+          flags[i] = 0;
+        }
+      }
+      __syncthreads();
+      // Philox draws in parallel (numpy choice semantics, sampler.py:160-162)
+      for (int m = tid; m < ndraw; m += NT) {
+        const double u = philox_uniform(a.key0, k1s, ppos + (uint64_t)m);
+        const int idx = upper_bound_d(cdf, nx, u);
+        const double lo = idx > 0 ? cdf[idx - 1] : -1.0;
+        const double hi = idx < nx ? cdf[idx] : 2.0;
+        if (u - lo <= 1e-12 || hi - u <= 1e-12) sh_amb = 1;
+        flags[idx < nx ? idx : nx - 1] = 1;
+      }
+      __syncthreads();
+      if (sh_amb) {  // a uniform within 1e-12 of a CDF boundary: exact sequential numpy cumsum, redo
+        if (tid == 0) {
+          double cacc = 0.0;
+          for (int i = 0; i < nx; ++i) {
+            cacc += pbuf[i];
+            cdf[i] = cacc;
+          }
+        }
+        __syncthreads();
+        const double last = cdf[nx - 1];
+        __syncthreads();
+        for (int i = tid; i < nx; i += NT) {
+          cdf[i] = cdf[i] / last;
+          flags[i] = 0;
+        }
+        __syncthreads();
+        for (int m = tid; m < ndraw; m += NT) {
+          const int idx = upper_bound_d(cdf, nx, philox_uniform(a.key0, k1s, ppos + (uint64_t)m));
+          flags[idx < nx ? idx : nx - 1] = 1;
+        }
+        __syncthreads();
+      }
+      if (warp == 0) {  // forced lines, then compaction -> sorted unique rows (np.union1d)
+        for (int m = lane; m < a.nforced; m += 32) {
+          const int fr = forced[m];
+          if (fr >= 0 && fr < nx) flags[fr] = 1;
+        }
+        __syncwarp();
+        const int chunk = (nx + 31) / 32;
+        const int q0 = min(nx, lane * chunk), q1 = min(nx, q0 + chunk);
+        int cnt = 0;
+        for (int i = q0; i < q1; ++i) cnt += flags[i];
+        int x = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        int o = x - cnt;
+        for (int i = q0; i < q1; ++i)
+          if (flags[i]) rows[o++] = i;
+        if (lane == 31) sh_S = x;
+      }
+      ppos += (uint64_t)max(a.k_draws - a.nforced, 0);
       STAMP(20);
-      const int ndraw = a.k_draws - a.nforced;
-      int Sd;
-      draw_with_replacement_block<false>(pbuf, cdf, flags, rows, Sd, nx, ndraw > 0 ? ndraw : 0, forced, a.nforced,
-                                  a.key0, a.key1 + (uint64_t)s, ppos, red, &sh_flag);
-      ppos += (uint64_t)(ndraw > 0 ? ndraw : 0);
-      S = Sd;
     } else {
       S = load_static_rows(a, f, s, rows, flags, &sh_err);
+      if (tid == 0) sh_S = S;
     }
-    if (tid == 0) sh_S = S;
     __syncthreads();
     STAMP(5);
     S = sh_S;
     status |= sh_err;
 
-    // ======== (b) publish own sampled rows of Ah; prefetch the first Y tile
+    // ======== (b) publish own sampled rows of Ah; list them; prefetch the first Y tile
+    if (tid == 0) sh_own = 0;
+    for (int li = tid; li < nI; li += NT) flags[li] = -1;
+    __syncthreads();
+    for (int k = tid; k < S; k += NT) {
+      const int i = rows[k];
+      if (i >= i0 && i < i0 + nI) flags[i - i0] = k;
+    }
     for (int o = tid; o < S * R; o += NT) {
       const int k = o / R, r = o - k * R;
       const int i = rows[k];
@@ -374,10 +475,9 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     }
     STAMP(6);
     cluster_arrive();  // ------------------------------------------------ B3 (split)
-    const float2* ybase = a.y_mode == TT_Y_GATHER
-                              ? (const float2*)a.ysrc + (size_t)f * a.y_frame_stride + (size_t)s * a.y_slice_stride + j0
-                              : (const float2*)a.ysrc + ((size_t)f * a.nslices + s) * Smax * ny + j0;
     const bool gather = a.y_mode == TT_Y_GATHER;
+    const float2* ybase = gather ? (const float2*)a.ysrc + (size_t)f * a.y_frame_stride + (size_t)s * a.y_slice_stride + j0
+                                 : (const float2*)a.ysrc + ((size_t)f * a.nslices + s) * Smax * ny + j0;
     {
       const int kt = min(KT, S);
       for (int o = tid; o < kt * nJ; o += NT) {
@@ -387,8 +487,32 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     }
     for (int o = tid; o < nJ * R; o += NT) wacc[o] = make_float2(0.f, 0.f);
     for (int e = eb + tid; e < ee; e += NT) G[e - eb] = make_double2(0.0, 0.0);
+    __syncthreads();  // row marks visible to warp 0
+    if (warp == 0) {  // compact the owned sampled rows (ascending local row)
+      const int chunk = (nI + 31) / 32;
+      const int q0 = min(nI, lane * chunk), q1 = min(nI, q0 + chunk);
+      int cnt = 0;
+      for (int li = q0; li < q1; ++li) cnt += flags[li] >= 0;
+      int x = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      int o = x - cnt;
+      for (int li = q0; li < q1; ++li)
+        if (flags[li] >= 0) {
+          own_k[o] = flags[li];
+          own_li[o] = li;
+          flags[li] = o;  // local row -> position in the owned list
+          ++o;
+        }
+      if (lane == 31) sh_own = x;
+    }
     cluster_wait();
+    __syncthreads();  // warp 0's owned-row list (written after its arrive) is visible to all warps
     STAMP(7);
+    const int nown = sh_own;
 
     // ======== (c) heavy phase over k tiles: W, Z partials, GA (own entries), ||Y||^2
     double ysq = 0.0;
@@ -402,8 +526,8 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       }
       for (int o = tid; o < kt * R; o += NT) {
         float2 v;
-        v.x = __ldcg(&g_ahs[(size_t)k0 * R + o].x);
-        v.y = __ldcg(&g_ahs[(size_t)k0 * R + o].y);
+        v.x = __ldcg(&g_ahs[(size_t)(k0) * R + o].x);
+        v.y = __ldcg(&g_ahs[(size_t)(k0) * R + o].y);
         ahs[o] = v;
       }
       cp_async_wait_all();
@@ -414,49 +538,25 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         const float2 v = ys[kk * pl.nJm + jj];
         ysq += (double)v.x * v.x + (double)v.y * v.y;
       }
-      // W[jj][r] += sum_k Y[k][jj] conj(Ah_S[k][r])   (thread-owned smem accumulators)
-      for (int o = tid; o < nJ * R; o += 2 * NT) {
-        const int o2 = o + NT;
-        const bool two = o2 < nJ * R;
-        const int jj = o / R, r = o - jj * R;
-        const int jj2 = two ? o2 / R : jj, r2 = two ? o2 - jj2 * R : r;
-        float2 w = wacc[o], w2 = two ? wacc[o2] : make_float2(0.f, 0.f);
-#pragma unroll 4
-        for (int kk = 0; kk < kt; ++kk) {
-          w = cfma_conj(ys[kk * pl.nJm + jj], ahs[kk * R + r], w);
-          w2 = cfma_conj(ys[kk * pl.nJm + jj2], ahs[kk * R + r2], w2);
-        }
-        wacc[o] = w;
-        if (two) wacc[o2] = w2;
+      // W[jj][r] += sum_k Y[k][jj] conj(Ah_S[k][r])
+      {
+        const int ks = gemm_split(nJ, R, kt, 2, 4, pl.red_cap);
+        cgemm_tile<2, 4, false, true>(nJ, R, kt, ys, 1, pl.nJm, ahs, R, 1, ks, red2,
+                                      [&](int m, int n, float2 v) { wacc[m * R + n] = cadd(wacc[m * R + n], v); });
       }
+      __syncthreads();
       if (k0 == 0) STAMP(17);
-      // Z partial over own columns
-      for (int ob = tid; ob < kt * R; ob += 4 * NT) {
-        int kq[4], rq[4];
-        float2 z[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int o = min(ob + u * NT, kt * R - 1);
-          kq[u] = o / R;
-          rq[u] = o - kq[u] * R;
-          z[u] = make_float2(0.f, 0.f);
-        }
-#pragma unroll 2
-        for (int jj = 0; jj < nJ; ++jj) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) z[u] = cfma_conj(ys[kq[u] * pl.nJm + jj], bhl[jj * R + rq[u]], z[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (ob + u * NT < kt * R) {
-            float2* dst = &g_zp[((size_t)c * Smax + k0 + kq[u]) * R + rq[u]];
-            __stcg(&dst->x, z[u].x);
-            __stcg(&dst->y, z[u].y);
-          }
-        }
+      // Z partial over own columns: Z[k][r] = sum_jj Y[k][jj] conj(Bh[jj][r])
+      {
+        const int ks = gemm_split(kt, R, nJ, 2, 4, pl.red_cap);
+        float2* zdst = g_zp + ((size_t)c * Smax + k0) * R;
+        cgemm_tile<2, 4, false, true>(kt, R, nJ, ys, pl.nJm, 1, bhl, R, 1, ks, red2, [&](int m, int n, float2 v) {
+          __stcg(&zdst[m * R + n].x, v.x);
+          __stcg(&zdst[m * R + n].y, v.y);
+        });
       }
       if (k0 == 0) STAMP(18);
-      // GA own packed entries
+      // GA own packed entries (4-way k split per entry, fixed-order quad reduction)
       const int nq = 4 * (ee - eb);
       for (int base = tid & ~31; base < nq; base += NT) {  // warp-uniform trip count
         const int eq = base + lane;
@@ -467,7 +567,6 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
           const int r = ij >> 8, q = ij & 255;
           for (int kk = part; kk < kt; kk += 4) g = zfma_cj(ahs[kk * R + r], ahs[kk * R + q], g);
         }
-        // lanes 4m..4m+3 hold the parts of one entry: (p0 + p1) + (p2 + p3)
         g.x += __shfl_xor_sync(0xffffffffu, g.x, 1);
         g.y += __shfl_xor_sync(0xffffffffu, g.y, 1);
         g.x += __shfl_xor_sync(0xffffffffu, g.x, 2);
@@ -497,7 +596,11 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     cluster_barrier();  // ---------------------------------------------- B4
     STAMP(10);
 
-    // ======== (d) redundant fp64 solve (every cross-CTA read is one parallel round trip)
+    // ======== (d) redundant fp64 solve; cluster sums of Z for owned rows prefetched alongside
+    for (int o = tid; o < nown * R; o += NT) {
+      const int m = o / R, r = o - m * R;
+      zs[o] = sum_parts_f2(g_zp + (size_t)own_k[m] * R + r, (size_t)Smax * R, CL);
+    }
     for (int e = tid; e < Rp; e += NT) {
       const int ij = tab[e];
       const int r = ij >> 8, q = ij & 255;
@@ -513,8 +616,10 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         gdb[r] = gbe.x;
       }
       G[e] = gg;
-      ga32[e] = to_f2(gae);
-      gb32[e] = to_f2(gbe);
+      gaf[r * R + q] = to_f2(gae);
+      gaf[q * R + r] = to_f2(zconj(gae));
+      gbf[r * R + q] = to_f2(gbe);
+      gbf[q * R + r] = to_f2(zconj(gbe));
     }
     if (tid < R) {
       const double2 h = sum_parts2(g_hp + tid, (size_t)R, CL);
@@ -584,41 +689,43 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     if (a.resid_out != nullptr) write_residual(a, pl, f, s, S, j0, nJ, rows, g_ahs, gamf, bhl, ys, ahs);
     STAMP(13);
 
-    // ======== (e) updates (k-space): Ah <- cfac Ah + mu conj(g) P_S ; Bh <- cfac Bh + mu conj(g) Q
+    // ======== (e) updates (k-space): Bh <- cfac Bh + mu conj(g) (W - Bh diag(g) GA^T)
+    //                                 Ah_S <- cfac Ah_S + mu conj(g) (Z - Ah_S diag(g) GB^T)
     if (update) {
       const float cfac = (float)(1.0 - mu_used * lt);
       const float muf = (float)mu_used;
-      for (int li = tid; li < nI; li += NT) flags[li] = -1;
+      for (int o = tid; o < nJ * R; o += NT) vop[o] = cmul(bhl[o], gamf[o % R]);
       __syncthreads();
-      for (int k = tid; k < S; k += NT) {
-        const int i = rows[k];
-        if (i >= i0 && i < i0 + nI) flags[i - i0] = k;
+      STAMP(21);
+      {
+        // corr[jj][r] = sum_q (Bh[jj][q] g_q) GA[r][q] = sum_q vop[jj][q] conj(GA[q][r])
+        const int ks = gemm_split(nJ, R, R, 2, 4, pl.red_cap);
+        cgemm_tile<2, 4, false, true>(nJ, R, R, vop, R, 1, gaf, R, 1, ks, red2, [&](int m, int n, float2 v) {
+          const int o = m * R + n;
+          wacc[o] = cadd(cscale(bhl[o], cfac), cscale(cmul(cconj(gamf[n]), csub(wacc[o], v)), muf));
+        });
       }
       __syncthreads();
-      // P_S rows owned here: Z (summed over the cluster) - Ah_S diag(gamma) GB^T
-      for (int o = tid; o < nI * R; o += NT) {
-        const int li = o / R, r = o - li * R;
-        const int k = flags[li];
-        if (k >= 0) {
-          const float2 z = sum_parts_f2(g_zp + (size_t)k * R + r, (size_t)Smax * R, CL);
-          float2 corr = make_float2(0.f, 0.f);
-          for (int q = 0; q < R; ++q) corr = cfma(cmul(ahl[li * R + q], gamf[q]), herm_at(gb32, r, q), corr);
-          prow[o] = csub(z, corr);
-        }
-      }
-      // Q = W - Bh diag(gamma) GA^T ; new Bh into wacc (W is consumed in place)
-      for (int o = tid; o < nJ * R; o += NT) {
-        const int jj = o / R, r = o - jj * R;
-        float2 corr = make_float2(0.f, 0.f);
-        for (int q = 0; q < R; ++q) corr = cfma(cmul(bhl[jj * R + q], gamf[q]), herm_at(ga32, r, q), corr);
-        const float2 qv = csub(wacc[o], corr);
-        wacc[o] = cadd(cscale(bhl[o], cfac), cscale(cmul(cconj(gamf[r]), qv), muf));
+      STAMP(22);
+      for (int o = tid; o < nown * R; o += NT) {
+        const int m = o / R, q = o - m * R;
+        vop[o] = cmul(ahl[own_li[m] * R + q], gamf[q]);
       }
       __syncthreads();
+      {
+        const int ks = gemm_split(nown, R, R, 2, 4, pl.red_cap);
+        cgemm_tile<2, 4, false, true>(nown, R, R, vop, R, 1, gbf, R, 1, ks, red2, [&](int m, int n, float2 v) {
+          const int o = m * R + n;
+          zs[o] = cscale(cmul(cconj(gamf[n]), csub(zs[o], v)), muf);  // mu conj(g) P
+        });
+      }
+      __syncthreads();
+      STAMP(23);
       for (int o = tid; o < nI * R; o += NT) {
         const int li = o / R, r = o - li * R;
         float2 v = cscale(ahl[o], cfac);
-        if (flags[li] >= 0) v = cadd(v, cscale(cmul(cconj(gamf[r]), prow[o]), muf));
+        const int m = flags[li];
+        if (m >= 0) v = cadd(v, zs[m * R + r]);
         ahl[o] = v;
       }
       for (int o = tid; o < nJ * R; o += NT) bhl[o] = wacc[o];

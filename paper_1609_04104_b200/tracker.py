@@ -228,6 +228,8 @@ def track_step(state: TrackerState, batch: MeasurementBatch):
     rows = desc.row_lines
     nmeas = desc.nmeas
 
+    if nmeas > 0 and rows is not None and not K.rows_plan_fits(nx, ny, R, int(rows.size)):
+        rows = None  # shared-memory plan does not fit (e.g. R = 64 at 1024^2): generic index kernels
     if nmeas > 0 and rows is not None:
         S = int(rows.size)
         y = batch.y_device().reshape(S, ny)

@@ -1,0 +1,41 @@
+import sys, os
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), '..', '..'))
+import numpy as np, torch
+import paper_1609_04104_b200 as tt
+from bench import CONFIGS, make_data, init_factors
+cfg = dict(CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c2"])
+assert "K" in cfg, "informative configs only"
+T = int(sys.argv[2]) if len(sys.argv) > 2 else 50
+cfg["T"] = T
+cl = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+ids = list(range(cfg["slices"]))
+ks, _ = make_data(cfg, ids)
+A0, B0 = init_factors(cfg, ids)
+pol = tt.Informative(k=cfg["K"], forced=cfg["forced"], beta=cfg["beta"], key0=2024)
+eng = tt.OnlineEngine(cfg["n"], cfg["n"], cfg["R"], len(ids), cfg["lam"], tt.Fixed(cfg["mu"]), pol, cluster=cl)
+eng.set_image_factors(A0, B0)
+ah0, bh0 = eng.ah.clone(), eng.bh.clone()
+kd = torch.from_numpy(ks).cuda()
+out = eng.make_outputs(T)
+args = eng.args(kd, T, out, ah_in=ah0, bh_in=bh0, frame0=0, t0=1)
+from paper_1609_04104_b200 import _ops as K
+for i in range(3):
+    eng.philox_pos.zero_()
+    s = torch.cuda.Event(enable_timing=True); e = torch.cuda.Event(enable_timing=True)
+    s.record(); K.track_rows(args); e.record(); torch.cuda.synchronize()
+    print(f"launch {i}: {s.elapsed_time(e):.3f} ms  {1000*s.elapsed_time(e)/T:.2f} us/frame  cluster {eng.cluster}")
+clk = torch.zeros(T, 32, dtype=torch.int64, device='cuda')
+args.phase_clock = clk.data_ptr()
+eng.philox_pos.zero_(); K.track_rows(args); torch.cuda.synchronize()
+c = clk.cpu().numpy().astype(np.int64)
+names = {26:"a:colnorm",21:"u:mark",22:"u:P",23:"u:Q",1:"a-partials",2:"B1",3:"scores(own)",4:"B2",20:"blend",5:"draw",6:"publishAhS",7:"B3",16:"h:tileload",17:"h:W",18:"h:Z",19:"h:GA",8:"heavy-rest",9:"h/ga/yn",10:"B4",11:"Gbuild",12:"LDL",13:"cost/mu",14:"update",15:"outputs"}
+order = [0,26,1,2,3,4,20,5,6,7,16,17,18,19,8,9,10,11,12,13,21,22,23,14,15]
+cc = c[5:]
+print("cycles per phase (median over frames 5..):")
+prev = None
+for k in order:
+    if prev is not None and (cc[:, k] > 0).all():
+        print(f"  {names.get(k, k):12s} {int(np.median(cc[:, k] - cc[:, prev])):7d}")
+    if (cc[:, k] > 0).all(): prev = k
+fr = np.median(np.diff(cc[:, 0]))
+print("frame total", fr, "cycles =", fr / 1.965e3, "us at 1965 MHz")
