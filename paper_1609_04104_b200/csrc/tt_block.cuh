@@ -432,6 +432,9 @@ TT_DEV void block_ldl2_solve(double2* Gio, const double2* hin, double2* gam, dou
                              int R) {
   const int tid = threadIdx.x, NT = blockDim.x;
   const int Rp = R * (R + 1) / 2, E = Rp + R, W = R + 1;
+  // Entries are handed out in column-major order (column j has rows j..R-1), so the
+  // columns eliminated first sit at the low thread indices: as the elimination proceeds
+  // whole warps retire and skip the update (warp-uniform branch).
   int ri[EPT], rj[EPT];
   double2 g[EPT];
 #pragma unroll
@@ -441,11 +444,15 @@ TT_DEV void block_ldl2_solve(double2* Gio, const double2* hin, double2* gam, dou
     rj[m] = -1;
     g[m] = make_double2(0.0, 0.0);
     if (e < Rp) {
-      int r, q;
-      tri_decode(e, r, q);
+      int q = 0, off = 0;
+      while (off + (R - q) <= e) {
+        off += R - q;
+        ++q;
+      }
+      const int r = q + (e - off);
       ri[m] = r;
       rj[m] = q;
-      g[m] = Gio[e];
+      g[m] = Gio[r * (r + 1) / 2 + q];
     } else if (e < E) {
       ri[m] = e - Rp;
       rj[m] = R;
@@ -481,33 +488,33 @@ TT_DEV void block_ldl2_solve(double2* Gio, const double2* hin, double2* gam, dou
       zf[k] = zconj(c0[R]);
       if (pair) zf[k + 1] = zconj(c1[R]);
     }
+    // B^-1 = (1/det) [[bb, -conj(c)], [-c, a]]; row projection w_i = (G_ik, G_i,k+1) B^-1, then
+    // G_ij -= w_i0 conj(G_jk) + w_i1 conj(G_j,k+1): 16 fp64 ops per entry
+    const double2 x00 = make_double2(bb * id, 0.0), x11 = make_double2(a * id, 0.0);
+    const double2 x01 = make_double2(-c.x * id, c.y * id);   // -conj(c)/det
+    const double2 x10 = make_double2(-c.x * id, -c.y * id);  // -c/det
 #pragma unroll
     for (int m = 0; m < EPT; ++m) {
       const int i = ri[m], j = rj[m];
       if ((j >= k + 2 && j < R && i >= j) || (j == R && i >= k + 2)) {  // trailing lower entry or rhs row
-        // u = (G_ik, G_i,k+1), v = (G_jk, G_j,k+1) [slot R: conj(h_k), conj(h_k+1)]
         const double2 u0 = c0[i], v0 = c0[j];
         double2 upd;
         if (pair) {
           const double2 u1 = c1[i], v1 = c1[j];
-          // t = B^-1 v^H * det : t0 = bb conj(v0) - conj(c) conj(v1); t1 = -c conj(v0) + a conj(v1)
-          const double2 cv0 = zconj(v0), cv1 = zconj(v1);
-          const double2 cc = zconj(c);
-          double2 t0 = zscale(cv0, bb);
-          t0 = zsub(t0, zmul(cc, cv1));
-          double2 t1 = zscale(cv1, a);
-          t1 = zsub(t1, zmul(c, cv0));
-          upd = zadd(zmul(u0, t0), zmul(u1, t1));
+          const double2 w0 = zfma(u1, x10, zmul(u0, x00));
+          const double2 w1 = zfma(u1, x11, zmul(u0, x01));
+          upd = zfma(w1, zconj(v1), zmul(w0, zconj(v0)));
+          g[m] = zsub(g[m], upd);
         } else {
           upd = zmul(u0, zconj(v0));
+          g[m].x -= upd.x * id;
+          g[m].y -= upd.y * id;
         }
-        g[m].x -= upd.x * id;
-        g[m].y -= upd.y * id;
         if (j == k + 2 || j == k + 3) n0[(j - k - 2) * W + i] = g[m];  // next pivot columns
         if (j == R && (i == k + 2 || i == k + 3)) n0[(i - k - 2) * W + R] = zconj(g[m]);
       }
       // entries of the two pivot columns are final now: keep them for the back substitution
-      if (j == k || (pair && j == k + 1)) Gio[tid + m * NT] = g[m];
+      if (j == k || (pair && j == k + 1)) Gio[i * (i + 1) / 2 + j] = g[m];
     }
     (void)n1;
     __syncthreads();

@@ -42,16 +42,17 @@
 namespace cg = cooperative_groups;
 
 #define ROWS_NT 256
+#define ROWS_UF 32  // frames of precomputed Philox uniforms per refill
 
 struct RowsPlan {
   int CL, KT, nIm, nJm, Rp, red_cap;
-  int o_ahl, o_bhl, o_u1, o_gaf, o_gbf, o_vec, o_tab, o_flags, o_rows, o_forced, o_own, o_wacc, o_zs, o_red2, o_u2,
-      o_red;
+  int o_ahl, o_bhl, o_u1, o_gaf, o_gbf, o_vec, o_tab, o_flags, o_rows, o_forced, o_usm, o_own, o_wacc, o_zs, o_red2,
+      o_u2, o_red;
   int smem;
 };
 
 struct RowsScratch {
-  size_t cn, gbp, gb, ga, sraw, ahs, zp, hp, yn, per_slice;
+  size_t cn, gbp, gb, ga, sraw, ahs, zp, hp, yn, unif, per_slice;
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -69,6 +70,7 @@ __host__ __device__ inline RowsScratch rows_scratch_layout(int nx, int ny, int R
   s.zp = o;   o = al16(o + sizeof(float2) * (size_t)CL * Smax * R);
   s.hp = o;   o = al16(o + sizeof(double2) * CL * R);
   s.yn = o;   o = al16(o + sizeof(double) * CL);
+  s.unif = o; o = al16(o + sizeof(double) * (size_t)ROWS_UF * Smax);  // Philox uniforms, ROWS_UF frames
   s.per_slice = al16(o + 256);
   (void)ny;
   return s;
@@ -108,6 +110,7 @@ static bool rows_make_plan_cap(int nx, int ny, int R, int Smax, int CL, int red_
   p->o_flags = (int)o;  o = al16(o + sizeof(int) * (nx > p->nIm ? nx : p->nIm));
   p->o_rows = (int)o;   o = al16(o + sizeof(int) * Smax);
   p->o_forced = (int)o; o = al16(o + sizeof(int) * Smax);
+  p->o_usm = (int)o;    o = al16(o + sizeof(double) * Smax);  // this frame's uniforms
   p->o_own = (int)o;    o = al16(o + sizeof(int) * 2 * p->nIm);
   p->o_wacc = (int)o;   o = al16(o + sizeof(float2) * p->nJm * R);
   p->o_zs = (int)o;     o = al16(o + sizeof(float2) * p->nIm * R);
@@ -234,6 +237,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
   int* flags = (int*)(smem + pl.o_flags);
   int* rows = (int*)(smem + pl.o_rows);
   int* forced = (int*)(smem + pl.o_forced);
+  double* usm = (double*)(smem + pl.o_usm);
   int* own_k = (int*)(smem + pl.o_own);  // sampled rows owned by this CTA: measurement index
   int* own_li = own_k + pl.nIm;          // and local row
   float2* wacc = (float2*)(smem + pl.o_wacc);
@@ -265,6 +269,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
   float2* g_zp = (float2*)(sb + L.zp);
   double2* g_hp = (double2*)(sb + L.hp);
   double* g_yn = (double*)(sb + L.yn);
+  double* g_unif = (double*)(sb + L.unif);
 
   // ---- load resident state and constants once
   {
@@ -319,6 +324,15 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       __stcg(&g_gbp[(size_t)c * Rp + e].x, acc.x);
       __stcg(&g_gbp[(size_t)c * Rp + e].y, acc.y);
     }
+    const int ndraw = a.policy == TT_POLICY_INFORMATIVE ? max(a.k_draws - a.nforced, 0) : 0;
+    const uint64_t k1s = a.key1 + (uint64_t)s;
+    if (ndraw > 0 && f % ROWS_UF == 0) {
+      // Philox uniforms of the next ROWS_UF frames (stream positions are state independent), split
+      // over the cluster; the barrier below publishes them. Saves a Philox block per draw per frame.
+      const int nf = min(ROWS_UF, a.frames - f);
+      for (int it = c * NT + tid; it < nf * ndraw; it += CL * NT)
+        __stcg(&g_unif[it], philox_uniform(a.key0, k1s, ppos + (uint64_t)it));
+    }
     STAMP(1);
     cluster_barrier();  // ---------------------------------------------- B1
     STAMP(2);
@@ -332,6 +346,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       nrm[r] = n2;
       inrm[r] = n2 > 0.0 ? fast_rcp(n2) : 0.0;
     }
+    for (int m = tid; m < ndraw; m += NT) usm[m] = __ldcg(&g_unif[(f % ROWS_UF) * ndraw + m]);
     if (tid == 0) sh_err = 0;
     __syncthreads();
     if (warp == 0) {  // ||Ah||^2, fixed order
@@ -360,8 +375,6 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       for (int i = tid; i < nx; i += NT) pbuf[i] = __ldcg(&g_sraw[i]);  // one parallel round trip
       if (tid == 0) sh_amb = 0;
       __syncthreads();
-      const int ndraw = max(a.k_draws - a.nforced, 0);
-      const uint64_t k1s = a.key1 + (uint64_t)s;
       if (warp == 0) {
         // probabilities: normalise, blend with the uniform law (sampler.py:88-92); the final
         // renormalisation is folded into cdf /= cdf[-1]. Chunked warp scan -> normalised CDF.
@@ -392,14 +405,30 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         }
       }
       __syncthreads();
-      // Philox draws in parallel (numpy choice semantics, sampler.py:160-162)
-      for (int m = tid; m < ndraw; m += NT) {
-        const double u = philox_uniform(a.key0, k1s, ppos + (uint64_t)m);
-        const int idx = upper_bound_d(cdf, nx, u);
-        const double lo = idx > 0 ? cdf[idx - 1] : -1.0;
-        const double hi = idx < nx ? cdf[idx] : 2.0;
-        if (u - lo <= 1e-12 || hi - u <= 1e-12) sh_amb = 1;
-        flags[idx < nx ? idx : nx - 1] = 1;
+      // draws (numpy choice semantics, sampler.py:160-162): groups of 8 lanes search the CDF
+      // cooperatively (3 rounds of 8 probes + ballot for nx = 256) with precomputed uniforms
+      {
+        const int g = tid >> 3, gl = tid & 7, ng = NT >> 3;
+        for (int mb = 0; mb < ndraw; mb += ng) {  // warp-uniform trip count
+          const int m = mb + g;
+          const double u = m < ndraw ? usm[m] : 2.0;
+          int lo = 0, sz = nx + 1;  // idx = first i with cdf[i] > u lies in [lo, lo + sz)
+          while (sz > 1) {
+            const int step = (sz + 7) >> 3;
+            const int probe = lo + (gl + 1) * step - 1;
+            const bool gt = probe >= nx || cdf[probe] > u;
+            const unsigned gm = (__ballot_sync(0xffffffffu, gt) >> (lane & 24)) & 0xffu;
+            const int fi = __ffs(gm) - 1;
+            lo += fi * step;
+            sz = step;
+          }
+          if (m < ndraw && gl == 0) {
+            const double lo_v = lo > 0 ? cdf[lo - 1] : -1.0;
+            const double hi_v = lo < nx ? cdf[lo] : 2.0;
+            if (u - lo_v <= 1e-12 || hi_v - u <= 1e-12) sh_amb = 1;
+            flags[lo < nx ? lo : nx - 1] = 1;
+          }
+        }
       }
       __syncthreads();
       if (sh_amb) {  // a uniform within 1e-12 of a CDF boundary: exact sequential numpy cumsum, redo
@@ -419,7 +448,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         }
         __syncthreads();
         for (int m = tid; m < ndraw; m += NT) {
-          const int idx = upper_bound_d(cdf, nx, philox_uniform(a.key0, k1s, ppos + (uint64_t)m));
+          const int idx = upper_bound_d(cdf, nx, usm[m]);
           flags[idx < nx ? idx : nx - 1] = 1;
         }
         __syncthreads();
