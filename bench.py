@@ -224,6 +224,104 @@ def run_reference(args, cfg):
 
 
 # ------------------------------------------------------------------ our arm
+def run_row_sharded(args, cfg):
+    """Config 4 across ranks: Ah row-sharded, one NCCL all-reduce pair per frame
+    (SURVEY §8e). `scaling: strong` (the single 1024^2 slice is split)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1609_04104_b200 as tt
+    from paper_1609_04104_b200 import _lib as L
+    from paper_1609_04104_b200 import _ops as K
+    from paper_1609_04104_b200.engine import RowShardedEngine
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    L.load()
+    n, R, T = cfg["n"], cfg["R"], cfg["T"]
+    ks_np, clean_np = make_data(cfg, [0])
+    A0, B0 = init_factors(cfg, [0])
+    Smax = int(np.ceil(cfg["vd"] * n))
+    gen = np.random.Generator(np.random.Philox(key=2024))
+    tab = np.stack([tt.variable_density_rows(n, -1.0, cfg["vd"], gen) for _ in range(T)])
+    ks = torch.from_numpy(ks_np[:, 0]).to(dev)
+
+    def allreduce(t):
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+
+    def fresh():
+        e = RowShardedEngine(n, n, R, cfg["lam"], tt.Fixed(cfg["mu"]), tab, np.full(T, Smax), world, rank,
+                             cluster=args.cluster, allreduce=allreduce)
+        e.set_image_factors(A0[0], B0[0])
+        return e
+
+    e = fresh()
+    r0, r1 = e.r0, e.r1
+    out = e.make_outputs(T)
+    Afull = torch.empty(T, n, R, dtype=torch.complex64, device=dev)
+    Xblk = torch.empty(T, r1 - r0, n, dtype=torch.complex64, device=dev)
+    lib = L.lib()
+    stream = torch.cuda.current_stream()
+
+    def step():
+        e.run(ks, T, out)
+        # all-gather of the owned k-space rows history, inverse FFTs, this rank's image-row block
+        if world > 1:
+            parts = [torch.empty(T, b - a, R, dtype=torch.complex64, device=dev)
+                     for a, b in [tuple((n * p) // world for p in (q, q + 1)) for q in range(world)]]
+            dist.all_gather(parts, out["ah"])
+            Afull.copy_(torch.cat(parts, dim=1))
+        else:
+            Afull.copy_(out["ah"])
+        K.fft_cols_(Afull, inverse=True)
+        K.fft_cols_(out["bh"], inverse=True)
+        Ablk = Afull[:, r0:r1].contiguous()
+        L.check(lib.tt_reconstruct(stream.cuda_stream, T, r1 - r0, n, R, Ablk.data_ptr(), out["bh"].data_ptr(),
+                                   out["gamma"].data_ptr(), Xblk.data_ptr()), "reconstruct")
+
+    for _ in range(args.warmup):
+        e = fresh()
+        step()
+    torch.cuda.synchronize()
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            e = fresh()
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+    tot = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+        dist.destroy_process_group()
+    L.raise_status(int(e.status.item()), "row-sharded engine")
+    total_ms = float(tot[0])
+    if rank != 0:
+        return 0
+    value = T * args.steps / (total_ms / 1e3)
+    line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "c64", "data": "synthetic",
+            "config": {"workload": cfg["desc"].replace("single GPU, unsharded", f"Ah row-sharded over {world}"),
+                       "frames_per_step": T, "rank": R, "nx": n, "ny": n, "parallelism": f"row-shard x{world}",
+                       "collectives": "2 NCCL all-reduces per frame (W fp32, GA/norms fp64) + 1 all-gather per step"},
+            "gpu_launches": (2 * T + 3) * args.steps, "clocks": clk.summary(), "e2e": None, "cpu_baseline": None}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
@@ -421,10 +519,13 @@ def main():
     ap.add_argument("--ref-frames", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--row-shard", action="store_true", help="config c4: use the row-sharded two-phase path")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if args.config == "c4" and (int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.row_shard):
+        return run_row_sharded(args, cfg)
     return run_ours(args, cfg)
 
 

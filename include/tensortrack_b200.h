@@ -104,8 +104,21 @@ typedef struct tt_rows_args {
   float* bh_hist;             /* [frames][nslices][ny][rank] or NULL */
   int32_t* status;            /* [nslices] OR-ed TT_ST_* bits */
   void* scratch;              /* tt_rows_scratch_bytes() bytes */
-  int64_t* phase_clock;       /* optional profiling: [frames][16] SM clock64 stamps of CTA 0, or NULL */
+  int64_t* phase_clock;       /* optional profiling: [frames][32] SM clock64 stamps of CTA 0, or NULL */
+  /* Row sharding across GPUs (BASELINE config 4; 0 = off). Rank `shard_rank` of
+   * `shard_world` owns k-space rows [nx*rank/world, nx*(rank+1)/world) of Ah; ah_in/ah_out
+   * then hold only those rows, Bh is replicated. Each frame is two launches:
+   * phase 1 writes this rank's partial payload (xw: W = Y^T conj(Ah_S) [ny][rank]
+   * complex64; xg: packed GA (R(R+1)/2 complex128), ||Y||^2, ||Ah||^2 as doubles),
+   * the caller all-reduces xw and xg (sum) over the ranks, phase 2 solves
+   * redundantly and updates the owned rows and the replicated Bh. Static row
+   * policy, nslices = 1, frames = 1 per launch. */
+  int32_t shard_rank, shard_world, shard_phase;
+  float* xw;
+  double* xg;
 } tt_rows_args;
+/* doubles in the fp64 payload xg of a sharded launch */
+size_t tt_rows_shard_xg_len(int rank);
 
 /* Choose the cluster size (if *cluster <= 0) and report the dynamic shared
  * memory per CTA; TT_EUNSUPPORTED if no cluster size fits. */

@@ -209,7 +209,13 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
   const int c = (int)(blockIdx.x % CL);
   const int s = (int)(blockIdx.x / CL);
   const int nx = a.nx, ny = a.ny, R = a.rank, Smax = a.max_rows, Rp = pl.Rp;
-  const int i0 = part_begin(nx, CL, c), nI = part_begin(nx, CL, c + 1) - i0;
+  // row sharding across GPUs: this rank holds k-space rows [R0, R0 + nxs) of Ah (all rows when off)
+  const bool shard = a.shard_world > 0;
+  const int phase = shard ? a.shard_phase : 0;  // 0 full step, 1 partials -> payload, 2 payload -> update
+  const int R0 = shard ? part_begin(nx, a.shard_world, a.shard_rank) : 0;
+  const int nxs = shard ? part_begin(nx, a.shard_world, a.shard_rank + 1) - R0 : nx;
+  const int i0 = R0 + part_begin(nxs, CL, c), nI = part_begin(nxs, CL, c + 1) - part_begin(nxs, CL, c);
+  const int aoff = i0 - R0;  // first own row inside the rank's Ah buffers
   const int j0 = part_begin(ny, CL, c), nJ = part_begin(ny, CL, c + 1) - j0;
   const int KT = pl.KT;
 
@@ -273,7 +279,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
 
   // ---- load resident state and constants once
   {
-    const float2* src = (const float2*)a.ah_in + ((size_t)s * nx + i0) * R;
+    const float2* src = (const float2*)a.ah_in + ((size_t)s * nxs + aoff) * R;
     for (int o = tid; o < nI * R; o += NT) ahl[o] = src[o];
     const float2* srb = (const float2*)a.bh_in + ((size_t)s * ny + j0) * R;
     for (int o = tid; o < nJ * R; o += NT) bhl[o] = srb[o];
@@ -292,6 +298,10 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     const long long t = a.t0 + f;
     const double lt = a.lam / (double)t;
     STAMP(0);
+    int S = 0;
+    const int ndraw = a.policy == TT_POLICY_INFORMATIVE ? max(a.k_draws - a.nforced, 0) : 0;
+    const uint64_t k1s = a.key1 + (uint64_t)s;
+    if (phase != 2) {
     // ======== (a) column-norm partials of Ah (own rows), Bh staged in fp64, packed GB partials
     if (tid < cparts * R) {
       const int r = tid % R, part = tid / R;
@@ -324,8 +334,6 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       __stcg(&g_gbp[(size_t)c * Rp + e].x, acc.x);
       __stcg(&g_gbp[(size_t)c * Rp + e].y, acc.y);
     }
-    const int ndraw = a.policy == TT_POLICY_INFORMATIVE ? max(a.k_draws - a.nforced, 0) : 0;
-    const uint64_t k1s = a.key1 + (uint64_t)s;
     if (ndraw > 0 && f % ROWS_UF == 0) {
       // Philox uniforms of the next ROWS_UF frames (stream positions are state independent), split
       // over the cluster; the barrier below publishes them. Saves a Philox block per draw per frame.
@@ -356,7 +364,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       if (lane == 0) scal[1] = v;
     }
 
-    int S = 0;
+    }  // phase != 2
     if (a.policy == TT_POLICY_INFORMATIVE) {
       // raw row scores for own rows (sampler.py:77-85, :126)
       const double cs = (double)ny, cr = (double)R, cd = 1.0 / ((double)R * (double)(nx + ny));
@@ -477,8 +485,26 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       ppos += (uint64_t)max(a.k_draws - a.nforced, 0);
       STAMP(20);
     } else {
+      if (tid == 0) sh_err = 0;
+      __syncthreads();
       S = load_static_rows(a, f, s, rows, flags, &sh_err);
-      if (tid == 0) sh_S = S;
+      if (shard && warp == 0) {
+        // keep only this rank's rows, in measurement order (the other ranks take the rest)
+        int cnt = 0;
+        for (int base = 0; base < S; base += 32) {
+          const int k = base + lane;
+          const int i = k < S ? rows[k] : -1;
+          const bool keep = i >= R0 && i < R0 + nxs;
+          const unsigned m = __ballot_sync(0xffffffffu, keep);
+          __syncwarp();
+          if (keep) rows[cnt + __popc(m & ((1u << lane) - 1u))] = i;
+          cnt += __popc(m);
+          __syncwarp();
+        }
+        if (lane == 0) sh_S = cnt;
+      } else if (tid == 0) {
+        sh_S = S;
+      }
     }
     __syncthreads();
     STAMP(5);
@@ -493,7 +519,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       const int i = rows[k];
       if (i >= i0 && i < i0 + nI) flags[i - i0] = k;
     }
-    for (int o = tid; o < S * R; o += NT) {
+    for (int o = tid; phase != 2 && o < S * R; o += NT) {
       const int k = o / R, r = o - k * R;
       const int i = rows[k];
       if (i >= i0 && i < i0 + nI) {
@@ -507,7 +533,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     const bool gather = a.y_mode == TT_Y_GATHER;
     const float2* ybase = gather ? (const float2*)a.ysrc + (size_t)f * a.y_frame_stride + (size_t)s * a.y_slice_stride + j0
                                  : (const float2*)a.ysrc + ((size_t)f * a.nslices + s) * Smax * ny + j0;
-    {
+    if (phase != 2) {
       const int kt = min(KT, S);
       for (int o = tid; o < kt * nJ; o += NT) {
         const int kk = o / nJ, jj = o - kk * nJ;
@@ -545,7 +571,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
 
     // ======== (c) heavy phase over k tiles: W, Z partials, GA (own entries), ||Y||^2
     double ysq = 0.0;
-    for (int k0 = 0; k0 < S; k0 += KT) {
+    for (int k0 = 0; phase != 2 && k0 < S; k0 += KT) {
       const int kt = min(KT, S - k0);
       if (k0 > 0) {
         for (int o = tid; o < kt * nJ; o += NT) {
@@ -606,6 +632,25 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       __syncthreads();
     }
     STAMP(8);
+    if (phase == 1) {
+      // this rank's partials -> payload (the caller all-reduces xw and xg across ranks)
+      for (int o = tid; o < nJ * R; o += NT) ((float2*)a.xw)[(size_t)j0 * R + o] = wacc[o];
+      for (int e = eb + tid; e < ee; e += NT) {
+        a.xg[2 * e] = G[e - eb].x;
+        a.xg[2 * e + 1] = G[e - eb].y;
+      }
+      const double yt = block_sum(ysq, red);
+      if (tid == 0) __stcg(&g_yn[c], yt);
+      cluster_barrier();
+      if (c == 0 && tid == 0) {
+        a.xg[2 * Rp] = sum_parts(g_yn, 1, CL);
+        a.xg[2 * Rp + 1] = scal[1];  // this rank's ||Ah||^2
+      }
+      continue;  // phase 2 finishes the frame after the all-reduce
+    }
+    if (phase == 2)  // reduced W of this CTA's columns
+      for (int o = tid; o < nJ * R; o += NT) wacc[o] = ((const float2*)a.xw)[(size_t)j0 * R + o];
+    __syncthreads();
     // h partial: sum_jj conj(Bh[jj][r]) W[jj][r]
     if (tid < R) {
       double2 h = make_double2(0.0, 0.0);
@@ -613,13 +658,13 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       __stcg(&g_hp[c * R + tid].x, h.x);
       __stcg(&g_hp[c * R + tid].y, h.y);
     }
-    for (int e = eb + tid; e < ee; e += NT) {
+    for (int e = eb + tid; phase == 0 && e < ee; e += NT) {
       __stcg(&g_ga[e].x, G[e - eb].x);
       __stcg(&g_ga[e].y, G[e - eb].y);
     }
     {
       const double yt = block_sum(ysq, red);
-      if (tid == 0) __stcg(&g_yn[c], yt);
+      if (tid == 0 && phase == 0) __stcg(&g_yn[c], yt);
     }
     STAMP(9);
     cluster_barrier();  // ---------------------------------------------- B4
@@ -634,8 +679,13 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       const int ij = tab[e];
       const int r = ij >> 8, q = ij & 255;
       double2 gae, gbe;
-      gae.x = __ldcg(&g_ga[e].x);
-      gae.y = __ldcg(&g_ga[e].y);
+      if (phase == 2) {
+        gae.x = a.xg[2 * e];
+        gae.y = a.xg[2 * e + 1];
+      } else {
+        gae.x = __ldcg(&g_ga[e].x);
+        gae.y = __ldcg(&g_ga[e].y);
+      }
       gbe.x = __ldcg(&g_gb[e].x);
       gbe.y = __ldcg(&g_gb[e].y);
       double2 gg = zmul(gae, gbe);
@@ -655,7 +705,14 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       hv[tid] = h;
       hsave[tid] = h;
     }
-    if (tid == 32) scal[0] = sum_parts(g_yn, 1, CL);
+    if (tid == 32) {
+      if (phase == 2) {
+        scal[0] = a.xg[2 * Rp];      // ||Y||^2 over all ranks
+        scal[1] = a.xg[2 * Rp + 1];  // ||Ah||^2 over all ranks
+      } else {
+        scal[0] = sum_parts(g_yn, 1, CL);
+      }
+    }
     __syncthreads();
     if (warp == 0) {  // ||Bh||^2 = trace(GB)
       double v = 0.0;
@@ -776,7 +833,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         for (int k = tid; k < Smax; k += NT) a.rows_out[fs * Smax + k] = k < S ? rows[k] : -1;
     }
     if (a.ah_hist) {
-      float2* dst = (float2*)a.ah_hist + (fs * nx + i0) * R;
+      float2* dst = (float2*)a.ah_hist + (fs * nxs + aoff) * R;
       for (int o = tid; o < nI * R; o += NT) dst[o] = ahl[o];
     }
     if (a.bh_hist) {
@@ -790,7 +847,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
 
   // ---- write back resident state
   {
-    float2* dst = (float2*)a.ah_out + ((size_t)s * nx + i0) * R;
+    float2* dst = (float2*)a.ah_out + ((size_t)s * nxs + aoff) * R;
     for (int o = tid; o < nI * R; o += NT) dst[o] = ahl[o];
     float2* dsb = (float2*)a.bh_out + ((size_t)s * ny + j0) * R;
     for (int o = tid; o < nJ * R; o += NT) dsb[o] = bhl[o];
@@ -833,6 +890,8 @@ extern "C" int tt_rows_plan(int nx, int ny, int rank, int max_rows, int policy, 
   return TT_OK;
 }
 
+extern "C" size_t tt_rows_shard_xg_len(int rank) { return (size_t)rank * (rank + 1) + 2; }
+
 extern "C" size_t tt_rows_scratch_bytes(int nslices, int nx, int ny, int rank, int max_rows, int cluster) {
   if (cluster < 1) cluster = 16;
   return rows_scratch_layout(nx, ny, rank, max_rows, cluster).per_slice * (size_t)(nslices > 0 ? nslices : 1);
@@ -855,6 +914,15 @@ extern "C" int tt_track_rows(void* stream, const tt_rows_args* a) {
     if (a->nforced > 0 && !a->forced) return tt_fail(TT_EINVAL, "null forced list");
   }
   if (a->lam < 0) return tt_fail(TT_EINVAL, "lambda must be nonnegative");
+  if (a->shard_world > 0) {
+    if (a->shard_rank < 0 || a->shard_rank >= a->shard_world || (a->shard_phase != 1 && a->shard_phase != 2))
+      return tt_fail(TT_EINVAL, "row sharding: need 0 <= rank < world and phase 1 or 2");
+    if (a->policy != TT_POLICY_STATIC || a->nslices != 1 || a->frames != 1 || a->y_mode != TT_Y_GATHER)
+      return tt_fail(TT_EUNSUPPORTED, "row sharding supports static row tables, one slice, one frame per launch, "
+                                      "gathered measurements");
+    if (!a->xw || !a->xg) return tt_fail(TT_EINVAL, "row sharding: null payload buffers");
+    if (a->resid_out) return tt_fail(TT_EUNSUPPORTED, "row sharding: residual output not supported");
+  }
   if (a->t0 < 1) return tt_fail(TT_EINVAL, "t must be >= 1");
   if (a->frames == 0) return TT_OK;
   RowsPlan pl;

@@ -253,3 +253,106 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1) -
     return OnlineResult(recon=X.cpu().numpy(), gamma=out["gamma"].cpu().numpy(), cost=out["cost"].cpu().numpy(),
                         mu=out["mu"].cpu().numpy(), rows=rows, nmse=nm, final_A=A.cpu().numpy(),
                         final_B=B.cpu().numpy())
+
+
+class RowShardedEngine:
+    """One rank of the row-sharded online loop (BASELINE config 4).
+
+    The rank owns k-space rows [r0, r1) of Ah; Bh is replicated. Per frame:
+    ``tt_track_rows`` phase 1 (partials of W, GA, ||Y||^2, ||Ah||^2 over the
+    rank's sampled rows) -> sum-all-reduce of the payload across ranks
+    (``allreduce``, NCCL over NVLink by default) -> phase 2 (redundant fp64
+    solve, update of the owned rows and the replicated Bh). Static row masks.
+    """
+
+    def __init__(self, nx, ny, rank, lam, step, rows, counts, world, rank_id, cluster=0, t0=1, allreduce=None):
+        from .sharding import row_partition
+
+        self.nx, self.ny, self.R = int(nx), int(ny), int(rank)
+        self.world, self.rank_id = int(world), int(rank_id)
+        self.r0, self.r1 = row_partition(self.nx, self.world, self.rank_id)
+        self.lam, self.step = float(lam), step
+        self.dev = L.device()
+        rows = np.asarray(rows).reshape(np.asarray(rows).shape[0], -1)
+        self.max_rows = int(rows.shape[1])
+        self.rows_tab = torch.from_numpy(np.ascontiguousarray(rows, dtype=np.int32)).to(self.dev)
+        self.rows_cnt = torch.from_numpy(np.ascontiguousarray(np.asarray(counts).reshape(-1), dtype=np.int32)).to(self.dev)
+        self.scr = K.RowsScratch(1, self.nx, self.ny, self.R, self.max_rows, cluster)
+        self.cluster = self.scr.cluster
+        self.ah = torch.zeros(self.r1 - self.r0, self.R, dtype=torch.complex64, device=self.dev)
+        self.bh = torch.zeros(self.ny, self.R, dtype=torch.complex64, device=self.dev)
+        self.xw = torch.empty(self.ny, self.R, dtype=torch.complex64, device=self.dev)
+        self.xg = torch.empty(int(L.lib().tt_rows_shard_xg_len(self.R)), dtype=torch.float64, device=self.dev)
+        self.alpha_bar = torch.zeros(1, dtype=torch.float64, device=self.dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.t = int(t0)
+        self.frame = 0
+        if allreduce is None:
+            import torch.distributed as dist
+
+            def allreduce(t):
+                dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        self.allreduce = allreduce
+
+    def set_image_factors(self, A, B):
+        """Full image-domain factors (nx, R), (ny, R) -> this rank's k-space rows and Bh."""
+        a = torch.as_tensor(np.asarray(A) if not isinstance(A, torch.Tensor) else A).to(self.dev, torch.complex64)
+        b = torch.as_tensor(np.asarray(B) if not isinstance(B, torch.Tensor) else B).to(self.dev, torch.complex64)
+        ah = K.fft_cols_(a.reshape(self.nx, self.R).contiguous())
+        self.ah = ah[self.r0:self.r1].contiguous()
+        self.bh = K.fft_cols_(b.reshape(self.ny, self.R).contiguous())
+
+    def make_outputs(self, frames):
+        d = self.dev
+        return dict(gamma=torch.empty(frames, self.R, dtype=torch.complex64, device=d),
+                    cost=torch.empty(frames, dtype=torch.float64, device=d),
+                    mu=torch.empty(frames, dtype=torch.float64, device=d),
+                    ah=torch.empty(frames, self.r1 - self.r0, self.R, dtype=torch.complex64, device=d),
+                    bh=torch.empty(frames, self.ny, self.R, dtype=torch.complex64, device=d))
+
+    def _args(self, kspace, f, out, fo, phase):
+        mode, mu, cf, cc = _step_params(self.step)
+        a = L.RowsArgs()
+        a.nslices, a.nx, a.ny, a.rank, a.frames = 1, self.nx, self.ny, self.R, 1
+        a.max_rows, a.cluster, a.t0 = self.max_rows, self.cluster, self.t
+        a.ah_in = a.ah_out = self.ah.data_ptr()
+        a.bh_in = a.bh_out = self.bh.data_ptr()
+        a.alpha_bar = self.alpha_bar.data_ptr()
+        a.policy = L.TT_POLICY_STATIC
+        a.rows_tab = self.rows_tab.data_ptr() + 4 * f * self.max_rows
+        a.rows_cnt = self.rows_cnt.data_ptr() + 4 * f
+        a.y_mode = L.TT_Y_GATHER
+        a.ysrc = kspace[f].data_ptr()
+        a.y_frame_stride, a.y_slice_stride = self.nx * self.ny, self.nx * self.ny
+        a.lam, a.step_mode, a.mu, a.c_floor, a.c_cap = self.lam, mode, mu, cf, cc
+        if phase == 2 and out is not None:
+            a.gamma_out = out["gamma"][fo].data_ptr()
+            a.cost_out = out["cost"][fo:].data_ptr()
+            a.mu_out = out["mu"][fo:].data_ptr()
+            a.ah_hist = out["ah"][fo].data_ptr()
+            a.bh_hist = out["bh"][fo].data_ptr()
+        a.status = self.status.data_ptr()
+        a.scratch = self.scr.buf.data_ptr()
+        a.shard_rank, a.shard_world, a.shard_phase = self.rank_id, self.world, phase
+        a.xw, a.xg = self.xw.data_ptr(), self.xg.data_ptr()
+        return a
+
+    def partial(self, kspace, f):
+        K.track_rows(self._args(kspace, f, None, 0, 1))
+
+    def finish(self, kspace, f, out, fo):
+        K.track_rows(self._args(kspace, f, out, fo, 2))
+        self.t += 1
+        self.frame += 1
+
+    def run(self, kspace, frames, out=None):
+        """kspace: (T, nx, ny) complex64 CUDA (full frames). Frames from the current index."""
+        if out is None:
+            out = self.make_outputs(frames)
+        for fo in range(frames):
+            f = self.frame
+            self.partial(kspace, f)
+            self.allreduce(self.xw.view(torch.float32))
+            self.allreduce(self.xg)
+            self.finish(kspace, f, out, fo)
+        return out
