@@ -156,6 +156,22 @@ typedef struct tt_entries_args {
 size_t tt_entries_scratch_bytes(int nx, int ny, int rank, int nmeas);
 int tt_track_entries(void* stream, const tt_entries_args* a);
 
+/* ------------------------------------------------------------------ standalone step pieces
+ * For the reference API functions called on their own, on measurement-domain
+ * factors (Fourier masks: Ah = F_x A, Bh = F_y B) and an (i, j) index list:
+ *  tt_residual:   e = y - Phi gamma (tracker.py:388; instantaneous_cost :163-173)
+ *  tt_data_terms: D_A = conj(gamma) . Xi conj(Bh) (nx x R), D_B = conj(gamma) . Xi^T conj(Ah)
+ *                 (ny x R), Xi = scatter(e) (_gradient_data_terms, tracker.py:208-228), and
+ *                 cmax[r] = max(max_i sum_{j:(i,j)} |Bh_jr|^2, max_j sum_i |Ah_ir|^2), the exact
+ *                 curvature of hessian_bound (tracker.py:337-364).
+ * gamma is complex64 [R]; scratch: tt_terms_scratch_bytes(). */
+size_t tt_terms_scratch_bytes(int nx, int ny, int rank);
+int tt_residual(void* stream, int nx, int ny, int rank, int nmeas, const float* ah, const float* bh,
+                const int32_t* idx, const float* y, const float* gamma, float* e_out);
+int tt_data_terms(void* stream, int nx, int ny, int rank, int nmeas, const float* ah, const float* bh,
+                  const int32_t* idx, const float* e, const float* gamma, float* dA, float* dB, double* cmax,
+                  void* scratch);
+
 /* ------------------------------------------------------------------ sampling
  * row_scores (sampler.py:115-128) on the factor `a` ([nslices][nx][rank]):
  * s(i) = (ny e_i + R)/(R (nx + ny)), e_i = sum_r |a_ir|^2/||a_r||^2,

@@ -39,7 +39,10 @@ from .tracker import (
     StepConfig,
     StepReport,
     TrackerState,
+    factor_gradient,
+    hessian_bound,
     init_state,
+    instantaneous_cost,
     random_subspace,
     run,
     solve_gamma,
@@ -52,7 +55,7 @@ __all__ = [
     "EntryMask", "FourierMask", "MeasurementBatch", "build_phi", "row_distances", "rows_to_entries",
     "unitary_dft2", "unitary_dft_matrix", "variable_density_rows", "weighted_draw_without_replacement",
     "Fixed", "HessianBound", "StepConfig", "StepReport", "TrackerState", "init_state", "random_subspace",
-    "run", "solve_gamma", "track_step",
+    "run", "solve_gamma", "track_step", "factor_gradient", "hessian_bound", "instantaneous_cost",
     "SamplePlan", "SamplingDistribution", "adaptive_step", "draw_samples", "entry_scores",
     "expected_count_trace", "expected_sample_count", "row_scores",
     "FrameEstimate", "interp_track_step", "reconstruct_frame",

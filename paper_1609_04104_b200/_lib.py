@@ -73,6 +73,9 @@ SIGNATURES = {
     "tt_rows_shard_xg_len": (C.c_size_t, [C.c_int]),
     "tt_entries_scratch_bytes": (C.c_size_t, [C.c_int] * 4),
     "tt_track_entries": (C.c_int, [_p, C.POINTER(EntriesArgs)]),
+    "tt_terms_scratch_bytes": (C.c_size_t, [C.c_int, C.c_int, C.c_int]),
+    "tt_residual": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, C.c_int, _p, _p, _p, _p, _p, _p]),
+    "tt_data_terms": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, C.c_int, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "tt_row_scores": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, C.c_int, _p, _f64, _p, _p]),
     "tt_entry_scores": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, _p, _p, _f64, _p, _p]),
     "tt_draw_with_replacement": (C.c_int, [_p, C.c_int, C.c_int, _p, C.c_int, _p, C.c_int, _u64, _u64, _p, _p,

@@ -32,6 +32,9 @@ __all__ = [
     "random_subspace",
     "init_state",
     "solve_gamma",
+    "instantaneous_cost",
+    "factor_gradient",
+    "hessian_bound",
     "track_step",
     "run",
 ]
@@ -181,6 +184,86 @@ def solve_gamma(phi, y, lam: float) -> np.ndarray:
     dev = L.device()
     g = K.solve_gamma(torch.from_numpy(np.ascontiguousarray(phi)).to(dev), torch.from_numpy(y).to(dev), float(lam))
     return g.cpu().numpy()
+
+
+def _index_inputs(subspace, descriptor, gamma):
+    """Measurement factors, device index list and complex64 gamma for the
+    standalone step pieces."""
+    if not isinstance(subspace, TensorSubspace):
+        subspace = TensorSubspace(subspace.factors)
+    if subspace.dims != descriptor.shape:
+        raise ValueError("descriptor does not match the subspace dimensions")
+    kind = descriptor_kind(descriptor)
+    ah, bh = subspace.measurement_factors(kind)
+    dev = ah.device
+    idx = torch.from_numpy(np.ascontiguousarray(descriptor.indices, dtype=np.int32)).to(dev)
+    g = torch.from_numpy(np.asarray(gamma, dtype=np.complex128).ravel().astype(np.complex64)).to(dev)
+    if g.numel() != subspace.rank:
+        raise ValueError("gamma length does not match the rank")
+    return subspace, kind, ah.contiguous(), bh.contiguous(), idx, g
+
+
+def instantaneous_cost(subspace, batch, lam: float, t: int, gamma) -> float:
+    """0.5 ||y - Phi gamma||^2 + 0.5 (lam/t)(||A||^2 + ||B||^2) (tracker.py:163-173),
+    residual from the device kernel ``tt_residual``."""
+    sub, kind, ah, bh, idx, g = _index_inputs(subspace, batch.descriptor, gamma)
+    nx, ny = sub.dims
+    L_ = batch.descriptor.nmeas
+    e = torch.empty(max(L_, 1), dtype=torch.complex64, device=ah.device)
+    if L_:
+        y = batch.y_device()
+        L.check(L.lib().tt_residual(L.stream_ptr(), nx, ny, sub.rank, L_, ah.data_ptr(), bh.data_ptr(),
+                                    idx.data_ptr(), y.data_ptr(), g.data_ptr(), e.data_ptr()), "residual")
+    en = float(torch.linalg.vector_norm(ah.to(torch.complex128)) ** 2 + torch.linalg.vector_norm(bh.to(torch.complex128)) ** 2)
+    r2 = float(torch.linalg.vector_norm(e[:L_].to(torch.complex128)) ** 2) if L_ else 0.0
+    return 0.5 * r2 + 0.5 * (lam / t) * en
+
+
+def _data_terms(sub, kind, ah, bh, idx, g, residual):
+    nx, ny = sub.dims
+    R = sub.rank
+    dev = ah.device
+    L_ = int(idx.shape[0])
+    e = torch.from_numpy(np.asarray(residual, dtype=np.complex128).ravel().astype(np.complex64)).to(dev) \
+        if residual is not None else torch.zeros(max(L_, 1), dtype=torch.complex64, device=dev)
+    dA = torch.empty(nx, R, dtype=torch.complex64, device=dev)
+    dB = torch.empty(ny, R, dtype=torch.complex64, device=dev)
+    cmax = torch.empty(R, dtype=torch.float64, device=dev)
+    scr = torch.empty(int(L.lib().tt_terms_scratch_bytes(nx, ny, R)), dtype=torch.uint8, device=dev)
+    L.check(L.lib().tt_data_terms(L.stream_ptr(), nx, ny, R, L_, ah.data_ptr(), bh.data_ptr(),
+                                  idx.data_ptr() if L_ else None, e.data_ptr() if L_ else None, g.data_ptr(),
+                                  dA.data_ptr(), dB.data_ptr(), cmax.data_ptr(), scr.data_ptr()), "data_terms")
+    return dA, dB, cmax
+
+
+def factor_gradient(subspace, gamma, descriptor, residual, lam: float, t: int) -> list:
+    """(lam/t) F - conj(gamma) . sum_l e_l conj(w_l) per mode (tracker.py:241-262) from the
+    device data terms. For Fourier masks the k-space gradient is mapped back with the
+    inverse column FFT (the data term is conj(gamma) . F^-1 P)."""
+    sub, kind, ah, bh, idx, g = _index_inputs(subspace, descriptor, gamma)
+    if np.asarray(residual).size != descriptor.nmeas:
+        raise ValueError("residual length does not match descriptor")
+    dA, dB, _ = _data_terms(sub, kind, ah, bh, idx, g, residual)
+    s_ = float(lam) / float(t)
+    gA = ah * s_ - dA
+    gB = bh * s_ - dB
+    if kind == "fourier":
+        gA = K.fft_cols(gA.contiguous(), inverse=True)
+        gB = K.fft_cols(gB.contiguous(), inverse=True)
+    return [gA.cpu().numpy().astype(np.complex128), gB.cpu().numpy().astype(np.complex128)]
+
+
+def hessian_bound(subspace, gamma, descriptor, lam: float, t: int, c_floor: float = 0.0, c_cap: float = np.inf,
+                  iters: int = 1000, tol: float = 1e-8) -> float:
+    """Curvature bound alpha_t (tracker.py:337-364) in closed form: for Fourier and entry
+    masks lambda_max(G_{m,r}) is exactly the largest per-line sum of |Bh|^2 (|Ah|^2), which
+    the reference's power iteration approaches from below (within its tolerance)."""
+    del iters, tol
+    sub, kind, ah, bh, idx, g = _index_inputs(subspace, descriptor, gamma)
+    _, _, cmax = _data_terms(sub, kind, ah, bh, idx, g, None)
+    gam = np.asarray(gamma, dtype=np.complex128).ravel()
+    top = float(np.max(np.abs(gam) ** 2 * cmax.cpu().numpy())) if descriptor.nmeas else 0.0
+    return float(np.clip(lam / t + top, c_floor, c_cap))
 
 
 def _step_params(cfg: StepConfig):

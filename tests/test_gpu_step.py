@@ -165,3 +165,30 @@ def test_solve_gamma_matches_reference_golden():
         got = tt.solve_gamma(g[f"c{c}__phi"], g[f"c{c}__y"], float(g[f"c{c}__lam"]))
         assert rel(got, g[f"c{c}__gamma"]) < 1e-9
     assert np.array_equal(tt.solve_gamma(np.zeros((0, 4)), np.zeros(0), 1.0), np.zeros(4))
+
+
+@pytest.mark.parametrize("name", [n for n in NAMES if n != "empty"])
+def test_standalone_gradient_cost_and_curvature(name):
+    """factor_gradient / instantaneous_cost / hessian_bound as standalone calls vs the oracle
+    (and the reference's power-method alpha from the golden case, within its tolerance)."""
+    import paper_1609_04104_b200 as tt
+
+    c = _case(name)
+    A, B = c["A"], c["B"]
+    n1, n2 = A.shape[0], B.shape[0]
+    Desc = tt.FourierMask if c["kind"] == "fourier" else tt.EntryMask
+    desc = Desc((n1, n2), c["idx"])
+    sub = tt.TensorSubspace((A, B))
+    gam, res = c["gamma"], c["residual"]
+    got = tt.factor_gradient(sub, gam, desc, res, c["lam"], c["t"])
+    dA, dB = O.data_terms(A, B, gam, c["idx"], res, c["kind"])
+    want = [(c["lam"] / c["t"]) * A - dA, (c["lam"] / c["t"]) * B - dB]
+    for gg, ww in zip(got, want):
+        assert rel(gg, ww) < 1e-5
+    cost = tt.instantaneous_cost(sub, tt.MeasurementBatch(c["y"], desc), c["lam"], c["t"], gam)
+    assert cost == pytest.approx(c["cost"], rel=1e-5)
+    alpha = tt.hessian_bound(sub, gam, desc, c["lam"], c["t"])
+    assert alpha == pytest.approx(O.alpha_closed(A, B, gam, c["idx"], c["kind"], c["lam"], c["t"]), rel=1e-5)
+    assert alpha == pytest.approx(O.alpha_power(A, B, gam, c["idx"], c["kind"], c["lam"], c["t"]), rel=1e-5)
+    assert tt.hessian_bound(sub, np.zeros_like(gam), desc, 0.6, 3) == pytest.approx(0.2)
+    assert tt.hessian_bound(sub, gam, desc, c["lam"], c["t"], c_floor=1e6, c_cap=1e7) == 1e6
