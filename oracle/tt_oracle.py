@@ -497,3 +497,19 @@ def row_shard_finish(Ah, Bh, rows, Y, r0, r1, red, lam, t, mu):
     A_own[rows[own] - r0] += mu * np.conj(gamma)[None, :] * P
     B_new = c * Bh + mu * np.conj(gamma)[None, :] * Q
     return A_own, B_new, gamma, cost
+
+
+def warm_up(kspace_warm, A, B, lam, step, epochs, t0=1):
+    """experiment._warm_up (experiment.py:219-239): `warm_n` fully sampled frames
+    tracked for `epochs` passes, rebalanced between passes (core.py:138-166), time
+    continuing across passes. Full frames are all rows (Fourier, row-major)."""
+    kspace_warm = np.asarray(kspace_warm)
+    n1 = kspace_warm.shape[1]
+    t, ab = t0, 0.0
+    rows = [np.arange(n1)] * kspace_warm.shape[0]
+    for epoch in range(epochs):
+        if epoch > 0:
+            A, B = rebalance(A, B)
+        out = online_run(kspace_warm, A, B, lam, step, {"kind": "static", "rows": rows}, t0=t, alpha_bar=ab)
+        A, B, t, ab, _ = out["final"]
+    return A, B, t, ab

@@ -9,7 +9,7 @@ anywhere, but every compute call needs a CUDA device and the built library.
 """
 
 from .core import TensorSubspace, rebalance, synthesize_slice
-from .engine import Informative, OnlineEngine, OnlineResult, StaticRows, run_online
+from .engine import Informative, OnlineEngine, OnlineResult, RowShardedEngine, StaticRows, run_online, warm_up
 from .mri import FrameEstimate, interp_track_step, reconstruct_frame
 from .observation import (
     EntryMask,
@@ -59,5 +59,6 @@ __all__ = [
     "SamplePlan", "SamplingDistribution", "adaptive_step", "draw_samples", "entry_scores",
     "expected_count_trace", "expected_sample_count", "row_scores",
     "FrameEstimate", "interp_track_step", "reconstruct_frame",
-    "OnlineEngine", "OnlineResult", "StaticRows", "Informative", "run_online", "NumericalError",
+    "OnlineEngine", "OnlineResult", "StaticRows", "Informative", "run_online", "warm_up", "RowShardedEngine",
+    "NumericalError",
 ]

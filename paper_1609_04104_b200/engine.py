@@ -32,7 +32,7 @@ from . import _lib as L
 from . import _ops as K
 from .tracker import Fixed, HessianBound
 
-__all__ = ["StaticRows", "Informative", "OnlineEngine", "run_online", "OnlineResult"]
+__all__ = ["StaticRows", "Informative", "OnlineEngine", "run_online", "OnlineResult", "warm_up", "RowShardedEngine"]
 
 
 @dataclass(frozen=True)
@@ -220,11 +220,36 @@ class OnlineResult:
     final_B: np.ndarray
 
 
-def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1) -> OnlineResult:
-    """Public end-to-end call (host in, host out): the online loop over all
+def warm_up(engine: "OnlineEngine", kspace_warm: torch.Tensor, epochs: int) -> None:
+    """experiment._warm_up (experiment.py:219-239) on device: the fully sampled
+    leading frames tracked for `epochs` passes with `rebalance` between passes
+    (core.py:138-166); t keeps growing. Leaves the engine's resident factors,
+    t and alpha_bar as the streaming phase's starting state."""
+    W = int(kspace_warm.shape[0])
+    ns, nx = engine.nslices, engine.nx
+    full = np.broadcast_to(np.arange(nx, dtype=np.int32), (W, ns, nx)).copy()
+    weng = OnlineEngine(nx, engine.ny, engine.rank, ns, engine.lam, engine.step, StaticRows(full, np.full((W, ns), nx)),
+                        0, engine.t)
+    weng.ah, weng.bh, weng.alpha_bar = engine.ah, engine.bh, engine.alpha_bar
+    st = torch.zeros(ns, dtype=torch.int32, device=engine.dev)
+    for epoch in range(int(epochs)):
+        if epoch > 0:
+            K.rebalance_(weng.ah, weng.bh, st)
+        weng.frame = 0
+        weng.run(kspace_warm, W, history=False)
+    L.raise_status(int(st.max().item()) & L.TT_ST_ZEROCOL, "warm-up rebalance")
+    engine.ah, engine.bh, engine.alpha_bar, engine.t = weng.ah, weng.bh, weng.alpha_bar, weng.t
+
+
+def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, warm_frames=0,
+               warm_epochs=20) -> OnlineResult:
+    """Public end-to-end call (host in, host out): the online loop over the
     frames of ``kspace`` (T, [nslices,] nx, ny) from image-domain initial
     factors, returning reconstructions and per-frame reports. The analogue of
-    ``experiment.run_adaptive`` for pre-noised truth without warm-up."""
+    ``experiment.run_adaptive`` for pre-noised truth: with ``warm_frames`` > 0
+    the leading frames are fully sampled and tracked for ``warm_epochs`` passes
+    first (experiment.py:219-239, default 5 x 20 in the reference config) and
+    the results cover the streaming frames only; the policy applies to those."""
     ks = np.asarray(kspace) if not isinstance(kspace, torch.Tensor) else kspace
     if ks.ndim == 3:
         ks = ks[:, None]
@@ -237,6 +262,13 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1) -
         kd = ks.to(eng.dev, torch.complex64).contiguous()
     else:
         kd = torch.from_numpy(np.ascontiguousarray(ks, dtype=np.complex64)).to(eng.dev)
+    W = int(warm_frames)
+    if W:
+        warm_up(eng, kd[:W], warm_epochs)
+        kd = kd[W:]
+        if clean is not None:
+            clean = np.asarray(clean).reshape(T, ns, nx, ny)[W:]
+        T -= W
     out = eng.run(kd, T)
     X = eng.reconstruct(out)
     eng.check_status()

@@ -105,3 +105,27 @@ def test_batched_slices_equal_single_slice_runs():
         np.testing.assert_array_equal(batched.gamma[:, s], single.gamma[:, 0])
         for f in range(T):
             np.testing.assert_array_equal(batched.rows[f][s], single.rows[f][0])
+
+
+def test_warm_up_protocol_then_informative_stream():
+    """experiment.run_adaptive order: 5 full frames x 20 epochs with rebalance, t -> 101,
+    then informative streaming frames; vs the oracle restatement of _warm_up."""
+    import paper_1609_04104_b200 as tt
+    from paper_1609_04104_b200.phantom import cine_phantom
+
+    n, R, T, W, E, lam = 64, 6, 9, 5, 20, 0.1
+    ph = cine_phantom(n, n, T, period=8.0, seed=21)
+    A0, B0 = O.random_subspace(n, n, R, seed=22)
+    Aw, Bw, t, ab = O.warm_up(ph.kspace[:W], A0, B0, lam, ("fixed", 0.01), E)
+    assert t == 1 + W * E
+    forced = [0, 1, n - 1]
+    ref = O.online_run(ph.kspace[W:], Aw, Bw, lam, ("fixed", 0.01),
+                       {"kind": "informative", "k": 16, "forced": forced, "beta": 0.1, "key": (3, 0)},
+                       clean=ph.clean[W:], t0=t)
+    res = tt.run_online(ph.kspace, A0[None], B0[None], lam, tt.Fixed(0.01),
+                        tt.Informative(k=16, forced=tuple(forced), beta=0.1, key0=3), clean=ph.clean,
+                        warm_frames=W, warm_epochs=E)
+    for f in range(T - W):
+        np.testing.assert_array_equal(res.rows[f][0], ref["rows"][f])
+        assert rel(res.gamma[f, 0], ref["gamma"][f]) < 1e-4
+    assert np.max(np.abs(np.sqrt(res.nmse[:, 0]) - np.sqrt(ref["nmse"]))) < 1e-3
