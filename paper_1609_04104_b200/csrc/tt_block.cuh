@@ -563,6 +563,118 @@ TT_DEV void block_ldl2_solve(double2* Gio, const double2* hin, double2* gam, dou
   __syncthreads();
 }
 
+// ---------------------------------------------------------------- Gauss-Jordan ridge solve
+// Solves G gamma = h for Hermitian positive (semi)definite G (packed lower
+// triangle) by Gauss-Jordan elimination of the full augmented R x (R+1)
+// system without pivoting: R fully parallel steps, one barrier each, and no
+// back substitution (the latency of a serial triangular solve dominates a
+// blocked LDL^H at R <= 32). Thread t owns entries e = t + m*NT, column-major
+// (column j = e / R, row i = e % R; column R is h), in registers; step k only
+// touches columns j > k, so retired columns idle whole warps. The pivot
+// column and row of the next step are published to a double-buffered scratch
+// right after they are updated. Non-positive pivots drop their component
+// (gamma_k = 0), mirroring the s > 0 filter of the reference SVD ridge
+// (tracker.py:154-155).
+//   scratch: colb 2*2*(R+1) double2. Ends with __syncthreads.
+TT_DEV uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+TT_DEV double2 lds_d2(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+  return v;
+}
+TT_DEV double lds_d(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+TT_DEV void sts_d2(uint32_t a, double2 v) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
+// predicated store without a branch
+TT_DEV void sts_d2_if(bool p, uint32_t a, double2 v) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q st.shared.v2.f64 [%0], {%1, %2};\n\t}" ::"r"(a),
+      "d"(v.x), "d"(v.y), "r"((unsigned)p)
+      : "memory");
+}
+// opaque copy: keeps a value in a register (stops rematerialisation of the shared window base)
+TT_DEV uint32_t pin_u32(uint32_t x) {
+  uint32_t y;
+  asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+
+// registers per thread needed by block_gj_solve: ceil((R + 1) / (NT / R))
+__host__ __device__ inline int gj_ept(int R, int NT) {
+  const int ng = NT / R;
+  return ng > 0 ? (R + ng) / ng : 1 << 20;
+}
+
+template <int EPT>
+TT_DEV void block_gj_solve(const double2* G, const double2* hin, double2* gam, double2* colb, int R) {
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int W = R + 1;
+  // thread = (row i, column group): columns j = grp + m * ng. One pivot-column load per
+  // step serves all of a thread's entries, and the pivot-row loads are near-broadcasts.
+  const int ng = NT / R, grp = tid / R, i = tid - grp * R;
+  const bool live = grp < ng;
+  int rj[EPT];  // 0 for unused slots: column 0 is never updated
+  double2 g[EPT];
+  double idk = 0.0;
+#pragma unroll
+  for (int m = 0; m < EPT; ++m) {
+    const int j = grp + m * ng;
+    rj[m] = 0;
+    g[m] = make_double2(0.0, 0.0);
+    if (live && j < W) {
+      rj[m] = j;
+      if (j == R) g[m] = hin[i];
+      else if (i >= j) g[m] = G[i * (i + 1) / 2 + j];
+      else g[m] = zconj(G[j * (j + 1) / 2 + i]);
+      if (j == 0) colb[i] = g[m];               // pivot column 0
+      else if (i == 0) colb[W + j] = g[m];      // pivot row 0
+    }
+  }
+  __syncthreads();
+  // byte addresses into the double-buffered pivot column/row scratch (buffer b at b * 32 W)
+  const uint32_t base = smem_addr(colb);
+  const uint32_t oc = base + 16u * (live ? i : 0);
+  uint32_t orr[EPT];
+#pragma unroll
+  for (int m = 0; m < EPT; ++m) orr[m] = base + 16u * (W + rj[m]);
+  const uint32_t bstride = 32u * W;
+  for (int k = 0; k < R; ++k) {
+    const uint32_t cur = (k & 1) ? bstride : 0u, nxt = bstride - cur;
+    // operands first: the products a_ik a_kj do not depend on the pivot inverse
+    const double2 aik = lds_d2(oc + cur);
+    double2 u[EPT];
+#pragma unroll
+    for (int m = 0; m < EPT; ++m) u[m] = zmul(aik, lds_d2(orr[m] + cur));
+    const double d = lds_d(base + cur + 16u * k);
+    const double id = d > 0.0 ? fast_rcp(d) : 0.0;
+    const double sc = i != k ? id : 0.0;
+#pragma unroll
+    for (int m = 0; m < EPT; ++m) {
+      const int j = rj[m];
+      const bool act = j > k;
+      const double s = act ? sc : 0.0;
+      g[m].x = fma(-u[m].x, s, g[m].x);
+      g[m].y = fma(-u[m].y, s, g[m].y);
+      const bool pc_next = act && j == k + 1;  // next pivot column (row k included: final)
+      sts_d2_if(pc_next || (act && i == k + 1), (pc_next ? oc : orr[m]) + nxt, g[m]);
+    }
+    if (i == k) idk = id;
+    __syncthreads();
+#ifdef TT_GJ_STAMPS
+    if (tid == 0) tt_gj_stamps[k] = clock64();
+#endif
+  }
+#pragma unroll
+  for (int m = 0; m < EPT; ++m)
+    if (live && rj[m] == R) gam[i] = zscale(g[m], idk);
+  __syncthreads();
+}
+
 // ---------------------------------------------------------------- register-tiled complex GEMM
 // C(m, n) = sum_{k<K} opA(A[m*a_m + k*a_k]) * opB(B[k*b_k + n*b_n]) over shared
 // memory operands (complex fp32). Work item = (TM x TN output tile, k part);
