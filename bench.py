@@ -452,8 +452,11 @@ def run_ours(args, cfg):
     h2d = d2h = 0
     if not args.no_e2e:
         ks_pin = torch.from_numpy(ks_np).pin_memory()
-        for _ in range(1):
-            tt.run_online(ks_pin, A0, B0, cfg["lam"], tt.Fixed(cfg["mu"]), pol, cluster=args.cluster)
+        # two warm-up calls in the timed loop's pattern (the previous result stays alive while the next
+        # call runs): both pinned result blocks are then in torch's host caching allocator
+        res = None
+        for _ in range(2):
+            res = tt.run_online(ks_pin, A0, B0, cfg["lam"], tt.Fixed(cfg["mu"]), pol, cluster=args.cluster)
         torch.cuda.synchronize()
         t_e2e = []
         for _ in range(max(1, args.steps)):

@@ -590,6 +590,13 @@ TT_DEV double lds_d(uint32_t a) {
 TT_DEV void sts_d2(uint32_t a, double2 v) {
   asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
 }
+// clock stamp stored by one thread, without a branch
+TT_DEV void stamp_if(bool p, long long* dst) {
+  const long long v = clock64();
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.global.s64 [%0], %1;\n\t}" ::"l"(dst), "l"(v),
+               "r"((unsigned)p)
+               : "memory");
+}
 // predicated store without a branch
 TT_DEV void sts_d2_if(bool p, uint32_t a, double2 v) {
   asm volatile(

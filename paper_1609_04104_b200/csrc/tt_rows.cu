@@ -258,9 +258,10 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
   (void)inv;
   __shared__ int sh_S, sh_err, sh_own, sh_amb;
   long long* pclk = (a.phase_clock != nullptr && blockIdx.x == 0) ? (long long*)a.phase_clock : nullptr;
-#define STAMP(k)                                                             \
-  do {                                                                       \
-    if (pclk != nullptr && tid == 0) pclk[(size_t)f * 32 + (k)] = clock64(); \
+  // branch-free (a lane-0 branch would leave warp 0 diverged and send later shuffles down the slow path)
+#define STAMP(k)                                                                                   \
+  do {                                                                                             \
+    if (pclk != nullptr) stamp_if(tid == 0, pclk + (size_t)f * 32 + (k));                          \
   } while (0)
 
   // global scratch for this slice
@@ -383,6 +384,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       for (int i = tid; i < nx; i += NT) pbuf[i] = __ldcg(&g_sraw[i]);  // one parallel round trip
       if (tid == 0) sh_amb = 0;
       __syncthreads();
+      STAMP(24);
       if (warp == 0) {
         // probabilities: normalise, blend with the uniform law (sampler.py:88-92); the final
         // renormalisation is folded into cdf /= cdf[-1]. Chunked warp scan -> normalised CDF.
@@ -391,6 +393,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         double loc = 0.0;
         for (int i = q0; i < q1; ++i) loc += pbuf[i];
         const double S1 = warp_sum(loc);
+        STAMP(29);
         const double w1 = (1.0 - a.beta) / S1, w0 = a.beta / (double)nx;
         loc = 0.0;
         for (int i = q0; i < q1; ++i) {
@@ -399,6 +402,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
           loc += v;
         }
         double x = loc;
+        STAMP(30);
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const double y = __shfl_up_sync(0xffffffffu, x, o);
@@ -411,8 +415,10 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
           cdf[i] = run * il;
           flags[i] = 0;
         }
+        STAMP(31);
       }
       __syncthreads();
+      STAMP(25);
       // draws (numpy choice semantics, sampler.py:160-162): groups of 8 lanes search the CDF
       // cooperatively (3 rounds of 8 probes + ballot for nx = 256) with precomputed uniforms
       {
@@ -439,6 +445,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         }
       }
       __syncthreads();
+      STAMP(27);
       if (sh_amb) {  // a uniform within 1e-12 of a CDF boundary: exact sequential numpy cumsum, redo
         if (tid == 0) {
           double cacc = 0.0;
@@ -461,6 +468,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         }
         __syncthreads();
       }
+      STAMP(28);
       if (warp == 0) {  // forced lines, then compaction -> sorted unique rows (np.union1d)
         for (int m = lane; m < a.nforced; m += 32) {
           const int fr = forced[m];

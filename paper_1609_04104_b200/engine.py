@@ -241,50 +241,101 @@ def warm_up(engine: "OnlineEngine", kspace_warm: torch.Tensor, epochs: int) -> N
     engine.ah, engine.bh, engine.alpha_bar, engine.t = weng.ah, weng.bh, weng.alpha_bar, weng.t
 
 
+def _host_source(kspace):
+    """(T, nslices, nx, ny) complex64 CPU tensor over the caller's host buffer (no copy when it
+    already is one; pinned buffers make the chunked uploads asynchronous)."""
+    if isinstance(kspace, torch.Tensor):
+        t = kspace
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(kspace), dtype=np.complex64))
+    if t.dim() == 3:
+        t = t[:, None]
+    return t.to(torch.complex64).contiguous()
+
+
 def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, warm_frames=0,
-               warm_epochs=20) -> OnlineResult:
+               warm_epochs=20, chunk=40) -> OnlineResult:
     """Public end-to-end call (host in, host out): the online loop over the
     frames of ``kspace`` (T, [nslices,] nx, ny) from image-domain initial
     factors, returning reconstructions and per-frame reports. The analogue of
     ``experiment.run_adaptive`` for pre-noised truth: with ``warm_frames`` > 0
     the leading frames are fully sampled and tracked for ``warm_epochs`` passes
     first (experiment.py:219-239, default 5 x 20 in the reference config) and
-    the results cover the streaming frames only; the policy applies to those."""
-    ks = np.asarray(kspace) if not isinstance(kspace, torch.Tensor) else kspace
-    if ks.ndim == 3:
-        ks = ks[:, None]
-    T, ns, nx, ny = ks.shape
+    the results cover the streaming frames only; the policy applies to those.
+
+    Pipelined in blocks of ``chunk`` frames: the truth uploads on one copy
+    stream, tracking + reconstruction of block c on the compute stream once
+    its upload landed, and the reconstructions download into pinned host
+    memory on a second copy stream while later blocks compute. Results do not
+    depend on ``chunk`` (the resident state and the Philox stream position
+    carry across launches)."""
+    on_dev = isinstance(kspace, torch.Tensor) and kspace.is_cuda
+    src = kspace.to(torch.complex64) if on_dev else _host_source(kspace)
+    if src.dim() == 3:
+        src = src[:, None]
+    T, ns, nx, ny = src.shape
     A0 = np.asarray(A0).reshape(ns, nx, -1)
     R = A0.shape[-1]
     eng = OnlineEngine(nx, ny, R, ns, lam, step, policy, cluster, t0)
     eng.set_image_factors(A0, np.asarray(B0).reshape(ns, ny, R))
-    if isinstance(ks, torch.Tensor):
-        kd = ks.to(eng.dev, torch.complex64).contiguous()
-    else:
-        kd = torch.from_numpy(np.ascontiguousarray(ks, dtype=np.complex64)).to(eng.dev)
+    dev = eng.dev
+    comp = torch.cuda.current_stream(dev)
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    kd = src.contiguous() if on_dev else torch.empty(T, ns, nx, ny, dtype=torch.complex64, device=dev)
     W = int(warm_frames)
+    C = max(1, int(chunk))
+    # upload blocks: the warm-up frames as one block, then the streaming frames in blocks of C
+    bounds = ([(0, W)] if W else []) + [(f, min(T, f + C)) for f in range(W, T, C)]
+    s_in.wait_stream(comp)
+    ev_in = []
+    with torch.cuda.stream(s_in):
+        for f0, f1 in bounds:
+            if not on_dev:
+                kd[f0:f1].copy_(src[f0:f1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(s_in)
+            ev_in.append(ev)
+    blocks = list(zip(bounds, ev_in))
     if W:
+        comp.wait_event(blocks[0][1])
         warm_up(eng, kd[:W], warm_epochs)
-        kd = kd[W:]
+        blocks = blocks[1:]
         if clean is not None:
             clean = np.asarray(clean).reshape(T, ns, nx, ny)[W:]
-        T -= W
-    out = eng.run(kd, T)
-    X = eng.reconstruct(out)
-    eng.check_status()
+    Ts = T - W
+    ks_stream = kd[W:]
+    out = eng.make_outputs(Ts)
+    recon = torch.empty(Ts, ns, nx, ny, dtype=torch.complex64, pin_memory=True)
+    Xd = torch.empty(Ts, ns, nx, ny, dtype=torch.complex64, device=dev)
+    s_out.wait_stream(comp)
+    for (f0, f1), ev in blocks:
+        a, b = f0 - W, f1 - W
+        comp.wait_event(ev)
+        part = {k: v[a:b] for k, v in out.items()}
+        eng.run(ks_stream, b - a, out=part)
+        Xd[a:b] = eng.reconstruct(part)
+        done = torch.cuda.Event()
+        done.record(comp)
+        s_out.wait_event(done)
+        with torch.cuda.stream(s_out):
+            recon[a:b].copy_(Xd[a:b], non_blocking=True)
+    Xd.record_stream(s_out)
+    small = {k: out[k].to("cpu", non_blocking=False) for k in ("gamma", "cost", "mu", "cnt", "rows")}
+    A, B = eng.image_factors()
+    A, B = A.cpu().numpy(), B.cpu().numpy()
     nm = None
     if clean is not None:
-        cl = torch.as_tensor(np.asarray(clean, dtype=np.complex64)).to(eng.dev).reshape(T, ns, nx, ny)
-        num = (cl - X).abs().pow(2).sum(dim=(-1, -2)).double()
+        cl = torch.as_tensor(np.asarray(clean, dtype=np.complex64)).to(dev).reshape(Ts, ns, nx, ny)
+        num = (cl - Xd).abs().pow(2).sum(dim=(-1, -2)).double()
         den = cl.abs().pow(2).sum(dim=(-1, -2)).double()
         nm = (num / den).cpu().numpy()
-    cnt = out["cnt"].cpu().numpy()
-    rows_np = out["rows"].cpu().numpy()
-    rows = [[rows_np[f, s, :cnt[f, s]].astype(np.int64) for s in range(ns)] for f in range(T)]
-    A, B = eng.image_factors()
-    return OnlineResult(recon=X.cpu().numpy(), gamma=out["gamma"].cpu().numpy(), cost=out["cost"].cpu().numpy(),
-                        mu=out["mu"].cpu().numpy(), rows=rows, nmse=nm, final_A=A.cpu().numpy(),
-                        final_B=B.cpu().numpy())
+    s_out.synchronize()
+    eng.check_status()
+    cnt = small["cnt"].numpy()
+    rows_np = small["rows"].numpy()
+    rows = [[rows_np[f, s, :cnt[f, s]].astype(np.int64) for s in range(ns)] for f in range(Ts)]
+    return OnlineResult(recon=recon.numpy(), gamma=small["gamma"].numpy(), cost=small["cost"].numpy(),
+                        mu=small["mu"].numpy(), rows=rows, nmse=nm, final_A=A, final_B=B)
 
 
 class RowShardedEngine:

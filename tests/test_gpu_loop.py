@@ -129,3 +129,26 @@ def test_warm_up_protocol_then_informative_stream():
         np.testing.assert_array_equal(res.rows[f][0], ref["rows"][f])
         assert rel(res.gamma[f, 0], ref["gamma"][f]) < 1e-4
     assert np.max(np.abs(np.sqrt(res.nmse[:, 0]) - np.sqrt(ref["nmse"]))) < 1e-3
+
+
+@pytest.mark.parametrize("chunk", [1, 7, 1000])
+def test_pipelined_run_online_is_chunk_invariant(chunk):
+    """run_online's block pipelining (uploads / tracking / downloads overlapped) gives the
+    same bits for any block size, from pinned, pageable and device inputs."""
+    import torch
+    import paper_1609_04104_b200 as tt
+    from paper_1609_04104_b200.phantom import cine_phantom
+
+    n, R, T = 64, 6, 23
+    ph = cine_phantom(n, n, T, period=8.0, seed=31)
+    A0, B0 = O.random_subspace(n, n, R, seed=32)
+    pol = tt.Informative(k=16, forced=(0, 1, n - 1), beta=0.1, key0=5)
+    ref = tt.run_online(ph.kspace, A0[None], B0[None], 0.1, tt.Fixed(0.01), pol, chunk=T)
+    for src in (torch.from_numpy(ph.kspace.astype(np.complex64)).pin_memory(), ph.kspace,
+                torch.from_numpy(ph.kspace.astype(np.complex64)).cuda()):
+        got = tt.run_online(src, A0[None], B0[None], 0.1, tt.Fixed(0.01), pol, chunk=chunk)
+        np.testing.assert_array_equal(got.gamma, ref.gamma)
+        np.testing.assert_array_equal(got.recon, ref.recon)
+        np.testing.assert_array_equal(got.final_A, ref.final_A)
+        for f in range(T):
+            np.testing.assert_array_equal(got.rows[f][0], ref.rows[f][0])
