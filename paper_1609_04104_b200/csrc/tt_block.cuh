@@ -82,6 +82,16 @@ TT_DEV double block_excl_scan_dbl(double v, double* red, double& total) {
   return off + (x - v);
 }
 
+// Sum of p[0..n) over the block (chunked, fixed order); every thread receives the total.
+TT_DEV double block_sum_range(const double* p, int n, double* red, double& total) {
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int chunk = (n + NT - 1) / NT;
+  const int c0 = min(n, tid * chunk), c1 = min(n, c0 + chunk);
+  double local = 0.0;
+  for (int i = c0; i < c1; ++i) local += p[i];
+  return block_excl_scan_dbl(local, red, total);
+}
+
 TT_DEV int upper_bound_d(const double* cdf, int n, double u) {
   int lo = 0, hi = n;
   while (lo < hi) {

@@ -288,6 +288,18 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       for (int m = tid; m < a.nforced; m += NT) forced[m] = a.forced[m];
   }
   ldl_table_init(tab, R);
+  // forced lines among this thread's rows of the block-wide draw (bits, registers for the whole launch)
+  unsigned fmask = 0u;
+  int top = 1;  // largest power of two <= nx (binary search of the CDF)
+  while (2 * top <= nx) top *= 2;
+  const double inx = 1.0 / (double)nx;
+  if (a.policy == TT_POLICY_INFORMATIVE && nx <= 4 * NT) {
+    const int ipt = (nx + NT - 1) / NT, r0 = tid * ipt;
+    for (int m = 0; m < a.nforced; ++m) {
+      const int d = a.forced[m] - r0;
+      if (d >= 0 && d < ipt && r0 + d < nx) fmask |= 1u << d;
+    }
+  }
   double alpha_bar = a.alpha_bar ? a.alpha_bar[s] : 0.0;
   uint64_t ppos = (a.policy == TT_POLICY_INFORMATIVE && a.philox_pos) ? a.philox_pos[s] : 0ull;
   int status = 0;
@@ -381,72 +393,78 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       STAMP(3);
       cluster_barrier();  // -------------------------------------------- B2
       STAMP(4);
-      for (int i = tid; i < nx; i += NT) pbuf[i] = __ldcg(&g_sraw[i]);  // one parallel round trip
-      if (tid == 0) sh_amb = 0;
-      __syncthreads();
-      STAMP(24);
-      if (warp == 0) {
-        // probabilities: normalise, blend with the uniform law (sampler.py:88-92); the final
-        // renormalisation is folded into cdf /= cdf[-1]. Chunked warp scan -> normalised CDF.
-        const int chunk = (nx + 31) / 32;
-        const int q0 = min(nx, lane * chunk), q1 = min(nx, q0 + chunk);
+      if (nx <= 4 * NT) {
+        // Block-wide probabilities -> CDF -> draws -> sorted union, every warp busy (sampler.py:88-92,
+        // :146-162). Thread t owns rows [r0, r1) (consecutive). One scan of the raw scores s gives
+        // the blended CDF in closed form: with w1 = (1-beta)/sum(s), w0 = beta/nx,
+        //   cdf_i = (w1 C_i + w0 (i+1)) / (w1 sum(s) + w0 nx),  C_i = s_0 + .. + s_i
+        // (numpy's cumsum(p) / cdf[-1] up to rounding; the 1e-12 guard below covers the difference).
+        const int ipt = (nx + NT - 1) / NT;
+        const int r0 = min(nx, tid * ipt), r1 = min(nx, r0 + ipt);
+        double sv[4], cv[4];
         double loc = 0.0;
-        for (int i = q0; i < q1; ++i) loc += pbuf[i];
-        const double S1 = warp_sum(loc);
-        STAMP(29);
-        const double w1 = (1.0 - a.beta) / S1, w0 = a.beta / (double)nx;
-        loc = 0.0;
-        for (int i = q0; i < q1; ++i) {
-          const double v = fma(pbuf[i], w1, w0);
-          pbuf[i] = v;
-          loc += v;
-        }
-        double x = loc;
-        STAMP(30);
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const double y = __shfl_up_sync(0xffffffffu, x, o);
-          if (lane >= o) x += y;
+        for (int j = 0; j < 4; ++j) {
+          sv[j] = (j < ipt && r0 + j < r1) ? __ldcg(&g_sraw[r0 + j]) : 0.0;
+          loc += sv[j];
         }
-        const double il = fast_rcp(__shfl_sync(0xffffffffu, x, 31));
-        double run = x - loc;
-        for (int i = q0; i < q1; ++i) {
-          run += pbuf[i];
-          cdf[i] = run * il;
-          flags[i] = 0;
+        double S1;
+        double run = block_excl_scan_dbl(loc, red, S1);
+        const double w1 = (1.0 - a.beta) * fast_rcp(S1), w0 = a.beta * inx;
+        const double il = fast_rcp(fma(w1, S1, w0 * (double)nx));
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (j < ipt && r0 + j < r1) {
+            run += sv[j];
+            cv[j] = fma(w1, run, w0 * (double)(r0 + j + 1)) * il;
+            cdf[r0 + j] = cv[j];
+            pbuf[r0 + j] = fma(sv[j], w1, w0);  // probabilities for the exact fallback
+            flags[r0 + j] = 0;
+          }
         }
+        if (tid == 0) sh_amb = 0;
+        __syncthreads();
+        STAMP(29);
+        // draws, one per thread: idx = searchsorted(cdf, u, 'right') by a branch-free binary search
+        for (int m = tid; m < ndraw; m += NT) {
+          const double u = usm[m];
+          int pos = -1;  // last index with cdf <= u
+          for (int step = top; step > 0; step >>= 1) {
+            const int cand = pos + step;
+            if (cand < nx && cdf[cand] <= u) pos = cand;
+          }
+          const int idx = min(pos + 1, nx - 1);
+          const double lo = idx > 0 ? cdf[idx - 1] : -1.0;
+          if (u - lo <= 1e-12 || (idx < nx - 1 && cdf[idx] - u <= 1e-12)) sh_amb = 1;
+          flags[idx] = 1;
+        }
+        __syncthreads();
+        STAMP(30);
+        unsigned hit = fmask;  // forced lines (np.union1d)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (j < ipt && r0 + j < r1 && flags[r0 + j]) hit |= 1u << j;
+        int tot;
+        int o = block_excl_scan_int(__popc(hit), (int*)red, tot);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (hit & (1u << j)) rows[o++] = r0 + j;
+        if (tid == 0) sh_S = tot;
         STAMP(31);
       }
-      __syncthreads();
-      STAMP(25);
-      // draws (numpy choice semantics, sampler.py:160-162): groups of 8 lanes search the CDF
-      // cooperatively (3 rounds of 8 probes + ballot for nx = 256) with precomputed uniforms
-      {
-        const int g = tid >> 3, gl = tid & 7, ng = NT >> 3;
-        for (int mb = 0; mb < ndraw; mb += ng) {  // warp-uniform trip count
-          const int m = mb + g;
-          const double u = m < ndraw ? usm[m] : 2.0;
-          int lo = 0, sz = nx + 1;  // idx = first i with cdf[i] > u lies in [lo, lo + sz)
-          while (sz > 1) {
-            const int step = (sz + 7) >> 3;
-            const int probe = lo + (gl + 1) * step - 1;
-            const bool gt = probe >= nx || cdf[probe] > u;
-            const unsigned gm = (__ballot_sync(0xffffffffu, gt) >> (lane & 24)) & 0xffu;
-            const int fi = __ffs(gm) - 1;
-            lo += fi * step;
-            sz = step;
-          }
-          if (m < ndraw && gl == 0) {
-            const double lo_v = lo > 0 ? cdf[lo - 1] : -1.0;
-            const double hi_v = lo < nx ? cdf[lo] : 2.0;
-            if (u - lo_v <= 1e-12 || hi_v - u <= 1e-12) sh_amb = 1;
-            flags[lo < nx ? lo : nx - 1] = 1;
-          }
+      if (nx > 4 * NT || sh_amb) {
+        // generic width, or a uniform within 1e-12 of a CDF boundary: numpy's sequential cumsum
+        // of the probabilities, cdf /= cdf[-1], per-draw searchsorted, forced union, compaction
+        if (nx > 4 * NT) {
+          for (int i = tid; i < nx; i += NT) pbuf[i] = __ldcg(&g_sraw[i]);
+          __syncthreads();
+          double S1;
+          const double loc = block_sum_range(pbuf, nx, red, S1);
+          (void)loc;
+          const double w1 = (1.0 - a.beta) / S1, w0 = a.beta / (double)nx;
+          for (int i = tid; i < nx; i += NT) pbuf[i] = fma(pbuf[i], w1, w0);
         }
-      }
-      __syncthreads();
-      STAMP(27);
-      if (sh_amb) {  // a uniform within 1e-12 of a CDF boundary: exact sequential numpy cumsum, redo
+        __syncthreads();
         if (tid == 0) {
           double cacc = 0.0;
           for (int i = 0; i < nx; ++i) {
@@ -467,28 +485,27 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
           flags[idx < nx ? idx : nx - 1] = 1;
         }
         __syncthreads();
-      }
-      STAMP(28);
-      if (warp == 0) {  // forced lines, then compaction -> sorted unique rows (np.union1d)
-        for (int m = lane; m < a.nforced; m += 32) {
-          const int fr = forced[m];
-          if (fr >= 0 && fr < nx) flags[fr] = 1;
-        }
-        __syncwarp();
-        const int chunk = (nx + 31) / 32;
-        const int q0 = min(nx, lane * chunk), q1 = min(nx, q0 + chunk);
-        int cnt = 0;
-        for (int i = q0; i < q1; ++i) cnt += flags[i];
-        int x = cnt;
+        if (warp == 0) {  // forced lines, then compaction -> sorted unique rows (np.union1d)
+          for (int m = lane; m < a.nforced; m += 32) {
+            const int fr = forced[m];
+            if (fr >= 0 && fr < nx) flags[fr] = 1;
+          }
+          __syncwarp();
+          const int chunk = (nx + 31) / 32;
+          const int q0 = min(nx, lane * chunk), q1 = min(nx, q0 + chunk);
+          int cnt = 0;
+          for (int i = q0; i < q1; ++i) cnt += flags[i];
+          int x = cnt;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, x, o);
-          if (lane >= o) x += y;
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+          }
+          int o = x - cnt;
+          for (int i = q0; i < q1; ++i)
+            if (flags[i]) rows[o++] = i;
+          if (lane == 31) sh_S = x;
         }
-        int o = x - cnt;
-        for (int i = q0; i < q1; ++i)
-          if (flags[i]) rows[o++] = i;
-        if (lane == 31) sh_S = x;
       }
       ppos += (uint64_t)max(a.k_draws - a.nforced, 0);
       STAMP(20);
