@@ -607,6 +607,12 @@ TT_DEV void stamp_if(bool p, long long* dst) {
                "r"((unsigned)p)
                : "memory");
 }
+// clock stamp taken once a shared load issued after the preceding barrier has returned
+TT_DEV void stamp_after(bool p, long long* dst, const int* dep) {
+  const int v = *(const volatile int*)dep;
+  if (v == 0x7fffffff) asm volatile("trap;");
+  stamp_if(p, dst);
+}
 // predicated store without a branch
 TT_DEV void sts_d2_if(bool p, uint32_t a, double2 v) {
   asm volatile(
@@ -754,6 +760,79 @@ TT_DEV void cgemm_tile(int M, int N, int K, const float2* A, int a_m, int a_k, c
       float2 s = red[o];
       for (int ks = 1; ks < KS; ++ks) s = cadd(s, red[(size_t)ks * M * N + o]);
       out(o / N, o % N, s);
+    }
+  }
+}
+
+// Register-tiled complex GEMM, K split across adjacent lanes: C(m, n) = sum_k opA(A[m*a_m + k*a_k]) *
+// opB(B[k*b_k + n*b_n]) over shared-memory operands. Work item = (TM x TN tile, k part); the KS parts of
+// a tile sit on adjacent lanes and are summed by a fixed-order shuffle butterfly (deterministic, no
+// reduction buffer, no barrier). Every (m, n) is delivered once to out(m, n, value) by the part-0 lane.
+// KS must be a power of two <= 32. Callers synchronise after.
+template <int TM, int TN, int KS, bool CA, bool CB, typename Out>
+TT_DEV void cgemm_v2(int M, int N, int K, const float2* A, int a_m, int a_k, const float2* B, int b_k, int b_n,
+                     Out out) {
+  static_assert(KS >= 1 && KS <= 32 && (KS & (KS - 1)) == 0, "KS: power of two <= 32");
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int tn = (N + TN - 1) / TN, tiles = ((M + TM - 1) / TM) * tn;
+  const int items = tiles * KS;
+  const int kc = (K + KS - 1) / KS;
+  for (int base = 0; base < items; base += NT) {  // uniform trip count: the butterfly stays convergent
+    const int it = base + tid;
+    const bool live = it < items;
+    const int tile = it / KS, part = it & (KS - 1);
+    const int mt = tile / tn, nt = tile - mt * tn;
+    const int m0 = mt * TM, n0 = nt * TN;
+    const int k0 = part * kc, k1 = min(K, k0 + kc);
+    float2 acc[TM][TN];
+#pragma unroll
+    for (int u = 0; u < TM; ++u)
+#pragma unroll
+      for (int v = 0; v < TN; ++v) acc[u][v] = make_float2(0.f, 0.f);
+    if (live) {
+      int ao[TM], bo[TN];
+#pragma unroll
+      for (int u = 0; u < TM; ++u) ao[u] = min(m0 + u, M - 1) * a_m + k0 * a_k;
+#pragma unroll
+      for (int v = 0; v < TN; ++v) bo[v] = min(n0 + v, N - 1) * b_n + k0 * b_k;
+#pragma unroll 4
+      for (int k = k0; k < k1; ++k) {
+        float2 a[TM], b[TN];
+#pragma unroll
+        for (int u = 0; u < TM; ++u) {
+          a[u] = A[ao[u]];
+          ao[u] += a_k;
+          if (CA) a[u].y = -a[u].y;
+        }
+#pragma unroll
+        for (int v = 0; v < TN; ++v) {
+          b[v] = B[bo[v]];
+          bo[v] += b_k;
+          if (CB) b[v].y = -b[v].y;
+        }
+#pragma unroll
+        for (int u = 0; u < TM; ++u)
+#pragma unroll
+          for (int v = 0; v < TN; ++v) acc[u][v] = cfma(a[u], b[v], acc[u][v]);
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < KS; o <<= 1)
+#pragma unroll
+      for (int u = 0; u < TM; ++u)
+#pragma unroll
+        for (int v = 0; v < TN; ++v) {
+          acc[u][v].x += __shfl_xor_sync(0xffffffffu, acc[u][v].x, o);
+          acc[u][v].y += __shfl_xor_sync(0xffffffffu, acc[u][v].y, o);
+        }
+    if (live && part == 0) {
+#pragma unroll
+      for (int u = 0; u < TM; ++u)
+#pragma unroll
+        for (int v = 0; v < TN; ++v) {
+          const int m = m0 + u, n = n0 + v;
+          if (m < M && n < N) out(m, n, acc[u][v]);
+        }
     }
   }
 }

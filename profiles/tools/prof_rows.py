@@ -28,8 +28,8 @@ clk = torch.zeros(T, 32, dtype=torch.int64, device='cuda')
 args.phase_clock = clk.data_ptr()
 eng.philox_pos.zero_(); K.track_rows(args); torch.cuda.synchronize()
 c = clk.cpu().numpy().astype(np.int64)
-names = {26:"a:colnorm",21:"u:mark",22:"u:P",23:"u:Q",1:"a-partials",2:"B1",3:"scores(own)",4:"B2",24:"b:sraw-load",29:"b:scan+cdf",30:"b:draws",31:"b:union",27:"b:draws",28:"b:amb",20:"b:compact",5:"draw",6:"publishAhS",7:"B3",16:"h:tileload",17:"h:W",18:"h:Z",19:"h:GA",8:"heavy-rest",9:"h/ga/yn",10:"B4",11:"Gbuild",12:"LDL",13:"cost/mu",14:"update",15:"outputs"}
-order = [0,26,1,2,3,4,29,30,31,20,5,6,7,16,17,18,19,8,9,10,11,12,13,21,22,23,14,15]
+names = {26:"a:colnorm",1:"a-partials",2:"B1",24:"s:nrm",25:"s:usm",27:"s:sync",28:"s:ahnorm",3:"s:scores",4:"B2",29:"b:scan+cdf",30:"b:draws",31:"b:union",20:"b:end",5:"draw",6:"publishAhS",7:"B3",16:"h:tileload",17:"h:W",18:"h:Z",19:"h:GA",8:"heavy-rest",9:"h/ga/yn",10:"B4",11:"Gbuild",12:"solve",13:"cost/mu",21:"u:mark",22:"u:P",23:"u:Q",14:"update",15:"outputs"}
+order = [0,26,1,2,24,25,27,28,3,4,29,30,31,20,5,6,7,16,17,18,19,8,9,10,11,12,13,21,22,23,14,15]
 cc = c[5:]
 print("cycles per phase (median over frames 5..):")
 prev = None
