@@ -253,6 +253,25 @@ def _host_source(kspace):
     return t.to(torch.complex64).contiguous()
 
 
+def _blocks(f0, f1, C):
+    """Frame blocks [a, b) covering [f0, f1): short first and last blocks (the pipeline's fill and
+    drain are one upload / one download of a block), ``C`` frames in between."""
+    n = f1 - f0
+    if n <= 0:
+        return []
+    e = max(1, min(C, 8))
+    if n <= 2 * e + C:
+        sizes = [n] if n <= C else [e, n - e]
+    else:
+        mid = n - 2 * e
+        sizes = [e] + [C] * (mid // C) + ([mid % C] if mid % C else []) + [e]
+    out, f = [], f0
+    for sz in sizes:
+        out.append((f, f + sz))
+        f += sz
+    return out
+
+
 def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, warm_frames=0,
                warm_epochs=20, chunk=40) -> OnlineResult:
     """Public end-to-end call (host in, host out): the online loop over the
@@ -285,7 +304,7 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
     W = int(warm_frames)
     C = max(1, int(chunk))
     # upload blocks: the warm-up frames as one block, then the streaming frames in blocks of C
-    bounds = ([(0, W)] if W else []) + [(f, min(T, f + C)) for f in range(W, T, C)]
+    bounds = ([(0, W)] if W else []) + _blocks(W, T, C)
     s_in.wait_stream(comp)
     ev_in = []
     with torch.cuda.stream(s_in):
