@@ -152,9 +152,21 @@ typedef struct tt_entries_args {
   float* resid_out;           /* [nmeas] or NULL */
   int32_t* status;            /* [1] */
   void* scratch;
+  /* Optional device-side count (appended): when non-NULL the step uses
+   * *nmeas_dev measurements and `nmeas` is only the capacity of idx / y.
+   * An empty batch then runs as a zero step (mu = 0) on the device, so the
+   * whole per-frame chain can be captured in a CUDA graph. */
+  const int32_t* nmeas_dev;
 } tt_entries_args;
 size_t tt_entries_scratch_bytes(int nx, int ny, int rank, int nmeas);
 int tt_track_entries(void* stream, const tt_entries_args* a);
+
+/* Acquisition at drawn entries (adaptive_step's truth lookup, sampler.py:204-206)
+ * on the device: omega [cap] flat indices i*ny + j (sorted unique, the first
+ * *count valid), frame [nx][ny] complex64 -> idx_out [cap][2] (i, j) and
+ * y_out [cap] complex64 for the first *count entries. */
+int tt_gather_entries(void* stream, int nx, int ny, const float* frame, const int32_t* omega,
+                      const int32_t* count, int cap, int32_t* idx_out, float* y_out);
 
 /* ------------------------------------------------------------------ standalone step pieces
  * For the reference API functions called on their own, on measurement-domain
@@ -188,6 +200,16 @@ int tt_entry_scores(void* stream, int nx, int ny, int rank, const float* a, cons
 int tt_draw_with_replacement(void* stream, int nslices, int n, const double* probs, int k,
                              const int32_t* forced, int nforced, uint64_t key0, uint64_t key1,
                              uint64_t* pos, int32_t* omega_out, int32_t* count_out);
+/* The same draw over a domain too large for one CTA (entry sampling over
+ * nx*ny): two-level parallel scan in global memory, one binary search per
+ * draw, exact sequential fallback near bucket edges, compaction. One slice;
+ * omega_out [k] sorted unique, *count_out valid; *pos advances by k - nforced.
+ * The flags in scratch must start zeroed (cudaMemset once) and are left
+ * zeroed. scratch: tt_draw_scratch_bytes(n). Graph-capturable. */
+size_t tt_draw_scratch_bytes(int n);
+int tt_draw_with_replacement_large(void* stream, int n, const double* probs, int k, const int32_t* forced,
+                                   int nforced, uint64_t key0, uint64_t key1, uint64_t* pos,
+                                   int32_t* omega_out, int32_t* count_out, void* scratch);
 /* weighted_draw_without_replacement (observation.py:279-297): k sequential
  * renormalised draws, draw order; consumes k uniforms from pos[0]. */
 int tt_draw_without_replacement(void* stream, int n, const double* weights, int k, uint64_t key0,

@@ -456,6 +456,45 @@ def online_run(kspace, A, B, lam, step, policy, clean=None, t0=1, alpha_bar=0.0,
     return out
 
 
+def online_run_entries(kspace, Ah, Bh, lam, step, policy, clean=None, t0=1, alpha_bar=0.0, record_factors=False):
+    """run_adaptive's entries mode (experiment.py:482-530 with sampler.adaptive_step(domain="entries"),
+    sampler.py:190-238) on k-space factors (Ah, Bh) with EntryMask steps (test_mri.py:258-286): per frame
+    [entry_scores of (Ah, Bh) (sampler.py:95-112), k trials with replacement over the nx*ny flat entries
+    i*ny + j, union with the forced ones (sampler.py:146-162)] or a given entry list; y = K_t at those
+    entries; one EntryMask track_step; image = F_x^-1 Ah' diag(gamma) (F_y^-1 Bh')^T with the
+    post-update factors. ``policy``: {"kind": "static", "entries": [...]} or {"kind": "informative",
+    "k": K, "forced": [...], "beta": b, "key": (k0, k1)}."""
+    kspace = np.asarray(kspace)
+    T, n1, n2 = kspace.shape
+    t, pos = t0, int(policy.get("position", 0))
+    out = dict(gamma=[], cost=[], mu=[], entries=[], nmse=[], A=[], B=[], probs=[], recon=[])
+    for f in range(T):
+        if policy["kind"] == "static":
+            om = np.asarray(policy["entries"][f], dtype=np.int64)
+        else:
+            p = entry_probs(Ah, Bh, policy.get("beta", 0.1)).ravel()
+            om, used = draw_rows(p, policy["k"], policy.get("forced"), policy["key"], pos)
+            pos += used
+            out["probs"].append(p)
+        idx = np.stack([om // n2, om % n2], axis=1)
+        y = np.asarray(kspace[f], np.complex128).ravel()[om]
+        rep = track_step(Ah, Bh, t, alpha_bar, y, idx, "entry", lam, step, power=False)
+        Ah, Bh, t, alpha_bar = rep["A"], rep["B"], rep["t"], rep["alpha_bar"]
+        X = synth(fft_cols(Ah, inverse=True), fft_cols(Bh, inverse=True), rep["gamma"])
+        out["gamma"].append(rep["gamma"])
+        out["cost"].append(rep["cost"])
+        out["mu"].append(rep["mu"])
+        out["entries"].append(om)
+        if record_factors:
+            out["A"].append(Ah)
+            out["B"].append(Bh)
+        if clean is not None:
+            out["nmse"].append(nmse(clean[f], X))
+        out["recon"].append(X)
+    out["final"] = (Ah, Bh, t, alpha_bar, pos)
+    return out
+
+
 # ---------------------------------------------------------------------------
 # row-sharded step (SURVEY §8e) — decomposition check, k-space form
 # ---------------------------------------------------------------------------

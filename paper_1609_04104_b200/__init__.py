@@ -9,7 +9,8 @@ anywhere, but every compute call needs a CUDA device and the built library.
 """
 
 from .core import TensorSubspace, rebalance, synthesize_slice
-from .engine import Informative, OnlineEngine, OnlineResult, RowShardedEngine, StaticRows, run_online, warm_up
+from .engine import (EntryEngine, Informative, InformativeEntries, OnlineEngine, OnlineResult, RowShardedEngine,
+                     StaticEntries, StaticRows, run_online, warm_up)
 from .mri import FrameEstimate, interp_track_step, reconstruct_frame
 from .observation import (
     EntryMask,
@@ -60,5 +61,6 @@ __all__ = [
     "expected_count_trace", "expected_sample_count", "row_scores",
     "FrameEstimate", "interp_track_step", "reconstruct_frame",
     "OnlineEngine", "OnlineResult", "StaticRows", "Informative", "run_online", "warm_up", "RowShardedEngine",
+    "EntryEngine", "InformativeEntries", "StaticEntries",
     "NumericalError",
 ]

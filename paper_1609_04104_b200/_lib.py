@@ -57,7 +57,7 @@ class EntriesArgs(C.Structure):
         ("ah_in", _p), ("bh_in", _p), ("ah_out", _p), ("bh_out", _p), ("alpha_bar", _p),
         ("idx", _p), ("y", _p), ("lam", _f64), ("step_mode", _i32), ("mu", _f64), ("c_floor", _f64),
         ("c_cap", _f64), ("gamma_out", _p), ("cost_out", _p), ("mu_out", _p), ("alpha_out", _p),
-        ("resid_out", _p), ("status", _p), ("scratch", _p),
+        ("resid_out", _p), ("status", _p), ("scratch", _p), ("nmeas_dev", _p),
     ]
 
 
@@ -73,6 +73,10 @@ SIGNATURES = {
     "tt_rows_shard_xg_len": (C.c_size_t, [C.c_int]),
     "tt_entries_scratch_bytes": (C.c_size_t, [C.c_int] * 4),
     "tt_track_entries": (C.c_int, [_p, C.POINTER(EntriesArgs)]),
+    "tt_gather_entries": (C.c_int, [_p, C.c_int, C.c_int, _p, _p, _p, C.c_int, _p, _p]),
+    "tt_draw_scratch_bytes": (C.c_size_t, [C.c_int]),
+    "tt_draw_with_replacement_large": (C.c_int, [_p, C.c_int, _p, C.c_int, _p, C.c_int, C.c_uint64, C.c_uint64, _p,
+                                                 _p, _p, _p]),
     "tt_terms_scratch_bytes": (C.c_size_t, [C.c_int, C.c_int, C.c_int]),
     "tt_residual": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, C.c_int, _p, _p, _p, _p, _p, _p]),
     "tt_data_terms": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, C.c_int, _p, _p, _p, _p, _p, _p, _p, _p, _p]),

@@ -144,6 +144,14 @@ def draw_with_replacement(probs: torch.Tensor, k: int, forced: torch.Tensor | No
     omega = torch.empty(ns, k, dtype=torch.int32, device=probs.device)
     cnt = torch.empty(ns, dtype=torch.int32, device=probs.device)
     nf = 0 if forced is None else int(forced.numel())
+    if 24 * n + 512 > 220 * 1024:  # domain beyond one CTA's shared memory (entry sampling): global-memory path
+        scr = torch.zeros(int(L.lib().tt_draw_scratch_bytes(n)), dtype=torch.uint8, device=probs.device)
+        for s in range(ns):
+            L.check(L.lib().tt_draw_with_replacement_large(
+                L.stream_ptr(), n, probs[s].data_ptr(), int(k), None if nf == 0 else forced.data_ptr(), nf,
+                int(key[0]), int(key[1]) + s, pos[s:s + 1].data_ptr(), omega[s].data_ptr(), cnt[s:s + 1].data_ptr(),
+                scr.data_ptr()), "draw_samples")
+        return omega, cnt
     L.check(L.lib().tt_draw_with_replacement(L.stream_ptr(), ns, n, probs.data_ptr(), int(k),
                                              None if nf == 0 else forced.data_ptr(), nf, int(key[0]),
                                              int(key[1]), pos.data_ptr(), omega.data_ptr(), cnt.data_ptr()),

@@ -50,10 +50,12 @@ static EntScratch ent_layout(int nx, int ny, int R) {
   return s;
 }
 
-__global__ void __launch_bounds__(ENT_NT) ent_gram_kernel(int nmeas, int R, const float2* __restrict__ ah,
+__global__ void __launch_bounds__(ENT_NT) ent_gram_kernel(int nmeas, const int* __restrict__ nmeas_dev, int R,
+                                                          const float2* __restrict__ ah,
                                                           const float2* __restrict__ bh, const int* __restrict__ idx,
                                                           const float2* __restrict__ y, double2* __restrict__ gp,
                                                           double2* __restrict__ hp, double* __restrict__ yp) {
+  if (nmeas_dev) nmeas = min(*nmeas_dev, nmeas);
   extern __shared__ __align__(16) unsigned char smem[];
   double2* phi = (double2*)smem;                   // [TL][R]
   double2* yv = phi + ENT_TL * R;                  // [TL]
@@ -106,13 +108,15 @@ __global__ void __launch_bounds__(ENT_NT) ent_gram_kernel(int nmeas, int R, cons
   if (tid == 0) yp[b] = ys;
 }
 
-__global__ void __launch_bounds__(ENT_NT) ent_solve_kernel(int nx, int ny, int R, int nmeas, int nb, double lam,
+__global__ void __launch_bounds__(ENT_NT) ent_solve_kernel(int nx, int ny, int R, int nmeas,
+                                                           const int* __restrict__ nmeas_dev, int nb, double lam,
                                                            long long t, const float2* __restrict__ ah,
                                                            const float2* __restrict__ bh, const double2* gp,
                                                            const double2* hp, const double* yp, double2* gam_out,
                                                            double* scal, float2* gamma_out, double* cost_out,
                                                            int32_t* status) {
   extern __shared__ __align__(16) unsigned char smem[];
+  if (nmeas_dev) nmeas = min(*nmeas_dev, nmeas);
   const int Rp = R * (R + 1) / 2;
   double2* G = (double2*)smem;
   double2* hv = G + Rp;
@@ -146,7 +150,13 @@ __global__ void __launch_bounds__(ENT_NT) ent_solve_kernel(int nx, int ny, int R
     int r, q;
     tri_decode(e, r, q);
     double2 g = make_double2(0.0, 0.0);
-    for (int b = 0; b < nb; ++b) g = zadd(g, gp[(size_t)b * Rp + e]);
+    int b = 0;
+    for (; b + 4 <= nb; b += 4) {  // four loads in flight, fixed association order
+      const double2 v0 = gp[(size_t)b * Rp + e], v1 = gp[(size_t)(b + 1) * Rp + e];
+      const double2 v2 = gp[(size_t)(b + 2) * Rp + e], v3 = gp[(size_t)(b + 3) * Rp + e];
+      g = zadd(g, zadd(zadd(v0, v1), zadd(v2, v3)));
+    }
+    for (; b < nb; ++b) g = zadd(g, gp[(size_t)b * Rp + e]);
     if (r == q) g.x += lam;
     G[e] = g;
   }
@@ -157,7 +167,16 @@ __global__ void __launch_bounds__(ENT_NT) ent_solve_kernel(int nx, int ny, int R
     hv[tid] = h;
   }
   for (int b = 0; b < nb; ++b) yn += yp[b];
-  block_ldl_solve(G, hv, gam, R);
+  __syncthreads();
+  {
+    double2* colb = (double2*)(red + 64);  // 4 (R+1) double2 after the reduction buffer
+    const int ept = gj_ept(R, blockDim.x);
+    if (ept <= 1) block_gj_solve<1>(G, hv, gam, colb, R);
+    else if (ept <= 2) block_gj_solve<2>(G, hv, gam, colb, R);
+    else if (ept <= 3) block_gj_solve<3>(G, hv, gam, colb, R);
+    else if (ept <= 5) block_gj_solve<5>(G, hv, gam, colb, R);
+    else block_ldl_solve(G, hv, gam, R);
+  }
   // reload h (eliminated in place) for the cost
   if (tid < R) {
     double2 h = make_double2(0.0, 0.0);
@@ -180,9 +199,11 @@ __global__ void __launch_bounds__(ENT_NT) ent_solve_kernel(int nx, int ny, int R
   }
 }
 
-__global__ void ent_resid_kernel(int nmeas, int ny, int R, const float2* __restrict__ ah, const float2* __restrict__ bh,
+__global__ void ent_resid_kernel(int nmeas, const int* __restrict__ nmeas_dev, int ny, int R,
+                                 const float2* __restrict__ ah, const float2* __restrict__ bh,
                                  const int* __restrict__ idx, const float2* __restrict__ y, const double2* gam,
                                  float2* __restrict__ xi, float* __restrict__ mk, float2* __restrict__ resid) {
+  if (nmeas_dev) nmeas = min(*nmeas_dev, nmeas);
   for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nmeas; l += gridDim.x * blockDim.x) {
     const int i = idx[2 * l], j = idx[2 * l + 1];
     double2 s = make_double2(0.0, 0.0);
@@ -197,44 +218,68 @@ __global__ void ent_resid_kernel(int nmeas, int ny, int R, const float2* __restr
   }
 }
 
-// role 0: rows i of P and c0 ; role 1: rows j of Q and c1
-__global__ void ent_backproj_kernel(int nx, int ny, int R, const float2* __restrict__ ah, const float2* __restrict__ bh,
-                                    const float2* __restrict__ xi, const float* __restrict__ mk, float2* __restrict__ P,
-                                    float2* __restrict__ Q, float* __restrict__ c0, float* __restrict__ c1) {
-  const int o = blockIdx.x * blockDim.x + threadIdx.x;
-  if (blockIdx.y == 0) {
-    if (o >= nx * R) return;
-    const int i = o / R, r = o - i * R;
-    float2 acc = make_float2(0.f, 0.f);
-    float cs = 0.f;
-    for (int j = 0; j < ny; ++j) {
-      const float2 b = bh[(size_t)j * R + r];
-      acc = cfma_conj(xi[(size_t)i * ny + j], b, acc);
-      cs = fmaf(mk[(size_t)i * ny + j], cabs2(b), cs);
+// role 0 (blockIdx.y = 0): rows i of P and c0; role 1: rows j of Q and c1. Block = 32 outputs x 8 parts
+// of the contraction index; the 8 parts are summed in fixed order through shared memory.
+#define BP_O 32
+#define BP_K 8
+__global__ void __launch_bounds__(BP_O * BP_K) ent_backproj_kernel(int nx, int ny, int R,
+                                                                   const float2* __restrict__ ah,
+                                                                   const float2* __restrict__ bh,
+                                                                   const float2* __restrict__ xi,
+                                                                   const float* __restrict__ mk,
+                                                                   float2* __restrict__ P, float2* __restrict__ Q,
+                                                                   float* __restrict__ c0, float* __restrict__ c1) {
+  __shared__ float2 sacc[BP_K][BP_O];
+  __shared__ float scs[BP_K][BP_O];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int o = blockIdx.x * BP_O + tx;
+  const bool rows = blockIdx.y == 0;
+  const int m = rows ? nx * R : ny * R;
+  float2 acc = make_float2(0.f, 0.f);
+  float cs = 0.f;
+  if (o < m) {
+    if (rows) {
+      const int i = o / R, r = o - i * R;
+      for (int j = ty; j < ny; j += BP_K) {
+        const float2 b = bh[(size_t)j * R + r];
+        acc = cfma_conj(xi[(size_t)i * ny + j], b, acc);
+        cs = fmaf(mk[(size_t)i * ny + j], cabs2(b), cs);
+      }
+    } else {
+      const int j = o / R, r = o - j * R;
+      for (int i = ty; i < nx; i += BP_K) {
+        const float2 a = ah[(size_t)i * R + r];
+        acc = cfma_conj(xi[(size_t)i * ny + j], a, acc);
+        cs = fmaf(mk[(size_t)i * ny + j], cabs2(a), cs);
+      }
     }
-    P[o] = acc;
-    c0[o] = cs;
-  } else {
-    if (o >= ny * R) return;
-    const int j = o / R, r = o - j * R;
-    float2 acc = make_float2(0.f, 0.f);
-    float cs = 0.f;
-    for (int i = 0; i < nx; ++i) {
-      const float2 a = ah[(size_t)i * R + r];
-      acc = cfma_conj(xi[(size_t)i * ny + j], a, acc);
-      cs = fmaf(mk[(size_t)i * ny + j], cabs2(a), cs);
+  }
+  sacc[ty][tx] = acc;
+  scs[ty][tx] = cs;
+  __syncthreads();
+  if (ty == 0 && o < m) {
+    for (int k = 1; k < BP_K; ++k) {
+      acc = cadd(acc, sacc[k][tx]);
+      cs += scs[k][tx];
     }
-    Q[o] = acc;
-    c1[o] = cs;
+    if (rows) {
+      P[o] = acc;
+      c0[o] = cs;
+    } else {
+      Q[o] = acc;
+      c1[o] = cs;
+    }
   }
 }
 
-__global__ void __launch_bounds__(ENT_NT) ent_step_kernel(int nx, int ny, int R, int nmeas, double lam, long long t,
+__global__ void __launch_bounds__(ENT_NT) ent_step_kernel(int nx, int ny, int R, int nmeas,
+                                                          const int* __restrict__ nmeas_dev, double lam, long long t,
                                                           int step_mode, double mu, double c_floor, double c_cap,
                                                           const double2* gam, const float* c0, const float* c1,
                                                           double* alpha_bar, double* scal, double* mu_out,
                                                           double* alpha_out) {
   __shared__ double red[64];
+  if (nmeas_dev) nmeas = min(*nmeas_dev, nmeas);
   const int tid = threadIdx.x, NT = blockDim.x;
   double top = 0.0;
   for (int o = tid; o < nx * R; o += NT) {
@@ -299,6 +344,7 @@ extern "C" size_t tt_entries_scratch_bytes(int nx, int ny, int rank, int nmeas) 
 extern "C" int tt_track_entries(void* stream, const tt_entries_args* a) {
   if (!a) return tt_fail(TT_EINVAL, "null args");
   const int nx = a->nx, ny = a->ny, R = a->rank, L = a->nmeas;
+  const int* Ld = a->nmeas_dev;  // device count (capacity L), graph-capturable chain
   if (nx < 1 || ny < 1 || R < 1 || L < 0) return tt_fail(TT_EINVAL, "tt_track_entries: bad shape");
   if (R > 64) return tt_fail(TT_EUNSUPPORTED, "rank > 64 is not supported");
   if (a->t < 1) return tt_fail(TT_EINVAL, "t must be >= 1");
@@ -328,18 +374,26 @@ extern "C" int tt_track_entries(void* stream, const tt_entries_args* a) {
     nb = (L + 255) / 256;
     if (nb > ENT_NB) nb = ENT_NB;
     const size_t sm = sizeof(double2) * (ENT_TL * (size_t)R + ENT_TL) + sizeof(double) * 64;
-    TT_CUDA_TRY(cudaFuncSetAttribute(ent_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    ent_gram_kernel<<<nb, ENT_NT, sm, st>>>(L, R, ah, bh, a->idx, (const float2*)a->y, gp, hp, yp);
+    static int set_gram = -1;
+    if (set_gram < (int)sm) {
+      TT_CUDA_TRY(cudaFuncSetAttribute(ent_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      set_gram = (int)sm;
+    }
+    ent_gram_kernel<<<nb, ENT_NT, sm, st>>>(L, Ld, R, ah, bh, a->idx, (const float2*)a->y, gp, hp, yp);
   }
   {
-    const size_t sm = sizeof(double2) * (Rp + 2 * (size_t)R) + sizeof(double) * 64;
-    TT_CUDA_TRY(cudaFuncSetAttribute(ent_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    ent_solve_kernel<<<1, ENT_NT, sm, st>>>(nx, ny, R, L, nb, a->lam, (long long)a->t, ah, bh, gp, hp, yp, gam, scal,
+    const size_t sm = sizeof(double2) * (Rp + 2 * (size_t)R) + sizeof(double) * 64 + sizeof(double2) * 4 * (R + 1);
+    static int set_solve = -1;
+    if (set_solve < (int)sm) {
+      TT_CUDA_TRY(cudaFuncSetAttribute(ent_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      set_solve = (int)sm;
+    }
+    ent_solve_kernel<<<1, ENT_NT, sm, st>>>(nx, ny, R, L, Ld, nb, a->lam, (long long)a->t, ah, bh, gp, hp, yp, gam, scal,
                                             (float2*)a->gamma_out, a->cost_out, a->status);
   }
   if (L == 0) {
     // empty batch: no update (tracker.py:380-384)
-    ent_step_kernel<<<1, ENT_NT, 0, st>>>(0, 0, R, 0, a->lam, (long long)a->t, a->step_mode, a->mu, a->c_floor,
+    ent_step_kernel<<<1, ENT_NT, 0, st>>>(0, 0, R, 0, nullptr, a->lam, (long long)a->t, a->step_mode, a->mu, a->c_floor,
                                           a->c_cap, gam, c0, c1, a->alpha_bar, scal, a->mu_out, a->alpha_out);
     if (a->ah_out != a->ah_in)
       TT_CUDA_TRY(cudaMemcpyAsync(a->ah_out, a->ah_in, sizeof(float2) * (size_t)nx * R, cudaMemcpyDeviceToDevice, st));
@@ -353,15 +407,15 @@ extern "C" int tt_track_entries(void* stream, const tt_entries_args* a) {
   {
     int blocks = (L + 255) / 256;
     if (blocks > 1184) blocks = 1184;
-    ent_resid_kernel<<<blocks, 256, 0, st>>>(L, ny, R, ah, bh, a->idx, (const float2*)a->y, gam, xi, mk,
+    ent_resid_kernel<<<blocks, 256, 0, st>>>(L, Ld, ny, R, ah, bh, a->idx, (const float2*)a->y, gam, xi, mk,
                                              (float2*)a->resid_out);
   }
   {
     const int m = (nx > ny ? nx : ny) * R;
-    dim3 grid((m + 127) / 128, 2);
-    ent_backproj_kernel<<<grid, 128, 0, st>>>(nx, ny, R, ah, bh, xi, mk, P, Q, c0, c1);
+    dim3 grid((m + BP_O - 1) / BP_O, 2);
+    ent_backproj_kernel<<<grid, dim3(BP_O, BP_K), 0, st>>>(nx, ny, R, ah, bh, xi, mk, P, Q, c0, c1);
   }
-  ent_step_kernel<<<1, ENT_NT, 0, st>>>(nx, ny, R, L, a->lam, (long long)a->t, a->step_mode, a->mu, a->c_floor,
+  ent_step_kernel<<<1, ENT_NT, 0, st>>>(nx, ny, R, L, Ld, a->lam, (long long)a->t, a->step_mode, a->mu, a->c_floor,
                                         a->c_cap, gam, c0, c1, a->alpha_bar, scal, a->mu_out, a->alpha_out);
   {
     const int n = (nx + ny) * R;
@@ -370,6 +424,32 @@ extern "C" int tt_track_entries(void* stream, const tt_entries_args* a) {
     ent_update_kernel<<<blocks, 256, 0, st>>>(nx, ny, R, a->lam, (long long)a->t, scal, gam, ah, bh, P, Q,
                                               (float2*)a->ah_out, (float2*)a->bh_out);
   }
+  TT_CUDA_TRY(cudaGetLastError());
+  return TT_OK;
+}
+
+// Acquisition at drawn entries (sampler.py:204-206 truth lookup): flat index -> (i, j), y = frame[i][j].
+__global__ void ent_gather_kernel(int ny, const float2* __restrict__ frame, const int* __restrict__ omega,
+                                  const int* __restrict__ count, int cap, int* __restrict__ idx, float2* __restrict__ y) {
+  const int n = min(*count, cap);
+  for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < n; m += gridDim.x * blockDim.x) {
+    const int w = omega[m];
+    const int i = w / ny;
+    idx[2 * m] = i;
+    idx[2 * m + 1] = w - i * ny;
+    y[m] = frame[w];
+  }
+}
+
+extern "C" int tt_gather_entries(void* stream, int nx, int ny, const float* frame, const int32_t* omega,
+                                 const int32_t* count, int cap, int32_t* idx_out, float* y_out) {
+  if (nx < 1 || ny < 1 || cap < 0) return tt_fail(TT_EINVAL, "tt_gather_entries: bad shape");
+  if (cap == 0) return TT_OK;
+  if (!frame || !omega || !count || !idx_out || !y_out) return tt_fail(TT_EINVAL, "tt_gather_entries: null buffer");
+  int blocks = (cap + 255) / 256;
+  if (blocks > 1184) blocks = 1184;
+  ent_gather_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(ny, (const float2*)frame, omega, count, cap, idx_out,
+                                                             (float2*)y_out);
   TT_CUDA_TRY(cudaGetLastError());
   return TT_OK;
 }

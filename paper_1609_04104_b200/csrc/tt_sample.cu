@@ -94,16 +94,37 @@ __global__ void __launch_bounds__(SMP_NT) entry_energy_kernel(int nx, int ny, in
   }
 }
 
-__global__ void entry_map_kernel(int nx, int ny, int R, const double* __restrict__ ws, double beta,
-                                 double* __restrict__ probs) {
+// blended probabilities (sampler.py:88-92) and their per-block partial sums (fixed order)
+__global__ void __launch_bounds__(SMP_NT) entry_map_kernel(int nx, int ny, int R, const double* __restrict__ ws,
+                                                           double beta, double* __restrict__ probs,
+                                                           double* __restrict__ part) {
+  __shared__ double red[64];
   const size_t n = (size_t)nx * ny;
   const double den = (double)R * (double)(nx + ny);
   const double tot = ws[nx + ny];
+  double loc = 0.0;
   for (size_t o = blockIdx.x * (size_t)blockDim.x + threadIdx.x; o < n; o += (size_t)gridDim.x * blockDim.x) {
     const size_t i = o / ny, j = o - i * ny;
     const double raw = (ws[i] + ws[nx + j]) / den;
-    probs[o] = (1.0 - beta) * (raw / tot) + beta / (double)n;
+    const double v = (1.0 - beta) * (raw / tot) + beta / (double)n;
+    probs[o] = v;
+    loc += v;
   }
+  const double s = block_sum(loc, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+// final renormalisation: every block sums the partials in the same order, then divides its share
+__global__ void __launch_bounds__(SMP_NT) entry_norm_kernel(size_t n, int nparts, const double* __restrict__ part,
+                                                            double* __restrict__ probs) {
+  __shared__ double red[64];
+  __shared__ double tot;
+  double loc = 0.0;
+  for (int b = threadIdx.x; b < nparts; b += blockDim.x) loc += part[b];
+  const double s = block_sum(loc, red);
+  if (threadIdx.x == 0) tot = s;
+  __syncthreads();
+  for (size_t o = blockIdx.x * (size_t)blockDim.x + threadIdx.x; o < n; o += (size_t)gridDim.x * blockDim.x)
+    probs[o] = probs[o] / tot;
 }
 __global__ void __launch_bounds__(SMP_NT) normalize_kernel(size_t n, double* __restrict__ probs) {
   __shared__ double red[64];
@@ -211,15 +232,15 @@ extern "C" int tt_entry_scores(void* stream, int nx, int ny, int rank, const flo
   if (!(beta >= 0.0 && beta < 1.0)) return tt_fail(TT_EINVAL, "uniform blend weight must be in [0, 1)");
   // probs_out doubles as workspace for the energies only if large enough; use a temporary
   double* ws = nullptr;
-  TT_CUDA_TRY(cudaMallocAsync((void**)&ws, sizeof(double) * (nx + ny + 1), (cudaStream_t)stream));
+  TT_CUDA_TRY(cudaMallocAsync((void**)&ws, sizeof(double) * (nx + ny + 1 + 4096), (cudaStream_t)stream));
   const size_t sm = sizeof(double) * ((size_t)rank + 64);
   entry_energy_kernel<<<1, SMP_NT, sm, (cudaStream_t)stream>>>(nx, ny, rank, (const float2*)a, (const float2*)b, ws,
                                                                 status);
   const size_t n = (size_t)nx * ny;
   int blocks = (int)((n + SMP_NT - 1) / SMP_NT);
   if (blocks > 4096) blocks = 4096;
-  entry_map_kernel<<<blocks, SMP_NT, 0, (cudaStream_t)stream>>>(nx, ny, rank, ws, beta, probs_out);
-  normalize_kernel<<<1, SMP_NT, 0, (cudaStream_t)stream>>>(n, probs_out);
+  entry_map_kernel<<<blocks, SMP_NT, 0, (cudaStream_t)stream>>>(nx, ny, rank, ws, beta, probs_out, ws + nx + ny + 1);
+  entry_norm_kernel<<<blocks, SMP_NT, 0, (cudaStream_t)stream>>>(n, blocks, ws + nx + ny + 1, probs_out);
   TT_CUDA_TRY(cudaFreeAsync(ws, (cudaStream_t)stream));
   TT_CUDA_TRY(cudaGetLastError());
   return TT_OK;
@@ -250,6 +271,244 @@ extern "C" int tt_draw_without_replacement(void* stream, int n, const double* we
   if (sm > 220 * 1024) return tt_fail(TT_EUNSUPPORTED, "draw domain too large for one CTA (n=%d)", n);
   TT_CUDA_TRY(cudaFuncSetAttribute(draw_wor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   draw_wor_kernel<<<1, SMP_NT, sm, (cudaStream_t)stream>>>(n, weights, k, key0, key1, pos, out, status);
+  TT_CUDA_TRY(cudaGetLastError());
+  return TT_OK;
+}
+
+// ---------------------------------------------------------------- draws over large domains (global memory)
+// draw_samples(replacement=True) when the domain does not fit one CTA's shared
+// memory (entry sampling over nx*ny, sampler.py:95-112 + :146-162). Same
+// numpy semantics as draw_wr_kernel: cdf = cumsum(p) / cdf[-1],
+// idx = searchsorted(cdf, u, 'right'), union with the forced indices. The
+// cumsum is a two-level parallel scan; a uniform closer to a bucket edge than
+// the scan's rounding bound triggers numpy's sequential cumsum and a redo, so
+// the result equals numpy's for the same probabilities. Every step is a
+// kernel with device-side control (graph-capturable).
+#define BIG_IPT 8  // entries per thread in the block scan
+struct BigDrawScratch {
+  size_t cdf, part, off, flags, ctl, cpart, coff, total;
+};
+static BigDrawScratch big_layout(int n) {
+  BigDrawScratch s;
+  const int nb = (n + SMP_NT * BIG_IPT - 1) / (SMP_NT * BIG_IPT);
+  size_t o = 0;
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  s.cdf = o;   o = al(o + sizeof(double) * (size_t)n);
+  s.part = o;  o = al(o + sizeof(double) * (size_t)nb);
+  s.off = o;   o = al(o + sizeof(double) * ((size_t)nb + 1));
+  s.flags = o; o = al(o + sizeof(int) * (size_t)n);
+  s.ctl = o;   o = al(o + sizeof(int) * 4);  // [0] ambiguity flag
+  s.cpart = o; o = al(o + sizeof(int) * (size_t)nb);
+  s.coff = o;  o = al(o + sizeof(int) * ((size_t)nb + 1));
+  s.total = o;
+  return s;
+}
+
+// level 1: block-local inclusive scan (thread-sequential chunks, fixed order) and block totals
+__global__ void __launch_bounds__(SMP_NT) big_scan_kernel(int n, const double* __restrict__ p, double* __restrict__ cdf,
+                                                          double* __restrict__ part) {
+  __shared__ double red[64];
+  const int tid = threadIdx.x;
+  const int base = blockIdx.x * SMP_NT * BIG_IPT + tid * BIG_IPT;
+  double v[BIG_IPT];
+  double loc = 0.0;
+#pragma unroll
+  for (int q = 0; q < BIG_IPT; ++q) {
+    v[q] = base + q < n ? p[base + q] : 0.0;
+    loc += v[q];
+  }
+  double tot;
+  double run = block_excl_scan_dbl(loc, red, tot);
+#pragma unroll
+  for (int q = 0; q < BIG_IPT; ++q) {
+    run += v[q];
+    if (base + q < n) cdf[base + q] = run;
+  }
+  if (tid == 0) part[blockIdx.x] = tot;
+}
+
+// level 2: exclusive offsets of the block totals (one block, fixed order); off[nb] = grand total
+__global__ void __launch_bounds__(SMP_NT) big_offsets_kernel(int nb, const double* __restrict__ part,
+                                                             double* __restrict__ off, int* __restrict__ ctl) {
+  __shared__ double red[64];
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int chunk = (nb + NT - 1) / NT;
+  const int c0 = min(nb, tid * chunk), c1 = min(nb, c0 + chunk);
+  double loc = 0.0;
+  for (int b = c0; b < c1; ++b) loc += part[b];
+  double tot;
+  double run = block_excl_scan_dbl(loc, red, tot);
+  for (int b = c0; b < c1; ++b) {
+    off[b] = run;
+    run += part[b];
+  }
+  if (tid == 0) {
+    off[nb] = tot;
+    ctl[0] = 0;
+  }
+}
+
+TT_DEV double big_cdf(const double* cdf, const double* off, int i) {
+  return cdf[i] + off[i / (SMP_NT * BIG_IPT)];
+}
+
+// draws: one uniform per thread, binary search on the (unnormalised) global CDF against u * total
+__global__ void big_draw_kernel(int n, int ndraw, const double* __restrict__ cdf, const double* __restrict__ off,
+                                int nb, const int* __restrict__ forced, int nforced, uint64_t k0, uint64_t k1,
+                                const uint64_t* __restrict__ pos, int* __restrict__ flags, int* __restrict__ ctl,
+                                double guard) {
+  const double total = off[nb];
+  const uint64_t p0 = pos[0];
+  int top = 1;
+  while (2 * top <= n) top *= 2;
+  for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < ndraw + nforced; m += gridDim.x * blockDim.x) {
+    if (m >= ndraw) {
+      const int f = forced[m - ndraw];
+      if (f >= 0 && f < n) flags[f] = 1;
+      continue;
+    }
+    const double u = philox_uniform(k0, k1, p0 + (uint64_t)m);
+    const double ut = u * total;
+    int q = -1;  // last index with cdf <= u (normalised)
+    for (int step = top; step > 0; step >>= 1) {
+      const int cand = q + step;
+      if (cand < n && big_cdf(cdf, off, cand) <= ut) q = cand;
+    }
+    const int idx = min(q + 1, n - 1);
+    const double lo = idx > 0 ? big_cdf(cdf, off, idx - 1) / total : -1.0;
+    const double hi = idx < n - 1 ? big_cdf(cdf, off, idx) / total : 2.0;
+    if (u - lo <= guard || hi - u <= guard) ctl[0] = 1;
+    flags[idx] = 1;
+  }
+}
+
+// exact fallback (runs only when a draw was ambiguous): numpy's sequential cumsum, cdf /= cdf[-1], redo
+__global__ void big_exact_kernel(int n, int ndraw, const double* __restrict__ p, double* __restrict__ cdf,
+                                 const int* __restrict__ forced, int nforced, uint64_t k0, uint64_t k1,
+                                 const uint64_t* __restrict__ pos, int* __restrict__ flags, const int* __restrict__ ctl) {
+  if (ctl[0] == 0) return;
+  const int tid = threadIdx.x, NT = blockDim.x;
+  if (tid == 0) {
+    double c = 0.0;
+    for (int i = 0; i < n; ++i) {
+      c += p[i];
+      cdf[i] = c;
+    }
+  }
+  __syncthreads();
+  const double last = cdf[n - 1];
+  __syncthreads();
+  for (int i = tid; i < n; i += NT) {
+    cdf[i] = cdf[i] / last;
+    flags[i] = 0;
+  }
+  __syncthreads();
+  for (int m = tid; m < ndraw; m += NT) {
+    const int idx = upper_bound_d(cdf, n, philox_uniform(k0, k1, pos[0] + (uint64_t)m));
+    flags[idx < n ? idx : n - 1] = 1;
+  }
+  for (int m = tid; m < nforced; m += NT) {
+    const int f = forced[m];
+    if (f >= 0 && f < n) flags[f] = 1;
+  }
+}
+
+// flags -> sorted unique indices + count, in three block-parallel passes (per-block counts, one-block
+// scan of the counts, writes); the writes clear the flags; the stream position advances by the draws
+__global__ void __launch_bounds__(SMP_NT) big_count_kernel(int n, const int* __restrict__ flags,
+                                                           int* __restrict__ cpart) {
+  __shared__ int red[64];
+  const int base = blockIdx.x * SMP_NT * BIG_IPT + threadIdx.x * BIG_IPT;
+  int c = 0;
+#pragma unroll
+  for (int q = 0; q < BIG_IPT; ++q) c += (base + q < n && flags[base + q]) ? 1 : 0;
+  int tot;
+  block_excl_scan_int(c, red, tot);
+  if (threadIdx.x == 0) cpart[blockIdx.x] = tot;
+}
+__global__ void __launch_bounds__(SMP_NT) big_count_offsets_kernel(int nb, const int* __restrict__ cpart,
+                                                                   int* __restrict__ coff) {
+  __shared__ int red[64];
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int chunk = (nb + NT - 1) / NT;
+  const int c0 = min(nb, tid * chunk), c1 = min(nb, c0 + chunk);
+  int loc = 0;
+  for (int b = c0; b < c1; ++b) loc += cpart[b];
+  int tot;
+  int run = block_excl_scan_int(loc, red, tot);
+  for (int b = c0; b < c1; ++b) {
+    coff[b] = run;
+    run += cpart[b];
+  }
+  if (tid == 0) coff[nb] = tot;
+}
+__global__ void __launch_bounds__(SMP_NT) big_write_kernel(int n, int nb, int ndraw, int cap, int* __restrict__ flags,
+                                                           const int* __restrict__ coff, uint64_t* __restrict__ pos,
+                                                           int* __restrict__ omega, int* __restrict__ count) {
+  __shared__ int red[64];
+  const int base = blockIdx.x * SMP_NT * BIG_IPT + threadIdx.x * BIG_IPT;
+  int f[BIG_IPT];
+  int c = 0;
+#pragma unroll
+  for (int q = 0; q < BIG_IPT; ++q) {
+    f[q] = (base + q < n) ? flags[base + q] : 0;
+    c += f[q] ? 1 : 0;
+  }
+  int tot;
+  int o = coff[blockIdx.x] + block_excl_scan_int(c, red, tot);
+#pragma unroll
+  for (int q = 0; q < BIG_IPT; ++q)
+    if (f[q]) {
+      if (o < cap) omega[o] = base + q;
+      ++o;
+      flags[base + q] = 0;
+    }
+  const int all = coff[nb];
+  if (blockIdx.x == 0) {
+    for (int i = all + threadIdx.x; i < cap; i += blockDim.x) omega[i] = -1;  // deterministic padding
+    if (threadIdx.x == 0) {
+      *count = min(all, cap);
+      pos[0] += (uint64_t)ndraw;
+    }
+  }
+}
+
+extern "C" size_t tt_draw_scratch_bytes(int n) { return n > 0 ? big_layout(n).total : 0; }
+
+extern "C" int tt_draw_with_replacement_large(void* stream, int n, const double* probs, int k, const int32_t* forced,
+                                              int nforced, uint64_t key0, uint64_t key1, uint64_t* pos,
+                                              int32_t* omega_out, int32_t* count_out, void* scratch) {
+  if (n < 1 || k < 1 || !probs || !omega_out || !count_out || !pos || !scratch)
+    return tt_fail(TT_EINVAL, "tt_draw_with_replacement_large: bad args");
+  if (nforced < 0 || nforced > k) return tt_fail(TT_EINVAL, "more forced indices than trials");
+  if (nforced > 0 && !forced) return tt_fail(TT_EINVAL, "null forced list");
+  cudaStream_t st = (cudaStream_t)stream;
+  const BigDrawScratch S = big_layout(n);
+  unsigned char* sb = (unsigned char*)scratch;
+  double* cdf = (double*)(sb + S.cdf);
+  double* part = (double*)(sb + S.part);
+  double* off = (double*)(sb + S.off);
+  int* flags = (int*)(sb + S.flags);
+  int* ctl = (int*)(sb + S.ctl);
+  const int nb = (n + SMP_NT * BIG_IPT - 1) / (SMP_NT * BIG_IPT);
+  const int ndraw = k - nforced;
+  // rounding bound of the parallel scan against numpy's sequential cumsum (relative to the total)
+  const double guard = 1e-12 * (1.0 + (double)n / 4096.0);
+  big_scan_kernel<<<nb, SMP_NT, 0, st>>>(n, probs, cdf, part);
+  big_offsets_kernel<<<1, SMP_NT, 0, st>>>(nb, part, off, ctl);
+  {
+    int blocks = (ndraw + nforced + 255) / 256;
+    if (blocks < 1) blocks = 1;
+    if (blocks > 1184) blocks = 1184;
+    big_draw_kernel<<<blocks, 256, 0, st>>>(n, ndraw, cdf, off, nb, forced, nforced, key0, key1, pos, flags, ctl,
+                                            guard);
+  }
+  big_exact_kernel<<<1, SMP_NT, 0, st>>>(n, ndraw, probs, cdf, forced, nforced, key0, key1, pos, flags, ctl);
+  int* cpart = (int*)(sb + S.cpart);
+  int* coff = (int*)(sb + S.coff);
+  big_count_kernel<<<nb, SMP_NT, 0, st>>>(n, flags, cpart);
+  big_count_offsets_kernel<<<1, SMP_NT, 0, st>>>(nb, cpart, coff);
+  big_write_kernel<<<nb, SMP_NT, 0, st>>>(n, nb, ndraw, k, flags, coff, pos, omega_out, count_out);
   TT_CUDA_TRY(cudaGetLastError());
   return TT_OK;
 }

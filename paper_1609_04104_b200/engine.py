@@ -32,7 +32,8 @@ from . import _lib as L
 from . import _ops as K
 from .tracker import Fixed, HessianBound
 
-__all__ = ["StaticRows", "Informative", "OnlineEngine", "run_online", "OnlineResult", "warm_up", "RowShardedEngine"]
+__all__ = ["StaticRows", "Informative", "OnlineEngine", "run_online", "OnlineResult", "warm_up", "RowShardedEngine",
+           "InformativeEntries", "StaticEntries", "EntryEngine"]
 
 
 @dataclass(frozen=True)
@@ -241,6 +242,183 @@ def warm_up(engine: "OnlineEngine", kspace_warm: torch.Tensor, epochs: int) -> N
     engine.ah, engine.bh, engine.alpha_bar, engine.t = weng.ah, weng.bh, weng.alpha_bar, weng.t
 
 
+@dataclass(frozen=True)
+class InformativeEntries:
+    """adaptive_step(domain="entries") per frame (sampler.py:190-238; experiment.run_adaptive's
+    entries mode): entry_scores of the k-space factors (sampler.py:95-112), ``k`` trials with
+    replacement over the nx*ny entries (flat index i*ny + j) including the forced ones, EntryMask step."""
+    k: int
+    forced: tuple = ()
+    beta: float = 0.1
+    key0: int = 0
+    key1: int = 0
+
+
+@dataclass(frozen=True)
+class StaticEntries:
+    """Fixed entry lists per frame: ``entries`` (T, Smax) flat indices i*ny + j (-1 padded, any order
+    without duplicates), ``counts`` (T,)."""
+    entries: np.ndarray
+    counts: np.ndarray
+
+
+class EntryEngine:
+    """Device-resident online loop for entry masks on k-space factors (the EntryMask /
+    k-space interpolation path; EntryMask on (F_x A, F_y B) is the FourierMask iteration,
+    test_mri.py:258-286). Per frame, on the device: [entry scores -> large-domain Philox draw] or the
+    static list -> y gathered at the entries from the resident truth -> the generic index-list step
+    (tt_track_entries with a device-side count) -> per-frame outputs and factor history. The T-frame
+    chain is captured once in a CUDA graph and replayed (no host round trip per frame). One slice."""
+
+    def __init__(self, nx, ny, rank, lam=0.1, step=Fixed(0.01), policy=None, t0=1):
+        self.nx, self.ny, self.rank = int(nx), int(ny), int(rank)
+        self.lam, self.step, self.policy = float(lam), step, policy
+        self.dev = L.device()
+        n = self.nx * self.ny
+        i32 = dict(dtype=torch.int32, device=self.dev)
+        if isinstance(policy, InformativeEntries):
+            if not 1 <= policy.k <= n:
+                raise ValueError("informative k must be in [1, nx*ny]")
+            forced = np.unique(np.asarray(policy.forced, dtype=np.int64))
+            if forced.size and (forced.min() < 0 or forced.max() >= n):
+                raise ValueError("forced index out of range")
+            if forced.size > policy.k:
+                raise ValueError("more forced indices than trials")
+            self.cap = int(policy.k)
+            self.forced = torch.from_numpy(forced.astype(np.int32)).to(self.dev)
+            self.probs = torch.empty(n, dtype=torch.float64, device=self.dev)
+            self.dscr = torch.zeros(int(L.lib().tt_draw_scratch_bytes(n)), dtype=torch.uint8, device=self.dev)
+            self.omega = torch.empty(self.cap, **i32)
+            self.count = torch.zeros(1, **i32)
+        elif isinstance(policy, StaticEntries):
+            ent = np.asarray(policy.entries)
+            cnt = np.asarray(policy.counts).reshape(-1)
+            if ent.ndim != 2 or cnt.shape[0] != ent.shape[0]:
+                raise ValueError("static entries must be (T, Smax) with counts (T,)")
+            for f in range(ent.shape[0]):
+                e = ent[f, :cnt[f]]
+                if cnt[f] < 0 or cnt[f] > ent.shape[1] or (e.size and (e.min() < 0 or e.max() >= n)):
+                    raise ValueError(f"frame {f}: entry index out of range")
+                if np.unique(e).size != e.size:
+                    raise ValueError(f"frame {f}: duplicate entries")  # observation.py:41-55
+            self.cap = int(max(1, ent.shape[1]))
+            self.tab = torch.from_numpy(np.ascontiguousarray(ent, dtype=np.int32)).to(self.dev)
+            self.tab_cnt = torch.from_numpy(np.ascontiguousarray(cnt, dtype=np.int32)).to(self.dev)
+        else:
+            raise TypeError("policy must be InformativeEntries or StaticEntries")
+        self.idx = torch.zeros(self.cap, 2, **i32)
+        self.y = torch.zeros(self.cap, dtype=torch.complex64, device=self.dev)
+        self.scr = torch.empty(int(L.lib().tt_entries_scratch_bytes(self.nx, self.ny, self.rank, self.cap)),
+                               dtype=torch.uint8, device=self.dev)
+        self.ah = torch.zeros(self.nx, self.rank, dtype=torch.complex64, device=self.dev)
+        self.bh = torch.zeros(self.ny, self.rank, dtype=torch.complex64, device=self.dev)
+        self.alpha_bar = torch.zeros(1, dtype=torch.float64, device=self.dev)
+        self.pos = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self.status = torch.zeros(1, **i32)
+        self.t = int(t0)
+        self.frame = 0
+
+    def set_image_factors(self, A, B):
+        a = torch.as_tensor(np.asarray(A) if not isinstance(A, torch.Tensor) else A)
+        b = torch.as_tensor(np.asarray(B) if not isinstance(B, torch.Tensor) else B)
+        self.ah = K.fft_cols_(a.to(self.dev, torch.complex64).reshape(self.nx, self.rank).contiguous())
+        self.bh = K.fft_cols_(b.to(self.dev, torch.complex64).reshape(self.ny, self.rank).contiguous())
+
+    def make_outputs(self, frames: int) -> dict:
+        d, R = self.dev, self.rank
+        return dict(gamma=torch.empty(frames, 1, R, dtype=torch.complex64, device=d),
+                    cost=torch.empty(frames, 1, dtype=torch.float64, device=d),
+                    mu=torch.empty(frames, 1, dtype=torch.float64, device=d),
+                    alpha=torch.empty(frames, 1, dtype=torch.float64, device=d),
+                    rows=torch.full((frames, 1, self.cap), -1, dtype=torch.int32, device=d),
+                    cnt=torch.empty(frames, 1, dtype=torch.int32, device=d),
+                    ah=torch.empty(frames, 1, self.nx, R, dtype=torch.complex64, device=d),
+                    bh=torch.empty(frames, 1, self.ny, R, dtype=torch.complex64, device=d))
+
+    def _frame(self, ks: torch.Tensor, f: int, fo: int, out: dict, keep: list) -> None:
+        lib, st = L.lib(), L.stream_ptr()
+        nx, ny, R = self.nx, self.ny, self.rank
+        if isinstance(self.policy, InformativeEntries):
+            pol = self.policy
+            L.check(lib.tt_entry_scores(st, nx, ny, R, self.ah.data_ptr(), self.bh.data_ptr(), float(pol.beta),
+                                        self.probs.data_ptr(), self.status.data_ptr()), "entry_scores")
+            L.check(lib.tt_draw_with_replacement_large(
+                st, nx * ny, self.probs.data_ptr(), int(pol.k),
+                self.forced.data_ptr() if self.forced.numel() else None, int(self.forced.numel()),
+                int(pol.key0), int(pol.key1), self.pos.data_ptr(), self.omega.data_ptr(), self.count.data_ptr(),
+                self.dscr.data_ptr()), "draw (entries)")
+            omega, count = self.omega, self.count
+        else:
+            omega, count = self.tab[f], self.tab_cnt[f:f + 1]
+        L.check(lib.tt_gather_entries(st, nx, ny, ks[f].data_ptr(), omega.data_ptr(), count.data_ptr(), self.cap,
+                                      self.idx.data_ptr(), self.y.data_ptr()), "gather_entries")
+        mode, mu, cf, cc = _step_params(self.step)
+        a = L.EntriesArgs()
+        a.nx, a.ny, a.rank, a.nmeas, a.t = nx, ny, R, self.cap, self.t
+        a.ah_in = a.ah_out = self.ah.data_ptr()
+        a.bh_in = a.bh_out = self.bh.data_ptr()
+        a.alpha_bar = self.alpha_bar.data_ptr()
+        a.idx, a.y = self.idx.data_ptr(), self.y.data_ptr()
+        a.lam, a.step_mode, a.mu, a.c_floor, a.c_cap = self.lam, mode, mu, cf, cc
+        a.gamma_out = out["gamma"][fo].data_ptr()
+        a.cost_out = out["cost"][fo].data_ptr()
+        a.mu_out = out["mu"][fo].data_ptr()
+        a.alpha_out = out["alpha"][fo].data_ptr()
+        a.status = self.status.data_ptr()
+        a.scratch = self.scr.data_ptr()
+        a.nmeas_dev = count.data_ptr()
+        keep.append(a)
+        K.track_entries(a)
+        out["ah"][fo, 0].copy_(self.ah)
+        out["bh"][fo, 0].copy_(self.bh)
+        out["cnt"][fo].copy_(count)
+        out["rows"][fo, 0, :omega.shape[0]].copy_(omega)
+        self.t += 1
+
+    def run(self, kspace: torch.Tensor, frames: int, out: dict | None = None, graph: bool = True) -> dict:
+        """Advance ``frames`` frames; ``kspace`` (T, nx, ny) complex64 resident truth, frames from the
+        current index. With ``graph`` the chain after the first frame is captured once and replayed."""
+        ks = kspace.reshape(kspace.shape[0], self.nx, self.ny)
+        if ks.dtype != torch.complex64 or not ks.is_cuda or not ks.is_contiguous():
+            raise TypeError("kspace must be a contiguous complex64 CUDA tensor (T, nx, ny)")
+        if self.frame + frames > ks.shape[0]:
+            raise ValueError("not enough truth frames")
+        if out is None:
+            out = self.make_outputs(frames)
+        keep: list = []
+        f0 = self.frame
+        first = min(frames, 1)
+        for fo in range(first):  # eager: one-time attribute setup happens outside any capture
+            self._frame(ks, f0 + fo, fo, out, keep)
+        rest = frames - first
+        if rest > 0 and graph:
+            g = torch.cuda.CUDAGraph()
+            t_save = self.t
+            with torch.cuda.graph(g):
+                for fo in range(first, frames):
+                    self._frame(ks, f0 + fo, fo, out, keep)
+            self._graph = (g, keep)  # the captured argument blocks must outlive the replay
+            g.replay()
+            assert self.t == t_save + rest
+        else:
+            for fo in range(first, frames):
+                self._frame(ks, f0 + fo, fo, out, keep)
+        self.frame += frames
+        return out
+
+    def check_status(self):
+        L.raise_status(int(self.status.max().item()), "entry engine")
+
+    def reconstruct(self, out: dict) -> torch.Tensor:
+        F = out["gamma"].shape[0]
+        A = K.fft_cols(out["ah"], inverse=True).reshape(F, self.nx, self.rank)
+        B = K.fft_cols(out["bh"], inverse=True).reshape(F, self.ny, self.rank)
+        return K.reconstruct(A, B, out["gamma"].reshape(F, self.rank)).reshape(F, 1, self.nx, self.ny)
+
+    def image_factors(self):
+        return K.fft_cols(self.ah, inverse=True)[None], K.fft_cols(self.bh, inverse=True)[None]
+
+
 def _host_source(kspace):
     """(T, nslices, nx, ny) complex64 CPU tensor over the caller's host buffer (no copy when it
     already is one; pinned buffers make the chunked uploads asynchronous)."""
@@ -295,6 +473,8 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
     T, ns, nx, ny = src.shape
     A0 = np.asarray(A0).reshape(ns, nx, -1)
     R = A0.shape[-1]
+    if isinstance(policy, (InformativeEntries, StaticEntries)):
+        return _run_online_entries(src, on_dev, A0, B0, lam, step, policy, clean, t0, warm_frames)
     eng = OnlineEngine(nx, ny, R, ns, lam, step, policy, cluster, t0)
     eng.set_image_factors(A0, np.asarray(B0).reshape(ns, ny, R))
     dev = eng.dev
@@ -355,6 +535,36 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
     rows = [[rows_np[f, s, :cnt[f, s]].astype(np.int64) for s in range(ns)] for f in range(Ts)]
     return OnlineResult(recon=recon.numpy(), gamma=small["gamma"].numpy(), cost=small["cost"].numpy(),
                         mu=small["mu"].numpy(), rows=rows, nmse=nm, final_A=A, final_B=B)
+
+
+def _run_online_entries(src, on_dev, A0, B0, lam, step, policy, clean, t0, warm_frames) -> OnlineResult:
+    """run_online for the entry policies (one slice): upload, the graph-replayed frame chain,
+    reconstruction, download. The entry lists are reported in ``rows`` (flat indices i*ny + j)."""
+    T, ns, nx, ny = src.shape
+    if ns != 1:
+        raise ValueError("entry sampling runs one slice per engine")
+    if warm_frames:
+        raise ValueError("warm-up applies to the row-mask engine")
+    R = A0.shape[-1]
+    eng = EntryEngine(nx, ny, R, lam, step, policy, t0)
+    eng.set_image_factors(A0.reshape(nx, R), np.asarray(B0).reshape(ny, R))
+    kd = src.to(eng.dev, torch.complex64).contiguous() if on_dev else src.to(eng.dev, non_blocking=True).contiguous()
+    out = eng.run(kd.reshape(T, nx, ny), T)
+    X = eng.reconstruct(out)
+    nm = None
+    if clean is not None:
+        cl = torch.as_tensor(np.asarray(clean, dtype=np.complex64)).to(eng.dev).reshape(T, 1, nx, ny)
+        num = (cl - X).abs().pow(2).sum(dim=(-1, -2)).double()
+        den = cl.abs().pow(2).sum(dim=(-1, -2)).double()
+        nm = (num / den).cpu().numpy()
+    eng.check_status()
+    cnt = out["cnt"].cpu().numpy()
+    rows_np = out["rows"].cpu().numpy()
+    rows = [[np.sort(rows_np[f, 0, :cnt[f, 0]].astype(np.int64))] for f in range(T)]
+    A, B = eng.image_factors()
+    return OnlineResult(recon=X.cpu().numpy(), gamma=out["gamma"].cpu().numpy(), cost=out["cost"].cpu().numpy(),
+                        mu=out["mu"].cpu().numpy(), rows=rows, nmse=nm, final_A=A.cpu().numpy(),
+                        final_B=B.cpu().numpy())
 
 
 class RowShardedEngine:

@@ -133,3 +133,21 @@ def test_choice_restatement_is_numpy_choice():
         want = gen.choice(n, size=size, replace=True, p=p)
         got = O.choice_with_replacement(p, size, O.philox_uniforms(key, 0, size))
         np.testing.assert_array_equal(got, want)
+
+
+def test_entries_loop_equals_rows_loop_on_kspace_factors():
+    """online_run_entries (EntryMask on (F_x A, F_y B), run_adaptive's entries mode) equals the FourierMask
+    row loop when the entry lists are whole rows (test_mri.py:258-286 at the loop level)."""
+    rng = np.random.default_rng(3)
+    n, R, T = 12, 3, 4
+    ks = rng.standard_normal((T, n, n)) + 1j * rng.standard_normal((T, n, n))
+    A, B = O.random_subspace(n, n, R, seed=4)
+    rows = [np.sort(rng.choice(n, 5, replace=False)) for _ in range(T)]
+    a = O.online_run(ks, A, B, 0.2, ("fixed", 0.02), {"kind": "static", "rows": rows}, record_factors=True)
+    ents = [(r[:, None] * n + np.arange(n)[None, :]).ravel() for r in rows]
+    b = O.online_run_entries(ks, O.fft_cols(A), O.fft_cols(B), 0.2, ("fixed", 0.02),
+                             {"kind": "static", "entries": ents}, record_factors=True)
+    for f in range(T):
+        np.testing.assert_allclose(b["gamma"][f], a["gamma"][f], rtol=1e-10, atol=1e-12)
+        np.testing.assert_allclose(b["recon"][f], a["recon"][f], rtol=1e-10, atol=1e-12)
+        np.testing.assert_allclose(b["A"][f], O.fft_cols(a["A"][f]), rtol=1e-10, atol=1e-12)
