@@ -215,6 +215,17 @@ int tt_draw_with_replacement_large(void* stream, int n, const double* probs, int
 int tt_draw_without_replacement(void* stream, int n, const double* weights, int k, uint64_t key0,
                                 uint64_t key1, uint64_t* pos, int32_t* out, int32_t* status);
 
+/* ------------------------------------------------------------------ CTEN container (cten.py:1-74)
+ * "CTEN" | u8 version 1 | u8 dtype (0 f32 pairs, 1 f64 pairs) | u8 ndim | ndim x u32 dims | payload.
+ * Malformed files -> TT_EINVAL (CtenFormatError). Host memory only.
+ *  tt_cten_info:     dtype code, ndim and dims (max_dims entries) of a file.
+ *  tt_cten_read:     payload into `out` (count complex elements) as complex64 (out_is_f64 = 0)
+ *                    or complex128 (1); bit-exact when the file holds the same precision.
+ *  tt_cten_write:    data complex64 (src_is_f64 = 0) or complex128 (1), stored as dtype_code. */
+int tt_cten_info(const char* path, int* dtype_code, int* ndim, uint32_t* dims, int max_dims);
+int tt_cten_read(const char* path, void* out, size_t count, int out_is_f64);
+int tt_cten_write(const char* path, const void* data, int src_is_f64, int dtype_code, int ndim, const uint32_t* dims);
+
 /* ------------------------------------------------------------------ values
  * Reconstruction X_f = A_f diag(gamma_f) B_f^T (core.py:91-104,
  * mri.py:107-121), batched over frames: a [frames][nx][rank],

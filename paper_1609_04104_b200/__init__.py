@@ -50,6 +50,8 @@ from .tracker import (
     track_step,
 )
 from ._lib import NumericalError
+from .acquisition import StreamingProvider, measure, project
+from .cten import CtenFormatError, read_cten, read_cten_tensor, write_cten
 
 __all__ = [
     "TensorSubspace", "rebalance", "synthesize_slice",
@@ -62,5 +64,6 @@ __all__ = [
     "FrameEstimate", "interp_track_step", "reconstruct_frame",
     "OnlineEngine", "OnlineResult", "StaticRows", "Informative", "run_online", "warm_up", "RowShardedEngine",
     "EntryEngine", "InformativeEntries", "StaticEntries",
-    "NumericalError",
+    "NumericalError", "StreamingProvider", "measure", "project",
+    "CtenFormatError", "read_cten", "read_cten_tensor", "write_cten",
 ]

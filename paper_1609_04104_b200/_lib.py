@@ -75,6 +75,9 @@ SIGNATURES = {
     "tt_track_entries": (C.c_int, [_p, C.POINTER(EntriesArgs)]),
     "tt_gather_entries": (C.c_int, [_p, C.c_int, C.c_int, _p, _p, _p, C.c_int, _p, _p]),
     "tt_draw_scratch_bytes": (C.c_size_t, [C.c_int]),
+    "tt_cten_info": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), _p, C.c_int]),
+    "tt_cten_read": (C.c_int, [C.c_char_p, _p, C.c_size_t, C.c_int]),
+    "tt_cten_write": (C.c_int, [C.c_char_p, _p, C.c_int, C.c_int, C.c_int, _p]),
     "tt_draw_with_replacement_large": (C.c_int, [_p, C.c_int, _p, C.c_int, _p, C.c_int, C.c_uint64, C.c_uint64, _p,
                                                  _p, _p, _p]),
     "tt_terms_scratch_bytes": (C.c_size_t, [C.c_int, C.c_int, C.c_int]),
