@@ -610,6 +610,27 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         v.y = __ldcg(&g_ahs[(size_t)(k0) * R + o].y);
         ahs[o] = v;
       }
+      __syncthreads();
+      // GA own packed entries first: they need only Ah_S, so they run while the Y rows are in flight
+      // (4-way k split per entry, fixed-order quad reduction)
+      {
+        const int nq = 4 * (ee - eb);
+        for (int base = tid & ~31; base < nq; base += NT) {  // warp-uniform trip count
+          const int eq = base + lane;
+          const int e = eb + (eq >> 2), part = eq & 3;
+          double2 g = make_double2(0.0, 0.0);
+          if (eq < nq) {
+            const int ij = tab[e];
+            const int r = ij >> 8, q = ij & 255;
+            for (int kk = part; kk < kt; kk += 4) g = zfma_cj(ahs[kk * R + r], ahs[kk * R + q], g);
+          }
+          g.x += __shfl_xor_sync(0xffffffffu, g.x, 1);
+          g.y += __shfl_xor_sync(0xffffffffu, g.y, 1);
+          g.x += __shfl_xor_sync(0xffffffffu, g.x, 2);
+          g.y += __shfl_xor_sync(0xffffffffu, g.y, 2);
+          if (part == 0 && eq < nq) G[e - eb] = zadd(G[e - eb], g);
+        }
+      }
       cp_async_wait_all();
       __syncthreads();
       if (k0 == 0) STAMP(16);
@@ -636,23 +657,6 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         });
       }
       if (k0 == 0) STAMP(18);
-      // GA own packed entries (4-way k split per entry, fixed-order quad reduction)
-      const int nq = 4 * (ee - eb);
-      for (int base = tid & ~31; base < nq; base += NT) {  // warp-uniform trip count
-        const int eq = base + lane;
-        const int e = eb + (eq >> 2), part = eq & 3;
-        double2 g = make_double2(0.0, 0.0);
-        if (eq < nq) {
-          const int ij = tab[e];
-          const int r = ij >> 8, q = ij & 255;
-          for (int kk = part; kk < kt; kk += 4) g = zfma_cj(ahs[kk * R + r], ahs[kk * R + q], g);
-        }
-        g.x += __shfl_xor_sync(0xffffffffu, g.x, 1);
-        g.y += __shfl_xor_sync(0xffffffffu, g.y, 1);
-        g.x += __shfl_xor_sync(0xffffffffu, g.x, 2);
-        g.y += __shfl_xor_sync(0xffffffffu, g.y, 2);
-        if (part == 0 && eq < nq) G[e - eb] = zadd(G[e - eb], g);
-      }
       if (k0 == 0) STAMP(19);
       __syncthreads();
     }
@@ -676,12 +680,25 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     if (phase == 2)  // reduced W of this CTA's columns
       for (int o = tid; o < nJ * R; o += NT) wacc[o] = ((const float2*)a.xw)[(size_t)j0 * R + o];
     __syncthreads();
-    // h partial: sum_jj conj(Bh[jj][r]) W[jj][r]
-    if (tid < R) {
-      double2 h = make_double2(0.0, 0.0);
-      for (int jj = 0; jj < nJ; ++jj) h = zfma_cj(bhl[jj * R + tid], wacc[jj * R + tid], h);
-      __stcg(&g_hp[c * R + tid].x, h.x);
-      __stcg(&g_hp[c * R + tid].y, h.y);
+    // h partial: sum_jj conj(Bh[jj][r]) W[jj][r], all threads: (column r, part) then a fixed-order sum
+    {
+      // hparts x R double2 in U2 (free between the heavy phase and the updates; the plan reserves
+      // >= 16 nJm R bytes there and hparts <= nJ)
+      const int hparts = max(1, min(NT / R, nJ));
+      double2* hpart = (double2*)(smem + pl.o_u2);
+      if (tid < hparts * R) {
+        const int r = tid % R, part = tid / R;
+        double2 h = make_double2(0.0, 0.0);
+        for (int jj = part; jj < nJ; jj += hparts) h = zfma_cj(bhl[jj * R + r], wacc[jj * R + r], h);
+        hpart[part * R + r] = h;
+      }
+      __syncthreads();
+      if (tid < R) {
+        double2 h = make_double2(0.0, 0.0);
+        for (int part = 0; part < hparts; ++part) h = zadd(h, hpart[part * R + tid]);
+        __stcg(&g_hp[c * R + tid].x, h.x);
+        __stcg(&g_hp[c * R + tid].y, h.y);
+      }
     }
     for (int e = eb + tid; phase == 0 && e < ee; e += NT) {
       __stcg(&g_ga[e].x, G[e - eb].x);
