@@ -52,6 +52,8 @@ from .tracker import (
 from ._lib import NumericalError
 from .acquisition import StreamingProvider, measure, project
 from .cten import CtenFormatError, read_cten, read_cten_tensor, write_cten
+from .reports import (MetricRow, online_budget_rows, online_mask_rows, write_budget_csv, write_mask_csv,
+                      write_metrics_csv, write_trace_csv)
 
 __all__ = [
     "TensorSubspace", "rebalance", "synthesize_slice",
@@ -66,4 +68,6 @@ __all__ = [
     "EntryEngine", "InformativeEntries", "StaticEntries",
     "NumericalError", "StreamingProvider", "measure", "project",
     "CtenFormatError", "read_cten", "read_cten_tensor", "write_cten",
+    "MetricRow", "write_metrics_csv", "write_mask_csv", "write_trace_csv", "write_budget_csv",
+    "online_mask_rows", "online_budget_rows",
 ]

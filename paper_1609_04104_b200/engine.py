@@ -219,6 +219,7 @@ class OnlineResult:
     nmse: np.ndarray | None
     final_A: np.ndarray
     final_B: np.ndarray
+    factor_history: object = None  # (T, nx, R) k-space Ah after each frame (slice 0), device; keep_history=True
 
 
 def warm_up(engine: "OnlineEngine", kspace_warm: torch.Tensor, epochs: int) -> None:
@@ -451,7 +452,7 @@ def _blocks(f0, f1, C):
 
 
 def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, warm_frames=0,
-               warm_epochs=20, chunk=40) -> OnlineResult:
+               warm_epochs=20, chunk=40, keep_history=False) -> OnlineResult:
     """Public end-to-end call (host in, host out): the online loop over the
     frames of ``kspace`` (T, [nslices,] nx, ny) from image-domain initial
     factors, returning reconstructions and per-frame reports. The analogue of
@@ -534,7 +535,8 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
     rows_np = small["rows"].numpy()
     rows = [[rows_np[f, s, :cnt[f, s]].astype(np.int64) for s in range(ns)] for f in range(Ts)]
     return OnlineResult(recon=recon.numpy(), gamma=small["gamma"].numpy(), cost=small["cost"].numpy(),
-                        mu=small["mu"].numpy(), rows=rows, nmse=nm, final_A=A, final_B=B)
+                        mu=small["mu"].numpy(), rows=rows, nmse=nm, final_A=A, final_B=B,
+                        factor_history=out["ah"][:, 0].clone() if keep_history else None)
 
 
 def _run_online_entries(src, on_dev, A0, B0, lam, step, policy, clean, t0, warm_frames) -> OnlineResult:

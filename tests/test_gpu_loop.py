@@ -152,3 +152,26 @@ def test_pipelined_run_online_is_chunk_invariant(chunk):
         np.testing.assert_array_equal(got.final_A, ref.final_A)
         for f in range(T):
             np.testing.assert_array_equal(got.rows[f][0], ref.rows[f][0])
+
+
+def test_online_mask_and_budget_rows():
+    """run_adaptive's mask/budget rows (experiment.py:495-510) from a device run: the budget's
+    expected count equals sum_i 1 - (1 - p_i)^K under each frame's (oracle) row scores."""
+    import paper_1609_04104_b200 as tt
+    from paper_1609_04104_b200 import reports
+    from paper_1609_04104_b200.phantom import cine_phantom
+
+    n, R, T, K = 64, 6, 6, 16
+    ph = cine_phantom(n, n, T, period=8.0, seed=61)
+    A0, B0 = O.random_subspace(n, n, R, seed=62)
+    pol = tt.Informative(k=K, forced=(0,), beta=0.1, key0=4)
+    res = tt.run_online(ph.kspace, A0[None], B0[None], 0.1, tt.Fixed(0.01), pol, keep_history=True)
+    ref = O.online_run(ph.kspace, A0, B0, 0.1, ("fixed", 0.01),
+                       {"kind": "informative", "k": K, "forced": [0], "beta": 0.1, "key": (4, 0)})
+    mrows = reports.online_mask_rows(res, t0=5)
+    assert mrows[0][0] == 5 and len(mrows) == sum(len(r[0]) for r in res.rows)
+    brows = reports.online_budget_rows(res, A0, B0, K, beta=0.1, t0=5)
+    for f, (t, k, size, expected) in enumerate(brows):
+        p = ref["probs"][f]
+        assert t == 5 + f and k == K and size == len(ref["rows"][f])
+        assert expected == pytest.approx(float(np.sum(1.0 - (1.0 - p) ** K)), rel=1e-5)
