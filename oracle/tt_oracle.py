@@ -495,6 +495,41 @@ def online_run_entries(kspace, Ah, Bh, lam, step, policy, clean=None, t0=1, alph
     return out
 
 
+def batch_run(kspace, A, B, lam, step, rows, epochs, rng=None, reshuffle=False, rebalance_epochs=True, t0=1,
+              alpha_bar=0.0):
+    """Multi-epoch batch mode (tracker.run tracker.py:456-500, experiment.run_tracking
+    experiment.py:284-313) on row masks with FourierMask steps: the frames' data is revisited for
+    ``epochs`` passes (rebalance between passes, order re-drawn by ``rng.permutation`` when
+    ``reshuffle``, t growing globally); then every frame is re-projected onto the final subspace
+    (gamma_t = ridge solve, tracker.py:139-156) when epochs > 1, else the online gammas are kept.
+    Returns per-step reports in processing order, the orders, the final gammas and images."""
+    kspace = np.asarray(kspace)
+    T, n1, n2 = kspace.shape
+    data = [(rows_to_entries(np.asarray(r), n2), np.asarray(kspace[f], np.complex128)[np.asarray(r), :].ravel())
+            for f, r in enumerate(rows)]
+    t, reps, orders, online = t0, [], [], {}
+    for epoch in range(epochs):
+        if rebalance_epochs and epoch > 0:
+            A, B = rebalance(A, B)
+        order = np.arange(T)
+        if reshuffle and epoch > 0:
+            order = rng.permutation(T)
+        orders.append(order)
+        for k in order:
+            idx, y = data[k]
+            rep = track_step(A, B, t, alpha_bar, y, idx, "fourier", lam, step, power=False)
+            A, B, t, alpha_bar = rep["A"], rep["B"], rep["t"], rep["alpha_bar"]
+            reps.append(rep)
+            online[int(k)] = rep["gamma"]
+    gammas = []
+    for f in range(T):
+        idx, y = data[f]
+        g = ridge_svd(phi_matrix(A, B, idx, "fourier"), y, lam) if epochs > 1 else online[f]
+        gammas.append(g)
+    recon = [synth(A, B, g) for g in gammas]
+    return dict(reports=reps, orders=orders, gamma=gammas, recon=recon, final=(A, B, t, alpha_bar))
+
+
 # ---------------------------------------------------------------------------
 # row-sharded step (SURVEY §8e) — decomposition check, k-space form
 # ---------------------------------------------------------------------------

@@ -33,7 +33,7 @@ from . import _ops as K
 from .tracker import Fixed, HessianBound
 
 __all__ = ["StaticRows", "Informative", "OnlineEngine", "run_online", "OnlineResult", "warm_up", "RowShardedEngine",
-           "InformativeEntries", "StaticEntries", "EntryEngine"]
+           "InformativeEntries", "StaticEntries", "EntryEngine", "run_batch", "BatchResult"]
 
 
 @dataclass(frozen=True)
@@ -55,7 +55,13 @@ class Informative:
     key1: int = 0
 
 
+class _Project:
+    """Internal step marker: solve gamma only (mu = 0, the factors stay fixed)."""
+
+
 def _step_params(step):
+    if isinstance(step, _Project):
+        return L.TT_STEP_FIXED, 0.0, 0.0, 0.0
     if isinstance(step, HessianBound):
         return L.TT_STEP_HESSIAN, 0.0, float(step.c_floor), float(step.c_cap)
     if isinstance(step, Fixed):
@@ -567,6 +573,76 @@ def _run_online_entries(src, on_dev, A0, B0, lam, step, policy, clean, t0, warm_
     return OnlineResult(recon=X.cpu().numpy(), gamma=out["gamma"].cpu().numpy(), cost=out["cost"].cpu().numpy(),
                         mu=out["mu"].cpu().numpy(), rows=rows, nmse=nm, final_A=A.cpu().numpy(),
                         final_B=B.cpu().numpy())
+
+
+@dataclass
+class BatchResult:
+    recon: np.ndarray     # (T, nx, ny) images at the final subspace
+    gamma: np.ndarray     # (T, R) final gammas (re-projected when epochs > 1)
+    step_gamma: np.ndarray  # (epochs * T, R) per-step gammas, processing order
+    step_cost: np.ndarray
+    step_mu: np.ndarray
+    orders: list          # frame order per epoch
+    final_A: np.ndarray
+    final_B: np.ndarray
+    t: int
+
+
+def run_batch(kspace, A0, B0, lam, step, rows, counts, epochs=1, rng=None, reshuffle=False,
+              rebalance_epochs=True, t0=1, cluster=0) -> BatchResult:
+    """Multi-epoch batch mode on the device (tracker.run tracker.py:456-500,
+    experiment.run_tracking experiment.py:284-313): the frames' row-mask data
+    (``rows`` (T, Smax) table, ``counts`` (T,)) is revisited for ``epochs`` passes of the rows
+    kernel, the factors rebalanced between passes, the order re-drawn with ``rng.permutation`` when
+    ``reshuffle`` (the caller's generator, consumed as the reference does), t growing globally.
+    With epochs > 1 every frame's gamma is then re-solved against the final subspace (a pass of the
+    same kernel with a zero step) and the images synthesised from it. One slice."""
+    if epochs < 1:
+        raise ValueError("epochs must be at least 1")
+    if reshuffle and epochs > 1 and rng is None:
+        raise ValueError("rng is required for reshuffling")
+    src = kspace.to(torch.complex64) if isinstance(kspace, torch.Tensor) else _host_source(kspace)
+    if src.dim() == 4:
+        src = src[:, 0]
+    T, nx, ny = src.shape
+    R = np.asarray(A0).reshape(nx, -1).shape[-1]
+    tab = np.asarray(rows).reshape(T, 1, -1)
+    cnt = np.asarray(counts).reshape(T, 1)
+    dev = L.device()
+    kd = src.to(dev).contiguous().reshape(T, 1, nx, ny)
+    base = OnlineEngine(nx, ny, R, 1, lam, step, StaticRows(tab, cnt), cluster, t0)
+    base.set_image_factors(np.asarray(A0).reshape(1, nx, R), np.asarray(B0).reshape(1, ny, R))
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+    g_steps, c_steps, m_steps, orders = [], [], [], []
+    ah, bh, ab, t = base.ah, base.bh, base.alpha_bar, base.t
+    for epoch in range(epochs):
+        if rebalance_epochs and epoch > 0:
+            K.rebalance_(ah, bh, st)
+        order = np.arange(T)
+        if reshuffle and epoch > 0:
+            order = np.asarray(rng.permutation(T))
+        orders.append(order)
+        eng = OnlineEngine(nx, ny, R, 1, lam, step, StaticRows(tab[order], cnt[order]), base.cluster, t)
+        eng.ah, eng.bh, eng.alpha_bar = ah, bh, ab
+        sel = torch.from_numpy(order.astype(np.int64)).to(dev)
+        out = eng.run(kd.index_select(0, sel).contiguous(), T, history=False)
+        g_steps.append(out["gamma"][:, 0])
+        c_steps.append(out["cost"][:, 0])
+        m_steps.append(out["mu"][:, 0])
+        ah, bh, ab, t = eng.ah, eng.bh, eng.alpha_bar, eng.t
+    L.raise_status(int(st.max().item()) & L.TT_ST_ZEROCOL, "batch rebalance")
+    if epochs > 1:  # re-projection onto the final subspace
+        proj = OnlineEngine(nx, ny, R, 1, lam, _Project(), StaticRows(tab, cnt), base.cluster, t)
+        proj.ah, proj.bh = ah.clone(), bh.clone()
+        gam = proj.run(kd, T, history=False)["gamma"][:, 0]
+    else:
+        gam = g_steps[0]
+    A = K.fft_cols(ah, inverse=True).reshape(nx, R)
+    B = K.fft_cols(bh, inverse=True).reshape(ny, R)
+    X = K.reconstruct(A[None].expand(T, nx, R).contiguous(), B[None].expand(T, ny, R).contiguous(), gam.contiguous())
+    return BatchResult(recon=X.cpu().numpy(), gamma=gam.cpu().numpy(), step_gamma=torch.cat(g_steps).cpu().numpy(),
+                       step_cost=torch.cat(c_steps).cpu().numpy(), step_mu=torch.cat(m_steps).cpu().numpy(),
+                       orders=orders, final_A=A.cpu().numpy(), final_B=B.cpu().numpy(), t=t)
 
 
 class RowShardedEngine:

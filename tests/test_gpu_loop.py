@@ -175,3 +175,31 @@ def test_online_mask_and_budget_rows():
         p = ref["probs"][f]
         assert t == 5 + f and k == K and size == len(ref["rows"][f])
         assert expected == pytest.approx(float(np.sum(1.0 - (1.0 - p) ** K)), rel=1e-5)
+
+
+@pytest.mark.parametrize("epochs,reshuffle", [(1, False), (3, True), (2, False)])
+def test_batch_mode_matches_oracle(epochs, reshuffle):
+    """tracker.run / run_tracking batch mode: epochs over the same row-mask data, rebalance between
+    epochs, rng.permutation reshuffles (the caller's generator, stepped as the reference does), then
+    the re-projection onto the final subspace; per-step gammas and final images vs the oracle."""
+    import paper_1609_04104_b200 as tt
+    from paper_1609_04104_b200.phantom import cine_phantom
+
+    n, R, T, lam = 64, 6, 8, 0.1
+    ph = cine_phantom(n, n, T, period=8.0, seed=71)
+    A0, B0 = O.random_subspace(n, n, R, seed=72)
+    rng = np.random.default_rng(73)
+    rows = [np.sort(rng.choice(n, 16, replace=False)) for _ in range(T)]
+    tab = np.stack(rows)
+    ref = O.batch_run(ph.kspace, A0, B0, lam, ("fixed", 0.01), rows, epochs, rng=np.random.default_rng(9),
+                      reshuffle=reshuffle)
+    got = tt.run_batch(ph.kspace, A0, B0, lam, tt.Fixed(0.01), tab, np.full(T, 16), epochs=epochs,
+                       rng=np.random.default_rng(9), reshuffle=reshuffle)
+    for a, b in zip(got.orders, ref["orders"]):
+        np.testing.assert_array_equal(a, b)
+    for k, rep in enumerate(ref["reports"]):
+        assert rel(got.step_gamma[k], rep["gamma"]) < 1e-4, k
+    for f in range(T):
+        assert rel(got.gamma[f], ref["gamma"][f]) < 1e-4, f
+        assert rel(got.recon[f], ref["recon"][f]) < 1e-4, f
+    assert got.t == ref["final"][2]
