@@ -770,12 +770,11 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       {
         // Gauss-Jordan (R parallel steps, no back substitution) up to R = 32; the 2x2-blocked
         // LDL^H has fewer flops per step and wins beyond (profiles/tools/ubench_gj.cu)
-        const int E = Rp + R, ept = gj_ept(R, ROWS_NT);
+        // (few instantiations: every inlined variant costs instruction-cache lines in the frame loop)
+        const int ept = gj_ept(R, ROWS_NT);
         if (ept <= 1) block_gj_solve<1>(G, hv, gam, colb, R);
         else if (ept <= 2) block_gj_solve<2>(G, hv, gam, colb, R);
-        else if (ept <= 3) block_gj_solve<3>(G, hv, gam, colb, R);
         else if (ept <= 5) block_gj_solve<5>(G, hv, gam, colb, R);
-        else if (E <= 4 * ROWS_NT) block_ldl2_solve<4>(G, hv, gam, colb, blk, zf, R);
         else block_ldl2_solve<9>(G, hv, gam, colb, blk, zf, R);
       }
       STAMP(12);
