@@ -120,7 +120,7 @@ static bool rows_make_plan_cap(int nx, int ny, int R, int Smax, int CL, int red_
   if (fixed > (size_t)maxsmem) return false;
   // U2: k-tiles (ys KT x nJm, ahs KT x R) | Bh in fp64 + colnorm partials (phase a) | gamma-scaled GEMM operands
   size_t other = sizeof(double2) * (size_t)p->nJm * R + sizeof(double) * 256;
-  const size_t v2 = sizeof(float2) * (size_t)R * (p->nJm > p->nIm ? p->nJm : p->nIm);
+  const size_t v2 = sizeof(float2) * (size_t)R * (p->nJm + p->nIm);  // both gamma-scaled GEMM operands
   if (v2 > other) other = v2;
   size_t avail = maxsmem - fixed;
   int KT = (int)(avail / (sizeof(float2) * (size_t)(p->nJm + R)));
@@ -137,6 +137,37 @@ static bool rows_make_plan_cap(int nx, int ny, int R, int Smax, int CL, int red_
   p->smem = (int)o;
   return true;
 }
+
+// ---------------------------------------------------------------- GEMM epilogues
+// The four small GEMMs of a frame share one cgemm_tile instantiation (one copy of its code in the
+// frame loop); the epilogue is selected by a block-uniform mode.
+enum { EPI_W_ACC = 0, EPI_Z_STORE = 1, EPI_Q_UPDATE = 2, EPI_P_UPDATE = 3 };
+struct RowsEpi {
+  int mode, R;
+  float2* acc;          // W: wacc | Q: wacc (in: W, out: new Bh rows) | P: zs (in: Z sums, out: mu conj(g) P)
+  const float2* base;   // Q: bhl
+  float2* gdst;         // Z: L2 partials
+  const float2* gamf;
+  float cfac, muf;
+  TT_DEV void operator()(int m, int n, float2 v) const {
+    const int o = m * R + n;
+    switch (mode) {
+      case EPI_W_ACC:
+        acc[o] = cadd(acc[o], v);
+        break;
+      case EPI_Z_STORE:
+        __stcg(&gdst[o].x, v.x);
+        __stcg(&gdst[o].y, v.y);
+        break;
+      case EPI_Q_UPDATE:
+        acc[o] = cadd(cscale(base[o], cfac), cscale(cmul(cconj(gamf[n]), csub(acc[o], v)), muf));
+        break;
+      default:
+        acc[o] = cscale(cmul(cconj(gamf[n]), csub(acc[o], v)), muf);  // mu conj(g) P
+        break;
+    }
+  }
+};
 
 // ---------------------------------------------------------------- cold paths (kept out of line)
 // Static row table validation: range and duplicates (observation.py:41-55).
@@ -639,22 +670,17 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         const float2 v = ys[kk * pl.nJm + jj];
         ysq += (double)v.x * v.x + (double)v.y * v.y;
       }
-      // W[jj][r] += sum_k Y[k][jj] conj(Ah_S[k][r])
-      {
-        const int ks = gemm_split(nJ, R, kt, 2, 4, pl.red_cap);
-        cgemm_tile<2, 4, false, true>(nJ, R, kt, ys, 1, pl.nJm, ahs, R, 1, ks, red2,
-                                      [&](int m, int n, float2 v) { wacc[m * R + n] = cadd(wacc[m * R + n], v); });
-      }
-      __syncthreads();
-      if (k0 == 0) STAMP(17);
-      // Z partial over own columns: Z[k][r] = sum_jj Y[k][jj] conj(Bh[jj][r])
-      {
-        const int ks = gemm_split(kt, R, nJ, 2, 4, pl.red_cap);
-        float2* zdst = g_zp + ((size_t)c * Smax + k0) * R;
-        cgemm_tile<2, 4, false, true>(kt, R, nJ, ys, pl.nJm, 1, bhl, R, 1, ks, red2, [&](int m, int n, float2 v) {
-          __stcg(&zdst[m * R + n].x, v.x);
-          __stcg(&zdst[m * R + n].y, v.y);
-        });
+      // W[jj][r] += sum_k Y[k][jj] conj(Ah_S[k][r]), then the Z partial over own columns
+      // Z[k][r] = sum_jj Y[k][jj] conj(Bh[jj][r]): one call site, so one copy of the GEMM code
+      for (int gsel = 0; gsel < 2; ++gsel) {
+        const bool w = gsel == 0;
+        const int M = w ? nJ : kt, Kd = w ? kt : nJ;
+        const int ks = gemm_split(M, R, Kd, 2, 4, pl.red_cap);
+        const RowsEpi epi{w ? EPI_W_ACC : EPI_Z_STORE, R, wacc, nullptr, g_zp + ((size_t)c * Smax + k0) * R,
+                          nullptr, 0.f, 0.f};
+        cgemm_tile<2, 4, false, true>(M, R, Kd, ys, w ? 1 : pl.nJm, w ? pl.nJm : 1, w ? ahs : bhl, R, 1, ks, red2,
+                                      epi);
+        if (w) __syncthreads();  // the K-split buffer is reused
       }
       if (k0 == 0) STAMP(18);
       if (k0 == 0) STAMP(19);
@@ -826,32 +852,26 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     if (update) {
       const float cfac = (float)(1.0 - mu_used * lt);
       const float muf = (float)mu_used;
+      // gamma-scaled operands of both corrections at once: Bh diag(g) and Ah_own diag(g)
+      float2* vop2 = vop + (size_t)pl.nJm * R;
       for (int o = tid; o < nJ * R; o += NT) vop[o] = cmul(bhl[o], gamf[o % R]);
-      __syncthreads();
-      STAMP(21);
-      {
-        // corr[jj][r] = sum_q (Bh[jj][q] g_q) GA[r][q] = sum_q vop[jj][q] conj(GA[q][r])
-        const int ks = gemm_split(nJ, R, R, 2, 4, pl.red_cap);
-        cgemm_tile<2, 4, false, true>(nJ, R, R, vop, R, 1, gaf, R, 1, ks, red2, [&](int m, int n, float2 v) {
-          const int o = m * R + n;
-          wacc[o] = cadd(cscale(bhl[o], cfac), cscale(cmul(cconj(gamf[n]), csub(wacc[o], v)), muf));
-        });
-      }
-      __syncthreads();
-      STAMP(22);
       for (int o = tid; o < nown * R; o += NT) {
         const int m = o / R, q = o - m * R;
-        vop[o] = cmul(ahl[own_li[m] * R + q], gamf[q]);
+        vop2[o] = cmul(ahl[own_li[m] * R + q], gamf[q]);
       }
       __syncthreads();
-      {
-        const int ks = gemm_split(nown, R, R, 2, 4, pl.red_cap);
-        cgemm_tile<2, 4, false, true>(nown, R, R, vop, R, 1, gbf, R, 1, ks, red2, [&](int m, int n, float2 v) {
-          const int o = m * R + n;
-          zs[o] = cscale(cmul(cconj(gamf[n]), csub(zs[o], v)), muf);  // mu conj(g) P
-        });
+      STAMP(21);
+      // Q: corr[jj][r] = sum_q vop[jj][q] conj(GA[q][r]) -> new Bh rows; P: same with GB on the owned
+      // sampled rows -> mu conj(g) P. One call site, so one copy of the GEMM code.
+      for (int gsel = 0; gsel < 2; ++gsel) {
+        const bool q = gsel == 0;
+        const int M = q ? nJ : nown;
+        const int ks = gemm_split(M, R, R, 2, 4, pl.red_cap);
+        const RowsEpi epi{q ? EPI_Q_UPDATE : EPI_P_UPDATE, R, q ? wacc : zs, bhl, nullptr, gamf, cfac, muf};
+        cgemm_tile<2, 4, false, true>(M, R, R, q ? vop : vop2, R, 1, q ? gaf : gbf, R, 1, ks, red2, epi);
+        __syncthreads();
       }
-      __syncthreads();
+      STAMP(22);
       STAMP(23);
       for (int o = tid; o < nI * R; o += NT) {
         const int li = o / R, r = o - li * R;
