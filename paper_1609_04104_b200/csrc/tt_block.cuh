@@ -711,9 +711,10 @@ TT_DEV void cgemm_tile(int M, int N, int K, const float2* A, int a_m, int a_k, c
   const int tn = (N + TN - 1) / TN, tiles = ((M + TM - 1) / TM) * tn;
   const int items = tiles * KS;
   for (int it = tid; it < items; it += NT) {
-    const int tile = it % tiles, ks = it / tiles;
-    const int m0 = (tile / tn) * TM, n0 = (tile % tn) * TN;
-    const int k0 = (K * ks) / KS, k1 = (K * (ks + 1)) / KS;
+    const int ks = idiv(it, tiles), tile = it - ks * tiles;
+    const int mt = idiv(tile, tn);
+    const int m0 = mt * TM, n0 = (tile - mt * tn) * TN;
+    const int k0 = idiv(K * ks, KS), k1 = idiv(K * (ks + 1), KS);
     float2 acc[TM][TN];
 #pragma unroll
     for (int u = 0; u < TM; ++u)
@@ -759,7 +760,8 @@ TT_DEV void cgemm_tile(int M, int N, int K, const float2* A, int a_m, int a_k, c
     for (int o = tid; o < M * N; o += NT) {
       float2 s = red[o];
       for (int ks = 1; ks < KS; ++ks) s = cadd(s, red[(size_t)ks * M * N + o]);
-      out(o / N, o % N, s);
+      const int om = idiv(o, N);
+      out(om, o - om * N, s);
     }
   }
 }

@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       if (i >= i0 && i < i0 + nI) flags[i - i0] = k;
     }
     for (int o = tid; phase != 2 && o < S * R; o += NT) {
-      const int k = o / R, r = o - k * R;
+      const int k = idiv(o, R), r = o - k * R;
       const int i = rows[k];
       if (i >= i0 && i < i0 + nI) {
         const float2 v = ahl[(i - i0) * R + r];
@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     if (phase != 2) {
       const int kt = min(KT, S);
       for (int o = tid; o < kt * nJ; o += NT) {
-        const int kk = o / nJ, jj = o - kk * nJ;
+        const int kk = idiv(o, nJ), jj = o - kk * nJ;
         cp_async8(&ys[kk * pl.nJm + jj], ybase + (size_t)(gather ? rows[kk] : kk) * ny + jj);
       }
     }
@@ -631,7 +631,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       const int kt = min(KT, S - k0);
       if (k0 > 0) {
         for (int o = tid; o < kt * nJ; o += NT) {
-          const int kk = o / nJ, jj = o - kk * nJ;
+          const int kk = idiv(o, nJ), jj = o - kk * nJ;
           cp_async8(&ys[kk * pl.nJm + jj], ybase + (size_t)(gather ? rows[k0 + kk] : k0 + kk) * ny + jj);
         }
       }
@@ -666,7 +666,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       __syncthreads();
       if (k0 == 0) STAMP(16);
       for (int o = tid; o < kt * nJ; o += NT) {
-        const int kk = o / nJ, jj = o - kk * nJ;
+        const int kk = idiv(o, nJ), jj = o - kk * nJ;
         const float2 v = ys[kk * pl.nJm + jj];
         ysq += (double)v.x * v.x + (double)v.y * v.y;
       }
@@ -740,7 +740,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
 
     // ======== (d) redundant fp64 solve; cluster sums of Z for owned rows prefetched alongside
     for (int o = tid; o < nown * R; o += NT) {
-      const int m = o / R, r = o - m * R;
+      const int m = idiv(o, R), r = o - m * R;
       zs[o] = sum_parts_f2(g_zp + (size_t)own_k[m] * R + r, (size_t)Smax * R, CL);
     }
     for (int e = tid; e < Rp; e += NT) {
@@ -854,9 +854,9 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       const float muf = (float)mu_used;
       // gamma-scaled operands of both corrections at once: Bh diag(g) and Ah_own diag(g)
       float2* vop2 = vop + (size_t)pl.nJm * R;
-      for (int o = tid; o < nJ * R; o += NT) vop[o] = cmul(bhl[o], gamf[o % R]);
+      for (int o = tid; o < nJ * R; o += NT) vop[o] = cmul(bhl[o], gamf[o - idiv(o, R) * R]);
       for (int o = tid; o < nown * R; o += NT) {
-        const int m = o / R, q = o - m * R;
+        const int m = idiv(o, R), q = o - m * R;
         vop2[o] = cmul(ahl[own_li[m] * R + q], gamf[q]);
       }
       __syncthreads();
@@ -874,7 +874,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       STAMP(22);
       STAMP(23);
       for (int o = tid; o < nI * R; o += NT) {
-        const int li = o / R, r = o - li * R;
+        const int li = idiv(o, R), r = o - li * R;
         float2 v = cscale(ahl[o], cfac);
         const int m = flags[li];
         if (m >= 0) v = cadd(v, zs[m * R + r]);
