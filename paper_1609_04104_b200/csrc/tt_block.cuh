@@ -759,7 +759,9 @@ TT_DEV void cgemm_tile(int M, int N, int K, const float2* A, int a_m, int a_k, c
     __syncthreads();
     for (int o = tid; o < M * N; o += NT) {
       float2 s = red[o];
-      for (int ks = 1; ks < KS; ++ks) s = cadd(s, red[(size_t)ks * M * N + o]);
+#pragma unroll
+      for (int ks = 1; ks < 8; ++ks)  // KS <= 8 (gemm_split): all partial loads in flight, fixed order
+        if (ks < KS) s = cadd(s, red[(size_t)ks * M * N + o]);
       const int om = idiv(o, N);
       out(om, o - om * N, s);
     }
@@ -842,7 +844,7 @@ TT_DEV void cgemm_v2(int M, int N, int K, const float2* A, int a_m, int a_k, con
 // K-split factor that fills the block without exceeding the reduction buffer
 TT_DEV int gemm_split(int M, int N, int K, int TM, int TN, int red_cap) {
   const int tiles = ((M + TM - 1) / TM) * ((N + TN - 1) / TN);
-  int ks = (int)blockDim.x / (tiles > 0 ? tiles : 1);
+  int ks = idiv((int)blockDim.x, tiles > 0 ? tiles : 1);
   if (ks > K / 4) ks = K / 4;
   if (ks > 8) ks = 8;
   while (ks > 1 && ks * M * N > red_cap) --ks;
