@@ -116,9 +116,15 @@ typedef struct tt_rows_args {
   int32_t shard_rank, shard_world, shard_phase;
   float* xw;
   double* xg;
+  /* Local multi-rank launch (appended; 0 = off): all shard_world ranks are clusters of one launch
+   * on this GPU (shard_rank ignored). ah_in/ah_out/ah_hist hold all nx rows; xw/xg hold one
+   * payload slot per rank; tt_rows_shard_reduce sums the slots into slot 0, which phase 2 reads. */
+  int32_t shard_local;
 } tt_rows_args;
 /* doubles in the fp64 payload xg of a sharded launch */
 size_t tt_rows_shard_xg_len(int rank);
+/* sum the `world` payload slots of a local multi-rank phase-1 launch into slot 0 (fixed order) */
+int tt_rows_shard_reduce(void* stream, int world, int ny, int rank, float* xw, double* xg);
 
 /* Choose the cluster size (if *cluster <= 0) and report the dynamic shared
  * memory per CTA; TT_EUNSUPPORTED if no cluster size fits. */

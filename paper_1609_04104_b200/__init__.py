@@ -9,8 +9,8 @@ anywhere, but every compute call needs a CUDA device and the built library.
 """
 
 from .core import TensorSubspace, rebalance, synthesize_slice
-from .engine import (BatchResult, EntryEngine, Informative, InformativeEntries, OnlineEngine, OnlineResult,
-                     RowShardedEngine, StaticEntries, StaticRows, run_batch, run_online, warm_up)
+from .engine import (BatchResult, EntryEngine, Informative, InformativeEntries, LocalShardedEngine, OnlineEngine,
+                     OnlineResult, RowShardedEngine, StaticEntries, StaticRows, run_batch, run_online, warm_up)
 from .mri import FrameEstimate, interp_track_step, reconstruct_frame
 from .observation import (
     EntryMask,
@@ -65,7 +65,7 @@ __all__ = [
     "expected_count_trace", "expected_sample_count", "row_scores",
     "FrameEstimate", "interp_track_step", "reconstruct_frame",
     "OnlineEngine", "OnlineResult", "StaticRows", "Informative", "run_online", "warm_up", "RowShardedEngine",
-    "EntryEngine", "InformativeEntries", "StaticEntries", "run_batch", "BatchResult",
+    "EntryEngine", "InformativeEntries", "StaticEntries", "run_batch", "BatchResult", "LocalShardedEngine",
     "NumericalError", "StreamingProvider", "measure", "project",
     "CtenFormatError", "read_cten", "read_cten_tensor", "write_cten",
     "MetricRow", "write_metrics_csv", "write_mask_csv", "write_trace_csv", "write_budget_csv",

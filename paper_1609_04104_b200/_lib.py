@@ -47,7 +47,7 @@ class RowsArgs(C.Structure):
         ("gamma_out", _p), ("cost_out", _p), ("mu_out", _p), ("alpha_out", _p), ("rows_out", _p),
         ("cnt_out", _p), ("resid_out", _p), ("ah_hist", _p), ("bh_hist", _p), ("status", _p), ("scratch", _p),
         ("phase_clock", _p), ("shard_rank", _i32), ("shard_world", _i32), ("shard_phase", _i32), ("xw", _p),
-        ("xg", _p),
+        ("xg", _p), ("shard_local", _i32),
     ]
 
 
@@ -71,6 +71,7 @@ SIGNATURES = {
     "tt_rows_scratch_bytes": (C.c_size_t, [C.c_int] * 6),
     "tt_track_rows": (C.c_int, [_p, C.POINTER(RowsArgs)]),
     "tt_rows_shard_xg_len": (C.c_size_t, [C.c_int]),
+    "tt_rows_shard_reduce": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, _p, _p]),
     "tt_entries_scratch_bytes": (C.c_size_t, [C.c_int] * 4),
     "tt_track_entries": (C.c_int, [_p, C.POINTER(EntriesArgs)]),
     "tt_gather_entries": (C.c_int, [_p, C.c_int, C.c_int, _p, _p, _p, C.c_int, _p, _p]),

@@ -238,15 +238,23 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
   const int lane = tid & 31, warp = tid >> 5;
   const int CL = pl.CL;
   const int c = (int)(blockIdx.x % CL);
-  const int s = (int)(blockIdx.x / CL);
+  const int qid = (int)(blockIdx.x / CL);  // cluster index: slice, or rank of a local multi-rank launch
   const int nx = a.nx, ny = a.ny, R = a.rank, Smax = a.max_rows, Rp = pl.Rp;
-  // row sharding across GPUs: this rank holds k-space rows [R0, R0 + nxs) of Ah (all rows when off)
+  // row sharding: this rank holds k-space rows [R0, R0 + nxs) of Ah (all rows when off). With
+  // shard_local every rank of the sharding is a cluster of this launch (one GPU, several clusters);
+  // each reads the full Ah at its row offset, has its own scratch and payload slot, and only rank 0
+  // writes the replicated outputs (Bh, gamma, cost, step state).
   const bool shard = a.shard_world > 0;
+  const bool multi = shard && a.shard_local != 0;
+  const int s = multi ? 0 : qid;  // slice
+  const int srank = multi ? qid : a.shard_rank;
+  const bool lead = !multi || qid == 0;
   const int phase = shard ? a.shard_phase : 0;  // 0 full step, 1 partials -> payload, 2 payload -> update
-  const int R0 = shard ? part_begin(nx, a.shard_world, a.shard_rank) : 0;
-  const int nxs = shard ? part_begin(nx, a.shard_world, a.shard_rank + 1) - R0 : nx;
+  const int R0 = shard ? part_begin(nx, a.shard_world, srank) : 0;
+  const int nxs = shard ? part_begin(nx, a.shard_world, srank + 1) - R0 : nx;
   const int i0 = R0 + part_begin(nxs, CL, c), nI = part_begin(nxs, CL, c + 1) - part_begin(nxs, CL, c);
   const int aoff = i0 - R0;  // first own row inside the rank's Ah buffers
+  const size_t arow = multi ? (size_t)i0 : (size_t)s * nxs + aoff;  // first own row in ah_in / ah_out
   const int j0 = part_begin(ny, CL, c), nJ = part_begin(ny, CL, c + 1) - j0;
   const int KT = pl.KT;
 
@@ -297,7 +305,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
 
   // global scratch for this slice
   const RowsScratch L = rows_scratch_layout(nx, ny, R, Smax, CL);
-  unsigned char* sb = (unsigned char*)a.scratch + (size_t)s * L.per_slice;
+  unsigned char* sb = (unsigned char*)a.scratch + (size_t)(multi ? qid : s) * L.per_slice;
   double* g_cn = (double*)(sb + L.cn);
   double2* g_gbp = (double2*)(sb + L.gbp);
   double2* g_gb = (double2*)(sb + L.gb);
@@ -311,7 +319,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
 
   // ---- load resident state and constants once
   {
-    const float2* src = (const float2*)a.ah_in + ((size_t)s * nxs + aoff) * R;
+    const float2* src = (const float2*)a.ah_in + arow * R;
     for (int o = tid; o < nI * R; o += NT) ahl[o] = src[o];
     const float2* srb = (const float2*)a.bh_in + ((size_t)s * ny + j0) * R;
     for (int o = tid; o < nJ * R; o += NT) bhl[o] = srb[o];
@@ -343,6 +351,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     const double lt = a.lam / (double)t;
     STAMP(0);
     int S = 0;
+    int Sglob = 0;  // measurements of the whole frame (S becomes this rank's share under row sharding)
     const int ndraw = a.policy == TT_POLICY_INFORMATIVE ? max(a.k_draws - a.nforced, 0) : 0;
     const uint64_t k1s = a.key1 + (uint64_t)s;
     if (phase != 2) {
@@ -544,6 +553,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       if (tid == 0) sh_err = 0;
       __syncthreads();
       S = load_static_rows(a, f, s, rows, flags, &sh_err);
+      Sglob = S;
       if (shard && warp == 0) {
         // keep only this rank's rows, in measurement order (the other ranks take the rest)
         int cnt = 0;
@@ -565,6 +575,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     __syncthreads();
     STAMP(5);
     S = sh_S;
+    if (!shard) Sglob = S;
     status |= sh_err;
 
     // ======== (b) publish own sampled rows of Ah; list them; prefetch the first Y tile
@@ -689,17 +700,19 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     STAMP(8);
     if (phase == 1) {
       // this rank's partials -> payload (the caller all-reduces xw and xg across ranks)
-      for (int o = tid; o < nJ * R; o += NT) ((float2*)a.xw)[(size_t)j0 * R + o] = wacc[o];
+      float2* xw1 = (float2*)a.xw + (multi ? (size_t)qid * ny * R : 0);  // this rank's payload slot
+      double* xg1 = a.xg + (multi ? (size_t)qid * (Rp * 2 + 2) : 0);
+      for (int o = tid; o < nJ * R; o += NT) xw1[(size_t)j0 * R + o] = wacc[o];
       for (int e = eb + tid; e < ee; e += NT) {
-        a.xg[2 * e] = G[e - eb].x;
-        a.xg[2 * e + 1] = G[e - eb].y;
+        xg1[2 * e] = G[e - eb].x;
+        xg1[2 * e + 1] = G[e - eb].y;
       }
       const double yt = block_sum(ysq, red);
       if (tid == 0) __stcg(&g_yn[c], yt);
       cluster_barrier();
       if (c == 0 && tid == 0) {
-        a.xg[2 * Rp] = sum_parts(g_yn, 1, CL);
-        a.xg[2 * Rp + 1] = scal[1];  // this rank's ||Ah||^2
+        xg1[2 * Rp] = sum_parts(g_yn, 1, CL);
+        xg1[2 * Rp + 1] = scal[1];  // this rank's ||Ah||^2
       }
       continue;  // phase 2 finishes the frame after the all-reduce
     }
@@ -791,7 +804,8 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     STAMP(11);
 
     double mu_used = 0.0, alpha = 0.0, cost;
-    const bool update = S > 0;
+    // the step is global: a rank whose rows hold no samples this frame still solves and scales them
+    const bool update = Sglob > 0;
     if (update) {
       {
         // Gauss-Jordan (R parallel steps, no back substitution) up to R = 32; the 2x2-blocked
@@ -887,7 +901,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
 
     // ======== outputs
     const size_t fs = (size_t)f * a.nslices + s;
-    if (c == 0) {
+    if (c == 0 && lead) {
       if (a.gamma_out && tid < R) ((float2*)a.gamma_out)[fs * R + tid] = gamf[tid];
       if (tid == 0) {
         if (a.cost_out) a.cost_out[fs] = cost;
@@ -899,10 +913,10 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         for (int k = tid; k < Smax; k += NT) a.rows_out[fs * Smax + k] = k < S ? rows[k] : -1;
     }
     if (a.ah_hist) {
-      float2* dst = (float2*)a.ah_hist + (fs * nxs + aoff) * R;
+      float2* dst = (float2*)a.ah_hist + (multi ? (size_t)f * nx + i0 : fs * nxs + aoff) * R;
       for (int o = tid; o < nI * R; o += NT) dst[o] = ahl[o];
     }
-    if (a.bh_hist) {
+    if (a.bh_hist && lead) {
       float2* dst = (float2*)a.bh_hist + (fs * ny + j0) * R;
       for (int o = tid; o < nJ * R; o += NT) dst[o] = bhl[o];
     }
@@ -913,12 +927,12 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
 
   // ---- write back resident state
   {
-    float2* dst = (float2*)a.ah_out + ((size_t)s * nxs + aoff) * R;
+    float2* dst = (float2*)a.ah_out + arow * R;
     for (int o = tid; o < nI * R; o += NT) dst[o] = ahl[o];
     float2* dsb = (float2*)a.bh_out + ((size_t)s * ny + j0) * R;
-    for (int o = tid; o < nJ * R; o += NT) dsb[o] = bhl[o];
+    for (int o = tid; lead && o < nJ * R; o += NT) dsb[o] = bhl[o];
   }
-  if (c == 0 && tid == 0) {
+  if (c == 0 && tid == 0 && lead) {
     if (a.alpha_bar) a.alpha_bar[s] = alpha_bar;
     if (a.policy == TT_POLICY_INFORMATIVE && a.philox_pos) a.philox_pos[s] = ppos;
   }
@@ -957,6 +971,34 @@ extern "C" int tt_rows_plan(int nx, int ny, int rank, int max_rows, int policy, 
 }
 
 extern "C" size_t tt_rows_shard_xg_len(int rank) { return (size_t)rank * (rank + 1) + 2; }
+
+// Sum the payload slots of a local multi-rank launch into slot 0 (fixed order over ranks): the
+// on-device counterpart of the all-reduce between the two phases.
+__global__ void shard_reduce_kernel(int world, size_t nw, size_t ng, float* __restrict__ xw, double* __restrict__ xg) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nw + ng; i += (size_t)gridDim.x * blockDim.x) {
+    if (i < nw) {
+      float v = xw[i];
+      for (int r = 1; r < world; ++r) v += xw[(size_t)r * nw + i];
+      xw[i] = v;
+    } else {
+      const size_t k = i - nw;
+      double v = xg[k];
+      for (int r = 1; r < world; ++r) v += xg[(size_t)r * ng + k];
+      xg[k] = v;
+    }
+  }
+}
+
+extern "C" int tt_rows_shard_reduce(void* stream, int world, int ny, int rank, float* xw, double* xg) {
+  if (world < 1 || ny < 1 || rank < 1 || !xw || !xg) return tt_fail(TT_EINVAL, "tt_rows_shard_reduce: bad args");
+  if (world == 1) return TT_OK;
+  const size_t nw = 2 * (size_t)ny * rank, ng = (size_t)rank * (rank + 1) + 2;
+  int blocks = (int)((nw + ng + 255) / 256);
+  if (blocks > 1184) blocks = 1184;
+  shard_reduce_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(world, nw, ng, xw, xg);
+  TT_CUDA_TRY(cudaGetLastError());
+  return TT_OK;
+}
 
 extern "C" size_t tt_rows_scratch_bytes(int nslices, int nx, int ny, int rank, int max_rows, int cluster) {
   if (cluster < 1) cluster = 16;
@@ -1002,7 +1044,8 @@ extern "C" int tt_track_rows(void* stream, const tt_rows_args* a) {
     configured_smem = pl.smem;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(a->nslices * pl.CL), 1, 1);
+  const int nclusters = (a->shard_world > 0 && a->shard_local) ? a->shard_world : a->nslices;
+  cfg.gridDim = dim3((unsigned)(nclusters * pl.CL), 1, 1);
   cfg.blockDim = dim3(ROWS_NT, 1, 1);
   cfg.dynamicSmemBytes = (size_t)pl.smem;
   cfg.stream = (cudaStream_t)stream;

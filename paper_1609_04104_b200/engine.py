@@ -33,7 +33,7 @@ from . import _ops as K
 from .tracker import Fixed, HessianBound
 
 __all__ = ["StaticRows", "Informative", "OnlineEngine", "run_online", "OnlineResult", "warm_up", "RowShardedEngine",
-           "InformativeEntries", "StaticEntries", "EntryEngine", "run_batch", "BatchResult"]
+           "InformativeEntries", "StaticEntries", "EntryEngine", "run_batch", "BatchResult", "LocalShardedEngine"]
 
 
 @dataclass(frozen=True)
@@ -543,6 +543,133 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
     return OnlineResult(recon=recon.numpy(), gamma=small["gamma"].numpy(), cost=small["cost"].numpy(),
                         mu=small["mu"].numpy(), rows=rows, nmse=nm, final_A=A, final_B=B,
                         factor_history=out["ah"][:, 0].clone() if keep_history else None)
+
+
+class LocalShardedEngine:
+    """The row-sharded step (BASELINE config 4) on one GPU: ``ranks`` thread-block clusters
+    each own a block of k-space rows of Ah (as a GPU of the multi-GPU sharding would); per frame one
+    phase-1 launch holds all ranks (partials of W, GA, ||Y||^2, ||Ah||^2 into one payload slot per
+    rank), a device kernel sums the slots in fixed order (the all-reduce of the multi-GPU path), and
+    one phase-2 launch solves redundantly and updates every rank's rows and the replicated Bh. Uses
+    ranks x 16 SMs instead of 16 for a single large slice; static row masks, one slice. The T-frame
+    chain of 3 launches per frame is replayed as one CUDA graph.
+
+    The replicated Bh is double-buffered across phase 2 (read one, rank 0 writes the other): when
+    the ranks' clusters do not fit the GPU at once they run in waves, and a later wave must still
+    read the frame's pre-update Bh."""
+
+    def __init__(self, nx, ny, rank, lam, step, rows, counts, ranks, cluster=0, t0=1):
+        self.nx, self.ny, self.R = int(nx), int(ny), int(rank)
+        self.ranks = int(ranks)
+        if self.ranks < 1 or self.ranks > self.nx:
+            raise ValueError("ranks must be in [1, nx]")
+        self.lam, self.step = float(lam), step
+        self.dev = L.device()
+        rows = np.asarray(rows).reshape(np.asarray(rows).shape[0], -1)
+        self.max_rows = int(rows.shape[1])
+        self.rows_tab = torch.from_numpy(np.ascontiguousarray(rows, dtype=np.int32)).to(self.dev)
+        self.rows_cnt = torch.from_numpy(np.ascontiguousarray(np.asarray(counts).reshape(-1), dtype=np.int32)).to(self.dev)
+        self.scr = K.RowsScratch(self.ranks, self.nx, self.ny, self.R, self.max_rows, cluster)  # one scratch per rank
+        self.cluster = self.scr.cluster
+        self.ah = torch.zeros(self.nx, self.R, dtype=torch.complex64, device=self.dev)
+        self._bhs = [torch.zeros(self.ny, self.R, dtype=torch.complex64, device=self.dev) for _ in range(2)]
+        self._cur = 0  # index of the buffer holding the current Bh
+        self.xg_len = int(L.lib().tt_rows_shard_xg_len(self.R))
+        self.xw = torch.zeros(self.ranks, self.ny, self.R, dtype=torch.complex64, device=self.dev)
+        self.xg = torch.zeros(self.ranks, self.xg_len, dtype=torch.float64, device=self.dev)
+        self.alpha_bar = torch.zeros(1, dtype=torch.float64, device=self.dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.t = int(t0)
+        self.frame = 0
+
+    def set_image_factors(self, A, B):
+        a = torch.as_tensor(np.asarray(A) if not isinstance(A, torch.Tensor) else A).to(self.dev, torch.complex64)
+        b = torch.as_tensor(np.asarray(B) if not isinstance(B, torch.Tensor) else B).to(self.dev, torch.complex64)
+        self.ah = K.fft_cols_(a.reshape(self.nx, self.R).contiguous())
+        self._bhs = [K.fft_cols_(b.reshape(self.ny, self.R).contiguous()), torch.empty(self.ny, self.R,
+                                                                                      dtype=torch.complex64,
+                                                                                      device=self.dev)]
+        self._cur = 0
+
+    @property
+    def bh(self) -> torch.Tensor:
+        return self._bhs[self._cur]
+
+    def image_factors(self):
+        return K.fft_cols(self.ah, inverse=True), K.fft_cols(self.bh, inverse=True)
+
+    def make_outputs(self, frames):
+        d = self.dev
+        return dict(gamma=torch.empty(frames, self.R, dtype=torch.complex64, device=d),
+                    cost=torch.empty(frames, dtype=torch.float64, device=d),
+                    mu=torch.empty(frames, dtype=torch.float64, device=d),
+                    ah=torch.empty(frames, self.nx, self.R, dtype=torch.complex64, device=d),
+                    bh=torch.empty(frames, self.ny, self.R, dtype=torch.complex64, device=d))
+
+    def _args(self, kspace, f, out, fo, phase, bh_cur, bh_nxt):
+        mode, mu, cf, cc = _step_params(self.step)
+        a = L.RowsArgs()
+        a.nslices, a.nx, a.ny, a.rank, a.frames = 1, self.nx, self.ny, self.R, 1
+        a.max_rows, a.cluster, a.t0 = self.max_rows, self.cluster, self.t
+        a.ah_in = a.ah_out = self.ah.data_ptr()
+        a.bh_in = bh_cur.data_ptr()
+        a.bh_out = (bh_nxt if phase == 2 else bh_cur).data_ptr()
+        a.alpha_bar = self.alpha_bar.data_ptr()
+        a.policy = L.TT_POLICY_STATIC
+        a.rows_tab = self.rows_tab.data_ptr() + 4 * f * self.max_rows
+        a.rows_cnt = self.rows_cnt.data_ptr() + 4 * f
+        a.y_mode = L.TT_Y_GATHER
+        a.ysrc = kspace[f].data_ptr()
+        a.y_frame_stride, a.y_slice_stride = self.nx * self.ny, self.nx * self.ny
+        a.lam, a.step_mode, a.mu, a.c_floor, a.c_cap = self.lam, mode, mu, cf, cc
+        if phase == 2 and out is not None:
+            a.gamma_out = out["gamma"][fo].data_ptr()
+            a.cost_out = out["cost"][fo:].data_ptr()
+            a.mu_out = out["mu"][fo:].data_ptr()
+            a.ah_hist = out["ah"][fo].data_ptr()
+            a.bh_hist = out["bh"][fo].data_ptr()
+        a.status = self.status.data_ptr()
+        a.scratch = self.scr.buf.data_ptr()
+        a.shard_rank, a.shard_world, a.shard_phase, a.shard_local = 0, self.ranks, phase, 1
+        a.xw, a.xg = self.xw.data_ptr(), self.xg.data_ptr()
+        return a
+
+    def _frame(self, kspace, f, out, fo, keep):
+        cur, nxt = self._bhs[self._cur], self._bhs[1 - self._cur]
+        a1 = self._args(kspace, f, None, fo, 1, cur, nxt)
+        a2 = self._args(kspace, f, out, fo, 2, cur, nxt)
+        keep += [a1, a2]
+        K.track_rows(a1)
+        L.check(L.lib().tt_rows_shard_reduce(L.stream_ptr(), self.ranks, self.ny, self.R, self.xw.data_ptr(),
+                                             self.xg.data_ptr()), "shard_reduce")
+        K.track_rows(a2)
+        self.t += 1
+        self._cur = 1 - self._cur
+
+    def run(self, kspace, frames, out=None, graph=True):
+        """kspace: (T, nx, ny) complex64 CUDA; frames from the current index."""
+        if out is None:
+            out = self.make_outputs(frames)
+        keep: list = []
+        f0 = self.frame
+        first = min(frames, 1)
+        for fo in range(first):  # eager first frame: one-time launch attributes outside any capture
+            self._frame(kspace, f0 + fo, out, fo, keep)
+        if frames > first and graph:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for fo in range(first, frames):
+                    self._frame(kspace, f0 + fo, out, fo, keep)
+            self._graph = (g, keep)
+            g.replay()
+        else:
+            for fo in range(first, frames):
+                self._frame(kspace, f0 + fo, out, fo, keep)
+        self.frame += frames
+        return out
+
+    def check_status(self):
+        L.raise_status(int(self.status.max().item()), "local sharded engine")
 
 
 def _run_online_entries(src, on_dev, A0, B0, lam, step, policy, clean, t0, warm_frames) -> OnlineResult:

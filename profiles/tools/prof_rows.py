@@ -4,14 +4,22 @@ import numpy as np, torch
 import paper_1609_04104_b200 as tt
 from bench import CONFIGS, make_data, init_factors
 cfg = dict(CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c2"])
-assert "K" in cfg, "informative configs only"
 T = int(sys.argv[2]) if len(sys.argv) > 2 else 50
 cfg["T"] = T
 cl = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 ids = list(range(cfg["slices"]))
 ks, _ = make_data(cfg, ids)
 A0, B0 = init_factors(cfg, ids)
-pol = tt.Informative(k=cfg["K"], forced=cfg["forced"], beta=cfg["beta"], key0=2024)
+if "vd" in cfg:  # static variable-density rows, as bench.py draws them
+    Smax = int(np.ceil(cfg["vd"] * cfg["n"]))
+    tab = np.zeros((T, len(ids), Smax), np.int64)
+    for si in range(len(ids)):
+        gen = np.random.Generator(np.random.Philox(key=2024 + (si << 64)))
+        for f in range(T):
+            tab[f, si] = tt.variable_density_rows(cfg["n"], -1.0, cfg["vd"], gen)
+    pol = tt.StaticRows(tab, np.full((T, len(ids)), Smax))
+else:
+    pol = tt.Informative(k=cfg["K"], forced=cfg["forced"], beta=cfg["beta"], key0=2024)
 eng = tt.OnlineEngine(cfg["n"], cfg["n"], cfg["R"], len(ids), cfg["lam"], tt.Fixed(cfg["mu"]), pol, cluster=cl)
 eng.set_image_factors(A0, B0)
 ah0, bh0 = eng.ah.clone(), eng.bh.clone()
