@@ -169,13 +169,16 @@ def draw_without_replacement(weights: torch.Tensor, k: int, key: tuple[int, int]
     return out[:k]
 
 
-def reconstruct(a: torch.Tensor, b: torch.Tensor, gamma: torch.Tensor) -> torch.Tensor:
-    """a (F, nx, R), b (F, ny, R), gamma (F, R) complex64 -> (F, nx, ny)."""
+def reconstruct(a: torch.Tensor, b: torch.Tensor, gamma: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """a (F, nx, R), b (F, ny, R), gamma (F, R) complex64 -> (F, nx, ny) (into ``out`` when given)."""
     for t, n in ((a, "a"), (b, "b"), (gamma, "gamma")):
         _need(t, C64, n)
     F, nx, R = a.shape
     ny = b.shape[1]
-    out = torch.empty(F, nx, ny, dtype=C64, device=a.device)
+    if out is None:
+        out = torch.empty(F, nx, ny, dtype=C64, device=a.device)
+    elif out.dtype != C64 or not out.is_contiguous() or out.numel() != F * nx * ny:
+        raise ValueError("reconstruct: out must be a contiguous complex64 tensor of F*nx*ny elements")
     done = 0
     while done < F:
         nf = min(65535, F - done)

@@ -204,14 +204,19 @@ class OnlineEngine:
     def check_status(self):
         L.raise_status(int(self.status.max().item()), "online engine")
 
-    def reconstruct(self, out: dict) -> torch.Tensor:
+    def reconstruct(self, out: dict, into: torch.Tensor | None = None, in_place: bool = False) -> torch.Tensor:
         """Image frames (F, nslices, nx, ny) from the recorded k-space factor
         history: inverse column FFT of each frame's factors, then the
-        gamma-weighted outer product."""
+        gamma-weighted outer product. ``in_place`` transforms the history
+        itself (no copies); ``into`` receives the images."""
         F, ns = out["gamma"].shape[:2]
-        A = K.fft_cols(out["ah"], inverse=True).reshape(F * ns, self.nx, self.rank)
-        B = K.fft_cols(out["bh"], inverse=True).reshape(F * ns, self.ny, self.rank)
-        X = K.reconstruct(A, B, out["gamma"].reshape(F * ns, self.rank))
+        if in_place:
+            A = K.fft_cols_(out["ah"], inverse=True).reshape(F * ns, self.nx, self.rank)
+            B = K.fft_cols_(out["bh"], inverse=True).reshape(F * ns, self.ny, self.rank)
+        else:
+            A = K.fft_cols(out["ah"], inverse=True).reshape(F * ns, self.nx, self.rank)
+            B = K.fft_cols(out["bh"], inverse=True).reshape(F * ns, self.ny, self.rank)
+        X = K.reconstruct(A, B, out["gamma"].reshape(F * ns, self.rank), out=into)
         return X.reshape(F, ns, self.nx, self.ny)
 
 
@@ -513,36 +518,55 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
     out = eng.make_outputs(Ts)
     recon = torch.empty(Ts, ns, nx, ny, dtype=torch.complex64, pin_memory=True)
     Xd = torch.empty(Ts, ns, nx, ny, dtype=torch.complex64, device=dev)
+    # tracking blocks run back to back on the compute stream; each block's reconstruction runs on its
+    # own stream once the block's tracking is done, and its download follows on the copy stream
+    s_rec = torch.cuda.Stream(dev)
+    s_rec.wait_stream(comp)
     s_out.wait_stream(comp)
+    hist = {k: out[k].clone() for k in ("ah",)} if keep_history else None
     for (f0, f1), ev in blocks:
         a, b = f0 - W, f1 - W
         comp.wait_event(ev)
         part = {k: v[a:b] for k, v in out.items()}
         eng.run(ks_stream, b - a, out=part)
-        Xd[a:b] = eng.reconstruct(part)
-        done = torch.cuda.Event()
-        done.record(comp)
+        tracked = torch.cuda.Event()
+        tracked.record(comp)
+        s_rec.wait_event(tracked)
+        with torch.cuda.stream(s_rec):
+            if keep_history:
+                hist["ah"][a:b].copy_(part["ah"])
+            eng.reconstruct(part, into=Xd[a:b], in_place=True)  # the history is not needed afterwards
+            done = torch.cuda.Event()
+            done.record(s_rec)
         s_out.wait_event(done)
         with torch.cuda.stream(s_out):
             recon[a:b].copy_(Xd[a:b], non_blocking=True)
-    Xd.record_stream(s_out)
-    small = {k: out[k].to("cpu", non_blocking=False) for k in ("gamma", "cost", "mu", "cnt", "rows")}
-    A, B = eng.image_factors()
-    A, B = A.cpu().numpy(), B.cpu().numpy()
+    comp.wait_stream(s_rec)
+    # small results, final factors and the status word: asynchronous copies into pinned memory, one sync
+    pinned = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True)  # noqa: E731
+    small = {k: pinned(out[k]) for k in ("gamma", "cost", "mu", "cnt", "rows")}
+    for k, v in small.items():
+        v.copy_(out[k], non_blocking=True)
+    Ad, Bd = eng.image_factors()
+    A, B, st = pinned(Ad), pinned(Bd), pinned(eng.status)
+    A.copy_(Ad, non_blocking=True)
+    B.copy_(Bd, non_blocking=True)
+    st.copy_(eng.status, non_blocking=True)
     nm = None
     if clean is not None:
         cl = torch.as_tensor(np.asarray(clean, dtype=np.complex64)).to(dev).reshape(Ts, ns, nx, ny)
         num = (cl - Xd).abs().pow(2).sum(dim=(-1, -2)).double()
         den = cl.abs().pow(2).sum(dim=(-1, -2)).double()
         nm = (num / den).cpu().numpy()
+    comp.synchronize()
     s_out.synchronize()
-    eng.check_status()
+    L.raise_status(int(st.max().item()), "online engine")
     cnt = small["cnt"].numpy()
     rows_np = small["rows"].numpy()
     rows = [[rows_np[f, s, :cnt[f, s]].astype(np.int64) for s in range(ns)] for f in range(Ts)]
     return OnlineResult(recon=recon.numpy(), gamma=small["gamma"].numpy(), cost=small["cost"].numpy(),
-                        mu=small["mu"].numpy(), rows=rows, nmse=nm, final_A=A, final_B=B,
-                        factor_history=out["ah"][:, 0].clone() if keep_history else None)
+                        mu=small["mu"].numpy(), rows=rows, nmse=nm, final_A=A.numpy(), final_B=B.numpy(),
+                        factor_history=hist["ah"][:, 0] if keep_history else None)
 
 
 class LocalShardedEngine:
