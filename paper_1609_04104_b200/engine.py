@@ -443,13 +443,16 @@ def _host_source(kspace):
     return t.to(torch.complex64).contiguous()
 
 
+EDGE_BLOCK = 8  # frames in the first and last pipeline blocks
+
+
 def _blocks(f0, f1, C):
     """Frame blocks [a, b) covering [f0, f1): short first and last blocks (the pipeline's fill and
     drain are one upload / one download of a block), ``C`` frames in between."""
     n = f1 - f0
     if n <= 0:
         return []
-    e = max(1, min(C, 8))
+    e = max(1, min(C, EDGE_BLOCK))
     if n <= 2 * e + C:
         sizes = [n] if n <= C else [e, n - e]
     else:
