@@ -203,3 +203,32 @@ def test_batch_mode_matches_oracle(epochs, reshuffle):
         assert rel(got.gamma[f], ref["gamma"][f]) < 1e-4, f
         assert rel(got.recon[f], ref["recon"][f]) < 1e-4, f
     assert got.t == ref["final"][2]
+
+
+@pytest.mark.parametrize("chunk", [1000, 3])
+def test_hessian_step_trajectory_matches_oracle(chunk):
+    """HessianBound through the device loop: alpha_t (closed form of the power method), the running
+    alpha_bar carried inside the kernel and across launches, mu_t = 1/alpha_bar, per-frame gamma and
+    the NRMSE trajectory vs the oracle with oracle masks fed in."""
+    import paper_1609_04104_b200 as tt
+    from paper_1609_04104_b200.phantom import cine_phantom
+
+    n, R, T, lam = 128, 10, 10, 0.1
+    ph = cine_phantom(n, n, T, period=8.0, seed=81)
+    A0, B0 = O.random_subspace(n, n, R, seed=82)
+    forced = list(range(4)) + list(range(n - 4, n))
+    ref = O.online_run(ph.kspace, A0, B0, lam, ("hessian", 1e-3, 1e6),
+                       {"kind": "informative", "k": 32, "forced": forced, "beta": 0.1, "key": (6, 0)},
+                       clean=ph.clean)
+    S = max(len(r) for r in ref["rows"])
+    tab = np.full((T, 1, S), -1, np.int64)
+    cnt = np.zeros((T, 1), np.int64)
+    for f, r in enumerate(ref["rows"]):
+        tab[f, 0, :len(r)] = r
+        cnt[f, 0] = len(r)
+    res = tt.run_online(ph.kspace, A0[None], B0[None], lam, tt.HessianBound(1e-3, 1e6), tt.StaticRows(tab, cnt),
+                        clean=ph.clean, chunk=chunk)
+    for f in range(T):
+        assert res.mu[f, 0] == pytest.approx(ref["mu"][f], rel=1e-5), f
+        assert rel(res.gamma[f, 0], ref["gamma"][f]) < 1e-4, f
+    assert np.max(np.abs(np.sqrt(res.nmse[:, 0]) - np.sqrt(np.array(ref["nmse"])))) < 1e-3
