@@ -631,14 +631,63 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         }
       if (lane == 31) sh_own = x;
     }
-    cluster_wait();
+    // ======== (c) heavy phase: W, Z partials, GA (own entries), ||Y||^2
+    double ysq = 0.0;
+    const bool one_tile = phase != 2 && S > 0 && S <= KT;
+    if (one_tile) {
+      // all sampled rows in one tile: the Z partial needs only Y and the resident Bh, so it runs inside
+      // the B3 window; B3 completes, Ah_S arrives and GA / W follow. Z and W share one GEMM call site.
+      cp_async_wait_all();
+      __syncthreads();
+      for (int o = tid; o < S * nJ; o += NT) {
+        const int kk = idiv(o, nJ), jj = o - kk * nJ;
+        const float2 v = ys[kk * pl.nJm + jj];
+        ysq += (double)v.x * v.x + (double)v.y * v.y;
+      }
+      for (int gsel = 0; gsel < 2; ++gsel) {
+        const bool z = gsel == 0;
+        if (!z) {
+          cluster_wait();  // ------------------------------------------------ B3 complete
+          for (int o = tid; o < S * R; o += NT) {
+            float2 v;
+            v.x = __ldcg(&g_ahs[o].x);
+            v.y = __ldcg(&g_ahs[o].y);
+            ahs[o] = v;
+          }
+          __syncthreads();
+          const int nq = 4 * (ee - eb);  // GA own packed entries (4-way k split, fixed-order quad sum)
+          for (int base = tid & ~31; base < nq; base += NT) {  // warp-uniform trip count
+            const int eq = base + lane;
+            const int e = eb + (eq >> 2), part = eq & 3;
+            double2 g = make_double2(0.0, 0.0);
+            if (eq < nq) {
+              const int ij = tab[e];
+              const int r = ij >> 8, q = ij & 255;
+              for (int kk = part; kk < S; kk += 4) g = zfma_cj(ahs[kk * R + r], ahs[kk * R + q], g);
+            }
+            g.x += __shfl_xor_sync(0xffffffffu, g.x, 1);
+            g.y += __shfl_xor_sync(0xffffffffu, g.y, 1);
+            g.x += __shfl_xor_sync(0xffffffffu, g.x, 2);
+            g.y += __shfl_xor_sync(0xffffffffu, g.y, 2);
+            if (part == 0 && eq < nq) G[e - eb] = zadd(G[e - eb], g);
+          }
+        }
+        const int M = z ? S : nJ, Kd = z ? nJ : S;
+        const int ks = gemm_split(M, R, Kd, 2, 4, pl.red_cap);
+        const RowsEpi epi{z ? EPI_Z_STORE : EPI_W_ACC, R, wacc, nullptr, g_zp + (size_t)c * Smax * R, nullptr, 0.f,
+                          0.f};
+        cgemm_tile<2, 4, false, true>(M, R, Kd, ys, z ? pl.nJm : 1, z ? 1 : pl.nJm, z ? bhl : ahs, R, 1, ks, red2,
+                                      epi);
+        __syncthreads();
+      }
+    } else {
+      cluster_wait();  // ---------------------------------------------------- B3 complete
+    }
     __syncthreads();  // warp 0's owned-row list (written after its arrive) is visible to all warps
     STAMP(7);
     const int nown = sh_own;
 
-    // ======== (c) heavy phase over k tiles: W, Z partials, GA (own entries), ||Y||^2
-    double ysq = 0.0;
-    for (int k0 = 0; phase != 2 && k0 < S; k0 += KT) {
+    for (int k0 = 0; !one_tile && phase != 2 && k0 < S; k0 += KT) {  // general case: several k tiles
       const int kt = min(KT, S - k0);
       if (k0 > 0) {
         for (int o = tid; o < kt * nJ; o += NT) {
