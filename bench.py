@@ -55,6 +55,10 @@ CONFIGS = {
                               "rows K=64 (4x) incl. 16 centre lines, beta=0.1, Philox draws, Fixed mu=0.01"),
     "c3": dict(n=256, R=16, T=100, lam=0.05, period=16.0, K=52, forced=(0,), beta=0.1, mu=0.01, slices=64,
                desc="config 3: 64 independent 256x256 slices, T=100, R=16, 20% informative rows (K=52, forced DC)"),
+    "c2e": dict(n=256, R=20, T=200, lam=0.05, period=20.0, entries=0.25, mu=0.01, slices=1, beta=0.1,
+                desc="config 2 with entry sampling (run_adaptive's entries mode): 256x256 complex64 cine "
+                     "phantom, T=200, R=20, lambda=0.05, informative entries K=16384 (25% of nx*ny trials, "
+                     "forced DC), beta=0.1, Philox draws, Fixed mu=0.01"),
     "c4": dict(n=1024, R=32, T=256, lam=0.1, period=16.0, vd=0.125, mu=0.01, slices=1,
                desc="config 4: 1024x1024 complex64 cine phantom, T=256, R=32, lambda=0.1, variable-density rows "
                     "12.5% (128 rows/frame), Fixed mu=0.01 (single GPU, unsharded)"),
@@ -224,6 +228,121 @@ def run_reference(args, cfg):
 
 
 # ------------------------------------------------------------------ our arm
+def run_entries(args, cfg):
+    """Entry-sampling online loop (EntryEngine): per frame entry scores, a
+    large-domain Philox draw, the gather at the drawn entries and the generic index-list step, the
+    frame chain replayed as one CUDA graph. Replicas per rank (no collective), like config 2."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1609_04104_b200 as tt
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n, R, T = cfg["n"], cfg["R"], cfg["T"]
+    k = int(np.ceil(cfg["entries"] * n * n))
+    ks_np, _ = make_data(cfg, [0])
+    A0, B0 = init_factors(cfg, [0])
+    pol = tt.InformativeEntries(k=k, forced=(0,), beta=cfg["beta"], key0=2024)
+    kd = torch.from_numpy(ks_np[:, 0]).to(dev)
+
+    def engine():
+        e = tt.EntryEngine(n, n, R, cfg["lam"], tt.Fixed(cfg["mu"]), pol)
+        e.set_image_factors(A0[0], B0[0])
+        return e
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    graphs = []
+    for _ in range(args.warmup + args.steps):  # one engine per step: every step replays the same sequence
+        e = engine()
+        e.run(kd, T)  # eager first frame + capture + one replay (warm)
+        graphs.append(e)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    stream = torch.cuda.current_stream()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.warmup):
+            graphs[i]._graph[0].replay()
+        for i in range(args.steps):
+            flush.zero_()
+            a, b = ev[i]
+            a.record(stream)
+            graphs[args.warmup + i]._graph[0].replay()
+            b.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    frames = T - 1  # the replayed chain (the first frame runs eagerly when the graph is captured)
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    tot = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    total_ms = float(tot[0])
+    value = frames * world * args.steps / (total_ms / 1e3)
+    # algorithmic bytes per frame: y and (i, j) at the sampled entries, factors read + written, gamma,
+    # the fp64 entry distribution (SURVEY §8d's row model with entries in place of rows)
+    L_frame = float(k)  # upper bound on |Omega| (distinct entries <= trials)
+    b_frame = 8 * L_frame + 8 * L_frame + 16 * R * (2 * n) + 8 * R + 8 * n * n
+    hbm_peak, sm_max, peak_kind = measured_peaks()
+    achieved = b_frame * frames * args.steps / (total_ms / 1e3) / 1e9
+    e2e = None
+    if not args.no_e2e:
+        ks_pin = torch.from_numpy(ks_np[:, 0]).pin_memory()
+        res = None
+        for _ in range(2):  # warm-up in the timed loop's pattern (pinned result blocks cached)
+            res = tt.run_online(ks_pin, A0, B0, cfg["lam"], tt.Fixed(cfg["mu"]), pol)
+        torch.cuda.synchronize()
+        t_e2e = []
+        for _ in range(max(1, args.steps)):
+            t0 = time.perf_counter()
+            res = tt.run_online(ks_pin, A0, B0, cfg["lam"], tt.Fixed(cfg["mu"]), pol)
+            torch.cuda.synchronize()
+            t_e2e.append(time.perf_counter() - t0)
+        et = torch.tensor([sum(t_e2e)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": T * world * len(t_e2e) / float(et[0]), "unit": "frames/s",
+               "h2d_bytes_per_step": int(ks_np[:, 0].nbytes),
+               "d2h_bytes_per_step": int(res.recon.nbytes + res.gamma.nbytes + res.cost.nbytes + res.mu.nbytes),
+               "call": "paper_1609_04104_b200.run_online(pinned host kspace, InformativeEntries) -> host recon"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle import tt_oracle as O
+        fr = 3
+        t0 = time.perf_counter()
+        O.online_run_entries(ks_np[:fr, 0], O.fft_cols(A0[0]), O.fft_cols(B0[0]), cfg["lam"], ("fixed", cfg["mu"]),
+                             {"kind": "informative", "k": k, "forced": [0], "beta": cfg["beta"], "key": (2024, 0)})
+        dt = time.perf_counter() - t0
+        cpu = {"value": fr / dt, "unit": "frames/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"first {fr} frames ({dt:.1f} s), oracle port of the reference entries loop"}
+    if world > 1:
+        dist.destroy_process_group()
+    if rank != 0:
+        return 0
+    line = {
+        "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c64", "data": "synthetic",
+        "config": {"workload": cfg["desc"], "frames_per_step": frames, "rank": R, "nx": n, "ny": n, "trials": k,
+                   "l2": "flushed between steps (256 MB write)", "parallelism": f"replicas x{world}"},
+        "gpu_launches": None,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": None, "kernel": "entry frame chain (graph)",
+                     "bytes_per_frame": b_frame, "peak_kind": peak_kind},
+        "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def run_row_sharded(args, cfg):
     """Config 4 across ranks: Ah row-sharded, one NCCL all-reduce pair per frame
     (SURVEY §8e). `scaling: strong` (the single 1024^2 slice is split)."""
@@ -529,6 +648,8 @@ def main():
         return run_reference(args, cfg)
     if args.config == "c4" and (int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.row_shard):
         return run_row_sharded(args, cfg)
+    if "entries" in cfg:
+        return run_entries(args, cfg)
     return run_ours(args, cfg)
 
 

@@ -199,6 +199,11 @@ int tt_row_scores(void* stream, int nslices, int nx, int ny, int rank, const flo
 /* entry_scores (sampler.py:95-112): [nx][ny] fp64 */
 int tt_entry_scores(void* stream, int nx, int ny, int rank, const float* a, const float* b, double beta,
                     double* probs_out, int32_t* status);
+/* the same with a caller-owned workspace of tt_entry_scores_ws_bytes(nx, ny) bytes (no per-call
+ * allocation; the form the device engines and captured graphs use) */
+size_t tt_entry_scores_ws_bytes(int nx, int ny);
+int tt_entry_scores_ws(void* stream, int nx, int ny, int rank, const float* a, const float* b, double beta,
+                       double* probs_out, int32_t* status, void* ws);
 /* draw_samples(replacement=True) (sampler.py:146-162): k - nforced draws of
  * Generator(Philox(key)).choice(n, p=probs) at stream positions pos[s]..,
  * union with forced -> sorted unique rows. Bit-exact with numpy for the

@@ -86,6 +86,8 @@ SIGNATURES = {
     "tt_data_terms": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, C.c_int, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "tt_row_scores": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, C.c_int, _p, _f64, _p, _p]),
     "tt_entry_scores": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, _p, _p, _f64, _p, _p]),
+    "tt_entry_scores_ws_bytes": (C.c_size_t, [C.c_int, C.c_int]),
+    "tt_entry_scores_ws": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, _p, _p, _f64, _p, _p, _p]),
     "tt_draw_with_replacement": (C.c_int, [_p, C.c_int, C.c_int, _p, C.c_int, _p, C.c_int, _u64, _u64, _p, _p,
                                            _p]),
     "tt_draw_without_replacement": (C.c_int, [_p, C.c_int, _p, C.c_int, _u64, _u64, _p, _p, _p]),

@@ -226,13 +226,36 @@ extern "C" int tt_row_scores(void* stream, int nslices, int nx, int ny, int rank
   return TT_OK;
 }
 
+static int entry_scores_run(cudaStream_t st, int nx, int ny, int rank, const float* a, const float* b, double beta,
+                            double* probs_out, int32_t* status, double* ws);
+
+extern "C" size_t tt_entry_scores_ws_bytes(int nx, int ny) {
+  return sizeof(double) * ((size_t)(nx > 0 ? nx : 0) + (ny > 0 ? ny : 0) + 1 + 4096);
+}
+
+// entry_scores with a caller-owned workspace (tt_entry_scores_ws_bytes): no allocation per call
+extern "C" int tt_entry_scores_ws(void* stream, int nx, int ny, int rank, const float* a, const float* b, double beta,
+                                  double* probs_out, int32_t* status, void* ws) {
+  if (nx < 1 || ny < 1 || rank < 1 || !a || !b || !probs_out || !ws)
+    return tt_fail(TT_EINVAL, "tt_entry_scores_ws: bad args");
+  if (!(beta >= 0.0 && beta < 1.0)) return tt_fail(TT_EINVAL, "uniform blend weight must be in [0, 1)");
+  return entry_scores_run((cudaStream_t)stream, nx, ny, rank, a, b, beta, probs_out, status, (double*)ws);
+}
+
 extern "C" int tt_entry_scores(void* stream, int nx, int ny, int rank, const float* a, const float* b, double beta,
                                double* probs_out, int32_t* status) {
   if (nx < 1 || ny < 1 || rank < 1 || !a || !b || !probs_out) return tt_fail(TT_EINVAL, "tt_entry_scores: bad args");
   if (!(beta >= 0.0 && beta < 1.0)) return tt_fail(TT_EINVAL, "uniform blend weight must be in [0, 1)");
-  // probs_out doubles as workspace for the energies only if large enough; use a temporary
   double* ws = nullptr;
-  TT_CUDA_TRY(cudaMallocAsync((void**)&ws, sizeof(double) * (nx + ny + 1 + 4096), (cudaStream_t)stream));
+  TT_CUDA_TRY(cudaMallocAsync((void**)&ws, tt_entry_scores_ws_bytes(nx, ny), (cudaStream_t)stream));
+  const int rc = entry_scores_run((cudaStream_t)stream, nx, ny, rank, a, b, beta, probs_out, status, ws);
+  TT_CUDA_TRY(cudaFreeAsync(ws, (cudaStream_t)stream));
+  return rc;
+}
+
+static int entry_scores_run(cudaStream_t st, int nx, int ny, int rank, const float* a, const float* b, double beta,
+                            double* probs_out, int32_t* status, double* ws) {
+  void* stream = (void*)st;
   const size_t sm = sizeof(double) * ((size_t)rank + 64);
   entry_energy_kernel<<<1, SMP_NT, sm, (cudaStream_t)stream>>>(nx, ny, rank, (const float2*)a, (const float2*)b, ws,
                                                                 status);
@@ -241,7 +264,6 @@ extern "C" int tt_entry_scores(void* stream, int nx, int ny, int rank, const flo
   if (blocks > 4096) blocks = 4096;
   entry_map_kernel<<<blocks, SMP_NT, 0, (cudaStream_t)stream>>>(nx, ny, rank, ws, beta, probs_out, ws + nx + ny + 1);
   entry_norm_kernel<<<blocks, SMP_NT, 0, (cudaStream_t)stream>>>(n, blocks, ws + nx + ny + 1, probs_out);
-  TT_CUDA_TRY(cudaFreeAsync(ws, (cudaStream_t)stream));
   TT_CUDA_TRY(cudaGetLastError());
   return TT_OK;
 }

@@ -24,6 +24,7 @@ Semantics kept from the reference loop:
 from __future__ import annotations
 
 from dataclasses import dataclass
+import ctypes as C
 
 import numpy as np
 import torch
@@ -299,6 +300,8 @@ class EntryEngine:
             self.cap = int(policy.k)
             self.forced = torch.from_numpy(forced.astype(np.int32)).to(self.dev)
             self.probs = torch.empty(n, dtype=torch.float64, device=self.dev)
+            self.sws = torch.empty(int(L.lib().tt_entry_scores_ws_bytes(self.nx, self.ny)), dtype=torch.uint8,
+                                   device=self.dev)
             self.dscr = torch.zeros(int(L.lib().tt_draw_scratch_bytes(n)), dtype=torch.uint8, device=self.dev)
             self.omega = torch.empty(self.cap, **i32)
             self.count = torch.zeros(1, **i32)
@@ -328,6 +331,7 @@ class EntryEngine:
         self.pos = torch.zeros(1, dtype=torch.int64, device=self.dev)
         self.status = torch.zeros(1, **i32)
         self.t = int(t0)
+        self._t0 = int(t0)
         self.frame = 0
 
     def set_image_factors(self, A, B):
@@ -335,6 +339,28 @@ class EntryEngine:
         b = torch.as_tensor(np.asarray(B) if not isinstance(B, torch.Tensor) else B)
         self.ah = K.fft_cols_(a.to(self.dev, torch.complex64).reshape(self.nx, self.rank).contiguous())
         self.bh = K.fft_cols_(b.to(self.dev, torch.complex64).reshape(self.ny, self.rank).contiguous())
+
+    def rerun(self, A, B) -> dict:
+        """Restart from image factors (A, B) and replay the sequence captured by the last
+        ``run(graph=True)`` over the same resident truth buffer (whose contents may have changed):
+        state reset, frame 0 eagerly, the captured frames replayed. Returns that run's outputs."""
+        if getattr(self, "_graph", None) is None:
+            raise RuntimeError("rerun needs a previous run(graph=True)")
+        g, keep, ks, frames, out = self._graph
+        self.set_image_factors(A, B)
+        self.alpha_bar.zero_()
+        self.pos.zero_()
+        self.status.zero_()
+        self.t, self.frame = self._t0, 0
+        P = self._P
+        P["ah0"], P["bh0"] = self.ah.data_ptr(), self.bh.data_ptr()
+        self._frame(ks.data_ptr(), 0, P, [])
+        g.replay()
+        self.t += frames - 1
+        self.ah = out["ah"][frames - 1, 0].clone()
+        self.bh = out["bh"][frames - 1, 0].clone()
+        self.frame = frames
+        return out
 
     def make_outputs(self, frames: int) -> dict:
         d, R = self.dev, self.rank
@@ -347,44 +373,43 @@ class EntryEngine:
                     ah=torch.empty(frames, 1, self.nx, R, dtype=torch.complex64, device=d),
                     bh=torch.empty(frames, 1, self.ny, R, dtype=torch.complex64, device=d))
 
-    def _frame(self, ks: torch.Tensor, f: int, fo: int, out: dict, keep: list) -> None:
+    def _frame(self, ks_ptr: int, fo: int, P: dict, keep: list) -> None:
+        """One frame. The step ping-pongs through the factor history (frame fo reads slot fo-1, writes
+        slot fo) and the draw writes its entry list and count straight into the outputs, so a frame is
+        four C calls and no copies. ``P`` holds the output base pointers and strides."""
         lib, st = L.lib(), L.stream_ptr()
         nx, ny, R = self.nx, self.ny, self.rank
+        ah_in = P["ah0"] if fo == 0 else P["ah"] + (fo - 1) * P["sah"]
+        bh_in = P["bh0"] if fo == 0 else P["bh"] + (fo - 1) * P["sbh"]
         if isinstance(self.policy, InformativeEntries):
             pol = self.policy
-            L.check(lib.tt_entry_scores(st, nx, ny, R, self.ah.data_ptr(), self.bh.data_ptr(), float(pol.beta),
-                                        self.probs.data_ptr(), self.status.data_ptr()), "entry_scores")
+            omega, count = P["rows"] + fo * P["srows"], P["cnt"] + 4 * fo
+            L.check(lib.tt_entry_scores_ws(st, nx, ny, R, ah_in, bh_in, float(pol.beta), self.probs.data_ptr(),
+                                           self.status.data_ptr(), self.sws.data_ptr()), "entry_scores")
             L.check(lib.tt_draw_with_replacement_large(
-                st, nx * ny, self.probs.data_ptr(), int(pol.k),
-                self.forced.data_ptr() if self.forced.numel() else None, int(self.forced.numel()),
-                int(pol.key0), int(pol.key1), self.pos.data_ptr(), self.omega.data_ptr(), self.count.data_ptr(),
+                st, nx * ny, self.probs.data_ptr(), int(pol.k), self.forced.data_ptr() if self.forced.numel() else None,
+                int(self.forced.numel()), int(pol.key0), int(pol.key1), self.pos.data_ptr(), omega, count,
                 self.dscr.data_ptr()), "draw (entries)")
-            omega, count = self.omega, self.count
         else:
-            omega, count = self.tab[f], self.tab_cnt[f:f + 1]
-        L.check(lib.tt_gather_entries(st, nx, ny, ks[f].data_ptr(), omega.data_ptr(), count.data_ptr(), self.cap,
-                                      self.idx.data_ptr(), self.y.data_ptr()), "gather_entries")
+            f = self.frame + fo
+            omega, count = P["tab"] + f * P["stab"], P["tcnt"] + 4 * f
+        L.check(lib.tt_gather_entries(st, nx, ny, ks_ptr, omega, count, self.cap, self.idx.data_ptr(),
+                                      self.y.data_ptr()), "gather_entries")
         mode, mu, cf, cc = _step_params(self.step)
         a = L.EntriesArgs()
         a.nx, a.ny, a.rank, a.nmeas, a.t = nx, ny, R, self.cap, self.t
-        a.ah_in = a.ah_out = self.ah.data_ptr()
-        a.bh_in = a.bh_out = self.bh.data_ptr()
+        a.ah_in, a.ah_out = ah_in, P["ah"] + fo * P["sah"]
+        a.bh_in, a.bh_out = bh_in, P["bh"] + fo * P["sbh"]
         a.alpha_bar = self.alpha_bar.data_ptr()
         a.idx, a.y = self.idx.data_ptr(), self.y.data_ptr()
         a.lam, a.step_mode, a.mu, a.c_floor, a.c_cap = self.lam, mode, mu, cf, cc
-        a.gamma_out = out["gamma"][fo].data_ptr()
-        a.cost_out = out["cost"][fo].data_ptr()
-        a.mu_out = out["mu"][fo].data_ptr()
-        a.alpha_out = out["alpha"][fo].data_ptr()
+        a.gamma_out = P["gamma"] + fo * 8 * R
+        a.cost_out, a.mu_out, a.alpha_out = P["cost"] + 8 * fo, P["mu"] + 8 * fo, P["alpha"] + 8 * fo
         a.status = self.status.data_ptr()
         a.scratch = self.scr.data_ptr()
-        a.nmeas_dev = count.data_ptr()
+        a.nmeas_dev = count
         keep.append(a)
-        K.track_entries(a)
-        out["ah"][fo, 0].copy_(self.ah)
-        out["bh"][fo, 0].copy_(self.bh)
-        out["cnt"][fo].copy_(count)
-        out["rows"][fo, 0, :omega.shape[0]].copy_(omega)
+        L.check(lib.tt_track_entries(st, C.byref(a)), "track_entries")
         self.t += 1
 
     def run(self, kspace: torch.Tensor, frames: int, out: dict | None = None, graph: bool = True) -> dict:
@@ -397,24 +422,41 @@ class EntryEngine:
             raise ValueError("not enough truth frames")
         if out is None:
             out = self.make_outputs(frames)
-        keep: list = []
+        if frames == 0:
+            return out
+        P = dict(ah0=self.ah.data_ptr(), bh0=self.bh.data_ptr(), ah=out["ah"].data_ptr(), bh=out["bh"].data_ptr(),
+                 sah=8 * self.nx * self.rank, sbh=8 * self.ny * self.rank, gamma=out["gamma"].data_ptr(),
+                 cost=out["cost"].data_ptr(), mu=out["mu"].data_ptr(), alpha=out["alpha"].data_ptr(),
+                 rows=out["rows"].data_ptr(), srows=4 * self.cap, cnt=out["cnt"].data_ptr())
+        if isinstance(self.policy, StaticEntries):
+            P.update(tab=self.tab.data_ptr(), stab=4 * self.tab.shape[1], tcnt=self.tab_cnt.data_ptr())
+        keep: list = [self.ah, self.bh]
         f0 = self.frame
+        kbase, kstride = ks.data_ptr(), 8 * self.nx * self.ny
         first = min(frames, 1)
         for fo in range(first):  # eager: one-time attribute setup happens outside any capture
-            self._frame(ks, f0 + fo, fo, out, keep)
+            self._frame(kbase + (f0 + fo) * kstride, fo, P, keep)
         rest = frames - first
         if rest > 0 and graph:
             g = torch.cuda.CUDAGraph()
             t_save = self.t
             with torch.cuda.graph(g):
                 for fo in range(first, frames):
-                    self._frame(ks, f0 + fo, fo, out, keep)
-            self._graph = (g, keep)  # the captured argument blocks must outlive the replay
+                    self._frame(kbase + (f0 + fo) * kstride, fo, P, keep)
+            self._graph = (g, keep, ks, frames, out)  # the captured argument blocks must outlive the replay
+            self._P = P
             g.replay()
             assert self.t == t_save + rest
         else:
             for fo in range(first, frames):
-                self._frame(ks, f0 + fo, fo, out, keep)
+                self._frame(kbase + (f0 + fo) * kstride, fo, P, keep)
+            self._keep = keep
+        if isinstance(self.policy, StaticEntries):
+            out["cnt"][:, 0].copy_(self.tab_cnt[f0:f0 + frames])
+            out["rows"][:, 0, :self.tab.shape[1]].copy_(self.tab[f0:f0 + frames])
+        # the state is the last history slot (copied: the outputs may be reused by the caller)
+        self.ah = out["ah"][frames - 1, 0].clone()
+        self.bh = out["bh"][frames - 1, 0].clone()
         self.frame += frames
         return out
 
@@ -699,6 +741,9 @@ class LocalShardedEngine:
         L.raise_status(int(self.status.max().item()), "local sharded engine")
 
 
+_ENTRY_PLANS: dict = {}  # (shape, policy, length) -> (EntryEngine with a captured graph, resident truth)
+
+
 def _run_online_entries(src, on_dev, A0, B0, lam, step, policy, clean, t0, warm_frames) -> OnlineResult:
     """run_online for the entry policies (one slice): upload, the graph-replayed frame chain,
     reconstruction, download. The entry lists are reported in ``rows`` (flat indices i*ny + j)."""
@@ -708,10 +753,24 @@ def _run_online_entries(src, on_dev, A0, B0, lam, step, policy, clean, t0, warm_
     if warm_frames:
         raise ValueError("warm-up applies to the row-mask engine")
     R = A0.shape[-1]
-    eng = EntryEngine(nx, ny, R, lam, step, policy, t0)
-    eng.set_image_factors(A0.reshape(nx, R), np.asarray(B0).reshape(ny, R))
-    kd = src.to(eng.dev, torch.complex64).contiguous() if on_dev else src.to(eng.dev, non_blocking=True).contiguous()
-    out = eng.run(kd.reshape(T, nx, ny), T)
+    # repeated calls with the same shapes, policy and length reuse the engine, its resident truth buffer
+    # and its captured frame graph (like an FFT plan): upload, replay, download
+    key = (nx, ny, R, T, float(lam), repr(step), repr(policy), int(t0), torch.cuda.current_device())
+    hit = _ENTRY_PLANS.get(key)
+    if hit is not None:
+        eng, kd = hit
+        kd.copy_(src.reshape(T, nx, ny), non_blocking=True)
+        out = eng.rerun(A0.reshape(nx, R), np.asarray(B0).reshape(ny, R))
+    else:
+        eng = EntryEngine(nx, ny, R, lam, step, policy, t0)
+        eng.set_image_factors(A0.reshape(nx, R), np.asarray(B0).reshape(ny, R))
+        kd = torch.empty(T, nx, ny, dtype=torch.complex64, device=eng.dev)
+        kd.copy_(src.reshape(T, nx, ny), non_blocking=True)
+        out = eng.run(kd, T, graph=T > 1)
+        if T > 1:
+            if len(_ENTRY_PLANS) >= 2:
+                _ENTRY_PLANS.pop(next(iter(_ENTRY_PLANS)))
+            _ENTRY_PLANS[key] = (eng, kd)
     X = eng.reconstruct(out)
     nm = None
     if clean is not None:
@@ -719,14 +778,24 @@ def _run_online_entries(src, on_dev, A0, B0, lam, step, policy, clean, t0, warm_
         num = (cl - X).abs().pow(2).sum(dim=(-1, -2)).double()
         den = cl.abs().pow(2).sum(dim=(-1, -2)).double()
         nm = (num / den).cpu().numpy()
-    eng.check_status()
-    cnt = out["cnt"].cpu().numpy()
-    rows_np = out["rows"].cpu().numpy()
-    rows = [[np.sort(rows_np[f, 0, :cnt[f, 0]].astype(np.int64))] for f in range(T)]
-    A, B = eng.image_factors()
-    return OnlineResult(recon=X.cpu().numpy(), gamma=out["gamma"].cpu().numpy(), cost=out["cost"].cpu().numpy(),
-                        mu=out["mu"].cpu().numpy(), rows=rows, nmse=nm, final_A=A.cpu().numpy(),
-                        final_B=B.cpu().numpy())
+    # asynchronous downloads into pinned memory, one synchronisation
+    pinned = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True)  # noqa: E731
+    Ad, Bd = eng.image_factors()
+    host = {k: pinned(v) for k, v in (("recon", X), ("gamma", out["gamma"]), ("cost", out["cost"]),
+                                      ("mu", out["mu"]), ("cnt", out["cnt"]), ("rows", out["rows"]),
+                                      ("A", Ad), ("B", Bd), ("st", eng.status))}
+    for k, v in (("recon", X), ("gamma", out["gamma"]), ("cost", out["cost"]), ("mu", out["mu"]),
+                 ("cnt", out["cnt"]), ("rows", out["rows"]), ("A", Ad), ("B", Bd), ("st", eng.status)):
+        host[k].copy_(v, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    L.raise_status(int(host["st"].max().item()), "entry engine")
+    cnt = host["cnt"].numpy()
+    rows_np = host["rows"].numpy()
+    # entry lists as measured: sorted for informative draws (np.union1d), the given order for static ones
+    rows = [[rows_np[f, 0, :cnt[f, 0]].astype(np.int64)] for f in range(T)]
+    return OnlineResult(recon=host["recon"].numpy(), gamma=host["gamma"].numpy(), cost=host["cost"].numpy(),
+                        mu=host["mu"].numpy(), rows=rows, nmse=nm, final_A=host["A"].numpy(),
+                        final_B=host["B"].numpy())
 
 
 @dataclass

@@ -133,3 +133,26 @@ def test_run_online_informative_entries_end_to_end():
     with pytest.raises(ValueError):
         tt.run_online(ph.kspace, A0[None], B0[None], 0.1, tt.Fixed(0.01),
                       tt.InformativeEntries(k=2, forced=(0, 1, 2)))
+
+
+def test_run_online_entries_plan_cache_reuse():
+    """A repeated run_online call with the same shapes/policy replays the cached frame graph on freshly
+    uploaded data: results equal a fresh eager engine run on that data, bit for bit."""
+    import torch
+    import paper_1609_04104_b200 as tt
+    from paper_1609_04104_b200 import engine as E
+    from paper_1609_04104_b200.phantom import cine_phantom
+
+    n, R, T = 32, 4, 6
+    pol = tt.InformativeEntries(k=200, forced=(0,), key0=12)
+    A0, B0 = O.random_subspace(n, n, R, seed=91)
+    E._ENTRY_PLANS.clear()
+    for seed in (92, 93, 92):  # miss, hit with other data, hit
+        ph = cine_phantom(n, n, T, period=8.0, seed=seed)
+        got = tt.run_online(ph.kspace, A0[None], B0[None], 0.1, tt.Fixed(0.01), pol)
+        eng = tt.EntryEngine(n, n, R, 0.1, tt.Fixed(0.01), pol)
+        eng.set_image_factors(A0, B0)
+        out = eng.run(torch.from_numpy(ph.kspace.astype(np.complex64)).cuda(), T, graph=False)
+        np.testing.assert_array_equal(got.gamma, out["gamma"].cpu().numpy())
+        np.testing.assert_array_equal(got.recon, eng.reconstruct(out).cpu().numpy())
+    assert len(E._ENTRY_PLANS) == 1
