@@ -10,6 +10,8 @@
 //                      variable_density_rows (:300-323)
 // All probability arithmetic is fp64. One CTA per slice (n <= 65536).
 
+#include <stdlib.h>
+
 #include "tt_block.cuh"
 
 #define SMP_NT 256
@@ -315,7 +317,7 @@ static BigDrawScratch big_layout(int n) {
   const int nb = (n + SMP_NT * BIG_IPT - 1) / (SMP_NT * BIG_IPT);
   size_t o = 0;
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-  s.cdf = o;   o = al(o + sizeof(double) * (size_t)n);
+  s.cdf = o;   o = al(o + sizeof(double) * ((size_t)n + 1));
   s.part = o;  o = al(o + sizeof(double) * (size_t)nb);
   s.off = o;   o = al(o + sizeof(double) * ((size_t)nb + 1));
   s.flags = o; o = al(o + sizeof(int) * (size_t)n);
@@ -410,28 +412,69 @@ __global__ void big_exact_kernel(int n, int ndraw, const double* __restrict__ p,
                                  const uint64_t* __restrict__ pos, int* __restrict__ flags, const int* __restrict__ ctl) {
   if (ctl[0] == 0) return;
   const int tid = threadIdx.x, NT = blockDim.x;
-  if (tid == 0) {
-    double c = 0.0;
-    for (int i = 0; i < n; ++i) {
-      c += p[i];
-      cdf[i] = c;
+  // numpy's sequential cumsum: the block stages p through shared memory in chunks (coalesced), one
+  // thread runs the dependent fp64 add chain out of shared memory, the block writes the chunk back
+  constexpr int CH = 4096;
+  __shared__ double buf[CH];
+  __shared__ double carry;
+  if (tid == 0) carry = 0.0;
+  for (int base = 0; base < n; base += CH) {
+    const int cnt = min(CH, n - base);
+    for (int i = tid; i < cnt; i += NT) buf[i] = p[base + i];
+    __syncthreads();
+    if (tid == 0) {
+      double c = carry;
+      int i = 0;
+      for (; i + 8 <= cnt; i += 8) {  // 8 loads in flight, then the dependent adds (numpy's order)
+        double v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = buf[i + q];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          c += v[q];
+          v[q] = c;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) buf[i + q] = v[q];
+      }
+      for (; i < cnt; ++i) {
+        c += buf[i];
+        buf[i] = c;
+      }
+      carry = c;
     }
+    __syncthreads();
+    for (int i = tid; i < cnt; i += NT) cdf[base + i] = buf[i];
+    __syncthreads();
   }
-  __syncthreads();
-  const double last = cdf[n - 1];
-  __syncthreads();
-  for (int i = tid; i < n; i += NT) {
+  if (tid == 0) cdf[n] = carry;  // cdf[-1] for the normalisation pass
+}
+
+// exact fallback, part 2 (grid): cdf /= cdf[-1] (numpy's normalisation) and the flags cleared
+__global__ void big_exact_norm_kernel(int n, double* __restrict__ cdf, int* __restrict__ flags,
+                                      const int* __restrict__ ctl) {
+  if (ctl[0] == 0) return;
+  const double last = cdf[n];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     cdf[i] = cdf[i] / last;
     flags[i] = 0;
   }
-  __syncthreads();
-  for (int m = tid; m < ndraw; m += NT) {
+}
+
+// exact fallback, part 3 (grid): every draw redone against numpy's CDF, forced entries re-marked
+__global__ void big_exact_redo_kernel(int n, int ndraw, const double* __restrict__ cdf,
+                                      const int* __restrict__ forced, int nforced, uint64_t k0, uint64_t k1,
+                                      const uint64_t* __restrict__ pos, int* __restrict__ flags,
+                                      const int* __restrict__ ctl) {
+  if (ctl[0] == 0) return;
+  for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < ndraw + nforced; m += gridDim.x * blockDim.x) {
+    if (m >= ndraw) {
+      const int f = forced[m - ndraw];
+      if (f >= 0 && f < n) flags[f] = 1;
+      continue;
+    }
     const int idx = upper_bound_d(cdf, n, philox_uniform(k0, k1, pos[0] + (uint64_t)m));
     flags[idx < n ? idx : n - 1] = 1;
-  }
-  for (int m = tid; m < nforced; m += NT) {
-    const int f = forced[m];
-    if (f >= 0 && f < n) flags[f] = 1;
   }
 }
 
@@ -515,7 +558,9 @@ extern "C" int tt_draw_with_replacement_large(void* stream, int n, const double*
   const int nb = (n + SMP_NT * BIG_IPT - 1) / (SMP_NT * BIG_IPT);
   const int ndraw = k - nforced;
   // rounding bound of the parallel scan against numpy's sequential cumsum (relative to the total)
-  const double guard = 1e-12 * (1.0 + (double)n / 4096.0);
+  double guard = 1e-12 * (1.0 + (double)n / 4096.0);
+  if (const char* e = getenv("TT_DRAW_FORCE_EXACT"))  // test hook: every draw takes the exact path
+    if (e[0] == '1') guard = 4.0;
   big_scan_kernel<<<nb, SMP_NT, 0, st>>>(n, probs, cdf, part);
   big_offsets_kernel<<<1, SMP_NT, 0, st>>>(nb, part, off, ctl);
   {
@@ -525,7 +570,16 @@ extern "C" int tt_draw_with_replacement_large(void* stream, int n, const double*
     big_draw_kernel<<<blocks, 256, 0, st>>>(n, ndraw, cdf, off, nb, forced, nforced, key0, key1, pos, flags, ctl,
                                             guard);
   }
-  big_exact_kernel<<<1, SMP_NT, 0, st>>>(n, ndraw, probs, cdf, forced, nforced, key0, key1, pos, flags, ctl);
+  {  // exact fallback (each part exits at once unless a draw was ambiguous)
+    big_exact_kernel<<<1, SMP_NT, 0, st>>>(n, ndraw, probs, cdf, forced, nforced, key0, key1, pos, flags, ctl);
+    int nbk = (n + 255) / 256;
+    if (nbk > 1184) nbk = 1184;
+    big_exact_norm_kernel<<<nbk, 256, 0, st>>>(n, cdf, flags, ctl);
+    int rbk = (ndraw + nforced + 255) / 256;
+    if (rbk < 1) rbk = 1;
+    if (rbk > 1184) rbk = 1184;
+    big_exact_redo_kernel<<<rbk, 256, 0, st>>>(n, ndraw, cdf, forced, nforced, key0, key1, pos, flags, ctl);
+  }
   int* cpart = (int*)(sb + S.cpart);
   int* coff = (int*)(sb + S.coff);
   big_count_kernel<<<nb, SMP_NT, 0, st>>>(n, flags, cpart);

@@ -17,13 +17,16 @@ def _probs(n, seed):
     return p / p.sum()
 
 
+@pytest.mark.parametrize("force_exact", [False, True])
 @pytest.mark.parametrize("n,k,nforced", [(65536, 16384, 16), (40000, 3000, 0), (20000, 1, 1), (100000, 50000, 7)])
-def test_large_domain_draw_matches_numpy_choice(n, k, nforced):
+def test_large_domain_draw_matches_numpy_choice(n, k, nforced, force_exact, monkeypatch):
     """tt_draw_with_replacement_large == Generator(Philox(key)).choice(n, k - |forced|, p) U forced, bit for bit,
     and the stream position advances by the draws consumed (sampler.py:146-162)."""
     import torch
     from paper_1609_04104_b200 import _lib as L
 
+    if force_exact:  # every uniform counts as ambiguous: numpy's sequential cumsum path
+        monkeypatch.setenv("TT_DRAW_FORCE_EXACT", "1")
     p = _probs(n, n + k)
     rng = np.random.default_rng(5)
     forced = np.sort(rng.choice(n, nforced, replace=False)).astype(np.int64)
