@@ -376,11 +376,25 @@ TT_DEV double big_cdf(const double* cdf, const double* off, int i) {
   return cdf[i] + off[i / (SMP_NT * BIG_IPT)];
 }
 
-// draws: one uniform per thread, binary search on the (unnormalised) global CDF against u * total
+// Rounding bound for the ambiguity test, in normalised CDF units. numpy's value at index i is
+// c_i = fl(N_i / N_{n-1}) with N the sequential cumsum; to first order in u = 2^-53 and with x_i the
+// exact normalised prefix, |c_i - x_i| <= u x_i (i (1 - x_i) + n - i + 1) (N_i carries i roundings;
+// N_{n-1} continues the same chain, so only the n-1-i later roundings and the first-i roundings
+// weighted by 1 - x_i survive the ratio). Our two-level scan passes every term through at most
+// `depth` additions, so our normalised prefix is within 2 depth u of x_i (absolute, since every
+// partial sum is <= the total). 5% margin for second-order terms and x_i estimated by our value.
+TT_DEV double big_bound(int i, int n, double x, double depth_term) {
+  const double u = 1.1102230246251565e-16;
+  x = fmin(fmax(x, 0.0), 1.0);
+  return 1.05 * u * (x * ((double)i * (1.0 - x) + (double)(n - i) + 1.0) + depth_term);
+}
+
+// draws: one uniform per thread, binary search on the (unnormalised) global CDF against u * total;
+// a draw whose uniform lies within the rounding bound of either bucket edge raises ctl[0]
 __global__ void big_draw_kernel(int n, int ndraw, const double* __restrict__ cdf, const double* __restrict__ off,
                                 int nb, const int* __restrict__ forced, int nforced, uint64_t k0, uint64_t k1,
                                 const uint64_t* __restrict__ pos, int* __restrict__ flags, int* __restrict__ ctl,
-                                double guard) {
+                                double depth_term, double gscale) {
   const double total = off[nb];
   const uint64_t p0 = pos[0];
   int top = 1;
@@ -399,55 +413,77 @@ __global__ void big_draw_kernel(int n, int ndraw, const double* __restrict__ cdf
       if (cand < n && big_cdf(cdf, off, cand) <= ut) q = cand;
     }
     const int idx = min(q + 1, n - 1);
-    const double lo = idx > 0 ? big_cdf(cdf, off, idx - 1) / total : -1.0;
-    const double hi = idx < n - 1 ? big_cdf(cdf, off, idx) / total : 2.0;
-    if (u - lo <= guard || hi - u <= guard) ctl[0] = 1;
+    bool amb = false;
+    if (idx > 0) {  // numpy must also see c_{idx-1} <= u
+      const double lo = big_cdf(cdf, off, idx - 1) / total;
+      amb |= u - lo <= gscale * big_bound(idx - 1, n, lo, depth_term);
+    }
+    if (idx < n - 1) {  // ... and c_idx > u (c_{n-1} == 1 exactly)
+      const double hi = big_cdf(cdf, off, idx) / total;
+      amb |= hi - u <= gscale * big_bound(idx, n, hi, depth_term);
+    }
+    if (amb) ctl[0] = 1;
     flags[idx] = 1;
   }
 }
 
-// exact fallback (runs only when a draw was ambiguous): numpy's sequential cumsum, cdf /= cdf[-1], redo
-__global__ void big_exact_kernel(int n, int ndraw, const double* __restrict__ p, double* __restrict__ cdf,
-                                 const int* __restrict__ forced, int nforced, uint64_t k0, uint64_t k1,
-                                 const uint64_t* __restrict__ pos, int* __restrict__ flags, const int* __restrict__ ctl) {
+// exact fallback (runs only when a draw was ambiguous), part 1: numpy's sequential cumsum. The chain
+// of dependent fp64 adds is inherently serial (8 cycles each); thread 0 runs it out of shared memory
+// and stores its results straight to global memory while warps 1.. stage the next chunk into the
+// other buffer, so the chain never waits on a load. cdf[n] = cdf[-1] for the normalisation pass.
+__global__ void __launch_bounds__(SMP_NT) big_exact_kernel(int n, const double* __restrict__ p,
+                                                           double* __restrict__ cdf, const int* __restrict__ ctl) {
   if (ctl[0] == 0) return;
-  const int tid = threadIdx.x, NT = blockDim.x;
-  // numpy's sequential cumsum: the block stages p through shared memory in chunks (coalesced), one
-  // thread runs the dependent fp64 add chain out of shared memory, the block writes the chunk back
-  constexpr int CH = 4096;
-  __shared__ double buf[CH];
-  __shared__ double carry;
-  if (tid == 0) carry = 0.0;
-  for (int base = 0; base < n; base += CH) {
-    const int cnt = min(CH, n - base);
-    for (int i = tid; i < cnt; i += NT) buf[i] = p[base + i];
-    __syncthreads();
-    if (tid == 0) {
-      double c = carry;
+  constexpr int CH = 2048;
+  __shared__ __align__(16) double buf[2][CH];
+  const int tid = threadIdx.x;
+  const int nch = (n + CH - 1) / CH;
+  auto stage = [&](int c) {  // warps 1.. load chunk c
+    const int base = c * CH, cnt = min(CH, n - base);
+    for (int i = tid - 32; i < cnt; i += SMP_NT - 32) buf[c & 1][i] = p[base + i];
+  };
+  if (tid >= 32) stage(0);
+  __syncthreads();
+  double c = 0.0;
+  for (int ch = 0; ch < nch; ++ch) {
+    if (tid >= 32) {
+      if (ch + 1 < nch) stage(ch + 1);
+    } else if (tid == 0) {
+      const double* b = buf[ch & 1];
+      double* out = cdf + (size_t)ch * CH;
+      const int cnt = min(CH, n - ch * CH);
       int i = 0;
-      for (; i + 8 <= cnt; i += 8) {  // 8 loads in flight, then the dependent adds (numpy's order)
-        double v[8];
+      constexpr int U = 16;
+      double v[U], w[U];  // register double buffer: the next U operands load under the current adds
+      auto ld = [&](double* r, int at) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = buf[i + q];
+        for (int q = 0; q < U; q += 2) {
+          const double2 t = *reinterpret_cast<const double2*>(b + min(at + q, CH - 2));
+          r[q] = t.x;
+          r[q + 1] = t.y;
+        }
+      };
+      ld(v, 0);
+      for (; i + U <= cnt; i += U) {
+        ld(w, i + U);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          c += v[q];
+        for (int q = 0; q < U; ++q) {
+          c += v[q];  // numpy's order
           v[q] = c;
         }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) buf[i + q] = v[q];
+        for (int q = 0; q < U; q += 2) *reinterpret_cast<double2*>(out + i + q) = make_double2(v[q], v[q + 1]);
+#pragma unroll
+        for (int q = 0; q < U; ++q) v[q] = w[q];
       }
       for (; i < cnt; ++i) {
-        c += buf[i];
-        buf[i] = c;
+        c += b[i];
+        out[i] = c;
       }
-      carry = c;
     }
     __syncthreads();
-    for (int i = tid; i < cnt; i += NT) cdf[base + i] = buf[i];
-    __syncthreads();
   }
-  if (tid == 0) cdf[n] = carry;  // cdf[-1] for the normalisation pass
+  if (tid == 0) cdf[n] = c;
 }
 
 // exact fallback, part 2 (grid): cdf /= cdf[-1] (numpy's normalisation) and the flags cleared
@@ -557,10 +593,13 @@ extern "C" int tt_draw_with_replacement_large(void* stream, int n, const double*
   int* ctl = (int*)(sb + S.ctl);
   const int nb = (n + SMP_NT * BIG_IPT - 1) / (SMP_NT * BIG_IPT);
   const int ndraw = k - nforced;
-  // rounding bound of the parallel scan against numpy's sequential cumsum (relative to the total)
-  double guard = 1e-12 * (1.0 + (double)n / 4096.0);
+  // addition depth of the two-level scan: thread chunk, warp shuffle scan, warp totals, x - v, block
+  // offsets (per-thread chunk + the same block scan), final cdf + off; generous
+  const double depth = 2.0 * BIG_IPT + 2.0 * (5 + SMP_NT / 32 + 2) + (double)((nb + SMP_NT - 1) / SMP_NT) + 8.0;
+  const double depth_term = 2.0 * depth + 8.0;
+  double gscale = 1.0;
   if (const char* e = getenv("TT_DRAW_FORCE_EXACT"))  // test hook: every draw takes the exact path
-    if (e[0] == '1') guard = 4.0;
+    if (e[0] == '1') gscale = 1e300;
   big_scan_kernel<<<nb, SMP_NT, 0, st>>>(n, probs, cdf, part);
   big_offsets_kernel<<<1, SMP_NT, 0, st>>>(nb, part, off, ctl);
   {
@@ -568,10 +607,10 @@ extern "C" int tt_draw_with_replacement_large(void* stream, int n, const double*
     if (blocks < 1) blocks = 1;
     if (blocks > 1184) blocks = 1184;
     big_draw_kernel<<<blocks, 256, 0, st>>>(n, ndraw, cdf, off, nb, forced, nforced, key0, key1, pos, flags, ctl,
-                                            guard);
+                                            depth_term, gscale);
   }
   {  // exact fallback (each part exits at once unless a draw was ambiguous)
-    big_exact_kernel<<<1, SMP_NT, 0, st>>>(n, ndraw, probs, cdf, forced, nforced, key0, key1, pos, flags, ctl);
+    big_exact_kernel<<<1, SMP_NT, 0, st>>>(n, probs, cdf, ctl);
     int nbk = (n + 255) / 256;
     if (nbk > 1184) nbk = 1184;
     big_exact_norm_kernel<<<nbk, 256, 0, st>>>(n, cdf, flags, ctl);
