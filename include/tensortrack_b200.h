@@ -245,6 +245,55 @@ int tt_reconstruct(void* stream, int frames, int nx, int ny, int rank, const flo
                    const float* gamma, float* x_out);
 /* rebalance (core.py:138-166) in place on [nslices][n][rank] factor pairs. */
 int tt_rebalance(void* stream, int nslices, int nx, int ny, int rank, float* a, float* b, int32_t* status);
+
+/* Per-patch independent trackers (experiment._run_tracking_patched, experiment.py:332-441;
+ * mri.PatchGrid / patch_partition / patch_assemble, mri.py:48-177). The nx x ny frame is tiled
+ * row-major into (nx/pn1) x (ny/pn2) patches of pn1 x pn2; each is a rank-`rank` EntryMask tracker
+ * (track_step, tracker.py:367-411) on its entries in local coordinates.
+ *
+ * tt_patch_bin: patch_batches' stable filter (experiment.py:352-370) for `frames` frames at once:
+ *   entries [frames][lmax][2] global (i, j) with counts [frames] (measurement order), frame_data
+ *   [frames][nx][ny] complex64 (pre-noised truth) -> per (frame, patch) lists in measurement order:
+ *   pidx [frames][npatch][pn1*pn2] local flat index i*pn2 + j, py [...] complex64 values,
+ *   pcnt [frames][npatch]. Out-of-range entries -> TT_ST_BADROW, overflow -> TT_ST_OVERFLOW in
+ *   status[0].
+ * tt_track_patches: one CTA per patch runs the schedule's steps (frame indices into the binned
+ *   table) in order on patches [patch0, patch0 + npatch_local); factors a [npatch_local][pn1][rank],
+ *   b [npatch_local][pn2][rank] complex64 (the EntryMask factors), t / alpha_bar [npatch_local]
+ *   in/out. Per step outputs [nsteps][npatch_local](...) when non-NULL. With `project` != 0 the
+ *   factors are not updated: each scheduled frame's gamma is the ridge solve on the current
+ *   subspace (experiment.py:419-431) and, with recon_out [frames][nx][ny], the patch tile
+ *   A diag(gamma) B^T is written into the assembled frame (patch_assemble). Ranks up to 16; the
+ *   patch must fit one CTA's shared memory (tt_patches_smem_bytes) -> else TT_EUNSUPPORTED. */
+typedef struct tt_patches_args {
+  int32_t nx, ny, pn1, pn2, rank;
+  int32_t patch0, npatch_local;
+  int32_t frames;
+  const int32_t* pidx;
+  const float* py;
+  const int32_t* pcnt;
+  int32_t nsteps;
+  const int32_t* sched;       /* [nsteps] device frame indices */
+  float* a;
+  float* b;
+  int64_t* t;
+  double* alpha_bar;
+  double lam;
+  int32_t step_mode;          /* 0 Fixed(mu), 1 HessianBound(c_floor, c_cap) */
+  double mu, c_floor, c_cap;
+  int32_t project;
+  float* gamma_out;           /* [nsteps][npatch_local][rank] */
+  double* cost_out;           /* [nsteps][npatch_local] */
+  double* mu_out;             /* [nsteps][npatch_local] */
+  float* resid_out;           /* [nsteps][npatch_local][pn1*pn2], measurement order */
+  float* recon_out;           /* project: [frames][nx][ny] */
+  int32_t* status;            /* [npatch_local] OR-ed TT_ST_* bits */
+} tt_patches_args;
+size_t tt_patches_smem_bytes(int pn1, int pn2, int rank);
+int tt_patch_bin(void* stream, int nx, int ny, int pn1, int pn2, int frames, int lmax, const float* frame_data,
+                 const int32_t* entries, const int32_t* counts, int32_t* pidx, float* py, int32_t* pcnt,
+                 int32_t* status);
+int tt_track_patches(void* stream, const tt_patches_args* a);
 /* solve_gamma (tracker.py:139-156) for a dense complex128 Phi [L][R]:
  * (Phi^H Phi + lam I)^-1 Phi^H y in fp64 (LDL^H); gamma_out complex128 [R].
  * scratch: tt_solve_scratch_bytes(R). */

@@ -587,3 +587,105 @@ def warm_up(kspace_warm, A, B, lam, step, epochs, t0=1):
         out = online_run(kspace_warm, A, B, lam, step, {"kind": "static", "rows": rows}, t0=t, alpha_bar=ab)
         A, B, t, ab, _ = out["final"]
     return A, B, t, ab
+
+
+# ---------------------------------------------------------------------------
+# per-patch independent trackers (experiment._run_tracking_patched, experiment.py:332-441;
+# mri.PatchGrid / patch_partition / patch_assemble, mri.py:48-177)
+# ---------------------------------------------------------------------------
+def full_entries(shape):
+    """All (i, j) of a frame, row-major (experiment.py:139-141)."""
+    g = np.meshgrid(*[np.arange(n, dtype=np.int64) for n in shape], indexing="ij")
+    return np.stack([x.ravel() for x in g], axis=1)
+
+
+def patch_split(entries, values, N1, N2, n1, n2):
+    """patch_batches' filter (experiment.py:352-370): for patch (p, q) in row-major order, the
+    entries inside it in measurement order, shifted to local coordinates, with their values."""
+    entries = np.asarray(entries, dtype=np.int64).reshape(-1, 2)
+    values = np.asarray(values)
+    out = []
+    for p in range(N1 // n1):
+        for q in range(N2 // n2):
+            inside = ((entries[:, 0] >= p * n1) & (entries[:, 0] < (p + 1) * n1)
+                      & (entries[:, 1] >= q * n2) & (entries[:, 1] < (q + 1) * n2))
+            out.append((entries[inside] - np.array([p * n1, q * n2]), values[inside]))
+    return out
+
+
+def patch_assemble(tiles, N1, N2, n1, n2):
+    """Inverse of the row-major tiling (mri.py:165-177)."""
+    out = np.empty((N1, N2), dtype=np.result_type(*[np.asarray(t).dtype for t in tiles]))
+    k2 = N2 // n2
+    for k, tile in enumerate(tiles):
+        p, q = divmod(k, k2)
+        out[p * n1:(p + 1) * n1, q * n2:(q + 1) * n2] = tile
+    return out
+
+
+def patched_run(frames, A0s, B0s, lam, step, n1, n2, entries, warm_n, warm_epochs, epochs, rng=None,
+                reshuffle=False, power=True):
+    """_run_tracking_patched (experiment.py:332-441) on pre-noised frames (frames leading,
+    (T, N1, N2)): one EntryMask tracker of rank rho per n1 x n2 patch, started from (A0s[p], B0s[p]);
+    ``entries[t]`` the frame's global (i, j) list (the warm frames' are the full frame). Warm-up:
+    ``warm_epochs`` passes over the warm frames, every patch rebalanced at the start of each pass
+    after the first; then ``epochs`` passes over the remaining frames (all patches rebalanced
+    between passes, order re-drawn by ``rng.permutation`` when ``reshuffle``); then every frame,
+    warm ones included, is re-projected onto each patch's final subspace (ridge solve) and the tiles
+    assembled. Returns the trace (per main step: gamma and residual concatenated over patches, cost
+    summed, patch 0's step size and the pre-step t, as StepReport carries it, tracker.py:409), the
+    reconstruction (T, N1, N2) and the final factors. ``power`` picks the reference's power method for
+    the HessianBound step (else the closed form the device uses)."""
+    frames = np.asarray(frames)
+    T, N1, N2 = frames.shape
+    npatch = (N1 // n1) * (N2 // n2)
+    states = [[np.asarray(A0s[p], np.complex128), np.asarray(B0s[p], np.complex128), 1, 0.0] for p in range(npatch)]
+    batches = [patch_split(entries[t], np.asarray(frames[t], np.complex128)[tuple(np.asarray(entries[t]).reshape(-1, 2).T)],
+                           N1, N2, n1, n2) for t in range(T)]
+
+    def step_patch(p, t):
+        A, B, tt, ab = states[p]
+        idx, y = batches[t][p]
+        rep = track_step(A, B, tt, ab, y, idx, "entry", lam, step, power=power)
+        states[p] = [rep["A"], rep["B"], rep["t"], rep["alpha_bar"]]
+        return rep
+
+    def rebalance_patch(p):
+        A, B = rebalance(states[p][0], states[p][1])
+        states[p][0], states[p][1] = A, B
+
+    for epoch in range(warm_epochs):
+        for t in range(warm_n):
+            for p in range(npatch):
+                if epoch > 0 and t == 0:
+                    rebalance_patch(p)
+                step_patch(p, t)
+    trace, orders = [], []
+    for epoch in range(epochs):
+        if epoch > 0:
+            for p in range(npatch):
+                rebalance_patch(p)
+        order = list(range(warm_n, T))
+        if reshuffle and epoch > 0:
+            order = [warm_n + int(i) for i in rng.permutation(T - warm_n)]
+        orders.append(order)
+        for t in order:
+            reps = [step_patch(p, t) for p in range(npatch)]
+            trace.append(dict(gamma=np.concatenate([r["gamma"] for r in reps]),
+                              residual=np.concatenate([r["residual"] for r in reps]),
+                              cost=float(sum(r["cost"] for r in reps)), mu=reps[0]["mu"], t=reps[0]["t"] - 1,
+                              patch_gamma=np.stack([r["gamma"] for r in reps]),
+                              patch_cost=np.array([r["cost"] for r in reps])))
+    recon = np.zeros((T, N1, N2), np.complex128)
+    gammas = np.zeros((T, npatch, A0s[0].shape[1]), np.complex128)
+    for t in range(T):
+        tiles = []
+        for p in range(npatch):
+            idx, y = batches[t][p]
+            A, B = states[p][0], states[p][1]
+            g = ridge_svd(phi_matrix(A, B, idx, "entry"), y, lam)
+            gammas[t, p] = g
+            tiles.append(synth(A, B, g))
+        recon[t] = patch_assemble(tiles, N1, N2, n1, n2)
+    return dict(trace=trace, orders=orders, recon=recon, gamma=gammas,
+                final=[(s[0], s[1], s[2], s[3]) for s in states])

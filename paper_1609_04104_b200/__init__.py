@@ -11,7 +11,7 @@ anywhere, but every compute call needs a CUDA device and the built library.
 from .core import TensorSubspace, rebalance, synthesize_slice
 from .engine import (BatchResult, EntryEngine, Informative, InformativeEntries, LocalShardedEngine, OnlineEngine,
                      OnlineResult, RowShardedEngine, StaticEntries, StaticRows, run_batch, run_online, warm_up)
-from .mri import FrameEstimate, interp_track_step, reconstruct_frame
+from .mri import FrameEstimate, PatchGrid, interp_track_step, patch_assemble, patch_partition, reconstruct_frame
 from .observation import (
     EntryMask,
     FourierMask,
@@ -51,6 +51,7 @@ from .tracker import (
 )
 from ._lib import NumericalError
 from .acquisition import StreamingProvider, measure, project
+from .patches import PatchedResult, draw_frame_entries, full_entries, init_patch_factors, run_tracking_patched
 from .cten import CtenFormatError, read_cten, read_cten_tensor, write_cten
 from .reports import (MetricRow, online_budget_rows, online_mask_rows, write_budget_csv, write_mask_csv,
                       write_metrics_csv, write_trace_csv)
@@ -63,7 +64,8 @@ __all__ = [
     "run", "solve_gamma", "track_step", "factor_gradient", "hessian_bound", "instantaneous_cost",
     "SamplePlan", "SamplingDistribution", "adaptive_step", "draw_samples", "entry_scores",
     "expected_count_trace", "expected_sample_count", "row_scores",
-    "FrameEstimate", "interp_track_step", "reconstruct_frame",
+    "FrameEstimate", "interp_track_step", "reconstruct_frame", "PatchGrid", "patch_partition", "patch_assemble",
+    "PatchedResult", "run_tracking_patched", "init_patch_factors", "draw_frame_entries", "full_entries",
     "OnlineEngine", "OnlineResult", "StaticRows", "Informative", "run_online", "warm_up", "RowShardedEngine",
     "EntryEngine", "InformativeEntries", "StaticEntries", "run_batch", "BatchResult", "LocalShardedEngine",
     "NumericalError", "StreamingProvider", "measure", "project",

@@ -61,6 +61,18 @@ class EntriesArgs(C.Structure):
     ]
 
 
+class PatchesArgs(C.Structure):
+    _fields_ = [
+        ("nx", _i32), ("ny", _i32), ("pn1", _i32), ("pn2", _i32), ("rank", _i32),
+        ("patch0", _i32), ("npatch_local", _i32), ("frames", _i32),
+        ("pidx", _p), ("py", _p), ("pcnt", _p), ("nsteps", _i32), ("sched", _p),
+        ("a", _p), ("b", _p), ("t", _p), ("alpha_bar", _p),
+        ("lam", _f64), ("step_mode", _i32), ("mu", _f64), ("c_floor", _f64), ("c_cap", _f64),
+        ("project", _i32), ("gamma_out", _p), ("cost_out", _p), ("mu_out", _p), ("resid_out", _p),
+        ("recon_out", _p), ("status", _p),
+    ]
+
+
 # (name, restype, argtypes) — every symbol declared in include/tensortrack_b200.h
 SIGNATURES = {
     "tt_version": (C.c_char_p, []),
@@ -93,6 +105,9 @@ SIGNATURES = {
     "tt_draw_without_replacement": (C.c_int, [_p, C.c_int, _p, C.c_int, _u64, _u64, _p, _p, _p]),
     "tt_reconstruct": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, C.c_int, _p, _p, _p, _p]),
     "tt_rebalance": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, C.c_int, _p, _p, _p]),
+    "tt_patches_smem_bytes": (C.c_size_t, [C.c_int, C.c_int, C.c_int]),
+    "tt_patch_bin": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _p, _p, _p, _p, _p, _p, _p]),
+    "tt_track_patches": (C.c_int, [_p, C.POINTER(PatchesArgs)]),
     "tt_solve_scratch_bytes": (C.c_size_t, [C.c_int, C.c_int]),
     "tt_solve_gamma": (C.c_int, [_p, C.c_int, C.c_int, _p, _p, _f64, _p, _p]),
 }
