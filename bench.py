@@ -59,6 +59,12 @@ CONFIGS = {
                 desc="config 2 with entry sampling (run_adaptive's entries mode): 256x256 complex64 cine "
                      "phantom, T=200, R=20, lambda=0.05, informative entries K=16384 (25% of nx*ny trials, "
                      "forced DC), beta=0.1, Philox draws, Fixed mu=0.01"),
+    "c2p": dict(n=256, R=4, patch=32, T=200, lam=0.05, period=20.0, vd=0.25, mu=0.01, slices=1, warm_n=5,
+                warm_epochs=20,
+                desc="per-patch trackers (experiment._run_tracking_patched): 256x256 complex64 cine phantom "
+                     "k-space, T=200, 8x8 grid of 32x32 patches with rank 4 each, lambda=0.05, variable-density "
+                     "rows 25% (Philox), Fixed mu=0.01, warm-up 5 full frames x 20 epochs, 1 epoch, "
+                     "re-projection of every frame"),
     "c4": dict(n=1024, R=32, T=256, lam=0.1, period=16.0, vd=0.125, mu=0.01, slices=1,
                desc="config 4: 1024x1024 complex64 cine phantom, T=256, R=32, lambda=0.1, variable-density rows "
                     "12.5% (128 rows/frame), Fixed mu=0.01 (single GPU, unsharded)"),
@@ -183,9 +189,52 @@ def measured_peaks():
 
 
 # ------------------------------------------------------------------ CPU oracle (reference arm / cpu_baseline)
+def patched_masks(cfg, T):
+    """Warm frames full, the rest variable-density rows (Philox stream 2024, the device VD draw)."""
+    import paper_1609_04104_b200 as tt
+
+    n = cfg["n"]
+    gen = np.random.Generator(np.random.Philox(key=2024))
+    warm = min(cfg["warm_n"], T)
+    full = tt.full_entries((n, n))
+    return [full] * warm + [tt.rows_to_entries(O_vd_rows(n, cfg["vd"], gen), n) for _ in range(T - warm)]
+
+
+def O_vd_rows(n, frac, gen):
+    from oracle import tt_oracle as O
+
+    return O.vd_rows(n, -1.0, frac, gen.random)
+
+
+def patched_init(cfg):
+    rng = np.random.default_rng(7)
+    k = cfg["n"] // cfg["patch"]
+    A, B = [], []
+    for _ in range(k * k):
+        for out in (A, B):
+            z = rng.standard_normal((cfg["patch"], cfg["R"])) + 1j * rng.standard_normal((cfg["patch"], cfg["R"]))
+            out.append(z / np.sqrt(2 * cfg["patch"]))
+    return np.stack(A), np.stack(B)
+
+
 def cpu_oracle_fps(cfg, frames, ks, A0, B0):
     from oracle import tt_oracle as O
 
+    if "patch" in cfg:  # streamed frames only (no warm-up), every patch stepped and re-projected
+        p = cfg["patch"]
+        masks = patched_masks(dict(cfg, warm_n=0), frames)
+        A0s, B0s = patched_init(cfg)
+        t0 = time.perf_counter()
+        O.patched_run(ks[:frames, 0], A0s, B0s, cfg["lam"], ("fixed", cfg["mu"]), p, p, masks, 0, 1, 1, power=False)
+        dt = time.perf_counter() - t0
+        return frames / dt, dt
+    if "entries" in cfg:
+        k = int(np.ceil(cfg["entries"] * cfg["n"] ** 2))
+        t0 = time.perf_counter()
+        O.online_run_entries(ks[:frames, 0], O.fft_cols(A0[0]), O.fft_cols(B0[0]), cfg["lam"], ("fixed", cfg["mu"]),
+                             {"kind": "informative", "k": k, "forced": [0], "beta": cfg["beta"], "key": (2024, 0)})
+        dt = time.perf_counter() - t0
+        return frames / dt, dt
     if "vd" in cfg:
         gen = np.random.Generator(np.random.Philox(key=2024))
         pol = {"kind": "static", "rows": [O.vd_rows(cfg["n"], -1.0, cfg["vd"], gen.random) for _ in range(frames)]}
@@ -336,6 +385,171 @@ def run_entries(args, cfg):
         "gpu_launches": None,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": None, "kernel": "entry frame chain (graph)",
+                     "bytes_per_frame": b_frame, "peak_kind": peak_kind},
+        "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_patched(args, cfg):
+    """Per-patch trackers (run_tracking_patched). A step is one whole patched run on
+    resident, binned inputs: the warm-up passes (one launch each, rebalanced between), the streamed
+    pass over the remaining frames, and the re-projection of every frame into the assembled
+    reconstructions. Replicas per rank (a frame's latency is one patch step, so splitting patches
+    across GPUs would not shorten it)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1609_04104_b200 as tt
+    from paper_1609_04104_b200 import patches as PT
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n, R, T, pch = cfg["n"], cfg["R"], cfg["T"], cfg["patch"]
+    warm_n, warm_ep = cfg["warm_n"], cfg["warm_epochs"]
+    grid = tt.PatchGrid((n, n), pch, pch, R)
+    ks_np, clean_np = make_data(cfg, [0])
+    masks = patched_masks(cfg, T)
+    A0s, B0s = patched_init(cfg)
+    ent, off = PT._entry_table(masks, (n, n), T)
+    cnt = np.diff(off)
+    fd = torch.from_numpy(ks_np[:, 0]).to(dev)
+    run = PT._PatchRun(grid, cfg["lam"], tt.Fixed(cfg["mu"]), fd, ent, off)
+    run.set_factors(A0s, B0s)
+    a0, b0 = run.a.clone(), run.b.clone()
+    npch = run.np
+    main = list(range(warm_n, T))
+    g = torch.empty((len(main), npch, R), dtype=torch.complex64, device=dev)
+    c = torch.empty((len(main), npch), dtype=torch.float64, device=dev)
+    m = torch.empty((len(main), npch), dtype=torch.float64, device=dev)
+    gp = torch.empty((T, npch, R), dtype=torch.complex64, device=dev)
+    rec = torch.empty((T, n, n), dtype=torch.complex64, device=dev)
+    warm_s = torch.arange(warm_n, dtype=torch.int32, device=dev)
+    main_s = torch.tensor(main, dtype=torch.int32, device=dev)
+    all_s = torch.arange(T, dtype=torch.int32, device=dev)
+    from paper_1609_04104_b200 import _lib as L
+
+    def launch(sd, nsteps, project=False, gamma=None, cost=None, mu=None, recon=None):
+        args_ = L.PatchesArgs(
+            nx=n, ny=n, pn1=pch, pn2=pch, rank=R, patch0=0, npatch_local=npch, frames=T, pidx=run.pidx.data_ptr(),
+            py=run.py.data_ptr(), pcnt=run.pcnt.data_ptr(), nsteps=nsteps, sched=sd.data_ptr(), a=run.a.data_ptr(),
+            b=run.b.data_ptr(), t=run.t.data_ptr(), alpha_bar=run.ab.data_ptr(), lam=run.lam, step_mode=run.mode,
+            mu=run.mu, c_floor=run.c_floor, c_cap=run.c_cap, project=int(project), gamma_out=L.ptr(gamma),
+            cost_out=L.ptr(cost), mu_out=L.ptr(mu), resid_out=None, recon_out=L.ptr(recon),
+            status=run.status.data_ptr())
+        L.check(L.lib().tt_track_patches(L.stream_ptr(), args_), "patch tracking")
+
+    stream = torch.cuda.current_stream()
+    ev_main = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    launches = [0]
+
+    def one_run(timed_main=None):
+        run.a.copy_(a0)
+        run.b.copy_(b0)
+        run.t.fill_(1)
+        run.ab.zero_()
+        launches[0] = 0
+        for e in range(warm_ep):
+            if e > 0:
+                run.rebalance()
+                launches[0] += 1
+            launch(warm_s, warm_n)
+            launches[0] += 1
+        if timed_main:
+            timed_main[0].record(stream)
+        launch(main_s, len(main), gamma=g, cost=c, mu=m)
+        if timed_main:
+            timed_main[1].record(stream)
+        launch(all_s, T, project=True, gamma=gp, recon=rec)
+        launches[0] += 2
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    for _ in range(args.warmup):
+        one_run()
+    torch.cuda.synchronize()
+    L.raise_status(int(run.status.max().item()) | int(run.bin_status.item()), "patched bench")
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    mains = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            one_run(mains[i])
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    main_ms = sum(a.elapsed_time(b) for a, b in mains)
+    tot = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    total_ms = float(tot[0])
+    value = T * world * args.steps / (total_ms / 1e3)
+    # the trackers work in the data domain (k-space): NRMSE against the clean frames' k-space
+    ck = np.fft.fft2(clean_np[:, 0], norm="ortho")
+    rh = rec.cpu().numpy()
+    nm = np.sum(np.abs(rh - ck) ** 2, axis=(1, 2)) / np.sum(np.abs(ck) ** 2, axis=(1, 2))
+    # dominant kernel = the streamed pass: per frame, every sampled entry's (index, value) read once,
+    # each patch's factors read + written, the per-step outputs (SURVEY §8d's model per patch)
+    L_main = float(cnt[warm_n:].mean()) if len(main) else 0.0
+    b_frame = 12 * L_main + npch * (16 * R * 2 * pch + 8 * R + 16)
+    hbm_peak, sm_max, peak_kind = measured_peaks()
+    achieved = b_frame * len(main) * args.steps / (main_ms / 1e3) / 1e9
+    e2e = None
+    if not args.no_e2e:
+        ks_pin = torch.from_numpy(ks_np[:, 0]).pin_memory()
+        res = None
+        for _ in range(2):
+            res = tt.run_tracking_patched(ks_pin, grid, cfg["lam"], tt.Fixed(cfg["mu"]), masks, warm_n=warm_n,
+                                          warm_epochs=warm_ep, A0s=A0s, B0s=B0s)
+        torch.cuda.synchronize()
+        t_e2e = []
+        for _ in range(max(1, args.steps)):
+            t0 = time.perf_counter()
+            res = tt.run_tracking_patched(ks_pin, grid, cfg["lam"], tt.Fixed(cfg["mu"]), masks, warm_n=warm_n,
+                                          warm_epochs=warm_ep, A0s=A0s, B0s=B0s)
+            torch.cuda.synchronize()
+            t_e2e.append(time.perf_counter() - t0)
+        et = torch.tensor([sum(t_e2e)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": T * world * len(t_e2e) / float(et[0]), "unit": "frames/s",
+               "h2d_bytes_per_step": int(ks_np[:, 0].nbytes + ent.nbytes + off.nbytes),
+               "d2h_bytes_per_step": int(res.recon.nbytes + res.gamma.nbytes + res.step_gamma.nbytes),
+               "call": "paper_1609_04104_b200.run_tracking_patched(pinned host frames, host masks) -> host recon"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        fr = min(T, 100)
+        fps, dt = cpu_oracle_fps(cfg, fr, ks_np, None, None)
+        cpu = {"value": fps, "unit": "frames/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"{fr} streamed frames x {npch} patch steps + re-projection ({dt:.1f} s), oracle port "
+                         "of _run_tracking_patched (no warm-up)"}
+    if world > 1:
+        dist.destroy_process_group()
+    if rank != 0:
+        return 0
+    line = {
+        "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c64", "data": "synthetic",
+        "config": {"workload": cfg["desc"], "frames_per_step": T, "patches": npch, "patch": [pch, pch], "rank": R,
+                   "warm_steps": warm_n * warm_ep, "streamed_frames": len(main),
+                   "streamed_ms_per_frame": main_ms / args.steps / max(1, len(main)),
+                   "l2": "flushed between steps (256 MB write)", "parallelism": f"replicas x{world}",
+                   "nrmse_last": float(np.sqrt(nm[-1]))},
+        "gpu_launches": launches[0],
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": None, "kernel": "patch_track_kernel (streamed pass)",
                      "bytes_per_frame": b_frame, "peak_kind": peak_kind},
         "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
     }
@@ -650,6 +864,8 @@ def main():
         return run_row_sharded(args, cfg)
     if "entries" in cfg:
         return run_entries(args, cfg)
+    if "patch" in cfg:
+        return run_patched(args, cfg)
     return run_ours(args, cfg)
 
 

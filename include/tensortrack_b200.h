@@ -252,7 +252,8 @@ int tt_rebalance(void* stream, int nslices, int nx, int ny, int rank, float* a, 
  * (track_step, tracker.py:367-411) on its entries in local coordinates.
  *
  * tt_patch_bin: patch_batches' stable filter (experiment.py:352-370) for `frames` frames at once:
- *   entries [frames][lmax][2] global (i, j) with counts [frames] (measurement order), frame_data
+ *   entries [total][2] global (i, j), frame f's list at [offsets[f], offsets[f+1]) in measurement
+ *   order (offsets [frames + 1], int64), frame_data
  *   [frames][nx][ny] complex64 (pre-noised truth) -> per (frame, patch) lists in measurement order:
  *   pidx [frames][npatch][pn1*pn2] local flat index i*pn2 + j, py [...] complex64 values,
  *   pcnt [frames][npatch]. Out-of-range entries -> TT_ST_BADROW, overflow -> TT_ST_OVERFLOW in
@@ -290,8 +291,8 @@ typedef struct tt_patches_args {
   int32_t* status;            /* [npatch_local] OR-ed TT_ST_* bits */
 } tt_patches_args;
 size_t tt_patches_smem_bytes(int pn1, int pn2, int rank);
-int tt_patch_bin(void* stream, int nx, int ny, int pn1, int pn2, int frames, int lmax, const float* frame_data,
-                 const int32_t* entries, const int32_t* counts, int32_t* pidx, float* py, int32_t* pcnt,
+int tt_patch_bin(void* stream, int nx, int ny, int pn1, int pn2, int frames, const float* frame_data,
+                 const int32_t* entries, const int64_t* offsets, int32_t* pidx, float* py, int32_t* pcnt,
                  int32_t* status);
 int tt_track_patches(void* stream, const tt_patches_args* a);
 /* solve_gamma (tracker.py:139-156) for a dense complex128 Phi [L][R]:

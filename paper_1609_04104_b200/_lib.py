@@ -106,7 +106,7 @@ SIGNATURES = {
     "tt_reconstruct": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, C.c_int, _p, _p, _p, _p]),
     "tt_rebalance": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, C.c_int, _p, _p, _p]),
     "tt_patches_smem_bytes": (C.c_size_t, [C.c_int, C.c_int, C.c_int]),
-    "tt_patch_bin": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _p, _p, _p, _p, _p, _p, _p]),
+    "tt_patch_bin": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _p, _p, _p, _p, _p, _p, _p]),
     "tt_track_patches": (C.c_int, [_p, C.POINTER(PatchesArgs)]),
     "tt_solve_scratch_bytes": (C.c_size_t, [C.c_int, C.c_int]),
     "tt_solve_gamma": (C.c_int, [_p, C.c_int, C.c_int, _p, _p, _f64, _p, _p]),

@@ -65,9 +65,9 @@ TT_DEV double warp_max_d(double v) {
 // the same patch rank themselves with __match_any_sync; the warps then take their per-patch base
 // counts in warp order. Out-of-range entries raise TT_ST_BADROW, more entries than a patch holds
 // (only possible with duplicates) TT_ST_OVERFLOW.
-__global__ void __launch_bounds__(PT_NT) patch_bin_kernel(int nx, int ny, int n1, int n2, int lmax,
+__global__ void __launch_bounds__(PT_NT) patch_bin_kernel(int nx, int ny, int n1, int n2,
                                                           const float2* __restrict__ frames,
-                                                          const int2* __restrict__ ent, const int32_t* __restrict__ cnt,
+                                                          const int2* __restrict__ ent, const int64_t* __restrict__ off,
                                                           int32_t* __restrict__ pidx, float2* __restrict__ py,
                                                           int32_t* __restrict__ pcnt, int32_t* __restrict__ status) {
   extern __shared__ int pc[];
@@ -75,8 +75,9 @@ __global__ void __launch_bounds__(PT_NT) patch_bin_kernel(int nx, int ny, int n1
   const int k2 = ny / n2, np = (nx / n1) * k2, cap = n1 * n2;
   for (int q = tid; q < np; q += PT_NT) pc[q] = 0;
   __syncthreads();
-  const int Lf = min(cnt[f], lmax);
-  const int2* e = ent + (size_t)f * lmax;
+  const long long l0 = off[f], l1 = off[f + 1];
+  const int Lf = l1 > l0 ? (int)min(l1 - l0, (long long)INT32_MAX) : 0;
+  const int2* e = ent + l0;
   int bad = 0;
   for (int base = 0; base < Lf; base += PT_NT) {
     const int l = base + tid;
@@ -377,22 +378,21 @@ extern "C" size_t tt_patches_smem_bytes(int pn1, int pn2, int rank) {
   return pt_layout(pn1, pn2, rank).total;
 }
 
-extern "C" int tt_patch_bin(void* stream, int nx, int ny, int pn1, int pn2, int frames, int lmax, const float* frame_data,
-                            const int32_t* entries, const int32_t* counts, int32_t* pidx, float* py, int32_t* pcnt,
+extern "C" int tt_patch_bin(void* stream, int nx, int ny, int pn1, int pn2, int frames, const float* frame_data,
+                            const int32_t* entries, const int64_t* offsets, int32_t* pidx, float* py, int32_t* pcnt,
                             int32_t* status) {
-  if (nx < 1 || ny < 1 || pn1 < 1 || pn2 < 1 || frames < 0 || lmax < 0)
-    return tt_fail(TT_EINVAL, "tt_patch_bin: bad sizes");
+  if (nx < 1 || ny < 1 || pn1 < 1 || pn2 < 1 || frames < 0) return tt_fail(TT_EINVAL, "tt_patch_bin: bad sizes");
   if (nx % pn1 || ny % pn2) return tt_fail(TT_EINVAL, "patch size does not tile the frame");
   if (frames == 0) return TT_OK;
-  if (!frame_data || !counts || !pidx || !py || !pcnt || !status || (lmax > 0 && !entries))
+  if (!frame_data || !entries || !offsets || !pidx || !py || !pcnt || !status)
     return tt_fail(TT_EINVAL, "tt_patch_bin: null pointer");
   const size_t np = (size_t)(nx / pn1) * (ny / pn2);
   const size_t sm = sizeof(int) * np;
   if (sm > 200 * 1024) return tt_fail(TT_EUNSUPPORTED, "too many patches for the binning kernel");
   if (sm > 48 * 1024) TT_CUDA_TRY(cudaFuncSetAttribute(patch_bin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  patch_bin_kernel<<<frames, PT_NT, sm, (cudaStream_t)stream>>>(nx, ny, pn1, pn2, lmax, (const float2*)frame_data,
-                                                                 (const int2*)entries, counts, pidx, (float2*)py, pcnt,
-                                                                 status);
+  patch_bin_kernel<<<frames, PT_NT, sm, (cudaStream_t)stream>>>(nx, ny, pn1, pn2, (const float2*)frame_data,
+                                                                 (const int2*)entries, (const int64_t*)offsets, pidx,
+                                                                 (float2*)py, pcnt, status);
   TT_CUDA_TRY(cudaGetLastError());
   return TT_OK;
 }

@@ -107,7 +107,7 @@ def _step_params(step):
 class _PatchRun:
     """Device state of one patched run: binned data, factors, and the launch helper."""
 
-    def __init__(self, grid: PatchGrid, lam, step, frames_dev, entries, counts):
+    def __init__(self, grid: PatchGrid, lam, step, frames_dev, entries, offsets):
         self.grid = grid
         self.lam = float(lam)
         self.mode, self.mu, self.c_floor, self.c_cap = _step_params(step)
@@ -118,16 +118,16 @@ class _PatchRun:
         self.cap = grid.n1 * grid.n2
         self.frames = frames_dev
         ent = torch.from_numpy(entries).to(self.dev, non_blocking=True)
-        cnt = torch.from_numpy(counts).to(self.dev, non_blocking=True)
+        off = torch.from_numpy(offsets).to(self.dev, non_blocking=True)
         self.pidx = torch.empty((T, self.np, self.cap), dtype=torch.int32, device=self.dev)
         self.py = torch.empty((T, self.np, self.cap), dtype=torch.complex64, device=self.dev)
         self.pcnt = torch.empty((T, self.np), dtype=torch.int32, device=self.dev)
         self.bin_status = torch.zeros(1, dtype=torch.int32, device=self.dev)
-        L.check(L.lib().tt_patch_bin(L.stream_ptr(), N1, N2, grid.n1, grid.n2, T, entries.shape[1],
-                                     frames_dev.data_ptr(), ent.data_ptr(), cnt.data_ptr(), self.pidx.data_ptr(),
+        L.check(L.lib().tt_patch_bin(L.stream_ptr(), N1, N2, grid.n1, grid.n2, T,
+                                     frames_dev.data_ptr(), ent.data_ptr(), off.data_ptr(), self.pidx.data_ptr(),
                                      self.py.data_ptr(), self.pcnt.data_ptr(), self.bin_status.data_ptr()),
                 "patch binning")
-        self._keep = (ent, cnt)
+        self._keep = (ent, off)
         self.status = torch.zeros(self.np, dtype=torch.int32, device=self.dev)
 
     def set_factors(self, A0s, B0s, t0=1):
@@ -155,14 +155,14 @@ class _PatchRun:
 
 
 def _entry_table(masks, shape, T):
-    L_ = max([len(m) for m in masks] + [1])
-    tab = np.full((T, L_, 2), -1, dtype=np.int32)
-    cnt = np.zeros(T, dtype=np.int32)
+    """Masks -> the compact device layout: concatenated (i, j) int32 pairs and int64 frame offsets."""
+    cnt = np.array([len(np.asarray(m).reshape(-1, 2)) for m in masks], dtype=np.int64)
+    off = np.zeros(T + 1, dtype=np.int64)
+    np.cumsum(cnt, out=off[1:])
+    ent = np.empty((max(int(off[-1]), 1), 2), dtype=np.int32)
     for t, m in enumerate(masks):
-        m = np.asarray(m, dtype=np.int64).reshape(-1, 2)
-        tab[t, :len(m)] = m
-        cnt[t] = len(m)
-    return tab, cnt
+        ent[off[t]:off[t + 1]] = np.asarray(m, dtype=np.int64).reshape(-1, 2)
+    return ent, off
 
 
 def run_tracking_patched(frames, grid: PatchGrid, lam, step, masks, warm_n=0, warm_epochs=1, epochs=1, rng=None,
@@ -196,10 +196,10 @@ def run_tracking_patched(frames, grid: PatchGrid, lam, step, masks, warm_n=0, wa
     if reshuffle and epochs > 1 and rng is None:
         raise ValueError("rng is required for reshuffling")
     dev = L.device()
-    fd = src.to(torch.complex64)
-    fd = (fd.pin_memory() if not fd.is_cuda else fd).to(dev, non_blocking=True).contiguous()
-    tab, cnt = _entry_table(masks, grid.frame_shape, T)
-    run = _PatchRun(grid, lam, step, fd, tab, cnt)
+    # pinned (or device) input uploads asynchronously; a pageable one is copied as is
+    fd = src.to(torch.complex64).to(dev, non_blocking=True).contiguous()
+    ent, off = _entry_table(masks, grid.frame_shape, T)
+    run = _PatchRun(grid, lam, step, fd, ent, off)
     run.set_factors(A0s, B0s)
     npch, R = run.np, grid.rho
 
@@ -242,22 +242,33 @@ def run_tracking_patched(frames, grid: PatchGrid, lam, step, masks, warm_n=0, wa
         ct = clean if isinstance(clean, torch.Tensor) else torch.from_numpy(np.asarray(clean))
         ref = (ct.permute(2, 0, 1) if frames_last else ct).to(dev, torch.complex64)
     err = (recon - ref).abs().pow(2).sum(dim=(1, 2)).double() / ref.abs().pow(2).sum(dim=(1, 2)).double()
-    st = int(run.status.max().item()) | int(run.bin_status.item())
-    L.raise_status(st, "patched tracking")
+    # asynchronous downloads into pinned memory, one synchronisation
+    pinned = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True)  # noqa: E731
+    dl = {"recon": recon, "gamma": gam, "err": err, "pcnt": run.pcnt, "A": run.a, "B": run.b, "t": run.t[:1],
+          "st": torch.stack([run.status.max(), run.bin_status[0]])}
+    if cost_s:
+        dl.update(cost=torch.cat(cost_s), mu=torch.cat(mu_s), sg=torch.cat(gam_s))
+    if keep_residual and res_s:
+        dl["resid"] = torch.cat([x for x in res_s if x is not None])
+    host = {k: pinned(v) for k, v in dl.items()}
+    for k, v in dl.items():
+        host[k].copy_(v, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    h = {k: v.numpy() for k, v in host.items()}
+    L.raise_status(int(h["st"][0]) | int(h["st"][1]), "patched tracking")
 
-    pcnt = run.pcnt.cpu().numpy()
-    cost = torch.cat(cost_s).cpu().numpy() if cost_s else np.zeros((0, npch))
-    mu = torch.cat(mu_s).cpu().numpy() if mu_s else np.zeros((0, npch))
-    sg = torch.cat(gam_s).cpu().numpy().reshape(-1, npch * R) if gam_s else np.zeros((0, npch * R), np.complex64)
+    pcnt = h["pcnt"]
+    cost = h["cost"] if cost_s else np.zeros((0, npch))
+    mu = h["mu"] if cost_s else np.zeros((0, npch))
+    sg = h["sg"].reshape(-1, npch * R) if cost_s else np.zeros((0, npch * R), np.complex64)
     t_first = 1 + warm_epochs * warm_n if warm_n else 1
     step_t = np.arange(t_first, t_first + len(scheds), dtype=np.int64)
     resid = None
     if keep_residual:
-        rr = torch.cat([x for x in res_s if x is not None]).cpu().numpy() if res_s else np.zeros((0, npch, run.cap))
+        rr = h.get("resid", np.zeros((0, npch, run.cap), np.complex64))
         resid = [np.concatenate([rr[k, p, :pcnt[f, p]] for p in range(npch)]) for k, f in enumerate(scheds)]
     return PatchedResult(
-        recon=recon.cpu().numpy(), gamma=gam.cpu().numpy(), step_gamma=sg,
+        recon=h["recon"], gamma=h["gamma"], step_gamma=sg,
         step_cost=np.array([float(sum(row)) for row in cost]), step_mu=mu[:, 0] if len(mu) else mu.reshape(0),
-        step_t=step_t, step_residual=resid, orders=orders,
-        final_A=run.a.cpu().numpy(), final_B=run.b.cpu().numpy(), t=int(run.t[0].item()) if npch else 1,
-        nmse=err.cpu().numpy(), samples=cnt.astype(np.int64))
+        step_t=step_t, step_residual=resid, orders=orders, final_A=h["A"], final_B=h["B"],
+        t=int(h["t"][0]) if npch else 1, nmse=h["err"], samples=np.diff(off))
