@@ -21,10 +21,11 @@
 
 #define PT_NT 256
 #define PT_MAXR 16
-#define PT_IPW 19  // Gram/rhs items per warp at R = 16: ceil((16*17/2 + 16) / 8)
+
+#define PT_SCH 1024  // schedule steps staged in shared memory at a time
 
 struct PtLayout {
-  size_t g, h, gam, colb, red, a, b, p, q, th, st, phi, ly, li, total;
+  size_t g, h, gam, colb, red, sc, cn, a, b, p, q, th, st, phi, ry, ri, total;
 };
 static __host__ __device__ inline size_t pt_al(size_t x) { return (x + 15) & ~(size_t)15; }
 static __host__ __device__ inline PtLayout pt_layout(int n1, int n2, int R) {
@@ -36,6 +37,8 @@ static __host__ __device__ inline PtLayout pt_layout(int n1, int n2, int R) {
   s.gam = o;  o = pt_al(o + 16 * (size_t)R);
   s.colb = o; o = pt_al(o + 16 * 4 * (size_t)(R + 1));
   s.red = o;  o = pt_al(o + 8 * 32);
+  s.sc = o;   o = pt_al(o + 4 * PT_SCH);  // schedule chunk: frame index per step
+  s.cn = o;   o = pt_al(o + 4 * PT_SCH);  // ... and this patch's entry count per step
   s.a = o;    o = pt_al(o + 8 * (size_t)n1 * R);
   s.b = o;    o = pt_al(o + 8 * (size_t)n2 * R);
   s.p = o;    o = pt_al(o + 8 * (size_t)n1 * R);
@@ -43,8 +46,8 @@ static __host__ __device__ inline PtLayout pt_layout(int n1, int n2, int R) {
   s.th = o;   o = pt_al(o + 8 * cap);
   s.st = o;   o = pt_al(o + 4 * cap);
   s.phi = o;  o = pt_al(o + 8 * cap * R);
-  s.ly = o;   o = pt_al(o + 8 * cap);
-  s.li = o;   o = pt_al(o + 4 * cap);
+  s.ry = o;   o = pt_al(o + 2 * 8 * cap);  // [2][cap] complex64 values (double-buffered across steps)
+  s.ri = o;   o = pt_al(o + 2 * 4 * cap);  // [2][cap] packed local (i << 16) | j
   s.total = o;
   return s;
 }
@@ -89,7 +92,7 @@ __global__ void __launch_bounds__(PT_NT) patch_bin_kernel(int nx, int ny, int n1
       if (i >= 0 && i < nx && j >= 0 && j < ny) {
         const int pi = i / n1, qj = j / n2;
         pid = pi * k2 + qj;
-        loc = (i - pi * n1) * n2 + (j - qj * n2);
+        loc = ((i - pi * n1) << 16) | (j - qj * n2);
       } else {
         bad |= TT_ST_BADROW;
       }
@@ -121,6 +124,9 @@ __global__ void __launch_bounds__(PT_NT) patch_bin_kernel(int nx, int ny, int n1
 }
 
 // ---------------------------------------------------------------- tracking
+// IPW = Gram / rhs items per warp (compile time: the item loop is branch-free; padding items are
+// computed on index 0 and discarded)
+template <int IPW>
 __global__ void __launch_bounds__(PT_NT) patch_track_kernel(tt_patches_args a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n1 = a.pn1, n2 = a.pn2, R = a.rank, cap = n1 * n2;
@@ -140,8 +146,10 @@ __global__ void __launch_bounds__(PT_NT) patch_track_kernel(tt_patches_args a) {
   float2* th = (float2*)(smem + S.th);
   int* st = (int*)(smem + S.st);
   float2* phi = (float2*)(smem + S.phi);
-  float2* ly = (float2*)(smem + S.ly);
-  int* li = (int*)(smem + S.li);
+  float2* ry = (float2*)(smem + S.ry);
+  int* rin = (int*)(smem + S.ri);
+  int* sc = (int*)(smem + S.sc);
+  int* cn = (int*)(smem + S.cn);
 
   float2* gA = (float2*)a.a + (size_t)pl * n1 * R;
   float2* gB = (float2*)a.b + (size_t)pl * n2 * R;
@@ -151,42 +159,71 @@ __global__ void __launch_bounds__(PT_NT) patch_track_kernel(tt_patches_args a) {
   long long t = a.t[pl];
   double ab = a.alpha_bar[pl];
   int status = 0;
-  // this warp's Gram / rhs items: packed lower triangle (i >= j) first, then the rhs entries
-  const int nG = R * (R + 1) / 2, NI = nG + R, ipw = (NI + 7) / 8;
-  int ri[PT_IPW], rj[PT_IPW];
+  // this warp's Gram / rhs items it = warp + 8 m: packed lower triangle (i >= j) first, then the rhs
+  const int nG = R * (R + 1) / 2, NI = nG + R;
+  int ri[IPW], rj[IPW];
 #pragma unroll
-  for (int m = 0; m < PT_IPW; ++m) {
-    const int it = warp * ipw + m;
-    ri[m] = -1;
-    rj[m] = -1;
-    if (m < ipw && it < NI) {
-      if (it < nG) {
-        int i = (int)((sqrtf(8.0f * it + 1.0f) - 1.0f) * 0.5f);
-        while (i * (i + 1) / 2 > it) --i;
-        while ((i + 1) * (i + 2) / 2 <= it) ++i;
-        ri[m] = i;
-        rj[m] = it - i * (i + 1) / 2;
-      } else {
-        ri[m] = it - nG;
-      }
+  for (int m = 0; m < IPW; ++m) {
+    const int it = warp + 8 * m;
+    ri[m] = 0;
+    rj[m] = 0;
+    if (it < nG) {
+      int i = (int)((sqrtf(8.0f * it + 1.0f) - 1.0f) * 0.5f);
+      while (i * (i + 1) / 2 > it) --i;
+      while ((i + 1) * (i + 2) / 2 <= it) ++i;
+      ri[m] = i;
+      rj[m] = it - i * (i + 1) / 2;
+    } else if (it < NI) {
+      ri[m] = it - nG;
+      rj[m] = -1;
     }
   }
   const bool hess = a.step_mode == 1;
+  // the entries of step s are staged into buffer s & 1 with cp.async while step s - 1 computes;
+  // every thread copies, and later reads first, the entries l = tid + k * PT_NT
+  auto load_chunk = [&](int base) {  // the schedule and this patch's counts for steps [base, base + PT_SCH)
+    for (int k = tid; k < min(PT_SCH, a.nsteps - base); k += PT_NT) {
+      const int fr = a.sched[base + k];
+      sc[k] = fr;
+      cn[k] = min(a.pcnt[(size_t)fr * np + p], cap);
+    }
+  };
+  auto prefetch = [&](int s, int buf) -> int {
+    const size_t slot = (size_t)sc[s % PT_SCH] * np + p;
+    const int Ln = cn[s % PT_SCH];
+    const int32_t* gi = a.pidx + slot * cap;
+    const float2* gy = (const float2*)a.py + slot * cap;
+    for (int l = tid; l < Ln; l += PT_NT) {
+      cp_async4(&rin[buf * cap + l], gi + l);
+      cp_async8(&ry[buf * cap + l], gy + l);
+    }
+    return Ln;
+  };
+  load_chunk(0);
+  __syncthreads();
+  int Lnext = a.nsteps > 0 ? prefetch(0, 0) : 0;
   __syncthreads();
 
   for (int s = 0; s < a.nsteps; ++s) {
-    const int f = a.sched[s];
-    const size_t slot = (size_t)f * np + p;
-    const int Lc = min(a.pcnt[slot], cap);
-    const int32_t* gi = a.pidx + slot * cap;
-    const float2* gy = (const float2*)a.py + slot * cap;
-    // stage the step's entries and regression rows Phi[l, r] = A[i, r] B[j, r] (observation.py:219-223)
+    const int buf = s & 1;
+    const int f = sc[s % PT_SCH];
+    const int Lc = Lnext;
+    const int* li = rin + buf * cap;
+    const float2* ly = ry + buf * cap;
+    cp_async_wait_all();
+    // regression rows Phi[l, r] = A[i, r] B[j, r] (observation.py:219-223)
     for (int l = tid; l < Lc; l += PT_NT) {
-      const int id = gi[l];
-      const int i = id / n2, j = id - (id / n2) * n2;
-      li[l] = id;
-      ly[l] = gy[l];
+      const int pk = li[l];
+      const int i = pk >> 16, j = pk & 0xffff;
       for (int r = 0; r < R; ++r) phi[l * R + r] = cmul(A[i * R + r], B[j * R + r]);
+    }
+    if (s + 1 < a.nsteps) {  // buffer buf ^ 1 was last read in step s - 1
+      if ((s + 1) % PT_SCH == 0) {
+        __syncthreads();
+        load_chunk(s + 1);
+        __syncthreads();
+      }
+      Lnext = prefetch(s + 1, buf ^ 1);
     }
     if (!a.project) {  // ||A||^2 + ||B||^2 for the cost (tracker.py:389)
       double en = 0.0;
@@ -195,31 +232,42 @@ __global__ void __launch_bounds__(PT_NT) patch_track_kernel(tt_patches_args a) {
       if (lane == 0) red[warp] = en;
     }
     __syncthreads();
-    // Gram Phi^H Phi + lam I (packed lower triangle) and rhs Phi^H y in fp64: warp w owns items
-    // [w * ipw, (w + 1) * ipw), its lanes split the entries, a shuffle tree sums them
+    // Gram Phi^H Phi + lam I (packed lower triangle) and rhs Phi^H y: products in fp32, sums in fp64;
+    // the lanes of a warp split the entries, a shuffle tree sums them
     {
-      double2 acc[PT_IPW];
+      double2 acc[IPW];
 #pragma unroll
-      for (int m = 0; m < PT_IPW; ++m) acc[m] = make_double2(0.0, 0.0);
-      if (warp * ipw < NI) {
-        for (int l = lane; l < Lc; l += 32) {
-          const float2* ph = phi + l * R;
-          const float2 y = ly[l];
+      for (int m = 0; m < IPW; ++m) acc[m] = make_double2(0.0, 0.0);
+      for (int l = lane; l < Lc; l += 32) {
+        const float2* ph = phi + l * R;
+        const float2 y = ly[l];
 #pragma unroll
-          for (int m = 0; m < PT_IPW; ++m)
-            if (ri[m] >= 0) acc[m] = zfma_cj(ph[ri[m]], rj[m] >= 0 ? ph[rj[m]] : y, acc[m]);
+        for (int m = 0; m < IPW; ++m) {
+          const float2 u = ph[ri[m]];
+          const float2 w = ph[max(rj[m], 0)];
+          const float2 v = rj[m] >= 0 ? w : y;
+          acc[m].x += (double)fmaf(u.x, v.x, u.y * v.y);
+          acc[m].y += (double)fmaf(u.x, v.y, -u.y * v.x);
         }
+      }
 #pragma unroll
-        for (int m = 0; m < PT_IPW; ++m) {
-          if (ri[m] < 0) continue;
-          double2 v = make_double2(warp_sum_d(acc[m].x), warp_sum_d(acc[m].y));
-          if (lane == 0) {
-            if (rj[m] >= 0) {
-              if (ri[m] == rj[m]) v.x += a.lam;
-              G[ri[m] * (ri[m] + 1) / 2 + rj[m]] = v;
-            } else {
-              h[ri[m]] = v;
-            }
+      for (int m = 0; m < IPW; ++m) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          acc[m].x += __shfl_xor_sync(0xffffffffu, acc[m].x, o);
+          acc[m].y += __shfl_xor_sync(0xffffffffu, acc[m].y, o);
+        }
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int m = 0; m < IPW; ++m) {
+          const int it = warp + 8 * m;
+          double2 v = acc[m];
+          if (it < nG) {
+            if (ri[m] == rj[m]) v.x += a.lam;
+            G[it] = v;
+          } else if (it < NI) {
+            h[ri[m]] = v;
           }
         }
       }
@@ -261,7 +309,8 @@ __global__ void __launch_bounds__(PT_NT) patch_track_kernel(tt_patches_args a) {
           ex -= px * g.x - py_ * g.y;
           ey -= px * g.y + py_ * g.x;
         }
-        const int id = li[l];
+        const int pk = li[l];
+        const int id = (pk >> 16) * n2 + (pk & 0xffff);
         if (atomicExch(&st[id], cur) == cur) status |= TT_ST_DUPROW;
         const float2 ef = make_float2((float)ex, (float)ey);
         th[id] = ef;
@@ -280,32 +329,21 @@ __global__ void __launch_bounds__(PT_NT) patch_track_kernel(tt_patches_args a) {
       for (int o = tid; o < (n1 + n2) * R; o += PT_NT) {
         float2 acc = make_float2(0.f, 0.f);
         float c = 0.f;
-        int r;
-        if (o < n1 * R) {
-          const int i = o / R;
-          r = o - i * R;
-          for (int j = 0; j < n2; ++j) {
-            const int k = i * n2 + j;
-            if (st[k] == cur) {
-              const float2 bv = B[j * R + r];
-              acc = cfma_conj(th[k], bv, acc);
-              c += cabs2(bv);
-            }
-          }
-          P[o] = acc;
-        } else {
-          const int o2 = o - n1 * R, j = o2 / R;
-          r = o2 - j * R;
-          for (int i = 0; i < n1; ++i) {
-            const int k = i * n2 + j;
-            if (st[k] == cur) {
-              const float2 av = A[i * R + r];
-              acc = cfma_conj(th[k], av, acc);
-              c += cabs2(av);
-            }
-          }
-          Q[o2] = acc;
+        const bool rowA = o < n1 * R;
+        const int o2 = rowA ? o : o - n1 * R;
+        const int x = o2 / R, r = o2 - x * R;
+        const int K = rowA ? n2 : n1;
+        const int kst = rowA ? 1 : n2, k0 = rowA ? x * n2 : x;
+        const float2* F = rowA ? B : A;
+        for (int k = 0; k < K; ++k) {
+          const int kk = k0 + k * kst;
+          const bool in = st[kk] == cur;
+          const float2 fv = F[k * R + r];
+          const float2 tv = in ? th[kk] : make_float2(0.f, 0.f);
+          acc = cfma_conj(tv, fv, acc);
+          c += in ? cabs2(fv) : 0.f;
         }
+        (rowA ? P : Q)[o2] = acc;
         if (hess) {
           const double2 g = gam[r];
           am = fmax(am, (g.x * g.x + g.y * g.y) * (double)c);
@@ -418,12 +456,25 @@ extern "C" int tt_track_patches(void* stream, const tt_patches_args* a) {
   TT_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   if (sm > (size_t)optin)
     return tt_fail(TT_EUNSUPPORTED, "patch too large for the fused patch kernel (shared memory)");
-  static size_t set_bytes = 0;
-  if (sm > 48 * 1024 && sm > set_bytes) {
-    TT_CUDA_TRY(cudaFuncSetAttribute(patch_track_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    set_bytes = sm;
+  if (a->pn1 > 32767 || a->pn2 > 65535) return tt_fail(TT_EUNSUPPORTED, "patch extent too large");
+  // items per warp: ceil((R (R + 1) / 2 + R) / 8), rounded up to an instantiated size
+  const int R = a->rank, need = (R * (R + 1) / 2 + R + 7) / 8;
+  static const int sizes[] = {1, 2, 3, 4, 6, 8, 12, 19};
+  static void (*const fns[])(tt_patches_args) = {patch_track_kernel<1>, patch_track_kernel<2>, patch_track_kernel<3>,
+                                                  patch_track_kernel<4>, patch_track_kernel<6>, patch_track_kernel<8>,
+                                                  patch_track_kernel<12>, patch_track_kernel<19>};
+  static size_t set_bytes[8] = {0};
+  int which = 7;
+  for (int k = 0; k < 8; ++k)
+    if (sizes[k] >= need) {
+      which = k;
+      break;
+    }
+  if (sm > 48 * 1024 && sm > set_bytes[which]) {
+    TT_CUDA_TRY(cudaFuncSetAttribute(fns[which], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    set_bytes[which] = sm;
   }
-  patch_track_kernel<<<a->npatch_local, PT_NT, sm, (cudaStream_t)stream>>>(*a);
+  fns[which]<<<a->npatch_local, PT_NT, sm, (cudaStream_t)stream>>>(*a);
   TT_CUDA_TRY(cudaGetLastError());
   return TT_OK;
 }
