@@ -66,7 +66,8 @@ def test_error_codes_map_to_reference_exceptions():
         _lib.raise_status(_lib.TT_ST_NONFINITE, "x")
 
 
-@pytest.mark.parametrize("struct,cname", [("RowsArgs", "tt_rows_args"), ("EntriesArgs", "tt_entries_args")])
+@pytest.mark.parametrize("struct,cname", [("RowsArgs", "tt_rows_args"), ("EntriesArgs", "tt_entries_args"),
+                                          ("PatchesArgs", "tt_patches_args")])
 def test_ctypes_struct_layout_matches_c(struct, cname):
     from paper_1609_04104_b200 import _lib
 
