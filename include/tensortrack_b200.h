@@ -164,6 +164,8 @@ typedef struct tt_entries_args {
    * whole per-frame chain can be captured in a CUDA graph. */
   const int32_t* nmeas_dev;
 } tt_entries_args;
+/* Scratch for tt_track_entries: zero-fill it before its first use and reuse it for later steps
+ * of the same shape (it carries a per-step stamp that replaces clearing the residual image). */
 size_t tt_entries_scratch_bytes(int nx, int ny, int rank, int nmeas);
 int tt_track_entries(void* stream, const tt_entries_args* a);
 

@@ -106,8 +106,8 @@ def entries_scratch(nx, ny, rank) -> torch.Tensor:
     k = (nx, ny, rank, torch.cuda.current_device())
     s = _ent_cache.get(k)
     if s is None:
-        s = torch.empty(int(L.lib().tt_entries_scratch_bytes(nx, ny, rank, 0)), dtype=torch.uint8,
-                        device=L.device())
+        s = torch.zeros(int(L.lib().tt_entries_scratch_bytes(nx, ny, rank, 0)), dtype=torch.uint8,
+                        device=L.device())  # zero-filled before first use (frame stamps)
         _ent_cache[k] = s
     return s
 

@@ -3,138 +3,191 @@
 // (Ah, Bh) = (F_x A, F_y B) for Fourier masks, (A, B) for entry masks — the
 // two are the same iteration (test_mri.py:258-286).
 //
-//   1. ent_gram     Phi_l = Ah[i_l] .* Bh[j_l] (exact fp64 products), block
-//                   partials of G = Phi^H Phi, h = Phi^H y, ||y||^2
-//                   (build_phi observation.py:219-228; solve_gamma
-//                   tracker.py:139-156 as normal equations)
-//   2. ent_solve    fixed-order reduction, G + lam I, fp64 LDL^H -> gamma,
-//                   cost (tracker.py:386-389)
-//   3. ent_resid    e_l = y_l - Phi_l gamma, scattered into a dense residual
-//                   image Xi and mask M (the scatter of _scatter_theta,
-//                   tracker.py:176-188)
-//   4. ent_backproj P = Xi conj(Bh), Q = Xi^T conj(Ah) and the closed-form
-//                   curvature sums c0 = M |Bh|^2, c1 = M^T |Ah|^2
-//                   (collapsed gradient data terms tracker.py:208-228;
-//                   hessian_bound tracker.py:337-364)
-//   5. ent_step     alpha / mu (tracker.py:391-400)
-//   6. ent_update   Ah <- (1 - mu lam/t) Ah + mu conj(gamma) P, same for Bh
-//                   (tracker.py:402-404)
-// Everything is deterministic (fixed reduction orders, no float atomics).
+//   1. ent_gram     thread-block clusters of 8 CTAs; each CTA stages its share of the entries
+//                   and their regression rows Phi_l = Ah[i_l] .* Bh[j_l] in shared memory,
+//                   accumulates G = Phi^H Phi, h = Phi^H y, ||y||^2 and its slice of
+//                   ||Ah||^2 + ||Bh||^2 (fp32 products, fp64 sums), and the cluster sums its 8
+//                   partials through distributed shared memory in fixed order
+//                   (build_phi observation.py:219-228; solve_gamma tracker.py:139-156 as
+//                   normal equations)
+//   2. ent_solve    fixed-order sum of the cluster partials, G + lam I, fp64 Gauss-Jordan
+//                   -> gamma, cost (tracker.py:386-389); advances the frame stamp
+//   3. ent_resid    e_l = y_l - Phi_l gamma, written into the dense residual image Xi with
+//                   the frame's stamp (the scatter of _scatter_theta, tracker.py:176-188)
+//   4. ent_backproj P = Xi conj(Bh), Q = Xi^T conj(Ah) over this frame's stamped entries
+//                   (collapsed gradient data terms, tracker.py:208-228); for HessianBound the
+//                   closed-form curvature max_{m,r} |gamma_r|^2 c_m[., r] (hessian_bound
+//                   tracker.py:337-364) as an order-free atomic max
+//   5. ent_update   alpha / mu (tracker.py:391-400) and Ah <- (1 - mu lam/t) Ah + mu conj(gamma) P,
+//                   same for Bh (tracker.py:402-404)
+// Everything is deterministic (fixed reduction orders; the only atomic is a max). The stamps
+// replace a per-frame clear of Xi: the scratch must be zero-filled before its first use.
+
+#include <cooperative_groups.h>
 
 #include "tt_block.cuh"
 
-#define ENT_NT 256
-#define ENT_NB 64
-#define ENT_TL 32
+namespace cg = cooperative_groups;
 
+#define ENT_NT 256
+#define EG_CL 8       // CTAs per gram cluster
+#define EG_NCL 16     // clusters at most (= partials the solve sums)
+#define EG_TL 256     // entries staged per tile
+#define EG_PER 128    // target entries per CTA
+#define EG_MI 9       // items per thread (R <= 64: R(R+1)/2 + R + 1 <= 2145 <= 9 * 256)
+
+// scal slots (8 bytes each): [0] cost, [1] mu, [2] curvature max (double bits, atomic max),
+// [3] frame stamp counter (int64), [4] alpha_bar at the step's start
 struct EntScratch {
-  size_t gp, hp, yp, gam, scal, xi, mk, P, Q, c0, c1, total;
+  size_t gp, gam, scal, xi, st, P, Q, total;
 };
 static EntScratch ent_layout(int nx, int ny, int R) {
   EntScratch s;
-  const size_t Rp = (size_t)R * (R + 1) / 2;
+  const size_t NI2 = (size_t)R * (R + 1) / 2 + R + 1;
   size_t o = 0;
   auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-  s.gp = o;   o = al(o + sizeof(double2) * ENT_NB * Rp);
-  s.hp = o;   o = al(o + sizeof(double2) * ENT_NB * R);
-  s.yp = o;   o = al(o + sizeof(double) * ENT_NB);
+  s.gp = o;   o = al(o + sizeof(double2) * EG_NCL * NI2);
   s.gam = o;  o = al(o + sizeof(double2) * R);
   s.scal = o; o = al(o + sizeof(double) * 16);
   s.xi = o;   o = al(o + sizeof(float2) * (size_t)nx * ny);
-  s.mk = o;   o = al(o + sizeof(float) * (size_t)nx * ny);
+  s.st = o;   o = al(o + sizeof(int) * (size_t)nx * ny);
   s.P = o;    o = al(o + sizeof(float2) * (size_t)nx * R);
   s.Q = o;    o = al(o + sizeof(float2) * (size_t)ny * R);
-  s.c0 = o;   o = al(o + sizeof(float) * (size_t)nx * R);
-  s.c1 = o;   o = al(o + sizeof(float) * (size_t)ny * R);
   s.total = o;
   return s;
 }
+static size_t gram_smem(int R) {
+  const size_t NI2 = (size_t)R * (R + 1) / 2 + R + 1;
+  return sizeof(float2) * (size_t)EG_TL * (R + 1) + sizeof(int2) * EG_TL + sizeof(double2) * NI2 + sizeof(double) * 64;
+}
 
-__global__ void __launch_bounds__(ENT_NT) ent_gram_kernel(int nmeas, const int* __restrict__ nmeas_dev, int R,
-                                                          const float2* __restrict__ ah,
-                                                          const float2* __restrict__ bh, const int* __restrict__ idx,
-                                                          const float2* __restrict__ y, double2* __restrict__ gp,
-                                                          double2* __restrict__ hp, double* __restrict__ yp) {
+__global__ void __cluster_dims__(EG_CL, 1, 1) __launch_bounds__(ENT_NT)
+    ent_gram_kernel(int nmeas, const int* __restrict__ nmeas_dev, int nx, int ny, int R,
+                    const float2* __restrict__ ah, const float2* __restrict__ bh, const int* __restrict__ idx,
+                    const float2* __restrict__ y, double2* __restrict__ gp) {
   if (nmeas_dev) nmeas = min(*nmeas_dev, nmeas);
   extern __shared__ __align__(16) unsigned char smem[];
-  double2* phi = (double2*)smem;                   // [TL][R]
-  double2* yv = phi + ENT_TL * R;                  // [TL]
-  double* red = (double*)(yv + ENT_TL);
+  float2* phi = (float2*)smem;                   // [TL][R]
+  float2* yv = phi + (size_t)EG_TL * R;          // [TL]
+  int2* ij = (int2*)(yv + EG_TL);                // [TL]
+  double2* part = (double2*)(ij + EG_TL);        // [NI2] this CTA's partial items
+  const int Rp = R * (R + 1) / 2, NI = Rp + R, NI2 = NI + 1;
+  double* red = (double*)(part + NI2);
   const int tid = threadIdx.x, NT = blockDim.x;
-  const int Rp = R * (R + 1) / 2;
   const int b = blockIdx.x;
   const int l0 = (int)(((long long)nmeas * b) / gridDim.x), l1 = (int)(((long long)nmeas * (b + 1)) / gridDim.x);
-  // per-thread accumulators for entries e = tid + m*NT (Rp <= 2080 -> m < 9)
-  double2 acc[9];
+  double2 acc[EG_MI];
 #pragma unroll
-  for (int m = 0; m < 9; ++m) acc[m] = make_double2(0.0, 0.0);
-  double2 hacc = make_double2(0.0, 0.0);
+  for (int m = 0; m < EG_MI; ++m) acc[m] = make_double2(0.0, 0.0);
   double ysq = 0.0;
-  for (int t0 = l0; t0 < l1; t0 += ENT_TL) {
-    const int tl = min(ENT_TL, l1 - t0);
-    for (int o = tid; o < tl * R; o += NT) {
-      const int ll = o / R, r = o - ll * R;
-      const int i = idx[2 * (t0 + ll)], j = idx[2 * (t0 + ll) + 1];
-      phi[o] = zmul(to_d2(ah[(size_t)i * R + r]), to_d2(bh[(size_t)j * R + r]));
-    }
+  for (int t0 = l0; t0 < l1; t0 += EG_TL) {
+    const int tl = min(EG_TL, l1 - t0);
     for (int ll = tid; ll < tl; ll += NT) {
       const float2 v = y[t0 + ll];
-      yv[ll] = to_d2(v);
+      ij[ll] = make_int2(idx[2 * (t0 + ll)], idx[2 * (t0 + ll) + 1]);
+      yv[ll] = v;
       ysq += (double)v.x * v.x + (double)v.y * v.y;
     }
     __syncthreads();
-#pragma unroll
-    for (int m = 0; m < 9; ++m) {
-      const int e = tid + m * NT;
-      if (e < Rp) {
-        int r, q;
-        tri_decode(e, r, q);
-        double2 g = acc[m];
-        for (int ll = 0; ll < tl; ++ll) g = zfma_cj(phi[ll * R + r], phi[ll * R + q], g);
-        acc[m] = g;
-      }
+    for (int o = tid; o < tl * R; o += NT) {
+      const int ll = idiv(o, R), r = o - ll * R;
+      const int2 q = ij[ll];
+      phi[o] = cmul(ah[(size_t)q.x * R + r], bh[(size_t)q.y * R + r]);
     }
-    if (tid < R)
-      for (int ll = 0; ll < tl; ++ll) hacc = zfma_cj(phi[ll * R + tid], yv[ll], hacc);
+    __syncthreads();
+    // item-outer: one guard per item, none per entry
+#pragma unroll
+    for (int m = 0; m < EG_MI; ++m) {
+      const int it = tid + m * NT;
+      if (it >= NI) break;
+      double2 g = acc[m];
+      if (it < Rp) {
+        int r, q;
+        tri_decode(it, r, q);
+        for (int ll = 0; ll < tl; ++ll) {
+          const float2 u = phi[ll * R + r], v = phi[ll * R + q];
+          g.x += (double)fmaf(u.x, v.x, u.y * v.y);
+          g.y += (double)fmaf(u.x, v.y, -u.y * v.x);
+        }
+      } else {
+        const int r = it - Rp;
+        for (int ll = 0; ll < tl; ++ll) {
+          const float2 u = phi[ll * R + r], v = yv[ll];
+          g.x += (double)fmaf(u.x, v.x, u.y * v.y);
+          g.y += (double)fmaf(u.x, v.y, -u.y * v.x);
+        }
+      }
+      acc[m] = g;
+    }
     __syncthreads();
   }
-#pragma unroll
-  for (int m = 0; m < 9; ++m) {
-    const int e = tid + m * NT;
-    if (e < Rp) gp[(size_t)b * Rp + e] = acc[m];
+  // this CTA's slice of ||Ah||^2 + ||Bh||^2 (the cost's regulariser, tracker.py:389)
+  double en = 0.0;
+  {
+    const int E = (nx + ny) * R;
+    const int e0 = (int)(((long long)E * b) / gridDim.x), e1 = (int)(((long long)E * (b + 1)) / gridDim.x);
+    for (int e = e0 + tid; e < e1; e += NT) en += (double)cabs2(e < nx * R ? ah[e] : bh[e - nx * R]);
   }
-  if (tid < R) hp[(size_t)b * R + tid] = hacc;
   const double ys = block_sum(ysq, red);
-  if (tid == 0) yp[b] = ys;
+  const double es = block_sum(en, red + 32);
+#pragma unroll
+  for (int m = 0; m < EG_MI; ++m) {
+    const int it = tid + m * NT;
+    if (it < NI) part[it] = acc[m];
+  }
+  if (tid == 0) part[NI] = make_double2(ys, es);
+  // cluster sum of the 8 partials in fixed rank order, each CTA taking a slice of the items
+  cg::cluster_group cl = cg::this_cluster();
+  cl.sync();
+  const int rank = (int)cl.block_rank();
+  const int per = (NI2 + EG_CL - 1) / EG_CL;
+  const int i0 = rank * per, i1 = min(NI2, i0 + per);
+  double2* dst = gp + (size_t)(b / EG_CL) * NI2;
+  for (int it = i0 + tid; it < i1; it += NT) {
+    double2 sum = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int c = 0; c < EG_CL; ++c) sum = zadd(sum, cl.map_shared_rank(part, c)[it]);
+    dst[it] = sum;
+  }
+  cl.sync();  // no CTA leaves while its partials are read
 }
 
-__global__ void __launch_bounds__(ENT_NT) ent_solve_kernel(int nx, int ny, int R, int nmeas,
-                                                           const int* __restrict__ nmeas_dev, int nb, double lam,
-                                                           long long t, const float2* __restrict__ ah,
-                                                           const float2* __restrict__ bh, const double2* gp,
-                                                           const double2* hp, const double* yp, double2* gam_out,
+__global__ void __launch_bounds__(ENT_NT) ent_solve_kernel(int R, int nmeas, const int* __restrict__ nmeas_dev, int ncl,
+                                                           double lam, long long t, const double2* __restrict__ gp,
+                                                           const double* __restrict__ alpha_bar, double2* gam_out,
                                                            double* scal, float2* gamma_out, double* cost_out,
                                                            int32_t* status) {
   extern __shared__ __align__(16) unsigned char smem[];
   if (nmeas_dev) nmeas = min(*nmeas_dev, nmeas);
-  const int Rp = R * (R + 1) / 2;
-  double2* G = (double2*)smem;
-  double2* hv = G + Rp;
-  double2* gam = hv + R;
-  double* red = (double*)(gam + R);
+  const int Rp = R * (R + 1) / 2, NI = Rp + R, NI2 = NI + 1;
+  double2* G = (double2*)smem;   // [NI2]: G packed, h, (||y||^2, energy)
+  double2* gam = G + NI2;
+  double2* colb = gam + R;       // 4 (R + 1)
   const int tid = threadIdx.x, NT = blockDim.x;
-  double en = 0.0;
-  for (int o = tid; o < nx * R; o += NT) {
-    const float2 v = ah[o];
-    en += (double)v.x * v.x + (double)v.y * v.y;
+  for (int it = tid; it < NI2; it += NT) {  // fixed-order sum of the cluster partials, loads in flight
+    double2 v[EG_NCL];
+#pragma unroll
+    for (int c = 0; c < EG_NCL; ++c) v[c] = c < ncl ? gp[(size_t)c * NI2 + it] : make_double2(0.0, 0.0);
+    double2 g = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int c = 0; c < EG_NCL; ++c) g = zadd(g, v[c]);
+    if (it < Rp) {
+      int r, q;
+      tri_decode(it, r, q);
+      if (r == q) g.x += lam;
+    }
+    G[it] = g;
   }
-  for (int o = tid; o < ny * R; o += NT) {
-    const float2 v = bh[o];
-    en += (double)v.x * v.x + (double)v.y * v.y;
-  }
-  const double energy = block_sum(en, red);
+  __syncthreads();
+  const double yn = G[NI].x, energy = G[NI].y;
   const double lt = lam / (double)t;
-  if (nmeas == 0) {
+  if (tid == 0) {
+    long long* sl = (long long*)scal;
+    sl[2] = 0;           // curvature max (bits of +0.0)
+    sl[3] += 1;          // this frame's stamp
+    scal[4] = alpha_bar[0];
+  }
+  if (nmeas == 0) {  // tracker.py:380-384
     if (tid < R) {
       gam_out[tid] = make_double2(0.0, 0.0);
       if (gamma_out) gamma_out[tid] = make_float2(0.f, 0.f);
@@ -146,53 +199,37 @@ __global__ void __launch_bounds__(ENT_NT) ent_solve_kernel(int nx, int ny, int R
     }
     return;
   }
-  for (int e = tid; e < Rp; e += NT) {
-    int r, q;
-    tri_decode(e, r, q);
-    double2 g = make_double2(0.0, 0.0);
-    int b = 0;
-    for (; b + 4 <= nb; b += 4) {  // four loads in flight, fixed association order
-      const double2 v0 = gp[(size_t)b * Rp + e], v1 = gp[(size_t)(b + 1) * Rp + e];
-      const double2 v2 = gp[(size_t)(b + 2) * Rp + e], v3 = gp[(size_t)(b + 3) * Rp + e];
-      g = zadd(g, zadd(zadd(v0, v1), zadd(v2, v3)));
-    }
-    for (; b < nb; ++b) g = zadd(g, gp[(size_t)b * Rp + e]);
-    if (r == q) g.x += lam;
-    G[e] = g;
-  }
-  double yn = 0.0;
-  if (tid < R) {
-    double2 h = make_double2(0.0, 0.0);
-    for (int b = 0; b < nb; ++b) h = zadd(h, hp[(size_t)b * R + tid]);
-    hv[tid] = h;
-  }
-  for (int b = 0; b < nb; ++b) yn += yp[b];
-  __syncthreads();
+  double2 hsave = make_double2(0.0, 0.0);
+  if (tid < R) hsave = G[Rp + tid];
   {
-    double2* colb = (double2*)(red + 64);  // 4 (R+1) double2 after the reduction buffer
     const int ept = gj_ept(R, blockDim.x);
-    if (ept <= 1) block_gj_solve<1>(G, hv, gam, colb, R);
-    else if (ept <= 2) block_gj_solve<2>(G, hv, gam, colb, R);
-    else if (ept <= 3) block_gj_solve<3>(G, hv, gam, colb, R);
-    else if (ept <= 5) block_gj_solve<5>(G, hv, gam, colb, R);
-    else block_ldl_solve(G, hv, gam, R);
+    if (ept <= 1) block_gj_solve<1>(G, G + Rp, gam, colb, R);
+    else if (ept <= 2) block_gj_solve<2>(G, G + Rp, gam, colb, R);
+    else if (ept <= 3) block_gj_solve<3>(G, G + Rp, gam, colb, R);
+    else if (ept <= 5) block_gj_solve<5>(G, G + Rp, gam, colb, R);
+    else block_ldl_solve(G, G + Rp, gam, R);
   }
-  // reload h (eliminated in place) for the cost
+  double gh = 0.0, gg = 0.0;
   if (tid < R) {
-    double2 h = make_double2(0.0, 0.0);
-    for (int b = 0; b < nb; ++b) h = zadd(h, hp[(size_t)b * R + tid]);
-    hv[tid] = h;
-    gam_out[tid] = gam[tid];
-    if (gamma_out) gamma_out[tid] = to_f2(gam[tid]);
+    const double2 g = gam[tid];
+    gam_out[tid] = g;
+    if (gamma_out) gamma_out[tid] = to_f2(g);
+    gh = g.x * hsave.x + g.y * hsave.y;
+    gg = g.x * g.x + g.y * g.y;
+  }
+  __shared__ double rgh[64], rgg[64];
+  if (tid < 64) {
+    rgh[tid] = tid < R ? gh : 0.0;
+    rgg[tid] = tid < R ? gg : 0.0;
   }
   __syncthreads();
   if (tid == 0) {
-    double gh = 0.0, gg = 0.0;
+    double sgh = 0.0, sgg = 0.0;
     for (int r = 0; r < R; ++r) {
-      gh += gam[r].x * hv[r].x + gam[r].y * hv[r].y;
-      gg += gam[r].x * gam[r].x + gam[r].y * gam[r].y;
+      sgh += rgh[r];
+      sgg += rgg[r];
     }
-    const double cost = 0.5 * (yn - gh - lam * gg) + 0.5 * lt * energy;
+    const double cost = 0.5 * (yn - sgh - lam * sgg) + 0.5 * lt * energy;
     scal[0] = cost;
     if (cost_out) cost_out[0] = cost;
     if (!isfinite(cost) && status) atomicOr(status, TT_ST_NONFINITE);
@@ -202,8 +239,10 @@ __global__ void __launch_bounds__(ENT_NT) ent_solve_kernel(int nx, int ny, int R
 __global__ void ent_resid_kernel(int nmeas, const int* __restrict__ nmeas_dev, int ny, int R,
                                  const float2* __restrict__ ah, const float2* __restrict__ bh,
                                  const int* __restrict__ idx, const float2* __restrict__ y, const double2* gam,
-                                 float2* __restrict__ xi, float* __restrict__ mk, float2* __restrict__ resid) {
+                                 const double* scal, float2* __restrict__ xi, int* __restrict__ st,
+                                 float2* __restrict__ resid) {
   if (nmeas_dev) nmeas = min(*nmeas_dev, nmeas);
+  const int cur = (int)((const long long*)scal)[3];
   for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nmeas; l += gridDim.x * blockDim.x) {
     const int i = idx[2 * l], j = idx[2 * l + 1];
     double2 s = make_double2(0.0, 0.0);
@@ -213,125 +252,130 @@ __global__ void ent_resid_kernel(int nmeas, const int* __restrict__ nmeas_dev, i
     }
     const float2 e = make_float2((float)((double)y[l].x - s.x), (float)((double)y[l].y - s.y));
     xi[(size_t)i * ny + j] = e;
-    mk[(size_t)i * ny + j] = 1.f;
+    st[(size_t)i * ny + j] = cur;
     if (resid) resid[l] = e;
   }
 }
 
-// role 0 (blockIdx.y = 0): rows i of P and c0; role 1: rows j of Q and c1. Block = 32 outputs x 8 parts
-// of the contraction index; the 8 parts are summed in fixed order through shared memory.
+// role 0 (blockIdx.y = 0): rows i of P; role 1: rows j of Q. Block = 32 outputs x 8 parts of the
+// contraction index, summed in fixed order through shared memory. HessianBound: the block's max of
+// |gamma_r|^2 sum_{stamped} |other factor|^2 joins the frame's max (order-free).
 #define BP_O 32
 #define BP_K 8
-__global__ void __launch_bounds__(BP_O * BP_K) ent_backproj_kernel(int nx, int ny, int R,
+__global__ void __launch_bounds__(BP_O * BP_K) ent_backproj_kernel(int nx, int ny, int R, int hess,
                                                                    const float2* __restrict__ ah,
                                                                    const float2* __restrict__ bh,
                                                                    const float2* __restrict__ xi,
-                                                                   const float* __restrict__ mk,
-                                                                   float2* __restrict__ P, float2* __restrict__ Q,
-                                                                   float* __restrict__ c0, float* __restrict__ c1) {
+                                                                   const int* __restrict__ st, const double2* gam,
+                                                                   double* scal, float2* __restrict__ P,
+                                                                   float2* __restrict__ Q) {
   __shared__ float2 sacc[BP_K][BP_O];
   __shared__ float scs[BP_K][BP_O];
+  __shared__ double smax[BP_O * BP_K / 32];
   const int tx = threadIdx.x, ty = threadIdx.y;
+  const int cur = (int)((const long long*)scal)[3];
   const int o = blockIdx.x * BP_O + tx;
   const bool rows = blockIdx.y == 0;
   const int m = rows ? nx * R : ny * R;
   float2 acc = make_float2(0.f, 0.f);
   float cs = 0.f;
   if (o < m) {
-    if (rows) {
-      const int i = o / R, r = o - i * R;
-      for (int j = ty; j < ny; j += BP_K) {
-        const float2 b = bh[(size_t)j * R + r];
-        acc = cfma_conj(xi[(size_t)i * ny + j], b, acc);
-        cs = fmaf(mk[(size_t)i * ny + j], cabs2(b), cs);
+    const int x = o / R, r = o - x * R;
+    const int K = rows ? ny : nx;
+    const size_t xs = rows ? 1 : (size_t)ny, base = rows ? (size_t)x * ny : (size_t)x;
+    const float2* F = rows ? bh : ah;
+    int k = ty;
+    for (; k + 3 * BP_K < K; k += 4 * BP_K) {  // four entries in flight
+      float2 tv[4], fv[4];
+      bool in[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const size_t kk = base + (size_t)(k + u * BP_K) * xs;
+        in[u] = st[kk] == cur;
+        tv[u] = xi[kk];
+        fv[u] = F[(size_t)(k + u * BP_K) * R + r];
       }
-    } else {
-      const int j = o / R, r = o - j * R;
-      for (int i = ty; i < nx; i += BP_K) {
-        const float2 a = ah[(size_t)i * R + r];
-        acc = cfma_conj(xi[(size_t)i * ny + j], a, acc);
-        cs = fmaf(mk[(size_t)i * ny + j], cabs2(a), cs);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc = cfma_conj(in[u] ? tv[u] : make_float2(0.f, 0.f), fv[u], acc);
+        cs += in[u] ? cabs2(fv[u]) : 0.f;
       }
+    }
+    for (; k < K; k += BP_K) {
+      const size_t kk = base + (size_t)k * xs;
+      const bool in = st[kk] == cur;
+      const float2 fv = F[(size_t)k * R + r];
+      acc = cfma_conj(in ? xi[kk] : make_float2(0.f, 0.f), fv, acc);
+      cs += in ? cabs2(fv) : 0.f;
     }
   }
   sacc[ty][tx] = acc;
   scs[ty][tx] = cs;
   __syncthreads();
+  double top = 0.0;
   if (ty == 0 && o < m) {
     for (int k = 1; k < BP_K; ++k) {
       acc = cadd(acc, sacc[k][tx]);
       cs += scs[k][tx];
     }
-    if (rows) {
-      P[o] = acc;
-      c0[o] = cs;
-    } else {
-      Q[o] = acc;
-      c1[o] = cs;
+    (rows ? P : Q)[o] = acc;
+    if (hess) {
+      const double2 g = gam[o % R];
+      top = (g.x * g.x + g.y * g.y) * (double)cs;
+    }
+  }
+  if (hess) {
+    const int w = (ty * BP_O + tx) >> 5, lane = tx & 31;
+    top = warp_max(top);
+    if (lane == 0) smax[w] = top;
+    __syncthreads();
+    if (ty == 0 && tx == 0) {
+      double t2 = 0.0;
+      for (int k = 0; k < BP_O * BP_K / 32; ++k) t2 = fmax(t2, smax[k]);
+      // non-negative doubles order like their bit patterns
+      atomicMax((unsigned long long*)&scal[2], (unsigned long long)__double_as_longlong(t2));
     }
   }
 }
 
-__global__ void __launch_bounds__(ENT_NT) ent_step_kernel(int nx, int ny, int R, int nmeas,
-                                                          const int* __restrict__ nmeas_dev, double lam, long long t,
-                                                          int step_mode, double mu, double c_floor, double c_cap,
-                                                          const double2* gam, const float* c0, const float* c1,
-                                                          double* alpha_bar, double* scal, double* mu_out,
-                                                          double* alpha_out) {
-  __shared__ double red[64];
+// step size (tracker.py:391-400) computed identically by every block from the step-start alpha_bar;
+// block 0 publishes it. Then Ah <- (1 - mu lam/t) Ah + mu conj(gamma) P, likewise Bh.
+__global__ void ent_update_kernel(int nx, int ny, int R, int nmeas, const int* __restrict__ nmeas_dev, double lam,
+                                  long long t, int step_mode, double mu_fixed, double c_floor, double c_cap,
+                                  double* scal, double* alpha_bar, const double2* gam, const float2* ah,
+                                  const float2* bh, const float2* __restrict__ P, const float2* __restrict__ Q,
+                                  float2* ah_out, float2* bh_out, double* mu_out, double* alpha_out) {
   if (nmeas_dev) nmeas = min(*nmeas_dev, nmeas);
-  const int tid = threadIdx.x, NT = blockDim.x;
-  double top = 0.0;
-  for (int o = tid; o < nx * R; o += NT) {
-    const int r = o % R;
-    const double g2 = gam[r].x * gam[r].x + gam[r].y * gam[r].y;
-    top = fmax(top, g2 * (double)c0[o]);
-  }
-  for (int o = tid; o < ny * R; o += NT) {
-    const int r = o % R;
-    const double g2 = gam[r].x * gam[r].x + gam[r].y * gam[r].y;
-    top = fmax(top, g2 * (double)c1[o]);
-  }
-  top = warp_max(top);
-  if ((tid & 31) == 0) red[tid >> 5] = top;
-  __syncthreads();
-  if (tid == 0) {
-    double tt = 0.0;
-    for (int w = 0; w < (NT >> 5); ++w) tt = fmax(tt, red[w]);
-    double m = 0.0, alpha = 0.0;
-    if (nmeas > 0) {
-      if (step_mode == TT_STEP_HESSIAN) {
-        alpha = fmin(fmax(lam / (double)t + tt, c_floor), c_cap);
-        const double ab = alpha_bar[0] + alpha;
-        alpha_bar[0] = ab;
-        m = 1.0 / ab;
-      } else {
-        m = mu;
-      }
+  const double lt = lam / (double)t;
+  double m = 0.0, alpha = 0.0, ab = scal[4];
+  if (nmeas > 0) {
+    if (step_mode == TT_STEP_HESSIAN) {
+      const double top = __longlong_as_double(((const long long*)scal)[2]);
+      alpha = fmin(fmax(lt + top, c_floor), c_cap);
+      ab += alpha;
+      m = 1.0 / ab;
+    } else {
+      m = mu_fixed;
     }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    alpha_bar[0] = ab;
     scal[1] = m;
     if (mu_out) mu_out[0] = m;
     if (alpha_out) alpha_out[0] = alpha;
   }
-}
-
-__global__ void ent_update_kernel(int nx, int ny, int R, double lam, long long t, const double* scal,
-                                  const double2* gam, const float2* __restrict__ ah, const float2* __restrict__ bh,
-                                  const float2* __restrict__ P, const float2* __restrict__ Q, float2* ah_out,
-                                  float2* bh_out) {
-  const double m = scal[1];
-  const float cfac = (float)(1.0 - m * lam / (double)t);
+  const float cfac = (float)(1.0 - m * lt);
   const float muf = (float)m;
   const int na = nx * R, nbb = ny * R;
   for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < na + nbb; o += gridDim.x * blockDim.x) {
     if (o < na) {
       const int r = o % R;
       const float2 g = cconj(to_f2(gam[r]));
-      ah_out[o] = cadd(cscale(ah[o], cfac), cscale(cmul(g, P[o]), muf));
+      ah_out[o] = nmeas > 0 ? cadd(cscale(ah[o], cfac), cscale(cmul(g, P[o]), muf)) : ah[o];
     } else {
       const int k = o - na, r = k % R;
       const float2 g = cconj(to_f2(gam[r]));
-      bh_out[k] = cadd(cscale(bh[k], cfac), cscale(cmul(g, Q[k]), muf));
+      bh_out[k] = nmeas > 0 ? cadd(cscale(bh[k], cfac), cscale(cmul(g, Q[k]), muf)) : bh[k];
     }
   }
 }
@@ -356,73 +400,55 @@ extern "C" int tt_track_entries(void* stream, const tt_entries_args* a) {
   const EntScratch S = ent_layout(nx, ny, R);
   unsigned char* sb = (unsigned char*)a->scratch;
   double2* gp = (double2*)(sb + S.gp);
-  double2* hp = (double2*)(sb + S.hp);
-  double* yp = (double*)(sb + S.yp);
   double2* gam = (double2*)(sb + S.gam);
   double* scal = (double*)(sb + S.scal);
   float2* xi = (float2*)(sb + S.xi);
-  float* mk = (float*)(sb + S.mk);
+  int* stp = (int*)(sb + S.st);
   float2* P = (float2*)(sb + S.P);
   float2* Q = (float2*)(sb + S.Q);
-  float* c0 = (float*)(sb + S.c0);
-  float* c1 = (float*)(sb + S.c1);
-  const int Rp = R * (R + 1) / 2;
+  const int Rp = R * (R + 1) / 2, NI2 = Rp + R + 1;
   const float2* ah = (const float2*)a->ah_in;
   const float2* bh = (const float2*)a->bh_in;
-  int nb = 0;
-  if (L > 0) {
-    nb = (L + 255) / 256;
-    if (nb > ENT_NB) nb = ENT_NB;
-    const size_t sm = sizeof(double2) * (ENT_TL * (size_t)R + ENT_TL) + sizeof(double) * 64;
-    static int set_gram = -1;
-    if (set_gram < (int)sm) {
+  // gram: clusters of 8 CTAs, about EG_PER entries per CTA, at most EG_NCL clusters
+  int ncl = (L + EG_CL * EG_PER - 1) / (EG_CL * EG_PER);
+  if (ncl < 1) ncl = 1;
+  if (ncl > EG_NCL) ncl = EG_NCL;
+  {
+    const size_t sm = gram_smem(R);
+    static size_t set_gram = 0;
+    if (sm > set_gram) {
       TT_CUDA_TRY(cudaFuncSetAttribute(ent_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      set_gram = (int)sm;
+      set_gram = sm;
     }
-    ent_gram_kernel<<<nb, ENT_NT, sm, st>>>(L, Ld, R, ah, bh, a->idx, (const float2*)a->y, gp, hp, yp);
+    ent_gram_kernel<<<ncl * EG_CL, ENT_NT, sm, st>>>(L, Ld, nx, ny, R, ah, bh, a->idx, (const float2*)a->y, gp);
   }
   {
-    const size_t sm = sizeof(double2) * (Rp + 2 * (size_t)R) + sizeof(double) * 64 + sizeof(double2) * 4 * (R + 1);
-    static int set_solve = -1;
-    if (set_solve < (int)sm) {
+    const size_t sm = sizeof(double2) * ((size_t)NI2 + R + 4 * (size_t)(R + 1));
+    static size_t set_solve = 0;
+    if (sm > set_solve) {
       TT_CUDA_TRY(cudaFuncSetAttribute(ent_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      set_solve = (int)sm;
+      set_solve = sm;
     }
-    ent_solve_kernel<<<1, ENT_NT, sm, st>>>(nx, ny, R, L, Ld, nb, a->lam, (long long)a->t, ah, bh, gp, hp, yp, gam, scal,
+    ent_solve_kernel<<<1, ENT_NT, sm, st>>>(R, L, Ld, ncl, a->lam, (long long)a->t, gp, a->alpha_bar, gam, scal,
                                             (float2*)a->gamma_out, a->cost_out, a->status);
   }
-  if (L == 0) {
-    // empty batch: no update (tracker.py:380-384)
-    ent_step_kernel<<<1, ENT_NT, 0, st>>>(0, 0, R, 0, nullptr, a->lam, (long long)a->t, a->step_mode, a->mu, a->c_floor,
-                                          a->c_cap, gam, c0, c1, a->alpha_bar, scal, a->mu_out, a->alpha_out);
-    if (a->ah_out != a->ah_in)
-      TT_CUDA_TRY(cudaMemcpyAsync(a->ah_out, a->ah_in, sizeof(float2) * (size_t)nx * R, cudaMemcpyDeviceToDevice, st));
-    if (a->bh_out != a->bh_in)
-      TT_CUDA_TRY(cudaMemcpyAsync(a->bh_out, a->bh_in, sizeof(float2) * (size_t)ny * R, cudaMemcpyDeviceToDevice, st));
-    TT_CUDA_TRY(cudaGetLastError());
-    return TT_OK;
-  }
-  TT_CUDA_TRY(cudaMemsetAsync(xi, 0, sizeof(float2) * (size_t)nx * ny, st));
-  TT_CUDA_TRY(cudaMemsetAsync(mk, 0, sizeof(float) * (size_t)nx * ny, st));
-  {
+  if (L > 0) {
     int blocks = (L + 255) / 256;
     if (blocks > 1184) blocks = 1184;
-    ent_resid_kernel<<<blocks, 256, 0, st>>>(L, Ld, ny, R, ah, bh, a->idx, (const float2*)a->y, gam, xi, mk,
+    ent_resid_kernel<<<blocks, 256, 0, st>>>(L, Ld, ny, R, ah, bh, a->idx, (const float2*)a->y, gam, scal, xi, stp,
                                              (float2*)a->resid_out);
-  }
-  {
     const int m = (nx > ny ? nx : ny) * R;
     dim3 grid((m + BP_O - 1) / BP_O, 2);
-    ent_backproj_kernel<<<grid, dim3(BP_O, BP_K), 0, st>>>(nx, ny, R, ah, bh, xi, mk, P, Q, c0, c1);
+    ent_backproj_kernel<<<grid, dim3(BP_O, BP_K), 0, st>>>(nx, ny, R, a->step_mode == TT_STEP_HESSIAN, ah, bh, xi,
+                                                          stp, gam, scal, P, Q);
   }
-  ent_step_kernel<<<1, ENT_NT, 0, st>>>(nx, ny, R, L, Ld, a->lam, (long long)a->t, a->step_mode, a->mu, a->c_floor,
-                                        a->c_cap, gam, c0, c1, a->alpha_bar, scal, a->mu_out, a->alpha_out);
   {
     const int n = (nx + ny) * R;
     int blocks = (n + 255) / 256;
     if (blocks > 1184) blocks = 1184;
-    ent_update_kernel<<<blocks, 256, 0, st>>>(nx, ny, R, a->lam, (long long)a->t, scal, gam, ah, bh, P, Q,
-                                              (float2*)a->ah_out, (float2*)a->bh_out);
+    ent_update_kernel<<<blocks, 256, 0, st>>>(nx, ny, R, L, Ld, a->lam, (long long)a->t, a->step_mode, a->mu,
+                                              a->c_floor, a->c_cap, scal, a->alpha_bar, gam, ah, bh, P, Q,
+                                              (float2*)a->ah_out, (float2*)a->bh_out, a->mu_out, a->alpha_out);
   }
   TT_CUDA_TRY(cudaGetLastError());
   return TT_OK;

@@ -323,8 +323,8 @@ class EntryEngine:
             raise TypeError("policy must be InformativeEntries or StaticEntries")
         self.idx = torch.zeros(self.cap, 2, **i32)
         self.y = torch.zeros(self.cap, dtype=torch.complex64, device=self.dev)
-        self.scr = torch.empty(int(L.lib().tt_entries_scratch_bytes(self.nx, self.ny, self.rank, self.cap)),
-                               dtype=torch.uint8, device=self.dev)
+        self.scr = torch.zeros(int(L.lib().tt_entries_scratch_bytes(self.nx, self.ny, self.rank, self.cap)),
+                               dtype=torch.uint8, device=self.dev)  # zero-filled before first use (frame stamps)
         self.ah = torch.zeros(self.nx, self.rank, dtype=torch.complex64, device=self.dev)
         self.bh = torch.zeros(self.ny, self.rank, dtype=torch.complex64, device=self.dev)
         self.alpha_bar = torch.zeros(1, dtype=torch.float64, device=self.dev)
