@@ -12,7 +12,11 @@
 
 #include <stdlib.h>
 
+#include <cooperative_groups.h>
+
 #include "tt_block.cuh"
+
+namespace cg = cooperative_groups;
 
 #define SMP_NT 256
 
@@ -30,12 +34,16 @@ TT_DEV bool row_energies(const float2* a, int n, int R, double* colsq, double* e
     if (lane == 0) colsq[r] = acc;
   }
   __syncthreads();
-  if (tid < R && colsq[tid] == 0.0) *sh_zero = 1;
+  if (tid < R) {  // reciprocal squared column norms, once per column
+    if (colsq[tid] == 0.0) *sh_zero = 1;
+    colsq[tid] = colsq[tid] > 0.0 ? 1.0 / colsq[tid] : 0.0;
+  }
+  __syncthreads();
   for (int i = tid; i < n; i += NT) {
     double e = 0.0;
     for (int r = 0; r < R; ++r) {
       const float2 v = a[(size_t)i * R + r];
-      if (colsq[r] > 0.0) e += ((double)v.x * v.x + (double)v.y * v.y) / colsq[r];
+      e += ((double)v.x * v.x + (double)v.y * v.y) * colsq[r];
     }
     en[i] = e;
   }
@@ -75,25 +83,31 @@ __global__ void __launch_bounds__(SMP_NT) row_scores_kernel(int nx, int ny, int 
   for (int i = threadIdx.x; i < nx; i += blockDim.x) out[i] = p[i] / s2;
 }
 
-// entry scores: en_a (nx), en_b (ny) then the nx x ny map, normalised twice
-__global__ void __launch_bounds__(SMP_NT) entry_energy_kernel(int nx, int ny, int R, const float2* __restrict__ a,
-                                                              const float2* __restrict__ b, double* __restrict__ ws,
-                                                              int32_t* status) {
+// entry scores: en_a (nx), en_b (ny) then the nx x ny map, normalised twice. A two-CTA cluster:
+// CTA 0 scores the rows of a, CTA 1 those of b; CTA 0 combines the two sums through DSMEM.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SMP_NT)
+    entry_energy_kernel(int nx, int ny, int R, const float2* __restrict__ a, const float2* __restrict__ b,
+                        double* __restrict__ ws, int32_t* status) {
   extern __shared__ __align__(16) unsigned char smem[];
   double* colsq = (double*)smem;
   double* red = colsq + R;
   __shared__ int sh_zero;
-  const bool oka = row_energies(a, nx, R, colsq, ws, red, &sh_zero);
-  __syncthreads();
-  const bool okb = row_energies(b, ny, R, colsq, ws + nx, red, &sh_zero);
-  if ((!oka || !okb) && threadIdx.x == 0 && status) atomicOr(status, TT_ST_ZEROCOL);
+  __shared__ double sh_sum;
+  cg::cluster_group cl = cg::this_cluster();
+  const int k = (int)cl.block_rank();
+  const int n = k ? ny : nx;
+  const bool ok = row_energies(k ? b : a, n, R, colsq, ws + (k ? nx : 0), red, &sh_zero);
+  if (!ok && threadIdx.x == 0 && status) atomicOr(status, TT_ST_ZEROCOL);
   // total of raw scores: sum_ij (ea_i + eb_j) / (R (nx+ny)) = (ny sum ea + nx sum eb) / (R (nx+ny))
-  const double sa = chunk_sum(ws, nx, red);
-  const double sb = chunk_sum(ws + nx, ny, red);
-  if (threadIdx.x == 0) {
+  const double sk = chunk_sum(ws + (k ? nx : 0), n, red);
+  if (threadIdx.x == 0) sh_sum = sk;
+  cl.sync();
+  if (k == 0 && threadIdx.x == 0) {
+    const double sb = *cl.map_shared_rank(&sh_sum, 1);
     const double den = (double)R * (double)(nx + ny);
-    ws[nx + ny] = ((double)ny * sa + (double)nx * sb) / den;
+    ws[nx + ny] = ((double)ny * sh_sum + (double)nx * sb) / den;
   }
+  cl.sync();
 }
 
 // blended probabilities (sampler.py:88-92) and their per-block partial sums (fixed order)
@@ -259,7 +273,7 @@ static int entry_scores_run(cudaStream_t st, int nx, int ny, int rank, const flo
                             double* probs_out, int32_t* status, double* ws) {
   void* stream = (void*)st;
   const size_t sm = sizeof(double) * ((size_t)rank + 64);
-  entry_energy_kernel<<<1, SMP_NT, sm, (cudaStream_t)stream>>>(nx, ny, rank, (const float2*)a, (const float2*)b, ws,
+  entry_energy_kernel<<<2, SMP_NT, sm, (cudaStream_t)stream>>>(nx, ny, rank, (const float2*)a, (const float2*)b, ws,
                                                                 status);
   const size_t n = (size_t)nx * ny;
   int blocks = (int)((n + SMP_NT - 1) / SMP_NT);
@@ -394,11 +408,15 @@ TT_DEV double big_bound(int i, int n, double x, double depth_term) {
 __global__ void big_draw_kernel(int n, int ndraw, const double* __restrict__ cdf, const double* __restrict__ off,
                                 int nb, const int* __restrict__ forced, int nforced, uint64_t k0, uint64_t k1,
                                 const uint64_t* __restrict__ pos, int* __restrict__ flags, int* __restrict__ ctl,
-                                double depth_term, double gscale) {
+                                double depth_term, double gscale, int lstride) {
+  // coarse copy of the CDF in shared memory: the last value of every 2^lstride-entry chunk; a draw
+  // searches the chunks there and only lstride levels in global memory
+  extern __shared__ double coarse[];
+  const int sw = 1 << lstride, nc = (n + sw - 1) >> lstride;
+  for (int k = threadIdx.x; k < nc; k += blockDim.x) coarse[k] = big_cdf(cdf, off, min(((k + 1) << lstride) - 1, n - 1));
+  __syncthreads();
   const double total = off[nb];
   const uint64_t p0 = pos[0];
-  int top = 1;
-  while (2 * top <= n) top *= 2;
   for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < ndraw + nforced; m += gridDim.x * blockDim.x) {
     if (m >= ndraw) {
       const int f = forced[m - ndraw];
@@ -407,10 +425,23 @@ __global__ void big_draw_kernel(int n, int ndraw, const double* __restrict__ cdf
     }
     const double u = philox_uniform(k0, k1, p0 + (uint64_t)m);
     const double ut = u * total;
-    int q = -1;  // last index with cdf <= u (normalised)
-    for (int step = top; step > 0; step >>= 1) {
-      const int cand = q + step;
-      if (cand < n && big_cdf(cdf, off, cand) <= ut) q = cand;
+    int lo = 0, hi = nc;  // first chunk whose last value exceeds ut
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (coarse[mid] <= ut) lo = mid + 1;
+      else hi = mid;
+    }
+    int q;  // last index with cdf <= u (normalised)
+    if (lo == nc) {
+      q = n - 1;
+    } else {
+      const int base = lo << lstride, end = min(base + sw, n);
+      q = base - 1;
+      for (int step = sw >> 1; step > 0; step >>= 1) {
+        const int cand = q + step;
+        if (cand < end && big_cdf(cdf, off, cand) <= ut) q = cand;
+      }
+      if (q + 1 < end && big_cdf(cdf, off, q + 1) <= ut) q = q + 1;  // chunk of one past the halvings
     }
     const int idx = min(q + 1, n - 1);
     bool amb = false;
@@ -606,8 +637,11 @@ extern "C" int tt_draw_with_replacement_large(void* stream, int n, const double*
     int blocks = (ndraw + nforced + 255) / 256;
     if (blocks < 1) blocks = 1;
     if (blocks > 1184) blocks = 1184;
-    big_draw_kernel<<<blocks, 256, 0, st>>>(n, ndraw, cdf, off, nb, forced, nforced, key0, key1, pos, flags, ctl,
-                                            depth_term, gscale);
+    int ls = 4;  // at most 4096 coarse values (32 KB)
+    while (((n + (1 << ls) - 1) >> ls) > 4096) ++ls;
+    const size_t csm = sizeof(double) * (size_t)((n + (1 << ls) - 1) >> ls);
+    big_draw_kernel<<<blocks, 256, csm, st>>>(n, ndraw, cdf, off, nb, forced, nforced, key0, key1, pos, flags, ctl,
+                                              depth_term, gscale, ls);
   }
   {  // exact fallback (each part exits at once unless a draw was ambiguous)
     big_exact_kernel<<<1, SMP_NT, 0, st>>>(n, probs, cdf, ctl);
