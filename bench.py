@@ -319,12 +319,14 @@ def run_entries(args, cfg):
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         for i in range(args.warmup):
-            graphs[i]._graph[0].replay()
+            for g, _, _ in graphs[i]._graph[0]:
+                g.replay()
         for i in range(args.steps):
             flush.zero_()
             a, b = ev[i]
             a.record(stream)
-            graphs[args.warmup + i]._graph[0].replay()
+            for g, _, _ in graphs[args.warmup + i]._graph[0]:
+                g.replay()
             b.record(stream)
         torch.cuda.synchronize()
     if world > 1:

@@ -340,13 +340,16 @@ class EntryEngine:
         self.ah = K.fft_cols_(a.to(self.dev, torch.complex64).reshape(self.nx, self.rank).contiguous())
         self.bh = K.fft_cols_(b.to(self.dev, torch.complex64).reshape(self.ny, self.rank).contiguous())
 
-    def rerun(self, A, B) -> dict:
+    def rerun(self, A, B, gate=None, done=None) -> dict:
         """Restart from image factors (A, B) and replay the sequence captured by the last
         ``run(graph=True)`` over the same resident truth buffer (whose contents may have changed):
-        state reset, frame 0 eagerly, the captured frames replayed. Returns that run's outputs."""
+        state reset, frame 0 eagerly, the captured blocks replayed. ``gate(f)`` is called before the
+        work that first reads truth frame f is enqueued (a pipelined caller makes the stream wait
+        for that frame's upload); ``done(b)`` after the frames before b are enqueued. Returns that
+        run's outputs."""
         if getattr(self, "_graph", None) is None:
             raise RuntimeError("rerun needs a previous run(graph=True)")
-        g, keep, ks, frames, out = self._graph
+        gs, keep, ks, frames, out = self._graph
         self.set_image_factors(A, B)
         self.alpha_bar.zero_()
         self.pos.zero_()
@@ -354,8 +357,17 @@ class EntryEngine:
         self.t, self.frame = self._t0, 0
         P = self._P
         P["ah0"], P["bh0"] = self.ah.data_ptr(), self.bh.data_ptr()
+        if gate:
+            gate(0)
         self._frame(ks.data_ptr(), 0, P, [])
-        g.replay()
+        if done and gs[0][1] > 1:
+            done(1)
+        for g, a, b in gs:
+            if gate:
+                gate(b - 1)
+            g.replay()
+            if done:
+                done(b)
         self.t += frames - 1
         self.ah = out["ah"][frames - 1, 0].clone()
         self.bh = out["bh"][frames - 1, 0].clone()
@@ -412,9 +424,12 @@ class EntryEngine:
         L.check(lib.tt_track_entries(st, C.byref(a)), "track_entries")
         self.t += 1
 
-    def run(self, kspace: torch.Tensor, frames: int, out: dict | None = None, graph: bool = True) -> dict:
+    def run(self, kspace: torch.Tensor, frames: int, out: dict | None = None, graph: bool = True,
+            blocks: list | None = None) -> dict:
         """Advance ``frames`` frames; ``kspace`` (T, nx, ny) complex64 resident truth, frames from the
-        current index. With ``graph`` the chain after the first frame is captured once and replayed."""
+        current index. With ``graph`` the chain after the first frame is captured once and replayed;
+        ``blocks`` (frame ranges [a, b) covering [1, frames)) captures one graph per range, so a
+        pipelined caller can start each block once its truth has arrived (``rerun(..., gate=...)``)."""
         ks = kspace.reshape(kspace.shape[0], self.nx, self.ny)
         if ks.dtype != torch.complex64 or not ks.is_cuda or not ks.is_contiguous():
             raise TypeError("kspace must be a contiguous complex64 CUDA tensor (T, nx, ny)")
@@ -438,14 +453,22 @@ class EntryEngine:
             self._frame(kbase + (f0 + fo) * kstride, fo, P, keep)
         rest = frames - first
         if rest > 0 and graph:
-            g = torch.cuda.CUDAGraph()
+            ranges = blocks if blocks else [(first, frames)]
+            if ranges[0][0] != first or ranges[-1][1] != frames or any(
+                    x[1] != y[0] for x, y in zip(ranges, ranges[1:])):
+                raise ValueError("graph blocks must cover frames [1, frames) in order")
             t_save = self.t
-            with torch.cuda.graph(g):
-                for fo in range(first, frames):
-                    self._frame(kbase + (f0 + fo) * kstride, fo, P, keep)
-            self._graph = (g, keep, ks, frames, out)  # the captured argument blocks must outlive the replay
+            gs = []
+            for (a, b) in ranges:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    for fo in range(a, b):
+                        self._frame(kbase + (f0 + fo) * kstride, fo, P, keep)
+                gs.append((g, a, b))
+            self._graph = (gs, keep, ks, frames, out)  # the captured argument blocks must outlive the replay
             self._P = P
-            g.replay()
+            for g, _, _ in gs:
+                g.replay()
             assert self.t == t_save + rest
         else:
             for fo in range(first, frames):
@@ -754,40 +777,89 @@ def _run_online_entries(src, on_dev, A0, B0, lam, step, policy, clean, t0, warm_
         raise ValueError("warm-up applies to the row-mask engine")
     R = A0.shape[-1]
     # repeated calls with the same shapes, policy and length reuse the engine, its resident truth buffer
-    # and its captured frame graph (like an FFT plan): upload, replay, download
+    # and its captured frame graphs (like an FFT plan). The call is pipelined in blocks of frames:
+    # uploads on a copy stream, each block's graph replayed once its truth landed, the block's
+    # images reconstructed on a second stream and downloaded into pinned memory on a third.
     key = (nx, ny, R, T, float(lam), repr(step), repr(policy), int(t0), torch.cuda.current_device())
+    ub = _blocks(0, T, 40)  # upload / reconstruction / download blocks
+    dev = L.device()
+    pinned = lambda shape, dt: torch.empty(shape, dtype=dt, pin_memory=True)  # noqa: E731
+    X = torch.empty(T, 1, nx, ny, dtype=torch.complex64, device=dev)
+    Xh = pinned((T, 1, nx, ny), torch.complex64)
     hit = _ENTRY_PLANS.get(key)
+    comp = torch.cuda.current_stream()
     if hit is not None:
-        eng, kd = hit
-        kd.copy_(src.reshape(T, nx, ny), non_blocking=True)
-        out = eng.rerun(A0.reshape(nx, R), np.asarray(B0).reshape(ny, R))
+        eng, kd, streams = hit
+        s_in, s_rec, s_out = streams
+        ev_up = [torch.cuda.Event() for _ in ub]
+        with torch.cuda.stream(s_in):
+            s_in.wait_stream(comp)  # the previous call's replays have read the buffer
+            for k, (a, b) in enumerate(ub):
+                kd[a:b].copy_(src.reshape(T, nx, ny)[a:b], non_blocking=True)
+                ev_up[k].record(s_in)
+        blk_of = lambda f: next(k for k, (a, b) in enumerate(ub) if a <= f < b)  # noqa: E731
+        waited = set()
+        pending = list(range(len(ub)))
+
+        def gate(f):
+            k = blk_of(f)
+            for j in range(k + 1):
+                if j not in waited:
+                    comp.wait_event(ev_up[j])
+                    waited.add(j)
+
+        outs = {}
+
+        def done(fend):  # frames [0, fend) are enqueued: reconstruct and download finished blocks
+            ev = torch.cuda.Event()
+            ev.record(comp)
+            while pending and ub[pending[0]][1] <= fend:
+                k = pending.pop(0)
+                a, b = ub[k]
+                s_rec.wait_event(ev)
+                with torch.cuda.stream(s_rec):
+                    o = outs["out"]
+                    A = K.fft_cols(o["ah"][a:b], inverse=True).reshape(b - a, nx, R)
+                    Bm = K.fft_cols(o["bh"][a:b], inverse=True).reshape(b - a, ny, R)
+                    X[a:b] = K.reconstruct(A, Bm, o["gamma"][a:b].reshape(b - a, R)).reshape(b - a, 1, nx, ny)
+                    er = torch.cuda.Event()
+                    er.record(s_rec)
+                s_out.wait_event(er)
+                with torch.cuda.stream(s_out):
+                    Xh[a:b].copy_(X[a:b], non_blocking=True)
+
+        outs["out"] = eng._graph[4]
+        out = eng.rerun(A0.reshape(nx, R), np.asarray(B0).reshape(ny, R), gate=gate, done=done)
+        comp.wait_stream(s_out)
+        comp.wait_stream(s_rec)
     else:
         eng = EntryEngine(nx, ny, R, lam, step, policy, t0)
         eng.set_image_factors(A0.reshape(nx, R), np.asarray(B0).reshape(ny, R))
         kd = torch.empty(T, nx, ny, dtype=torch.complex64, device=eng.dev)
         kd.copy_(src.reshape(T, nx, ny), non_blocking=True)
-        out = eng.run(kd, T, graph=T > 1)
+        gblocks = [(max(a, 1), b) for a, b in ub if b > 1]
+        out = eng.run(kd, T, graph=T > 1, blocks=gblocks if T > 1 else None)
+        X.copy_(eng.reconstruct(out))
+        Xh.copy_(X, non_blocking=True)
         if T > 1:
             if len(_ENTRY_PLANS) >= 2:
                 _ENTRY_PLANS.pop(next(iter(_ENTRY_PLANS)))
-            _ENTRY_PLANS[key] = (eng, kd)
-    X = eng.reconstruct(out)
+            _ENTRY_PLANS[key] = (eng, kd, (torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()))
     nm = None
     if clean is not None:
         cl = torch.as_tensor(np.asarray(clean, dtype=np.complex64)).to(eng.dev).reshape(T, 1, nx, ny)
         num = (cl - X).abs().pow(2).sum(dim=(-1, -2)).double()
         den = cl.abs().pow(2).sum(dim=(-1, -2)).double()
         nm = (num / den).cpu().numpy()
-    # asynchronous downloads into pinned memory, one synchronisation
-    pinned = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True)  # noqa: E731
+    # the small results: asynchronous copies into pinned memory, one synchronisation
     Ad, Bd = eng.image_factors()
-    host = {k: pinned(v) for k, v in (("recon", X), ("gamma", out["gamma"]), ("cost", out["cost"]),
-                                      ("mu", out["mu"]), ("cnt", out["cnt"]), ("rows", out["rows"]),
-                                      ("A", Ad), ("B", Bd), ("st", eng.status))}
-    for k, v in (("recon", X), ("gamma", out["gamma"]), ("cost", out["cost"]), ("mu", out["mu"]),
-                 ("cnt", out["cnt"]), ("rows", out["rows"]), ("A", Ad), ("B", Bd), ("st", eng.status)):
+    small = (("gamma", out["gamma"]), ("cost", out["cost"]), ("mu", out["mu"]), ("cnt", out["cnt"]),
+             ("rows", out["rows"]), ("A", Ad), ("B", Bd), ("st", eng.status))
+    host = {k: pinned(tuple(v.shape), v.dtype) for k, v in small}
+    for k, v in small:
         host[k].copy_(v, non_blocking=True)
-    torch.cuda.current_stream().synchronize()
+    comp.synchronize()
+    host["recon"] = Xh
     L.raise_status(int(host["st"].max().item()), "entry engine")
     cnt = host["cnt"].numpy()
     rows_np = host["rows"].numpy()
