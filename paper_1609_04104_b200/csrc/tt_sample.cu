@@ -463,7 +463,8 @@ __global__ void big_draw_kernel(int n, int ndraw, const double* __restrict__ cdf
 // and stores its results straight to global memory while warps 1.. stage the next chunk into the
 // other buffer, so the chain never waits on a load. cdf[n] = cdf[-1] for the normalisation pass.
 __global__ void __launch_bounds__(SMP_NT) big_exact_kernel(int n, const double* __restrict__ p,
-                                                           double* __restrict__ cdf, const int* __restrict__ ctl) {
+                                                           double* __restrict__ cdf, int* __restrict__ flags,
+                                                           const int* __restrict__ ctl) {
   if (ctl[0] == 0) return;
   constexpr int CH = 2048;
   __shared__ __align__(16) double buf[2][CH];
@@ -515,33 +516,31 @@ __global__ void __launch_bounds__(SMP_NT) big_exact_kernel(int n, const double* 
     __syncthreads();
   }
   if (tid == 0) cdf[n] = c;
+  for (int i = tid; i < n; i += SMP_NT) flags[i] = 0;  // the redo re-marks every draw
 }
 
-// exact fallback, part 2 (grid): cdf /= cdf[-1] (numpy's normalisation) and the flags cleared
-__global__ void big_exact_norm_kernel(int n, double* __restrict__ cdf, int* __restrict__ flags,
-                                      const int* __restrict__ ctl) {
-  if (ctl[0] == 0) return;
-  const double last = cdf[n];
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    cdf[i] = cdf[i] / last;
-    flags[i] = 0;
-  }
-}
-
-// exact fallback, part 3 (grid): every draw redone against numpy's CDF, forced entries re-marked
+// exact fallback, part 2 (grid): every draw redone against numpy's CDF, cdf[i] / cdf[-1] evaluated at
+// each probe (the same rounding as numpy's cdf /= cdf[-1]), forced entries re-marked
 __global__ void big_exact_redo_kernel(int n, int ndraw, const double* __restrict__ cdf,
                                       const int* __restrict__ forced, int nforced, uint64_t k0, uint64_t k1,
                                       const uint64_t* __restrict__ pos, int* __restrict__ flags,
                                       const int* __restrict__ ctl) {
   if (ctl[0] == 0) return;
+  const double last = cdf[n];
   for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < ndraw + nforced; m += gridDim.x * blockDim.x) {
     if (m >= ndraw) {
       const int f = forced[m - ndraw];
       if (f >= 0 && f < n) flags[f] = 1;
       continue;
     }
-    const int idx = upper_bound_d(cdf, n, philox_uniform(k0, k1, pos[0] + (uint64_t)m));
-    flags[idx < n ? idx : n - 1] = 1;
+    const double u = philox_uniform(k0, k1, pos[0] + (uint64_t)m);
+    int lo = 0, hi = n;  // searchsorted(cdf / cdf[-1], u, 'right')
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (cdf[mid] / last <= u) lo = mid + 1;
+      else hi = mid;
+    }
+    flags[lo < n ? lo : n - 1] = 1;
   }
 }
 
@@ -644,10 +643,7 @@ extern "C" int tt_draw_with_replacement_large(void* stream, int n, const double*
                                               depth_term, gscale, ls);
   }
   {  // exact fallback (each part exits at once unless a draw was ambiguous)
-    big_exact_kernel<<<1, SMP_NT, 0, st>>>(n, probs, cdf, ctl);
-    int nbk = (n + 255) / 256;
-    if (nbk > 1184) nbk = 1184;
-    big_exact_norm_kernel<<<nbk, 256, 0, st>>>(n, cdf, flags, ctl);
+    big_exact_kernel<<<1, SMP_NT, 0, st>>>(n, probs, cdf, flags, ctl);
     int rbk = (ndraw + nforced + 255) / 256;
     if (rbk < 1) rbk = 1;
     if (rbk > 1184) rbk = 1184;
