@@ -231,6 +231,10 @@ static __device__ __noinline__ void write_residual(const tt_rows_args& a, const 
 }
 
 // ---------------------------------------------------------------- the kernel
+// SOLV: the one solver compiled in (1 / 2 / 5: Gauss-Jordan entries per thread, 9: 2x2-blocked LDL^H);
+// SHARD: whether the row-sharding phases are compiled in. Every inlined variant costs
+// instruction-cache lines in the frame loop, so each launch gets only the code it runs.
+template <int SOLV, bool SHARD>
 __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_constant__ tt_rows_args a,
                                                              const __grid_constant__ RowsPlan pl) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -244,7 +248,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
   // shard_local every rank of the sharding is a cluster of this launch (one GPU, several clusters);
   // each reads the full Ah at its row offset, has its own scratch and payload slot, and only rank 0
   // writes the replicated outputs (Bh, gamma, cost, step state).
-  const bool shard = a.shard_world > 0;
+  const bool shard = SHARD && a.shard_world > 0;
   const bool multi = shard && a.shard_local != 0;
   const int s = multi ? 0 : qid;  // slice
   const int srank = multi ? qid : a.shard_rank;
@@ -860,10 +864,9 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         // Gauss-Jordan (R parallel steps, no back substitution) up to R = 32; the 2x2-blocked
         // LDL^H has fewer flops per step and wins beyond (profiles/tools/ubench_gj.cu)
         // (few instantiations: every inlined variant costs instruction-cache lines in the frame loop)
-        const int ept = gj_ept(R, ROWS_NT);
-        if (ept <= 1) block_gj_solve<1>(G, hv, gam, colb, R);
-        else if (ept <= 2) block_gj_solve<2>(G, hv, gam, colb, R);
-        else if (ept <= 5) block_gj_solve<5>(G, hv, gam, colb, R);
+        if (SOLV == 1) block_gj_solve<1>(G, hv, gam, colb, R);
+        else if (SOLV == 2) block_gj_solve<2>(G, hv, gam, colb, R);
+        else if (SOLV == 5) block_gj_solve<5>(G, hv, gam, colb, R);
         else block_ldl2_solve<9>(G, hv, gam, colb, blk, zf, R);
       }
       STAMP(12);
@@ -1086,11 +1089,19 @@ extern "C" int tt_track_rows(void* stream, const tt_rows_args* a) {
   int rc = rows_choose_cluster(a->nx, a->ny, a->rank, a->max_rows, a->cluster, &pl);
   if (rc) return rc;
   if (a->cluster > 0 && a->cluster != pl.CL) return tt_fail(TT_EINVAL, "cluster mismatch");
-  static int configured_smem = -1;
-  if (configured_smem < pl.smem) {
-    TT_CUDA_TRY(cudaFuncSetAttribute(tt_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
-    TT_CUDA_TRY(cudaFuncSetAttribute(tt_rows_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    configured_smem = pl.smem;
+  // the instantiation: solver by Gauss-Jordan entries per thread, sharding phases only when sharded
+  typedef void (*RowsFn)(const tt_rows_args, const RowsPlan);
+  static const RowsFn fns[8] = {tt_rows_kernel<1, false>, tt_rows_kernel<2, false>, tt_rows_kernel<5, false>,
+                                tt_rows_kernel<9, false>, tt_rows_kernel<1, true>,  tt_rows_kernel<2, true>,
+                                tt_rows_kernel<5, true>,  tt_rows_kernel<9, true>};
+  static int configured_smem[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+  const int ept = gj_ept(a->rank, ROWS_NT);
+  const int which = (ept <= 1 ? 0 : ept <= 2 ? 1 : ept <= 5 ? 2 : 3) + (a->shard_world > 0 ? 4 : 0);
+  const RowsFn fn = fns[which];
+  if (configured_smem[which] < pl.smem) {
+    TT_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
+    TT_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    configured_smem[which] = pl.smem;
   }
   cudaLaunchConfig_t cfg = {};
   const int nclusters = (a->shard_world > 0 && a->shard_local) ? a->shard_world : a->nslices;
@@ -1105,6 +1116,6 @@ extern "C" int tt_track_rows(void* stream, const tt_rows_args* a) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  TT_CUDA_TRY(cudaLaunchKernelEx(&cfg, tt_rows_kernel, *a, pl));
+  TT_CUDA_TRY(cudaLaunchKernelEx(&cfg, fn, *a, pl));
   return TT_OK;
 }
