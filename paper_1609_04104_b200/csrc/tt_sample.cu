@@ -344,7 +344,7 @@ static BigDrawScratch big_layout(int n) {
 
 // level 1: block-local inclusive scan (thread-sequential chunks, fixed order) and block totals
 __global__ void __launch_bounds__(SMP_NT) big_scan_kernel(int n, const double* __restrict__ p, double* __restrict__ cdf,
-                                                          double* __restrict__ part) {
+                                                          double* __restrict__ part, int* __restrict__ ctl) {
   __shared__ double red[64];
   const int tid = threadIdx.x;
   const int base = blockIdx.x * SMP_NT * BIG_IPT + tid * BIG_IPT;
@@ -363,12 +363,12 @@ __global__ void __launch_bounds__(SMP_NT) big_scan_kernel(int n, const double* _
     if (base + q < n) cdf[base + q] = run;
   }
   if (tid == 0) part[blockIdx.x] = tot;
+  if (blockIdx.x == 0 && tid == 0) ctl[0] = 0;  // the draw raises it for an ambiguous uniform
 }
 
-// level 2: exclusive offsets of the block totals (one block, fixed order); off[nb] = grand total
-__global__ void __launch_bounds__(SMP_NT) big_offsets_kernel(int nb, const double* __restrict__ part,
-                                                             double* __restrict__ off, int* __restrict__ ctl) {
-  __shared__ double red[64];
+// level 2: exclusive offsets of the block totals (block-wide, fixed order) into `off` (shared memory
+// of the draw kernel); off[nb] = grand total
+TT_DEV void big_offsets(int nb, const double* __restrict__ part, double* off, double* red) {
   const int tid = threadIdx.x, NT = blockDim.x;
   const int chunk = (nb + NT - 1) / NT;
   const int c0 = min(nb, tid * chunk), c1 = min(nb, c0 + chunk);
@@ -380,10 +380,8 @@ __global__ void __launch_bounds__(SMP_NT) big_offsets_kernel(int nb, const doubl
     off[b] = run;
     run += part[b];
   }
-  if (tid == 0) {
-    off[nb] = tot;
-    ctl[0] = 0;
-  }
+  if (tid == 0) off[nb] = tot;
+  __syncthreads();
 }
 
 TT_DEV double big_cdf(const double* cdf, const double* off, int i) {
@@ -405,7 +403,7 @@ TT_DEV double big_bound(int i, int n, double x, double depth_term) {
 
 // draws: one uniform per thread, binary search on the (unnormalised) global CDF against u * total;
 // a draw whose uniform lies within the rounding bound of either bucket edge raises ctl[0]
-__global__ void big_draw_kernel(int n, int ndraw, const double* __restrict__ cdf, const double* __restrict__ off,
+__global__ void big_draw_kernel(int n, int ndraw, const double* __restrict__ cdf, const double* __restrict__ part,
                                 int nb, const int* __restrict__ forced, int nforced, uint64_t k0, uint64_t k1,
                                 const uint64_t* __restrict__ pos, int* __restrict__ flags, int* __restrict__ ctl,
                                 double depth_term, double gscale, int lstride) {
@@ -413,6 +411,9 @@ __global__ void big_draw_kernel(int n, int ndraw, const double* __restrict__ cdf
   // searches the chunks there and only lstride levels in global memory
   extern __shared__ double coarse[];
   const int sw = 1 << lstride, nc = (n + sw - 1) >> lstride;
+  double* off = coarse + nc;   // [nb + 1] block offsets
+  double* red = off + nb + 1;  // [64]
+  big_offsets(nb, part, off, red);
   for (int k = threadIdx.x; k < nc; k += blockDim.x) coarse[k] = big_cdf(cdf, off, min(((k + 1) << lstride) - 1, n - 1));
   __syncthreads();
   const double total = off[nb];
@@ -557,26 +558,27 @@ __global__ void __launch_bounds__(SMP_NT) big_count_kernel(int n, const int* __r
   block_excl_scan_int(c, red, tot);
   if (threadIdx.x == 0) cpart[blockIdx.x] = tot;
 }
-__global__ void __launch_bounds__(SMP_NT) big_count_offsets_kernel(int nb, const int* __restrict__ cpart,
-                                                                   int* __restrict__ coff) {
-  __shared__ int red[64];
-  const int tid = threadIdx.x, NT = blockDim.x;
-  const int chunk = (nb + NT - 1) / NT;
-  const int c0 = min(nb, tid * chunk), c1 = min(nb, c0 + chunk);
-  int loc = 0;
-  for (int b = c0; b < c1; ++b) loc += cpart[b];
-  int tot;
-  int run = block_excl_scan_int(loc, red, tot);
-  for (int b = c0; b < c1; ++b) {
-    coff[b] = run;
-    run += cpart[b];
-  }
-  if (tid == 0) coff[nb] = tot;
-}
 __global__ void __launch_bounds__(SMP_NT) big_write_kernel(int n, int nb, int ndraw, int cap, int* __restrict__ flags,
-                                                           const int* __restrict__ coff, uint64_t* __restrict__ pos,
+                                                           const int* __restrict__ cpart, uint64_t* __restrict__ pos,
                                                            int* __restrict__ omega, int* __restrict__ count) {
   __shared__ int red[64];
+  __shared__ int sh_pre, sh_all;
+  {  // this block's offset (counts of the blocks before it) and the total: integer sums
+    int pre = 0, all = 0;
+    for (int q = threadIdx.x; q < nb; q += blockDim.x) {
+      const int v = cpart[q];
+      all += v;
+      pre += q < (int)blockIdx.x ? v : 0;
+    }
+    int tp, ta;
+    block_excl_scan_int(pre, red, tp);
+    block_excl_scan_int(all, red, ta);
+    if (threadIdx.x == 0) {
+      sh_pre = tp;
+      sh_all = ta;
+    }
+    __syncthreads();
+  }
   const int base = blockIdx.x * SMP_NT * BIG_IPT + threadIdx.x * BIG_IPT;
   int f[BIG_IPT];
   int c = 0;
@@ -586,7 +588,7 @@ __global__ void __launch_bounds__(SMP_NT) big_write_kernel(int n, int nb, int nd
     c += f[q] ? 1 : 0;
   }
   int tot;
-  int o = coff[blockIdx.x] + block_excl_scan_int(c, red, tot);
+  int o = sh_pre + block_excl_scan_int(c, red, tot);
 #pragma unroll
   for (int q = 0; q < BIG_IPT; ++q)
     if (f[q]) {
@@ -594,7 +596,7 @@ __global__ void __launch_bounds__(SMP_NT) big_write_kernel(int n, int nb, int nd
       ++o;
       flags[base + q] = 0;
     }
-  const int all = coff[nb];
+  const int all = sh_all;
   if (blockIdx.x == 0) {
     for (int i = all + threadIdx.x; i < cap; i += blockDim.x) omega[i] = -1;  // deterministic padding
     if (threadIdx.x == 0) {
@@ -630,16 +632,22 @@ extern "C" int tt_draw_with_replacement_large(void* stream, int n, const double*
   double gscale = 1.0;
   if (const char* e = getenv("TT_DRAW_FORCE_EXACT"))  // test hook: every draw takes the exact path
     if (e[0] == '1') gscale = 1e300;
-  big_scan_kernel<<<nb, SMP_NT, 0, st>>>(n, probs, cdf, part);
-  big_offsets_kernel<<<1, SMP_NT, 0, st>>>(nb, part, off, ctl);
+  big_scan_kernel<<<nb, SMP_NT, 0, st>>>(n, probs, cdf, part, ctl);
   {
     int blocks = (ndraw + nforced + 255) / 256;
     if (blocks < 1) blocks = 1;
     if (blocks > 1184) blocks = 1184;
     int ls = 4;  // at most 4096 coarse values (32 KB)
     while (((n + (1 << ls) - 1) >> ls) > 4096) ++ls;
-    const size_t csm = sizeof(double) * (size_t)((n + (1 << ls) - 1) >> ls);
-    big_draw_kernel<<<blocks, 256, csm, st>>>(n, ndraw, cdf, off, nb, forced, nforced, key0, key1, pos, flags, ctl,
+    const size_t csm = sizeof(double) * ((size_t)((n + (1 << ls) - 1) >> ls) + nb + 1 + 64);
+    if (csm > 48 * 1024) {
+      static size_t set_draw = 0;
+      if (csm > set_draw) {
+        TT_CUDA_TRY(cudaFuncSetAttribute(big_draw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+        set_draw = csm;
+      }
+    }
+    big_draw_kernel<<<blocks, 256, csm, st>>>(n, ndraw, cdf, part, nb, forced, nforced, key0, key1, pos, flags, ctl,
                                               depth_term, gscale, ls);
   }
   {  // exact fallback (each part exits at once unless a draw was ambiguous)
@@ -652,8 +660,7 @@ extern "C" int tt_draw_with_replacement_large(void* stream, int n, const double*
   int* cpart = (int*)(sb + S.cpart);
   int* coff = (int*)(sb + S.coff);
   big_count_kernel<<<nb, SMP_NT, 0, st>>>(n, flags, cpart);
-  big_count_offsets_kernel<<<1, SMP_NT, 0, st>>>(nb, cpart, coff);
-  big_write_kernel<<<nb, SMP_NT, 0, st>>>(n, nb, ndraw, k, flags, coff, pos, omega_out, count_out);
+  big_write_kernel<<<nb, SMP_NT, 0, st>>>(n, nb, ndraw, k, flags, cpart, pos, omega_out, count_out);
   TT_CUDA_TRY(cudaGetLastError());
   return TT_OK;
 }
