@@ -163,6 +163,11 @@ typedef struct tt_entries_args {
    * An empty batch then runs as a zero step (mu = 0) on the device, so the
    * whole per-frame chain can be captured in a CUDA graph. */
   const int32_t* nmeas_dev;
+  /* Optional flat-index form (appended): when `omega` is non-NULL the step reads entry l as
+   * w = omega[l], (i, j) = (w / ny, w % ny), y = frame[w] (frame [nx][ny] complex64, the resident
+   * truth) and ignores idx / y, so a device-side draw feeds the step without a gather pass. */
+  const int32_t* omega;
+  const float* frame;
 } tt_entries_args;
 /* Scratch for tt_track_entries: zero-fill it before its first use and reuse it for later steps
  * of the same shape (it carries a per-step stamp that replaces clearing the residual image). */

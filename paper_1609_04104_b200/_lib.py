@@ -57,7 +57,7 @@ class EntriesArgs(C.Structure):
         ("ah_in", _p), ("bh_in", _p), ("ah_out", _p), ("bh_out", _p), ("alpha_bar", _p),
         ("idx", _p), ("y", _p), ("lam", _f64), ("step_mode", _i32), ("mu", _f64), ("c_floor", _f64),
         ("c_cap", _f64), ("gamma_out", _p), ("cost_out", _p), ("mu_out", _p), ("alpha_out", _p),
-        ("resid_out", _p), ("status", _p), ("scratch", _p), ("nmeas_dev", _p),
+        ("resid_out", _p), ("status", _p), ("scratch", _p), ("nmeas_dev", _p), ("omega", _p), ("frame", _p),
     ]
 
 

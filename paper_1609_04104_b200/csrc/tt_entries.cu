@@ -61,10 +61,31 @@ static size_t gram_smem(int R) {
   return sizeof(float2) * (size_t)EG_TL * (R + 1) + sizeof(int2) * EG_TL + sizeof(double2) * NI2 + sizeof(double) * 64;
 }
 
+// entry l of the step: (i, j) and y from the index list, or from the flat index into the resident frame
+struct EntSrc {
+  const int* idx;
+  const float2* y;
+  const int* omega;
+  const float2* frame;
+  int ny;
+  TT_DEV void get(int l, int& i, int& j, float2& v) const {
+    if (omega) {
+      const int w = omega[l];
+      i = w / ny;
+      j = w - i * ny;
+      v = frame[w];
+    } else {
+      i = idx[2 * l];
+      j = idx[2 * l + 1];
+      v = y[l];
+    }
+  }
+};
+
 __global__ void __cluster_dims__(EG_CL, 1, 1) __launch_bounds__(ENT_NT)
     ent_gram_kernel(int nmeas, const int* __restrict__ nmeas_dev, int nx, int ny, int R,
-                    const float2* __restrict__ ah, const float2* __restrict__ bh, const int* __restrict__ idx,
-                    const float2* __restrict__ y, double2* __restrict__ gp) {
+                    const float2* __restrict__ ah, const float2* __restrict__ bh, const EntSrc src,
+                    double2* __restrict__ gp) {
   if (nmeas_dev) nmeas = min(*nmeas_dev, nmeas);
   extern __shared__ __align__(16) unsigned char smem[];
   float2* phi = (float2*)smem;                   // [TL][R]
@@ -83,8 +104,10 @@ __global__ void __cluster_dims__(EG_CL, 1, 1) __launch_bounds__(ENT_NT)
   for (int t0 = l0; t0 < l1; t0 += EG_TL) {
     const int tl = min(EG_TL, l1 - t0);
     for (int ll = tid; ll < tl; ll += NT) {
-      const float2 v = y[t0 + ll];
-      ij[ll] = make_int2(idx[2 * (t0 + ll)], idx[2 * (t0 + ll) + 1]);
+      int i, j;
+      float2 v;
+      src.get(t0 + ll, i, j, v);
+      ij[ll] = make_int2(i, j);
       yv[ll] = v;
       ysq += (double)v.x * v.x + (double)v.y * v.y;
     }
@@ -237,20 +260,21 @@ __global__ void __launch_bounds__(ENT_NT) ent_solve_kernel(int R, int nmeas, con
 }
 
 __global__ void ent_resid_kernel(int nmeas, const int* __restrict__ nmeas_dev, int ny, int R,
-                                 const float2* __restrict__ ah, const float2* __restrict__ bh,
-                                 const int* __restrict__ idx, const float2* __restrict__ y, const double2* gam,
-                                 const double* scal, float2* __restrict__ xi, int* __restrict__ st,
-                                 float2* __restrict__ resid) {
+                                 const float2* __restrict__ ah, const float2* __restrict__ bh, const EntSrc src,
+                                 const double2* gam, const double* scal, float2* __restrict__ xi,
+                                 int* __restrict__ st, float2* __restrict__ resid) {
   if (nmeas_dev) nmeas = min(*nmeas_dev, nmeas);
   const int cur = (int)((const long long*)scal)[3];
   for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nmeas; l += gridDim.x * blockDim.x) {
-    const int i = idx[2 * l], j = idx[2 * l + 1];
+    int i, j;
+    float2 yl;
+    src.get(l, i, j, yl);
     double2 s = make_double2(0.0, 0.0);
     for (int r = 0; r < R; ++r) {
       const double2 ph = zmul(to_d2(ah[(size_t)i * R + r]), to_d2(bh[(size_t)j * R + r]));
       s = zfma(ph, gam[r], s);
     }
-    const float2 e = make_float2((float)((double)y[l].x - s.x), (float)((double)y[l].y - s.y));
+    const float2 e = make_float2((float)((double)yl.x - s.x), (float)((double)yl.y - s.y));
     xi[(size_t)i * ny + j] = e;
     st[(size_t)i * ny + j] = cur;
     if (resid) resid[l] = e;
@@ -395,7 +419,9 @@ extern "C" int tt_track_entries(void* stream, const tt_entries_args* a) {
   if (a->lam < 0) return tt_fail(TT_EINVAL, "lambda must be nonnegative");
   if (!a->ah_in || !a->bh_in || !a->ah_out || !a->bh_out || !a->scratch || !a->alpha_bar)
     return tt_fail(TT_EINVAL, "tt_track_entries: null buffer");
-  if (L > 0 && (!a->idx || !a->y)) return tt_fail(TT_EINVAL, "tt_track_entries: null idx/y");
+  if (L > 0 && !a->omega && (!a->idx || !a->y)) return tt_fail(TT_EINVAL, "tt_track_entries: null idx/y");
+  if (a->omega && !a->frame) return tt_fail(TT_EINVAL, "tt_track_entries: omega without frame");
+  const EntSrc src{a->idx, (const float2*)a->y, a->omega, (const float2*)a->frame, ny};
   cudaStream_t st = (cudaStream_t)stream;
   const EntScratch S = ent_layout(nx, ny, R);
   unsigned char* sb = (unsigned char*)a->scratch;
@@ -420,7 +446,7 @@ extern "C" int tt_track_entries(void* stream, const tt_entries_args* a) {
       TT_CUDA_TRY(cudaFuncSetAttribute(ent_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       set_gram = sm;
     }
-    ent_gram_kernel<<<ncl * EG_CL, ENT_NT, sm, st>>>(L, Ld, nx, ny, R, ah, bh, a->idx, (const float2*)a->y, gp);
+    ent_gram_kernel<<<ncl * EG_CL, ENT_NT, sm, st>>>(L, Ld, nx, ny, R, ah, bh, src, gp);
   }
   {
     const size_t sm = sizeof(double2) * ((size_t)NI2 + R + 4 * (size_t)(R + 1));
@@ -435,8 +461,7 @@ extern "C" int tt_track_entries(void* stream, const tt_entries_args* a) {
   if (L > 0) {
     int blocks = (L + 255) / 256;
     if (blocks > 1184) blocks = 1184;
-    ent_resid_kernel<<<blocks, 256, 0, st>>>(L, Ld, ny, R, ah, bh, a->idx, (const float2*)a->y, gam, scal, xi, stp,
-                                             (float2*)a->resid_out);
+    ent_resid_kernel<<<blocks, 256, 0, st>>>(L, Ld, ny, R, ah, bh, src, gam, scal, xi, stp, (float2*)a->resid_out);
     const int m = (nx > ny ? nx : ny) * R;
     dim3 grid((m + BP_O - 1) / BP_O, 2);
     ent_backproj_kernel<<<grid, dim3(BP_O, BP_K), 0, st>>>(nx, ny, R, a->step_mode == TT_STEP_HESSIAN, ah, bh, xi,

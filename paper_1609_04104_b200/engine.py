@@ -279,7 +279,7 @@ class EntryEngine:
     """Device-resident online loop for entry masks on k-space factors (the EntryMask /
     k-space interpolation path; EntryMask on (F_x A, F_y B) is the FourierMask iteration,
     test_mri.py:258-286). Per frame, on the device: [entry scores -> large-domain Philox draw] or the
-    static list -> y gathered at the entries from the resident truth -> the generic index-list step
+    static list -> the generic index-list step reading y at the flat entries of the resident truth
     (tt_track_entries with a device-side count) -> per-frame outputs and factor history. The T-frame
     chain is captured once in a CUDA graph and replayed (no host round trip per frame). One slice."""
 
@@ -321,8 +321,6 @@ class EntryEngine:
             self.tab_cnt = torch.from_numpy(np.ascontiguousarray(cnt, dtype=np.int32)).to(self.dev)
         else:
             raise TypeError("policy must be InformativeEntries or StaticEntries")
-        self.idx = torch.zeros(self.cap, 2, **i32)
-        self.y = torch.zeros(self.cap, dtype=torch.complex64, device=self.dev)
         self.scr = torch.zeros(int(L.lib().tt_entries_scratch_bytes(self.nx, self.ny, self.rank, self.cap)),
                                dtype=torch.uint8, device=self.dev)  # zero-filled before first use (frame stamps)
         self.ah = torch.zeros(self.nx, self.rank, dtype=torch.complex64, device=self.dev)
@@ -387,8 +385,9 @@ class EntryEngine:
 
     def _frame(self, ks_ptr: int, fo: int, P: dict, keep: list) -> None:
         """One frame. The step ping-pongs through the factor history (frame fo reads slot fo-1, writes
-        slot fo) and the draw writes its entry list and count straight into the outputs, so a frame is
-        four C calls and no copies. ``P`` holds the output base pointers and strides."""
+        slot fo), the draw writes its entry list and count straight into the outputs, and the step
+        reads the drawn entries' values from the resident frame (no gather pass), so a frame is three
+        C calls and no copies. ``P`` holds the output base pointers and strides."""
         lib, st = L.lib(), L.stream_ptr()
         nx, ny, R = self.nx, self.ny, self.rank
         ah_in = P["ah0"] if fo == 0 else P["ah"] + (fo - 1) * P["sah"]
@@ -405,15 +404,13 @@ class EntryEngine:
         else:
             f = self.frame + fo
             omega, count = P["tab"] + f * P["stab"], P["tcnt"] + 4 * f
-        L.check(lib.tt_gather_entries(st, nx, ny, ks_ptr, omega, count, self.cap, self.idx.data_ptr(),
-                                      self.y.data_ptr()), "gather_entries")
         mode, mu, cf, cc = _step_params(self.step)
         a = L.EntriesArgs()
         a.nx, a.ny, a.rank, a.nmeas, a.t = nx, ny, R, self.cap, self.t
         a.ah_in, a.ah_out = ah_in, P["ah"] + fo * P["sah"]
         a.bh_in, a.bh_out = bh_in, P["bh"] + fo * P["sbh"]
         a.alpha_bar = self.alpha_bar.data_ptr()
-        a.idx, a.y = self.idx.data_ptr(), self.y.data_ptr()
+        a.omega, a.frame = omega, ks_ptr  # the step reads the drawn entries from the resident frame
         a.lam, a.step_mode, a.mu, a.c_floor, a.c_cap = self.lam, mode, mu, cf, cc
         a.gamma_out = P["gamma"] + fo * 8 * R
         a.cost_out, a.mu_out, a.alpha_out = P["cost"] + 8 * fo, P["mu"] + 8 * fo, P["alpha"] + 8 * fo
