@@ -112,10 +112,26 @@ __global__ void __cluster_dims__(EG_CL, 1, 1) __launch_bounds__(ENT_NT)
       ysq += (double)v.x * v.x + (double)v.y * v.y;
     }
     __syncthreads();
-    for (int o = tid; o < tl * R; o += NT) {
-      const int ll = idiv(o, R), r = o - ll * R;
-      const int2 q = ij[ll];
-      phi[o] = cmul(ah[(size_t)q.x * R + r], bh[(size_t)q.y * R + r]);
+    {  // gathered factor rows: eight iterations' loads in flight before any use
+      constexpr int UP = 8;
+      for (int o0 = tid; o0 < tl * R; o0 += NT * UP) {
+        float2 av[UP], bv[UP];
+#pragma unroll
+        for (int u = 0; u < UP; ++u) {
+          const int o = o0 + u * NT;
+          if (o < tl * R) {
+            const int ll = idiv(o, R), r = o - ll * R;
+            const int2 q = ij[ll];
+            av[u] = ah[(size_t)q.x * R + r];
+            bv[u] = bh[(size_t)q.y * R + r];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < UP; ++u) {
+          const int o = o0 + u * NT;
+          if (o < tl * R) phi[o] = cmul(av[u], bv[u]);
+        }
+      }
     }
     __syncthreads();
     // item-outer: one guard per item, none per entry
@@ -270,10 +286,20 @@ __global__ void ent_resid_kernel(int nmeas, const int* __restrict__ nmeas_dev, i
     float2 yl;
     src.get(l, i, j, yl);
     double2 s = make_double2(0.0, 0.0);
-    for (int r = 0; r < R; ++r) {
-      const double2 ph = zmul(to_d2(ah[(size_t)i * R + r]), to_d2(bh[(size_t)j * R + r]));
-      s = zfma(ph, gam[r], s);
+    const float2* ar = ah + (size_t)i * R;
+    const float2* br = bh + (size_t)j * R;
+    int r = 0;
+    for (; r + 8 <= R; r += 8) {  // eight row entries in flight
+      float2 av[8], bv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        av[u] = ar[r + u];
+        bv[u] = br[r + u];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s = zfma(zmul(to_d2(av[u]), to_d2(bv[u])), gam[r + u], s);
     }
+    for (; r < R; ++r) s = zfma(zmul(to_d2(ar[r]), to_d2(br[r])), gam[r], s);
     const float2 e = make_float2((float)((double)yl.x - s.x), (float)((double)yl.y - s.y));
     xi[(size_t)i * ny + j] = e;
     st[(size_t)i * ny + j] = cur;

@@ -324,8 +324,14 @@ extern "C" int tt_draw_without_replacement(void* stream, int n, const double* we
 // kernel with device-side control (graph-capturable).
 #define BIG_IPT 8  // entries per thread in the block scan
 struct BigDrawScratch {
-  size_t cdf, part, off, flags, ctl, cpart, coff, total;
+  size_t cdf, part, off, flags, ctl, cpart, coff, cq, total;
 };
+// log2 of the coarse CDF stride: at most 4096 coarse points (32 KB of shared memory in the draw)
+static inline int big_lstride(int n) {
+  int ls = 4;
+  while (((n + (1 << ls) - 1) >> ls) > 4096) ++ls;
+  return ls;
+}
 static BigDrawScratch big_layout(int n) {
   BigDrawScratch s;
   const int nb = (n + SMP_NT * BIG_IPT - 1) / (SMP_NT * BIG_IPT);
@@ -338,13 +344,15 @@ static BigDrawScratch big_layout(int n) {
   s.ctl = o;   o = al(o + sizeof(int) * 4);  // [0] ambiguity flag
   s.cpart = o; o = al(o + sizeof(int) * (size_t)nb);
   s.coff = o;  o = al(o + sizeof(int) * ((size_t)nb + 1));
+  s.cq = o;    o = al(o + sizeof(double) * (size_t)((n + (1 << big_lstride(n)) - 1) >> big_lstride(n)));
   s.total = o;
   return s;
 }
 
 // level 1: block-local inclusive scan (thread-sequential chunks, fixed order) and block totals
 __global__ void __launch_bounds__(SMP_NT) big_scan_kernel(int n, const double* __restrict__ p, double* __restrict__ cdf,
-                                                          double* __restrict__ part, int* __restrict__ ctl) {
+                                                          double* __restrict__ part, int* __restrict__ ctl,
+                                                          double* __restrict__ cq, int lstride) {
   __shared__ double red[64];
   const int tid = threadIdx.x;
   const int base = blockIdx.x * SMP_NT * BIG_IPT + tid * BIG_IPT;
@@ -357,10 +365,15 @@ __global__ void __launch_bounds__(SMP_NT) big_scan_kernel(int n, const double* _
   }
   double tot;
   double run = block_excl_scan_dbl(loc, red, tot);
+  const int msk = (1 << lstride) - 1;
 #pragma unroll
   for (int q = 0; q < BIG_IPT; ++q) {
     run += v[q];
-    if (base + q < n) cdf[base + q] = run;
+    const int i = base + q;
+    if (i < n) {
+      cdf[i] = run;
+      if ((i & msk) == msk || i == n - 1) cq[i >> lstride] = run;  // coarse point: last of its chunk
+    }
   }
   if (tid == 0) part[blockIdx.x] = tot;
   if (blockIdx.x == 0 && tid == 0) ctl[0] = 0;  // the draw raises it for an ambiguous uniform
@@ -403,7 +416,8 @@ TT_DEV double big_bound(int i, int n, double x, double depth_term) {
 
 // draws: one uniform per thread, binary search on the (unnormalised) global CDF against u * total;
 // a draw whose uniform lies within the rounding bound of either bucket edge raises ctl[0]
-__global__ void big_draw_kernel(int n, int ndraw, const double* __restrict__ cdf, const double* __restrict__ part,
+__global__ void big_draw_kernel(int n, int ndraw, const double* __restrict__ cdf, const double* __restrict__ cq,
+                                const double* __restrict__ part,
                                 int nb, const int* __restrict__ forced, int nforced, uint64_t k0, uint64_t k1,
                                 const uint64_t* __restrict__ pos, int* __restrict__ flags, int* __restrict__ ctl,
                                 double depth_term, double gscale, int lstride) {
@@ -413,8 +427,23 @@ __global__ void big_draw_kernel(int n, int ndraw, const double* __restrict__ cdf
   const int sw = 1 << lstride, nc = (n + sw - 1) >> lstride;
   double* off = coarse + nc;   // [nb + 1] block offsets
   double* red = off + nb + 1;  // [64]
-  big_offsets(nb, part, off, red);
-  for (int k = threadIdx.x; k < nc; k += blockDim.x) coarse[k] = big_cdf(cdf, off, min(((k + 1) << lstride) - 1, n - 1));
+  {  // coarse points written by the scan (block-local prefixes), all loads in flight
+    constexpr int U = 16;
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = threadIdx.x + u * blockDim.x;
+      v[u] = k < nc ? cq[k] : 0.0;
+    }
+    big_offsets(nb, part, off, red);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = threadIdx.x + u * blockDim.x;
+      if (k < nc) coarse[k] = v[u] + off[min(((k + 1) << lstride) - 1, n - 1) / (SMP_NT * BIG_IPT)];
+    }
+    for (int k = threadIdx.x + U * blockDim.x; k < nc; k += blockDim.x)
+      coarse[k] = cq[k] + off[min(((k + 1) << lstride) - 1, n - 1) / (SMP_NT * BIG_IPT)];
+  }
   __syncthreads();
   const double total = off[nb];
   const uint64_t p0 = pos[0];
@@ -632,13 +661,13 @@ extern "C" int tt_draw_with_replacement_large(void* stream, int n, const double*
   double gscale = 1.0;
   if (const char* e = getenv("TT_DRAW_FORCE_EXACT"))  // test hook: every draw takes the exact path
     if (e[0] == '1') gscale = 1e300;
-  big_scan_kernel<<<nb, SMP_NT, 0, st>>>(n, probs, cdf, part, ctl);
+  const int ls = big_lstride(n);
+  double* cq = (double*)(sb + S.cq);
+  big_scan_kernel<<<nb, SMP_NT, 0, st>>>(n, probs, cdf, part, ctl, cq, ls);
   {
     int blocks = (ndraw + nforced + 255) / 256;
     if (blocks < 1) blocks = 1;
     if (blocks > 1184) blocks = 1184;
-    int ls = 4;  // at most 4096 coarse values (32 KB)
-    while (((n + (1 << ls) - 1) >> ls) > 4096) ++ls;
     const size_t csm = sizeof(double) * ((size_t)((n + (1 << ls) - 1) >> ls) + nb + 1 + 64);
     if (csm > 48 * 1024) {
       static size_t set_draw = 0;
@@ -647,8 +676,8 @@ extern "C" int tt_draw_with_replacement_large(void* stream, int n, const double*
         set_draw = csm;
       }
     }
-    big_draw_kernel<<<blocks, 256, csm, st>>>(n, ndraw, cdf, part, nb, forced, nforced, key0, key1, pos, flags, ctl,
-                                              depth_term, gscale, ls);
+    big_draw_kernel<<<blocks, 256, csm, st>>>(n, ndraw, cdf, cq, part, nb, forced, nforced, key0, key1, pos, flags,
+                                              ctl, depth_term, gscale, ls);
   }
   {  // exact fallback (each part exits at once unless a draw was ambiguous)
     big_exact_kernel<<<1, SMP_NT, 0, st>>>(n, probs, cdf, flags, ctl);
