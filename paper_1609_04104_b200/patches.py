@@ -107,7 +107,7 @@ def _step_params(step):
 class _PatchRun:
     """Device state of one patched run: binned data, factors, and the launch helper."""
 
-    def __init__(self, grid: PatchGrid, lam, step, frames_dev, entries, offsets):
+    def __init__(self, grid: PatchGrid, lam, step, frames_dev, entries=None, offsets=None):
         self.grid = grid
         self.lam = float(lam)
         self.mode, self.mu, self.c_floor, self.c_cap = _step_params(step)
@@ -117,18 +117,26 @@ class _PatchRun:
         self.np = grid.k1 * grid.k2
         self.cap = grid.n1 * grid.n2
         self.frames = frames_dev
-        ent = torch.from_numpy(entries).to(self.dev, non_blocking=True)
-        off = torch.from_numpy(offsets).to(self.dev, non_blocking=True)
         self.pidx = torch.empty((T, self.np, self.cap), dtype=torch.int32, device=self.dev)
         self.py = torch.empty((T, self.np, self.cap), dtype=torch.complex64, device=self.dev)
-        self.pcnt = torch.empty((T, self.np), dtype=torch.int32, device=self.dev)
+        self.pcnt = torch.zeros((T, self.np), dtype=torch.int32, device=self.dev)
         self.bin_status = torch.zeros(1, dtype=torch.int32, device=self.dev)
-        L.check(L.lib().tt_patch_bin(L.stream_ptr(), N1, N2, grid.n1, grid.n2, T,
-                                     frames_dev.data_ptr(), ent.data_ptr(), off.data_ptr(), self.pidx.data_ptr(),
-                                     self.py.data_ptr(), self.pcnt.data_ptr(), self.bin_status.data_ptr()),
-                "patch binning")
-        self._keep = (ent, off)
         self.status = torch.zeros(self.np, dtype=torch.int32, device=self.dev)
+        self._keep = []
+        if entries is not None:
+            self.bin(torch.from_numpy(entries).to(self.dev), torch.from_numpy(offsets).to(self.dev), 0, T)
+
+    def bin(self, ent_dev, off_dev, f0, f1):
+        """Split frames [f0, f1) per patch (``ent_dev`` / ``off_dev``: their compact mask table)."""
+        g = self.grid
+        fb = 8 * self.N1 * self.N2
+        pb = self.np * self.cap
+        L.check(L.lib().tt_patch_bin(L.stream_ptr(), self.N1, self.N2, g.n1, g.n2, f1 - f0,
+                                     self.frames.data_ptr() + f0 * fb, ent_dev.data_ptr(), off_dev.data_ptr(),
+                                     self.pidx.data_ptr() + 4 * f0 * pb, self.py.data_ptr() + 8 * f0 * pb,
+                                     self.pcnt.data_ptr() + 4 * f0 * self.np, self.bin_status.data_ptr()),
+                "patch binning")
+        self._keep.append((ent_dev, off_dev))
 
     def set_factors(self, A0s, B0s, t0=1):
         g = self.grid
@@ -196,13 +204,28 @@ def run_tracking_patched(frames, grid: PatchGrid, lam, step, masks, warm_n=0, wa
     if reshuffle and epochs > 1 and rng is None:
         raise ValueError("rng is required for reshuffling")
     dev = L.device()
+    comp = torch.cuda.current_stream()
     # pinned (or device) input uploads asynchronously; a pageable one is copied as is
     fd = src.to(torch.complex64).to(dev, non_blocking=True).contiguous()
-    ent, off = _entry_table(masks, grid.frame_shape, T)
-    run = _PatchRun(grid, lam, step, fd, ent, off)
+    run = _PatchRun(grid, lam, step, fd)
     run.set_factors(A0s, B0s)
     npch, R = run.np, grid.rho
 
+    def upload_bin(f0, f1, stream):
+        ent, off = _entry_table(masks[f0:f1], grid.frame_shape, f1 - f0)
+        with torch.cuda.stream(stream):  # the driver stages the pageable copy; the compute stream runs on
+            ed = torch.from_numpy(ent).to(dev, non_blocking=True)
+            od = torch.from_numpy(off).to(dev, non_blocking=True)
+        comp.wait_stream(stream)
+        run.bin(ed, od, f0, f1)
+        return np.diff(off)
+
+    # the warm frames' masks first, so the warm-up starts; the streamed frames' masks are built on the
+    # host and uploaded on a copy stream while it runs
+    s_copy = torch.cuda.Stream()
+    samples = []
+    if warm_n:
+        samples.append(upload_bin(0, warm_n, s_copy))
     keep = []
     for epoch in range(warm_epochs):
         if warm_n == 0:
@@ -210,6 +233,9 @@ def run_tracking_patched(frames, grid: PatchGrid, lam, step, masks, warm_n=0, wa
         if epoch > 0:
             run.rebalance()
         keep.append(run.launch(list(range(warm_n))))
+    if warm_n < T:
+        samples.append(upload_bin(warm_n, T, s_copy))
+    samples = np.concatenate(samples) if samples else np.zeros(0, np.int64)
     gam_s, cost_s, mu_s, res_s, orders, scheds = [], [], [], [], [], []
     main = T - warm_n
     for epoch in range(epochs):
@@ -232,19 +258,26 @@ def run_tracking_patched(frames, grid: PatchGrid, lam, step, masks, warm_n=0, wa
         mu_s.append(m)
         res_s.append(r)
         scheds.extend(order)
-    # re-projection of every frame onto the final subspaces, tiles assembled in place
+    # re-projection of every frame onto the final subspaces, tiles assembled in place; in blocks, each
+    # downloaded into pinned memory while the next is computed
     gam = torch.empty((T, npch, R), dtype=torch.complex64, device=dev)
     recon = torch.empty((T,) + grid.frame_shape, dtype=torch.complex64, device=dev)
-    keep.append(run.launch(list(range(T)), project=True, gamma=gam, recon=recon))
+    recon_h = torch.empty((T,) + grid.frame_shape, dtype=torch.complex64, pin_memory=True)
+    for a0 in range(0, T, 50):
+        a1 = min(T, a0 + 50)
+        keep.append(run.launch(list(range(a0, a1)), project=True, gamma=gam[a0:a1], recon=recon))
+        s_copy.wait_stream(comp)
+        with torch.cuda.stream(s_copy):
+            recon_h[a0:a1].copy_(recon[a0:a1], non_blocking=True)
     if clean is None:
         ref = fd
     else:
         ct = clean if isinstance(clean, torch.Tensor) else torch.from_numpy(np.asarray(clean))
         ref = (ct.permute(2, 0, 1) if frames_last else ct).to(dev, torch.complex64)
     err = (recon - ref).abs().pow(2).sum(dim=(1, 2)).double() / ref.abs().pow(2).sum(dim=(1, 2)).double()
-    # asynchronous downloads into pinned memory, one synchronisation
+    # the small results: asynchronous downloads into pinned memory, one synchronisation
     pinned = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True)  # noqa: E731
-    dl = {"recon": recon, "gamma": gam, "err": err, "pcnt": run.pcnt, "A": run.a, "B": run.b, "t": run.t[:1],
+    dl = {"gamma": gam, "err": err, "pcnt": run.pcnt, "A": run.a, "B": run.b, "t": run.t[:1],
           "st": torch.stack([run.status.max(), run.bin_status[0]])}
     if cost_s:
         dl.update(cost=torch.cat(cost_s), mu=torch.cat(mu_s), sg=torch.cat(gam_s))
@@ -253,8 +286,10 @@ def run_tracking_patched(frames, grid: PatchGrid, lam, step, masks, warm_n=0, wa
     host = {k: pinned(v) for k, v in dl.items()}
     for k, v in dl.items():
         host[k].copy_(v, non_blocking=True)
-    torch.cuda.current_stream().synchronize()
+    comp.wait_stream(s_copy)
+    comp.synchronize()
     h = {k: v.numpy() for k, v in host.items()}
+    h["recon"] = recon_h.numpy()
     L.raise_status(int(h["st"][0]) | int(h["st"][1]), "patched tracking")
 
     pcnt = h["pcnt"]
@@ -267,8 +302,10 @@ def run_tracking_patched(frames, grid: PatchGrid, lam, step, masks, warm_n=0, wa
     if keep_residual:
         rr = h.get("resid", np.zeros((0, npch, run.cap), np.complex64))
         resid = [np.concatenate([rr[k, p, :pcnt[f, p]] for p in range(npch)]) for k, f in enumerate(scheds)]
+    # per-step cost summed over patches left to right, as Python's sum does (experiment.py:402)
+    step_cost = np.cumsum(cost, axis=1)[:, -1] if cost.shape[0] and npch else np.zeros(cost.shape[0])
     return PatchedResult(
         recon=h["recon"], gamma=h["gamma"], step_gamma=sg,
-        step_cost=np.array([float(sum(row)) for row in cost]), step_mu=mu[:, 0] if len(mu) else mu.reshape(0),
+        step_cost=step_cost, step_mu=mu[:, 0] if len(mu) else mu.reshape(0),
         step_t=step_t, step_residual=resid, orders=orders, final_A=h["A"], final_B=h["B"],
-        t=int(h["t"][0]) if npch else 1, nmse=h["err"], samples=np.diff(off))
+        t=int(h["t"][0]) if npch else 1, nmse=h["err"], samples=samples)
