@@ -40,6 +40,8 @@ from .tracker import (
     StepConfig,
     StepReport,
     TrackerState,
+    empirical_cost,
+    empirical_cost_gradient,
     factor_gradient,
     hessian_bound,
     init_state,
@@ -62,6 +64,7 @@ __all__ = [
     "unitary_dft2", "unitary_dft_matrix", "variable_density_rows", "weighted_draw_without_replacement",
     "Fixed", "HessianBound", "StepConfig", "StepReport", "TrackerState", "init_state", "random_subspace",
     "run", "solve_gamma", "track_step", "factor_gradient", "hessian_bound", "instantaneous_cost",
+    "empirical_cost", "empirical_cost_gradient",
     "SamplePlan", "SamplingDistribution", "adaptive_step", "draw_samples", "entry_scores",
     "expected_count_trace", "expected_sample_count", "row_scores",
     "FrameEstimate", "interp_track_step", "reconstruct_frame", "PatchGrid", "patch_partition", "patch_assemble",

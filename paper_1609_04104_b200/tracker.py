@@ -368,6 +368,42 @@ def track_step(state: TrackerState, batch: MeasurementBatch):
     return TrackerState(subspace=new_sub, config=cfg, t=t + 1, alpha_bar=alpha_bar), report
 
 
+def empirical_cost(state: TrackerState, batches) -> float:
+    """Averaged cost (1/T) sum_tau f_tau at the current subspace, coefficients re-solved per frame
+    (tracker.py:414-430): build_phi, the device ridge solve and the device residual per batch."""
+    from .observation import build_phi
+
+    batches = list(batches)
+    if not batches:
+        raise ValueError("empirical cost needs at least one batch")
+    total = 0.0
+    for tau, batch in enumerate(batches, start=1):
+        phi = build_phi(state.subspace, batch.descriptor)
+        gamma = solve_gamma(phi, np.asarray(batch.y), state.config.lam)
+        total += instantaneous_cost(state.subspace, batch, state.config.lam, tau, gamma)
+    return total / len(batches)
+
+
+def empirical_cost_gradient(state: TrackerState, batches) -> list:
+    """Per-mode partial factor gradient at the re-solved coefficients, averaged over the batches
+    (tracker.py:433-453; the stationarity diagnostic)."""
+    from .observation import build_phi
+
+    batches = list(batches)
+    if not batches:
+        raise ValueError("empirical cost gradient needs at least one batch")
+    sums = [np.zeros(f.shape, dtype=np.complex128) for f in state.subspace.factors]
+    for tau, batch in enumerate(batches, start=1):
+        phi = build_phi(state.subspace, batch.descriptor)
+        y = np.asarray(batch.y, dtype=np.complex128).ravel()
+        gamma = solve_gamma(phi, y, state.config.lam)
+        residual = y - phi @ gamma
+        grads = factor_gradient(state.subspace, gamma, batch.descriptor, residual, state.config.lam, tau)
+        for acc, g in zip(sums, grads):
+            acc += g
+    return [g / len(batches) for g in sums]
+
+
 def run(stream, config: StepConfig, epochs: int = 1, reshuffle: bool = False, rng=None,
         initial: TrackerState | None = None, rebalance_epochs: bool = True):
     """Fold track_step over a stream, optionally for several epochs

@@ -192,3 +192,38 @@ def test_standalone_gradient_cost_and_curvature(name):
     assert alpha == pytest.approx(O.alpha_power(A, B, gam, c["idx"], c["kind"], c["lam"], c["t"]), rel=1e-5)
     assert tt.hessian_bound(sub, np.zeros_like(gam), desc, 0.6, 3) == pytest.approx(0.2)
     assert tt.hessian_bound(sub, gam, desc, c["lam"], c["t"], c_floor=1e6, c_cap=1e7) == 1e6
+
+
+def test_empirical_cost_and_gradient():
+    """empirical_cost / empirical_cost_gradient (tracker.py:414-453): per batch the ridge re-solve, the
+    cost at tau = 1..T, and the partial factor gradient, averaged; against the same sums from the
+    oracle (ridge by SVD, explicit residual and data terms)."""
+    import paper_1609_04104_b200 as tt
+
+    rng = np.random.default_rng(3)
+    n1, n2, R, lam = 16, 12, 3, 0.2
+    A, B = O.random_subspace(n1, n2, R, seed=5)
+    batches, ref_cost = [], 0.0
+    ref_g = [np.zeros_like(A), np.zeros_like(B)]
+    for tau in range(1, 5):
+        kind = "fourier" if tau % 2 else "entry"
+        rows = np.sort(rng.choice(n1, 5, replace=False))
+        idx = O.rows_to_entries(rows, n2) if kind == "fourier" else np.stack(
+            [rng.choice(n1, 40), rng.choice(n2, 40)], axis=1)
+        idx = np.unique(idx, axis=0) if kind == "entry" else idx
+        y = rng.standard_normal(len(idx)) + 1j * rng.standard_normal(len(idx))
+        Desc = tt.FourierMask if kind == "fourier" else tt.EntryMask
+        batches.append(tt.MeasurementBatch(y, Desc((n1, n2), idx)))
+        phi = O.phi_matrix(A, B, idx, kind)
+        g = O.ridge_svd(phi, y, lam)
+        e = y - phi @ g
+        ref_cost += 0.5 * np.linalg.norm(e) ** 2 + 0.5 * (lam / tau) * (np.linalg.norm(A) ** 2 + np.linalg.norm(B) ** 2)
+        dA, dB = O.data_terms(A, B, g, idx, e, kind)
+        ref_g[0] += (lam / tau) * A - dA
+        ref_g[1] += (lam / tau) * B - dB
+    st = tt.TrackerState(tt.TensorSubspace((A, B)), tt.StepConfig(lam=lam, rank=R))
+    assert tt.empirical_cost(st, batches) == pytest.approx(ref_cost / 4, rel=1e-5)
+    for got, want in zip(tt.empirical_cost_gradient(st, batches), ref_g):
+        assert rel(got, want / 4) < 1e-4
+    with pytest.raises(ValueError):
+        tt.empirical_cost(st, [])
