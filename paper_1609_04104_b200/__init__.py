@@ -8,7 +8,8 @@ sm_100a CUDA library ``libtensortrack_b200.so`` (C ABI in
 anywhere, but every compute call needs a CUDA device and the built library.
 """
 
-from .core import TensorSubspace, rebalance, synthesize_slice
+from .core import (TensorSubspace, outer_rank_one, rank_surrogate, rebalance, refold, singular_values,
+                   synthesize_slice, unfold)
 from .engine import (BatchResult, EntryEngine, Informative, InformativeEntries, LocalShardedEngine, OnlineEngine,
                      OnlineResult, RowShardedEngine, StaticEntries, StaticRows, run_batch, run_online, warm_up)
 from .mri import FrameEstimate, PatchGrid, interp_track_step, patch_assemble, patch_partition, reconstruct_frame
@@ -59,7 +60,8 @@ from .reports import (MetricRow, online_budget_rows, online_mask_rows, write_bud
                       write_metrics_csv, write_trace_csv)
 
 __all__ = [
-    "TensorSubspace", "rebalance", "synthesize_slice",
+    "TensorSubspace", "rebalance", "synthesize_slice", "outer_rank_one", "singular_values", "rank_surrogate",
+    "unfold", "refold",
     "EntryMask", "FourierMask", "MeasurementBatch", "build_phi", "row_distances", "rows_to_entries",
     "unitary_dft2", "unitary_dft_matrix", "variable_density_rows", "weighted_draw_without_replacement",
     "Fixed", "HessianBound", "StepConfig", "StepReport", "TrackerState", "init_state", "random_subspace",

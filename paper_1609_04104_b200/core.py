@@ -24,7 +24,8 @@ import torch
 from . import _lib as L
 from . import _ops as K
 
-__all__ = ["TensorSubspace", "synthesize_slice", "rebalance"]
+__all__ = ["TensorSubspace", "synthesize_slice", "rebalance", "outer_rank_one", "singular_values", "rank_surrogate",
+           "unfold", "refold"]
 
 
 def _as_factor(a) -> np.ndarray:
@@ -186,3 +187,54 @@ def rebalance(subspace: TensorSubspace) -> TensorSubspace:
     if int(st.item()) & L.TT_ST_ZEROCOL:
         raise ValueError("a component is zero in some modes but not all")
     return TensorSubspace._from_device(a, b, kind)
+
+
+# ---------------------------------------------------------------- small host utilities (core.py:76-190)
+# Off the hot path: shape bookkeeping and norms the reference exposes next to the subspace type.
+def outer_rank_one(vectors) -> np.ndarray:
+    """Outer product of the given vectors (core.py:76-88)."""
+    from functools import reduce
+
+    vecs = [np.asarray(v, dtype=np.complex128).ravel() for v in vectors]
+    if not vecs:
+        raise ValueError("outer product of an empty vector list")
+    if any(v.size == 0 for v in vecs):
+        raise ValueError("outer product with an empty vector")
+    return reduce(np.multiply.outer, vecs)
+
+
+def singular_values(subspace: TensorSubspace, mode_m_factor=None) -> np.ndarray:
+    """Per-component sigma_r = prod_m ||a_r^(m)|| over the factors (plus an optional trailing
+    mode-M factor), in column order (core.py:107-121)."""
+    mats = list(subspace.factors)
+    if mode_m_factor is not None:
+        f = _as_factor(mode_m_factor)
+        if f.shape[1] != subspace.rank:
+            raise ValueError("mode-M factor rank does not match subspace rank")
+        mats.append(f)
+    return np.prod(np.stack([np.linalg.norm(f, axis=0) for f in mats]), axis=0)
+
+
+def rank_surrogate(factors) -> float:
+    """(1/M) sum_m ||A_m||_F^2 (core.py:124-135)."""
+    mats = [_as_factor(f) for f in factors]
+    if not mats:
+        raise ValueError("rank surrogate of an empty factor list")
+    return float(sum(np.linalg.norm(f) ** 2 for f in mats)) / len(mats)
+
+
+def unfold(tensor, mode: int) -> np.ndarray:
+    """Mode-``mode`` (1-based) unfolding, remaining indices ascending, last fastest (core.py:169-178)."""
+    tensor = np.asarray(tensor)
+    if not 1 <= mode <= tensor.ndim:
+        raise ValueError(f"mode {mode} out of range for {tensor.ndim}-way tensor")
+    return np.moveaxis(tensor, mode - 1, 0).reshape(tensor.shape[mode - 1], -1)
+
+
+def refold(matrix, mode: int, dims) -> np.ndarray:
+    """Inverse of :func:`unfold` (core.py:181-190)."""
+    dims = tuple(int(d) for d in dims)
+    if not 1 <= mode <= len(dims):
+        raise ValueError(f"mode {mode} out of range for dims {dims}")
+    rest = dims[: mode - 1] + dims[mode:]
+    return np.moveaxis(np.asarray(matrix).reshape((dims[mode - 1],) + rest), 0, mode - 1)
