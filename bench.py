@@ -65,6 +65,11 @@ CONFIGS = {
                      "k-space, T=200, 8x8 grid of 32x32 patches with rank 4 each, lambda=0.05, variable-density "
                      "rows 25% (Philox), Fixed mu=0.01, warm-up 5 full frames x 20 epochs, 1 epoch, "
                      "re-projection of every frame"),
+    "c2b": dict(n=256, R=20, T=200, lam=0.05, period=20.0, vd=0.25, mu=0.01, slices=1, epochs=4, batch=True,
+                desc="multi-epoch batch mode (tracker.run / experiment.run_tracking with epochs > 1): 256x256 "
+                     "complex64 cine phantom, T=200, R=20, lambda=0.05, variable-density rows 25% (Philox), "
+                     "Fixed mu=0.01, 4 epochs with reshuffling and rebalancing, then the re-projection of every "
+                     "frame onto the final subspace"),
     "c4": dict(n=1024, R=32, T=256, lam=0.1, period=16.0, vd=0.125, mu=0.01, slices=1,
                desc="config 4: 1024x1024 complex64 cine phantom, T=256, R=32, lambda=0.1, variable-density rows "
                     "12.5% (128 rows/frame), Fixed mu=0.01 (single GPU, unsharded)"),
@@ -559,6 +564,109 @@ def run_patched(args, cfg):
     return 0
 
 
+def run_batch_mode(args, cfg):
+    """Multi-epoch batch mode (run_batch): a step is the whole batch run, epochs x T
+    tracked steps (rebalanced between epochs, reshuffled order from the caller's generator) and the
+    re-projection of every frame; value = tracked frame-steps per second with the k-space resident.
+    Replicas per rank."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1609_04104_b200 as tt
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n, R, T, E = cfg["n"], cfg["R"], cfg["T"], cfg["epochs"]
+    ks_np, clean_np = make_data(cfg, [0])
+    A0, B0 = init_factors(cfg, [0])
+    S = int(np.ceil(cfg["vd"] * n))
+    gen = np.random.Generator(np.random.Philox(key=2024))
+    tab = np.stack([tt.variable_density_rows(n, -1.0, cfg["vd"], gen) for _ in range(T)])
+    cnt = np.full(T, S)
+    kd = torch.from_numpy(ks_np[:, 0]).to(dev)
+
+    def one(src):
+        return tt.run_batch(src, A0[0], B0[0], cfg["lam"], tt.Fixed(cfg["mu"]), tab, cnt, epochs=E,
+                            rng=np.random.default_rng(5), reshuffle=True)
+
+    for _ in range(args.warmup):
+        one(kd)
+    torch.cuda.synchronize()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            res = one(kd)  # ends with the host readback of the results
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    tot = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    total_ms = float(tot[0])
+    value = E * T * world * args.steps / (total_ms / 1e3)
+    nm = [float(np.linalg.norm(res.recon[t] - clean_np[t, 0]) ** 2 / np.linalg.norm(clean_np[t, 0]) ** 2)
+          for t in range(T)]
+    e2e = None
+    if not args.no_e2e:
+        kp = torch.from_numpy(ks_np[:, 0]).pin_memory()
+        one(kp)
+        torch.cuda.synchronize()
+        t_e2e = []
+        for _ in range(max(1, args.steps)):
+            t0 = time.perf_counter()
+            res = one(kp)
+            torch.cuda.synchronize()
+            t_e2e.append(time.perf_counter() - t0)
+        et = torch.tensor([sum(t_e2e)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": E * T * world * len(t_e2e) / float(et[0]), "unit": "frame-steps/s",
+               "h2d_bytes_per_step": int(ks_np[:, 0].nbytes),
+               "d2h_bytes_per_step": int(res.recon.nbytes + res.gamma.nbytes + res.step_gamma.nbytes),
+               "call": "paper_1609_04104_b200.run_batch(pinned host kspace, row tables) -> host recon"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle import tt_oracle as O
+        fr = 20
+        rows = [tab[f] for f in range(fr)]
+        t0 = time.perf_counter()
+        O.batch_run(ks_np[:fr, 0], A0[0], B0[0], cfg["lam"], ("fixed", cfg["mu"]), rows, 2,
+                    rng=np.random.default_rng(5), reshuffle=True)
+        dt = time.perf_counter() - t0
+        cpu = {"value": 2 * fr / dt, "unit": "frame-steps/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"2 epochs over the first {fr} frames + re-projection ({dt:.1f} s), oracle port of "
+                         "tracker.run / the batch re-projection"}
+    if world > 1:
+        dist.destroy_process_group()
+    if rank != 0:
+        return 0
+    line = {
+        "metric": METRIC, "value": value, "unit": "frame-steps/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c64", "data": "synthetic",
+        "config": {"workload": cfg["desc"], "frames": T, "epochs": E, "rank": R, "rows_per_frame": S,
+                   "l2": "flushed between steps (256 MB write)", "parallelism": f"replicas x{world}",
+                   "nrmse_last": float(np.sqrt(nm[-1]))},
+        "gpu_launches": None,
+        "roofline": None,
+        "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def run_row_sharded(args, cfg):
     """Config 4 across ranks: Ah row-sharded, one NCCL all-reduce pair per frame
     (SURVEY §8e). `scaling: strong` (the single 1024^2 slice is split)."""
@@ -868,6 +976,8 @@ def main():
         return run_entries(args, cfg)
     if "patch" in cfg:
         return run_patched(args, cfg)
+    if cfg.get("batch"):
+        return run_batch_mode(args, cfg)
     return run_ours(args, cfg)
 
 

@@ -932,9 +932,16 @@ def run_batch(kspace, A0, B0, lam, step, rows, counts, epochs=1, rng=None, reshu
     A = K.fft_cols(ah, inverse=True).reshape(nx, R)
     B = K.fft_cols(bh, inverse=True).reshape(ny, R)
     X = K.reconstruct(A[None].expand(T, nx, R).contiguous(), B[None].expand(T, ny, R).contiguous(), gam.contiguous())
-    return BatchResult(recon=X.cpu().numpy(), gamma=gam.cpu().numpy(), step_gamma=torch.cat(g_steps).cpu().numpy(),
-                       step_cost=torch.cat(c_steps).cpu().numpy(), step_mu=torch.cat(m_steps).cpu().numpy(),
-                       orders=orders, final_A=A.cpu().numpy(), final_B=B.cpu().numpy(), t=t)
+    # asynchronous downloads into pinned memory, one synchronisation
+    dl = {"recon": X, "gamma": gam, "sg": torch.cat(g_steps), "sc": torch.cat(c_steps), "sm": torch.cat(m_steps),
+          "A": A, "B": B}
+    host = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in dl.items()}
+    for k, v in dl.items():
+        host[k].copy_(v, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    h = {k: v.numpy() for k, v in host.items()}
+    return BatchResult(recon=h["recon"], gamma=h["gamma"], step_gamma=h["sg"], step_cost=h["sc"], step_mu=h["sm"],
+                       orders=orders, final_A=h["A"], final_B=h["B"], t=t)
 
 
 class RowShardedEngine:
