@@ -13,6 +13,20 @@
 
 #define TT_DEV __device__ __forceinline__
 
+// ---------------------------------------------------------------- launch attributes
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device, size increase). Function
+// attributes are per device, so each call site keeps one cached size per device in `cache`.
+#define TT_MAXDEV 64
+inline cudaError_t tt_smem_attr(const void* fn, size_t bytes, size_t* cache) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < TT_MAXDEV && cache[dev] >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess && dev < TT_MAXDEV) cache[dev] = bytes;
+  return e;
+}
+
 // ---------------------------------------------------------------- complex
 TT_DEV float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 TT_DEV float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }

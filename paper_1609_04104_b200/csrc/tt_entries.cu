@@ -467,20 +467,14 @@ extern "C" int tt_track_entries(void* stream, const tt_entries_args* a) {
   if (ncl > EG_NCL) ncl = EG_NCL;
   {
     const size_t sm = gram_smem(R);
-    static size_t set_gram = 0;
-    if (sm > set_gram) {
-      TT_CUDA_TRY(cudaFuncSetAttribute(ent_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      set_gram = sm;
-    }
+    static size_t set_gram[TT_MAXDEV] = {0};
+    TT_CUDA_TRY(tt_smem_attr((const void*)ent_gram_kernel, sm, set_gram));
     ent_gram_kernel<<<ncl * EG_CL, ENT_NT, sm, st>>>(L, Ld, nx, ny, R, ah, bh, src, gp);
   }
   {
     const size_t sm = sizeof(double2) * ((size_t)NI2 + R + 4 * (size_t)(R + 1));
-    static size_t set_solve = 0;
-    if (sm > set_solve) {
-      TT_CUDA_TRY(cudaFuncSetAttribute(ent_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      set_solve = sm;
-    }
+    static size_t set_solve[TT_MAXDEV] = {0};
+    TT_CUDA_TRY(tt_smem_attr((const void*)ent_solve_kernel, sm, set_solve));
     ent_solve_kernel<<<1, ENT_NT, sm, st>>>(R, L, Ld, ncl, a->lam, (long long)a->t, gp, a->alpha_bar, gam, scal,
                                             (float2*)a->gamma_out, a->cost_out, a->status);
   }

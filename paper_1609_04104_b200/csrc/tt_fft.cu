@@ -116,11 +116,8 @@ extern "C" int tt_fft_cols(void* stream, float* data, int n, int ncols, int batc
     while (CB > 1 && (size_t)(2 * CB * n + n / 2) * sizeof(float2) > 200 * 1024) CB >>= 1;
     if (CB > ncols) CB = ncols;
     const size_t sm = (size_t)(2 * CB * n + n / 2) * sizeof(float2);
-    static size_t cfg = 0;
-    if (sm > cfg) {
-      TT_CUDA_TRY(cudaFuncSetAttribute(fft_pow2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      cfg = sm;
-    }
+    static size_t cfg[TT_MAXDEV] = {0};
+    TT_CUDA_TRY(tt_smem_attr((const void*)fft_pow2_kernel, sm, cfg));
     dim3 grid((ncols + CB - 1) / CB, batch);
     fft_pow2_kernel<<<grid, FFT_NT, sm, st>>>((float2*)data, n, logn, ncols, CB, inverse);
   } else if (n == 1) {
@@ -131,11 +128,8 @@ extern "C" int tt_fft_cols(void* stream, float* data, int n, int ncols, int batc
     while (CB > 1 && (size_t)(CB * n + n) * sizeof(float2) > 200 * 1024) CB >>= 1;
     if (CB > ncols) CB = ncols;
     const size_t sm = (size_t)(CB * n + n) * sizeof(float2);
-    static size_t cfg2 = 0;
-    if (sm > cfg2) {
-      TT_CUDA_TRY(cudaFuncSetAttribute(dft_direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      cfg2 = sm;
-    }
+    static size_t cfg2[TT_MAXDEV] = {0};
+    TT_CUDA_TRY(tt_smem_attr((const void*)dft_direct_kernel, sm, cfg2));
     dim3 grid((ncols + CB - 1) / CB, batch);
     dft_direct_kernel<<<grid, FFT_NT, sm, st>>>((float2*)data, n, ncols, CB, inverse);
   }

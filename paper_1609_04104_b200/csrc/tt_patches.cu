@@ -463,17 +463,14 @@ extern "C" int tt_track_patches(void* stream, const tt_patches_args* a) {
   static void (*const fns[])(tt_patches_args) = {patch_track_kernel<1>, patch_track_kernel<2>, patch_track_kernel<3>,
                                                   patch_track_kernel<4>, patch_track_kernel<6>, patch_track_kernel<8>,
                                                   patch_track_kernel<12>, patch_track_kernel<19>};
-  static size_t set_bytes[8] = {0};
+  static size_t set_bytes[8][TT_MAXDEV] = {{0}};
   int which = 7;
   for (int k = 0; k < 8; ++k)
     if (sizes[k] >= need) {
       which = k;
       break;
     }
-  if (sm > 48 * 1024 && sm > set_bytes[which]) {
-    TT_CUDA_TRY(cudaFuncSetAttribute(fns[which], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    set_bytes[which] = sm;
-  }
+  if (sm > 48 * 1024) TT_CUDA_TRY(tt_smem_attr((const void*)fns[which], sm, set_bytes[which]));
   fns[which]<<<a->npatch_local, PT_NT, sm, (cudaStream_t)stream>>>(*a);
   TT_CUDA_TRY(cudaGetLastError());
   return TT_OK;

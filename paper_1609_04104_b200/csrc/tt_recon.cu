@@ -73,11 +73,8 @@ extern "C" int tt_reconstruct(void* stream, int frames, int nx, int ny, int rank
   if (frames == 0) return TT_OK;
   if (frames > 65535) return tt_fail(TT_EINVAL, "tt_reconstruct: frames > 65535 per call");
   const size_t sm = sizeof(float2) * 2 * RC_T * (size_t)rank;
-  static size_t cfg = 0;
-  if (sm > cfg) {
-    TT_CUDA_TRY(cudaFuncSetAttribute(recon_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    cfg = sm;
-  }
+  static size_t cfg[TT_MAXDEV] = {0};
+  TT_CUDA_TRY(tt_smem_attr((const void*)recon_kernel, sm, cfg));
   dim3 grid((ny + RC_T - 1) / RC_T, (nx + RC_T - 1) / RC_T, frames);
   recon_kernel<<<grid, RC_NT, sm, (cudaStream_t)stream>>>(nx, ny, rank, (const float2*)a, (const float2*)b,
                                                           (const float2*)gamma, (float2*)x_out);

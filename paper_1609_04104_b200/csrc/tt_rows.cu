@@ -1094,14 +1094,17 @@ extern "C" int tt_track_rows(void* stream, const tt_rows_args* a) {
   static const RowsFn fns[8] = {tt_rows_kernel<1, false>, tt_rows_kernel<2, false>, tt_rows_kernel<5, false>,
                                 tt_rows_kernel<9, false>, tt_rows_kernel<1, true>,  tt_rows_kernel<2, true>,
                                 tt_rows_kernel<5, true>,  tt_rows_kernel<9, true>};
-  static int configured_smem[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+  static size_t configured_smem[8][TT_MAXDEV] = {{0}};
   const int ept = gj_ept(a->rank, ROWS_NT);
   const int which = (ept <= 1 ? 0 : ept <= 2 ? 1 : ept <= 5 ? 2 : 3) + (a->shard_world > 0 ? 4 : 0);
   const RowsFn fn = fns[which];
-  if (configured_smem[which] < pl.smem) {
-    TT_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
-    TT_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    configured_smem[which] = pl.smem;
+  {
+    int dev = 0;
+    TT_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev >= TT_MAXDEV || configured_smem[which][dev] < (size_t)pl.smem) {
+      TT_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      TT_CUDA_TRY(tt_smem_attr((const void*)fn, (size_t)pl.smem, configured_smem[which]));
+    }
   }
   cudaLaunchConfig_t cfg = {};
   const int nclusters = (a->shard_world > 0 && a->shard_local) ? a->shard_world : a->nslices;

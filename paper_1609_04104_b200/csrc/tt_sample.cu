@@ -670,11 +670,8 @@ extern "C" int tt_draw_with_replacement_large(void* stream, int n, const double*
     if (blocks > 1184) blocks = 1184;
     const size_t csm = sizeof(double) * ((size_t)((n + (1 << ls) - 1) >> ls) + nb + 1 + 64);
     if (csm > 48 * 1024) {
-      static size_t set_draw = 0;
-      if (csm > set_draw) {
-        TT_CUDA_TRY(cudaFuncSetAttribute(big_draw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
-        set_draw = csm;
-      }
+      static size_t set_draw[TT_MAXDEV] = {0};
+      TT_CUDA_TRY(tt_smem_attr((const void*)big_draw_kernel, csm, set_draw));
     }
     big_draw_kernel<<<blocks, 256, csm, st>>>(n, ndraw, cdf, cq, part, nb, forced, nforced, key0, key1, pos, flags,
                                               ctl, depth_term, gscale, ls);
