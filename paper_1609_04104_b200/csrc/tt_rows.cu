@@ -36,6 +36,7 @@
 #include <cooperative_groups.h>
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "tt_block.cuh"
 
@@ -45,7 +46,7 @@ namespace cg = cooperative_groups;
 #define ROWS_UF 32  // frames of precomputed Philox uniforms per refill
 
 struct RowsPlan {
-  int CL, KT, nIm, nJm, Rp, red_cap;
+  int CL, KT, nIm, nJm, Rp, red_cap, tight;
   int o_ahl, o_bhl, o_u1, o_gaf, o_gbf, o_vec, o_tab, o_flags, o_rows, o_forced, o_usm, o_own, o_wacc, o_zs, o_red2,
       o_u2, o_red;
   int smem;
@@ -76,14 +77,20 @@ __host__ __device__ inline RowsScratch rows_scratch_layout(int nx, int ny, int R
   return s;
 }
 
-static bool rows_make_plan_cap(int nx, int ny, int R, int Smax, int CL, int red_cap, RowsPlan* p);
+static bool rows_make_plan_cap(int nx, int ny, int R, int Smax, int CL, int red_cap, bool tight, RowsPlan* p);
 // The K-split reduction buffer of the small GEMMs is optional: when shared
-// memory is tight (R = 64 at large N) the plan drops it and every GEMM runs
-// with KS = 1.
+// memory is tight the plan drops it and every GEMM runs with KS = 1. When even
+// that does not fit (R = 64 at 1024^2) the "tight" plan also drops the fp32
+// copies of GA / GB and the fp64 staging of Bh: the GB partials convert Bh on
+// the fly, and the two update GEMMs run one after the other with their
+// gamma-scaled R x R operand built in the (then free) solver workspace U1.
 static bool rows_make_plan(int nx, int ny, int R, int Smax, int CL, RowsPlan* p) {
-  return rows_make_plan_cap(nx, ny, R, Smax, CL, 2048, p) || rows_make_plan_cap(nx, ny, R, Smax, CL, 0, p);
+  if (const char* e = getenv("TT_ROWS_FORCE_TIGHT"))  // test hook: the tight plan at any shape (R >= 24)
+    if (e[0] == '1' && R >= 24) return rows_make_plan_cap(nx, ny, R, Smax, CL, 0, true, p);
+  return rows_make_plan_cap(nx, ny, R, Smax, CL, 2048, false, p) ||
+         rows_make_plan_cap(nx, ny, R, Smax, CL, 0, false, p) || rows_make_plan_cap(nx, ny, R, Smax, CL, 0, true, p);
 }
-static bool rows_make_plan_cap(int nx, int ny, int R, int Smax, int CL, int red_cap, RowsPlan* p) {
+static bool rows_make_plan_cap(int nx, int ny, int R, int Smax, int CL, int red_cap, bool tight, RowsPlan* p) {
   const int maxsmem = 227 * 1024;
   if (R > 64) return false;
   p->CL = CL;
@@ -91,17 +98,22 @@ static bool rows_make_plan_cap(int nx, int ny, int R, int Smax, int CL, int red_
   p->nJm = (ny + CL - 1) / CL;
   p->Rp = R * (R + 1) / 2;
   p->red_cap = red_cap;
+  p->tight = tight ? 1 : 0;
   size_t o = 0;
   p->o_ahl = (int)o;    o = al16(o + sizeof(float2) * p->nIm * R);
   p->o_bhl = (int)o;    o = al16(o + sizeof(float2) * p->nJm * R);
-  p->o_u1 = (int)o;     // packed fp64 Gram / LDL workspace  |  p + cdf (draw phase)
+  p->o_u1 = (int)o;     // packed fp64 Gram / LDL workspace  |  p + cdf (draw phase)  |  tight: update operand
   {
     size_t g = sizeof(double2) * (size_t)p->Rp;
     size_t d = sizeof(double) * 2 * (size_t)nx;
-    o = al16(o + (g > d ? g : d));
+    size_t m = tight ? sizeof(float2) * (size_t)R * R : 0;
+    if (d > g) g = d;
+    if (m > g) g = m;
+    o = al16(o + g);
   }
-  p->o_gaf = (int)o;    o = al16(o + sizeof(float2) * R * R);  // full Hermitian fp32 GA, GB
-  p->o_gbf = (int)o;    o = al16(o + sizeof(float2) * R * R);
+  const size_t gfull = tight ? 0 : sizeof(float2) * R * R;
+  p->o_gaf = (int)o;    o = al16(o + gfull);  // full Hermitian fp32 GA, GB (not in the tight plan)
+  p->o_gbf = (int)o;    o = al16(o + gfull);
   // vec: gam, hv, hsave (double2 R); nrm, inrm, inv, gda, gdb (double R); gamf (float2 R); 16 scalars
   //      + LDL scratch: colb 4 (R+1) double2, blk 4 (R/2+1) double, zf R double2
   p->o_vec = (int)o;    o = al16(o + sizeof(double2) * R * 3 + sizeof(double) * R * 5 + sizeof(float2) * R + 128 +
@@ -119,8 +131,9 @@ static bool rows_make_plan_cap(int nx, int ny, int R, int Smax, int CL, int red_
   size_t fixed = o + sizeof(double) * 64;
   if (fixed > (size_t)maxsmem) return false;
   // U2: k-tiles (ys KT x nJm, ahs KT x R) | Bh in fp64 + colnorm partials (phase a) | gamma-scaled GEMM operands
-  size_t other = sizeof(double2) * (size_t)p->nJm * R + sizeof(double) * 256;
-  const size_t v2 = sizeof(float2) * (size_t)R * (p->nJm + p->nIm);  // both gamma-scaled GEMM operands
+  // (tight: only the column-norm and h partials, <= NT doubles / double2s)
+  size_t other = tight ? sizeof(double2) * ROWS_NT + 256 : sizeof(double2) * (size_t)p->nJm * R + sizeof(double) * 256;
+  const size_t v2 = tight ? 0 : sizeof(float2) * (size_t)R * (p->nJm + p->nIm);  // both gamma-scaled GEMM operands
   if (v2 > other) other = v2;
   size_t avail = maxsmem - fixed;
   int KT = (int)(avail / (sizeof(float2) * (size_t)(p->nJm + R)));
@@ -141,7 +154,7 @@ static bool rows_make_plan_cap(int nx, int ny, int R, int Smax, int CL, int red_
 // ---------------------------------------------------------------- GEMM epilogues
 // The four small GEMMs of a frame share one cgemm_tile instantiation (one copy of its code in the
 // frame loop); the epilogue is selected by a block-uniform mode.
-enum { EPI_W_ACC = 0, EPI_Z_STORE = 1, EPI_Q_UPDATE = 2, EPI_P_UPDATE = 3 };
+enum { EPI_W_ACC = 0, EPI_Z_STORE = 1, EPI_Q_UPDATE = 2, EPI_P_UPDATE = 3, EPI_P_MAPPED = 4 };
 struct RowsEpi {
   int mode, R;
   float2* acc;          // W: wacc | Q: wacc (in: W, out: new Bh rows) | P: zs (in: Z sums, out: mu conj(g) P)
@@ -149,8 +162,9 @@ struct RowsEpi {
   float2* gdst;         // Z: L2 partials
   const float2* gamf;
   float cfac, muf;
+  const int* rmap;      // P_MAPPED (tight plan): local row -> position in the owned sampled rows, or -1
   TT_DEV void operator()(int m, int n, float2 v) const {
-    const int o = m * R + n;
+    int o = m * R + n;
     switch (mode) {
       case EPI_W_ACC:
         acc[o] = cadd(acc[o], v);
@@ -161,6 +175,11 @@ struct RowsEpi {
         break;
       case EPI_Q_UPDATE:
         acc[o] = cadd(cscale(base[o], cfac), cscale(cmul(cconj(gamf[n]), csub(acc[o], v)), muf));
+        break;
+      case EPI_P_MAPPED:  // tight plan: the GEMM ran over every local row, keep the sampled ones
+        if (rmap[m] < 0) break;
+        o = rmap[m] * R + n;
+        acc[o] = cscale(cmul(cconj(gamf[n]), csub(acc[o], v)), muf);
         break;
       default:
         acc[o] = cscale(cmul(cconj(gamf[n]), csub(acc[o], v)), muf);  // mu conj(g) P
@@ -232,9 +251,10 @@ static __device__ __noinline__ void write_residual(const tt_rows_args& a, const 
 
 // ---------------------------------------------------------------- the kernel
 // SOLV: the one solver compiled in (1 / 2 / 5: Gauss-Jordan entries per thread, 9: 2x2-blocked LDL^H);
-// SHARD: whether the row-sharding phases are compiled in. Every inlined variant costs
-// instruction-cache lines in the frame loop, so each launch gets only the code it runs.
-template <int SOLV, bool SHARD>
+// SHARD: whether the row-sharding phases are compiled in; TIGHT: the tight shared-memory plan
+// (rows_make_plan_cap). Every inlined variant costs instruction-cache lines in the frame loop,
+// so each launch gets only the code it runs.
+template <int SOLV, bool SHARD, bool TIGHT = false>
 __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_constant__ tt_rows_args a,
                                                              const __grid_constant__ RowsPlan pl) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -295,7 +315,8 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
   float2* ys = (float2*)(smem + pl.o_u2);
   float2* ahs = ys + (size_t)KT * pl.nJm;
   double2* bh64 = (double2*)(smem + pl.o_u2);          // phase (a) only
-  double* cnp = (double*)(bh64 + (size_t)pl.nJm * R);   // phase (a) only: colnorm partials [parts][R]
+  // phase (a) only: colnorm partials [parts][R] (after the fp64 Bh, which the tight plan does not stage)
+  double* cnp = TIGHT ? (double*)(smem + pl.o_u2) : (double*)(bh64 + (size_t)pl.nJm * R);
   float2* vop = (float2*)(smem + pl.o_u2);              // update only: gamma-scaled GEMM operand
   double* red = (double*)(smem + pl.o_red);
   (void)inv;
@@ -369,7 +390,8 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       }
       cnp[part * R + r] = acc;
     }
-    for (int o = tid; o < nJ * R; o += NT) bh64[o] = to_d2(bhl[o]);
+    if (!TIGHT)
+      for (int o = tid; o < nJ * R; o += NT) bh64[o] = to_d2(bhl[o]);
     __syncthreads();
     if (tid < R) {
       double acc = 0.0;
@@ -382,11 +404,19 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       const int r = ij >> 8, q = ij & 255;
       double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
       int jj = 0;
-      for (; jj + 1 < nJ; jj += 2) {
-        acc = zfma_cj(bh64[jj * R + r], bh64[jj * R + q], acc);
-        acc2 = zfma_cj(bh64[(jj + 1) * R + r], bh64[(jj + 1) * R + q], acc2);
+      if (TIGHT) {  // same products as the fp64 staging (exact fp32 -> fp64 conversion in zfma_cj)
+        for (; jj + 1 < nJ; jj += 2) {
+          acc = zfma_cj(bhl[jj * R + r], bhl[jj * R + q], acc);
+          acc2 = zfma_cj(bhl[(jj + 1) * R + r], bhl[(jj + 1) * R + q], acc2);
+        }
+        if (jj < nJ) acc = zfma_cj(bhl[jj * R + r], bhl[jj * R + q], acc);
+      } else {
+        for (; jj + 1 < nJ; jj += 2) {
+          acc = zfma_cj(bh64[jj * R + r], bh64[jj * R + q], acc);
+          acc2 = zfma_cj(bh64[(jj + 1) * R + r], bh64[(jj + 1) * R + q], acc2);
+        }
+        if (jj < nJ) acc = zfma_cj(bh64[jj * R + r], bh64[jj * R + q], acc);
       }
-      if (jj < nJ) acc = zfma_cj(bh64[jj * R + r], bh64[jj * R + q], acc);
       acc = zadd(acc, acc2);
       __stcg(&g_gbp[(size_t)c * Rp + e].x, acc.x);
       __stcg(&g_gbp[(size_t)c * Rp + e].y, acc.y);
@@ -829,10 +859,12 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         gdb[r] = gbe.x;
       }
       G[e] = gg;
-      gaf[r * R + q] = to_f2(gae);
-      gaf[q * R + r] = to_f2(zconj(gae));
-      gbf[r * R + q] = to_f2(gbe);
-      gbf[q * R + r] = to_f2(zconj(gbe));
+      if (!TIGHT) {
+        gaf[r * R + q] = to_f2(gae);
+        gaf[q * R + r] = to_f2(zconj(gae));
+        gbf[r * R + q] = to_f2(gbe);
+        gbf[q * R + r] = to_f2(zconj(gbe));
+      }
     }
     if (tid < R) {
       const double2 h = sum_parts2(g_hp + tid, (size_t)R, CL);
@@ -918,24 +950,55 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     if (update) {
       const float cfac = (float)(1.0 - mu_used * lt);
       const float muf = (float)mu_used;
-      // gamma-scaled operands of both corrections at once: Bh diag(g) and Ah_own diag(g)
-      float2* vop2 = vop + (size_t)pl.nJm * R;
-      for (int o = tid; o < nJ * R; o += NT) vop[o] = cmul(bhl[o], gamf[o - idiv(o, R) * R]);
-      for (int o = tid; o < nown * R; o += NT) {
-        const int m = idiv(o, R), q = o - m * R;
-        vop2[o] = cmul(ahl[own_li[m] * R + q], gamf[q]);
-      }
-      __syncthreads();
-      STAMP(21);
-      // Q: corr[jj][r] = sum_q vop[jj][q] conj(GA[q][r]) -> new Bh rows; P: same with GB on the owned
-      // sampled rows -> mu conj(g) P. One call site, so one copy of the GEMM code.
-      for (int gsel = 0; gsel < 2; ++gsel) {
-        const bool q = gsel == 0;
-        const int M = q ? nJ : nown;
-        const int ks = gemm_split(M, R, R, 2, 4, pl.red_cap);
-        const RowsEpi epi{q ? EPI_Q_UPDATE : EPI_P_UPDATE, R, q ? wacc : zs, bhl, nullptr, gamf, cfac, muf};
-        cgemm_tile<2, 4, false, true>(M, R, R, q ? vop : vop2, R, 1, q ? gaf : gbf, R, 1, ks, red2, epi);
+      if (TIGHT) {
+        // one correction at a time, the gamma scaling moved onto the R x R factor:
+        // corr[m][r] = sum_q X[m][q] conj(conj(g_q) G[q][r]) with (X, G) = (Bh, GA) then (Ah, GB)
+        // (the P GEMM runs over every local row; its epilogue keeps the sampled ones)
+        float2* mq = (float2*)(smem + pl.o_u1);  // the solver workspace is free now
+        for (int gsel = 0; gsel < 2; ++gsel) {
+          const bool q = gsel == 0;
+          for (int e = tid; e < Rp; e += NT) {
+            const int ij = tab[e];
+            const int r = ij >> 8, qq = ij & 255;
+            double2 gv;
+            if (q && phase == 2) {
+              gv.x = a.xg[2 * e];
+              gv.y = a.xg[2 * e + 1];
+            } else {
+              const double2* src = q ? g_ga : g_gb;
+              gv.x = __ldcg(&src[e].x);
+              gv.y = __ldcg(&src[e].y);
+            }
+            const float2 g = to_f2(gv);
+            mq[r * R + qq] = cmul(cconj(gamf[r]), g);
+            mq[qq * R + r] = cmul(cconj(gamf[qq]), cconj(g));
+          }
+          __syncthreads();
+          const int M = q ? nJ : (nown > 0 ? nI : 0);
+          const RowsEpi epi{q ? EPI_Q_UPDATE : EPI_P_MAPPED, R, q ? wacc : zs, bhl, nullptr, gamf, cfac, muf, flags};
+          cgemm_tile<2, 4, false, true>(M, R, R, q ? bhl : ahl, R, 1, mq, R, 1, 1, red2, epi);
+          __syncthreads();
+        }
+      } else {
+        // gamma-scaled operands of both corrections at once: Bh diag(g) and Ah_own diag(g)
+        float2* vop2 = vop + (size_t)pl.nJm * R;
+        for (int o = tid; o < nJ * R; o += NT) vop[o] = cmul(bhl[o], gamf[o - idiv(o, R) * R]);
+        for (int o = tid; o < nown * R; o += NT) {
+          const int m = idiv(o, R), q = o - m * R;
+          vop2[o] = cmul(ahl[own_li[m] * R + q], gamf[q]);
+        }
         __syncthreads();
+        STAMP(21);
+        // Q: corr[jj][r] = sum_q vop[jj][q] conj(GA[q][r]) -> new Bh rows; P: same with GB on the owned
+        // sampled rows -> mu conj(g) P. One call site, so one copy of the GEMM code.
+        for (int gsel = 0; gsel < 2; ++gsel) {
+          const bool q = gsel == 0;
+          const int M = q ? nJ : nown;
+          const int ks = gemm_split(M, R, R, 2, 4, pl.red_cap);
+          const RowsEpi epi{q ? EPI_Q_UPDATE : EPI_P_UPDATE, R, q ? wacc : zs, bhl, nullptr, gamf, cfac, muf};
+          cgemm_tile<2, 4, false, true>(M, R, R, q ? vop : vop2, R, 1, q ? gaf : gbf, R, 1, ks, red2, epi);
+          __syncthreads();
+        }
       }
       STAMP(22);
       STAMP(23);
@@ -1091,12 +1154,21 @@ extern "C" int tt_track_rows(void* stream, const tt_rows_args* a) {
   if (a->cluster > 0 && a->cluster != pl.CL) return tt_fail(TT_EINVAL, "cluster mismatch");
   // the instantiation: solver by Gauss-Jordan entries per thread, sharding phases only when sharded
   typedef void (*RowsFn)(const tt_rows_args, const RowsPlan);
-  static const RowsFn fns[8] = {tt_rows_kernel<1, false>, tt_rows_kernel<2, false>, tt_rows_kernel<5, false>,
-                                tt_rows_kernel<9, false>, tt_rows_kernel<1, true>,  tt_rows_kernel<2, true>,
-                                tt_rows_kernel<5, true>,  tt_rows_kernel<9, true>};
-  static size_t configured_smem[8][TT_MAXDEV] = {{0}};
+  static const RowsFn fns[10] = {tt_rows_kernel<1, false>, tt_rows_kernel<2, false>, tt_rows_kernel<5, false>,
+                                 tt_rows_kernel<9, false>, tt_rows_kernel<1, true>,  tt_rows_kernel<2, true>,
+                                 tt_rows_kernel<5, true>,  tt_rows_kernel<9, true>,
+                                 tt_rows_kernel<5, false, true>, tt_rows_kernel<9, false, true>};
+  static size_t configured_smem[10][TT_MAXDEV] = {{0}};
   const int ept = gj_ept(a->rank, ROWS_NT);
-  const int which = (ept <= 1 ? 0 : ept <= 2 ? 1 : ept <= 5 ? 2 : 3) + (a->shard_world > 0 ? 4 : 0);
+  const int solv = ept <= 1 ? 0 : ept <= 2 ? 1 : ept <= 5 ? 2 : 3;
+  int which = solv + (a->shard_world > 0 ? 4 : 0);
+  if (pl.tight) {
+    // the tight plan is needed only at large N x R (R = 64 at 1024^2); compiled for the two wide solvers
+    if (a->shard_world > 0 || solv < 2)
+      return tt_fail(TT_EUNSUPPORTED, "row-mask step (nx=%d R=%d rows=%d) needs the tight shared-memory plan, "
+                                      "which is not built for this solver / sharding", a->nx, a->rank, a->max_rows);
+    which = 8 + (solv - 2);
+  }
   const RowsFn fn = fns[which];
   {
     int dev = 0;

@@ -79,3 +79,55 @@ def test_patch_ranks_on_non_square_patches(rho, n1, n2):
         assert rel(res.step_gamma[k], st["gamma"]) < 1e-4, k
         assert rel(res.step_mu[k], st["mu"]) < 1e-4, k
     assert rel(res.recon, ref["recon"]) < 1e-4
+
+
+@pytest.mark.parametrize("nx,ny,R", [(64, 48, 33), (48, 40, 40), (40, 36, 64)])
+def test_row_engine_tight_plan(nx, ny, R, monkeypatch):
+    """The tight shared-memory plan (no fp32 GA/GB copies, no fp64 Bh staging, the two update GEMMs in
+    sequence with a gamma-scaled R x R operand; rows_make_plan_cap) forced at small shapes."""
+    import paper_1609_04104_b200 as tt
+
+    monkeypatch.setenv("TT_ROWS_FORCE_TIGHT", "1")
+    T, lam = 6, 0.1
+    ks = _lowrank(T, nx, ny, nx + R + 1)
+    A0, B0 = O.random_subspace(nx, ny, R, seed=R + 1)
+    g = np.random.default_rng(R + 1)
+    S = max(2, nx // 3)
+    rows = [np.sort(g.choice(nx, S, replace=False)) for _ in range(T)]
+    ref = O.online_run(ks, A0, B0, lam, ("fixed", 0.05), {"kind": "static", "rows": rows}, record_factors=True)
+    tab = np.stack(rows)[:, None, :]
+    res = tt.run_online(ks, A0[None], B0[None], lam, tt.Fixed(0.05), tt.StaticRows(tab, np.full((T, 1), S)))
+    for f in range(T):
+        assert rel(res.gamma[f, 0], ref["gamma"][f]) < 1e-4, f
+    assert rel(res.final_A[0], ref["A"][-1]) < 1e-4
+    assert rel(res.final_B[0], ref["B"][-1]) < 1e-4
+
+
+@pytest.mark.parametrize("kind", ["static", "informative"])
+def test_row_engine_1024_rank64(kind):
+    """1024^2 at R = 64 (BASELINE C5's largest point): only the tight plan fits; several k tiles per
+    frame (KT < S). Three frames against the oracle."""
+    import paper_1609_04104_b200 as tt
+
+    n, R, T, lam = 1024, 64, 3, 0.05
+    ks = _lowrank(T, n, n, 11)
+    A0, B0 = O.random_subspace(n, n, R, seed=12)
+    if kind == "static":
+        gen = np.random.Generator(np.random.Philox(key=5))
+        rows = [O.vd_rows(n, -1.0, 0.1, gen.random) for _ in range(T)]
+        S = len(rows[0])
+        ref = O.online_run(ks, A0, B0, lam, ("fixed", 0.01), {"kind": "static", "rows": rows}, record_factors=True)
+        res = tt.run_online(ks, A0[None], B0[None], lam, tt.Fixed(0.01),
+                            tt.StaticRows(np.stack(rows)[:, None, :], np.full((T, 1), S)))
+    else:
+        ref = O.online_run(ks, A0, B0, lam, ("fixed", 0.01),
+                           {"kind": "informative", "k": 103, "forced": [0], "beta": 0.1, "key": (9, 0)},
+                           record_factors=True)
+        res = tt.run_online(ks, A0[None], B0[None], lam, tt.Fixed(0.01),
+                            tt.Informative(k=103, forced=(0,), beta=0.1, key0=9))
+        for f in range(T):
+            assert np.array_equal(res.rows[f][0], ref["rows"][f]), f
+    for f in range(T):
+        assert rel(res.gamma[f, 0], ref["gamma"][f]) < 1e-4, f
+    assert rel(res.final_A[0], ref["A"][-1]) < 1e-4
+    assert rel(res.final_B[0], ref["B"][-1]) < 1e-4
