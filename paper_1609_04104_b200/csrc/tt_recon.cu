@@ -15,24 +15,45 @@
 #define RC_T 64
 #define RC_NT 256
 #define RC_RMAX 64
+#define RC_TP (RC_T + 1)  // padded row of the staged [r][64] tiles: conflict-free transposing stores
 
 __global__ void __launch_bounds__(RC_NT) recon_kernel(int nx, int ny, int R, const float2* __restrict__ A,
                                                       const float2* __restrict__ B, const float2* __restrict__ gamma,
                                                       float2* __restrict__ X) {
   extern __shared__ __align__(16) float2 rsm[];
-  float2* as = rsm;               // [R][64]
-  float2* bs = rsm + R * RC_T;    // [R][64]
+  float2* as = rsm;               // [R][RC_TP]
+  float2* bs = rsm + R * RC_TP;   // [R][RC_TP]
   const int tid = threadIdx.x;
   const int f = blockIdx.z;
   const int i0 = blockIdx.y * RC_T, j0 = blockIdx.x * RC_T;
   const float2* Af = A + (size_t)f * nx * R;
   const float2* Bf = B + (size_t)f * ny * R;
   const float2* gf = gamma + (size_t)f * R;
-  for (int o = tid; o < RC_T * R; o += RC_NT) {
-    const int ii = o / R, r = o - ii * R;
-    const int i = i0 + ii, j = j0 + ii;
-    as[r * RC_T + ii] = i < nx ? cmul(Af[(size_t)i * R + r], gf[r]) : make_float2(0.f, 0.f);
-    bs[r * RC_T + ii] = j < ny ? Bf[(size_t)j * R + r] : make_float2(0.f, 0.f);
+  // staging: all of a thread's global loads in flight before the first shared-memory store
+  // (the A / B tiles are contiguous rows of R values; up to 4 (A, B) pairs per thread per batch)
+  for (int base = 0; base < RC_T * R; base += 4 * RC_NT) {
+    float2 va[4], vb[4], vg[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int o = base + u * RC_NT + tid;
+      va[u] = vb[u] = vg[u] = make_float2(0.f, 0.f);
+      if (o < RC_T * R) {
+        const int ii = idiv(o, R), r = o - ii * R;
+        const int i = i0 + ii, j = j0 + ii;
+        vg[u] = gf[r];
+        if (i < nx) va[u] = Af[(size_t)i * R + r];
+        if (j < ny) vb[u] = Bf[(size_t)j * R + r];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int o = base + u * RC_NT + tid;
+      if (o < RC_T * R) {
+        const int ii = idiv(o, R), r = o - ii * R;
+        as[r * RC_TP + ii] = cmul(va[u], vg[u]);
+        bs[r * RC_TP + ii] = vb[u];
+      }
+    }
   }
   __syncthreads();
   const int tj = tid & 15, ti = tid >> 4;  // 16 x 16 threads, 4 x 4 outputs each
@@ -44,9 +65,9 @@ __global__ void __launch_bounds__(RC_NT) recon_kernel(int nx, int ny, int R, con
   for (int r = 0; r < R; ++r) {
     float2 av[4], bv[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) av[u] = as[r * RC_T + ti + 16 * u];
+    for (int u = 0; u < 4; ++u) av[u] = as[r * RC_TP + ti + 16 * u];
 #pragma unroll
-    for (int v = 0; v < 4; ++v) bv[v] = bs[r * RC_T + tj + 16 * v];
+    for (int v = 0; v < 4; ++v) bv[v] = bs[r * RC_TP + tj + 16 * v];
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
@@ -72,7 +93,7 @@ extern "C" int tt_reconstruct(void* stream, int frames, int nx, int ny, int rank
   if (rank > RC_RMAX) return tt_fail(TT_EUNSUPPORTED, "tt_reconstruct: rank > %d", RC_RMAX);
   if (frames == 0) return TT_OK;
   if (frames > 65535) return tt_fail(TT_EINVAL, "tt_reconstruct: frames > 65535 per call");
-  const size_t sm = sizeof(float2) * 2 * RC_T * (size_t)rank;
+  const size_t sm = sizeof(float2) * 2 * RC_TP * (size_t)rank;
   static size_t cfg[TT_MAXDEV] = {0};
   TT_CUDA_TRY(tt_smem_attr((const void*)recon_kernel, sm, cfg));
   dim3 grid((ny + RC_T - 1) / RC_T, (nx + RC_T - 1) / RC_T, frames);
