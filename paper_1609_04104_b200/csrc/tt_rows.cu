@@ -81,8 +81,7 @@ static bool rows_make_plan_cap(int nx, int ny, int R, int Smax, int CL, int red_
 // The K-split reduction buffer of the small GEMMs is optional: when shared
 // memory is tight the plan drops it and every GEMM runs with KS = 1. When even
 // that does not fit (R = 64 at 1024^2) the "tight" plan also drops the fp32
-// copies of GA / GB and the fp64 staging of Bh: the GB partials convert Bh on
-// the fly, and the two update GEMMs run one after the other with their
+// copies of GA / GB: the two update GEMMs run one after the other with their
 // gamma-scaled R x R operand built in the (then free) solver workspace U1.
 static bool rows_make_plan(int nx, int ny, int R, int Smax, int CL, RowsPlan* p) {
   if (const char* e = getenv("TT_ROWS_FORCE_TIGHT"))  // test hook: the tight plan at any shape (R >= 24)
@@ -131,8 +130,11 @@ static bool rows_make_plan_cap(int nx, int ny, int R, int Smax, int CL, int red_
   size_t fixed = o + sizeof(double) * 64;
   if (fixed > (size_t)maxsmem) return false;
   // U2: k-tiles (ys KT x nJm, ahs KT x R) | Bh in fp64 + colnorm partials (phase a) | gamma-scaled GEMM operands
-  // (tight: only the column-norm and h partials, <= NT doubles / double2s)
-  size_t other = tight ? sizeof(double2) * ROWS_NT + 256 : sizeof(double2) * (size_t)p->nJm * R + sizeof(double) * 256;
+  // phase (a): Bh in fp64 (not in the tight plan) + GB partial tiles (4 double2 per item, <= max(2 NT,
+  // tiles) items) + colnorm partials (<= NT doubles); the h partials later (<= NT double2)
+  const int gb_rt = (R + 1) / 2, gb_nt = gb_rt * (gb_rt + 1) / 2;
+  size_t other = (tight ? 0 : sizeof(double2) * (size_t)p->nJm * R) +
+                 4 * sizeof(double2) * (size_t)(gb_nt > 2 * ROWS_NT ? gb_nt : 2 * ROWS_NT) + sizeof(double) * ROWS_NT + 256;
   const size_t v2 = tight ? 0 : sizeof(float2) * (size_t)R * (p->nJm + p->nIm);  // both gamma-scaled GEMM operands
   if (v2 > other) other = v2;
   size_t avail = maxsmem - fixed;
@@ -249,6 +251,58 @@ static __device__ __noinline__ void write_residual(const tt_rows_args& a, const 
   }
 }
 
+// GB partial over a CTA's columns for wide column blocks (out of line: narrow blocks, config 2, keep
+// the frame loop's instruction footprint): 2 x 2 register tiles of the lower triangle (four products
+// per four operand loads), the columns split in `parts` interleaved parts, then a fixed-order sum of
+// the parts per packed entry into dst_g.
+template <bool TIGHT>
+static __device__ __noinline__ void gb_partials_tiled(const float2* bhl, const double2* bh64, int R, int nJ, int Rp,
+                                                      int gb_nt, int gb_parts, const unsigned short* tab,
+                                                      double2* gbt, double2* dst_g) {
+  const int tid = threadIdx.x, NT = blockDim.x;
+  for (int it = tid; it < gb_nt * gb_parts; it += NT) {
+    const int part = idiv(it, gb_nt), t = it - part * gb_nt;
+    int tr, tq;
+    tri_decode(t, tr, tq);
+    const int r0 = 2 * tr, q0 = 2 * tq, r1 = min(r0 + 1, R - 1), q1 = min(q0 + 1, R - 1);
+    double2 a00 = make_double2(0.0, 0.0), a01 = a00, a10 = a00, a11 = a00;
+    if (TIGHT) {  // fp32 operands converted on the fly (same products)
+      for (int jj = part; jj < nJ; jj += gb_parts) {
+        const float2* row = bhl + jj * R;
+        const float2 br0 = row[r0], br1 = row[r1], bq0 = row[q0], bq1 = row[q1];
+        a00 = zfma_cj(br0, bq0, a00);
+        a01 = zfma_cj(br0, bq1, a01);
+        a10 = zfma_cj(br1, bq0, a10);
+        a11 = zfma_cj(br1, bq1, a11);
+      }
+    } else {
+      for (int jj = part; jj < nJ; jj += gb_parts) {
+        const double2* row = bh64 + jj * R;
+        const double2 br0 = row[r0], br1 = row[r1], bq0 = row[q0], bq1 = row[q1];
+        a00 = zfma_cj(br0, bq0, a00);
+        a01 = zfma_cj(br0, bq1, a01);
+        a10 = zfma_cj(br1, bq0, a10);
+        a11 = zfma_cj(br1, bq1, a11);
+      }
+    }
+    double2* dst = gbt + 4 * (size_t)it;
+    dst[0] = a00;
+    dst[1] = a01;
+    dst[2] = a10;
+    dst[3] = a11;
+  }
+  __syncthreads();
+  for (int e = tid; e < Rp; e += NT) {
+    const int ij = tab[e];
+    const int r = ij >> 8, q = ij & 255;
+    const int t = tri_idx(r >> 1, q >> 1), sub = ((r & 1) << 1) | (q & 1);
+    double2 acc = gbt[4 * t + sub];
+    for (int part = 1; part < gb_parts; ++part) acc = zadd(acc, gbt[4 * ((size_t)part * gb_nt + t) + sub]);
+    __stcg(&dst_g[e].x, acc.x);
+    __stcg(&dst_g[e].y, acc.y);
+  }
+}
+
 // ---------------------------------------------------------------- the kernel
 // SOLV: the one solver compiled in (1 / 2 / 5: Gauss-Jordan entries per thread, 9: 2x2-blocked LDL^H);
 // SHARD: whether the row-sharding phases are compiled in; TIGHT: the tight shared-memory plan
@@ -314,9 +368,15 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
   float2* red2 = (float2*)(smem + pl.o_red2);
   float2* ys = (float2*)(smem + pl.o_u2);
   float2* ahs = ys + (size_t)KT * pl.nJm;
-  double2* bh64 = (double2*)(smem + pl.o_u2);          // phase (a) only
-  // phase (a) only: colnorm partials [parts][R] (after the fp64 Bh, which the tight plan does not stage)
-  double* cnp = TIGHT ? (double*)(smem + pl.o_u2) : (double*)(bh64 + (size_t)pl.nJm * R);
+  // phase (a) only: Bh in fp64 (not in the tight plan), GB partial tiles [parts][tiles][4], then the
+  // colnorm partials [parts][R]
+  const int gb_rt = (R + 1) >> 1, gb_nt = gb_rt * (gb_rt + 1) / 2;  // 2 x 2 tiles of the lower triangle
+  // one packed entry per thread unless that leaves threads idle over a long column block (config 3)
+  const bool gb_tiled = nJ * R >= 1024 && Rp <= NT;
+  const int gb_parts = max(1, (NT + gb_nt / 2) / gb_nt);
+  double2* bh64 = (double2*)(smem + pl.o_u2);
+  double2* gbt = TIGHT ? bh64 : bh64 + (size_t)pl.nJm * R;
+  double* cnp = (double*)(gbt + 4 * (size_t)max(2 * NT, gb_nt));
   float2* vop = (float2*)(smem + pl.o_u2);              // update only: gamma-scaled GEMM operand
   double* red = (double*)(smem + pl.o_red);
   (void)inv;
@@ -399,27 +459,33 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       __stcg(&g_cn[c * R + tid], acc);
     }
     STAMP(26);
-    for (int e = tid; e < Rp; e += NT) {
-      const int ij = tab[e];
-      const int r = ij >> 8, q = ij & 255;
-      double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
-      int jj = 0;
-      if (TIGHT) {  // same products as the fp64 staging (exact fp32 -> fp64 conversion in zfma_cj)
-        for (; jj + 1 < nJ; jj += 2) {
-          acc = zfma_cj(bhl[jj * R + r], bhl[jj * R + q], acc);
-          acc2 = zfma_cj(bhl[(jj + 1) * R + r], bhl[(jj + 1) * R + q], acc2);
+    // GB partial over own columns: wide column blocks tiled (gb_partials_tiled), narrow ones one
+    // packed entry per thread
+    if (gb_tiled) {
+      gb_partials_tiled<TIGHT>(bhl, bh64, R, nJ, Rp, gb_nt, gb_parts, tab, gbt, g_gbp + (size_t)c * Rp);
+    } else {
+      for (int e = tid; e < Rp; e += NT) {
+        const int ij = tab[e];
+        const int r = ij >> 8, q = ij & 255;
+        double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
+        int jj = 0;
+        if (TIGHT) {
+          for (; jj + 1 < nJ; jj += 2) {
+            acc = zfma_cj(bhl[jj * R + r], bhl[jj * R + q], acc);
+            acc2 = zfma_cj(bhl[(jj + 1) * R + r], bhl[(jj + 1) * R + q], acc2);
+          }
+          if (jj < nJ) acc = zfma_cj(bhl[jj * R + r], bhl[jj * R + q], acc);
+        } else {
+          for (; jj + 1 < nJ; jj += 2) {
+            acc = zfma_cj(bh64[jj * R + r], bh64[jj * R + q], acc);
+            acc2 = zfma_cj(bh64[(jj + 1) * R + r], bh64[(jj + 1) * R + q], acc2);
+          }
+          if (jj < nJ) acc = zfma_cj(bh64[jj * R + r], bh64[jj * R + q], acc);
         }
-        if (jj < nJ) acc = zfma_cj(bhl[jj * R + r], bhl[jj * R + q], acc);
-      } else {
-        for (; jj + 1 < nJ; jj += 2) {
-          acc = zfma_cj(bh64[jj * R + r], bh64[jj * R + q], acc);
-          acc2 = zfma_cj(bh64[(jj + 1) * R + r], bh64[(jj + 1) * R + q], acc2);
-        }
-        if (jj < nJ) acc = zfma_cj(bh64[jj * R + r], bh64[jj * R + q], acc);
+        acc = zadd(acc, acc2);
+        __stcg(&g_gbp[(size_t)c * Rp + e].x, acc.x);
+        __stcg(&g_gbp[(size_t)c * Rp + e].y, acc.y);
       }
-      acc = zadd(acc, acc2);
-      __stcg(&g_gbp[(size_t)c * Rp + e].x, acc.x);
-      __stcg(&g_gbp[(size_t)c * Rp + e].y, acc.y);
     }
     if (ndraw > 0 && f % ROWS_UF == 0) {
       // Philox uniforms of the next ROWS_UF frames (stream positions are state independent), split
@@ -804,8 +870,8 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     __syncthreads();
     // h partial: sum_jj conj(Bh[jj][r]) W[jj][r], all threads: (column r, part) then a fixed-order sum
     {
-      // hparts x R double2 in U2 (free between the heavy phase and the updates; the plan reserves
-      // >= 16 nJm R bytes there and hparts <= nJ)
+      // hparts x R <= NT double2 in U2 (free between the heavy phase and the updates; the plan reserves
+      // >= 64 NT bytes there)
       const int hparts = max(1, min(NT / R, nJ));
       double2* hpart = (double2*)(smem + pl.o_u2);
       if (tid < hparts * R) {
