@@ -44,6 +44,9 @@ namespace cg = cooperative_groups;
 
 #define ROWS_NT 256
 #define ROWS_UF 32  // frames of precomputed Philox uniforms per refill
+// register tile of the small GEMMs (cgemm_tile): 4 rows x 2 columns of the output per thread beat 2 x 4
+// at every rows-kernel shape, same accumulator count (profiles/tools/ubench_gemm42.cu: C4 Z 27.6k -> 21.3k cycles)
+constexpr int GTM = 4, GTN = 2;
 
 struct RowsPlan {
   int CL, KT, nIm, nJm, Rp, red_cap, tight;
@@ -773,10 +776,10 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
           }
         }
         const int M = z ? S : nJ, Kd = z ? nJ : S;
-        const int ks = gemm_split(M, R, Kd, 2, 4, pl.red_cap);
+        const int ks = gemm_split(M, R, Kd, GTM, GTN, pl.red_cap);
         const RowsEpi epi{z ? EPI_Z_STORE : EPI_W_ACC, R, wacc, nullptr, g_zp + (size_t)c * Smax * R, nullptr, 0.f,
                           0.f};
-        cgemm_tile<2, 4, false, true>(M, R, Kd, ys, z ? pl.nJm : 1, z ? 1 : pl.nJm, z ? bhl : ahs, R, 1, ks, red2,
+        cgemm_tile<GTM, GTN, false, true>(M, R, Kd, ys, z ? pl.nJm : 1, z ? 1 : pl.nJm, z ? bhl : ahs, R, 1, ks, red2,
                                       epi);
         __syncthreads();
       }
@@ -835,10 +838,10 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       for (int gsel = 0; gsel < 2; ++gsel) {
         const bool w = gsel == 0;
         const int M = w ? nJ : kt, Kd = w ? kt : nJ;
-        const int ks = gemm_split(M, R, Kd, 2, 4, pl.red_cap);
+        const int ks = gemm_split(M, R, Kd, GTM, GTN, pl.red_cap);
         const RowsEpi epi{w ? EPI_W_ACC : EPI_Z_STORE, R, wacc, nullptr, g_zp + ((size_t)c * Smax + k0) * R,
                           nullptr, 0.f, 0.f};
-        cgemm_tile<2, 4, false, true>(M, R, Kd, ys, w ? 1 : pl.nJm, w ? pl.nJm : 1, w ? ahs : bhl, R, 1, ks, red2,
+        cgemm_tile<GTM, GTN, false, true>(M, R, Kd, ys, w ? 1 : pl.nJm, w ? pl.nJm : 1, w ? ahs : bhl, R, 1, ks, red2,
                                       epi);
         if (w) __syncthreads();  // the K-split buffer is reused
       }
@@ -1042,7 +1045,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
           __syncthreads();
           const int M = q ? nJ : (nown > 0 ? nI : 0);
           const RowsEpi epi{q ? EPI_Q_UPDATE : EPI_P_MAPPED, R, q ? wacc : zs, bhl, nullptr, gamf, cfac, muf, flags};
-          cgemm_tile<2, 4, false, true>(M, R, R, q ? bhl : ahl, R, 1, mq, R, 1, 1, red2, epi);
+          cgemm_tile<GTM, GTN, false, true>(M, R, R, q ? bhl : ahl, R, 1, mq, R, 1, 1, red2, epi);
           __syncthreads();
         }
       } else {
@@ -1060,9 +1063,9 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         for (int gsel = 0; gsel < 2; ++gsel) {
           const bool q = gsel == 0;
           const int M = q ? nJ : nown;
-          const int ks = gemm_split(M, R, R, 2, 4, pl.red_cap);
+          const int ks = gemm_split(M, R, R, GTM, GTN, pl.red_cap);
           const RowsEpi epi{q ? EPI_Q_UPDATE : EPI_P_UPDATE, R, q ? wacc : zs, bhl, nullptr, gamf, cfac, muf};
-          cgemm_tile<2, 4, false, true>(M, R, R, q ? vop : vop2, R, 1, q ? gaf : gbf, R, 1, ks, red2, epi);
+          cgemm_tile<GTM, GTN, false, true>(M, R, R, q ? vop : vop2, R, 1, q ? gaf : gbf, R, 1, ks, red2, epi);
           __syncthreads();
         }
       }
