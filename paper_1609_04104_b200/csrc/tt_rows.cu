@@ -903,24 +903,42 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     cluster_barrier();  // ---------------------------------------------- B4
     STAMP(10);
 
-    // ======== (d) redundant fp64 solve; cluster sums of Z for owned rows prefetched alongside
+    // ======== (d) redundant fp64 solve; cluster sums of Z for owned rows prefetched alongside.
+    // The L2 loads of this phase are issued together: the thread's first packed Gram entry before the
+    // Z sums, the h and ||Y||^2 partial sums on the top threads (which own no Z row / Gram entry).
+    double2 gae0 = make_double2(0.0, 0.0), gbe0 = gae0;
+    if (tid < Rp) {
+      gae0 = phase == 2 ? make_double2(a.xg[2 * tid], a.xg[2 * tid + 1]) : __ldcg(&g_ga[tid]);
+      gbe0 = __ldcg(&g_gb[tid]);
+    }
     for (int o = tid; o < nown * R; o += NT) {
       const int m = idiv(o, R), r = o - m * R;
       zs[o] = sum_parts_f2(g_zp + (size_t)own_k[m] * R + r, (size_t)Smax * R, CL);
     }
+    {
+      const int hr = tid - (NT - R);
+      if (hr >= 0) {
+        const double2 h = sum_parts2(g_hp + hr, (size_t)R, CL);
+        hv[hr] = h;
+        hsave[hr] = h;
+      }
+      if (tid == NT - R - 1) {
+        if (phase == 2) {
+          scal[0] = a.xg[2 * Rp];      // ||Y||^2 over all ranks
+          scal[1] = a.xg[2 * Rp + 1];  // ||Ah||^2 over all ranks
+        } else {
+          scal[0] = sum_parts(g_yn, 1, CL);
+        }
+      }
+    }
     for (int e = tid; e < Rp; e += NT) {
       const int ij = tab[e];
       const int r = ij >> 8, q = ij & 255;
-      double2 gae, gbe;
-      if (phase == 2) {
-        gae.x = a.xg[2 * e];
-        gae.y = a.xg[2 * e + 1];
-      } else {
-        gae.x = __ldcg(&g_ga[e].x);
-        gae.y = __ldcg(&g_ga[e].y);
+      double2 gae = gae0, gbe = gbe0;
+      if (e != tid) {
+        gae = phase == 2 ? make_double2(a.xg[2 * e], a.xg[2 * e + 1]) : __ldcg(&g_ga[e]);
+        gbe = __ldcg(&g_gb[e]);
       }
-      gbe.x = __ldcg(&g_gb[e].x);
-      gbe.y = __ldcg(&g_gb[e].y);
       double2 gg = zmul(gae, gbe);
       if (r == q) {
         gg.x += a.lam;
@@ -933,19 +951,6 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         gaf[q * R + r] = to_f2(zconj(gae));
         gbf[r * R + q] = to_f2(gbe);
         gbf[q * R + r] = to_f2(zconj(gbe));
-      }
-    }
-    if (tid < R) {
-      const double2 h = sum_parts2(g_hp + tid, (size_t)R, CL);
-      hv[tid] = h;
-      hsave[tid] = h;
-    }
-    if (tid == 32) {
-      if (phase == 2) {
-        scal[0] = a.xg[2 * Rp];      // ||Y||^2 over all ranks
-        scal[1] = a.xg[2 * Rp + 1];  // ||Ah||^2 over all ranks
-      } else {
-        scal[0] = sum_parts(g_yn, 1, CL);
       }
     }
     __syncthreads();
