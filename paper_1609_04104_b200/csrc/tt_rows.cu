@@ -505,12 +505,12 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       __stcg(&g_gb[e].x, g.x);
       __stcg(&g_gb[e].y, g.y);
     }
-    for (int r = tid; r < R && tid < 32; r += 32) {
+    for (int m = tid; m < ndraw; m += NT) usm[m] = __ldcg(&g_unif[(f % ROWS_UF) * ndraw + m]);  // in flight with
+    for (int r = tid; r < R && tid < 32; r += 32) {                                                // the norm sums
       const double n2 = sum_parts(g_cn + r, (size_t)R, CL);
       nrm[r] = n2;
       inrm[r] = n2 > 0.0 ? fast_rcp(n2) : 0.0;
     }
-    for (int m = tid; m < ndraw; m += NT) usm[m] = __ldcg(&g_unif[(f % ROWS_UF) * ndraw + m]);
     if (tid == 0) sh_err = 0;
     __syncthreads();
     if (warp == 0) {  // ||Ah||^2, fixed order
@@ -524,13 +524,20 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     if (a.policy == TT_POLICY_INFORMATIVE) {
       // raw row scores for own rows (sampler.py:77-85, :126)
       const double cs = (double)ny, cr = (double)R, cd = 1.0 / ((double)R * (double)(nx + ny));
-      for (int i = tid; i < nI; i += NT) {
+      // tpr lanes per row (rank terms split, fixed-order butterfly), so the fp64 chain is R / tpr long
+      int tpr = 32;
+      while (tpr > 1 && tpr * nI > NT) tpr >>= 1;
+      const int sub = lane & (tpr - 1);
+      for (int base = 0; base < nI; base += NT / tpr) {  // uniform trip count (full-warp shuffles)
+        const int i = base + tid / tpr;
         double e = 0.0;
-        for (int r = 0; r < R; ++r) {
-          const float2 v = ahl[i * R + r];
-          e = fma((double)v.x * v.x + (double)v.y * v.y, inrm[r], e);
-        }
-        __stcg(&g_sraw[i0 + i], (cs * e + cr) * cd);
+        if (i < nI)
+          for (int r = sub; r < R; r += tpr) {
+            const float2 v = ahl[i * R + r];
+            e = fma((double)v.x * v.x + (double)v.y * v.y, inrm[r], e);
+          }
+        for (int o = 1; o < tpr; o <<= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+        if (sub == 0 && i < nI) __stcg(&g_sraw[i0 + i], (cs * e + cr) * cd);
       }
       if (tid < R && nrm[tid] == 0.0) atomicOr(&sh_err, TT_ST_ZEROCOL);
       STAMP(3);
