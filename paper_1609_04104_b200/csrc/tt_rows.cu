@@ -511,14 +511,10 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       nrm[r] = n2;
       inrm[r] = n2 > 0.0 ? fast_rcp(n2) : 0.0;
     }
+    STAMP(24);
     if (tid == 0) sh_err = 0;
     __syncthreads();
-    if (warp == 0) {  // ||Ah||^2, fixed order
-      double v = 0.0;
-      for (int r = lane; r < R; r += 32) v += nrm[r];
-      v = warp_sum(v);
-      if (lane == 0) scal[1] = v;
-    }
+    STAMP(27);
 
     }  // phase != 2
     if (a.policy == TT_POLICY_INFORMATIVE) {
@@ -866,6 +862,12 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         xg1[2 * e] = G[e - eb].x;
         xg1[2 * e + 1] = G[e - eb].y;
       }
+      if (warp == 0) {  // this rank's ||Ah||^2, fixed order
+        double v = 0.0;
+        for (int r = lane; r < R; r += 32) v += nrm[r];
+        v = warp_sum(v);
+        if (lane == 0) scal[1] = v;
+      }
       const double yt = block_sum(ysq, red);
       if (tid == 0) __stcg(&g_yn[c], yt);
       cluster_barrier();
@@ -961,11 +963,20 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       }
     }
     __syncthreads();
-    if (warp == 0) {  // ||Bh||^2 = trace(GB)
-      double v = 0.0;
-      for (int r = lane; r < R; r += 32) v += gdb[r];
-      v = warp_sum(v);
-      if (lane == 0) scal[2] = v;
+    if (warp == 0) {  // ||Bh||^2 = trace(GB); ||Ah||^2 from the column norms (phase 2: from the payload)
+      double v = 0.0, w = 0.0;
+      for (int r = lane; r < R; r += 32) {
+        v += gdb[r];
+        w += nrm[r];
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        v += __shfl_xor_sync(0xffffffffu, v, o);
+        w += __shfl_xor_sync(0xffffffffu, w, o);
+      }
+      if (lane == 0) {
+        scal[2] = v;
+        if (phase == 0) scal[1] = w;
+      }
     }
     STAMP(11);
 
