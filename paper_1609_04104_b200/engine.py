@@ -117,12 +117,31 @@ class OnlineEngine:
     # ------------------------------------------------------------------ state
     def set_image_factors(self, A, B):
         """Image-domain factors (nslices, N, R) -> resident k-space factors."""
-        a = torch.as_tensor(np.asarray(A) if not isinstance(A, torch.Tensor) else A)
-        b = torch.as_tensor(np.asarray(B) if not isinstance(B, torch.Tensor) else B)
-        a = a.to(self.dev, torch.complex64).reshape(self.nslices, self.nx, self.rank).contiguous()
-        b = b.to(self.dev, torch.complex64).reshape(self.nslices, self.ny, self.rank).contiguous()
-        self.ah = K.fft_cols_(a)
-        self.bh = K.fft_cols_(b)
+        na, nb = self.nslices * self.nx * self.rank, self.nslices * self.ny * self.rank
+        if isinstance(A, torch.Tensor) or isinstance(B, torch.Tensor):
+            a = torch.as_tensor(A).to(self.dev, torch.complex64).reshape(self.nslices, self.nx, self.rank)
+            b = torch.as_tensor(B).to(self.dev, torch.complex64).reshape(self.nslices, self.ny, self.rank)
+            self.ah = K.fft_cols_(a.contiguous())
+            self.bh = K.fft_cols_(b.contiguous())
+            return
+        # host arrays: one complex64 staging buffer, one upload, two in-place column FFTs
+        a, b = np.asarray(A), np.asarray(B)
+        if a.size != na or b.size != nb:
+            raise ValueError("factor shapes do not match (nslices, nx, R) / (nslices, ny, R)")
+        host = np.empty(na + nb, np.complex64)
+        host[:na] = a.reshape(-1)
+        host[na:] = b.reshape(-1)
+        d = torch.from_numpy(host).to(self.dev)
+        self.ah = K.fft_cols_(d[:na].view(self.nslices, self.nx, self.rank))
+        self.bh = K.fft_cols_(d[na:].view(self.nslices, self.ny, self.rank))
+
+    def reset(self, t0: int = 1) -> None:
+        """Back to frame 0 at time ``t0``: step accumulator, Philox position and status cleared."""
+        self.t = int(t0)
+        self.frame = 0
+        self.alpha_bar.zero_()
+        self.philox_pos.zero_()
+        self.status.zero_()
 
     def image_factors(self):
         return K.fft_cols(self.ah, inverse=True), K.fft_cols(self.bh, inverse=True)
@@ -506,6 +525,40 @@ def _host_source(kspace):
 
 
 EDGE_BLOCK = 8  # frames in the first and last pipeline blocks
+_STREAMS: dict = {}  # device index -> (upload, reconstruction, download) streams of run_online
+_ENGINES: dict = {}  # run_online's informative-policy engines, reused across calls of the same configuration
+
+
+def _take_engine(nx, ny, R, ns, lam, step, policy, cluster, t0):
+    """An OnlineEngine for run_online: a cached one (reset) when the configuration repeats, else new.
+    The engine is taken out of the cache for the duration of the call (concurrent calls never share)."""
+    key = None
+    if isinstance(policy, Informative):
+        try:
+            key = (torch.cuda.current_device(), nx, ny, R, ns, float(lam), repr(step), policy, int(cluster))
+            hash(key)
+        except TypeError:
+            key = None
+    eng = _ENGINES.pop(key, None) if key is not None else None
+    if eng is None:
+        eng = OnlineEngine(nx, ny, R, ns, lam, step, policy, cluster, t0)
+    else:
+        eng.reset(t0)
+    return eng, key
+
+
+def _give_engine(key, eng):
+    if key is not None:
+        while len(_ENGINES) >= 4:
+            _ENGINES.pop(next(iter(_ENGINES)))
+        _ENGINES[key] = eng
+
+
+def _pipeline_streams(dev):
+    key = dev.index if dev.index is not None else torch.cuda.current_device()
+    if key not in _STREAMS:
+        _STREAMS[key] = tuple(torch.cuda.Stream(dev) for _ in range(3))
+    return _STREAMS[key]
 
 
 def _blocks(f0, f1, C):
@@ -552,11 +605,13 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
     R = A0.shape[-1]
     if isinstance(policy, (InformativeEntries, StaticEntries)):
         return _run_online_entries(src, on_dev, A0, B0, lam, step, policy, clean, t0, warm_frames)
-    eng = OnlineEngine(nx, ny, R, ns, lam, step, policy, cluster, t0)
-    eng.set_image_factors(A0, np.asarray(B0).reshape(ns, ny, R))
-    dev = eng.dev
+    dev = L.device()
     comp = torch.cuda.current_stream(dev)
-    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    s_in, s_rec, s_out = _pipeline_streams(dev)
+    # the engine (cached for repeated informative configurations) and its initial factors first: their
+    # small upload must not queue behind the truth uploads on the copy engine
+    eng, ekey = _take_engine(nx, ny, R, ns, lam, step, policy, cluster, t0)
+    eng.set_image_factors(A0, np.asarray(B0).reshape(ns, ny, R))
     kd = src.contiguous() if on_dev else torch.empty(T, ns, nx, ny, dtype=torch.complex64, device=dev)
     W = int(warm_frames)
     C = max(1, int(chunk))
@@ -585,7 +640,6 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
     Xd = torch.empty(Ts, ns, nx, ny, dtype=torch.complex64, device=dev)
     # tracking blocks run back to back on the compute stream; each block's reconstruction runs on its
     # own stream once the block's tracking is done, and its download follows on the copy stream
-    s_rec = torch.cuda.Stream(dev)
     s_rec.wait_stream(comp)
     s_out.wait_stream(comp)
     hist = {k: out[k].clone() for k in ("ah",)} if keep_history else None
@@ -626,6 +680,7 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
     comp.synchronize()
     s_out.synchronize()
     L.raise_status(int(st.max().item()), "online engine")
+    _give_engine(ekey, eng)
     cnt = small["cnt"].numpy()
     rows_np = small["rows"].numpy()
     rows = [[rows_np[f, s, :cnt[f, s]].astype(np.int64) for s in range(ns)] for f in range(Ts)]
