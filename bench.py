@@ -6,9 +6,11 @@ cine phantom slice, T=200 frames, R=20, lambda=0.05, Fixed mu=0.01,
 informative row sampling at 4x (K=64 trials incl. 16 forced centre lines,
 beta=0.1, Philox draws). One bench *step* = the whole T-frame online
 sequence from the same initial state: per frame [row scores -> Philox draw
--> gather y -> Gram/ridge -> k-space factor update] in one persistent
-cluster-kernel launch, then the inverse column FFTs of the per-frame factors
-and the reconstruction of all T image frames (4 launches of our kernels).
+-> gather y -> Gram/ridge -> k-space factor update] in persistent
+cluster-kernel launches over blocks of frames (`--blocks`, default 4; the
+state stays resident across them), each block's inverse column FFTs of the
+per-frame factors and reconstruction overlapping the next block's tracking
+on a second stream (4 launches of our kernels per block).
 
 `value`  = frames reconstructed per second over all ranks (device time,
            inputs resident, L2 flushed between steps).
@@ -810,26 +812,40 @@ def run_ours(args, cfg):
     eng = tt.OnlineEngine(n, n, R, ns, cfg["lam"], tt.Fixed(cfg["mu"]), pol, cluster=args.cluster)
     eng.set_image_factors(A0, B0)
     ah0, bh0 = eng.ah.clone(), eng.bh.clone()
-    ahf, bhf = torch.empty_like(ah0), torch.empty_like(bh0)
     ks = torch.from_numpy(ks_np).to(dev)
     out = eng.make_outputs(T, history=True)
-    X = torch.empty(T * ns, n, n, dtype=torch.complex64, device=dev)
-    rows_args = eng.args(ks, T, out, ah_in=ah0, bh_in=bh0, ah_out=ahf, bh_out=bhf, frame0=0, t0=1)
+    X = torch.empty(T, ns, n, n, dtype=torch.complex64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    lib = L.lib()
     stream = torch.cuda.current_stream()
+    s_rec = torch.cuda.Stream(dev)
+    # one step = the T-frame sequence in `nblk` tracking launches on the compute stream (the resident
+    # state carries across launches; results are launch-boundary invariant); each block's inverse column
+    # FFTs + reconstruction run on a second stream as soon as its tracking is done, on the SMs the
+    # tracking clusters leave free (run_online's pipeline without the host transfers)
+    nblk = max(1, min(args.blocks, T))
+    bounds = [(T * i // nblk, T * (i + 1) // nblk) for i in range(nblk)]
+    parts = [{k: v[a:b] for k, v in out.items()} for a, b in bounds]
+    tracked = [torch.cuda.Event() for _ in bounds]
 
     def reset():
+        eng.ah.copy_(ah0)
+        eng.bh.copy_(bh0)
         eng.philox_pos.zero_()
         eng.alpha_bar.zero_()
+        eng.frame, eng.t = 0, 1
 
-    def step_kernels():
-        K.track_rows(rows_args)                                   # 1: fused online loop, T frames
-        K.fft_cols_(out["ah"], inverse=True)                      # 2: A_t = F^-1 Ah_t (all frames)
-        K.fft_cols_(out["bh"], inverse=True)                      # 3: B_t = F^-1 Bh_t
-        L.check(lib.tt_reconstruct(stream.cuda_stream, T * ns, n, n, R, out["ah"].data_ptr(),
-                                   out["bh"].data_ptr(), out["gamma"].data_ptr(), X.data_ptr()), "reconstruct")  # 4
-    launches_per_step = 4
+    def step_kernels(e_track=None):
+        s_rec.wait_stream(stream)
+        for (a, b), part, ev in zip(bounds, parts, tracked):
+            eng.run(ks, b - a, out=part)                          # fused online loop over frames [a, b)
+            ev.record(stream)
+            s_rec.wait_event(ev)
+            with torch.cuda.stream(s_rec):
+                eng.reconstruct(part, into=X[a:b], in_place=True)  # 2 inverse column FFTs + reconstruction
+        if e_track is not None:
+            e_track.record(stream)
+        stream.wait_stream(s_rec)
+    launches_per_step = 4 * nblk
 
     for _ in range(args.warmup):
         reset()
@@ -848,12 +864,7 @@ def run_ours(args, cfg):
             reset()
             e0, e1, e2 = ev[i]
             e0.record(stream)
-            K.track_rows(rows_args)
-            e1.record(stream)
-            K.fft_cols_(out["ah"], inverse=True)
-            K.fft_cols_(out["bh"], inverse=True)
-            L.check(lib.tt_reconstruct(stream.cuda_stream, T * ns, n, n, R, out["ah"].data_ptr(),
-                                       out["bh"].data_ptr(), out["gamma"].data_ptr(), X.data_ptr()), "reconstruct")
+            step_kernels(e1)
             e2.record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -934,6 +945,7 @@ def run_ours(args, cfg):
         "vs_baseline": None, "dtype": "c64", "data": "synthetic",
         "config": {"workload": cfg["desc"], "frames_per_step": T, "slices_per_gpu": ns, "rank": R,
                    "nx": n, "ny": n, "cluster_ctas_per_slice": eng.cluster, "l2": "flushed between steps (256 MB write)",
+                   "tracking_launches_per_step": nblk,
                    "parallelism": f"{'replicas' if cfg['slices'] == 1 else 'slice-shard'} x{world}"},
         "gpu_launches": launches_per_step * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
@@ -966,6 +978,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--row-shard", action="store_true", help="config c4: use the row-sharded two-phase path")
+    ap.add_argument("--blocks", type=int, default=4, help="tracking launches per step (reconstruction overlaps)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
