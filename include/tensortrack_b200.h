@@ -250,6 +250,12 @@ int tt_cten_write(const char* path, const void* data, int src_is_f64, int dtype_
  * b [frames][ny][rank], gamma [frames][rank] -> x [frames][nx][ny]. */
 int tt_reconstruct(void* stream, int frames, int nx, int ny, int rank, const float* a, const float* b,
                    const float* gamma, float* x_out);
+/* NMSE per frame (metrics.nmse, metrics.py:53-62): out[f] = ||truth_f - est_f||^2 / ||truth_f||^2 over
+ * `frames` complex64 frames of n elements (NaN for an all-zero truth frame; the Python mirror raises
+ * ValueError there as the reference does). `work` holds tt_nmse_work_doubles(frames) doubles. Fixed
+ * summation order: repeat calls are bit-identical. */
+int tt_nmse(void* stream, int frames, size_t n, const float* truth, const float* est, double* work, double* out);
+size_t tt_nmse_work_doubles(int frames);
 /* rebalance (core.py:138-166) in place on [nslices][n][rank] factor pairs. */
 int tt_rebalance(void* stream, int nslices, int nx, int ny, int rank, float* a, float* b, int32_t* status);
 

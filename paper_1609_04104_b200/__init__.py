@@ -53,6 +53,8 @@ from .tracker import (
     track_step,
 )
 from ._lib import NumericalError
+from .config import ConfigError
+from .metrics import nmse, nmse_frames
 from .acquisition import StreamingProvider, measure, project
 from .patches import PatchedResult, draw_frame_entries, full_entries, init_patch_factors, run_tracking_patched
 from .cten import CtenFormatError, read_cten, read_cten_tensor, write_cten
@@ -73,7 +75,7 @@ __all__ = [
     "PatchedResult", "run_tracking_patched", "init_patch_factors", "draw_frame_entries", "full_entries",
     "OnlineEngine", "OnlineResult", "StaticRows", "Informative", "run_online", "warm_up", "RowShardedEngine",
     "EntryEngine", "InformativeEntries", "StaticEntries", "run_batch", "BatchResult", "LocalShardedEngine",
-    "NumericalError", "StreamingProvider", "measure", "project",
+    "NumericalError", "ConfigError", "nmse", "nmse_frames", "StreamingProvider", "measure", "project",
     "CtenFormatError", "read_cten", "read_cten_tensor", "write_cten",
     "MetricRow", "write_metrics_csv", "write_mask_csv", "write_trace_csv", "write_budget_csv",
     "online_mask_rows", "online_budget_rows",

@@ -102,3 +102,58 @@ extern "C" int tt_reconstruct(void* stream, int frames, int nx, int ny, int rank
   TT_CUDA_TRY(cudaGetLastError());
   return TT_OK;
 }
+
+// NMSE per frame (metrics.nmse, metrics.py:53-62): ||X_f - Xhat_f||^2 / ||X_f||^2 over complex64 frames,
+// fp64 sums. Deterministic: fixed per-block partials ([frames][NB]), then one warp per frame sums them in
+// a fixed order. Off the timed path (the bench's and run_online's quality check).
+#define NM_NT 256
+#define NM_NB 32
+__global__ void __launch_bounds__(NM_NT) nmse_part_kernel(size_t n, const float2* __restrict__ truth,
+                                                          const float2* __restrict__ est, double2* __restrict__ part) {
+  const int f = blockIdx.y;
+  const float2* t = truth + (size_t)f * n;
+  const float2* e = est + (size_t)f * n;
+  double num = 0.0, den = 0.0;
+  for (size_t i = (size_t)blockIdx.x * NM_NT + threadIdx.x; i < n; i += (size_t)NM_NB * NM_NT) {
+    const float2 a = t[i], b = e[i];
+    const double dx = (double)a.x - b.x, dy = (double)a.y - b.y;
+    num += dx * dx + dy * dy;
+    den += (double)a.x * a.x + (double)a.y * a.y;
+  }
+  __shared__ double sn[NM_NT / 32], sd[NM_NT / 32];
+  num = warp_sum(num);
+  den = warp_sum(den);
+  if ((threadIdx.x & 31) == 0) {
+    sn[threadIdx.x >> 5] = num;
+    sd[threadIdx.x >> 5] = den;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < NM_NT / 32; ++w) {
+      a += sn[w];
+      b += sd[w];
+    }
+    part[(size_t)f * NM_NB + blockIdx.x] = make_double2(a, b);
+  }
+}
+__global__ void nmse_final_kernel(int frames, const double2* __restrict__ part, double* __restrict__ out) {
+  const int f = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (f >= frames) return;
+  const double2 v = part[(size_t)f * NM_NB + lane];  // NM_NB == 32: one partial per lane
+  const double num = warp_sum(v.x), den = warp_sum(v.y);
+  if (lane == 0) out[f] = den > 0.0 ? num / den : __longlong_as_double(0x7ff8000000000000ll);
+}
+
+extern "C" int tt_nmse(void* stream, int frames, size_t n, const float* truth, const float* est, double* work,
+                       double* out) {
+  if (frames < 0 || !truth || !est || !work || !out) return tt_fail(TT_EINVAL, "tt_nmse: bad arguments");
+  if (frames == 0) return TT_OK;
+  if (frames > 65535) return tt_fail(TT_EINVAL, "tt_nmse: frames > 65535 per call");
+  cudaStream_t st = (cudaStream_t)stream;
+  nmse_part_kernel<<<dim3(NM_NB, frames), NM_NT, 0, st>>>(n, (const float2*)truth, (const float2*)est, (double2*)work);
+  nmse_final_kernel<<<(frames + 7) / 8, 256, 0, st>>>(frames, (const double2*)work, out);
+  TT_CUDA_TRY(cudaGetLastError());
+  return TT_OK;
+}
+extern "C" size_t tt_nmse_work_doubles(int frames) { return (size_t)(frames > 0 ? frames : 0) * NM_NB * 2; }

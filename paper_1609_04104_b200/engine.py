@@ -29,6 +29,7 @@ import ctypes as C
 import numpy as np
 import torch
 
+from .metrics import nmse_frames
 from . import _lib as L
 from . import _ops as K
 from .tracker import Fixed, HessianBound
@@ -673,10 +674,8 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
     st.copy_(eng.status, non_blocking=True)
     nm = None
     if clean is not None:
-        cl = torch.as_tensor(np.asarray(clean, dtype=np.complex64)).to(dev).reshape(Ts, ns, nx, ny)
-        num = (cl - Xd).abs().pow(2).sum(dim=(-1, -2)).double()
-        den = cl.abs().pow(2).sum(dim=(-1, -2)).double()
-        nm = (num / den).cpu().numpy()
+        cl = torch.as_tensor(np.asarray(clean, dtype=np.complex64)).to(dev).reshape(Ts * ns, nx * ny)
+        nm = nmse_frames(cl, Xd.reshape(Ts * ns, nx * ny)).reshape(Ts, ns).cpu().numpy()  # metrics.py:53-62
     comp.synchronize()
     s_out.synchronize()
     L.raise_status(int(st.max().item()), "online engine")
@@ -899,10 +898,8 @@ def _run_online_entries(src, on_dev, A0, B0, lam, step, policy, clean, t0, warm_
             _ENTRY_PLANS[key] = (eng, kd, (torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()))
     nm = None
     if clean is not None:
-        cl = torch.as_tensor(np.asarray(clean, dtype=np.complex64)).to(eng.dev).reshape(T, 1, nx, ny)
-        num = (cl - X).abs().pow(2).sum(dim=(-1, -2)).double()
-        den = cl.abs().pow(2).sum(dim=(-1, -2)).double()
-        nm = (num / den).cpu().numpy()
+        cl = torch.as_tensor(np.asarray(clean, dtype=np.complex64)).to(eng.dev).reshape(T, nx * ny)
+        nm = nmse_frames(cl, X.reshape(T, nx * ny)).reshape(T, 1).cpu().numpy()  # metrics.py:53-62
     # the small results: asynchronous copies into pinned memory, one synchronisation
     Ad, Bd = eng.image_factors()
     small = (("gamma", out["gamma"]), ("cost", out["cost"]), ("mu", out["mu"]), ("cnt", out["cnt"]),

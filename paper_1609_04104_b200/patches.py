@@ -27,6 +27,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from .metrics import nmse_frames
 from . import _lib as L
 from . import _ops as K
 from .mri import PatchGrid
@@ -274,7 +275,7 @@ def run_tracking_patched(frames, grid: PatchGrid, lam, step, masks, warm_n=0, wa
     else:
         ct = clean if isinstance(clean, torch.Tensor) else torch.from_numpy(np.asarray(clean))
         ref = (ct.permute(2, 0, 1) if frames_last else ct).to(dev, torch.complex64)
-    err = (recon - ref).abs().pow(2).sum(dim=(1, 2)).double() / ref.abs().pow(2).sum(dim=(1, 2)).double()
+    err = nmse_frames(ref, recon)  # metrics.py:53-62, per frame
     # the small results: asynchronous downloads into pinned memory, one synchronisation
     pinned = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True)  # noqa: E731
     dl = {"gamma": gam, "err": err, "pcnt": run.pcnt, "A": run.a, "B": run.b, "t": run.t[:1],

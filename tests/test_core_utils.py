@@ -38,3 +38,13 @@ def test_outer_rank_one_and_norm_helpers():  # TensorSubspace holds device buffe
     # balanced factors: (1/M) sum ||A_m||_F^2 = sum_r sigma_r^(2/M) at M = 2
     Ab, Bb = tt.rebalance(sub).factors
     assert tt.rank_surrogate([Ab, Bb]) == pytest.approx(np.sum(tt.singular_values(sub)), rel=1e-5)
+
+
+def test_config_error_and_metric_exports():
+    """ConfigError (config.py:19) is a ValueError; nmse / ConfigError exported like the reference's
+    package namespace (__init__.py:3-62)."""
+    import paper_1609_04104_b200 as tt
+
+    assert issubclass(tt.ConfigError, ValueError)
+    for name in ("ConfigError", "nmse", "nmse_frames"):
+        assert name in tt.__all__ and hasattr(tt, name)

@@ -67,3 +67,40 @@ def test_batched_reconstruct_matches_outer_product(shape):
     X = K.reconstruct(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), torch.from_numpy(gm).cuda()).cpu().numpy()
     for f in range(F):
         assert rel(X[f], O.synth(A[f], B[f], gm[f])) < 1e-5
+
+
+@pytest.mark.parametrize("n,ncols", [(256, 1), (256, 20), (256, 33), (1024, 64), (2048, 5), (8, 70)])
+def test_fft_cols_column_blocking(n, ncols):
+    """Column counts that split over several CTAs (up to 32 whole columns per CTA, fewer at large n)
+    with a partial last block, odd log2 n (one radix-2 pass) and even log2 n."""
+    import torch
+
+    from paper_1609_04104_b200 import _ops as K
+
+    rng = np.random.default_rng(n + ncols)
+    x = (rng.standard_normal((2, n, ncols)) + 1j * rng.standard_normal((2, n, ncols))).astype(np.complex64)
+    for inverse in (False, True):
+        got = K.fft_cols(torch.from_numpy(x).cuda(), inverse).cpu().numpy()
+        want = np.stack([O.fft_cols(x[b], inverse) for b in range(2)])
+        assert rel(got, want) < 2e-6
+
+
+def test_nmse_matches_reference_semantics():
+    """metrics.nmse (metrics.py:53-62): value against the oracle, per-frame batch form, ValueError for
+    a shape mismatch and for an all-zero reference."""
+    import paper_1609_04104_b200 as tt
+
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((3, 40, 24)) + 1j * rng.standard_normal((3, 40, 24))
+    y = x + 0.1 * (rng.standard_normal(x.shape) + 1j * rng.standard_normal(x.shape))
+    assert abs(tt.nmse(x, y) - O.nmse(x, y)) <= 1e-5 * O.nmse(x, y)
+    per = tt.nmse_frames(x, y).cpu().numpy()
+    want = np.array([O.nmse(x[f], y[f]) for f in range(3)])
+    assert np.max(np.abs(per - want) / want) < 1e-5
+    assert tt.nmse(x.real, y.real) == pytest.approx(O.nmse(x.real, y.real), rel=1e-5)
+    a, b = tt.nmse_frames(x, y), tt.nmse_frames(x, y)
+    assert bool((a == b).all())  # fixed summation order
+    with pytest.raises(ValueError):
+        tt.nmse(x, y[:, :, :5])
+    with pytest.raises(ValueError):
+        tt.nmse(np.zeros((4, 4)), np.ones((4, 4)))
