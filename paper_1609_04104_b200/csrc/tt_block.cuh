@@ -772,6 +772,85 @@ TT_DEV void cgemm_tile(int M, int N, int K, const float2* A, int a_m, int a_k, c
   }
 }
 
+// Two independent GEMMs of the same shape class in one pass (cgemm_tile's items of both problems
+// spread over the block, one barrier, one fixed-order reduction pass for both): problem p is
+// C_p(m, n) = sum_k A_p[m*a_m + k] * conj(B_p[k*b_k + n]) (CB) with common N, K, strides and split KS;
+// red holds KS * (M0 + M1) * N partials.
+template <int TM, int TN, bool CA, bool CB, typename Out>
+TT_DEV void cgemm_tile_pair(int M0, int M1, int N, int K, const float2* A0, const float2* A1, int a_m, int a_k,
+                            const float2* B0, const float2* B1, int b_k, int b_n, int KS, float2* red,
+                            const Out& out0, const Out& out1) {
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int tn = (N + TN - 1) / TN;
+  const int tiles0 = ((M0 + TM - 1) / TM) * tn, tiles1 = ((M1 + TM - 1) / TM) * tn;
+  const int items0 = tiles0 * KS, items = items0 + tiles1 * KS;
+  for (int it = tid; it < items; it += NT) {
+    const bool p1 = it >= items0;
+    const int jt = p1 ? it - items0 : it, tiles = p1 ? tiles1 : tiles0, M = p1 ? M1 : M0;
+    const float2* A = p1 ? A1 : A0;
+    const float2* B = p1 ? B1 : B0;
+    float2* rp = p1 ? red + (size_t)KS * M0 * N : red;
+    const int ks = idiv(jt, tiles), tile = jt - ks * tiles;
+    const int mt = idiv(tile, tn);
+    const int m0 = mt * TM, n0 = (tile - mt * tn) * TN;
+    const int k0 = idiv(K * ks, KS), k1 = idiv(K * (ks + 1), KS);
+    float2 acc[TM][TN];
+#pragma unroll
+    for (int u = 0; u < TM; ++u)
+#pragma unroll
+      for (int v = 0; v < TN; ++v) acc[u][v] = make_float2(0.f, 0.f);
+    const float2* Ap[TM];
+    const float2* Bp[TN];
+#pragma unroll
+    for (int u = 0; u < TM; ++u) Ap[u] = A + (size_t)min(m0 + u, M - 1) * a_m;
+#pragma unroll
+    for (int v = 0; v < TN; ++v) Bp[v] = B + (size_t)min(n0 + v, N - 1) * b_n;
+#pragma unroll 2
+    for (int k = k0; k < k1; ++k) {
+      float2 a[TM], b[TN];
+#pragma unroll
+      for (int u = 0; u < TM; ++u) {
+        a[u] = Ap[u][(size_t)k * a_k];
+        if (CA) a[u].y = -a[u].y;
+      }
+#pragma unroll
+      for (int v = 0; v < TN; ++v) {
+        b[v] = Bp[v][(size_t)k * b_k];
+        if (CB) b[v].y = -b[v].y;
+      }
+#pragma unroll
+      for (int u = 0; u < TM; ++u)
+#pragma unroll
+        for (int v = 0; v < TN; ++v) acc[u][v] = cfma(a[u], b[v], acc[u][v]);
+    }
+#pragma unroll
+    for (int u = 0; u < TM; ++u)
+#pragma unroll
+      for (int v = 0; v < TN; ++v) {
+        const int m = m0 + u, n = n0 + v;
+        if (m < M && n < N) {
+          if (KS == 1) (p1 ? out1 : out0)(m, n, acc[u][v]);
+          else rp[((size_t)ks * M + m) * N + n] = acc[u][v];
+        }
+      }
+  }
+  if (KS > 1) {
+    __syncthreads();
+    const int n0s = M0 * N;
+    for (int o = tid; o < (M0 + M1) * N; o += NT) {
+      const bool p1 = o >= n0s;
+      const int oo = p1 ? o - n0s : o, MN = p1 ? M1 * N : n0s;
+      const float2* rp = p1 ? red + (size_t)KS * n0s : red;
+      float2 s = rp[oo];
+#pragma unroll
+      for (int ks = 1; ks < 8; ++ks)
+        if (ks < KS) s = cadd(s, rp[(size_t)ks * MN + oo]);
+      const int om = idiv(oo, N);
+      (p1 ? out1 : out0)(om, oo - om * N, s);
+    }
+  }
+}
+
 // Register-tiled complex GEMM, K split across adjacent lanes: C(m, n) = sum_k opA(A[m*a_m + k*a_k]) *
 // opB(B[k*b_k + n*b_n]) over shared-memory operands. Work item = (TM x TN tile, k part); the KS parts of
 // a tile sit on adjacent lanes and are summed by a fixed-order shuffle butterfly (deterministic, no

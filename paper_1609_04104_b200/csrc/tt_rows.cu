@@ -1082,13 +1082,17 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         __syncthreads();
         STAMP(21);
         // Q: corr[jj][r] = sum_q vop[jj][q] conj(GA[q][r]) -> new Bh rows; P: same with GB on the owned
-        // sampled rows -> mu conj(g) P. One call site, so one copy of the GEMM code.
-        for (int gsel = 0; gsel < 2; ++gsel) {
-          const bool q = gsel == 0;
-          const int M = q ? nJ : nown;
-          const int ks = gemm_split(M, R, R, GTM, GTN, pl.red_cap);
-          const RowsEpi epi{q ? EPI_Q_UPDATE : EPI_P_UPDATE, R, q ? wacc : zs, bhl, nullptr, gamf, cfac, muf};
-          cgemm_tile<GTM, GTN, false, true>(M, R, R, q ? vop : vop2, R, 1, q ? gaf : gbf, R, 1, ks, red2, epi);
+        // sampled rows -> mu conj(g) P. Both in one pass (one barrier, one reduction pass).
+        {
+          const int tn = (R + GTN - 1) / GTN;
+          const int tiles = ((nJ + GTM - 1) / GTM + (nown + GTM - 1) / GTM) * tn;
+          int ks = idiv(NT, tiles > 0 ? tiles : 1);
+          ks = min(ks, min(R / 4, 8));
+          while (ks > 1 && ks * (nJ + nown) * R > pl.red_cap) --ks;
+          ks = max(ks, 1);
+          const RowsEpi eq{EPI_Q_UPDATE, R, wacc, bhl, nullptr, gamf, cfac, muf};
+          const RowsEpi ep{EPI_P_UPDATE, R, zs, bhl, nullptr, gamf, cfac, muf};
+          cgemm_tile_pair<GTM, GTN, false, true>(nJ, nown, R, R, vop, vop2, R, 1, gaf, gbf, R, 1, ks, red2, eq, ep);
           __syncthreads();
         }
       }
