@@ -120,6 +120,13 @@ typedef struct tt_rows_args {
    * on this GPU (shard_rank ignored). ah_in/ah_out/ah_hist hold all nx rows; xw/xg hold one
    * payload slot per rank; tt_rows_shard_reduce sums the slots into slot 0, which phase 2 reads. */
   int32_t shard_local;
+  /* Fused local multi-rank launch (appended; 0 = off; needs shard_local, static rows): one
+   * cooperative cluster launch runs all `frames` frames, both phases per frame, with two
+   * inter-cluster barriers per frame on `grid_sync` (one zeroed uint32 per launch) around an
+   * in-kernel payload reduction in tt_rows_shard_reduce's order. xw/xg then hold two sets of
+   * shard_world slots (frame parity). */
+  int32_t shard_fused;
+  uint32_t* grid_sync;
 } tt_rows_args;
 /* doubles in the fp64 payload xg of a sharded launch */
 size_t tt_rows_shard_xg_len(int rank);

@@ -47,7 +47,7 @@ class RowsArgs(C.Structure):
         ("gamma_out", _p), ("cost_out", _p), ("mu_out", _p), ("alpha_out", _p), ("rows_out", _p),
         ("cnt_out", _p), ("resid_out", _p), ("ah_hist", _p), ("bh_hist", _p), ("status", _p), ("scratch", _p),
         ("phase_clock", _p), ("shard_rank", _i32), ("shard_world", _i32), ("shard_phase", _i32), ("xw", _p),
-        ("xg", _p), ("shard_local", _i32),
+        ("xg", _p), ("shard_local", _i32), ("shard_fused", _i32), ("grid_sync", _p),
     ]
 
 

@@ -193,6 +193,25 @@ struct RowsEpi {
   }
 };
 
+// Inter-cluster barrier of a cooperative launch (every CTA co-resident): a monotonic arrival counter,
+// one zeroed uint32 per launch; the k-th barrier completes when it reaches k * gridDim.x.
+TT_DEV void grid_sync(unsigned* ctr, unsigned& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned target = (++gen) * gridDim.x;
+    atomicAdd(ctr, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    } while (v < target);
+    __threadfence();
+  } else {
+    ++gen;
+  }
+  __syncthreads();
+}
+
 // ---------------------------------------------------------------- cold paths (kept out of line)
 // Static row table validation: range and duplicates (observation.py:41-55).
 static __device__ __noinline__ int load_static_rows(const tt_rows_args& a, int f, int s, int* rows, int* flags,
@@ -330,7 +349,10 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
   const int s = multi ? 0 : qid;  // slice
   const int srank = multi ? qid : a.shard_rank;
   const bool lead = !multi || qid == 0;
-  const int phase = shard ? a.shard_phase : 0;  // 0 full step, 1 partials -> payload, 2 payload -> update
+  // fused: one cooperative launch runs both phases of every frame, the payload reduced in-kernel between
+  // two inter-cluster barriers; payload slots double-buffered by frame parity
+  const bool fused = multi && a.shard_fused != 0;
+  unsigned gsync_gen = 0;
   const int R0 = shard ? part_begin(nx, a.shard_world, srank) : 0;
   const int nxs = shard ? part_begin(nx, a.shard_world, srank + 1) - R0 : nx;
   const int i0 = R0 + part_begin(nxs, CL, c), nI = part_begin(nxs, CL, c + 1) - part_begin(nxs, CL, c);
@@ -388,7 +410,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
   // branch-free (a lane-0 branch would leave warp 0 diverged and send later shuffles down the slow path)
 #define STAMP(k)                                                                                   \
   do {                                                                                             \
-    if (pclk != nullptr) stamp_if(tid == 0, pclk + (size_t)f * 32 + (k));                          \
+    if (pclk != nullptr) stamp_if(tid == 0, pclk + (size_t)it * 32 + (k));                          \
   } while (0)
 
   // global scratch for this slice
@@ -434,7 +456,14 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
   const int cparts = NT / R;  // column-norm partial sums per column
   __syncthreads();
 
-  for (int f = 0; f < a.frames; ++f) {
+  for (int it = 0; it < (fused ? 2 * a.frames : a.frames); ++it) {
+    const int f = fused ? it >> 1 : it;
+    // 0 full step, 1 partials -> payload, 2 payload -> update
+    const int phase = !shard ? 0 : fused ? 1 + (it & 1) : a.shard_phase;
+    const size_t xgl = (size_t)Rp * 2 + 2;
+    float2* xwp = (float2*)a.xw + (fused ? (size_t)(f & 1) * a.shard_world * ny * R : 0);
+    double* xgp = a.xg + (fused ? (size_t)(f & 1) * a.shard_world * xgl : 0);
+    auto xg_at = [&](size_t k) { return __ldcg(xgp + k); };  // the reduced payload (slot 0)
     const long long t = a.t0 + f;
     const double lt = a.lam / (double)t;
     STAMP(0);
@@ -855,8 +884,8 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     STAMP(8);
     if (phase == 1) {
       // this rank's partials -> payload (the caller all-reduces xw and xg across ranks)
-      float2* xw1 = (float2*)a.xw + (multi ? (size_t)qid * ny * R : 0);  // this rank's payload slot
-      double* xg1 = a.xg + (multi ? (size_t)qid * (Rp * 2 + 2) : 0);
+      float2* xw1 = xwp + (multi ? (size_t)qid * ny * R : 0);  // this rank's payload slot
+      double* xg1 = xgp + (multi ? (size_t)qid * xgl : 0);
       for (int o = tid; o < nJ * R; o += NT) xw1[(size_t)j0 * R + o] = wacc[o];
       for (int e = eb + tid; e < ee; e += NT) {
         xg1[2 * e] = G[e - eb].x;
@@ -875,10 +904,42 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         xg1[2 * Rp] = sum_parts(g_yn, 1, CL);
         xg1[2 * Rp + 1] = scal[1];  // this rank's ||Ah||^2
       }
+      if (fused) {
+        // every rank's slot written -> fixed-order sum into slot 0 (tt_rows_shard_reduce's arithmetic),
+        // split over all CTAs of the launch (four elements per thread in flight) -> phase 2
+        grid_sync(a.grid_sync, gsync_gen);
+        const size_t nw = 2 * (size_t)ny * R, ntot = nw + xgl, step = (size_t)gridDim.x * NT;
+        float* xwf = (float*)xwp;
+        for (size_t i0r = (size_t)blockIdx.x * NT + tid; i0r < ntot; i0r += 4 * step) {
+          double v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const size_t i = i0r + u * step;
+            v[u] = 0.0;
+            if (i < nw) {
+              float x = __ldcg(xwf + i);
+              for (int r = 1; r < a.shard_world; ++r) x += __ldcg(xwf + (size_t)r * nw + i);
+              v[u] = x;
+            } else if (i < ntot) {
+              const size_t k = i - nw;
+              double x = __ldcg(xgp + k);
+              for (int r = 1; r < a.shard_world; ++r) x += __ldcg(xgp + (size_t)r * xgl + k);
+              v[u] = x;
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const size_t i = i0r + u * step;
+            if (i < nw) __stcg(xwf + i, (float)v[u]);
+            else if (i < ntot) __stcg(xgp + (i - nw), v[u]);
+          }
+        }
+        grid_sync(a.grid_sync, gsync_gen);
+      }
       continue;  // phase 2 finishes the frame after the all-reduce
     }
     if (phase == 2)  // reduced W of this CTA's columns
-      for (int o = tid; o < nJ * R; o += NT) wacc[o] = ((const float2*)a.xw)[(size_t)j0 * R + o];
+      for (int o = tid; o < nJ * R; o += NT) wacc[o] = __ldcg(xwp + (size_t)j0 * R + o);
     __syncthreads();
     // h partial: sum_jj conj(Bh[jj][r]) W[jj][r], all threads: (column r, part) then a fixed-order sum
     {
@@ -917,7 +978,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     // Z sums, the h and ||Y||^2 partial sums on the top threads (which own no Z row / Gram entry).
     double2 gae0 = make_double2(0.0, 0.0), gbe0 = gae0;
     if (tid < Rp) {
-      gae0 = phase == 2 ? make_double2(a.xg[2 * tid], a.xg[2 * tid + 1]) : __ldcg(&g_ga[tid]);
+      gae0 = phase == 2 ? make_double2(xg_at(2 * tid), xg_at(2 * tid + 1)) : __ldcg(&g_ga[tid]);
       gbe0 = __ldcg(&g_gb[tid]);
     }
     for (int o = tid; o < nown * R; o += NT) {
@@ -933,8 +994,8 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       }
       if (tid == NT - R - 1) {
         if (phase == 2) {
-          scal[0] = a.xg[2 * Rp];      // ||Y||^2 over all ranks
-          scal[1] = a.xg[2 * Rp + 1];  // ||Ah||^2 over all ranks
+          scal[0] = xg_at(2 * Rp);      // ||Y||^2 over all ranks
+          scal[1] = xg_at(2 * Rp + 1);  // ||Ah||^2 over all ranks
         } else {
           scal[0] = sum_parts(g_yn, 1, CL);
         }
@@ -945,7 +1006,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       const int r = ij >> 8, q = ij & 255;
       double2 gae = gae0, gbe = gbe0;
       if (e != tid) {
-        gae = phase == 2 ? make_double2(a.xg[2 * e], a.xg[2 * e + 1]) : __ldcg(&g_ga[e]);
+        gae = phase == 2 ? make_double2(xg_at(2 * e), xg_at(2 * e + 1)) : __ldcg(&g_ga[e]);
         gbe = __ldcg(&g_gb[e]);
       }
       double2 gg = zmul(gae, gbe);
@@ -1054,8 +1115,8 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
             const int r = ij >> 8, qq = ij & 255;
             double2 gv;
             if (q && phase == 2) {
-              gv.x = a.xg[2 * e];
-              gv.y = a.xg[2 * e + 1];
+              gv.x = xg_at(2 * e);
+              gv.y = xg_at(2 * e + 1);
             } else {
               const double2* src = q ? g_ga : g_gb;
               gv.x = __ldcg(&src[e].x);
@@ -1236,9 +1297,12 @@ extern "C" int tt_track_rows(void* stream, const tt_rows_args* a) {
   if (a->shard_world > 0) {
     if (a->shard_rank < 0 || a->shard_rank >= a->shard_world || (a->shard_phase != 1 && a->shard_phase != 2))
       return tt_fail(TT_EINVAL, "row sharding: need 0 <= rank < world and phase 1 or 2");
-    if (a->policy != TT_POLICY_STATIC || a->nslices != 1 || a->frames != 1 || a->y_mode != TT_Y_GATHER)
-      return tt_fail(TT_EUNSUPPORTED, "row sharding supports static row tables, one slice, one frame per launch, "
-                                      "gathered measurements");
+    const bool fused = a->shard_local && a->shard_fused;
+    if (a->policy != TT_POLICY_STATIC || a->nslices != 1 || (a->frames != 1 && !fused) || a->y_mode != TT_Y_GATHER)
+      return tt_fail(TT_EUNSUPPORTED, "row sharding supports static row tables, one slice, one frame per launch "
+                                      "(any number when fused), gathered measurements");
+    if (a->shard_fused && (!a->shard_local || !a->grid_sync))
+      return tt_fail(TT_EINVAL, "fused row sharding needs shard_local and a grid_sync counter");
     if (!a->xw || !a->xg) return tt_fail(TT_EINVAL, "row sharding: null payload buffers");
     if (a->resid_out) return tt_fail(TT_EUNSUPPORTED, "row sharding: residual output not supported");
   }
@@ -1280,13 +1344,28 @@ extern "C" int tt_track_rows(void* stream, const tt_rows_args* a) {
   cfg.blockDim = dim3(ROWS_NT, 1, 1);
   cfg.dynamicSmemBytes = (size_t)pl.smem;
   cfg.stream = (cudaStream_t)stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = (unsigned)pl.CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (a->shard_world > 0 && a->shard_local && a->shard_fused) {
+    // the in-kernel inter-cluster barriers need every CTA resident: a cooperative launch, which fails
+    // cleanly (TT_ECUDA) when the ranks' clusters do not fit the GPU at once
+    attr[1].id = cudaLaunchAttributeCooperative;
+    attr[1].val.cooperative = 1;
+    cfg.numAttrs = 2;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, fn, *a, pl);
+    if (e == cudaErrorCooperativeLaunchTooLarge) {
+      (void)cudaGetLastError();  // not sticky: clear it so the caller's fallback launches run
+      return tt_fail(TT_ECUDA, "fused row sharding: %d ranks x %d CTAs do not fit the GPU at once "
+                               "(cooperative launch too large)", a->shard_world, pl.CL);
+    }
+    TT_CUDA_TRY(e);
+    return TT_OK;
+  }
   TT_CUDA_TRY(cudaLaunchKernelEx(&cfg, fn, *a, pl));
   return TT_OK;
 }

@@ -699,9 +699,15 @@ class LocalShardedEngine:
 
     The replicated Bh is double-buffered across phase 2 (read one, rank 0 writes the other): when
     the ranks' clusters do not fit the GPU at once they run in waves, and a later wave must still
-    read the frame's pre-update Bh."""
+    read the frame's pre-update Bh.
 
-    def __init__(self, nx, ny, rank, lam, step, rows, counts, ranks, cluster=0, t0=1):
+    ``fused`` (default): one cooperative cluster launch runs every frame of a ``run`` call, both phases
+    per frame, the payload summed inside the kernel between two inter-cluster barriers (same fixed
+    order as ``tt_rows_shard_reduce``, so the results equal the 3-launch path); the factors stay in
+    shared memory across frames. It needs all ranks' clusters resident at once (up to 7 clusters of
+    16 CTAs on a B200); when they do not fit, ``run`` falls back to the 3-launch frames."""
+
+    def __init__(self, nx, ny, rank, lam, step, rows, counts, ranks, cluster=0, t0=1, fused=True):
         self.nx, self.ny, self.R = int(nx), int(ny), int(rank)
         self.ranks = int(ranks)
         if self.ranks < 1 or self.ranks > self.nx:
@@ -718,8 +724,11 @@ class LocalShardedEngine:
         self._bhs = [torch.zeros(self.ny, self.R, dtype=torch.complex64, device=self.dev) for _ in range(2)]
         self._cur = 0  # index of the buffer holding the current Bh
         self.xg_len = int(L.lib().tt_rows_shard_xg_len(self.R))
-        self.xw = torch.zeros(self.ranks, self.ny, self.R, dtype=torch.complex64, device=self.dev)
-        self.xg = torch.zeros(self.ranks, self.xg_len, dtype=torch.float64, device=self.dev)
+        self.fused = bool(fused)
+        sets = 2 if self.fused else 1  # the fused launch double-buffers the payload by frame parity
+        self.xw = torch.zeros(sets * self.ranks, self.ny, self.R, dtype=torch.complex64, device=self.dev)
+        self.xg = torch.zeros(sets * self.ranks, self.xg_len, dtype=torch.float64, device=self.dev)
+        self.grid_sync = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.alpha_bar = torch.zeros(1, dtype=torch.float64, device=self.dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.t = int(t0)
@@ -749,10 +758,10 @@ class LocalShardedEngine:
                     ah=torch.empty(frames, self.nx, self.R, dtype=torch.complex64, device=d),
                     bh=torch.empty(frames, self.ny, self.R, dtype=torch.complex64, device=d))
 
-    def _args(self, kspace, f, out, fo, phase, bh_cur, bh_nxt):
+    def _args(self, kspace, f, out, fo, phase, bh_cur, bh_nxt, frames=1):
         mode, mu, cf, cc = _step_params(self.step)
         a = L.RowsArgs()
-        a.nslices, a.nx, a.ny, a.rank, a.frames = 1, self.nx, self.ny, self.R, 1
+        a.nslices, a.nx, a.ny, a.rank, a.frames = 1, self.nx, self.ny, self.R, int(frames)
         a.max_rows, a.cluster, a.t0 = self.max_rows, self.cluster, self.t
         a.ah_in = a.ah_out = self.ah.data_ptr()
         a.bh_in = bh_cur.data_ptr()
@@ -765,7 +774,7 @@ class LocalShardedEngine:
         a.ysrc = kspace[f].data_ptr()
         a.y_frame_stride, a.y_slice_stride = self.nx * self.ny, self.nx * self.ny
         a.lam, a.step_mode, a.mu, a.c_floor, a.c_cap = self.lam, mode, mu, cf, cc
-        if phase == 2 and out is not None:
+        if phase in (0, 2) and out is not None:  # phase 2 of a frame, or a fused launch (phase 0 here)
             a.gamma_out = out["gamma"][fo].data_ptr()
             a.cost_out = out["cost"][fo:].data_ptr()
             a.mu_out = out["mu"][fo:].data_ptr()
@@ -775,7 +784,16 @@ class LocalShardedEngine:
         a.scratch = self.scr.buf.data_ptr()
         a.shard_rank, a.shard_world, a.shard_phase, a.shard_local = 0, self.ranks, phase, 1
         a.xw, a.xg = self.xw.data_ptr(), self.xg.data_ptr()
+        if phase == 0:  # fused launch: both phases of every frame
+            a.shard_phase, a.shard_fused, a.grid_sync = 1, 1, self.grid_sync.data_ptr()
         return a
+
+    def _run_fused(self, kspace, frames, out):
+        cur, nxt = self._bhs[self._cur], self._bhs[1 - self._cur]
+        a = self._args(kspace, self.frame, out, 0, 0, cur, nxt, frames=frames)
+        self.grid_sync.zero_()
+        K.track_rows(a)  # Bh in place: every rank loads it at the start, rank 0 writes it back at the end
+        self.t += frames
 
     def _frame(self, kspace, f, out, fo, keep):
         cur, nxt = self._bhs[self._cur], self._bhs[1 - self._cur]
@@ -793,6 +811,15 @@ class LocalShardedEngine:
         """kspace: (T, nx, ny) complex64 CUDA; frames from the current index."""
         if out is None:
             out = self.make_outputs(frames)
+        if self.fused and frames > 0:
+            try:
+                self._run_fused(kspace, frames, out)
+                self.frame += frames
+                return out
+            except RuntimeError as e:
+                if "cooperative" not in str(e).lower():
+                    raise
+                self.fused = False  # the ranks' clusters do not fit at once: 3-launch frames
         keep: list = []
         f0 = self.frame
         first = min(frames, 1)

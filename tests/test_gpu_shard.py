@@ -60,7 +60,8 @@ def test_row_sharded_equals_unsharded(world, n, R, S, T):
                                            (8, 512, 32, 64, 3)])
 def test_local_multi_rank_launch_equals_unsharded(ranks, n, R, S, T):
     """Every rank of the sharding as a cluster of one launch (phase 1), the payload slots summed on the
-    device, phase 2: equals the unsharded fused run and the host-reduced emulation; graph == eager."""
+    device, phase 2: equals the unsharded fused run and the host-reduced emulation; graph == eager; the
+    fused cooperative launch (both phases of every frame, in-kernel reduction) == the 3-launch frames."""
     import torch
 
     import paper_1609_04104_b200 as tt
@@ -74,15 +75,19 @@ def test_local_multi_rank_launch_equals_unsharded(ranks, n, R, S, T):
     ref = tt.run_online(ph.kspace, A0[None], B0[None], 0.1, tt.Fixed(0.01),
                         tt.StaticRows(rows[:, None, :], np.full((T, 1), S)))
     outs = []
-    for graph in (True, False):
-        e = tt.LocalShardedEngine(n, n, R, 0.1, tt.Fixed(0.01), rows, np.full(T, S), ranks)
+    for fused, graph in ((False, True), (False, False), (True, False)):
+        e = tt.LocalShardedEngine(n, n, R, 0.1, tt.Fixed(0.01), rows, np.full(T, S), ranks, fused=fused)
         e.set_image_factors(A0, B0)
         out = e.run(ks, T, graph=graph)
         torch.cuda.synchronize()
         e.check_status()
         outs.append(({k: v.cpu().numpy() for k, v in out.items()}, e.ah.cpu().numpy(), e.bh.cpu().numpy()))
-    for k in outs[0][0]:
-        np.testing.assert_array_equal(outs[0][0][k], outs[1][0][k])
+    # graph == eager, and the fused single launch (in-kernel reduction in the same order) == both
+    for o in outs[1:]:
+        for k in outs[0][0]:
+            np.testing.assert_array_equal(outs[0][0][k], o[0][k])
+        np.testing.assert_array_equal(outs[0][1], o[1])
+        np.testing.assert_array_equal(outs[0][2], o[2])
     out, ah, bh = outs[0]
     # the fp32 W partials are summed over the ranks in another order than the unsharded kernel's k
     # tiles (~1e-5 at 8 ranks, R = 32): the BASELINE parity bar, 1e-4 relative, is the tolerance
