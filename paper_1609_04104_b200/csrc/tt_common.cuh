@@ -27,6 +27,31 @@ inline cudaError_t tt_smem_attr(const void* fn, size_t bytes, size_t* cache) {
   return e;
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// The entry-sampling frame is a chain of ~14 small kernels. Launched with programmatic stream
+// serialisation, each kernel's CTAs are scheduled while its predecessor drains (the predecessor
+// triggers at its start); the kernel then waits (griddepcontrol.wait: predecessor complete, memory
+// visible) before its first global access. Without the attribute both instructions are no-ops.
+TT_DEV void pdl_wait_and_trigger() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t tt_launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                 Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, ((KArgs)args)...);
+}
+
 // ---------------------------------------------------------------- complex
 TT_DEV float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 TT_DEV float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }

@@ -86,6 +86,7 @@ __global__ void __cluster_dims__(EG_CL, 1, 1) __launch_bounds__(ENT_NT)
     ent_gram_kernel(int nmeas, const int* __restrict__ nmeas_dev, int nx, int ny, int R,
                     const float2* __restrict__ ah, const float2* __restrict__ bh, const EntSrc src,
                     double2* __restrict__ gp) {
+  pdl_wait_and_trigger();
   if (nmeas_dev) nmeas = min(*nmeas_dev, nmeas);
   extern __shared__ __align__(16) unsigned char smem[];
   float2* phi = (float2*)smem;                   // [TL][R]
@@ -196,6 +197,7 @@ __global__ void __launch_bounds__(ENT_NT) ent_solve_kernel(int R, int nmeas, con
                                                            const double* __restrict__ alpha_bar, double2* gam_out,
                                                            double* scal, float2* gamma_out, double* cost_out,
                                                            int32_t* status) {
+  pdl_wait_and_trigger();
   extern __shared__ __align__(16) unsigned char smem[];
   if (nmeas_dev) nmeas = min(*nmeas_dev, nmeas);
   const int Rp = R * (R + 1) / 2, NI = Rp + R, NI2 = NI + 1;
@@ -279,6 +281,7 @@ __global__ void ent_resid_kernel(int nmeas, const int* __restrict__ nmeas_dev, i
                                  const float2* __restrict__ ah, const float2* __restrict__ bh, const EntSrc src,
                                  const double2* gam, const double* scal, float2* __restrict__ xi,
                                  int* __restrict__ st, float2* __restrict__ resid) {
+  pdl_wait_and_trigger();
   if (nmeas_dev) nmeas = min(*nmeas_dev, nmeas);
   const int cur = (int)((const long long*)scal)[3];
   for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nmeas; l += gridDim.x * blockDim.x) {
@@ -319,6 +322,7 @@ __global__ void __launch_bounds__(BP_O * BP_K) ent_backproj_kernel(int nx, int n
                                                                    const int* __restrict__ st, const double2* gam,
                                                                    double* scal, float2* __restrict__ P,
                                                                    float2* __restrict__ Q) {
+  pdl_wait_and_trigger();
   __shared__ float2 sacc[BP_K][BP_O];
   __shared__ float scs[BP_K][BP_O];
   __shared__ double smax[BP_O * BP_K / 32];
@@ -395,6 +399,7 @@ __global__ void ent_update_kernel(int nx, int ny, int R, int nmeas, const int* _
                                   double* scal, double* alpha_bar, const double2* gam, const float2* ah,
                                   const float2* bh, const float2* __restrict__ P, const float2* __restrict__ Q,
                                   float2* ah_out, float2* bh_out, double* mu_out, double* alpha_out) {
+  pdl_wait_and_trigger();
   if (nmeas_dev) nmeas = min(*nmeas_dev, nmeas);
   const double lt = lam / (double)t;
   double m = 0.0, alpha = 0.0, ab = scal[4];
@@ -469,31 +474,31 @@ extern "C" int tt_track_entries(void* stream, const tt_entries_args* a) {
     const size_t sm = gram_smem(R);
     static size_t set_gram[TT_MAXDEV] = {0};
     TT_CUDA_TRY(tt_smem_attr((const void*)ent_gram_kernel, sm, set_gram));
-    ent_gram_kernel<<<ncl * EG_CL, ENT_NT, sm, st>>>(L, Ld, nx, ny, R, ah, bh, src, gp);
+    TT_CUDA_TRY(tt_launch_pdl(ent_gram_kernel, dim3(ncl * EG_CL), dim3(ENT_NT), sm, st, L, Ld, nx, ny, R, ah, bh, src, gp));
   }
   {
     const size_t sm = sizeof(double2) * ((size_t)NI2 + R + 4 * (size_t)(R + 1));
     static size_t set_solve[TT_MAXDEV] = {0};
     TT_CUDA_TRY(tt_smem_attr((const void*)ent_solve_kernel, sm, set_solve));
-    ent_solve_kernel<<<1, ENT_NT, sm, st>>>(R, L, Ld, ncl, a->lam, (long long)a->t, gp, a->alpha_bar, gam, scal,
-                                            (float2*)a->gamma_out, a->cost_out, a->status);
+    TT_CUDA_TRY(tt_launch_pdl(ent_solve_kernel, dim3(1), dim3(ENT_NT), sm, st, R, L, Ld, ncl, a->lam, (long long)a->t, gp, a->alpha_bar, gam, scal,
+                                            (float2*)a->gamma_out, a->cost_out, a->status));
   }
   if (L > 0) {
     int blocks = (L + 255) / 256;
     if (blocks > 1184) blocks = 1184;
-    ent_resid_kernel<<<blocks, 256, 0, st>>>(L, Ld, ny, R, ah, bh, src, gam, scal, xi, stp, (float2*)a->resid_out);
+    TT_CUDA_TRY(tt_launch_pdl(ent_resid_kernel, dim3(blocks), dim3(256), 0, st, L, Ld, ny, R, ah, bh, src, gam, scal, xi, stp, (float2*)a->resid_out));
     const int m = (nx > ny ? nx : ny) * R;
     dim3 grid((m + BP_O - 1) / BP_O, 2);
-    ent_backproj_kernel<<<grid, dim3(BP_O, BP_K), 0, st>>>(nx, ny, R, a->step_mode == TT_STEP_HESSIAN, ah, bh, xi,
-                                                          stp, gam, scal, P, Q);
+    TT_CUDA_TRY(tt_launch_pdl(ent_backproj_kernel, dim3(grid), dim3(dim3(BP_O, BP_K)), 0, st, nx, ny, R, a->step_mode == TT_STEP_HESSIAN, ah, bh, xi,
+                                                          stp, gam, scal, P, Q));
   }
   {
     const int n = (nx + ny) * R;
     int blocks = (n + 255) / 256;
     if (blocks > 1184) blocks = 1184;
-    ent_update_kernel<<<blocks, 256, 0, st>>>(nx, ny, R, L, Ld, a->lam, (long long)a->t, a->step_mode, a->mu,
+    TT_CUDA_TRY(tt_launch_pdl(ent_update_kernel, dim3(blocks), dim3(256), 0, st, nx, ny, R, L, Ld, a->lam, (long long)a->t, a->step_mode, a->mu,
                                               a->c_floor, a->c_cap, scal, a->alpha_bar, gam, ah, bh, P, Q,
-                                              (float2*)a->ah_out, (float2*)a->bh_out, a->mu_out, a->alpha_out);
+                                              (float2*)a->ah_out, (float2*)a->bh_out, a->mu_out, a->alpha_out));
   }
   TT_CUDA_TRY(cudaGetLastError());
   return TT_OK;

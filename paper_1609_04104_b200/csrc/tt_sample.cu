@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(SMP_NT) row_scores_kernel(int nx, int ny, int 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SMP_NT)
     entry_energy_kernel(int nx, int ny, int R, const float2* __restrict__ a, const float2* __restrict__ b,
                         double* __restrict__ ws, int32_t* status) {
+  pdl_wait_and_trigger();
   extern __shared__ __align__(16) unsigned char smem[];
   double* colsq = (double*)smem;
   double* red = colsq + R;
@@ -114,6 +115,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SMP_NT)
 __global__ void __launch_bounds__(SMP_NT) entry_map_kernel(int nx, int ny, int R, const double* __restrict__ ws,
                                                            double beta, double* __restrict__ probs,
                                                            double* __restrict__ part) {
+  pdl_wait_and_trigger();
   __shared__ double red[64];
   const size_t n = (size_t)nx * ny;
   const double den = (double)R * (double)(nx + ny);
@@ -132,6 +134,7 @@ __global__ void __launch_bounds__(SMP_NT) entry_map_kernel(int nx, int ny, int R
 // final renormalisation: every block sums the partials in the same order, then divides its share
 __global__ void __launch_bounds__(SMP_NT) entry_norm_kernel(size_t n, int nparts, const double* __restrict__ part,
                                                             double* __restrict__ probs) {
+  pdl_wait_and_trigger();
   __shared__ double red[64];
   __shared__ double tot;
   double loc = 0.0;
@@ -273,13 +276,13 @@ static int entry_scores_run(cudaStream_t st, int nx, int ny, int rank, const flo
                             double* probs_out, int32_t* status, double* ws) {
   void* stream = (void*)st;
   const size_t sm = sizeof(double) * ((size_t)rank + 64);
-  entry_energy_kernel<<<2, SMP_NT, sm, (cudaStream_t)stream>>>(nx, ny, rank, (const float2*)a, (const float2*)b, ws,
-                                                                status);
+  TT_CUDA_TRY(tt_launch_pdl(entry_energy_kernel, dim3(2), dim3(SMP_NT), sm, (cudaStream_t)stream, nx, ny, rank, (const float2*)a, (const float2*)b, ws,
+                                                                status));
   const size_t n = (size_t)nx * ny;
   int blocks = (int)((n + SMP_NT - 1) / SMP_NT);
   if (blocks > 4096) blocks = 4096;
-  entry_map_kernel<<<blocks, SMP_NT, 0, (cudaStream_t)stream>>>(nx, ny, rank, ws, beta, probs_out, ws + nx + ny + 1);
-  entry_norm_kernel<<<blocks, SMP_NT, 0, (cudaStream_t)stream>>>(n, blocks, ws + nx + ny + 1, probs_out);
+  TT_CUDA_TRY(tt_launch_pdl(entry_map_kernel, dim3(blocks), dim3(SMP_NT), 0, (cudaStream_t)stream, nx, ny, rank, ws, beta, probs_out, ws + nx + ny + 1));
+  TT_CUDA_TRY(tt_launch_pdl(entry_norm_kernel, dim3(blocks), dim3(SMP_NT), 0, (cudaStream_t)stream, n, blocks, ws + nx + ny + 1, probs_out));
   TT_CUDA_TRY(cudaGetLastError());
   return TT_OK;
 }
@@ -353,6 +356,7 @@ static BigDrawScratch big_layout(int n) {
 __global__ void __launch_bounds__(SMP_NT) big_scan_kernel(int n, const double* __restrict__ p, double* __restrict__ cdf,
                                                           double* __restrict__ part, int* __restrict__ ctl,
                                                           double* __restrict__ cq, int lstride) {
+  pdl_wait_and_trigger();
   __shared__ double red[64];
   const int tid = threadIdx.x;
   const int base = blockIdx.x * SMP_NT * BIG_IPT + tid * BIG_IPT;
@@ -421,6 +425,7 @@ __global__ void big_draw_kernel(int n, int ndraw, const double* __restrict__ cdf
                                 int nb, const int* __restrict__ forced, int nforced, uint64_t k0, uint64_t k1,
                                 const uint64_t* __restrict__ pos, int* __restrict__ flags, int* __restrict__ ctl,
                                 double depth_term, double gscale, int lstride) {
+  pdl_wait_and_trigger();
   // coarse copy of the CDF in shared memory: the last value of every 2^lstride-entry chunk; a draw
   // searches the chunks there and only lstride levels in global memory
   extern __shared__ double coarse[];
@@ -495,6 +500,7 @@ __global__ void big_draw_kernel(int n, int ndraw, const double* __restrict__ cdf
 __global__ void __launch_bounds__(SMP_NT) big_exact_kernel(int n, const double* __restrict__ p,
                                                            double* __restrict__ cdf, int* __restrict__ flags,
                                                            const int* __restrict__ ctl) {
+  pdl_wait_and_trigger();
   if (ctl[0] == 0) return;
   constexpr int CH = 2048;
   __shared__ __align__(16) double buf[2][CH];
@@ -555,6 +561,7 @@ __global__ void big_exact_redo_kernel(int n, int ndraw, const double* __restrict
                                       const int* __restrict__ forced, int nforced, uint64_t k0, uint64_t k1,
                                       const uint64_t* __restrict__ pos, int* __restrict__ flags,
                                       const int* __restrict__ ctl) {
+  pdl_wait_and_trigger();
   if (ctl[0] == 0) return;
   const double last = cdf[n];
   for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < ndraw + nforced; m += gridDim.x * blockDim.x) {
@@ -578,6 +585,7 @@ __global__ void big_exact_redo_kernel(int n, int ndraw, const double* __restrict
 // scan of the counts, writes); the writes clear the flags; the stream position advances by the draws
 __global__ void __launch_bounds__(SMP_NT) big_count_kernel(int n, const int* __restrict__ flags,
                                                            int* __restrict__ cpart) {
+  pdl_wait_and_trigger();
   __shared__ int red[64];
   const int base = blockIdx.x * SMP_NT * BIG_IPT + threadIdx.x * BIG_IPT;
   int c = 0;
@@ -590,6 +598,7 @@ __global__ void __launch_bounds__(SMP_NT) big_count_kernel(int n, const int* __r
 __global__ void __launch_bounds__(SMP_NT) big_write_kernel(int n, int nb, int ndraw, int cap, int* __restrict__ flags,
                                                            const int* __restrict__ cpart, uint64_t* __restrict__ pos,
                                                            int* __restrict__ omega, int* __restrict__ count) {
+  pdl_wait_and_trigger();
   __shared__ int red[64];
   __shared__ int sh_pre, sh_all;
   {  // this block's offset (counts of the blocks before it) and the total: integer sums
@@ -663,7 +672,7 @@ extern "C" int tt_draw_with_replacement_large(void* stream, int n, const double*
     if (e[0] == '1') gscale = 1e300;
   const int ls = big_lstride(n);
   double* cq = (double*)(sb + S.cq);
-  big_scan_kernel<<<nb, SMP_NT, 0, st>>>(n, probs, cdf, part, ctl, cq, ls);
+  TT_CUDA_TRY(tt_launch_pdl(big_scan_kernel, dim3(nb), dim3(SMP_NT), 0, st, n, probs, cdf, part, ctl, cq, ls));
   {
     int blocks = (ndraw + nforced + 255) / 256;
     if (blocks < 1) blocks = 1;
@@ -673,20 +682,20 @@ extern "C" int tt_draw_with_replacement_large(void* stream, int n, const double*
       static size_t set_draw[TT_MAXDEV] = {0};
       TT_CUDA_TRY(tt_smem_attr((const void*)big_draw_kernel, csm, set_draw));
     }
-    big_draw_kernel<<<blocks, 256, csm, st>>>(n, ndraw, cdf, cq, part, nb, forced, nforced, key0, key1, pos, flags,
-                                              ctl, depth_term, gscale, ls);
+    TT_CUDA_TRY(tt_launch_pdl(big_draw_kernel, dim3(blocks), dim3(256), csm, st, n, ndraw, cdf, cq, part, nb, forced, nforced, key0, key1, pos, flags,
+                                              ctl, depth_term, gscale, ls));
   }
   {  // exact fallback (each part exits at once unless a draw was ambiguous)
-    big_exact_kernel<<<1, SMP_NT, 0, st>>>(n, probs, cdf, flags, ctl);
+    TT_CUDA_TRY(tt_launch_pdl(big_exact_kernel, dim3(1), dim3(SMP_NT), 0, st, n, probs, cdf, flags, ctl));
     int rbk = (ndraw + nforced + 255) / 256;
     if (rbk < 1) rbk = 1;
     if (rbk > 1184) rbk = 1184;
-    big_exact_redo_kernel<<<rbk, 256, 0, st>>>(n, ndraw, cdf, forced, nforced, key0, key1, pos, flags, ctl);
+    TT_CUDA_TRY(tt_launch_pdl(big_exact_redo_kernel, dim3(rbk), dim3(256), 0, st, n, ndraw, cdf, forced, nforced, key0, key1, pos, flags, ctl));
   }
   int* cpart = (int*)(sb + S.cpart);
   int* coff = (int*)(sb + S.coff);
-  big_count_kernel<<<nb, SMP_NT, 0, st>>>(n, flags, cpart);
-  big_write_kernel<<<nb, SMP_NT, 0, st>>>(n, nb, ndraw, k, flags, cpart, pos, omega_out, count_out);
+  TT_CUDA_TRY(tt_launch_pdl(big_count_kernel, dim3(nb), dim3(SMP_NT), 0, st, n, flags, cpart));
+  TT_CUDA_TRY(tt_launch_pdl(big_write_kernel, dim3(nb), dim3(SMP_NT), 0, st, n, nb, ndraw, k, flags, cpart, pos, omega_out, count_out));
   TT_CUDA_TRY(cudaGetLastError());
   return TT_OK;
 }
