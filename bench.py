@@ -950,7 +950,8 @@ def run_ours(args, cfg):
         "gpu_launches": launches_per_step * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "kernel": "tt_rows_kernel",
-                     "bytes_per_slice_frame": b_upd, "peak_kind": peak_kind},
+                     "bytes_per_slice_frame": b_upd, "frames_per_launch": T / nblk,
+                     "algorithmic_bytes_per_launch": b_upd * ns * T / nblk, "peak_kind": peak_kind},
         "extra": {"track_ms_per_step": track_total / args.steps,
                   "us_per_frame_tracking": 1e6 * track_s / T,
                   "step_hbm_frac": (b_upd + b_rec) * value / 1e9 / hbm_peak / (1 if cfg["slices"] == 1 else 1),
