@@ -581,8 +581,11 @@ def _blocks(f0, f1, C):
     return out
 
 
+BLOCK_BYTES = 128 << 20  # run_online's default pipeline block: ~128 MB of truth per upload
+
+
 def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, warm_frames=0,
-               warm_epochs=20, chunk=40, keep_history=False) -> OnlineResult:
+               warm_epochs=20, chunk=None, keep_history=False) -> OnlineResult:
     """Public end-to-end call (host in, host out): the online loop over the
     frames of ``kspace`` (T, [nslices,] nx, ny) from image-domain initial
     factors, returning reconstructions and per-frame reports. The analogue of
@@ -591,7 +594,9 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
     first (experiment.py:219-239, default 5 x 20 in the reference config) and
     the results cover the streaming frames only; the policy applies to those.
 
-    Pipelined in blocks of ``chunk`` frames: the truth uploads on one copy
+    Pipelined in blocks of ``chunk`` frames (default: ~BLOCK_BYTES of truth per block, at most 40
+    frames — 40 frames at 256^2 x 1 slice, 4 at config 3's 64 slices, so that the uploads and the
+    downloads overlap on the two copy engines): the truth uploads on one copy
     stream, tracking + reconstruction of block c on the compute stream once
     its upload landed, and the reconstructions download into pinned host
     memory on a second copy stream while later blocks compute. Results do not
@@ -615,6 +620,8 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
     eng.set_image_factors(A0, np.asarray(B0).reshape(ns, ny, R))
     kd = src.contiguous() if on_dev else torch.empty(T, ns, nx, ny, dtype=torch.complex64, device=dev)
     W = int(warm_frames)
+    if chunk is None:
+        chunk = min(40, max(1, BLOCK_BYTES // max(1, ns * nx * ny * 8)))
     C = max(1, int(chunk))
     # upload blocks: the warm-up frames as one block, then the streaming frames in blocks of C
     bounds = ([(0, W)] if W else []) + _blocks(W, T, C)
