@@ -474,31 +474,34 @@ extern "C" int tt_track_entries(void* stream, const tt_entries_args* a) {
     const size_t sm = gram_smem(R);
     static size_t set_gram[TT_MAXDEV] = {0};
     TT_CUDA_TRY(tt_smem_attr((const void*)ent_gram_kernel, sm, set_gram));
-    TT_CUDA_TRY(tt_launch_pdl(ent_gram_kernel, dim3(ncl * EG_CL), dim3(ENT_NT), sm, st, L, Ld, nx, ny, R, ah, bh, src, gp));
+    TT_CUDA_TRY(tt_launch_pdl(ent_gram_kernel, dim3(ncl * EG_CL), dim3(ENT_NT), sm, st,
+        L, Ld, nx, ny, R, ah, bh, src, gp));
   }
   {
     const size_t sm = sizeof(double2) * ((size_t)NI2 + R + 4 * (size_t)(R + 1));
     static size_t set_solve[TT_MAXDEV] = {0};
     TT_CUDA_TRY(tt_smem_attr((const void*)ent_solve_kernel, sm, set_solve));
-    TT_CUDA_TRY(tt_launch_pdl(ent_solve_kernel, dim3(1), dim3(ENT_NT), sm, st, R, L, Ld, ncl, a->lam, (long long)a->t, gp, a->alpha_bar, gam, scal,
-                                            (float2*)a->gamma_out, a->cost_out, a->status));
+    TT_CUDA_TRY(tt_launch_pdl(ent_solve_kernel, dim3(1), dim3(ENT_NT), sm, st,
+        R, L, Ld, ncl, a->lam, (long long)a->t, gp, a->alpha_bar, gam, scal, (float2*)a->gamma_out, a->cost_out,
+        a->status));
   }
   if (L > 0) {
     int blocks = (L + 255) / 256;
     if (blocks > 1184) blocks = 1184;
-    TT_CUDA_TRY(tt_launch_pdl(ent_resid_kernel, dim3(blocks), dim3(256), 0, st, L, Ld, ny, R, ah, bh, src, gam, scal, xi, stp, (float2*)a->resid_out));
+    TT_CUDA_TRY(tt_launch_pdl(ent_resid_kernel, dim3(blocks), dim3(256), 0, st,
+        L, Ld, ny, R, ah, bh, src, gam, scal, xi, stp, (float2*)a->resid_out));
     const int m = (nx > ny ? nx : ny) * R;
     dim3 grid((m + BP_O - 1) / BP_O, 2);
-    TT_CUDA_TRY(tt_launch_pdl(ent_backproj_kernel, dim3(grid), dim3(dim3(BP_O, BP_K)), 0, st, nx, ny, R, a->step_mode == TT_STEP_HESSIAN, ah, bh, xi,
-                                                          stp, gam, scal, P, Q));
+    TT_CUDA_TRY(tt_launch_pdl(ent_backproj_kernel, grid, dim3(BP_O, BP_K), 0, st,
+        nx, ny, R, a->step_mode == TT_STEP_HESSIAN, ah, bh, xi, stp, gam, scal, P, Q));
   }
   {
     const int n = (nx + ny) * R;
     int blocks = (n + 255) / 256;
     if (blocks > 1184) blocks = 1184;
-    TT_CUDA_TRY(tt_launch_pdl(ent_update_kernel, dim3(blocks), dim3(256), 0, st, nx, ny, R, L, Ld, a->lam, (long long)a->t, a->step_mode, a->mu,
-                                              a->c_floor, a->c_cap, scal, a->alpha_bar, gam, ah, bh, P, Q,
-                                              (float2*)a->ah_out, (float2*)a->bh_out, a->mu_out, a->alpha_out));
+    TT_CUDA_TRY(tt_launch_pdl(ent_update_kernel, dim3(blocks), dim3(256), 0, st,
+        nx, ny, R, L, Ld, a->lam, (long long)a->t, a->step_mode, a->mu, a->c_floor, a->c_cap, scal, a->alpha_bar,
+        gam, ah, bh, P, Q, (float2*)a->ah_out, (float2*)a->bh_out, a->mu_out, a->alpha_out));
   }
   TT_CUDA_TRY(cudaGetLastError());
   return TT_OK;

@@ -276,13 +276,15 @@ static int entry_scores_run(cudaStream_t st, int nx, int ny, int rank, const flo
                             double* probs_out, int32_t* status, double* ws) {
   void* stream = (void*)st;
   const size_t sm = sizeof(double) * ((size_t)rank + 64);
-  TT_CUDA_TRY(tt_launch_pdl(entry_energy_kernel, dim3(2), dim3(SMP_NT), sm, (cudaStream_t)stream, nx, ny, rank, (const float2*)a, (const float2*)b, ws,
-                                                                status));
+  TT_CUDA_TRY(tt_launch_pdl(entry_energy_kernel, dim3(2), dim3(SMP_NT), sm, (cudaStream_t)stream,
+      nx, ny, rank, (const float2*)a, (const float2*)b, ws, status));
   const size_t n = (size_t)nx * ny;
   int blocks = (int)((n + SMP_NT - 1) / SMP_NT);
   if (blocks > 4096) blocks = 4096;
-  TT_CUDA_TRY(tt_launch_pdl(entry_map_kernel, dim3(blocks), dim3(SMP_NT), 0, (cudaStream_t)stream, nx, ny, rank, ws, beta, probs_out, ws + nx + ny + 1));
-  TT_CUDA_TRY(tt_launch_pdl(entry_norm_kernel, dim3(blocks), dim3(SMP_NT), 0, (cudaStream_t)stream, n, blocks, ws + nx + ny + 1, probs_out));
+  TT_CUDA_TRY(tt_launch_pdl(entry_map_kernel, dim3(blocks), dim3(SMP_NT), 0, (cudaStream_t)stream,
+      nx, ny, rank, ws, beta, probs_out, ws + nx + ny + 1));
+  TT_CUDA_TRY(tt_launch_pdl(entry_norm_kernel, dim3(blocks), dim3(SMP_NT), 0, (cudaStream_t)stream,
+      n, blocks, ws + nx + ny + 1, probs_out));
   TT_CUDA_TRY(cudaGetLastError());
   return TT_OK;
 }
@@ -682,20 +684,22 @@ extern "C" int tt_draw_with_replacement_large(void* stream, int n, const double*
       static size_t set_draw[TT_MAXDEV] = {0};
       TT_CUDA_TRY(tt_smem_attr((const void*)big_draw_kernel, csm, set_draw));
     }
-    TT_CUDA_TRY(tt_launch_pdl(big_draw_kernel, dim3(blocks), dim3(256), csm, st, n, ndraw, cdf, cq, part, nb, forced, nforced, key0, key1, pos, flags,
-                                              ctl, depth_term, gscale, ls));
+    TT_CUDA_TRY(tt_launch_pdl(big_draw_kernel, dim3(blocks), dim3(256), csm, st,
+        n, ndraw, cdf, cq, part, nb, forced, nforced, key0, key1, pos, flags, ctl, depth_term, gscale, ls));
   }
   {  // exact fallback (each part exits at once unless a draw was ambiguous)
     TT_CUDA_TRY(tt_launch_pdl(big_exact_kernel, dim3(1), dim3(SMP_NT), 0, st, n, probs, cdf, flags, ctl));
     int rbk = (ndraw + nforced + 255) / 256;
     if (rbk < 1) rbk = 1;
     if (rbk > 1184) rbk = 1184;
-    TT_CUDA_TRY(tt_launch_pdl(big_exact_redo_kernel, dim3(rbk), dim3(256), 0, st, n, ndraw, cdf, forced, nforced, key0, key1, pos, flags, ctl));
+    TT_CUDA_TRY(tt_launch_pdl(big_exact_redo_kernel, dim3(rbk), dim3(256), 0, st,
+        n, ndraw, cdf, forced, nforced, key0, key1, pos, flags, ctl));
   }
   int* cpart = (int*)(sb + S.cpart);
   int* coff = (int*)(sb + S.coff);
   TT_CUDA_TRY(tt_launch_pdl(big_count_kernel, dim3(nb), dim3(SMP_NT), 0, st, n, flags, cpart));
-  TT_CUDA_TRY(tt_launch_pdl(big_write_kernel, dim3(nb), dim3(SMP_NT), 0, st, n, nb, ndraw, k, flags, cpart, pos, omega_out, count_out));
+  TT_CUDA_TRY(tt_launch_pdl(big_write_kernel, dim3(nb), dim3(SMP_NT), 0, st,
+      n, nb, ndraw, k, flags, cpart, pos, omega_out, count_out));
   TT_CUDA_TRY(cudaGetLastError());
   return TT_OK;
 }
