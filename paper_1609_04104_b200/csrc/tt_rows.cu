@@ -280,7 +280,7 @@ static __device__ __noinline__ void write_residual(const tt_rows_args& a, const 
 template <bool TIGHT>
 static __device__ __noinline__ void gb_partials_tiled(const float2* bhl, const double2* bh64, int R, int nJ, int Rp,
                                                       int gb_nt, int gb_parts, const unsigned short* tab,
-                                                      double2* gbt, double2* dst_g) {
+                                                      double2* gbt, double2* dst_g, int jo, int jstep) {
   const int tid = threadIdx.x, NT = blockDim.x;
   for (int it = tid; it < gb_nt * gb_parts; it += NT) {
     const int part = idiv(it, gb_nt), t = it - part * gb_nt;
@@ -289,7 +289,7 @@ static __device__ __noinline__ void gb_partials_tiled(const float2* bhl, const d
     const int r0 = 2 * tr, q0 = 2 * tq, r1 = min(r0 + 1, R - 1), q1 = min(q0 + 1, R - 1);
     double2 a00 = make_double2(0.0, 0.0), a01 = a00, a10 = a00, a11 = a00;
     if (TIGHT) {  // fp32 operands converted on the fly (same products)
-      for (int jj = part; jj < nJ; jj += gb_parts) {
+      for (int jj = jo + part * jstep; jj < nJ; jj += gb_parts * jstep) {
         const float2* row = bhl + jj * R;
         const float2 br0 = row[r0], br1 = row[r1], bq0 = row[q0], bq1 = row[q1];
         a00 = zfma_cj(br0, bq0, a00);
@@ -298,7 +298,7 @@ static __device__ __noinline__ void gb_partials_tiled(const float2* bhl, const d
         a11 = zfma_cj(br1, bq1, a11);
       }
     } else {
-      for (int jj = part; jj < nJ; jj += gb_parts) {
+      for (int jj = jo + part * jstep; jj < nJ; jj += gb_parts * jstep) {
         const double2* row = bh64 + jj * R;
         const double2 br0 = row[r0], br1 = row[r1], bq0 = row[q0], bq1 = row[q1];
         a00 = zfma_cj(br0, bq0, a00);
@@ -353,6 +353,9 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
   // two inter-cluster barriers; payload slots double-buffered by frame parity
   const bool fused = multi && a.shard_fused != 0;
   unsigned gsync_gen = 0;
+  // fused: the replicated Bh's GB partial Gram is split across the ranks (rank q takes the columns
+  // jj = q (mod world) of every CTA's block) and summed with the payload
+  const int gb_jo = fused ? qid : 0, gb_js = fused ? a.shard_world : 1;
   const int R0 = shard ? part_begin(nx, a.shard_world, srank) : 0;
   const int nxs = shard ? part_begin(nx, a.shard_world, srank + 1) - R0 : nx;
   const int i0 = R0 + part_begin(nxs, CL, c), nI = part_begin(nxs, CL, c + 1) - part_begin(nxs, CL, c);
@@ -405,7 +408,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
   float2* vop = (float2*)(smem + pl.o_u2);              // update only: gamma-scaled GEMM operand
   double* red = (double*)(smem + pl.o_red);
   (void)inv;
-  __shared__ int sh_S, sh_err, sh_own, sh_amb;
+  __shared__ int sh_S, sh_err, sh_own, sh_amb, sh_Sglob;
   long long* pclk = (a.phase_clock != nullptr && blockIdx.x == 0) ? (long long*)a.phase_clock : nullptr;
   // branch-free (a lane-0 branch would leave warp 0 diverged and send later shuffles down the slow path)
 #define STAMP(k)                                                                                   \
@@ -460,7 +463,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     const int f = fused ? it >> 1 : it;
     // 0 full step, 1 partials -> payload, 2 payload -> update
     const int phase = !shard ? 0 : fused ? 1 + (it & 1) : a.shard_phase;
-    const size_t xgl = (size_t)Rp * 2 + 2;
+    const size_t xgl = (size_t)Rp * (fused ? 4 : 2) + 2;  // fused slots also carry GB: [GA][2 scalars][GB]
     float2* xwp = (float2*)a.xw + (fused ? (size_t)(f & 1) * a.shard_world * ny * R : 0);
     double* xgp = a.xg + (fused ? (size_t)(f & 1) * a.shard_world * xgl : 0);
     auto xg_at = [&](size_t k) { return __ldcg(xgp + k); };  // the reduced payload (slot 0)
@@ -494,23 +497,23 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     // GB partial over own columns: wide column blocks tiled (gb_partials_tiled), narrow ones one
     // packed entry per thread
     if (gb_tiled) {
-      gb_partials_tiled<TIGHT>(bhl, bh64, R, nJ, Rp, gb_nt, gb_parts, tab, gbt, g_gbp + (size_t)c * Rp);
+      gb_partials_tiled<TIGHT>(bhl, bh64, R, nJ, Rp, gb_nt, gb_parts, tab, gbt, g_gbp + (size_t)c * Rp, gb_jo, gb_js);
     } else {
       for (int e = tid; e < Rp; e += NT) {
         const int ij = tab[e];
         const int r = ij >> 8, q = ij & 255;
         double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
-        int jj = 0;
+        int jj = gb_jo;
         if (TIGHT) {
-          for (; jj + 1 < nJ; jj += 2) {
+          for (; jj + gb_js < nJ; jj += 2 * gb_js) {
             acc = zfma_cj(bhl[jj * R + r], bhl[jj * R + q], acc);
-            acc2 = zfma_cj(bhl[(jj + 1) * R + r], bhl[(jj + 1) * R + q], acc2);
+            acc2 = zfma_cj(bhl[(jj + gb_js) * R + r], bhl[(jj + gb_js) * R + q], acc2);
           }
           if (jj < nJ) acc = zfma_cj(bhl[jj * R + r], bhl[jj * R + q], acc);
         } else {
-          for (; jj + 1 < nJ; jj += 2) {
+          for (; jj + gb_js < nJ; jj += 2 * gb_js) {
             acc = zfma_cj(bh64[jj * R + r], bh64[jj * R + q], acc);
-            acc2 = zfma_cj(bh64[(jj + 1) * R + r], bh64[(jj + 1) * R + q], acc2);
+            acc2 = zfma_cj(bh64[(jj + gb_js) * R + r], bh64[(jj + gb_js) * R + q], acc2);
           }
           if (jj < nJ) acc = zfma_cj(bh64[jj * R + r], bh64[jj * R + q], acc);
         }
@@ -531,8 +534,9 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     STAMP(2);
     for (int e = eb + tid - 32; tid >= 32 && e < ee; e += NT - 32) {
       const double2 g = sum_parts2(g_gbp + e, (size_t)Rp, CL);
-      __stcg(&g_gb[e].x, g.x);
-      __stcg(&g_gb[e].y, g.y);
+      double* dst = fused ? xgp + (size_t)qid * xgl + 2 * Rp + 2 + 2 * e : (double*)&g_gb[e];  // rank's share
+      __stcg(dst, g.x);
+      __stcg(dst + 1, g.y);
     }
     for (int m = tid; m < ndraw; m += NT) usm[m] = __ldcg(&g_unif[(f % ROWS_UF) * ndraw + m]);  // in flight with
     for (int r = tid; r < R && tid < 32; r += 32) {                                                // the norm sums
@@ -684,11 +688,15 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       }
       ppos += (uint64_t)max(a.k_draws - a.nforced, 0);
       STAMP(20);
+    } else if (fused && phase == 2) {
+      // the frame's row table (this rank's share, filtered in phase 1) is still in shared memory
+      Sglob = sh_Sglob;
     } else {
       if (tid == 0) sh_err = 0;
       __syncthreads();
       S = load_static_rows(a, f, s, rows, flags, &sh_err);
       Sglob = S;
+      if (tid == 0) sh_Sglob = S;
       if (shard && warp == 0) {
         // keep only this rank's rows, in measurement order (the other ranks take the rest)
         int cnt = 0;
@@ -979,7 +987,8 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     double2 gae0 = make_double2(0.0, 0.0), gbe0 = gae0;
     if (tid < Rp) {
       gae0 = phase == 2 ? make_double2(xg_at(2 * tid), xg_at(2 * tid + 1)) : __ldcg(&g_ga[tid]);
-      gbe0 = __ldcg(&g_gb[tid]);
+      gbe0 = fused ? make_double2(__ldcg(xgp + 2 * Rp + 2 + 2 * tid), __ldcg(xgp + 2 * Rp + 3 + 2 * tid))
+                   : __ldcg(&g_gb[tid]);
     }
     for (int o = tid; o < nown * R; o += NT) {
       const int m = idiv(o, R), r = o - m * R;
@@ -1007,7 +1016,8 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       double2 gae = gae0, gbe = gbe0;
       if (e != tid) {
         gae = phase == 2 ? make_double2(xg_at(2 * e), xg_at(2 * e + 1)) : __ldcg(&g_ga[e]);
-        gbe = __ldcg(&g_gb[e]);
+        gbe = fused ? make_double2(__ldcg(xgp + 2 * Rp + 2 + 2 * e), __ldcg(xgp + 2 * Rp + 3 + 2 * e))
+                    : __ldcg(&g_gb[e]);
       }
       double2 gg = zmul(gae, gbe);
       if (r == q) {

@@ -710,8 +710,10 @@ class LocalShardedEngine:
 
     ``fused`` (default): one cooperative cluster launch runs every frame of a ``run`` call, both phases
     per frame, the payload summed inside the kernel between two inter-cluster barriers (same fixed
-    order as ``tt_rows_shard_reduce``, so the results equal the 3-launch path); the factors stay in
-    shared memory across frames. It needs all ranks' clusters resident at once (up to 7 clusters of
+    order as ``tt_rows_shard_reduce``); the factors and the frame's row table stay in shared memory
+    across the phases and frames, and the replicated Bh's GB Gram is split across the ranks (rank q
+    takes every world-th column) and summed with the payload, so GB rounds differently from the
+    3-launch path (~1e-16 relative). It needs all ranks' clusters resident at once (up to 7 clusters of
     16 CTAs on a B200); when they do not fit, ``run`` falls back to the 3-launch frames."""
 
     def __init__(self, nx, ny, rank, lam, step, rows, counts, ranks, cluster=0, t0=1, fused=True):
@@ -734,7 +736,9 @@ class LocalShardedEngine:
         self.fused = bool(fused)
         sets = 2 if self.fused else 1  # the fused launch double-buffers the payload by frame parity
         self.xw = torch.zeros(sets * self.ranks, self.ny, self.R, dtype=torch.complex64, device=self.dev)
-        self.xg = torch.zeros(sets * self.ranks, self.xg_len, dtype=torch.float64, device=self.dev)
+        # fused slots also carry the ranks' GB partials: [GA packed][||Y||^2, ||Ah||^2][GB packed]
+        slot = 2 * self.xg_len - 2 if self.fused else self.xg_len
+        self.xg = torch.zeros(sets * self.ranks, slot, dtype=torch.float64, device=self.dev)
         self.grid_sync = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.alpha_bar = torch.zeros(1, dtype=torch.float64, device=self.dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=self.dev)

@@ -61,7 +61,8 @@ def test_row_sharded_equals_unsharded(world, n, R, S, T):
 def test_local_multi_rank_launch_equals_unsharded(ranks, n, R, S, T):
     """Every rank of the sharding as a cluster of one launch (phase 1), the payload slots summed on the
     device, phase 2: equals the unsharded fused run and the host-reduced emulation; graph == eager; the
-    fused cooperative launch (both phases of every frame, in-kernel reduction) == the 3-launch frames."""
+    fused cooperative launch (both phases of every frame, in-kernel reduction, GB split over the ranks)
+    agrees with the 3-launch frames to rounding."""
     import torch
 
     import paper_1609_04104_b200 as tt
@@ -82,12 +83,17 @@ def test_local_multi_rank_launch_equals_unsharded(ranks, n, R, S, T):
         torch.cuda.synchronize()
         e.check_status()
         outs.append(({k: v.cpu().numpy() for k, v in out.items()}, e.ah.cpu().numpy(), e.bh.cpu().numpy()))
-    # graph == eager, and the fused single launch (in-kernel reduction in the same order) == both
-    for o in outs[1:]:
-        for k in outs[0][0]:
-            np.testing.assert_array_equal(outs[0][0][k], o[0][k])
-        np.testing.assert_array_equal(outs[0][1], o[1])
-        np.testing.assert_array_equal(outs[0][2], o[2])
+    # graph == eager bit for bit; the fused single launch sums GB over the ranks' column subsets (another
+    # fp64 order), so it agrees to rounding
+    for k in outs[0][0]:
+        np.testing.assert_array_equal(outs[0][0][k], outs[1][0][k])
+    np.testing.assert_array_equal(outs[0][1], outs[1][1])
+    np.testing.assert_array_equal(outs[0][2], outs[1][2])
+    fo = outs[2]
+    for f in range(T):
+        assert rel(fo[0]["gamma"][f], outs[0][0]["gamma"][f]) < 1e-5, f
+    assert rel(fo[1], outs[0][1]) < 1e-5 and rel(fo[2], outs[0][2]) < 1e-5
+    np.testing.assert_allclose(fo[0]["cost"], outs[0][0]["cost"], rtol=1e-5)
     out, ah, bh = outs[0]
     # the fp32 W partials are summed over the ranks in another order than the unsharded kernel's k
     # tiles (~1e-5 at 8 ranks, R = 32): the BASELINE parity bar, 1e-4 relative, is the tolerance
