@@ -767,6 +767,80 @@ def run_row_sharded(args, cfg):
     return 0
 
 
+def run_local_sharded(args, cfg):
+    """Config 4 on one GPU with the row sharding's ranks as thread-block clusters (SURVEY §8e emulated
+    in one fused cooperative launch: `LocalShardedEngine(fused=True)`), then the inverse column FFTs and
+    the reconstruction of all T frames. Device-timed like `run_ours` (L2 flushed between steps)."""
+    import torch
+
+    import paper_1609_04104_b200 as tt
+    from paper_1609_04104_b200 import _lib as L
+    from paper_1609_04104_b200 import _ops as K
+
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    L.load()
+    n, R, T = cfg["n"], cfg["R"], cfg["T"]
+    ks_np, clean_np = make_data(cfg, [0])
+    A0, B0 = init_factors(cfg, [0])
+    Smax = int(np.ceil(cfg["vd"] * n))
+    gen = np.random.Generator(np.random.Philox(key=2024))
+    tab = np.stack([tt.variable_density_rows(n, -1.0, cfg["vd"], gen) for _ in range(T)])
+    ks = torch.from_numpy(ks_np[:, 0]).to(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    X = torch.empty(T, n, n, dtype=torch.complex64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def fresh():
+        e = tt.LocalShardedEngine(n, n, R, cfg["lam"], tt.Fixed(cfg["mu"]), tab, np.full(T, Smax), args.local_ranks)
+        e.set_image_factors(A0[0], B0[0])
+        return e, e.make_outputs(T)
+
+    def step(e, out, ev=None):
+        e.run(ks, T, out=out)
+        if ev is not None:
+            ev.record(stream)
+        A = K.fft_cols_(out["ah"], inverse=True)
+        B = K.fft_cols_(out["bh"], inverse=True)
+        K.reconstruct(A, B, out["gamma"], out=X)
+
+    for _ in range(args.warmup):
+        e, out = fresh()
+        step(e, out)
+    torch.cuda.synchronize()
+    tot = trk = 0.0
+    with ClockSampler(0) as clk:
+        for _ in range(args.steps):
+            e, out = fresh()
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(stream)
+            step(e, out, e1)
+            e2.record(stream)
+            torch.cuda.synchronize()
+            tot += e0.elapsed_time(e2)
+            trk += e0.elapsed_time(e1)
+    e.check_status()
+    cl = torch.from_numpy(clean_np[:, 0]).to(dev)
+    nm = tt.nmse_frames(cl.reshape(T, -1), X.reshape(T, -1)).sqrt()
+    value = T * args.steps / (tot / 1e3)
+    line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "c64", "data": "synthetic",
+            "config": {"workload": cfg["desc"].replace("single GPU, unsharded",
+                                                       f"Ah row-sharded over {args.local_ranks} clusters of one GPU"),
+                       "frames_per_step": T, "rank": R, "nx": n, "ny": n, "l2": "flushed between steps (256 MB write)",
+                       "parallelism": f"local row-shard x{args.local_ranks} (fused cooperative launch: "
+                                      f"{'yes' if e.fused else 'no, 3-launch frames'})"},
+            "gpu_launches": (1 if e.fused else 3 * T) + 3,
+            "extra": {"us_per_frame_tracking": 1e3 * trk / args.steps / T, "mean_nrmse": float(nm.mean()),
+                      "last_nrmse": float(nm[-1])},
+            "clocks": clk.summary(), "e2e": None, "cpu_baseline": None}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
@@ -980,12 +1054,16 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--row-shard", action="store_true", help="config c4: use the row-sharded two-phase path")
     ap.add_argument("--blocks", type=int, default=4, help="tracking launches per step (reconstruction overlaps)")
+    ap.add_argument("--local-ranks", type=int, default=0,
+                    help="config c4 on one GPU: row-shard over this many thread-block clusters (fused launch)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)
     if args.config == "c4" and (int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.row_shard):
         return run_row_sharded(args, cfg)
+    if args.config == "c4" and args.local_ranks > 0:
+        return run_local_sharded(args, cfg)
     if "entries" in cfg:
         return run_entries(args, cfg)
     if "patch" in cfg:
