@@ -644,18 +644,20 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
     Ts = T - W
     ks_stream = kd[W:]
     out = eng.make_outputs(Ts)
-    recon = torch.empty(Ts, ns, nx, ny, dtype=torch.complex64, pin_memory=True)
-    Xd = torch.empty(Ts, ns, nx, ny, dtype=torch.complex64, device=dev)
+    recon = Xd = None
     # tracking blocks run back to back on the compute stream; each block's reconstruction runs on its
     # own stream once the block's tracking is done, and its download follows on the copy stream
-    s_rec.wait_stream(comp)
-    s_out.wait_stream(comp)
     hist = {k: out[k].clone() for k in ("ah",)} if keep_history else None
     for (f0, f1), ev in blocks:
         a, b = f0 - W, f1 - W
         comp.wait_event(ev)
         part = {k: v[a:b] for k, v in out.items()}
         eng.run(ks_stream, b - a, out=part)
+        if recon is None:  # the result buffers are set up while the first block tracks
+            recon = torch.empty(Ts, ns, nx, ny, dtype=torch.complex64, pin_memory=True)
+            Xd = torch.empty(Ts, ns, nx, ny, dtype=torch.complex64, device=dev)
+            s_rec.wait_stream(comp)
+            s_out.wait_stream(comp)
         tracked = torch.cuda.Event()
         tracked.record(comp)
         s_rec.wait_event(tracked)
@@ -668,6 +670,9 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
         s_out.wait_event(done)
         with torch.cuda.stream(s_out):
             recon[a:b].copy_(Xd[a:b], non_blocking=True)
+    if recon is None:  # no streaming frames
+        recon = torch.empty(Ts, ns, nx, ny, dtype=torch.complex64, pin_memory=True)
+        Xd = torch.empty(Ts, ns, nx, ny, dtype=torch.complex64, device=dev)
     comp.wait_stream(s_rec)
     # small results, final factors and the status word: asynchronous copies into pinned memory, one sync
     pinned = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True)  # noqa: E731
