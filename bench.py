@@ -391,7 +391,8 @@ def run_entries(args, cfg):
         "vs_baseline": None, "dtype": "c64", "data": "synthetic",
         "config": {"workload": cfg["desc"], "frames_per_step": frames, "rank": R, "nx": n, "ny": n, "trials": k,
                    "l2": "flushed between steps (256 MB write)", "parallelism": f"replicas x{world}"},
-        "gpu_launches": None,
+        # per replayed frame: entry scores (3 kernels), large-domain draw (6), generic step (5)
+        "gpu_launches": 14 * frames * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": None, "kernel": "entry frame chain (graph)",
                      "bytes_per_frame": b_frame, "peak_kind": peak_kind},
