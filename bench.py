@@ -1,27 +1,27 @@
 #!/usr/bin/env python
 """Frames/s of the online per-frame MM reconstruction loop on B200.
 
-Default workload = BASELINE.json configs[1] ("c2"): one 256x256 complex64
-cine phantom slice, T=200 frames, R=20, lambda=0.05, Fixed mu=0.01,
-informative row sampling at 4x (K=64 trials incl. 16 forced centre lines,
-beta=0.1, Philox draws). One bench *step* = the whole T-frame online
-sequence from the same initial state: per frame [row scores -> Philox draw
--> gather y -> Gram/ridge -> k-space factor update] in persistent
-cluster-kernel launches over blocks of frames (`--blocks`, default 4; the
-state stays resident across them), each block's inverse column FFTs of the
-per-frame factors and reconstruction overlapping the next block's tracking
-on a second stream (4 launches of our kernels per block).
+Default workload = BASELINE.json configs[2] ("c3"), the largest configuration that fits one GPU:
+64 independent 256x256 complex64 cine phantom slices, T=100 frames, R=16, lambda=0.05, Fixed
+mu=0.01, informative row sampling at 20% (K=52 trials incl. the forced DC line, beta=0.1, Philox
+draws per slice). One bench *step* = the whole T-frame online sequence of every slice from the same
+initial state: per slice-frame [row scores -> Philox draw -> gather y -> Gram/ridge -> k-space factor
+update] in persistent cluster-kernel launches over blocks of frames (`--blocks`, default 4; the state
+stays resident across them), each block's reconstruction of the image frames overlapping the next
+block's tracking on a second stream. `--config c2` (single 256^2 slice, T=200, R=20, K=64 with 16
+forced centre lines), `c1`, `c4` and the widening configs select the others.
 
-`value`  = frames reconstructed per second over all ranks (device time,
-           inputs resident, L2 flushed between steps).
-`e2e`    = the same through the public call `run_online` with the truth
-           k-space in pinned host memory (H2D) and the reconstructions +
-           per-frame reports read back (D2H) inside the timed region.
-`--impl reference` times the CPU oracle port of the reference algorithm
-(numpy SVD ridge etc.) on the host cores for a bounded sample.
-Multi-GPU (torchrun): one independent C2 replica per rank (the single-slice
-config does not shard), `scaling: weak`. `--config c3` runs
-the 64-slice config sharded over ranks (no collective, `scaling: strong`).
+`value`  = slice-frames reconstructed per second over all ranks (device time, inputs resident, L2
+           flushed between steps).
+`e2e`    = the same through the public call `run_online` with the truth k-space in pinned host
+           memory (H2D) and the reconstructions + per-frame reports read back (D2H) inside the timed
+           region.
+`--impl reference` times the UNMODIFIED reference package (baseline/_ref, `bench_reference.py`):
+its own `run_adaptive` per slice, one process per host core, full T per step.
+`--gpus N` without torchrun re-launches itself under `torch.distributed.run` with N ranks. The
+64-slice config is sharded over ranks (64/N slices each, no collective, `scaling: strong`); the
+single-slice configs run one replica per rank (`scaling: weak`); `c4` under N ranks runs the row
+sharding.
 """
 
 from __future__ import annotations
@@ -254,11 +254,82 @@ def cpu_oracle_fps(cfg, frames, ks, A0, B0):
     return frames / dt, dt
 
 
+REF_CONFIGS = ("c1", "c2", "c3", "c4")  # the BASELINE configs: timed through the reference package itself
+REF_FRAMES = {"c4": 8}  # ~1 s per frame at 1024^2: a bounded sample of frames (>= 8 frames)
+
+
+def reference_sample(args, cfg):
+    """Frames per reference step: the config's full T unless bounded (c4, or --ref-frames)."""
+    if args.ref_frames > 0:
+        return min(cfg["T"], args.ref_frames)
+    return min(cfg["T"], REF_FRAMES.get(args.config, cfg["T"]))
+
+
 def run_reference(args, cfg):
+    """The reference arm: the unmodified reference package (bench_reference.py) on the host cores,
+    this config's workload, one process per core (single-threaded BLAS each). Rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    frames = args.ref_frames
+    if args.config not in REF_CONFIGS:
+        return run_reference_port(args, cfg)
+    import bench_reference as BR
+
+    try:
+        BR.load_reference()
+    except Exception as e:  # the install is missing: the pinned oracle port stands in (kind "port")
+        print(f"reference package unavailable ({e!r}); timing the oracle port", file=sys.stderr)
+        return run_reference_port(args, dict(cfg))
+    fr = reference_sample(args, cfg)
+    m = BR.measure(dict(cfg, T=fr), args.steps, args.warmup)
+    nsl = cfg.get("slices", 1)
+    value = m["value"]
+    sample = (f"{m['slices']} of {nsl} slices x {fr} of {cfg['T']} frames per step through the stock "
+              f"run_adaptive (experiment.py:444-556; SSIM stubbed), {m['slices']} processes x 1 BLAS thread "
+              f"on {m['cores']} host cores")
+    line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": m["ms_per_step"], "higher_is_better": True,
+            "scaling": "strong" if nsl > 1 else "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "config": workload_config(args, cfg), "impl": "reference",
+            "same_config": bool(fr == cfg["T"] and m["slices"] == nsl),
+            "cpu_baseline": {"value": value, "unit": "frames/s", "cores": m["slices"], "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "extra": {"host_cores": m["cores"], "last_nmse": m["last_nmse"][:4]}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(args, cfg):
+    """The config keys both arms report."""
+    return {"workload": cfg["desc"], "frames_per_step": cfg["T"], "slices": cfg.get("slices", 1), "rank": cfg["R"],
+            "nx": cfg["n"], "ny": cfg["n"], "l2": "flushed between steps (256 MB write)", "init": "cold start"}
+
+
+def cpu_baseline_reference(args, cfg):
+    """cpu_baseline of our arm: the reference package itself on the box's host cores, a bounded sample
+    (one step of min(slices, cores) slices, full T except c4), plus one core alone and the stock
+    track_step by itself (SURVEY §8d's two numbers)."""
+    import bench_reference as BR
+
+    BR.load_reference()
+    fr = reference_sample(args, cfg)
+    t0 = time.perf_counter()
+    allc = BR.measure(dict(cfg, T=fr), 1, 0)
+    one = BR.measure(dict(cfg, T=min(fr, 50)), 1, 0, max_slices=1)
+    ts = BR.track_step_ms(cfg, frames=6 if cfg["n"] >= 1024 else 12)
+    dt = time.perf_counter() - t0
+    return {"value": allc["value"], "unit": "frames/s", "cores": allc["slices"], "kind": "reference",
+            "sample": f"{allc['slices']} slices x {fr} frames of the stock run_adaptive, one process per core "
+                      f"({allc['cores']} host cores), single-threaded BLAS; {dt:.0f} s for all three numbers",
+            "one_core_frames_per_s": one["value"], "track_step_ms_median": ts}
+
+
+def run_reference_port(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    frames = args.ref_frames or 8
     ks, _ = make_data(dict(cfg, T=frames), [0])
     A0, B0 = init_factors(cfg, [0])
     for _ in range(args.warmup):
@@ -1004,11 +1075,20 @@ def run_ours(args, cfg):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        fr = args.cpu_frames
-        fps, dt = cpu_oracle_fps(cfg, fr, ks_np, A0, B0)
-        cpu = {"value": fps, "unit": "frames/s", "cores": os.cpu_count(), "kind": "port",
-               "sample": f"first {fr} frames of slice 0 ({dt:.1f} s), oracle port of the reference algorithm "
-                         "(numpy SVD ridge, pocketfft), all host threads"}
+        try:
+            cpu = cpu_baseline_reference(args, cfg)
+        except Exception as e:  # reference package missing: the pinned oracle port on slice 0
+            fr = args.cpu_frames
+            fps, dt = cpu_oracle_fps(cfg, fr, ks_np, A0, B0)
+            cpu = {"value": fps, "unit": "frames/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"first {fr} frames of slice 0 ({dt:.1f} s), oracle port of the reference algorithm "
+                             f"(numpy SVD ridge, pocketfft), all host threads; reference unavailable: {e!r}"}
+
+    # ---- parity of this run (rank 0's first slice) against the oracle on the same masks: the device's
+    # own rows fed to the oracle restatement, every frame's gamma and NRMSE compared (north_star tolerances)
+    parity = None
+    if rank == 0 and not args.no_parity:
+        parity = run_parity(cfg, ks_np[:, 0], clean_np[:, 0], A0[0], B0[0], out, Xr[:, 0], cnt[:, 0])
 
     if world > 1:
         dist.destroy_process_group()
@@ -1018,10 +1098,9 @@ def run_ours(args, cfg):
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "c64", "data": "synthetic",
-        "config": {"workload": cfg["desc"], "frames_per_step": T, "slices_per_gpu": ns, "rank": R,
-                   "nx": n, "ny": n, "cluster_ctas_per_slice": eng.cluster, "l2": "flushed between steps (256 MB write)",
-                   "tracking_launches_per_step": nblk,
-                   "parallelism": f"{'replicas' if cfg['slices'] == 1 else 'slice-shard'} x{world}"},
+        "config": dict(workload_config(args, cfg), slices_per_gpu=ns, cluster_ctas_per_slice=eng.cluster,
+                       tracking_launches_per_step=nblk,
+                       parallelism=f"{'replicas' if cfg['slices'] == 1 else 'slice-shard'} x{world}"),
         "gpu_launches": launches_per_step * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "kernel": "tt_rows_kernel",
@@ -1036,9 +1115,53 @@ def run_ours(args, cfg):
         "clocks": clk.summary(),
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "parity": parity,
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+PARITY_FRAMES = {"c4": 12}  # the oracle's numpy SVD at 1024^2 takes ~1 s per frame
+
+
+def run_parity(cfg, ks, clean, A0, B0, out, X, cnt):
+    """Slice 0 of the last timed step against the CPU oracle (oracle/tt_oracle.py, pinned to the
+    reference) fed the same per-frame rows the device drew: per-frame gamma (relative) and the NRMSE
+    trajectory (absolute) over the first T frames (PARITY_FRAMES bounds c4); the device's masks are
+    also compared with the oracle's own free-running draws (first frame that differs, if any)."""
+    from oracle import tt_oracle as O
+
+    T = min(cfg["T"], PARITY_FRAMES.get(cfg.get("name", ""), cfg["T"]))
+    if cfg["n"] >= 1024:
+        T = min(T, PARITY_FRAMES["c4"])
+    rows_d = out["rows"][:T, 0].cpu().numpy()
+    rows = [rows_d[f, :int(cnt[f])].astype(np.int64) for f in range(T)]
+    A0c = np.asarray(A0).astype(np.complex64).astype(np.complex128)
+    B0c = np.asarray(B0).astype(np.complex64).astype(np.complex128)
+    t0 = time.perf_counter()
+    ref = O.online_run(ks[:T], A0c, B0c, cfg["lam"], ("fixed", cfg["mu"]), {"kind": "static", "rows": rows},
+                       clean=clean[:T])
+    gam = out["gamma"][:T, 0].cpu().numpy()
+    ge = max(float(np.linalg.norm(gam[f] - ref["gamma"][f]) / max(np.linalg.norm(ref["gamma"][f]), 1e-300))
+             for f in range(T))
+    nd = X[:T].cpu().numpy().reshape(T, -1)
+    cl = clean[:T].reshape(T, -1)
+    nr_dev = np.sqrt(np.sum(np.abs(cl - nd) ** 2, axis=1) / np.sum(np.abs(cl) ** 2, axis=1))
+    ne = float(np.max(np.abs(nr_dev - np.sqrt(np.asarray(ref["nmse"])))))
+    first_div = None
+    if "K" in cfg:  # the oracle's own draws from its own probabilities (device masks bit-exact until a near-tie)
+        free = O.online_run(ks[:T], A0c, B0c, cfg["lam"], ("fixed", cfg["mu"]),
+                            {"kind": "informative", "k": cfg["K"], "forced": list(cfg["forced"]), "beta": cfg["beta"],
+                             "key": (2024, 0)})
+        for f in range(T):
+            if not np.array_equal(free["rows"][f], rows[f]):
+                first_div = f
+                break
+    return {"slice": 0, "frames": T, "gamma_max_rel": ge, "nrmse_max_abs": ne,
+            "tol": {"gamma_rel": 1e-4, "nrmse_abs": 1e-3}, "pass": bool(ge < 1e-4 and ne < 1e-3),
+            "masks": "device rows fed to the oracle",
+            "free_running_masks_equal_frames": (T if first_div is None else first_div) if "K" in cfg else None,
+            "oracle_s": round(time.perf_counter() - t0, 1)}
 
 
 def main():
@@ -1047,20 +1170,35 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
     ap.add_argument("--cluster", type=int, default=0)
     ap.add_argument("--cpu-frames", type=int, default=100)
-    ap.add_argument("--ref-frames", type=int, default=8)
+    ap.add_argument("--ref-frames", type=int, default=0,
+                    help="frames per reference step (default: the config's T; 8 for c4, SURVEY §8d)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--row-shard", action="store_true", help="config c4: use the row-sharded two-phase path")
     ap.add_argument("--blocks", type=int, default=4, help="tracking launches per step (reconstruction overlaps)")
     ap.add_argument("--local-ranks", type=int, default=0,
                     help="config c4 on one GPU: row-shard over this many thread-block clusters (fused launch)")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config], name=args.config)
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-launch under torch.distributed.run (rendezvous on 127.0.0.1)
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.config == "c4" and (int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.row_shard):
         return run_row_sharded(args, cfg)
     if args.config == "c4" and args.local_ranks > 0:

@@ -239,6 +239,20 @@ int tt_draw_with_replacement_large(void* stream, int n, const double* probs, int
  * renormalised draws, draw order; consumes k uniforms from pos[0]. */
 int tt_draw_without_replacement(void* stream, int n, const double* weights, int k, uint64_t key0,
                                 uint64_t key1, uint64_t* pos, int32_t* out, int32_t* status);
+/* The three draws with caller-supplied uniforms instead of the Philox stream: uniforms[m] is the
+ * Generator.random() value draw m consumes (one per draw, as numpy's choice and the sequential draws
+ * consume them), so a caller holding any other bit generator (np.random.default_rng(seed), PCG64,
+ * as the reference builds them: experiment.py:257,338,453) draws them on the host with rng.random(k)
+ * and gets numpy's result for the same probabilities. _u: uniforms [nslices][k - nforced];
+ * large_u: [k - nforced], pos is an 8-byte device scratch word; without_u: [k]. */
+int tt_draw_with_replacement_u(void* stream, int nslices, int n, const double* probs, int k,
+                               const int32_t* forced, int nforced, const double* uniforms,
+                               int32_t* omega_out, int32_t* count_out);
+int tt_draw_with_replacement_large_u(void* stream, int n, const double* probs, int k, const int32_t* forced,
+                                     int nforced, const double* uniforms, uint64_t* pos, int32_t* omega_out,
+                                     int32_t* count_out, void* scratch);
+int tt_draw_without_replacement_u(void* stream, int n, const double* weights, int k, const double* uniforms,
+                                  int32_t* out, int32_t* status);
 
 /* ------------------------------------------------------------------ CTEN container (cten.py:1-74)
  * "CTEN" | u8 version 1 | u8 dtype (0 f32 pairs, 1 f64 pairs) | u8 ndim | ndim x u32 dims | payload.

@@ -103,6 +103,9 @@ SIGNATURES = {
     "tt_draw_with_replacement": (C.c_int, [_p, C.c_int, C.c_int, _p, C.c_int, _p, C.c_int, _u64, _u64, _p, _p,
                                            _p]),
     "tt_draw_without_replacement": (C.c_int, [_p, C.c_int, _p, C.c_int, _u64, _u64, _p, _p, _p]),
+    "tt_draw_with_replacement_u": (C.c_int, [_p, C.c_int, C.c_int, _p, C.c_int, _p, C.c_int, _p, _p, _p]),
+    "tt_draw_with_replacement_large_u": (C.c_int, [_p, C.c_int, _p, C.c_int, _p, C.c_int, _p, _p, _p, _p, _p]),
+    "tt_draw_without_replacement_u": (C.c_int, [_p, C.c_int, _p, C.c_int, _p, _p, _p]),
     "tt_reconstruct": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, C.c_int, _p, _p, _p, _p]),
     "tt_nmse": (C.c_int, [_p, C.c_int, C.c_size_t, _p, _p, _p, _p]),
     "tt_nmse_work_doubles": (C.c_size_t, [C.c_int]),

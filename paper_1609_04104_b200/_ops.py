@@ -136,33 +136,59 @@ def entry_scores(a: torch.Tensor, b: torch.Tensor, beta: float, status: torch.Te
     return out
 
 
-def draw_with_replacement(probs: torch.Tensor, k: int, forced: torch.Tensor | None, key: tuple[int, int],
-                          pos: torch.Tensor):
-    """probs (nslices, n) fp64; pos (nslices,) uint64-as-int64 in/out."""
+def draw_with_replacement(probs: torch.Tensor, k: int, forced: torch.Tensor | None, key: tuple[int, int] | None,
+                          pos: torch.Tensor | None, uniforms: torch.Tensor | None = None):
+    """probs (nslices, n) fp64; pos (nslices,) uint64-as-int64 in/out (Philox stream ``key``), or
+    ``uniforms`` (nslices, k - nforced) fp64: the Generator.random() values the draws consume."""
     _need(probs, torch.float64, "probs")
     ns, n = probs.shape
     omega = torch.empty(ns, k, dtype=torch.int32, device=probs.device)
     cnt = torch.empty(ns, dtype=torch.int32, device=probs.device)
     nf = 0 if forced is None else int(forced.numel())
+    if uniforms is not None:
+        _need(uniforms, torch.float64, "uniforms")
+        if uniforms.numel() != ns * (k - nf):
+            raise ValueError("uniforms: one value per draw and slice")
+    fp = None if nf == 0 else forced.data_ptr()
+    up = None if uniforms is None or uniforms.numel() == 0 else uniforms.data_ptr()
     if 24 * n + 512 > 220 * 1024:  # domain beyond one CTA's shared memory (entry sampling): global-memory path
         scr = torch.zeros(int(L.lib().tt_draw_scratch_bytes(n)), dtype=torch.uint8, device=probs.device)
         for s in range(ns):
+            if uniforms is not None:
+                p1 = torch.zeros(1, dtype=torch.int64, device=probs.device)
+                L.check(L.lib().tt_draw_with_replacement_large_u(
+                    L.stream_ptr(), n, probs[s].data_ptr(), int(k), fp, nf,
+                    None if up is None else up + 8 * s * (k - nf), p1.data_ptr(), omega[s].data_ptr(),
+                    cnt[s:s + 1].data_ptr(), scr.data_ptr()), "draw_samples")
+                continue
             L.check(L.lib().tt_draw_with_replacement_large(
-                L.stream_ptr(), n, probs[s].data_ptr(), int(k), None if nf == 0 else forced.data_ptr(), nf,
+                L.stream_ptr(), n, probs[s].data_ptr(), int(k), fp, nf,
                 int(key[0]), int(key[1]) + s, pos[s:s + 1].data_ptr(), omega[s].data_ptr(), cnt[s:s + 1].data_ptr(),
                 scr.data_ptr()), "draw_samples")
         return omega, cnt
-    L.check(L.lib().tt_draw_with_replacement(L.stream_ptr(), ns, n, probs.data_ptr(), int(k),
-                                             None if nf == 0 else forced.data_ptr(), nf, int(key[0]),
+    if uniforms is not None:
+        L.check(L.lib().tt_draw_with_replacement_u(L.stream_ptr(), ns, n, probs.data_ptr(), int(k), fp, nf, up,
+                                                   omega.data_ptr(), cnt.data_ptr()), "draw_samples")
+        return omega, cnt
+    L.check(L.lib().tt_draw_with_replacement(L.stream_ptr(), ns, n, probs.data_ptr(), int(k), fp, nf, int(key[0]),
                                              int(key[1]), pos.data_ptr(), omega.data_ptr(), cnt.data_ptr()),
             "draw_samples")
     return omega, cnt
 
 
-def draw_without_replacement(weights: torch.Tensor, k: int, key: tuple[int, int], pos: torch.Tensor,
-                             status: torch.Tensor) -> torch.Tensor:
+def draw_without_replacement(weights: torch.Tensor, k: int, key: tuple[int, int] | None, pos: torch.Tensor | None,
+                             status: torch.Tensor, uniforms: torch.Tensor | None = None) -> torch.Tensor:
+    """k sequential draws from the Philox stream ``key`` at ``pos``, or from ``uniforms`` (k fp64)."""
     _need(weights, torch.float64, "weights")
     out = torch.empty(max(k, 1), dtype=torch.int32, device=weights.device)
+    if uniforms is not None:
+        _need(uniforms, torch.float64, "uniforms")
+        if uniforms.numel() != k:
+            raise ValueError("uniforms: one value per draw")
+        L.check(L.lib().tt_draw_without_replacement_u(L.stream_ptr(), weights.numel(), weights.data_ptr(), int(k),
+                                                      uniforms.data_ptr() if k else None, out.data_ptr(),
+                                                      status.data_ptr()), "weighted_draw_without_replacement")
+        return out[:k]
     L.check(L.lib().tt_draw_without_replacement(L.stream_ptr(), weights.numel(), weights.data_ptr(), int(k),
                                                 int(key[0]), int(key[1]), pos.data_ptr(), out.data_ptr(),
                                                 status.data_ptr()), "weighted_draw_without_replacement")

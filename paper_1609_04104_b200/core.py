@@ -49,6 +49,24 @@ class TensorSubspace:
     def __init__(self, factors):
         if isinstance(factors, TensorSubspace):
             factors = factors.factors
+        factors = tuple(factors)
+        if len(factors) == 2 and all(isinstance(f, torch.Tensor) and f.is_cuda for f in factors):
+            # device factors stay on the device (no host round trip): copied once as complex64, the
+            # reference's copy-on-construction (core.py:47-52), validated like host factors
+            for f in factors:
+                if f.dim() != 2:
+                    raise ValueError(f"factor matrix must be 2-D, got shape {tuple(f.shape)}")
+                if f.shape[0] < 1 or f.shape[1] < 1:
+                    raise ValueError(f"factor matrix must be nonempty, got shape {tuple(f.shape)}")
+            if factors[0].shape[1] != factors[1].shape[1]:
+                raise ValueError(f"factor ranks differ: {sorted({int(f.shape[1]) for f in factors})}")
+            dev = L.device()
+            a, b = (f.detach().to(dev, torch.complex64).clone().contiguous() for f in factors)
+            self._host, self._dev, self._kind = None, (a, b), "direct"
+            self._dims = (int(a.shape[0]), int(b.shape[0]))
+            self._rank = int(a.shape[1])
+            self._cache = {}
+            return
         facs = []
         for f in factors:
             if isinstance(f, torch.Tensor):

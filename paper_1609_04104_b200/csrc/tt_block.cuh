@@ -146,7 +146,8 @@ TT_DEV void block_cumsum(const double* p, double* cdf, int n, bool exact, double
 template <bool EXACT_DIV = true>
 TT_DEV void draw_with_replacement_block(const double* p, double* cdf, int* flags, int* rows, int& S, int n,
                                         int ndraw, const int* forced, int nforced, uint64_t k0, uint64_t k1,
-                                        uint64_t pos, double* red, int* sh_flag) {
+                                        uint64_t pos, double* red, int* sh_flag,
+                                        const double* utab = nullptr) {
   const int tid = threadIdx.x, NT = blockDim.x;
   for (int i = tid; i < n; i += NT) flags[i] = 0;
   if (tid == 0) *sh_flag = 0;
@@ -162,7 +163,7 @@ TT_DEV void draw_with_replacement_block(const double* p, double* cdf, int* flags
     }
     __syncthreads();
     for (int m = tid; m < ndraw; m += NT) {
-      const double u = philox_uniform(k0, k1, pos + (uint64_t)m);
+      const double u = draw_uniform(utab, k0, k1, pos, (uint64_t)m);
       int idx = upper_bound_d(cdf, n, u);
       if (!exact) {
         const double lo = idx > 0 ? cdf[idx - 1] : -1.0;

@@ -177,6 +177,12 @@ TT_DEV double philox_uniform(uint64_t k0, uint64_t k1, uint64_t n) {
   const uint64_t w = b.v[n & 3ull];
   return (double)(w >> 11) * (1.0 / 9007199254740992.0);
 }
+// Uniform of draw m: word pos + m of the Philox stream (key0, key1), or utab[m] when the caller
+// supplied the uniforms (a host Generator over another bit generator drew them: Generator.random()
+// values, which is what choice / the sequential draws consume one per draw)
+TT_DEV double draw_uniform(const double* utab, uint64_t k0, uint64_t k1, uint64_t pos, uint64_t m) {
+  return utab ? utab[m] : philox_uniform(k0, k1, pos + m);
+}
 
 // ---------------------------------------------------------------- misc
 TT_DEV int iceil_div(int a, int b) { return (a + b - 1) / b; }

@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(SMP_NT) normalize_kernel(size_t n, double* __r
 __global__ void __launch_bounds__(SMP_NT) draw_wr_kernel(int n, const double* __restrict__ probs, int ndraw,
                                                          const int32_t* forced, int nforced, uint64_t k0,
                                                          uint64_t k1, uint64_t* pos, int32_t* omega,
-                                                         int32_t* count, int k) {
+                                                         int32_t* count, int k, const double* utab) {
   extern __shared__ __align__(16) unsigned char smem[];
   double* p = (double*)smem;
   double* cdf = p + n;
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(SMP_NT) draw_wr_kernel(int n, const double* __
   const uint64_t p0 = pos ? pos[s] : 0ull;
   int S;
   draw_with_replacement_block(p, cdf, flags, rows, S, n, ndraw, forced, nforced, k0, k1 + (uint64_t)s, p0, red,
-                              &sh_flag);
+                              &sh_flag, utab ? utab + (size_t)s * ndraw : nullptr);
   for (int i = threadIdx.x; i < k; i += blockDim.x) omega[(size_t)s * k + i] = i < S ? rows[i] : -1;
   if (threadIdx.x == 0) {
     count[s] = S;
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(SMP_NT) draw_wr_kernel(int n, const double* __
 // sequential renormalised draws without replacement (draw order)
 __global__ void __launch_bounds__(SMP_NT) draw_wor_kernel(int n, const double* __restrict__ weights, int k,
                                                           uint64_t k0, uint64_t k1, uint64_t* pos,
-                                                          int32_t* out, int32_t* status) {
+                                                          int32_t* out, int32_t* status, const double* utab) {
   extern __shared__ __align__(16) unsigned char smem[];
   double* w = (double*)smem;
   double* cdf = w + n;
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(SMP_NT) draw_wor_kernel(int n, const double* _
   }
   const uint64_t p0 = pos ? pos[0] : 0ull;
   for (int m = 0; m < k; ++m) {
-    const double u01 = philox_uniform(k0, k1, p0 + (uint64_t)m);
+    const double u01 = draw_uniform(utab, k0, k1, p0, (uint64_t)m);
     for (int exact = 0; exact < 2; ++exact) {
       block_cumsum(w, cdf, n, exact != 0, red);
       const double total = cdf[n - 1];
@@ -289,9 +289,9 @@ static int entry_scores_run(cudaStream_t st, int nx, int ny, int rank, const flo
   return TT_OK;
 }
 
-extern "C" int tt_draw_with_replacement(void* stream, int nslices, int n, const double* probs, int k,
-                                        const int32_t* forced, int nforced, uint64_t key0, uint64_t key1,
-                                        uint64_t* pos, int32_t* omega_out, int32_t* count_out) {
+static int draw_wr_run(void* stream, int nslices, int n, const double* probs, int k, const int32_t* forced,
+                       int nforced, uint64_t key0, uint64_t key1, uint64_t* pos, int32_t* omega_out,
+                       int32_t* count_out, const double* utab) {
   if (nslices < 1 || n < 1 || k < 1 || !probs || !omega_out || !count_out)
     return tt_fail(TT_EINVAL, "trial count must be at least 1");
   if (nforced < 0 || nforced > k) return tt_fail(TT_EINVAL, "more forced indices than trials");
@@ -300,22 +300,46 @@ extern "C" int tt_draw_with_replacement(void* stream, int nslices, int n, const 
   if (sm > 220 * 1024) return tt_fail(TT_EUNSUPPORTED, "draw domain too large for one CTA (n=%d)", n);
   TT_CUDA_TRY(cudaFuncSetAttribute(draw_wr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   draw_wr_kernel<<<nslices, SMP_NT, sm, (cudaStream_t)stream>>>(n, probs, k - nforced, forced, nforced, key0, key1,
-                                                                  pos, omega_out, count_out, k);
+                                                                  pos, omega_out, count_out, k, utab);
   TT_CUDA_TRY(cudaGetLastError());
   return TT_OK;
 }
 
-extern "C" int tt_draw_without_replacement(void* stream, int n, const double* weights, int k, uint64_t key0,
-                                           uint64_t key1, uint64_t* pos, int32_t* out, int32_t* status) {
+extern "C" int tt_draw_with_replacement(void* stream, int nslices, int n, const double* probs, int k,
+                                        const int32_t* forced, int nforced, uint64_t key0, uint64_t key1,
+                                        uint64_t* pos, int32_t* omega_out, int32_t* count_out) {
+  return draw_wr_run(stream, nslices, n, probs, k, forced, nforced, key0, key1, pos, omega_out, count_out, nullptr);
+}
+
+extern "C" int tt_draw_with_replacement_u(void* stream, int nslices, int n, const double* probs, int k,
+                                          const int32_t* forced, int nforced, const double* uniforms,
+                                          int32_t* omega_out, int32_t* count_out) {
+  if (!uniforms && k > nforced) return tt_fail(TT_EINVAL, "tt_draw_with_replacement_u: null uniforms");
+  return draw_wr_run(stream, nslices, n, probs, k, forced, nforced, 0, 0, nullptr, omega_out, count_out, uniforms);
+}
+
+static int draw_wor_run(void* stream, int n, const double* weights, int k, uint64_t key0, uint64_t key1,
+                        uint64_t* pos, int32_t* out, int32_t* status, const double* utab) {
   if (n < 1 || k < 0 || !weights || (!out && k > 0)) return tt_fail(TT_EINVAL, "tt_draw_without_replacement: bad args");
   if (k > n) return tt_fail(TT_EINVAL, "cannot draw more items than have positive weight");
   if (k == 0) return TT_OK;
   const size_t sm = sizeof(double) * (2 * (size_t)n + 64);
   if (sm > 220 * 1024) return tt_fail(TT_EUNSUPPORTED, "draw domain too large for one CTA (n=%d)", n);
   TT_CUDA_TRY(cudaFuncSetAttribute(draw_wor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  draw_wor_kernel<<<1, SMP_NT, sm, (cudaStream_t)stream>>>(n, weights, k, key0, key1, pos, out, status);
+  draw_wor_kernel<<<1, SMP_NT, sm, (cudaStream_t)stream>>>(n, weights, k, key0, key1, pos, out, status, utab);
   TT_CUDA_TRY(cudaGetLastError());
   return TT_OK;
+}
+
+extern "C" int tt_draw_without_replacement(void* stream, int n, const double* weights, int k, uint64_t key0,
+                                           uint64_t key1, uint64_t* pos, int32_t* out, int32_t* status) {
+  return draw_wor_run(stream, n, weights, k, key0, key1, pos, out, status, nullptr);
+}
+
+extern "C" int tt_draw_without_replacement_u(void* stream, int n, const double* weights, int k,
+                                             const double* uniforms, int32_t* out, int32_t* status) {
+  if (!uniforms && k > 0) return tt_fail(TT_EINVAL, "tt_draw_without_replacement_u: null uniforms");
+  return draw_wor_run(stream, n, weights, k, 0, 0, nullptr, out, status, uniforms);
 }
 
 // ---------------------------------------------------------------- draws over large domains (global memory)
@@ -426,7 +450,7 @@ __global__ void big_draw_kernel(int n, int ndraw, const double* __restrict__ cdf
                                 const double* __restrict__ part,
                                 int nb, const int* __restrict__ forced, int nforced, uint64_t k0, uint64_t k1,
                                 const uint64_t* __restrict__ pos, int* __restrict__ flags, int* __restrict__ ctl,
-                                double depth_term, double gscale, int lstride) {
+                                double depth_term, double gscale, int lstride, const double* __restrict__ utab) {
   pdl_wait_and_trigger();
   // coarse copy of the CDF in shared memory: the last value of every 2^lstride-entry chunk; a draw
   // searches the chunks there and only lstride levels in global memory
@@ -460,7 +484,7 @@ __global__ void big_draw_kernel(int n, int ndraw, const double* __restrict__ cdf
       if (f >= 0 && f < n) flags[f] = 1;
       continue;
     }
-    const double u = philox_uniform(k0, k1, p0 + (uint64_t)m);
+    const double u = draw_uniform(utab, k0, k1, p0, (uint64_t)m);
     const double ut = u * total;
     int lo = 0, hi = nc;  // first chunk whose last value exceeds ut
     while (lo < hi) {
@@ -562,7 +586,7 @@ __global__ void __launch_bounds__(SMP_NT) big_exact_kernel(int n, const double* 
 __global__ void big_exact_redo_kernel(int n, int ndraw, const double* __restrict__ cdf,
                                       const int* __restrict__ forced, int nforced, uint64_t k0, uint64_t k1,
                                       const uint64_t* __restrict__ pos, int* __restrict__ flags,
-                                      const int* __restrict__ ctl) {
+                                      const int* __restrict__ ctl, const double* __restrict__ utab) {
   pdl_wait_and_trigger();
   if (ctl[0] == 0) return;
   const double last = cdf[n];
@@ -572,7 +596,7 @@ __global__ void big_exact_redo_kernel(int n, int ndraw, const double* __restrict
       if (f >= 0 && f < n) flags[f] = 1;
       continue;
     }
-    const double u = philox_uniform(k0, k1, pos[0] + (uint64_t)m);
+    const double u = draw_uniform(utab, k0, k1, pos[0], (uint64_t)m);
     int lo = 0, hi = n;  // searchsorted(cdf / cdf[-1], u, 'right')
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
@@ -648,9 +672,9 @@ __global__ void __launch_bounds__(SMP_NT) big_write_kernel(int n, int nb, int nd
 
 extern "C" size_t tt_draw_scratch_bytes(int n) { return n > 0 ? big_layout(n).total : 0; }
 
-extern "C" int tt_draw_with_replacement_large(void* stream, int n, const double* probs, int k, const int32_t* forced,
-                                              int nforced, uint64_t key0, uint64_t key1, uint64_t* pos,
-                                              int32_t* omega_out, int32_t* count_out, void* scratch) {
+static int draw_large_run(void* stream, int n, const double* probs, int k, const int32_t* forced, int nforced,
+                          uint64_t key0, uint64_t key1, uint64_t* pos, int32_t* omega_out, int32_t* count_out,
+                          void* scratch, const double* utab) {
   if (n < 1 || k < 1 || !probs || !omega_out || !count_out || !pos || !scratch)
     return tt_fail(TT_EINVAL, "tt_draw_with_replacement_large: bad args");
   if (nforced < 0 || nforced > k) return tt_fail(TT_EINVAL, "more forced indices than trials");
@@ -685,7 +709,7 @@ extern "C" int tt_draw_with_replacement_large(void* stream, int n, const double*
       TT_CUDA_TRY(tt_smem_attr((const void*)big_draw_kernel, csm, set_draw));
     }
     TT_CUDA_TRY(tt_launch_pdl(big_draw_kernel, dim3(blocks), dim3(256), csm, st,
-        n, ndraw, cdf, cq, part, nb, forced, nforced, key0, key1, pos, flags, ctl, depth_term, gscale, ls));
+        n, ndraw, cdf, cq, part, nb, forced, nforced, key0, key1, pos, flags, ctl, depth_term, gscale, ls, utab));
   }
   {  // exact fallback (each part exits at once unless a draw was ambiguous)
     TT_CUDA_TRY(tt_launch_pdl(big_exact_kernel, dim3(1), dim3(SMP_NT), 0, st, n, probs, cdf, flags, ctl));
@@ -693,7 +717,7 @@ extern "C" int tt_draw_with_replacement_large(void* stream, int n, const double*
     if (rbk < 1) rbk = 1;
     if (rbk > 1184) rbk = 1184;
     TT_CUDA_TRY(tt_launch_pdl(big_exact_redo_kernel, dim3(rbk), dim3(256), 0, st,
-        n, ndraw, cdf, forced, nforced, key0, key1, pos, flags, ctl));
+        n, ndraw, cdf, forced, nforced, key0, key1, pos, flags, ctl, utab));
   }
   int* cpart = (int*)(sb + S.cpart);
   int* coff = (int*)(sb + S.coff);
@@ -702,4 +726,18 @@ extern "C" int tt_draw_with_replacement_large(void* stream, int n, const double*
       n, nb, ndraw, k, flags, cpart, pos, omega_out, count_out));
   TT_CUDA_TRY(cudaGetLastError());
   return TT_OK;
+}
+
+extern "C" int tt_draw_with_replacement_large(void* stream, int n, const double* probs, int k, const int32_t* forced,
+                                              int nforced, uint64_t key0, uint64_t key1, uint64_t* pos,
+                                              int32_t* omega_out, int32_t* count_out, void* scratch) {
+  return draw_large_run(stream, n, probs, k, forced, nforced, key0, key1, pos, omega_out, count_out, scratch, nullptr);
+}
+
+extern "C" int tt_draw_with_replacement_large_u(void* stream, int n, const double* probs, int k,
+                                                const int32_t* forced, int nforced, const double* uniforms,
+                                                uint64_t* pos, int32_t* omega_out, int32_t* count_out,
+                                                void* scratch) {
+  if (!uniforms && k > nforced) return tt_fail(TT_EINVAL, "tt_draw_with_replacement_large_u: null uniforms");
+  return draw_large_run(stream, n, probs, k, forced, nforced, 0, 0, pos, omega_out, count_out, scratch, uniforms);
 }

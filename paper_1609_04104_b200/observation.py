@@ -222,6 +222,20 @@ def philox_position(rng) -> tuple:
     return key[0], key[1], pos
 
 
+def device_uniforms(rng, k: int):
+    """Where the device draws take their k uniforms from: ``("philox", key0, key1, pos)`` for a
+    Generator over Philox (the kernels index the stream directly; the host generator is advanced
+    afterwards), else ``("table", u)`` with u = rng.random(k) uploaded — exactly the
+    Generator.random() values numpy's choice / the sequential draws consume, one per draw, so any
+    bit generator (np.random.default_rng(seed) is PCG64, as the reference builds them:
+    experiment.py:257,338,453) gets numpy's draws."""
+    try:
+        return ("philox",) + tuple(philox_position(rng))
+    except TypeError:
+        u = np.ascontiguousarray(rng.random(int(k)), dtype=np.float64)
+        return ("table", torch.from_numpy(u).to(L.device()))
+
+
 def _advance(rng, n: int) -> None:
     """Keep the host Generator in step with the words consumed on device."""
     if n > 0:
@@ -230,20 +244,24 @@ def _advance(rng, n: int) -> None:
 
 def weighted_draw_without_replacement(weights, k: int, rng) -> np.ndarray:
     """Sequential renormalised draws (observation.py:279-297), on device,
-    bit-identical to numpy for a Philox Generator."""
+    bit-identical to numpy (any bit generator: ``device_uniforms``)."""
     w = np.asarray(weights, dtype=float)
     if k > np.count_nonzero(w):
         raise ValueError("cannot draw more items than have positive weight")
     if k == 0:
         return np.empty(0, dtype=np.int64)
-    k0, k1, pos = philox_position(rng)
+    src = device_uniforms(rng, k)
     dev = L.device()
     wt = torch.from_numpy(np.ascontiguousarray(w)).to(dev)
-    pt = torch.tensor([pos], dtype=torch.int64, device=dev)
     st = torch.zeros(1, dtype=torch.int32, device=dev)
-    out = K.draw_without_replacement(wt, int(k), (k0, k1), pt, st)
+    if src[0] == "philox":
+        _, k0, k1, pos = src
+        pt = torch.tensor([pos], dtype=torch.int64, device=dev)
+        out = K.draw_without_replacement(wt, int(k), (k0, k1), pt, st)
+        _advance(rng, int(k))
+    else:
+        out = K.draw_without_replacement(wt, int(k), None, None, st, uniforms=src[1])
     L.raise_status(int(st.item()), "weighted_draw_without_replacement")
-    _advance(rng, int(k))
     return out.cpu().numpy().astype(np.int64)
 
 
