@@ -285,14 +285,14 @@ def run_reference(args, cfg):
     nsl = cfg.get("slices", 1)
     value = m["value"]
     sample = (f"{m['slices']} of {nsl} slices x {fr} of {cfg['T']} frames per step through the stock "
-              f"run_adaptive (experiment.py:444-556; SSIM stubbed), {m['slices']} processes x 1 BLAS thread "
+              f"run_adaptive (experiment.py:444-556; SSIM stubbed), {m['procs']} processes x 1 BLAS thread "
               f"on {m['cores']} host cores")
     line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": m["ms_per_step"], "higher_is_better": True,
             "scaling": "strong" if nsl > 1 else "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
             "config": workload_config(args, cfg), "impl": "reference",
             "same_config": bool(fr == cfg["T"] and m["slices"] == nsl),
-            "cpu_baseline": {"value": value, "unit": "frames/s", "cores": m["slices"], "kind": "reference",
+            "cpu_baseline": {"value": value, "unit": "frames/s", "cores": m["procs"], "kind": "reference",
                              "sample": sample},
             "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "extra": {"host_cores": m["cores"], "last_nmse": m["last_nmse"][:4]}}
@@ -315,11 +315,11 @@ def cpu_baseline_reference(args, cfg):
     BR.load_reference()
     fr = reference_sample(args, cfg)
     t0 = time.perf_counter()
-    allc = BR.measure(dict(cfg, T=fr), 1, 0)
+    allc = BR.measure(dict(cfg, T=fr), 1, 0, max_slices=BR.host_cores())
     one = BR.measure(dict(cfg, T=min(fr, 50)), 1, 0, max_slices=1)
     ts = BR.track_step_ms(cfg, frames=6 if cfg["n"] >= 1024 else 12)
     dt = time.perf_counter() - t0
-    return {"value": allc["value"], "unit": "frames/s", "cores": allc["slices"], "kind": "reference",
+    return {"value": allc["value"], "unit": "frames/s", "cores": allc["procs"], "kind": "reference",
             "sample": f"{allc['slices']} slices x {fr} frames of the stock run_adaptive, one process per core "
                       f"({allc['cores']} host cores), single-threaded BLAS; {dt:.0f} s for all three numbers",
             "one_core_frames_per_s": one["value"], "track_step_ms_median": ts}

@@ -90,10 +90,10 @@ def _truth(cfg, s, frames):
 _THREAD_VARS = ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS")
 
 
-def _worker(conn, cfg, s, frames):
+def _worker(conn, cfg, slices, frames):
     try:
         ref, _ = load_reference()
-        truth = _truth(cfg, s, frames)
+        truths = [_truth(cfg, s, frames) for s in slices]
         ecfg = adaptive_config(ref, cfg)
         conn.send(("ready", None))
         while True:
@@ -102,17 +102,18 @@ def _worker(conn, cfg, s, frames):
                 break
             nf = int(msg)
             t0 = time.perf_counter()
-            res = ref.experiment.run_adaptive(truth[..., :nf], ecfg)
+            nm = [float(ref.experiment.run_adaptive(tr[..., :nf], ecfg).metrics[-1].nmse) for tr in truths]
             dt = time.perf_counter() - t0
-            conn.send(("done", (dt, float(res.metrics[-1].nmse))))
+            conn.send(("done", (dt, nm[0])))
     except Exception as e:  # report, never hang the parent
         conn.send(("error", repr(e)))
 
 
 class WorkerPool:
-    """One process per slice (single BLAS thread each), truth resident in the worker."""
+    """``procs`` processes (single BLAS thread each) sharing the slices round-robin, each slice's truth
+    resident in its worker; a step runs every slice once."""
 
-    def __init__(self, cfg, slices, frames):
+    def __init__(self, cfg, slices, frames, procs):
         ctx = mp.get_context("spawn")
         self.conns, self.procs = [], []
         # one BLAS thread per worker: set before the children start (a spawned child imports numpy, and
@@ -120,9 +121,9 @@ class WorkerPool:
         saved = {k: os.environ.get(k) for k in _THREAD_VARS}
         os.environ.update({k: "1" for k in _THREAD_VARS})
         try:
-            for s in slices:
+            for w in range(procs):
                 a, b = ctx.Pipe()
-                p = ctx.Process(target=_worker, args=(b, cfg, s, frames), daemon=True)
+                p = ctx.Process(target=_worker, args=(b, cfg, list(slices[w::procs]), frames), daemon=True)
                 p.start()
                 self.conns.append(a)
                 self.procs.append(p)
@@ -196,13 +197,15 @@ def track_step_ms(cfg, frames=12):
 
 
 def measure(cfg, steps, warmup, max_slices=None):
-    """Slice-frames/s of the stock run_adaptive over ``min(slices, cores)`` concurrent slices for
-    the config's full T per step. Returns a dict for the bench line."""
+    """Slice-frames/s of the stock run_adaptive over the config's slices (all of them, or the first
+    ``max_slices``) for the config's T per step, one process per host core (at most one per slice).
+    Returns a dict for the bench line."""
     cores = host_cores()
     nsl = cfg.get("slices", 1)
-    take = max(1, min(nsl, cores if max_slices is None else max_slices))
+    take = max(1, min(nsl, nsl if max_slices is None else max_slices))
+    procs = max(1, min(take, cores))
     T = cfg["T"]
-    pool = WorkerPool(cfg, list(range(take)), T)
+    pool = WorkerPool(cfg, list(range(take)), T, procs)
     try:
         for _ in range(warmup):
             pool.step(min(T, 4))
@@ -214,5 +217,5 @@ def measure(cfg, steps, warmup, max_slices=None):
     finally:
         pool.close()
     total = sum(dts)
-    return dict(value=take * T * steps / total, ms_per_step=1e3 * total / steps, slices=take, cores=cores,
-                frames=T, last_nmse=nm)
+    return dict(value=take * T * steps / total, ms_per_step=1e3 * total / steps, slices=take, procs=procs,
+                cores=cores, frames=T, last_nmse=nm)

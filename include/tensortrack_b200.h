@@ -109,12 +109,14 @@ typedef struct tt_rows_args {
    * `shard_world` owns k-space rows [nx*rank/world, nx*(rank+1)/world) of Ah; ah_in/ah_out
    * then hold only those rows, Bh is replicated. Each frame is two launches:
    * phase 1 writes this rank's partial payload (xw: W = Y^T conj(Ah_S) [ny][rank]
-   * complex64; xg: packed GA (R(R+1)/2 complex128), ||Y||^2, ||Ah||^2 as doubles),
-   * the caller all-reduces xw and xg (sum) over the ranks, phase 2 solves
+   * complex128 (fp64 sums of exact products); xg: packed GA (R(R+1)/2 complex128), ||Y||^2,
+   * ||Ah||^2 as doubles), all doubles, so a caller that places xg right after xw
+   * (xg = xw + 2*ny*rank) all-reduces the frame's payload in ONE sum over the ranks
+   * (2*ny*rank + tt_rows_shard_xg_len(rank) doubles); phase 2 solves
    * redundantly and updates the owned rows and the replicated Bh. Static row
    * policy, nslices = 1, frames = 1 per launch. */
   int32_t shard_rank, shard_world, shard_phase;
-  float* xw;
+  double* xw;
   double* xg;
   /* Local multi-rank launch (appended; 0 = off): all shard_world ranks are clusters of one launch
    * on this GPU (shard_rank ignored). ah_in/ah_out/ah_hist hold all nx rows; xw/xg hold one
@@ -131,7 +133,7 @@ typedef struct tt_rows_args {
 /* doubles in the fp64 payload xg of a sharded launch */
 size_t tt_rows_shard_xg_len(int rank);
 /* sum the `world` payload slots of a local multi-rank phase-1 launch into slot 0 (fixed order) */
-int tt_rows_shard_reduce(void* stream, int world, int ny, int rank, float* xw, double* xg);
+int tt_rows_shard_reduce(void* stream, int world, int ny, int rank, double* xw, double* xg);
 
 /* Choose the cluster size (if *cluster <= 0) and report the dynamic shared
  * memory per CTA; TT_EUNSUPPORTED if no cluster size fits. */

@@ -773,6 +773,76 @@ TT_DEV void cgemm_tile(int M, int N, int K, const float2* A, int a_m, int a_k, c
   }
 }
 
+// Mixed-precision variant for the data GEMMs of the rows kernel (W = Y^T conj(Ah_S), Z = Y conj(Bh)):
+// fp32 complex operands in shared memory, converted on load, products and accumulation in fp64, so
+// every product of two fp32 values is exact and only the fp64 sums round. The updates subtract the
+// model part from W and Z (Q = W - Bh diag(g) GA^T, P = Z - Ah_S diag(g) GB^T); with a good fit the
+// difference is ~1e-2 of W, Z, so fp32 sums would lose two digits there. Same item /
+// K-split structure as cgemm_tile; `red` holds KS * M * N double2.
+template <int TM, int TN, bool CA, bool CB, typename Out>
+TT_DEV void zgemm_tile(int M, int N, int K, const float2* A, int a_m, int a_k, const float2* B, int b_k, int b_n,
+                       int KS, double2* red, Out out) {
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int tn = (N + TN - 1) / TN, tiles = ((M + TM - 1) / TM) * tn;
+  const int items = tiles * KS;
+  for (int it = tid; it < items; it += NT) {
+    const int ks = idiv(it, tiles), tile = it - ks * tiles;
+    const int mt = idiv(tile, tn);
+    const int m0 = mt * TM, n0 = (tile - mt * tn) * TN;
+    const int k0 = idiv(K * ks, KS), k1 = idiv(K * (ks + 1), KS);
+    double2 acc[TM][TN];
+#pragma unroll
+    for (int u = 0; u < TM; ++u)
+#pragma unroll
+      for (int v = 0; v < TN; ++v) acc[u][v] = make_double2(0.0, 0.0);
+    const float2* Ap[TM];
+    const float2* Bp[TN];
+#pragma unroll
+    for (int u = 0; u < TM; ++u) Ap[u] = A + (size_t)min(m0 + u, M - 1) * a_m;
+#pragma unroll
+    for (int v = 0; v < TN; ++v) Bp[v] = B + (size_t)min(n0 + v, N - 1) * b_n;
+#pragma unroll 2
+    for (int k = k0; k < k1; ++k) {
+      double2 a[TM], b[TN];
+#pragma unroll
+      for (int u = 0; u < TM; ++u) {
+        a[u] = to_d2(Ap[u][(size_t)k * a_k]);
+        if (CA) a[u].y = -a[u].y;
+      }
+#pragma unroll
+      for (int v = 0; v < TN; ++v) {
+        b[v] = to_d2(Bp[v][(size_t)k * b_k]);
+        if (CB) b[v].y = -b[v].y;
+      }
+#pragma unroll
+      for (int u = 0; u < TM; ++u)
+#pragma unroll
+        for (int v = 0; v < TN; ++v) acc[u][v] = zfma(a[u], b[v], acc[u][v]);
+    }
+#pragma unroll
+    for (int u = 0; u < TM; ++u)
+#pragma unroll
+      for (int v = 0; v < TN; ++v) {
+        const int m = m0 + u, n = n0 + v;
+        if (m < M && n < N) {
+          if (KS == 1) out(m, n, acc[u][v]);
+          else red[((size_t)ks * M + m) * N + n] = acc[u][v];
+        }
+      }
+  }
+  if (KS > 1) {
+    __syncthreads();
+    for (int o = tid; o < M * N; o += NT) {
+      double2 s = red[o];
+#pragma unroll
+      for (int ks = 1; ks < 8; ++ks)  // KS <= 8 (gemm_split): all partial loads in flight, fixed order
+        if (ks < KS) s = zadd(s, red[(size_t)ks * M * N + o]);
+      const int om = idiv(o, N);
+      out(om, o - om * N, s);
+    }
+  }
+}
+
 // Two independent GEMMs of the same shape class in one pass (cgemm_tile's items of both problems
 // spread over the block, one barrier, one fixed-order reduction pass for both): problem p is
 // C_p(m, n) = sum_k A_p[m*a_m + k] * conj(B_p[k*b_k + n]) (CB) with common N, K, strides and split KS;

@@ -47,6 +47,9 @@ namespace cg = cooperative_groups;
 // register tile of the small GEMMs (cgemm_tile): 4 rows x 2 columns of the output per thread beat 2 x 4
 // at every rows-kernel shape, same accumulator count (profiles/tools/ubench_gemm42.cu: C4 Z 27.6k -> 21.3k cycles)
 constexpr int GTM = 4, GTN = 2;
+// register tile of the fp64-accumulating data GEMMs (zgemm_tile): F2F conversions per k step = TM + TN
+// complex operands, DFMA = 4 TM TN
+constexpr int ZTM = 4, ZTN = 4;
 
 struct RowsPlan {
   int CL, KT, nIm, nJm, Rp, red_cap, tight;
@@ -71,7 +74,7 @@ __host__ __device__ inline RowsScratch rows_scratch_layout(int nx, int ny, int R
   s.ga = o;   o = al16(o + sizeof(double2) * Rp);
   s.sraw = o; o = al16(o + sizeof(double) * nx);
   s.ahs = o;  o = al16(o + sizeof(float2) * (size_t)Smax * R);
-  s.zp = o;   o = al16(o + sizeof(float2) * (size_t)CL * Smax * R);
+  s.zp = o;   o = al16(o + sizeof(double2) * (size_t)CL * Smax * R);  // Z partials, fp64
   s.hp = o;   o = al16(o + sizeof(double2) * CL * R);
   s.yn = o;   o = al16(o + sizeof(double) * CL);
   s.unif = o; o = al16(o + sizeof(double) * (size_t)ROWS_UF * Smax);  // Philox uniforms, ROWS_UF frames
@@ -93,7 +96,7 @@ static bool rows_make_plan(int nx, int ny, int R, int Smax, int CL, RowsPlan* p)
          rows_make_plan_cap(nx, ny, R, Smax, CL, 0, false, p) || rows_make_plan_cap(nx, ny, R, Smax, CL, 0, true, p);
 }
 static bool rows_make_plan_cap(int nx, int ny, int R, int Smax, int CL, int red_cap, bool tight, RowsPlan* p) {
-  const int maxsmem = 227 * 1024;
+  const int maxsmem = 227 * 1024 - 256;  // the opt-in limit less the kernel's static __shared__ words
   if (R > 64) return false;
   p->CL = CL;
   p->nIm = (nx + CL - 1) / CL;
@@ -126,9 +129,10 @@ static bool rows_make_plan_cap(int nx, int ny, int R, int Smax, int CL, int red_
   p->o_forced = (int)o; o = al16(o + sizeof(int) * Smax);
   p->o_usm = (int)o;    o = al16(o + sizeof(double) * Smax);  // this frame's uniforms
   p->o_own = (int)o;    o = al16(o + sizeof(int) * 2 * p->nIm);
-  p->o_wacc = (int)o;   o = al16(o + sizeof(float2) * p->nJm * R);
-  p->o_zs = (int)o;     o = al16(o + sizeof(float2) * p->nIm * R);
-  p->o_red2 = (int)o;   o = al16(o + sizeof(float2) * p->red_cap);
+  p->o_wacc = (int)o;   o = al16(o + sizeof(double2) * p->nJm * R);  // W (fp64 sums), then the new Bh rows
+  p->o_zs = (int)o;     o = al16(o + (tight ? 0 : sizeof(double2) * p->nIm * R));  // Z of owned rows, then mu conj(g) P
+                                                                                 // (tight plan: in U2, free after B4)
+  p->o_red2 = (int)o;   o = al16(o + sizeof(double2) * p->red_cap);  // K-split partials (fp64 or fp32)
   p->o_u2 = (int)o;
   size_t fixed = o + sizeof(double) * 64;
   if (fixed > (size_t)maxsmem) return false;
@@ -138,7 +142,8 @@ static bool rows_make_plan_cap(int nx, int ny, int R, int Smax, int CL, int red_
   const int gb_rt = (R + 1) / 2, gb_nt = gb_rt * (gb_rt + 1) / 2;
   size_t other = (tight ? 0 : sizeof(double2) * (size_t)p->nJm * R) +
                  4 * sizeof(double2) * (size_t)(gb_nt > 2 * ROWS_NT ? gb_nt : 2 * ROWS_NT) + sizeof(double) * ROWS_NT + 256;
-  const size_t v2 = tight ? 0 : sizeof(float2) * (size_t)R * (p->nJm + p->nIm);  // both gamma-scaled GEMM operands
+  const size_t v2 = tight ? sizeof(float2) * (size_t)R * p->nIm              // tight: the P increments
+                          : sizeof(float2) * (size_t)R * (p->nJm + p->nIm);  // both gamma-scaled GEMM operands
   if (v2 > other) other = v2;
   size_t avail = maxsmem - fixed;
   int KT = (int)(avail / (sizeof(float2) * (size_t)(p->nJm + R)));
@@ -159,35 +164,51 @@ static bool rows_make_plan_cap(int nx, int ny, int R, int Smax, int CL, int red_
 // ---------------------------------------------------------------- GEMM epilogues
 // The four small GEMMs of a frame share one cgemm_tile instantiation (one copy of its code in the
 // frame loop); the epilogue is selected by a block-uniform mode.
+// The data GEMMs (W, Z) accumulate in fp64 (zgemm_tile) and deliver double2; the model-part corrections
+// (K = R, fp32 operands: cgemm_tile) deliver float2 and are subtracted from the fp64 W / Z in fp64, so the
+// update keeps the digits the cancellation would cost in fp32.
 enum { EPI_W_ACC = 0, EPI_Z_STORE = 1, EPI_Q_UPDATE = 2, EPI_P_UPDATE = 3, EPI_P_MAPPED = 4 };
-struct RowsEpi {
+struct RowsEpiD {     // W / Z: fp64 values
   int mode, R;
-  float2* acc;          // W: wacc | Q: wacc (in: W, out: new Bh rows) | P: zs (in: Z sums, out: mu conj(g) P)
+  double2* acc;       // W: wacc
+  double2* gdst;      // Z: L2 partials
+  TT_DEV void operator()(int m, int n, double2 v) const {
+    const int o = m * R + n;
+    if (mode == EPI_W_ACC) {
+      acc[o] = zadd(acc[o], v);
+    } else {
+      __stcg(&gdst[o].x, v.x);
+      __stcg(&gdst[o].y, v.y);
+    }
+  }
+};
+struct RowsEpi {      // Q / P updates: fp32 correction v, fp64 arithmetic
+  int mode, R;
+  double2* acc;         // Q: wacc (in: W, out: new Bh rows) | P: zs (in: Z sums, out: mu conj(g) P)
   const float2* base;   // Q: bhl
-  float2* gdst;         // Z: L2 partials
-  const float2* gamf;
-  float cfac, muf;
+  const double2* gam;   // this frame's gamma (fp64)
+  double cfac, mu;
   const int* rmap;      // P_MAPPED (tight plan): local row -> position in the owned sampled rows, or -1
+  // P_MAPPED (tight plan): Z summed straight from the CTAs' fp64 partials in L2, the increment stored fp32
+  const int* own_k;
+  const double2* zp;
+  int zstride, CL;
+  float2* inc32;
   TT_DEV void operator()(int m, int n, float2 v) const {
     int o = m * R + n;
     switch (mode) {
-      case EPI_W_ACC:
-        acc[o] = cadd(acc[o], v);
-        break;
-      case EPI_Z_STORE:
-        __stcg(&gdst[o].x, v.x);
-        __stcg(&gdst[o].y, v.y);
-        break;
       case EPI_Q_UPDATE:
-        acc[o] = cadd(cscale(base[o], cfac), cscale(cmul(cconj(gamf[n]), csub(acc[o], v)), muf));
+        acc[o] = zadd(zscale(to_d2(base[o]), cfac), zscale(zmul(zconj(gam[n]), zsub(acc[o], to_d2(v))), mu));
         break;
-      case EPI_P_MAPPED:  // tight plan: the GEMM ran over every local row, keep the sampled ones
-        if (rmap[m] < 0) break;
-        o = rmap[m] * R + n;
-        acc[o] = cscale(cmul(cconj(gamf[n]), csub(acc[o], v)), muf);
+      case EPI_P_MAPPED: {  // tight plan: the GEMM ran over every local row, keep the sampled ones
+        const int q = rmap[m];
+        if (q < 0) break;
+        const double2 z = sum_parts2(zp + (size_t)own_k[q] * R + n, (size_t)zstride, CL);
+        inc32[q * R + n] = to_f2(zscale(zmul(zconj(gam[n]), zsub(z, to_d2(v))), mu));
         break;
+      }
       default:
-        acc[o] = cscale(cmul(cconj(gamf[n]), csub(acc[o], v)), muf);  // mu conj(g) P
+        acc[o] = zscale(zmul(zconj(gam[n]), zsub(acc[o], to_d2(v))), mu);  // mu conj(g) P
         break;
     }
   }
@@ -391,9 +412,11 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
   double* usm = (double*)(smem + pl.o_usm);
   int* own_k = (int*)(smem + pl.o_own);  // sampled rows owned by this CTA: measurement index
   int* own_li = own_k + pl.nIm;          // and local row
-  float2* wacc = (float2*)(smem + pl.o_wacc);
-  float2* zs = (float2*)(smem + pl.o_zs);
-  float2* red2 = (float2*)(smem + pl.o_red2);
+  double2* wacc = (double2*)(smem + pl.o_wacc);
+  double2* zs = (double2*)(smem + pl.o_zs);
+  float2* zs32 = (float2*)(smem + pl.o_u2);  // tight plan: the P increments (U2 is free from B4 on)
+  float2* red2 = (float2*)(smem + pl.o_red2);     // fp32 K-split partials (corrections)
+  double2* red2d = (double2*)(smem + pl.o_red2);  // fp64 K-split partials (W, Z)
   float2* ys = (float2*)(smem + pl.o_u2);
   float2* ahs = ys + (size_t)KT * pl.nJm;
   // phase (a) only: Bh in fp64 (not in the tight plan), GB partial tiles [parts][tiles][4], then the
@@ -425,7 +448,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
   double2* g_ga = (double2*)(sb + L.ga);
   double* g_sraw = (double*)(sb + L.sraw);
   float2* g_ahs = (float2*)(sb + L.ahs);
-  float2* g_zp = (float2*)(sb + L.zp);
+  double2* g_zp = (double2*)(sb + L.zp);
   double2* g_hp = (double2*)(sb + L.hp);
   double* g_yn = (double*)(sb + L.yn);
   double* g_unif = (double*)(sb + L.unif);
@@ -464,7 +487,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     // 0 full step, 1 partials -> payload, 2 payload -> update
     const int phase = !shard ? 0 : fused ? 1 + (it & 1) : a.shard_phase;
     const size_t xgl = (size_t)Rp * (fused ? 4 : 2) + 2;  // fused slots also carry GB: [GA][2 scalars][GB]
-    float2* xwp = (float2*)a.xw + (fused ? (size_t)(f & 1) * a.shard_world * ny * R : 0);
+    double2* xwp = (double2*)a.xw + (fused ? (size_t)(f & 1) * a.shard_world * ny * R : 0);
     double* xgp = a.xg + (fused ? (size_t)(f & 1) * a.shard_world * xgl : 0);
     auto xg_at = [&](size_t k) { return __ldcg(xgp + k); };  // the reduced payload (slot 0)
     const long long t = a.t0 + f;
@@ -750,7 +773,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         cp_async8(&ys[kk * pl.nJm + jj], ybase + (size_t)(gather ? rows[kk] : kk) * ny + jj);
       }
     }
-    for (int o = tid; o < nJ * R; o += NT) wacc[o] = make_float2(0.f, 0.f);
+    for (int o = tid; o < nJ * R; o += NT) wacc[o] = make_double2(0.0, 0.0);
     for (int e = eb + tid; e < ee; e += NT) G[e - eb] = make_double2(0.0, 0.0);
     __syncthreads();  // row marks visible to warp 0
     if (warp == 0) {  // compact the owned sampled rows (ascending local row)
@@ -782,6 +805,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       // the B3 window; B3 completes, Ah_S arrives and GA / W follow. Z and W share one GEMM call site.
       cp_async_wait_all();
       __syncthreads();
+      STAMP(16);
       for (int o = tid; o < S * nJ; o += NT) {
         const int kk = idiv(o, nJ), jj = o - kk * nJ;
         const float2 v = ys[kk * pl.nJm + jj];
@@ -814,14 +838,15 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
             g.y += __shfl_xor_sync(0xffffffffu, g.y, 2);
             if (part == 0 && eq < nq) G[e - eb] = zadd(G[e - eb], g);
           }
+          STAMP(18);
         }
         const int M = z ? S : nJ, Kd = z ? nJ : S;
-        const int ks = gemm_split(M, R, Kd, GTM, GTN, pl.red_cap);
-        const RowsEpi epi{z ? EPI_Z_STORE : EPI_W_ACC, R, wacc, nullptr, g_zp + (size_t)c * Smax * R, nullptr, 0.f,
-                          0.f};
-        cgemm_tile<GTM, GTN, false, true>(M, R, Kd, ys, z ? pl.nJm : 1, z ? 1 : pl.nJm, z ? bhl : ahs, R, 1, ks, red2,
-                                      epi);
+        const int ks = gemm_split(M, R, Kd, ZTM, ZTN, pl.red_cap);
+        const RowsEpiD epi{z ? EPI_Z_STORE : EPI_W_ACC, R, wacc, g_zp + (size_t)c * Smax * R};
+        zgemm_tile<ZTM, ZTN, false, true>(M, R, Kd, ys, z ? pl.nJm : 1, z ? 1 : pl.nJm, z ? bhl : ahs, R, 1, ks, red2d,
+                                          epi);
         __syncthreads();
+        STAMP(z ? 17 : 19);
       }
     } else {
       cluster_wait();  // ---------------------------------------------------- B3 complete
@@ -878,11 +903,10 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       for (int gsel = 0; gsel < 2; ++gsel) {
         const bool w = gsel == 0;
         const int M = w ? nJ : kt, Kd = w ? kt : nJ;
-        const int ks = gemm_split(M, R, Kd, GTM, GTN, pl.red_cap);
-        const RowsEpi epi{w ? EPI_W_ACC : EPI_Z_STORE, R, wacc, nullptr, g_zp + ((size_t)c * Smax + k0) * R,
-                          nullptr, 0.f, 0.f};
-        cgemm_tile<GTM, GTN, false, true>(M, R, Kd, ys, w ? 1 : pl.nJm, w ? pl.nJm : 1, w ? ahs : bhl, R, 1, ks, red2,
-                                      epi);
+        const int ks = gemm_split(M, R, Kd, ZTM, ZTN, pl.red_cap);
+        const RowsEpiD epi{w ? EPI_W_ACC : EPI_Z_STORE, R, wacc, g_zp + ((size_t)c * Smax + k0) * R};
+        zgemm_tile<ZTM, ZTN, false, true>(M, R, Kd, ys, w ? 1 : pl.nJm, w ? pl.nJm : 1, w ? ahs : bhl, R, 1, ks, red2d,
+                                          epi);
         if (w) __syncthreads();  // the K-split buffer is reused
       }
       if (k0 == 0) STAMP(18);
@@ -892,7 +916,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     STAMP(8);
     if (phase == 1) {
       // this rank's partials -> payload (the caller all-reduces xw and xg across ranks)
-      float2* xw1 = xwp + (multi ? (size_t)qid * ny * R : 0);  // this rank's payload slot
+      double2* xw1 = xwp + (multi ? (size_t)qid * ny * R : 0);  // this rank's payload slot
       double* xg1 = xgp + (multi ? (size_t)qid * xgl : 0);
       for (int o = tid; o < nJ * R; o += NT) xw1[(size_t)j0 * R + o] = wacc[o];
       for (int e = eb + tid; e < ee; e += NT) {
@@ -917,7 +941,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         // split over all CTAs of the launch (four elements per thread in flight) -> phase 2
         grid_sync(a.grid_sync, gsync_gen);
         const size_t nw = 2 * (size_t)ny * R, ntot = nw + xgl, step = (size_t)gridDim.x * NT;
-        float* xwf = (float*)xwp;
+        double* xwf = (double*)xwp;
         for (size_t i0r = (size_t)blockIdx.x * NT + tid; i0r < ntot; i0r += 4 * step) {
           double v[4];
 #pragma unroll
@@ -925,7 +949,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
             const size_t i = i0r + u * step;
             v[u] = 0.0;
             if (i < nw) {
-              float x = __ldcg(xwf + i);
+              double x = __ldcg(xwf + i);
               for (int r = 1; r < a.shard_world; ++r) x += __ldcg(xwf + (size_t)r * nw + i);
               v[u] = x;
             } else if (i < ntot) {
@@ -938,7 +962,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const size_t i = i0r + u * step;
-            if (i < nw) __stcg(xwf + i, (float)v[u]);
+            if (i < nw) __stcg(xwf + i, v[u]);
             else if (i < ntot) __stcg(xgp + (i - nw), v[u]);
           }
         }
@@ -947,7 +971,10 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       continue;  // phase 2 finishes the frame after the all-reduce
     }
     if (phase == 2)  // reduced W of this CTA's columns
-      for (int o = tid; o < nJ * R; o += NT) wacc[o] = __ldcg(xwp + (size_t)j0 * R + o);
+      for (int o = tid; o < nJ * R; o += NT) {
+        const double2* src = xwp + (size_t)j0 * R + o;
+        wacc[o] = make_double2(__ldcg(&src->x), __ldcg(&src->y));
+      }
     __syncthreads();
     // h partial: sum_jj conj(Bh[jj][r]) W[jj][r], all threads: (column r, part) then a fixed-order sum
     {
@@ -958,7 +985,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       if (tid < hparts * R) {
         const int r = tid % R, part = tid / R;
         double2 h = make_double2(0.0, 0.0);
-        for (int jj = part; jj < nJ; jj += hparts) h = zfma_cj(bhl[jj * R + r], wacc[jj * R + r], h);
+        for (int jj = part; jj < nJ; jj += hparts) h = zfma_cj(to_d2(bhl[jj * R + r]), wacc[jj * R + r], h);
         hpart[part * R + r] = h;
       }
       __syncthreads();
@@ -992,7 +1019,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     }
     for (int o = tid; o < nown * R; o += NT) {
       const int m = idiv(o, R), r = o - m * R;
-      zs[o] = sum_parts_f2(g_zp + (size_t)own_k[m] * R + r, (size_t)Smax * R, CL);
+      if (!TIGHT) zs[o] = sum_parts2(g_zp + (size_t)own_k[m] * R + r, (size_t)Smax * R, CL);
     }
     {
       const int hr = tid - (NT - R);
@@ -1111,8 +1138,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     // ======== (e) updates (k-space): Bh <- cfac Bh + mu conj(g) (W - Bh diag(g) GA^T)
     //                                 Ah_S <- cfac Ah_S + mu conj(g) (Z - Ah_S diag(g) GB^T)
     if (update) {
-      const float cfac = (float)(1.0 - mu_used * lt);
-      const float muf = (float)mu_used;
+      const double cfac_d = 1.0 - mu_used * lt;
       if (TIGHT) {
         // one correction at a time, the gamma scaling moved onto the R x R factor:
         // corr[m][r] = sum_q X[m][q] conj(conj(g_q) G[q][r]) with (X, G) = (Bh, GA) then (Ah, GB)
@@ -1138,7 +1164,8 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
           }
           __syncthreads();
           const int M = q ? nJ : (nown > 0 ? nI : 0);
-          const RowsEpi epi{q ? EPI_Q_UPDATE : EPI_P_MAPPED, R, q ? wacc : zs, bhl, nullptr, gamf, cfac, muf, flags};
+          const RowsEpi epi{q ? EPI_Q_UPDATE : EPI_P_MAPPED, R, wacc, bhl, gam, cfac_d, mu_used, flags,
+                            own_k, g_zp, Smax * R, CL, zs32};
           cgemm_tile<GTM, GTN, false, true>(M, R, R, q ? bhl : ahl, R, 1, mq, R, 1, 1, red2, epi);
           __syncthreads();
         }
@@ -1161,8 +1188,8 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
           ks = min(ks, min(R / 4, 8));
           while (ks > 1 && ks * (nJ + nown) * R > pl.red_cap) --ks;
           ks = max(ks, 1);
-          const RowsEpi eq{EPI_Q_UPDATE, R, wacc, bhl, nullptr, gamf, cfac, muf};
-          const RowsEpi ep{EPI_P_UPDATE, R, zs, bhl, nullptr, gamf, cfac, muf};
+          const RowsEpi eq{EPI_Q_UPDATE, R, wacc, bhl, gam, cfac_d, mu_used, nullptr};
+          const RowsEpi ep{EPI_P_UPDATE, R, zs, bhl, gam, cfac_d, mu_used, nullptr};
           cgemm_tile_pair<GTM, GTN, false, true>(nJ, nown, R, R, vop, vop2, R, 1, gaf, gbf, R, 1, ks, red2, eq, ep);
           __syncthreads();
         }
@@ -1171,12 +1198,12 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       STAMP(23);
       for (int o = tid; o < nI * R; o += NT) {
         const int li = idiv(o, R), r = o - li * R;
-        float2 v = cscale(ahl[o], cfac);
+        double2 v = zscale(to_d2(ahl[o]), cfac_d);
         const int m = flags[li];
-        if (m >= 0) v = cadd(v, zs[m * R + r]);
-        ahl[o] = v;
+        if (m >= 0) v = zadd(v, TIGHT ? to_d2(zs32[m * R + r]) : zs[m * R + r]);
+        ahl[o] = to_f2(v);
       }
-      for (int o = tid; o < nJ * R; o += NT) bhl[o] = wacc[o];
+      for (int o = tid; o < nJ * R; o += NT) bhl[o] = to_f2(wacc[o]);
       __syncthreads();
     }
     STAMP(14);
@@ -1256,10 +1283,10 @@ extern "C" size_t tt_rows_shard_xg_len(int rank) { return (size_t)rank * (rank +
 
 // Sum the payload slots of a local multi-rank launch into slot 0 (fixed order over ranks): the
 // on-device counterpart of the all-reduce between the two phases.
-__global__ void shard_reduce_kernel(int world, size_t nw, size_t ng, float* __restrict__ xw, double* __restrict__ xg) {
+__global__ void shard_reduce_kernel(int world, size_t nw, size_t ng, double* __restrict__ xw, double* __restrict__ xg) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nw + ng; i += (size_t)gridDim.x * blockDim.x) {
     if (i < nw) {
-      float v = xw[i];
+      double v = xw[i];
       for (int r = 1; r < world; ++r) v += xw[(size_t)r * nw + i];
       xw[i] = v;
     } else {
@@ -1271,7 +1298,7 @@ __global__ void shard_reduce_kernel(int world, size_t nw, size_t ng, float* __re
   }
 }
 
-extern "C" int tt_rows_shard_reduce(void* stream, int world, int ny, int rank, float* xw, double* xg) {
+extern "C" int tt_rows_shard_reduce(void* stream, int world, int ny, int rank, double* xw, double* xg) {
   if (world < 1 || ny < 1 || rank < 1 || !xw || !xg) return tt_fail(TT_EINVAL, "tt_rows_shard_reduce: bad args");
   if (world == 1) return TT_OK;
   const size_t nw = 2 * (size_t)ny * rank, ng = (size_t)rank * (rank + 1) + 2;

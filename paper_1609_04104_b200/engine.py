@@ -740,7 +740,7 @@ class LocalShardedEngine:
         self.xg_len = int(L.lib().tt_rows_shard_xg_len(self.R))
         self.fused = bool(fused)
         sets = 2 if self.fused else 1  # the fused launch double-buffers the payload by frame parity
-        self.xw = torch.zeros(sets * self.ranks, self.ny, self.R, dtype=torch.complex64, device=self.dev)
+        self.xw = torch.zeros(sets * self.ranks, self.ny, self.R, dtype=torch.complex128, device=self.dev)
         # fused slots also carry the ranks' GB partials: [GA packed][||Y||^2, ||Ah||^2][GB packed]
         slot = 2 * self.xg_len - 2 if self.fused else self.xg_len
         self.xg = torch.zeros(sets * self.ranks, slot, dtype=torch.float64, device=self.dev)
@@ -1065,8 +1065,12 @@ class RowShardedEngine:
         self.cluster = self.scr.cluster
         self.ah = torch.zeros(self.r1 - self.r0, self.R, dtype=torch.complex64, device=self.dev)
         self.bh = torch.zeros(self.ny, self.R, dtype=torch.complex64, device=self.dev)
-        self.xw = torch.empty(self.ny, self.R, dtype=torch.complex64, device=self.dev)
-        self.xg = torch.empty(int(L.lib().tt_rows_shard_xg_len(self.R)), dtype=torch.float64, device=self.dev)
+        # the frame's payload in one fp64 buffer: W (ny x R complex128) then GA / ||Y||^2 / ||Ah||^2, so one
+        # all-reduce per frame carries all of it
+        nw = 2 * self.ny * self.R
+        self.payload = torch.zeros(nw + int(L.lib().tt_rows_shard_xg_len(self.R)), dtype=torch.float64, device=self.dev)
+        self.xw = self.payload[:nw].view(torch.complex128).view(self.ny, self.R)
+        self.xg = self.payload[nw:]
         self.alpha_bar = torch.zeros(1, dtype=torch.float64, device=self.dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.t = int(t0)
@@ -1136,7 +1140,6 @@ class RowShardedEngine:
         for fo in range(frames):
             f = self.frame
             self.partial(kspace, f)
-            self.allreduce(self.xw.view(torch.float32))
-            self.allreduce(self.xg)
+            self.allreduce(self.payload)  # one sum over the ranks per frame
             self.finish(kspace, f, out, fo)
         return out

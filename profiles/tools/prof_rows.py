@@ -36,14 +36,19 @@ clk = torch.zeros(T, 32, dtype=torch.int64, device='cuda')
 args.phase_clock = clk.data_ptr()
 eng.philox_pos.zero_(); K.track_rows(args); torch.cuda.synchronize()
 c = clk.cpu().numpy().astype(np.int64)
-names = {26:"a:colnorm",1:"a-partials",2:"B1",24:"s:nrm",25:"s:usm",27:"s:sync",28:"s:ahnorm",3:"s:scores",4:"B2",29:"b:scan+cdf",30:"b:draws",31:"b:union",20:"b:end",5:"draw",6:"publishAhS",7:"B3",16:"h:tileload",17:"h:W",18:"h:Z",19:"h:GA",8:"heavy-rest",9:"h/ga/yn",10:"B4",11:"Gbuild",12:"solve",13:"cost/mu",21:"u:mark",22:"u:P",23:"u:Q",14:"update",15:"outputs"}
-order = [0,26,1,2,24,25,27,28,3,4,29,30,31,20,5,6,7,16,17,18,19,8,9,10,11,12,13,21,22,23,14,15]
+names = {0: "frame start", 26: "a:colnorm", 1: "a-partials", 2: "B1", 24: "s:nrm", 25: "s:usm", 27: "s:sync",
+         28: "s:ahnorm", 3: "s:scores", 4: "B2", 29: "b:scan+cdf", 30: "b:draws", 31: "b:union", 20: "b:end", 5: "draw",
+         6: "publishAhS", 7: "B3 complete", 16: "h:tile landed", 17: "h:Z (one tile) / W", 18: "h:Ah_S + GA",
+         19: "h:W (one tile) / Z", 8: "heavy-rest", 9: "h/ga/yn", 10: "B4", 11: "Gbuild", 12: "solve", 13: "cost/mu",
+         21: "u:mark", 22: "u:P", 23: "u:Q", 14: "update", 15: "outputs"}
 cc = c[5:]
-print("cycles per phase (median over frames 5..):")
-prev = None
-for k in order:
-    if prev is not None and (cc[:, k] > 0).all():
-        print(f"  {names.get(k, k):12s} {int(np.median(cc[:, k] - cc[:, prev])):7d}")
-    if (cc[:, k] > 0).all(): prev = k
+# stamps present in every frame, ordered by their median offset from the frame start (the one-tile and the
+# k-tiled heavy phases stamp 16-19 on different sides of B3)
+ks = [k for k in range(32) if (cc[:, k] > 0).all()]
+off = {k: np.median(cc[:, k] - cc[:, 0]) for k in ks}
+ks.sort(key=lambda k: off[k])
+print("cycles per phase (median over frames 5.., each row = time since the previous stamp):")
+for p_, k in zip(ks, ks[1:]):
+    print(f"  {names.get(k, k):22s} {int(np.median(cc[:, k] - cc[:, p_])):7d}")
 fr = np.median(np.diff(cc[:, 0]))
 print("frame total", fr, "cycles =", fr / 1.965e3, "us at 1965 MHz")
