@@ -130,6 +130,9 @@ typedef struct tt_rows_args {
   int32_t shard_fused;
   uint32_t* grid_sync;
 } tt_rows_args;
+/* plan of a row-mask launch at `cluster` (0: smallest that fits): out[6] = cluster, rows per k tile,
+ * shared-memory bytes, tight plan (0/1), padded Y row stride, K-split buffer entries (diagnostics) */
+int tt_rows_plan_info(int nx, int ny, int rank, int max_rows, int cluster, int* out);
 /* doubles in the fp64 payload xg of a sharded launch */
 size_t tt_rows_shard_xg_len(int rank);
 /* sum the `world` payload slots of a local multi-rank phase-1 launch into slot 0 (fixed order) */

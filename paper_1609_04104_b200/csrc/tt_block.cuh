@@ -22,6 +22,36 @@ TT_DEV void cp_async4(void* smem, const void* gmem) {
 }
 TT_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
+// mbarrier + bulk-copy (TMA) helpers: a row of Y is one cp.async.bulk of contiguous bytes into shared
+// memory, completion counted in bytes on an mbarrier (one arrival per phase: the issuing lane's
+// arrive.expect_tx), every consumer thread waits on the phase parity.
+TT_DEV unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+TT_DEV void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+TT_DEV void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+TT_DEV void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "TT_MBW_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra TT_MBW_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// generic-proxy accesses of shared memory ordered before later async-proxy (bulk copy) accesses
+TT_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+TT_DEV void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 // packed lower-triangular index helpers (r >= q)
 TT_DEV void tri_decode(int e, int& r, int& q) {
   int rr = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
@@ -268,6 +298,21 @@ TT_DEV double2 sum_parts2(const double2* p, size_t stride, int CL) {
   double2 s = make_double2(0.0, 0.0);
 #pragma unroll
   for (int c = 0; c < 16; ++c) s = zadd(s, v[c]);
+  return s;
+}
+// Any number of parts (the Z partials: CL CTAs x K parts): batches of 16 loads in flight, fixed order.
+TT_DEV double2 sum_parts2n(const double2* p, size_t stride, int n) {
+  double2 s = make_double2(0.0, 0.0);
+  for (int c0 = 0; c0 < n; c0 += 16) {
+    double2 v[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      v[c].x = c0 + c < n ? __ldcg(&p[(size_t)(c0 + c) * stride].x) : 0.0;
+      v[c].y = c0 + c < n ? __ldcg(&p[(size_t)(c0 + c) * stride].y) : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < 16; ++c) s = zadd(s, v[c]);
+  }
   return s;
 }
 TT_DEV float2 sum_parts_f2(const float2* p, size_t stride, int CL) {
@@ -839,6 +884,155 @@ TT_DEV void zgemm_tile(int M, int N, int K, const float2* A, int a_m, int a_k, c
         if (ks < KS) s = zadd(s, red[(size_t)ks * M * N + o]);
       const int om = idiv(o, N);
       out(om, o - om * N, s);
+    }
+  }
+}
+
+// zgemm_tile with the B operand already in fp64 (the rows kernel keeps fp64 copies of the resident Bh
+// rows and of the frame's Ah_S rows, so only the Y operand is converted on load: TM conversions per k step
+// for TM * TN complex products). PARTS: every K part is delivered as it is, out(m, n, ks, value), for a
+// consumer that sums the parts later in a fixed order (the cluster's Z partials); otherwise the KS > 1
+// parts are summed through `red` (KS * M * N double2) and delivered once, out(m, n, 0, value).
+TT_DEV double2 ld_d2(const double2* p) { return *p; }
+TT_DEV double2 ld_d2(const float2* p) { return to_d2(*p); }
+template <int TM, int TN, bool CB, bool PARTS, typename BT, typename Out>
+TT_DEV void zgemm_fd(int M, int N, int K, const float2* A, int a_m, int a_k, const BT* B, int b_k, int b_n,
+                     int KS, double2* red, Out out) {
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int tn = (N + TN - 1) / TN, tiles = ((M + TM - 1) / TM) * tn;
+  const int items = tiles * KS;
+  for (int it = tid; it < items; it += NT) {
+    const int ks = idiv(it, tiles), tile = it - ks * tiles;
+    const int mt = idiv(tile, tn);
+    const int m0 = mt * TM, n0 = (tile - mt * tn) * TN;
+    const int k0 = idiv(K * ks, KS), k1 = idiv(K * (ks + 1), KS);
+    double2 acc[TM][TN];
+#pragma unroll
+    for (int u = 0; u < TM; ++u)
+#pragma unroll
+      for (int v = 0; v < TN; ++v) acc[u][v] = make_double2(0.0, 0.0);
+    const float2* Ap[TM];
+    const BT* Bp[TN];
+#pragma unroll
+    for (int u = 0; u < TM; ++u) Ap[u] = A + (size_t)min(m0 + u, M - 1) * a_m + (size_t)k0 * a_k;
+#pragma unroll
+    for (int v = 0; v < TN; ++v) Bp[v] = B + (size_t)min(n0 + v, N - 1) * b_n + (size_t)k0 * b_k;
+    // software pipeline: the shared-memory loads of step k+1 are in flight while step k's DFMAs issue
+    // (two resident warps per scheduler cannot hide the load + F2F latency on their own)
+    float2 an[TM];
+    BT bn[TN];
+    if (k0 < k1) {
+#pragma unroll
+      for (int u = 0; u < TM; ++u) an[u] = *Ap[u];
+#pragma unroll
+      for (int v = 0; v < TN; ++v) bn[v] = *Bp[v];
+    }
+    for (int k = k0; k < k1; ++k) {
+      double2 a[TM], b[TN];
+#pragma unroll
+      for (int u = 0; u < TM; ++u) a[u] = to_d2(an[u]);
+#pragma unroll
+      for (int v = 0; v < TN; ++v) {
+        b[v] = ld_d2(&bn[v]);
+        if (CB) b[v].y = -b[v].y;
+      }
+      if (k + 1 < k1) {
+#pragma unroll
+        for (int u = 0; u < TM; ++u) {
+          Ap[u] += a_k;
+          an[u] = *Ap[u];
+        }
+#pragma unroll
+        for (int v = 0; v < TN; ++v) {
+          Bp[v] += b_k;
+          bn[v] = *Bp[v];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < TM; ++u)
+#pragma unroll
+        for (int v = 0; v < TN; ++v) acc[u][v] = zfma(a[u], b[v], acc[u][v]);
+    }
+#pragma unroll
+    for (int u = 0; u < TM; ++u)
+#pragma unroll
+      for (int v = 0; v < TN; ++v) {
+        const int m = m0 + u, n = n0 + v;
+        if (m < M && n < N) {
+          if (PARTS || KS == 1) out(m, n, PARTS ? ks : 0, acc[u][v]);
+          else red[((size_t)ks * M + m) * N + n] = acc[u][v];
+        }
+      }
+  }
+  if (!PARTS && KS > 1) {
+    __syncthreads();
+    for (int o = tid; o < M * N; o += NT) {
+      double2 s = red[o];
+#pragma unroll
+      for (int ks = 1; ks < 8; ++ks)
+        if (ks < KS) s = zadd(s, red[(size_t)ks * M * N + o]);
+      const int om = idiv(o, N);
+      out(om, o - om * N, 0, s);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- fp64 tensor-core (DMMA) complex GEMM
+// C(m, r) = sum_k A(m, k) conj(B(k, r)) with A fp32 complex (converted: products exact), B fp64 complex,
+// on mma.sync m8n8k4 f64 (the B200's fp64 matrix path: the same peak as DFMA at a fraction of the issued
+// instructions). The complex product is a real GEMM with interleaved (re, im) K and N: output column
+// n = 2r + q; for k = 4t + kq two K slots per complex k, the A (re) slot with B coefficient (b.x, -b.y)
+// and the A (im) slot with (b.y, b.x) — so a lane loads one float2 of A and one double2 of B per complex
+// k and feeds two DMMAs. A lane of an 8x8 output block then holds C(m0 + lane/4, r0 + lane%4) as one
+// complex value. Work item = (group of G 8-row M blocks, one 4-wide r block, K part); warps take items
+// round-robin. PARTS: each K part delivered as it is, out(m, r, ks, value); else KS must be 1.
+TT_DEV void dmma_m8n8k4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+template <int G, typename Out>
+TT_DEV void zgemm_dmma(int M, int R, int K, const float2* A, int a_m, int a_k, const double2* B, int b_k, int KS,
+                       Out out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int row = lane >> 2, kq = lane & 3;
+  const int MB = (M + 7) >> 3, NB = (R + 3) >> 2, MG = (MB + G - 1) / G;
+  const int kpairs = (K + 3) >> 2;
+  const int items = MG * NB * KS;
+  for (int it = warp; it < items; it += nw) {
+    const int ks = idiv(it, MG * NB), rest = it - ks * MG * NB;
+    const int mg = idiv(rest, NB), nb = rest - mg * NB;
+    const int t0 = idiv(kpairs * ks, KS), t1 = idiv(kpairs * (ks + 1), KS);
+    const int col = row;  // B fragment column of this lane: n = nb * 8 + col
+    const int rb = nb * 4 + (col >> 1), q = col & 1;
+    double acc[G][2];
+#pragma unroll
+    for (int g = 0; g < G; ++g) acc[g][0] = acc[g][1] = 0.0;
+    for (int t = t0; t < t1; ++t) {
+      const int k = 4 * t + kq;
+      double2 b = make_double2(0.0, 0.0);
+      if (k < K && rb < R) b = B[(size_t)k * b_k + rb];
+      const double b0 = q == 0 ? b.x : -b.y, b1 = q == 0 ? b.y : b.x;
+      double ar[G], ai[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const int m = ((mg * G + g) << 3) + row;
+        float2 a = make_float2(0.f, 0.f);
+        if (m < M && k < K) a = A[(size_t)m * a_m + (size_t)k * a_k];
+        ar[g] = (double)a.x;
+        ai[g] = (double)a.y;
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        dmma_m8n8k4(acc[g][0], acc[g][1], ar[g], b0);
+        dmma_m8n8k4(acc[g][0], acc[g][1], ai[g], b1);
+      }
+    }
+    const int r = nb * 4 + kq;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int m = ((mg * G + g) << 3) + row;
+      if ((mg * G + g) < MB && m < M && r < R) out(m, r, ks, make_double2(acc[g][0], acc[g][1]));
     }
   }
 }

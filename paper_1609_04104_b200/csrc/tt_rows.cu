@@ -44,16 +44,18 @@ namespace cg = cooperative_groups;
 
 #define ROWS_NT 256
 #define ROWS_UF 32  // frames of precomputed Philox uniforms per refill
+#define ROWS_ZKS 8  // K parts of the Z GEMM per CTA (fp64 partials in L2, summed by the rows' owners)
 // register tile of the small GEMMs (cgemm_tile): 4 rows x 2 columns of the output per thread beat 2 x 4
 // at every rows-kernel shape, same accumulator count (profiles/tools/ubench_gemm42.cu: C4 Z 27.6k -> 21.3k cycles)
 constexpr int GTM = 4, GTN = 2;
 // register tile of the fp64-accumulating data GEMMs (zgemm_tile): F2F conversions per k step = TM + TN
 // complex operands, DFMA = 4 TM TN
-constexpr int ZTM = 4, ZTN = 4;
+constexpr int ZTM = 2, ZTN = 4;
+constexpr int ZG = 4;  // 8-row M blocks per DMMA work item (zgemm_dmma)
 
 struct RowsPlan {
-  int CL, KT, nIm, nJm, Rp, red_cap, tight;
-  int o_ahl, o_bhl, o_u1, o_gaf, o_gbf, o_vec, o_tab, o_flags, o_rows, o_forced, o_usm, o_own, o_wacc, o_zs, o_red2,
+  int CL, KT, nIm, nJm, Rp, red_cap, tight, ysr;
+  int o_ahl, o_bhl, o_bh64, o_u1, o_gaf, o_gbf, o_vec, o_tab, o_flags, o_rows, o_forced, o_usm, o_own, o_wacc, o_zs, o_red2,
       o_u2, o_red;
   int smem;
 };
@@ -74,7 +76,7 @@ __host__ __device__ inline RowsScratch rows_scratch_layout(int nx, int ny, int R
   s.ga = o;   o = al16(o + sizeof(double2) * Rp);
   s.sraw = o; o = al16(o + sizeof(double) * nx);
   s.ahs = o;  o = al16(o + sizeof(float2) * (size_t)Smax * R);
-  s.zp = o;   o = al16(o + sizeof(double2) * (size_t)CL * Smax * R);  // Z partials, fp64
+  s.zp = o;   o = al16(o + sizeof(double2) * (size_t)CL * ROWS_ZKS * Smax * R);  // Z partials [CTA][K part], fp64
   s.hp = o;   o = al16(o + sizeof(double2) * CL * R);
   s.yn = o;   o = al16(o + sizeof(double) * CL);
   s.unif = o; o = al16(o + sizeof(double) * (size_t)ROWS_UF * Smax);  // Philox uniforms, ROWS_UF frames
@@ -92,8 +94,23 @@ static bool rows_make_plan_cap(int nx, int ny, int R, int Smax, int CL, int red_
 static bool rows_make_plan(int nx, int ny, int R, int Smax, int CL, RowsPlan* p) {
   if (const char* e = getenv("TT_ROWS_FORCE_TIGHT"))  // test hook: the tight plan at any shape (R >= 24)
     if (e[0] == '1' && R >= 24) return rows_make_plan_cap(nx, ny, R, Smax, CL, 0, true, p);
-  return rows_make_plan_cap(nx, ny, R, Smax, CL, 2048, false, p) ||
-         rows_make_plan_cap(nx, ny, R, Smax, CL, 0, false, p) || rows_make_plan_cap(nx, ny, R, Smax, CL, 0, true, p);
+  // prefer the K-split buffer, but not at the cost of a second k tile of Y rows (the one-tile path overlaps the
+  // Z partial with the cluster's Ah_S exchange)
+  RowsPlan q;
+  const bool with_red = rows_make_plan_cap(nx, ny, R, Smax, CL, 2048, false, &q);
+  if (with_red && q.KT >= Smax) {
+    *p = q;
+    return true;
+  }
+  if (rows_make_plan_cap(nx, ny, R, Smax, CL, 0, false, p)) {
+    if (with_red && q.KT > p->KT) *p = q;
+    return true;
+  }
+  if (with_red) {
+    *p = q;
+    return true;
+  }
+  return rows_make_plan_cap(nx, ny, R, Smax, CL, 0, true, p);
 }
 static bool rows_make_plan_cap(int nx, int ny, int R, int Smax, int CL, int red_cap, bool tight, RowsPlan* p) {
   const int maxsmem = 227 * 1024 - 256;  // the opt-in limit less the kernel's static __shared__ words
@@ -107,6 +124,7 @@ static bool rows_make_plan_cap(int nx, int ny, int R, int Smax, int CL, int red_
   size_t o = 0;
   p->o_ahl = (int)o;    o = al16(o + sizeof(float2) * p->nIm * R);
   p->o_bhl = (int)o;    o = al16(o + sizeof(float2) * p->nJm * R);
+  p->o_bh64 = (int)o;   o = al16(o + (tight ? 0 : sizeof(double2) * p->nJm * R));  // fp64 copy of the Bh rows
   p->o_u1 = (int)o;     // packed fp64 Gram / LDL workspace  |  p + cdf (draw phase)  |  tight: update operand
   {
     size_t g = sizeof(double2) * (size_t)p->Rp;
@@ -130,28 +148,31 @@ static bool rows_make_plan_cap(int nx, int ny, int R, int Smax, int CL, int red_
   p->o_usm = (int)o;    o = al16(o + sizeof(double) * Smax);  // this frame's uniforms
   p->o_own = (int)o;    o = al16(o + sizeof(int) * 2 * p->nIm);
   p->o_wacc = (int)o;   o = al16(o + sizeof(double2) * p->nJm * R);  // W (fp64 sums), then the new Bh rows
-  p->o_zs = (int)o;     o = al16(o + (tight ? 0 : sizeof(double2) * p->nIm * R));  // Z of owned rows, then mu conj(g) P
+  p->o_zs = (int)o;     o = al16(o + (tight ? 0 : sizeof(double2) * (p->nIm < Smax ? p->nIm : Smax) * R));  // Z of
+                                                                                 // owned sampled rows, then mu conj(g) P
                                                                                  // (tight plan: in U2, free after B4)
   p->o_red2 = (int)o;   o = al16(o + sizeof(double2) * p->red_cap);  // K-split partials (fp64 or fp32)
   p->o_u2 = (int)o;
   size_t fixed = o + sizeof(double) * 64;
   if (fixed > (size_t)maxsmem) return false;
-  // U2: k-tiles (ys KT x nJm, ahs KT x R) | Bh in fp64 + colnorm partials (phase a) | gamma-scaled GEMM operands
-  // phase (a): Bh in fp64 (not in the tight plan) + GB partial tiles (4 double2 per item, <= max(2 NT,
-  // tiles) items) + colnorm partials (<= NT doubles); the h partials later (<= NT double2)
+  // U2: k-tiles (ys KT x ysr fp32, ahs KT x R fp64) | GB partial tiles + colnorm partials (phase a) |
+  // gamma-scaled GEMM operands. Phase (a): GB partial tiles (4 double2 per item, <= max(2 NT, tiles) items)
+  // + colnorm partials (<= NT doubles); the h partials later (<= NT double2)
   const int gb_rt = (R + 1) / 2, gb_nt = gb_rt * (gb_rt + 1) / 2;
-  size_t other = (tight ? 0 : sizeof(double2) * (size_t)p->nJm * R) +
-                 4 * sizeof(double2) * (size_t)(gb_nt > 2 * ROWS_NT ? gb_nt : 2 * ROWS_NT) + sizeof(double) * ROWS_NT + 256;
+  size_t other = 4 * sizeof(double2) * (size_t)(gb_nt > 2 * ROWS_NT ? gb_nt : 2 * ROWS_NT) + sizeof(double) * ROWS_NT + 256;
+  // Y tile row stride = 4 (mod 16) complex: 16 B aligned rows (bulk copies), 8 banks apart (the Z GEMM's
+  // DMMA A fragments read 4 consecutive columns of 8 rows: conflict-free)
+  p->ysr = ((p->nJm + 11) & ~15) + 4;
   const size_t v2 = tight ? sizeof(float2) * (size_t)R * p->nIm              // tight: the P increments
                           : sizeof(float2) * (size_t)R * (p->nJm + p->nIm);  // both gamma-scaled GEMM operands
   if (v2 > other) other = v2;
   size_t avail = maxsmem - fixed;
-  int KT = (int)(avail / (sizeof(float2) * (size_t)(p->nJm + R)));
+  int KT = (int)(avail / (sizeof(float2) * (size_t)p->ysr + sizeof(double2) * (size_t)R));
   if (KT > Smax) KT = Smax;
   if (KT > 128) KT = 128;
   if (KT < 1) return false;
   p->KT = KT;
-  size_t tiles = sizeof(float2) * (size_t)KT * (p->nJm + R);
+  size_t tiles = (sizeof(float2) * (size_t)p->ysr + sizeof(double2) * (size_t)R) * (size_t)KT;
   size_t u2 = tiles > other ? tiles : other;
   if (fixed + u2 > (size_t)maxsmem) return false;
   o = al16(o + u2);
@@ -171,14 +192,16 @@ enum { EPI_W_ACC = 0, EPI_Z_STORE = 1, EPI_Q_UPDATE = 2, EPI_P_UPDATE = 3, EPI_P
 struct RowsEpiD {     // W / Z: fp64 values
   int mode, R;
   double2* acc;       // W: wacc
-  double2* gdst;      // Z: L2 partials
-  TT_DEV void operator()(int m, int n, double2 v) const {
+  double2* gdst;      // Z: L2 partials of this CTA, one slot of `pstride` per K part
+  int pstride;
+  TT_DEV void operator()(int m, int n, int ks, double2 v) const {
     const int o = m * R + n;
     if (mode == EPI_W_ACC) {
       acc[o] = zadd(acc[o], v);
     } else {
-      __stcg(&gdst[o].x, v.x);
-      __stcg(&gdst[o].y, v.y);
+      double2* d = gdst + (size_t)ks * pstride + o;
+      __stcg(&d->x, v.x);
+      __stcg(&d->y, v.y);
     }
   }
 };
@@ -203,7 +226,7 @@ struct RowsEpi {      // Q / P updates: fp32 correction v, fp64 arithmetic
       case EPI_P_MAPPED: {  // tight plan: the GEMM ran over every local row, keep the sampled ones
         const int q = rmap[m];
         if (q < 0) break;
-        const double2 z = sum_parts2(zp + (size_t)own_k[q] * R + n, (size_t)zstride, CL);
+        const double2 z = sum_parts2n(zp + (size_t)own_k[q] * R + n, (size_t)zstride, CL);
         inc32[q * R + n] = to_f2(zscale(zmul(zconj(gam[n]), zsub(z, to_d2(v))), mu));
         break;
       }
@@ -273,7 +296,7 @@ static __device__ __noinline__ void write_residual(const tt_rows_args& a, const 
                               ? (const float2*)a.ysrc + (size_t)f * a.y_frame_stride + (size_t)s * a.y_slice_stride +
                                     (size_t)rows[k0 + kk] * ny + j0
                               : (const float2*)a.ysrc + (((size_t)f * a.nslices + s) * Smax + k0 + kk) * ny + j0;
-      ys[kk * pl.nJm + jj] = src[jj];
+      ys[kk * pl.ysr + jj] = src[jj];
     }
     for (int o = tid; o < kt * R; o += NT) {
       float2 v;
@@ -284,7 +307,7 @@ static __device__ __noinline__ void write_residual(const tt_rows_args& a, const 
     __syncthreads();
     for (int o = tid; o < kt * nJ; o += NT) {
       const int kk = o / nJ, jj = o - kk * nJ;
-      float2 e = ys[kk * pl.nJm + jj];
+      float2 e = ys[kk * pl.ysr + jj];
       float2 sacc = make_float2(0.f, 0.f);
       for (int r = 0; r < R; ++r) sacc = cfma(ahs[kk * R + r], bhl[jj * R + r], sacc);
       float2* dst = (float2*)a.resid_out + (((size_t)f * a.nslices + s) * Smax + k0 + kk) * ny + j0 + jj;
@@ -417,21 +440,23 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
   float2* zs32 = (float2*)(smem + pl.o_u2);  // tight plan: the P increments (U2 is free from B4 on)
   float2* red2 = (float2*)(smem + pl.o_red2);     // fp32 K-split partials (corrections)
   double2* red2d = (double2*)(smem + pl.o_red2);  // fp64 K-split partials (W, Z)
-  float2* ys = (float2*)(smem + pl.o_u2);
-  float2* ahs = ys + (size_t)KT * pl.nJm;
+  float2* ys = (float2*)(smem + pl.o_u2);                   // [KT][ysr] the frame's Y rows (own columns)
+  double2* ahs64 = (double2*)(ys + (size_t)KT * pl.ysr);    // [KT][R] the frame's Ah_S rows, fp64
+  float2* ahs = (float2*)ahs64;                             // scratch of write_residual
   // phase (a) only: Bh in fp64 (not in the tight plan), GB partial tiles [parts][tiles][4], then the
   // colnorm partials [parts][R]
   const int gb_rt = (R + 1) >> 1, gb_nt = gb_rt * (gb_rt + 1) / 2;  // 2 x 2 tiles of the lower triangle
   // one packed entry per thread unless that leaves threads idle over a long column block (config 3)
   const bool gb_tiled = nJ * R >= 1024 && Rp <= NT;
   const int gb_parts = max(1, (NT + gb_nt / 2) / gb_nt);
-  double2* bh64 = (double2*)(smem + pl.o_u2);
-  double2* gbt = TIGHT ? bh64 : bh64 + (size_t)pl.nJm * R;
+  double2* bh64 = (double2*)(smem + pl.o_bh64);  // fp64 copy of the Bh rows (not in the tight plan)
+  double2* gbt = (double2*)(smem + pl.o_u2);
   double* cnp = (double*)(gbt + 4 * (size_t)max(2 * NT, gb_nt));
   float2* vop = (float2*)(smem + pl.o_u2);              // update only: gamma-scaled GEMM operand
   double* red = (double*)(smem + pl.o_red);
   (void)inv;
   __shared__ int sh_S, sh_err, sh_own, sh_amb, sh_Sglob;
+  __shared__ __align__(8) unsigned long long ybar;  // completion of the frame's bulk Y-row copies
   long long* pclk = (a.phase_clock != nullptr && blockIdx.x == 0) ? (long long*)a.phase_clock : nullptr;
   // branch-free (a lane-0 branch would leave warp 0 diverged and send later shuffles down the slow path)
 #define STAMP(k)                                                                                   \
@@ -458,11 +483,23 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     const float2* src = (const float2*)a.ah_in + arow * R;
     for (int o = tid; o < nI * R; o += NT) ahl[o] = src[o];
     const float2* srb = (const float2*)a.bh_in + ((size_t)s * ny + j0) * R;
-    for (int o = tid; o < nJ * R; o += NT) bhl[o] = srb[o];
+    for (int o = tid; o < nJ * R; o += NT) {
+      bhl[o] = srb[o];
+      if (!TIGHT) bh64[o] = to_d2(srb[o]);
+    }
     if (a.policy == TT_POLICY_INFORMATIVE)
       for (int m = tid; m < a.nforced; m += NT) forced[m] = a.forced[m];
   }
   ldl_table_init(tab, R);
+  // Y rows by bulk copy (TMA) when every row segment is 16-byte aligned and sized, else cp.async
+  const bool y_bulk = (nJ & 1) == 0 && (j0 & 1) == 0 && (ny & 1) == 0 && ((size_t)a.ysrc & 15) == 0 &&
+                      (size_t)KT * nJ * sizeof(float2) < (1u << 20);
+  unsigned yph = 0;
+  if (tid == 0) {
+    mbar_init(&ybar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  fence_proxy_async_smem();
   // forced lines among this thread's rows of the block-wide draw (bits, registers for the whole launch)
   unsigned fmask = 0u;
   int top = 1;  // largest power of two <= nx (binary search of the CDF)
@@ -508,8 +545,6 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       }
       cnp[part * R + r] = acc;
     }
-    if (!TIGHT)
-      for (int o = tid; o < nJ * R; o += NT) bh64[o] = to_d2(bhl[o]);
     __syncthreads();
     if (tid < R) {
       double acc = 0.0;
@@ -738,11 +773,25 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         sh_S = S;
       }
     }
+    fence_proxy_async_smem();  // this frame's generic accesses of U2 before the bulk copies into it
     __syncthreads();
     STAMP(5);
     S = sh_S;
     if (!shard) Sglob = S;
     status |= sh_err;
+    // K parts of the Z GEMM: enough items for the block, the same count in every CTA of the cluster (the
+    // rows' owners sum CL * zks partial slots)
+    int zks;
+    {
+      const int zM = min(KT, max(S, 1));
+      if (TIGHT) {  // CUDA-core tiles, one per thread
+        const int ztiles = ((zM + ZTM - 1) / ZTM) * ((R + ZTN - 1) / ZTN);
+        zks = max(1, min(NT / ztiles, min(ROWS_ZKS, pl.nJm / 4)));
+      } else {      // DMMA items (4 M blocks x 1 r block), one per warp
+        const int items = ((((zM + 7) >> 3) + ZG - 1) / ZG) * ((R + 3) >> 2);
+        zks = max(1, min((NT / 32) / items, min(ROWS_ZKS, (pl.nJm + 3) / 4)));
+      }
+    }
 
     // ======== (b) publish own sampled rows of Ah; list them; prefetch the first Y tile
     if (tid == 0) sh_own = 0;
@@ -766,13 +815,35 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     const bool gather = a.y_mode == TT_Y_GATHER;
     const float2* ybase = gather ? (const float2*)a.ysrc + (size_t)f * a.y_frame_stride + (size_t)s * a.y_slice_stride + j0
                                  : (const float2*)a.ysrc + ((size_t)f * a.nslices + s) * Smax * ny + j0;
-    if (phase != 2) {
-      const int kt = min(KT, S);
-      for (int o = tid; o < kt * nJ; o += NT) {
-        const int kk = idiv(o, nJ), jj = o - kk * nJ;
-        cp_async8(&ys[kk * pl.nJm + jj], ybase + (size_t)(gather ? rows[kk] : kk) * ny + jj);
+    // Y rows [k0, k0 + kt) of this CTA's columns into the k tile: one bulk copy per row issued by warp 0
+    // (completion on ybar), or 8-byte cp.async by every thread
+    auto issue_y = [&](int k0, int kt) {
+      if (kt <= 0 || nJ <= 0) return;
+      if (y_bulk) {
+        if (warp == 0) {
+          if (lane == 0) mbar_arrive_expect_tx(&ybar, (unsigned)(kt * nJ * sizeof(float2)));
+          __syncwarp();
+          for (int kk = lane; kk < kt; kk += 32)
+            bulk_g2s(&ys[(size_t)kk * pl.ysr], ybase + (size_t)(gather ? rows[k0 + kk] : k0 + kk) * ny,
+                     (unsigned)(nJ * sizeof(float2)), &ybar);
+        }
+      } else {
+        for (int o = tid; o < kt * nJ; o += NT) {
+          const int kk = idiv(o, nJ), jj = o - kk * nJ;
+          cp_async8(&ys[kk * pl.ysr + jj], ybase + (size_t)(gather ? rows[k0 + kk] : k0 + kk) * ny + jj);
+        }
       }
-    }
+    };
+    auto wait_y = [&](int kt) {
+      if (kt <= 0 || nJ <= 0) return;
+      if (y_bulk) {
+        mbar_wait(&ybar, yph);
+        yph ^= 1u;
+      } else {
+        cp_async_wait_all();
+      }
+    };
+    if (phase != 2) issue_y(0, min(KT, S));
     for (int o = tid; o < nJ * R; o += NT) wacc[o] = make_double2(0.0, 0.0);
     for (int e = eb + tid; e < ee; e += NT) G[e - eb] = make_double2(0.0, 0.0);
     __syncthreads();  // row marks visible to warp 0
@@ -803,12 +874,12 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     if (one_tile) {
       // all sampled rows in one tile: the Z partial needs only Y and the resident Bh, so it runs inside
       // the B3 window; B3 completes, Ah_S arrives and GA / W follow. Z and W share one GEMM call site.
-      cp_async_wait_all();
+      wait_y(S);
       __syncthreads();
       STAMP(16);
       for (int o = tid; o < S * nJ; o += NT) {
         const int kk = idiv(o, nJ), jj = o - kk * nJ;
-        const float2 v = ys[kk * pl.nJm + jj];
+        const float2 v = ys[kk * pl.ysr + jj];
         ysq += (double)v.x * v.x + (double)v.y * v.y;
       }
       for (int gsel = 0; gsel < 2; ++gsel) {
@@ -819,7 +890,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
             float2 v;
             v.x = __ldcg(&g_ahs[o].x);
             v.y = __ldcg(&g_ahs[o].y);
-            ahs[o] = v;
+            ahs64[o] = to_d2(v);
           }
           __syncthreads();
           const int nq = 4 * (ee - eb);  // GA own packed entries (4-way k split, fixed-order quad sum)
@@ -830,7 +901,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
             if (eq < nq) {
               const int ij = tab[e];
               const int r = ij >> 8, q = ij & 255;
-              for (int kk = part; kk < S; kk += 4) g = zfma_cj(ahs[kk * R + r], ahs[kk * R + q], g);
+              for (int kk = part; kk < S; kk += 4) g = zfma_cj(ahs64[kk * R + r], ahs64[kk * R + q], g);
             }
             g.x += __shfl_xor_sync(0xffffffffu, g.x, 1);
             g.y += __shfl_xor_sync(0xffffffffu, g.y, 1);
@@ -840,11 +911,20 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
           }
           STAMP(18);
         }
-        const int M = z ? S : nJ, Kd = z ? nJ : S;
-        const int ks = gemm_split(M, R, Kd, ZTM, ZTN, pl.red_cap);
-        const RowsEpiD epi{z ? EPI_Z_STORE : EPI_W_ACC, R, wacc, g_zp + (size_t)c * Smax * R};
-        zgemm_tile<ZTM, ZTN, false, true>(M, R, Kd, ys, z ? pl.nJm : 1, z ? 1 : pl.nJm, z ? bhl : ahs, R, 1, ks, red2d,
-                                          epi);
+        if (z) {  // Z partial over own columns, K split into zks parts delivered to L2 as they are
+          const RowsEpiD epi{EPI_Z_STORE, R, wacc, g_zp + (size_t)c * zks * Smax * R, Smax * R};
+          if (TIGHT)
+            zgemm_fd<ZTM, ZTN, true, true>(S, R, nJ, ys, pl.ysr, 1, bhl, R, 1, zks, red2d, epi);
+          else
+            zgemm_dmma<ZG>(S, R, nJ, ys, pl.ysr, 1, bh64, R, zks, epi);
+        } else {
+          const RowsEpiD epi{EPI_W_ACC, R, wacc, nullptr, 0};
+          if (TIGHT)
+            zgemm_fd<ZTM, ZTN, true, false>(nJ, R, S, ys, 1, pl.ysr, ahs64, R, 1,
+                                            gemm_split(nJ, R, S, ZTM, ZTN, pl.red_cap), red2d, epi);
+          else
+            zgemm_dmma<ZG>(nJ, R, S, ys, 1, pl.ysr, ahs64, R, 1, epi);
+        }
         __syncthreads();
         STAMP(z ? 17 : 19);
       }
@@ -857,17 +937,12 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
 
     for (int k0 = 0; !one_tile && phase != 2 && k0 < S; k0 += KT) {  // general case: several k tiles
       const int kt = min(KT, S - k0);
-      if (k0 > 0) {
-        for (int o = tid; o < kt * nJ; o += NT) {
-          const int kk = idiv(o, nJ), jj = o - kk * nJ;
-          cp_async8(&ys[kk * pl.nJm + jj], ybase + (size_t)(gather ? rows[k0 + kk] : k0 + kk) * ny + jj);
-        }
-      }
+      if (k0 > 0) issue_y(k0, kt);
       for (int o = tid; o < kt * R; o += NT) {
         float2 v;
         v.x = __ldcg(&g_ahs[(size_t)(k0) * R + o].x);
         v.y = __ldcg(&g_ahs[(size_t)(k0) * R + o].y);
-        ahs[o] = v;
+        ahs64[o] = to_d2(v);
       }
       __syncthreads();
       // GA own packed entries first: they need only Ah_S, so they run while the Y rows are in flight
@@ -881,7 +956,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
           if (eq < nq) {
             const int ij = tab[e];
             const int r = ij >> 8, q = ij & 255;
-            for (int kk = part; kk < kt; kk += 4) g = zfma_cj(ahs[kk * R + r], ahs[kk * R + q], g);
+            for (int kk = part; kk < kt; kk += 4) g = zfma_cj(ahs64[kk * R + r], ahs64[kk * R + q], g);
           }
           g.x += __shfl_xor_sync(0xffffffffu, g.x, 1);
           g.y += __shfl_xor_sync(0xffffffffu, g.y, 1);
@@ -890,27 +965,37 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
           if (part == 0 && eq < nq) G[e - eb] = zadd(G[e - eb], g);
         }
       }
-      cp_async_wait_all();
+      wait_y(kt);
       __syncthreads();
       if (k0 == 0) STAMP(16);
       for (int o = tid; o < kt * nJ; o += NT) {
         const int kk = idiv(o, nJ), jj = o - kk * nJ;
-        const float2 v = ys[kk * pl.nJm + jj];
+        const float2 v = ys[kk * pl.ysr + jj];
         ysq += (double)v.x * v.x + (double)v.y * v.y;
       }
       // W[jj][r] += sum_k Y[k][jj] conj(Ah_S[k][r]), then the Z partial over own columns
       // Z[k][r] = sum_jj Y[k][jj] conj(Bh[jj][r]): one call site, so one copy of the GEMM code
       for (int gsel = 0; gsel < 2; ++gsel) {
         const bool w = gsel == 0;
-        const int M = w ? nJ : kt, Kd = w ? kt : nJ;
-        const int ks = gemm_split(M, R, Kd, ZTM, ZTN, pl.red_cap);
-        const RowsEpiD epi{w ? EPI_W_ACC : EPI_Z_STORE, R, wacc, g_zp + ((size_t)c * Smax + k0) * R};
-        zgemm_tile<ZTM, ZTN, false, true>(M, R, Kd, ys, w ? 1 : pl.nJm, w ? pl.nJm : 1, w ? ahs : bhl, R, 1, ks, red2d,
-                                          epi);
+        if (w) {
+          const RowsEpiD epi{EPI_W_ACC, R, wacc, nullptr, 0};
+          if (TIGHT)
+            zgemm_fd<ZTM, ZTN, true, false>(nJ, R, kt, ys, 1, pl.ysr, ahs64, R, 1,
+                                            gemm_split(nJ, R, kt, ZTM, ZTN, pl.red_cap), red2d, epi);
+          else
+            zgemm_dmma<ZG>(nJ, R, kt, ys, 1, pl.ysr, ahs64, R, 1, epi);
+        } else {
+          const RowsEpiD epi{EPI_Z_STORE, R, wacc, g_zp + ((size_t)c * zks * Smax + k0) * R, Smax * R};
+          if (TIGHT)
+            zgemm_fd<ZTM, ZTN, true, true>(kt, R, nJ, ys, pl.ysr, 1, bhl, R, 1, zks, red2d, epi);
+          else
+            zgemm_dmma<ZG>(kt, R, nJ, ys, pl.ysr, 1, bh64, R, zks, epi);
+        }
         if (w) __syncthreads();  // the K-split buffer is reused
       }
       if (k0 == 0) STAMP(18);
       if (k0 == 0) STAMP(19);
+      fence_proxy_async_smem();  // the tile's generic reads before the next tile's bulk copies
       __syncthreads();
     }
     STAMP(8);
@@ -985,7 +1070,8 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       if (tid < hparts * R) {
         const int r = tid % R, part = tid / R;
         double2 h = make_double2(0.0, 0.0);
-        for (int jj = part; jj < nJ; jj += hparts) h = zfma_cj(to_d2(bhl[jj * R + r]), wacc[jj * R + r], h);
+        for (int jj = part; jj < nJ; jj += hparts)
+          h = zfma_cj(TIGHT ? to_d2(bhl[jj * R + r]) : bh64[jj * R + r], wacc[jj * R + r], h);
         hpart[part * R + r] = h;
       }
       __syncthreads();
@@ -1019,7 +1105,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     }
     for (int o = tid; o < nown * R; o += NT) {
       const int m = idiv(o, R), r = o - m * R;
-      if (!TIGHT) zs[o] = sum_parts2(g_zp + (size_t)own_k[m] * R + r, (size_t)Smax * R, CL);
+      if (!TIGHT) zs[o] = sum_parts2n(g_zp + (size_t)own_k[m] * R + r, (size_t)Smax * R, CL * zks);
     }
     {
       const int hr = tid - (NT - R);
@@ -1165,7 +1251,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
           __syncthreads();
           const int M = q ? nJ : (nown > 0 ? nI : 0);
           const RowsEpi epi{q ? EPI_Q_UPDATE : EPI_P_MAPPED, R, wacc, bhl, gam, cfac_d, mu_used, flags,
-                            own_k, g_zp, Smax * R, CL, zs32};
+                            own_k, g_zp, Smax * R, CL * zks, zs32};
           cgemm_tile<GTM, GTN, false, true>(M, R, R, q ? bhl : ahl, R, 1, mq, R, 1, 1, red2, epi);
           __syncthreads();
         }
@@ -1203,7 +1289,11 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         if (m >= 0) v = zadd(v, TIGHT ? to_d2(zs32[m * R + r]) : zs[m * R + r]);
         ahl[o] = to_f2(v);
       }
-      for (int o = tid; o < nJ * R; o += NT) bhl[o] = to_f2(wacc[o]);
+      for (int o = tid; o < nJ * R; o += NT) {
+        const float2 v = to_f2(wacc[o]);  // the state is fp32; the fp64 copy holds the same values
+        bhl[o] = v;
+        if (!TIGHT) bh64[o] = to_d2(v);
+      }
       __syncthreads();
     }
     STAMP(14);
@@ -1280,6 +1370,22 @@ extern "C" int tt_rows_plan(int nx, int ny, int rank, int max_rows, int policy, 
 }
 
 extern "C" size_t tt_rows_shard_xg_len(int rank) { return (size_t)rank * (rank + 1) + 2; }
+
+// Shared-memory plan of a row-mask launch at a given cluster size (diagnostics / tests): out[0..5] =
+// cluster, rows per k tile (KT), smem bytes, tight (1/0), padded Y row stride, K-split buffer entries.
+extern "C" int tt_rows_plan_info(int nx, int ny, int rank, int max_rows, int cluster, int* out) {
+  if (!out || nx < 1 || ny < 1 || rank < 1 || max_rows < 1) return tt_fail(TT_EINVAL, "tt_rows_plan_info: bad args");
+  RowsPlan pl;
+  int rc = rows_choose_cluster(nx, ny, rank, max_rows, cluster, &pl);
+  if (rc) return rc;
+  out[0] = pl.CL;
+  out[1] = pl.KT;
+  out[2] = pl.smem;
+  out[3] = pl.tight;
+  out[4] = pl.ysr;
+  out[5] = pl.red_cap;
+  return TT_OK;
+}
 
 // Sum the payload slots of a local multi-rank launch into slot 0 (fixed order over ranks): the
 // on-device counterpart of the all-reduce between the two phases.
