@@ -988,11 +988,11 @@ TT_DEV void zgemm_fd(int M, int N, int K, const float2* A, int a_m, int a_k, con
 // round-robin. PARTS: each K part delivered as it is, out(m, r, ks, value); else KS must be 1.
 TT_DEV void dmma_m8n8k4(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
 }
-template <int G, typename Out>
-TT_DEV void zgemm_dmma(int M, int R, int K, const float2* A, int a_m, int a_k, const double2* B, int b_k, int KS,
+template <int G, typename AT, typename Out>
+TT_DEV void zgemm_dmma(int M, int R, int K, const AT* A, int a_m, int a_k, const double2* B, int b_k, int KS,
                        Out out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int row = lane >> 2, kq = lane & 3;
@@ -1002,37 +1002,50 @@ TT_DEV void zgemm_dmma(int M, int R, int K, const float2* A, int a_m, int a_k, c
   for (int it = warp; it < items; it += nw) {
     const int ks = idiv(it, MG * NB), rest = it - ks * MG * NB;
     const int mg = idiv(rest, NB), nb = rest - mg * NB;
+    const int gcount = min(G, MB - mg * G);  // warp-uniform: empty 8-row blocks issue no DMMA
     const int t0 = idiv(kpairs * ks, KS), t1 = idiv(kpairs * (ks + 1), KS);
-    const int col = row;  // B fragment column of this lane: n = nb * 8 + col
-    const int rb = nb * 4 + (col >> 1), q = col & 1;
+    const int rb = nb * 4 + (row >> 1), q = row & 1;  // B fragment column n = nb * 8 + row = 2 rb + q
+    const bool rok = rb < R;
+    const AT* ap[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int m = ((mg * G + g) << 3) + row;
+      ap[g] = A + (size_t)min(m, M - 1) * a_m;
+    }
     double acc[G][2];
 #pragma unroll
     for (int g = 0; g < G; ++g) acc[g][0] = acc[g][1] = 0.0;
+    const double2* bp = B + min(rb, R - 1);
     for (int t = t0; t < t1; ++t) {
       const int k = 4 * t + kq;
-      double2 b = make_double2(0.0, 0.0);
-      if (k < K && rb < R) b = B[(size_t)k * b_k + rb];
-      const double b0 = q == 0 ? b.x : -b.y, b1 = q == 0 ? b.y : b.x;
+      const bool kok = k < K;
+      const int kc = min(k, K - 1);  // loads always in range (no branches around them), invalid ones zeroed
+      const double2 braw = bp[(size_t)kc * b_k];
+      const bool bv = kok && rok;
+      const double2 b = make_double2(bv ? braw.x : 0.0, bv ? braw.y : 0.0);
       double ar[G], ai[G];
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         const int m = ((mg * G + g) << 3) + row;
-        float2 a = make_float2(0.f, 0.f);
-        if (m < M && k < K) a = A[(size_t)m * a_m + (size_t)k * a_k];
-        ar[g] = (double)a.x;
-        ai[g] = (double)a.y;
+        const AT a = ap[g][(size_t)kc * a_k];
+        const bool av = kok && m < M;
+        ar[g] = av ? (double)a.x : 0.0;
+        ai[g] = av ? (double)a.y : 0.0;
       }
+      const double b0 = q == 0 ? b.x : -b.y, b1 = q == 0 ? b.y : b.x;
+      // the re slots of all blocks before the im slots: consecutive DMMAs never chain on one accumulator
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        dmma_m8n8k4(acc[g][0], acc[g][1], ar[g], b0);
-        dmma_m8n8k4(acc[g][0], acc[g][1], ai[g], b1);
-      }
+      for (int g = 0; g < G; ++g)
+        if (g < gcount) dmma_m8n8k4(acc[g][0], acc[g][1], ar[g], b0);
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+        if (g < gcount) dmma_m8n8k4(acc[g][0], acc[g][1], ai[g], b1);
     }
     const int r = nb * 4 + kq;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const int m = ((mg * G + g) << 3) + row;
-      if ((mg * G + g) < MB && m < M && r < R) out(m, r, ks, make_double2(acc[g][0], acc[g][1]));
+      if (g < gcount && m < M && r < R) out(m, r, ks, make_double2(acc[g][0], acc[g][1]));
     }
   }
 }

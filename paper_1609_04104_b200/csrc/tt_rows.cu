@@ -134,8 +134,8 @@ static bool rows_make_plan_cap(int nx, int ny, int R, int Smax, int CL, int red_
     if (m > g) g = m;
     o = al16(o + g);
   }
-  const size_t gfull = tight ? 0 : sizeof(float2) * R * R;
-  p->o_gaf = (int)o;    o = al16(o + gfull);  // full Hermitian fp32 GA, GB (not in the tight plan)
+  const size_t gfull = tight ? 0 : sizeof(double2) * R * R;
+  p->o_gaf = (int)o;    o = al16(o + gfull);  // full Hermitian fp64 GA, GB (not in the tight plan)
   p->o_gbf = (int)o;    o = al16(o + gfull);
   // vec: gam, hv, hsave (double2 R); nrm, inrm, inv, gda, gdb (double R); gamf (float2 R); 16 scalars
   //      + LDL scratch: colb 4 (R+1) double2, blk 4 (R/2+1) double, zf R double2
@@ -163,8 +163,7 @@ static bool rows_make_plan_cap(int nx, int ny, int R, int Smax, int CL, int red_
   // Y tile row stride = 4 (mod 16) complex: 16 B aligned rows (bulk copies), 8 banks apart (the Z GEMM's
   // DMMA A fragments read 4 consecutive columns of 8 rows: conflict-free)
   p->ysr = ((p->nJm + 11) & ~15) + 4;
-  const size_t v2 = tight ? sizeof(float2) * (size_t)R * p->nIm              // tight: the P increments
-                          : sizeof(float2) * (size_t)R * (p->nJm + p->nIm);  // both gamma-scaled GEMM operands
+  const size_t v2 = sizeof(float2) * (size_t)R * p->nIm;  // tight: the P increments; else the owned sampled Ah rows
   if (v2 > other) other = v2;
   size_t avail = maxsmem - fixed;
   int KT = (int)(avail / (sizeof(float2) * (size_t)p->ysr + sizeof(double2) * (size_t)R));
@@ -217,6 +216,15 @@ struct RowsEpi {      // Q / P updates: fp32 correction v, fp64 arithmetic
   const double2* zp;
   int zstride, CL;
   float2* inc32;
+  // the fp64 corrections of the DMMA path
+  TT_DEV void operator()(int m, int n, int ks, double2 v) const {
+    (void)ks;
+    const int o = m * R + n;
+    if (mode == EPI_Q_UPDATE)
+      acc[o] = zadd(zscale(to_d2(base[o]), cfac), zscale(zmul(zconj(gam[n]), zsub(acc[o], v)), mu));
+    else  // EPI_P_UPDATE: mu conj(g) P
+      acc[o] = zscale(zmul(zconj(gam[n]), zsub(acc[o], v)), mu);
+  }
   TT_DEV void operator()(int m, int n, float2 v) const {
     int o = m * R + n;
     switch (mode) {
@@ -413,8 +421,8 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
   double2* G = (double2*)(smem + pl.o_u1);
   double* pbuf = (double*)(smem + pl.o_u1);
   double* cdf = pbuf + nx;
-  float2* gaf = (float2*)(smem + pl.o_gaf);  // full Hermitian GA, GB (fp32, row-major)
-  float2* gbf = (float2*)(smem + pl.o_gbf);
+  double2* gaf = (double2*)(smem + pl.o_gaf);  // full Hermitian GA, GB (fp64, row-major)
+  double2* gbf = (double2*)(smem + pl.o_gbf);
   double2* gam = (double2*)(smem + pl.o_vec);
   double2* hv = gam + R;
   double2* hsave = hv + R;
@@ -1140,10 +1148,10 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       }
       G[e] = gg;
       if (!TIGHT) {
-        gaf[r * R + q] = to_f2(gae);
-        gaf[q * R + r] = to_f2(zconj(gae));
-        gbf[r * R + q] = to_f2(gbe);
-        gbf[q * R + r] = to_f2(zconj(gbe));
+        gaf[r * R + q] = gae;
+        gaf[q * R + r] = zconj(gae);
+        gbf[r * R + q] = gbe;
+        gbf[q * R + r] = zconj(gbe);
       }
     }
     __syncthreads();
@@ -1256,27 +1264,28 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
           __syncthreads();
         }
       } else {
-        // gamma-scaled operands of both corrections at once: Bh diag(g) and Ah_own diag(g)
-        float2* vop2 = vop + (size_t)pl.nJm * R;
-        for (int o = tid; o < nJ * R; o += NT) vop[o] = cmul(bhl[o], gamf[o - idiv(o, R) * R]);
+        // the corrections on the fp64 tensor-core path, exact fp32 operands, the gamma scaling on the
+        // fp64 R x R factor: corr[m][r] = sum_q X[m][q] conj(conj(g_q) G[q][r]) with (X, G) = (Bh, GA) for
+        // Q and (the owned sampled Ah rows, GB) for P
+        double2* gqa = gaf;  // scaled in place: GA, GB are not read again this frame
+        double2* gqb = gbf;
+        float2* aown = vop;
+        for (int o = tid; o < R * R; o += NT) {
+          const double2 cg = zconj(gam[idiv(o, R)]);
+          gqa[o] = zmul(cg, gaf[o]);
+          gqb[o] = zmul(cg, gbf[o]);
+        }
         for (int o = tid; o < nown * R; o += NT) {
           const int m = idiv(o, R), q = o - m * R;
-          vop2[o] = cmul(ahl[own_li[m] * R + q], gamf[q]);
+          aown[o] = ahl[own_li[m] * R + q];
         }
         __syncthreads();
         STAMP(21);
-        // Q: corr[jj][r] = sum_q vop[jj][q] conj(GA[q][r]) -> new Bh rows; P: same with GB on the owned
-        // sampled rows -> mu conj(g) P. Both in one pass (one barrier, one reduction pass).
-        {
-          const int tn = (R + GTN - 1) / GTN;
-          const int tiles = ((nJ + GTM - 1) / GTM + (nown + GTM - 1) / GTM) * tn;
-          int ks = idiv(NT, tiles > 0 ? tiles : 1);
-          ks = min(ks, min(R / 4, 8));
-          while (ks > 1 && ks * (nJ + nown) * R > pl.red_cap) --ks;
-          ks = max(ks, 1);
+        {  // both products in one pass (disjoint outputs): one barrier
           const RowsEpi eq{EPI_Q_UPDATE, R, wacc, bhl, gam, cfac_d, mu_used, nullptr};
           const RowsEpi ep{EPI_P_UPDATE, R, zs, bhl, gam, cfac_d, mu_used, nullptr};
-          cgemm_tile_pair<GTM, GTN, false, true>(nJ, nown, R, R, vop, vop2, R, 1, gaf, gbf, R, 1, ks, red2, eq, ep);
+          zgemm_dmma<ZG>(nJ, R, R, bhl, R, 1, gqa, R, 1, eq);
+          zgemm_dmma<ZG>(nown, R, R, aown, R, 1, gqb, R, 1, ep);
           __syncthreads();
         }
       }

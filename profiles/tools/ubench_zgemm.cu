@@ -228,6 +228,56 @@ void check(const char* name, float2* gy, double2* gb) {
   printf("%s: DMMA vs zgemm_fd rel %.3e\n", name, sqrt(num / den));
 }
 
+
+// the rows kernel's zgemm_dmma (tt_block.cuh) at the config-3 shapes
+template <int G, int WHICH>
+__global__ void __launch_bounds__(256, 1) bench_zd(const float2* gy, const double2* gb, double2* gout, long long* cyc) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  float2* ys = (float2*)sm;
+  double2* bh = (double2*)(ys + 48 * YSR);
+  double2* ah = bh + NJ * R;
+  double2* w = ah + 48 * R;
+  float2* bl = (float2*)(w + NJ * R);
+  for (int o = threadIdx.x; o < 48 * YSR; o += 256) ys[o] = o < S * YSR ? gy[o] : make_float2(0.f, 0.f);
+  for (int o = threadIdx.x; o < NJ * R; o += 256) { bh[o] = gb[o]; bl[o] = make_float2((float)gb[o].x, (float)gb[o].y); }
+  for (int o = threadIdx.x; o < S * R; o += 256) ah[o] = gb[o];
+  for (int o = threadIdx.x; o < NJ * R; o += 256) w[o] = make_double2(0, 0);
+  __syncthreads();
+  for (int rep = 0; rep < 21; ++rep) {
+    __syncthreads();
+    long long t0 = clock64();
+    if (WHICH == 0) {
+      OutZ o{gout + (size_t)blockIdx.x * 8 * S * R, S * R};
+      const int items = ((((S + 7) >> 3) + G - 1) / G) * ((R + 3) >> 2);
+      zgemm_dmma<G>(S, R, NJ, ys, YSR, 1, bh, R, max(1, 8 / items), o);
+    } else if (WHICH == 1) {
+      OutW o{w};
+      zgemm_dmma<G>(NJ, R, S, ys, 1, YSR, ah, R, 1, o);
+    } else {  // the Q correction: M = NJ, K = R, A = fp32 Bh rows, B = an R x R fp64 factor
+      OutW o{w};
+      zgemm_dmma<G>(NJ, R, R, bl, R, 1, ah, R, 1, o);
+    }
+    __syncthreads();
+    long long t1 = clock64();
+    if (threadIdx.x == 0 && rep > 0) cyc[blockIdx.x * 20 + rep - 1] = t1 - t0;
+  }
+  if (WHICH == 1)
+    for (int o = threadIdx.x; o < NJ * R; o += 256) gout[o] = w[o];
+}
+template <int G, int WHICH>
+void run_zd(const char* name, float2* gy, double2* gb, double2* go, long long* cyc) {
+  size_t sm = 48 * YSR * 8 + NJ * R * 16 + 48 * R * 16 + NJ * R * 16 + NJ * R * 8;
+  cudaFuncSetAttribute(bench_zd<G, WHICH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  bench_zd<G, WHICH><<<148, 256, sm>>>(gy, gb, go, cyc);
+  cudaError_t e = cudaDeviceSynchronize();
+  std::vector<long long> h(148 * 20);
+  cudaMemcpy(h.data(), cyc, h.size() * 8, cudaMemcpyDeviceToHost);
+  std::sort(h.begin(), h.end());
+  const double dfma = 4.0 * (WHICH == 2 ? (double)NJ * R * R : (double)S * NJ * R);
+  printf("%-28s %s  median %lld cycles  (%.1f DFMA/clk/SM of 64)\n", name, cudaGetErrorString(e), h[h.size() / 2],
+         dfma / h[h.size() / 2]);
+}
+
 int main() {
   float2* gy; double2* gb; double2* go; long long* cyc;
   cudaMalloc(&gy, S * YSR * 8); cudaMalloc(&gb, NJ * R * 16); cudaMalloc(&go, 148 * 8 * S * R * 16 + NJ * R * 16);
@@ -248,6 +298,14 @@ int main() {
   run<4, 2, 1>("W 4x2", gy, gb, go, cyc);
   run_dmma<0>("Z dmma", gy, gb, go, cyc);
   run_dmma<1>("W dmma", gy, gb, go, cyc);
+  run_zd<4, 0>("Z zgemm_dmma G4", gy, gb, go, cyc);
+  run_zd<2, 0>("Z zgemm_dmma G2", gy, gb, go, cyc);
+  run_zd<8, 0>("Z zgemm_dmma G8", gy, gb, go, cyc);
+  run_zd<4, 1>("W zgemm_dmma G4", gy, gb, go, cyc);
+  run_zd<2, 1>("W zgemm_dmma G2", gy, gb, go, cyc);
+  run_zd<8, 1>("W zgemm_dmma G8", gy, gb, go, cyc);
+  run_zd<4, 2>("Qcorr zgemm_dmma G4", gy, gb, go, cyc);
+  run_zd<2, 2>("Qcorr zgemm_dmma G2", gy, gb, go, cyc);
   check<0>("Z", gy, gb);
   check<1>("W", gy, gb);
   return 0;
