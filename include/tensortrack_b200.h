@@ -129,6 +129,16 @@ typedef struct tt_rows_args {
    * shard_world slots (frame parity). */
   int32_t shard_fused;
   uint32_t* grid_sync;
+  /* Informative draws without replacement (appended; 0 = with replacement): draw_samples(replacement=False)
+   * (sampler.py:163-169): the forced rows' weights zeroed, k - nforced sequential renormalised draws
+   * (observation.py:279-297, one uniform each), union with the forced rows, sorted. */
+  int32_t draw_wor;
+  /* TrackerConfig.norm_cap (tracker.py:406-408; appended): when norm_out is non-NULL,
+   * norm_out[f][s] = 1 if frame f's post-update ||A||_F or ||B||_F exceeds norm_cap, else 0 (the DFT is
+   * unitary, so ||Ah||_F = ||A||_F; 0 for a frame without samples, which does not update). Not with
+   * row sharding. */
+  double norm_cap;
+  int32_t* norm_out;
 } tt_rows_args;
 /* plan of a row-mask launch at `cluster` (0: smallest that fits): out[6] = cluster, rows per k tile,
  * shared-memory bytes, tight plan (0/1), padded Y row stride, K-split buffer entries (diagnostics) */
@@ -244,6 +254,14 @@ int tt_draw_with_replacement_large(void* stream, int n, const double* probs, int
  * renormalised draws, draw order; consumes k uniforms from pos[0]. */
 int tt_draw_without_replacement(void* stream, int n, const double* weights, int k, uint64_t key0,
                                 uint64_t key1, uint64_t* pos, int32_t* out, int32_t* status);
+/* variable_density_rows (observation.py:300-323) for `frames` frames of `nslices` slices in one launch:
+ * frame f of slice s is the DC row then n_rows - 1 sequential draws without replacement with `weights`
+ * (the reference's d**alpha / 2 per row, DC 0; computed by the caller) from the Philox stream
+ * (key0, key1 + s) at position pos0[s] + f (n_rows - 1) (pos0 NULL: 0), in draw order ->
+ * out [frames][nslices][n_rows]. The VD phase of run_adaptive (experiment.py:484-497) for a block of
+ * frames. */
+int tt_vd_rows_batch(void* stream, int frames, int nslices, int n, const double* weights, int n_rows,
+                     uint64_t key0, uint64_t key1, const uint64_t* pos0, int32_t* out);
 /* The three draws with caller-supplied uniforms instead of the Philox stream: uniforms[m] is the
  * Generator.random() value draw m consumes (one per draw, as numpy's choice and the sequential draws
  * consume them), so a caller holding any other bit generator (np.random.default_rng(seed), PCG64,

@@ -335,6 +335,23 @@ def draw_rows(p, k, forced, key, position):
     return np.union1d(forced, drawn).astype(np.int64), remaining
 
 
+def draw_rows_wor(p, k, forced, key, position):
+    """draw_samples(replacement=False) (sampler.py:163-169) on a Philox stream at ``position``: the
+    forced indices' weights zeroed, k - |forced| sequential renormalised draws, union with the forced
+    ones; returns (sorted unique omega, uniforms consumed)."""
+    forced = np.unique(np.asarray([] if forced is None else forced, dtype=np.int64))
+    remaining = k - forced.size
+    if remaining < 0:
+        raise ValueError("more forced indices than trials")
+    if k > np.asarray(p).size:
+        raise ValueError("cannot draw more distinct indices than the domain holds")
+    w = np.asarray(p, np.float64).copy()
+    w[forced] = 0.0
+    u = iter(philox_uniforms(key, position, remaining))
+    drawn = draw_without_replacement(w, remaining, lambda: next(u)) if remaining else np.empty(0, np.int64)
+    return np.union1d(forced, drawn).astype(np.int64), remaining
+
+
 def draw_without_replacement(weights, k, uniform_fn):
     """Sequential renormalised draws (observation.py:279-297)."""
     w = np.asarray(weights, dtype=np.float64).copy()
@@ -423,7 +440,10 @@ def online_run(kspace, A, B, lam, step, policy, clean=None, t0=1, alpha_bar=0.0,
 
     ``policy``: {"kind": "static", "rows": [rows_f ...]} or
     {"kind": "informative", "k": K, "forced": [...], "beta": b, "key": (k0, k1),
-     "position": 0}.
+     "position": 0, "replacement": True} or the run_adaptive schedule (experiment.py:462-497)
+    {"kind": "schedule", "vd_frames": V, "alpha": a, "fraction": f, + the informative keys}: the first V
+    frames take variable_density_rows (observation.py:300-323, draw order) from the same Philox stream,
+    the rest informative draws (with or without replacement, sampler.py:146-169).
     """
     kspace = np.asarray(kspace)
     T, n1, n2 = kspace.shape
@@ -432,9 +452,15 @@ def online_run(kspace, A, B, lam, step, policy, clean=None, t0=1, alpha_bar=0.0,
     for f in range(T):
         if policy["kind"] == "static":
             rows = np.asarray(policy["rows"][f], dtype=np.int64)
+        elif policy["kind"] == "schedule" and f < policy["vd_frames"]:
+            nr = int(np.ceil(policy["fraction"] * n1))
+            u = iter(philox_uniforms(policy["key"], pos, max(nr - 1, 0)))
+            rows = vd_rows(n1, policy["alpha"], policy["fraction"], lambda: next(u))
+            pos += max(nr - 1, 0)
         else:
             p = row_probs(fft_cols(A), n2, policy.get("beta", 0.1))
-            rows, used = draw_rows(p, policy["k"], policy.get("forced"), policy["key"], pos)
+            draw = draw_rows if policy.get("replacement", True) else draw_rows_wor
+            rows, used = draw(p, policy["k"], policy.get("forced"), policy["key"], pos)
             pos += used
             out["probs"].append(p)
         idx = rows_to_entries(rows, n2)

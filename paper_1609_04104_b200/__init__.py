@@ -10,7 +10,7 @@ anywhere, but every compute call needs a CUDA device and the built library.
 
 from .core import (TensorSubspace, outer_rank_one, rank_surrogate, rebalance, refold, singular_values,
                    synthesize_slice, unfold)
-from .engine import (BatchResult, EntryEngine, Informative, InformativeEntries, LocalShardedEngine, OnlineEngine,
+from .engine import (AdaptiveSchedule, BatchResult, EntryEngine, Informative, InformativeEntries, LocalShardedEngine, OnlineEngine,
                      OnlineResult, RowShardedEngine, StaticEntries, StaticRows, run_batch, run_online, warm_up)
 from .mri import FrameEstimate, PatchGrid, interp_track_step, patch_assemble, patch_partition, reconstruct_frame
 from .observation import (
@@ -73,7 +73,7 @@ __all__ = [
     "expected_count_trace", "expected_sample_count", "row_scores",
     "FrameEstimate", "interp_track_step", "reconstruct_frame", "PatchGrid", "patch_partition", "patch_assemble",
     "PatchedResult", "run_tracking_patched", "init_patch_factors", "draw_frame_entries", "full_entries",
-    "OnlineEngine", "OnlineResult", "StaticRows", "Informative", "run_online", "warm_up", "RowShardedEngine",
+    "OnlineEngine", "OnlineResult", "StaticRows", "Informative", "AdaptiveSchedule", "run_online", "warm_up", "RowShardedEngine",
     "EntryEngine", "InformativeEntries", "StaticEntries", "run_batch", "BatchResult", "LocalShardedEngine",
     "NumericalError", "ConfigError", "nmse", "nmse_frames", "StreamingProvider", "measure", "project",
     "CtenFormatError", "read_cten", "read_cten_tensor", "write_cten",

@@ -195,6 +195,30 @@ def draw_without_replacement(weights: torch.Tensor, k: int, key: tuple[int, int]
     return out[:k]
 
 
+def vd_rows_batch(frames: int, nslices: int, n: int, alpha: float, n_rows: int, key: tuple[int, int],
+                  pos0: torch.Tensor | None, out: torch.Tensor | None = None) -> torch.Tensor:
+    """variable_density_rows for ``frames`` x ``nslices`` (frame f of slice s from the Philox stream
+    (key0, key1 + s) at pos0[s] + f (n_rows - 1)) -> (frames, nslices, n_rows) int32, draw order."""
+    from .observation import row_distances
+
+    dist = row_distances(n)
+    w = np.zeros(n)
+    nz = dist > 0
+    w[nz] = dist[nz].astype(float) ** alpha / 2.0  # observation.py:317-318, on the host exactly as numpy
+    if n_rows - 1 > int(np.count_nonzero(w)):
+        raise ValueError("cannot draw more items than have positive weight")
+    dev = L.device()
+    wt = torch.from_numpy(w).to(dev)
+    if out is None:
+        out = torch.empty(frames, nslices, n_rows, dtype=torch.int32, device=dev)
+    if pos0 is not None:
+        _need(pos0, torch.int64, "pos0")
+    L.check(L.lib().tt_vd_rows_batch(L.stream_ptr(), int(frames), int(nslices), int(n), wt.data_ptr(), int(n_rows),
+                                     int(key[0]), int(key[1]), pos0.data_ptr() if pos0 is not None else None,
+                                     out.data_ptr()), "variable_density_rows")
+    return out
+
+
 def reconstruct(a: torch.Tensor, b: torch.Tensor, gamma: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
     """a (F, nx, R), b (F, ny, R), gamma (F, R) complex64 -> (F, nx, ny) (into ``out`` when given)."""
     for t, n in ((a, "a"), (b, "b"), (gamma, "gamma")):

@@ -325,6 +325,66 @@ static __device__ __noinline__ void write_residual(const tt_rows_args& a, const 
   }
 }
 
+// Informative rows without replacement (draw_samples(replacement=False), sampler.py:163-169): the
+// probabilities w (forced rows zeroed here) drawn from by k sequential renormalised draws
+// (weighted_draw_without_replacement, observation.py:279-297): per draw cumsum(w), u = u01 * total,
+// searchsorted(cdf, u, 'right'), w[idx] = 0. The cumsum is a block scan; a uniform within 1e-12 total of a
+// bucket edge redoes that draw over numpy's sequential cumsum, so the rows equal numpy's for identical
+// probabilities. Marks flags[idx] = 1 (cleared here); the caller adds the forced rows and compacts.
+static __device__ __noinline__ void rows_draw_wor(double* w, double* cdf, int* flags, int nx, int ndraw,
+                                                  const double* usm, const int* forced, int nforced, double* red) {
+  const int tid = threadIdx.x, NT = blockDim.x;
+  __shared__ int s_idx, s_amb;
+  for (int i = tid; i < nx; i += NT) flags[i] = 0;
+  __syncthreads();
+  for (int m = tid; m < nforced; m += NT) {
+    const int fr = forced[m];
+    if (fr >= 0 && fr < nx) w[fr] = 0.0;
+  }
+  __syncthreads();
+  for (int m = 0; m < ndraw; ++m) {
+    for (int exact = 0; exact < 2; ++exact) {
+      block_cumsum(w, cdf, nx, exact != 0, red);
+      if (tid == 0) {
+        const double total = cdf[nx - 1];
+        const double u = usm[m] * total;
+        const int idx = upper_bound_d(cdf, nx, u);
+        const double lo = idx > 0 ? cdf[idx - 1] : -1.0;
+        const double hi = idx < nx ? cdf[idx] : 2.0 * total + 1.0;
+        const double tol = 1e-12 * (total > 0.0 ? total : 1.0);
+        s_amb = (!exact && (u - lo <= tol || hi - u <= tol)) ? 1 : 0;
+        s_idx = idx < nx - 1 ? idx : nx - 1;
+      }
+      __syncthreads();
+      const int amb = s_amb;
+      __syncthreads();
+      if (!amb) break;
+    }
+    if (tid == 0) {
+      flags[s_idx] = 1;
+      w[s_idx] = 0.0;
+    }
+    __syncthreads();
+  }
+}
+
+// Post-update ||Ah||_F^2, ||Bh||_F^2 of the resident state (own rows / columns), summed over the cluster
+// in CTA order through `slot` (CL double2 in L2); the result is valid in CTA 0 after the call.
+static __device__ __noinline__ double2 cluster_state_norms(const float2* ahl, int nIA, const float2* bhl, int nJB,
+                                                           double2* slot, int c, int CL, double* red) {
+  double pa = 0.0, pb = 0.0;
+  for (int o = threadIdx.x; o < nIA; o += blockDim.x) pa += (double)ahl[o].x * ahl[o].x + (double)ahl[o].y * ahl[o].y;
+  for (int o = threadIdx.x; o < nJB; o += blockDim.x) pb += (double)bhl[o].x * bhl[o].x + (double)bhl[o].y * bhl[o].y;
+  pa = block_sum(pa, red);
+  pb = block_sum(pb, red);
+  if (threadIdx.x == 0) {
+    __stcg(&slot[c].x, pa);
+    __stcg(&slot[c].y, pb);
+  }
+  cluster_barrier();
+  return sum_parts2(slot, 1, CL);
+}
+
 // GB partial over a CTA's columns for wide column blocks (out of line: narrow blocks, config 2, keep
 // the frame loop's instruction footprint): 2 x 2 register tiles of the lower triangle (four products
 // per four operand loads), the columns split in `parts` interleaved parts, then a fixed-order sum of
@@ -521,6 +581,8 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     }
   }
   double alpha_bar = a.alpha_bar ? a.alpha_bar[s] : 0.0;
+  const double ncap2 = a.norm_cap * a.norm_cap;
+  bool prev_upd = false;  // norm_cap: whether the previous frame updated the state
   uint64_t ppos = (a.policy == TT_POLICY_INFORMATIVE && a.philox_pos) ? a.philox_pos[s] : 0ull;
   int status = 0;
   const int eb = part_begin(Rp, CL, c), ee = part_begin(Rp, CL, c + 1);
@@ -638,7 +700,8 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       STAMP(3);
       cluster_barrier();  // -------------------------------------------- B2
       STAMP(4);
-      if (nx <= 4 * NT) {
+      const bool wor = a.draw_wor != 0;
+      if (nx <= 4 * NT && !wor) {
         // Block-wide probabilities -> CDF -> draws -> sorted union, every warp busy (sampler.py:88-92,
         // :146-162). Thread t owns rows [r0, r1) (consecutive). One scan of the raw scores s gives
         // the blended CDF in closed form: with w1 = (1-beta)/sum(s), w0 = beta/nx,
@@ -697,10 +760,11 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         if (tid == 0) sh_S = tot;
         STAMP(31);
       }
-      if (nx > 4 * NT || sh_amb) {
+      if (nx > 4 * NT || wor || sh_amb) {
         // generic width, or a uniform within 1e-12 of a CDF boundary: numpy's sequential cumsum
-        // of the probabilities, cdf /= cdf[-1], per-draw searchsorted, forced union, compaction
-        if (nx > 4 * NT) {
+        // of the probabilities, cdf /= cdf[-1], per-draw searchsorted, forced union, compaction;
+        // draws without replacement: the sequential renormalised draws over the same probabilities
+        if (nx > 4 * NT || wor) {
           for (int i = tid; i < nx; i += NT) pbuf[i] = __ldcg(&g_sraw[i]);
           __syncthreads();
           double S1;
@@ -710,26 +774,30 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
           for (int i = tid; i < nx; i += NT) pbuf[i] = fma(pbuf[i], w1, w0);
         }
         __syncthreads();
-        if (tid == 0) {
-          double cacc = 0.0;
-          for (int i = 0; i < nx; ++i) {
-            cacc += pbuf[i];
-            cdf[i] = cacc;
+        if (wor) {
+          rows_draw_wor(pbuf, cdf, flags, nx, ndraw, usm, forced, a.nforced, red);
+        } else {
+          if (tid == 0) {
+            double cacc = 0.0;
+            for (int i = 0; i < nx; ++i) {
+              cacc += pbuf[i];
+              cdf[i] = cacc;
+            }
           }
+          __syncthreads();
+          const double last = cdf[nx - 1];
+          __syncthreads();
+          for (int i = tid; i < nx; i += NT) {
+            cdf[i] = cdf[i] / last;
+            flags[i] = 0;
+          }
+          __syncthreads();
+          for (int m = tid; m < ndraw; m += NT) {
+            const int idx = upper_bound_d(cdf, nx, usm[m]);
+            flags[idx < nx ? idx : nx - 1] = 1;
+          }
+          __syncthreads();
         }
-        __syncthreads();
-        const double last = cdf[nx - 1];
-        __syncthreads();
-        for (int i = tid; i < nx; i += NT) {
-          cdf[i] = cdf[i] / last;
-          flags[i] = 0;
-        }
-        __syncthreads();
-        for (int m = tid; m < ndraw; m += NT) {
-          const int idx = upper_bound_d(cdf, nx, usm[m]);
-          flags[idx < nx ? idx : nx - 1] = 1;
-        }
-        __syncthreads();
         if (warp == 0) {  // forced lines, then compaction -> sorted unique rows (np.union1d)
           for (int m = lane; m < a.nforced; m += 32) {
             const int fr = forced[m];
@@ -1309,6 +1377,9 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
 
     // ======== outputs
     const size_t fs = (size_t)f * a.nslices + s;
+    if (a.norm_out && !shard && c == 0 && tid == 0 && f > 0)  // the previous frame's post-update norms
+      a.norm_out[fs - a.nslices] = (prev_upd && (scal[1] > ncap2 || scal[2] > ncap2)) ? 1 : 0;
+    prev_upd = update;
     if (c == 0 && lead) {
       if (a.gamma_out && tid < R) ((float2*)a.gamma_out)[fs * R + tid] = gamf[tid];
       if (tid == 0) {
@@ -1345,6 +1416,11 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     if (a.policy == TT_POLICY_INFORMATIVE && a.philox_pos) a.philox_pos[s] = ppos;
   }
   if (status && tid == 0 && a.status) atomicOr(&a.status[s], status);
+  if (a.norm_out && !shard && a.frames > 0) {  // the last frame's post-update norms
+    const double2 nn = cluster_state_norms(ahl, nI * R, bhl, nJ * R, g_hp, c, CL, red);
+    if (c == 0 && tid == 0)
+      a.norm_out[(size_t)(a.frames - 1) * a.nslices + s] = (prev_upd && (nn.x > ncap2 || nn.y > ncap2)) ? 1 : 0;
+  }
   // keep the cluster alive until every CTA is done with the shared scratch
   cluster_barrier();
 }
@@ -1457,6 +1533,7 @@ extern "C" int tt_track_rows(void* stream, const tt_rows_args* a) {
       return tt_fail(TT_EINVAL, "fused row sharding needs shard_local and a grid_sync counter");
     if (!a->xw || !a->xg) return tt_fail(TT_EINVAL, "row sharding: null payload buffers");
     if (a->resid_out) return tt_fail(TT_EUNSUPPORTED, "row sharding: residual output not supported");
+    if (a->norm_out) return tt_fail(TT_EUNSUPPORTED, "row sharding: norm_cap flags not supported");
   }
   if (a->t0 < 1) return tt_fail(TT_EINVAL, "t must be >= 1");
   if (a->frames == 0) return TT_OK;

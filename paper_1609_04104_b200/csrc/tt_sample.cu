@@ -183,26 +183,13 @@ __global__ void __launch_bounds__(SMP_NT) draw_wr_kernel(int n, const double* __
   }
 }
 
-// sequential renormalised draws without replacement (draw order)
-__global__ void __launch_bounds__(SMP_NT) draw_wor_kernel(int n, const double* __restrict__ weights, int k,
-                                                          uint64_t k0, uint64_t k1, uint64_t* pos,
-                                                          int32_t* out, int32_t* status, const double* utab) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  double* w = (double*)smem;
-  double* cdf = w + n;
-  double* red = cdf + n;
+// sequential renormalised draws without replacement (draw order) of k items from the weights in w
+// (shared memory, modified), uniforms m = 0..k-1 from the table or the Philox stream at pos p0 + m;
+// out[m] (global) receives draw m
+TT_DEV void wor_draw_block(double* w, double* cdf, double* red, int n, int k, const double* utab, uint64_t k0,
+                           uint64_t k1, uint64_t p0, int32_t* out) {
   __shared__ int sh_amb, sh_idx;
-  const int tid = threadIdx.x, NT = blockDim.x;
-  for (int i = tid; i < n; i += NT) w[i] = weights[i];
-  __syncthreads();
-  int nz = 0;
-  for (int i = tid; i < n; i += NT) nz += w[i] != 0.0;
-  double nzd = block_sum((double)nz, red);
-  if (nzd < (double)k) {
-    if (tid == 0 && status) atomicOr(status, TT_ST_OVERFLOW);
-    return;
-  }
-  const uint64_t p0 = pos ? pos[0] : 0ull;
+  const int tid = threadIdx.x;
   for (int m = 0; m < k; ++m) {
     const double u01 = draw_uniform(utab, k0, k1, p0, (uint64_t)m);
     for (int exact = 0; exact < 2; ++exact) {
@@ -228,7 +215,62 @@ __global__ void __launch_bounds__(SMP_NT) draw_wor_kernel(int n, const double* _
     }
     __syncthreads();
   }
+}
+
+__global__ void __launch_bounds__(SMP_NT) draw_wor_kernel(int n, const double* __restrict__ weights, int k,
+                                                          uint64_t k0, uint64_t k1, uint64_t* pos,
+                                                          int32_t* out, int32_t* status, const double* utab) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* w = (double*)smem;
+  double* cdf = w + n;
+  double* red = cdf + n;
+  const int tid = threadIdx.x, NT = blockDim.x;
+  for (int i = tid; i < n; i += NT) w[i] = weights[i];
+  __syncthreads();
+  int nz = 0;
+  for (int i = tid; i < n; i += NT) nz += w[i] != 0.0;
+  double nzd = block_sum((double)nz, red);
+  if (nzd < (double)k) {
+    if (tid == 0 && status) atomicOr(status, TT_ST_OVERFLOW);
+    return;
+  }
+  const uint64_t p0 = pos ? pos[0] : 0ull;
+  wor_draw_block(w, cdf, red, n, k, utab, k0, k1, p0, out);
   if (tid == 0 && pos) pos[0] = p0 + (uint64_t)k;
+}
+
+// variable_density_rows (observation.py:300-323) for a block of frames of every slice at once: block
+// (f, s) draws frame f of slice s from the Philox stream (key0, key1 + s) at position
+// pos0[s] + f (n_rows - 1): the DC row, then n_rows - 1 sequential draws without replacement with the
+// host's weights d**alpha / 2, in draw order -> out[f][s][n_rows]
+__global__ void __launch_bounds__(SMP_NT) vd_rows_batch_kernel(int nslices, int n, const double* __restrict__ weights,
+                                                               int n_rows, uint64_t k0, uint64_t k1,
+                                                               const uint64_t* __restrict__ pos0, int32_t* out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* w = (double*)smem;
+  double* cdf = w + n;
+  double* red = cdf + n;
+  const int f = blockIdx.x / nslices, s = blockIdx.x % nslices;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] = weights[i];
+  __syncthreads();
+  int32_t* o = out + ((size_t)f * nslices + s) * n_rows;
+  if (threadIdx.x == 0) o[0] = 0;
+  const uint64_t p0 = (pos0 ? pos0[s] : 0ull) + (uint64_t)f * (uint64_t)(n_rows - 1);
+  wor_draw_block(w, cdf, red, n, n_rows - 1, nullptr, k0, k1 + (uint64_t)s, p0, o + 1);
+}
+
+extern "C" int tt_vd_rows_batch(void* stream, int frames, int nslices, int n, const double* weights, int n_rows,
+                                uint64_t key0, uint64_t key1, const uint64_t* pos0, int32_t* out) {
+  if (frames < 0 || nslices < 1 || n < 1 || n_rows < 1 || n_rows > n || !weights || !out)
+    return tt_fail(TT_EINVAL, "tt_vd_rows_batch: bad args");
+  if (frames == 0) return TT_OK;
+  const size_t sm = sizeof(double) * (2 * (size_t)n + 64);
+  if (sm > 220 * 1024) return tt_fail(TT_EUNSUPPORTED, "draw domain too large for one CTA (n=%d)", n);
+  TT_CUDA_TRY(cudaFuncSetAttribute(vd_rows_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  vd_rows_batch_kernel<<<(unsigned)frames * (unsigned)nslices, SMP_NT, sm, (cudaStream_t)stream>>>(
+      nslices, n, weights, n_rows, key0, key1, pos0, out);
+  TT_CUDA_TRY(cudaGetLastError());
+  return TT_OK;
 }
 
 extern "C" int tt_row_scores(void* stream, int nslices, int nx, int ny, int rank, const float* a, double beta,

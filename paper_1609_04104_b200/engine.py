@@ -34,7 +34,7 @@ from . import _lib as L
 from . import _ops as K
 from .tracker import Fixed, HessianBound
 
-__all__ = ["StaticRows", "Informative", "OnlineEngine", "run_online", "OnlineResult", "warm_up", "RowShardedEngine",
+__all__ = ["StaticRows", "Informative", "AdaptiveSchedule", "OnlineEngine", "run_online", "OnlineResult", "warm_up", "RowShardedEngine",
            "InformativeEntries", "StaticEntries", "EntryEngine", "run_batch", "BatchResult", "LocalShardedEngine"]
 
 
@@ -48,13 +48,39 @@ class StaticRows:
 
 @dataclass(frozen=True)
 class Informative:
-    """Subspace-driven row sampling (sampler.row_scores + draw_samples)."""
+    """Subspace-driven row sampling (sampler.row_scores + draw_samples): ``k`` trials from the Philox
+    stream (key0, key1 + slice) starting at word ``pos0``, with replacement (the deduplicated draws) or
+    without (``replacement=False``: k distinct rows by sequential renormalised draws, sampler.py:163-169);
+    the forced rows count toward k."""
 
     k: int
     forced: tuple = (0,)
     beta: float = 0.1
     key0: int = 0
     key1: int = 0
+    replacement: bool = True
+    pos0: int = 0
+
+
+@dataclass(frozen=True)
+class AdaptiveSchedule:
+    """run_adaptive's acquisition schedule (experiment.py:462-497): variable-density rows
+    (variable_density_rows, observation.py:300-323, with ``alpha`` and ``fraction``; DC first, draw order)
+    for the frames before ``switch_frame``, then ``informative`` draws. ``switch_frame`` counts frames from
+    the start of the sequence, warm-up frames included, as the reference's loop index does (None: right
+    after the warm-up, the reference default). Both phases draw from one Philox stream per slice,
+    (informative.key0, informative.key1 + slice) from word informative.pos0, as the reference's single
+    ``rng`` does."""
+
+    informative: Informative
+    switch_frame: int | None = None
+    alpha: float = -1.0
+    fraction: float = 0.25
+
+    def n_rows(self, nx: int) -> int:
+        if not 0.0 < self.fraction <= 1.0:
+            raise ValueError(f"fraction must be in (0, 1], got {self.fraction}")
+        return int(np.ceil(self.fraction * nx))
 
 
 class _Project:
@@ -72,17 +98,24 @@ def _step_params(step):
 
 
 class OnlineEngine:
-    def __init__(self, nx, ny, rank, nslices=1, lam=0.1, step=Fixed(0.01), policy=None, cluster=0, t0=1):
+    """``norm_cap`` (StepConfig.norm_cap, tracker.py:406-408): when set, every frame reports whether its
+    post-update factors exceed the cap in Frobenius norm (``out["norm"]``, StepReport.norm_exceeded)."""
+
+    def __init__(self, nx, ny, rank, nslices=1, lam=0.1, step=Fixed(0.01), policy=None, cluster=0, t0=1,
+                 norm_cap=None):
         if policy is None:
             raise ValueError("policy is required (StaticRows or Informative)")
         self.nx, self.ny, self.rank, self.nslices = int(nx), int(ny), int(rank), int(nslices)
         self.lam = float(lam)
         self.step = step
         self.policy = policy
+        self.norm_cap = None if norm_cap is None else float(norm_cap)
         self.dev = L.device()
         if isinstance(policy, Informative):
             if not 1 <= policy.k <= nx:
                 raise ValueError("informative k must be in [1, nx]")
+            if policy.pos0 < 0:
+                raise ValueError("Philox start position must be nonnegative")
             forced = np.unique(np.asarray(policy.forced, dtype=np.int64))
             if forced.size and (forced.min() < 0 or forced.max() >= nx):
                 raise ValueError("forced index out of range")
@@ -92,15 +125,24 @@ class OnlineEngine:
             self.forced = torch.from_numpy(forced.astype(np.int32)).to(self.dev)
             self.rows_tab = self.rows_cnt = None
         elif isinstance(policy, StaticRows):
-            rows = np.asarray(policy.rows)
-            if rows.ndim == 2:
-                rows = rows[:, None, :]
-            cnt = np.asarray(policy.counts).reshape(rows.shape[0], -1)
-            if rows.shape[1] != nslices or cnt.shape != rows.shape[:2]:
-                raise ValueError("static row table must be (T, nslices, Smax) with counts (T, nslices)")
-            self.max_rows = int(rows.shape[2])
-            self.rows_tab = torch.from_numpy(np.ascontiguousarray(rows, dtype=np.int32)).to(self.dev)
-            self.rows_cnt = torch.from_numpy(np.ascontiguousarray(cnt, dtype=np.int32)).to(self.dev)
+            if isinstance(policy.rows, torch.Tensor) and policy.rows.is_cuda:  # device table (drawn on device)
+                rows = policy.rows if policy.rows.dim() == 3 else policy.rows[:, None, :]
+                cnt = torch.as_tensor(policy.counts).reshape(rows.shape[0], -1)
+                if rows.shape[1] != nslices or tuple(cnt.shape) != tuple(rows.shape[:2]):
+                    raise ValueError("static row table must be (T, nslices, Smax) with counts (T, nslices)")
+                self.max_rows = int(rows.shape[2])
+                self.rows_tab = rows.to(torch.int32).contiguous()
+                self.rows_cnt = cnt.to(self.dev, torch.int32).contiguous()
+            else:
+                rows = np.asarray(policy.rows)
+                if rows.ndim == 2:
+                    rows = rows[:, None, :]
+                cnt = np.asarray(policy.counts).reshape(rows.shape[0], -1)
+                if rows.shape[1] != nslices or cnt.shape != rows.shape[:2]:
+                    raise ValueError("static row table must be (T, nslices, Smax) with counts (T, nslices)")
+                self.max_rows = int(rows.shape[2])
+                self.rows_tab = torch.from_numpy(np.ascontiguousarray(rows, dtype=np.int32)).to(self.dev)
+                self.rows_cnt = torch.from_numpy(np.ascontiguousarray(cnt, dtype=np.int32)).to(self.dev)
             self.forced = None
         else:
             raise TypeError("policy must be StaticRows or Informative")
@@ -111,6 +153,8 @@ class OnlineEngine:
         self.bh = z(nslices, ny, rank)
         self.alpha_bar = torch.zeros(nslices, dtype=torch.float64, device=self.dev)
         self.philox_pos = torch.zeros(nslices, dtype=torch.int64, device=self.dev)
+        if isinstance(policy, Informative) and policy.pos0:
+            self.philox_pos.fill_(int(policy.pos0))
         self.status = torch.zeros(nslices, dtype=torch.int32, device=self.dev)
         self.t = int(t0)
         self.frame = 0
@@ -141,7 +185,7 @@ class OnlineEngine:
         self.t = int(t0)
         self.frame = 0
         self.alpha_bar.zero_()
-        self.philox_pos.zero_()
+        self.philox_pos.fill_(int(self.policy.pos0) if isinstance(self.policy, Informative) else 0)
         self.status.zero_()
 
     def image_factors(self):
@@ -161,6 +205,8 @@ class OnlineEngine:
         if history:
             out["ah"] = torch.empty(frames, ns, self.nx, R, dtype=torch.complex64, device=d)
             out["bh"] = torch.empty(frames, ns, self.ny, R, dtype=torch.complex64, device=d)
+        if self.norm_cap is not None:
+            out["norm"] = torch.empty(frames, ns, dtype=torch.int32, device=d)
         return out
 
     def args(self, kspace: torch.Tensor, frames: int, out: dict, ah_in=None, bh_in=None, ah_out=None,
@@ -191,6 +237,7 @@ class OnlineEngine:
             a.beta = float(self.policy.beta)
             a.key0, a.key1 = int(self.policy.key0), int(self.policy.key1)
             a.philox_pos = self.philox_pos.data_ptr()
+            a.draw_wor = 0 if self.policy.replacement else 1
         else:
             a.policy = L.TT_POLICY_STATIC
             rs = self.nslices * self.max_rows
@@ -211,6 +258,9 @@ class OnlineEngine:
         a.bh_hist = out["bh"].data_ptr() if "bh" in out else None
         a.status = self.status.data_ptr()
         a.scratch = self.scr.buf.data_ptr()
+        if self.norm_cap is not None and "norm" in out:
+            a.norm_cap = self.norm_cap
+            a.norm_out = out["norm"].data_ptr()
         return a
 
     def run(self, kspace: torch.Tensor, frames: int, history: bool = True, out: dict | None = None) -> dict:
@@ -252,6 +302,7 @@ class OnlineResult:
     final_A: np.ndarray
     final_B: np.ndarray
     factor_history: object = None  # (T, nx, R) k-space Ah after each frame (slice 0), device; keep_history=True
+    norm_exceeded: np.ndarray | None = None  # (T, nslices) bool, StepReport.norm_exceeded (norm_cap set)
 
 
 def warm_up(engine: "OnlineEngine", kspace_warm: torch.Tensor, epochs: int) -> None:
@@ -530,19 +581,19 @@ _STREAMS: dict = {}  # device index -> (upload, reconstruction, download) stream
 _ENGINES: dict = {}  # run_online's informative-policy engines, reused across calls of the same configuration
 
 
-def _take_engine(nx, ny, R, ns, lam, step, policy, cluster, t0):
+def _take_engine(nx, ny, R, ns, lam, step, policy, cluster, t0, norm_cap=None):
     """An OnlineEngine for run_online: a cached one (reset) when the configuration repeats, else new.
     The engine is taken out of the cache for the duration of the call (concurrent calls never share)."""
     key = None
     if isinstance(policy, Informative):
         try:
-            key = (torch.cuda.current_device(), nx, ny, R, ns, float(lam), repr(step), policy, int(cluster))
+            key = (torch.cuda.current_device(), nx, ny, R, ns, float(lam), repr(step), policy, int(cluster), norm_cap)
             hash(key)
         except TypeError:
             key = None
     eng = _ENGINES.pop(key, None) if key is not None else None
     if eng is None:
-        eng = OnlineEngine(nx, ny, R, ns, lam, step, policy, cluster, t0)
+        eng = OnlineEngine(nx, ny, R, ns, lam, step, policy, cluster, t0, norm_cap)
     else:
         eng.reset(t0)
     return eng, key
@@ -585,7 +636,7 @@ BLOCK_BYTES = 128 << 20  # run_online's default pipeline block: ~128 MB of truth
 
 
 def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, warm_frames=0,
-               warm_epochs=20, chunk=None, keep_history=False) -> OnlineResult:
+               warm_epochs=20, chunk=None, keep_history=False, norm_cap=None) -> OnlineResult:
     """Public end-to-end call (host in, host out): the online loop over the
     frames of ``kspace`` (T, [nslices,] nx, ny) from image-domain initial
     factors, returning reconstructions and per-frame reports. The analogue of
@@ -593,6 +644,9 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
     the leading frames are fully sampled and tracked for ``warm_epochs`` passes
     first (experiment.py:219-239, default 5 x 20 in the reference config) and
     the results cover the streaming frames only; the policy applies to those.
+    ``policy`` is StaticRows, Informative, AdaptiveSchedule (variable-density rows until the switch
+    frame, then informative draws, experiment.py:462-497) or an entries policy. ``norm_cap`` flags
+    the frames whose post-update factors exceed it (``norm_exceeded``, tracker.py:406-408).
 
     Pipelined in blocks of ``chunk`` frames (default: ~BLOCK_BYTES of truth per block, at most 40
     frames — 40 frames at 256^2 x 1 slice, 4 at config 3's 64 slices, so that the uploads and the
@@ -610,21 +664,32 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
     A0 = np.asarray(A0).reshape(ns, nx, -1)
     R = A0.shape[-1]
     if isinstance(policy, (InformativeEntries, StaticEntries)):
+        if norm_cap is not None:
+            raise ValueError("norm_cap is reported by the row-mask engines")
         return _run_online_entries(src, on_dev, A0, B0, lam, step, policy, clean, t0, warm_frames)
+    sched = policy if isinstance(policy, AdaptiveSchedule) else None
     dev = L.device()
     comp = torch.cuda.current_stream(dev)
     s_in, s_rec, s_out = _pipeline_streams(dev)
     # the engine (cached for repeated informative configurations) and its initial factors first: their
     # small upload must not queue behind the truth uploads on the copy engine
-    eng, ekey = _take_engine(nx, ny, R, ns, lam, step, policy, cluster, t0)
+    eng, ekey = _take_engine(nx, ny, R, ns, lam, step, sched.informative if sched else policy, cluster, t0, norm_cap)
     eng.set_image_factors(A0, np.asarray(B0).reshape(ns, ny, R))
     kd = src.contiguous() if on_dev else torch.empty(T, ns, nx, ny, dtype=torch.complex64, device=dev)
     W = int(warm_frames)
+    if W < 0 or W > T:
+        raise ValueError("warm_frames must be in [0, T]")
+    # AdaptiveSchedule: the variable-density frames [W, W + nvd) first (experiment.py:484-497)
+    nvd = 0
+    if sched is not None:
+        sw = W if sched.switch_frame is None else int(sched.switch_frame)
+        nvd = min(max(sw - W, 0), T - W)
     if chunk is None:
         chunk = min(40, max(1, BLOCK_BYTES // max(1, ns * nx * ny * 8)))
     C = max(1, int(chunk))
-    # upload blocks: the warm-up frames as one block, then the streaming frames in blocks of C
-    bounds = ([(0, W)] if W else []) + _blocks(W, T, C)
+    # upload blocks: the warm-up frames as one block, then the streaming frames in blocks of C (a block
+    # never straddles the switch frame)
+    bounds = ([(0, W)] if W else []) + _blocks(W, W + nvd, C) + _blocks(W + nvd, T, C)
     s_in.wait_stream(comp)
     ev_in = []
     with torch.cuda.stream(s_in):
@@ -643,16 +708,32 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
             clean = np.asarray(clean).reshape(T, ns, nx, ny)[W:]
     Ts = T - W
     ks_stream = kd[W:]
-    out = eng.make_outputs(Ts)
+    # segments of the streaming frames: (engine, outputs, first frame); the VD engine shares the state
+    segs = []
+    if nvd:
+        inf = sched.informative
+        nr = sched.n_rows(nx)
+        tab = K.vd_rows_batch(nvd, ns, nx, float(sched.alpha), nr, (int(inf.key0), int(inf.key1)), eng.philox_pos)
+        veng = OnlineEngine(nx, ny, R, ns, lam, step,
+                            StaticRows(tab, torch.full((nvd, ns), nr, dtype=torch.int32, device=dev)), cluster,
+                            eng.t, norm_cap)
+        veng.ah, veng.bh, veng.alpha_bar, veng.status = eng.ah, eng.bh, eng.alpha_bar, eng.status
+        eng.philox_pos += nvd * (nr - 1)  # the informative draws continue the stream
+        segs.append((veng, veng.make_outputs(nvd), 0))
+    if Ts - nvd > 0 or not segs:
+        segs.append((eng, eng.make_outputs(Ts - nvd), nvd))
     recon = Xd = None
+    hist = torch.empty(Ts, nx, R, dtype=torch.complex64, device=dev) if keep_history else None
     # tracking blocks run back to back on the compute stream; each block's reconstruction runs on its
     # own stream once the block's tracking is done, and its download follows on the copy stream
-    hist = {k: out[k].clone() for k in ("ah",)} if keep_history else None
     for (f0, f1), ev in blocks:
         a, b = f0 - W, f1 - W
+        e, out, base = segs[-1] if a >= segs[-1][2] else segs[0]
+        if e is eng and nvd and e.frame < nvd:  # hand over from the VD phase: same state, next frame, t
+            e.frame, e.t = nvd, segs[0][0].t
         comp.wait_event(ev)
-        part = {k: v[a:b] for k, v in out.items()}
-        eng.run(ks_stream, b - a, out=part)
+        part = {k: v[a - base:b - base] for k, v in out.items()}
+        e.run(ks_stream, b - a, out=part)
         if recon is None:  # the result buffers are set up while the first block tracks
             recon = torch.empty(Ts, ns, nx, ny, dtype=torch.complex64, pin_memory=True)
             Xd = torch.empty(Ts, ns, nx, ny, dtype=torch.complex64, device=dev)
@@ -663,8 +744,8 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
         s_rec.wait_event(tracked)
         with torch.cuda.stream(s_rec):
             if keep_history:
-                hist["ah"][a:b].copy_(part["ah"])
-            eng.reconstruct(part, into=Xd[a:b], in_place=True)  # the history is not needed afterwards
+                hist[a:b].copy_(part["ah"][:, 0])
+            e.reconstruct(part, into=Xd[a:b], in_place=True)  # the history is not needed afterwards
             done = torch.cuda.Event()
             done.record(s_rec)
         s_out.wait_event(done)
@@ -676,9 +757,13 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
     comp.wait_stream(s_rec)
     # small results, final factors and the status word: asynchronous copies into pinned memory, one sync
     pinned = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True)  # noqa: E731
-    small = {k: pinned(out[k]) for k in ("gamma", "cost", "mu", "cnt", "rows")}
-    for k, v in small.items():
-        v.copy_(out[k], non_blocking=True)
+    keys = ("gamma", "cost", "mu", "cnt", "rows") + (("norm",) if norm_cap is not None else ())
+    small = []
+    for _, out, _ in segs:
+        sm = {k: pinned(out[k]) for k in keys}
+        for k, v in sm.items():
+            v.copy_(out[k], non_blocking=True)
+        small.append(sm)
     Ad, Bd = eng.image_factors()
     A, B, st = pinned(Ad), pinned(Bd), pinned(eng.status)
     A.copy_(Ad, non_blocking=True)
@@ -692,12 +777,14 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
     s_out.synchronize()
     L.raise_status(int(st.max().item()), "online engine")
     _give_engine(ekey, eng)
-    cnt = small["cnt"].numpy()
-    rows_np = small["rows"].numpy()
-    rows = [[rows_np[f, s, :cnt[f, s]].astype(np.int64) for s in range(ns)] for f in range(Ts)]
-    return OnlineResult(recon=recon.numpy(), gamma=small["gamma"].numpy(), cost=small["cost"].numpy(),
-                        mu=small["mu"].numpy(), rows=rows, nmse=nm, final_A=A.numpy(), final_B=B.numpy(),
-                        factor_history=hist["ah"][:, 0] if keep_history else None)
+    cat = lambda k: np.concatenate([sm[k].numpy() for sm in small], axis=0)  # noqa: E731
+    rows = []
+    for sm in small:
+        cnt, rows_np = sm["cnt"].numpy(), sm["rows"].numpy()
+        rows += [[rows_np[f, s, :cnt[f, s]].astype(np.int64) for s in range(ns)] for f in range(cnt.shape[0])]
+    return OnlineResult(recon=recon.numpy(), gamma=cat("gamma"), cost=cat("cost"), mu=cat("mu"), rows=rows, nmse=nm,
+                        final_A=A.numpy(), final_B=B.numpy(), factor_history=hist,
+                        norm_exceeded=cat("norm").astype(bool) if norm_cap is not None else None)
 
 
 class LocalShardedEngine:
