@@ -8,6 +8,7 @@ sm_100a CUDA library ``libtensortrack_b200.so`` (C ABI in
 anywhere, but every compute call needs a CUDA device and the built library.
 """
 
+from . import checkpoint
 from .core import (TensorSubspace, outer_rank_one, rank_surrogate, rebalance, refold, singular_values,
                    synthesize_slice, unfold)
 from .engine import (AdaptiveSchedule, BatchResult, EntryEngine, Informative, InformativeEntries, LocalShardedEngine, OnlineEngine,
@@ -59,7 +60,7 @@ from .acquisition import StreamingProvider, measure, project
 from .patches import PatchedResult, draw_frame_entries, full_entries, init_patch_factors, run_tracking_patched
 from .cten import CtenFormatError, read_cten, read_cten_tensor, write_cten
 from .reports import (MetricRow, online_budget_rows, online_mask_rows, write_budget_csv, write_mask_csv,
-                      write_metrics_csv, write_trace_csv)
+                      write_manifest, write_metrics_csv, write_trace_csv)
 
 __all__ = [
     "TensorSubspace", "rebalance", "synthesize_slice", "outer_rank_one", "singular_values", "rank_surrogate",
@@ -78,5 +79,5 @@ __all__ = [
     "NumericalError", "ConfigError", "nmse", "nmse_frames", "StreamingProvider", "measure", "project",
     "CtenFormatError", "read_cten", "read_cten_tensor", "write_cten",
     "MetricRow", "write_metrics_csv", "write_mask_csv", "write_trace_csv", "write_budget_csv",
-    "online_mask_rows", "online_budget_rows",
+    "online_mask_rows", "online_budget_rows", "write_manifest", "checkpoint",
 ]

@@ -20,7 +20,7 @@ import torch
 from . import _ops as K
 
 __all__ = ["MetricRow", "write_metrics_csv", "write_mask_csv", "write_trace_csv", "write_budget_csv",
-           "online_mask_rows", "online_budget_rows"]
+           "online_mask_rows", "online_budget_rows", "write_manifest"]
 
 
 @dataclass
@@ -69,15 +69,24 @@ def write_budget_csv(path, rows) -> None:
 
 
 def online_mask_rows(result, t0: int = 0, slice_index: int = 0) -> list[tuple]:
-    """(t, i) per sampled row, frames numbered from ``t0`` (experiment.py:495-510)."""
-    return [(t0 + f, int(i)) for f, rows in enumerate(result.rows) for i in rows[slice_index]]
+    """(t, i) per sampled row, frames numbered from ``t0``, each frame's rows ascending as the reference
+    records both its variable-density and its informative masks (experiment.py:495, :507)."""
+    return [(t0 + f, int(i)) for f, rows in enumerate(result.rows) for i in np.sort(rows[slice_index])]
 
 
 def online_budget_rows(result, A0, B0, k_draws: int, beta: float = 0.1, t0: int = 0,
-                       slice_index: int = 0) -> list[tuple]:
-    """(t, K, |Omega_t|, E|Omega_t|) per frame: the expected distinct count sum_i 1 - (1 - p_i)^K
-    under frame t's row scores, computed on the device from the pre-update factors (A0 for the first
-    frame, then the previous frame's factors from the run's history)."""
+                       slice_index: int = 0, replacement: bool = True, vd_frames: int = 0) -> list[tuple]:
+    """(t, K, |Omega_t|, E|Omega_t|) per frame (experiment.py:496, :508-509): for the first ``vd_frames``
+    (an AdaptiveSchedule's variable-density frames) (t, |rows|, |rows|, |rows|); for informative frames
+    with replacement the expected distinct count sum_i 1 - (1 - p_i)^K under frame t's row scores,
+    computed on the device from the pre-update factors (A0 for the first frame, then the previous
+    frame's factors from the run's history); without replacement the plan size."""
+    if not replacement or len(result.rows) <= vd_frames:
+        out = []
+        for f in range(len(result.rows)):
+            m = len(result.rows[f][slice_index])
+            out.append((t0 + f, m, m, float(m)) if f < vd_frames else (t0 + f, int(k_draws), m, float(m)))
+        return out
     hist = getattr(result, "factor_history", None)
     if hist is None:
         raise ValueError("the result carries no factor history (run_online(..., keep_history=True))")
@@ -89,5 +98,36 @@ def online_budget_rows(result, A0, B0, k_draws: int, beta: float = 0.1, t0: int 
     ny = int(np.asarray(B0).shape[0])
     p = K.row_scores(pre.contiguous(), ny, beta)  # (T, nx) fp64
     expected = (1.0 - (1.0 - p) ** int(k_draws)).sum(dim=1).cpu().numpy()
-    return [(t0 + f, int(k_draws), len(result.rows[f][slice_index]), float(expected[f]))
-            for f in range(len(result.rows))]
+    out = []
+    for f in range(len(result.rows)):
+        m = len(result.rows[f][slice_index])
+        out.append((t0 + f, m, m, float(m)) if f < vd_frames else (t0 + f, int(k_draws), m, float(expected[f])))
+    return out
+
+
+def write_manifest(path, mode: str, input_path, config: dict, per_frame_ms, nmse_values, total_s: float,
+                   commit: str | None = None) -> dict:
+    """manifest.json as run_experiment writes it (experiment.py:727-741): mode, input path, the config
+    echo, the git commit, timings (total seconds, per-frame milliseconds rounded to 3 places) and the
+    mean NMSE; indent 2, sorted keys, trailing newline. Returns the dict."""
+    import json
+    import subprocess
+
+    if commit is None:
+        try:
+            out = subprocess.run(["git", "rev-parse", "HEAD"], capture_output=True, text=True, timeout=5, check=False)
+            commit = out.stdout.strip() if out.returncode == 0 else "unknown"
+        except OSError:
+            commit = "unknown"
+    manifest = {
+        "mode": mode,
+        "input": str(input_path),
+        "config": config,
+        "commit": commit,
+        "timings": {"total_s": float(total_s), "per_frame_ms": [round(float(x), 3) for x in per_frame_ms]},
+        "mean_nmse": float(np.mean(np.asarray(nmse_values, dtype=float))),
+    }
+    with open(path, "w", encoding="utf-8") as fh:
+        json.dump(manifest, fh, indent=2, sort_keys=True)
+        fh.write("\n")
+    return manifest
