@@ -139,7 +139,21 @@ typedef struct tt_rows_args {
    * row sharding. */
   double norm_cap;
   int32_t* norm_out;
+  /* Informative draws under row sharding (appended; NULL = off): the raw row scores of all nx rows
+   * (tt_rows_shard_scores over the all-gathered row energies), identical on every rank, so every rank
+   * draws the same rows from the shared Philox stream. Phase 1 only, one GPU per rank: the full drawn
+   * row set goes to rows_out / cnt_out (frame 0 slots), which the caller passes to phase 2 as its
+   * static table. */
+  const double* sraw_in;
 } tt_rows_args;
+/* Row energies of a rank's owned k-space rows: energy [nx][rank] (fp64) gets E[i][r] = |Ah_ir|^2 for the owned
+ * rows [r0, r0 + nrows) (ah_rows [nrows][rank] complex64) and 0 elsewhere, so a sum all-reduce over the ranks
+ * assembles the full matrix exactly (x + 0 = x). */
+int tt_rows_shard_energy(void* stream, int nx, int rank, int r0, int nrows, const float* ah_rows, double* energy);
+/* Raw row scores from the full energy matrix (row_scores before normalisation, sampler.py:115-126):
+ * nrm_r = sum_i E[i][r] (fixed order), s_i = (ny sum_r E[i][r] / nrm_r + R) / (R (nx + ny)) -> sraw [nx];
+ * a zero column ORs TT_ST_ZEROCOL into status[0]. Identical bits on every rank for identical inputs. */
+int tt_rows_shard_scores(void* stream, int nx, int ny, int rank, const double* energy, double* sraw, int32_t* status);
 /* plan of a row-mask launch at `cluster` (0: smallest that fits): out[6] = cluster, rows per k tile,
  * shared-memory bytes, tight plan (0/1), padded Y row stride, K-split buffer entries (diagnostics) */
 int tt_rows_plan_info(int nx, int ny, int rank, int max_rows, int cluster, int* out);

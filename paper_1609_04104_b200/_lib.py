@@ -48,7 +48,7 @@ class RowsArgs(C.Structure):
         ("cnt_out", _p), ("resid_out", _p), ("ah_hist", _p), ("bh_hist", _p), ("status", _p), ("scratch", _p),
         ("phase_clock", _p), ("shard_rank", _i32), ("shard_world", _i32), ("shard_phase", _i32), ("xw", _p),
         ("xg", _p), ("shard_local", _i32), ("shard_fused", _i32), ("grid_sync", _p),
-        ("draw_wor", _i32), ("norm_cap", _f64), ("norm_out", _p),
+        ("draw_wor", _i32), ("norm_cap", _f64), ("norm_out", _p), ("sraw_in", _p),
     ]
 
 
@@ -95,6 +95,8 @@ SIGNATURES = {
     "tt_cten_write": (C.c_int, [C.c_char_p, _p, C.c_int, C.c_int, C.c_int, _p]),
     "tt_draw_with_replacement_large": (C.c_int, [_p, C.c_int, _p, C.c_int, _p, C.c_int, C.c_uint64, C.c_uint64, _p,
                                                  _p, _p, _p]),
+    "tt_rows_shard_energy": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, C.c_int, _p, _p]),
+    "tt_rows_shard_scores": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, _p, _p, _p]),
     "tt_vd_rows_batch": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, _p, C.c_int, C.c_uint64, C.c_uint64, _p, _p]),
     "tt_terms_scratch_bytes": (C.c_size_t, [C.c_int, C.c_int, C.c_int]),
     "tt_residual": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, C.c_int, _p, _p, _p, _p, _p, _p]),

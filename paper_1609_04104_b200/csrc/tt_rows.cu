@@ -679,6 +679,10 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
 
     }  // phase != 2
     if (a.policy == TT_POLICY_INFORMATIVE) {
+      // row sharding: every rank draws the frame's rows from the same full raw-score vector (sraw_in,
+      // built from the all-gathered row energies); otherwise each CTA scores its own rows
+      const double* sraw = a.sraw_in ? a.sraw_in : g_sraw;
+      if (!a.sraw_in) {
       // raw row scores for own rows (sampler.py:77-85, :126)
       const double cs = (double)ny, cr = (double)R, cd = 1.0 / ((double)R * (double)(nx + ny));
       // tpr lanes per row (rank terms split, fixed-order butterfly), so the fp64 chain is R / tpr long
@@ -699,6 +703,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       if (tid < R && nrm[tid] == 0.0) atomicOr(&sh_err, TT_ST_ZEROCOL);
       STAMP(3);
       cluster_barrier();  // -------------------------------------------- B2
+      }
       STAMP(4);
       const bool wor = a.draw_wor != 0;
       if (nx <= 4 * NT && !wor) {
@@ -713,7 +718,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         double loc = 0.0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          sv[j] = (j < ipt && r0 + j < r1) ? __ldcg(&g_sraw[r0 + j]) : 0.0;
+          sv[j] = (j < ipt && r0 + j < r1) ? __ldcg(&sraw[r0 + j]) : 0.0;
           loc += sv[j];
         }
         double S1;
@@ -765,7 +770,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         // of the probabilities, cdf /= cdf[-1], per-draw searchsorted, forced union, compaction;
         // draws without replacement: the sequential renormalised draws over the same probabilities
         if (nx > 4 * NT || wor) {
-          for (int i = tid; i < nx; i += NT) pbuf[i] = __ldcg(&g_sraw[i]);
+          for (int i = tid; i < nx; i += NT) pbuf[i] = __ldcg(&sraw[i]);
           __syncthreads();
           double S1;
           const double loc = block_sum_range(pbuf, nx, red, S1);
@@ -821,6 +826,32 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         }
       }
       ppos += (uint64_t)max(a.k_draws - a.nforced, 0);
+      if (shard) {
+        // the frame's full row set -> rows_out / cnt_out (the host hands it to phase 2 as its static
+        // table), then keep this rank's rows like a static table
+        __syncthreads();
+        const int Sall = sh_S;
+        Sglob = Sall;
+        if (c == 0) {
+          for (int k = tid; a.rows_out && k < Smax; k += NT) a.rows_out[k] = k < Sall ? rows[k] : -1;
+          if (tid == 0 && a.cnt_out) a.cnt_out[0] = Sall;
+        }
+        __syncthreads();
+        if (warp == 0) {
+          int cnt = 0;
+          for (int base = 0; base < Sall; base += 32) {
+            const int k = base + lane;
+            const int i = k < Sall ? rows[k] : -1;
+            const bool keep = i >= R0 && i < R0 + nxs;
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            __syncwarp();
+            if (keep) rows[cnt + __popc(m & ((1u << lane) - 1u))] = i;
+            cnt += __popc(m);
+            __syncwarp();
+          }
+          if (lane == 0) sh_S = cnt;
+        }
+      }
       STAMP(20);
     } else if (fused && phase == 2) {
       // the frame's row table (this rank's share, filtered in phase 1) is still in shared memory
@@ -1500,6 +1531,70 @@ extern "C" int tt_rows_shard_reduce(void* stream, int world, int ny, int rank, d
   return TT_OK;
 }
 
+// ---------------------------------------------------------------- informative draws under row sharding
+__global__ void shard_energy_kernel(int nx, int R, int r0, int nrows, const float2* __restrict__ a,
+                                    double* __restrict__ e) {
+  const int n = nx * R;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int row = i / R;
+    double v = 0.0;
+    if (row >= r0 && row < r0 + nrows) {
+      const float2 x = a[(size_t)(row - r0) * R + (i - row * R)];
+      v = (double)x.x * x.x + (double)x.y * x.y;
+    }
+    e[i] = v;
+  }
+}
+
+extern "C" int tt_rows_shard_energy(void* stream, int nx, int rank, int r0, int nrows, const float* ah_rows,
+                                    double* energy) {
+  if (nx < 1 || rank < 1 || r0 < 0 || nrows < 0 || r0 + nrows > nx || !energy || (nrows > 0 && !ah_rows))
+    return tt_fail(TT_EINVAL, "tt_rows_shard_energy: bad args");
+  const int n = nx * rank;
+  shard_energy_kernel<<<(n + 255) / 256 < 592 ? (n + 255) / 256 : 592, 256, 0, (cudaStream_t)stream>>>(
+      nx, rank, r0, nrows, (const float2*)ah_rows, energy);
+  TT_CUDA_TRY(cudaGetLastError());
+  return TT_OK;
+}
+
+// one CTA: column sums of the energy matrix in a fixed order (thread (r, part) sums rows part, part + P, ...,
+// then the parts in order), then every row's raw score with the rows kernel's formula
+__global__ void __launch_bounds__(256) shard_scores_kernel(int nx, int ny, int R, const double* __restrict__ e,
+                                                           double* __restrict__ sraw, int32_t* status) {
+  __shared__ double part[256];
+  __shared__ double inrm[64];
+  const int tid = threadIdx.x, P = blockDim.x / R;
+  if (tid < P * R) {
+    const int r = tid % R, p = tid / R;
+    double acc = 0.0;
+    for (int i = p; i < nx; i += P) acc += e[(size_t)i * R + r];
+    part[p * R + r] = acc;
+  }
+  __syncthreads();
+  if (tid < R) {
+    double n2 = 0.0;
+    for (int p = 0; p < P; ++p) n2 += part[p * R + tid];
+    inrm[tid] = n2 > 0.0 ? fast_rcp(n2) : 0.0;
+    if (n2 == 0.0 && status) atomicOr(status, TT_ST_ZEROCOL);
+  }
+  __syncthreads();
+  const double cs = (double)ny, cr = (double)R, cd = 1.0 / ((double)R * (double)(nx + ny));
+  for (int i = tid; i < nx; i += blockDim.x) {
+    double acc = 0.0;
+    for (int r = 0; r < R; ++r) acc = fma(e[(size_t)i * R + r], inrm[r], acc);
+    sraw[i] = (cs * acc + cr) * cd;
+  }
+}
+
+extern "C" int tt_rows_shard_scores(void* stream, int nx, int ny, int rank, const double* energy, double* sraw,
+                                    int32_t* status) {
+  if (nx < 1 || ny < 1 || rank < 1 || rank > 64 || !energy || !sraw)
+    return tt_fail(TT_EINVAL, "tt_rows_shard_scores: bad args");
+  shard_scores_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(nx, ny, rank, energy, sraw, status);
+  TT_CUDA_TRY(cudaGetLastError());
+  return TT_OK;
+}
+
 extern "C" size_t tt_rows_scratch_bytes(int nslices, int nx, int ny, int rank, int max_rows, int cluster) {
   if (cluster < 1) cluster = 16;
   return rows_scratch_layout(nx, ny, rank, max_rows, cluster).per_slice * (size_t)(nslices > 0 ? nslices : 1);
@@ -1526,9 +1621,12 @@ extern "C" int tt_track_rows(void* stream, const tt_rows_args* a) {
     if (a->shard_rank < 0 || a->shard_rank >= a->shard_world || (a->shard_phase != 1 && a->shard_phase != 2))
       return tt_fail(TT_EINVAL, "row sharding: need 0 <= rank < world and phase 1 or 2");
     const bool fused = a->shard_local && a->shard_fused;
-    if (a->policy != TT_POLICY_STATIC || a->nslices != 1 || (a->frames != 1 && !fused) || a->y_mode != TT_Y_GATHER)
-      return tt_fail(TT_EUNSUPPORTED, "row sharding supports static row tables, one slice, one frame per launch "
-                                      "(any number when fused), gathered measurements");
+    const bool inf_ok = a->policy == TT_POLICY_INFORMATIVE && a->shard_phase == 1 && a->sraw_in && !a->shard_local;
+    if ((a->policy != TT_POLICY_STATIC && !inf_ok) || a->nslices != 1 || (a->frames != 1 && !fused) ||
+        a->y_mode != TT_Y_GATHER)
+      return tt_fail(TT_EUNSUPPORTED, "row sharding supports static row tables (informative draws in phase 1 "
+                                      "with sraw_in, one GPU per rank), one slice, one frame per launch (any "
+                                      "number when fused), gathered measurements");
     if (a->shard_fused && (!a->shard_local || !a->grid_sync))
       return tt_fail(TT_EINVAL, "fused row sharding needs shard_local and a grid_sync counter");
     if (!a->xw || !a->xg) return tt_fail(TT_EINVAL, "row sharding: null payload buffers");

@@ -1126,28 +1126,83 @@ def run_batch(kspace, A0, B0, lam, step, rows, counts, epochs=1, rng=None, reshu
                        orders=orders, final_A=h["A"], final_B=h["B"], t=t)
 
 
-class RowShardedEngine:
-    """One rank of the row-sharded online loop (BASELINE config 4).
+class RowShardLoop:
+    """Host orchestration of one rank of the row-sharded online loop (BASELINE config 4),
+    independent of where the phases run. Per frame:
 
-    The rank owns k-space rows [r0, r1) of Ah; Bh is replicated. Per frame:
-    ``tt_track_rows`` phase 1 (partials of W, GA, ||Y||^2, ||Ah||^2 over the
-    rank's sampled rows) -> sum-all-reduce of the payload across ranks
-    (``allreduce``, NCCL over NVLink by default) -> phase 2 (redundant fp64
-    solve, update of the owned rows and the replicated Bh). Static row masks.
+    1. informative draws only: the rank's row energies |Ah_ir|^2 into a zeroed full (nx, R) fp64 matrix,
+       summed over the ranks (``allreduce``; x + 0 = x, so every rank gets the exact full matrix) and
+       turned into raw row scores (``_scores``) — every rank then draws the same rows;
+    2. phase 1 (``_phase1``): the rank's partials W, GA, ||Y||^2, ||Ah||^2 into ``payload`` (float64, the
+       kernel layout of ``sharding.pack_payload``);
+    3. ONE sum all-reduce of ``payload`` across the ranks;
+    4. phase 2 (``_phase2``): redundant fp64 solve, update of the owned rows and the replicated Bh.
+
+    ``allreduce(tensor)`` sums in place over the ranks (NCCL over NVLink in ``RowShardedEngine``; gloo
+    in the CPU tests). Subclasses provide the buffers and the phases."""
+
+    informative = False
+
+    def _frame(self, kspace, f, out, fo):
+        if self.informative:
+            self._energy()
+            self.allreduce(self.energy)
+            self._scores()
+        self._phase1(kspace, f)
+        self.allreduce(self.payload)  # one sum over the ranks per frame (SURVEY §8e)
+        self._phase2(kspace, f, out, fo)
+        self.t += 1
+        self.frame += 1
+
+    def run_frames(self, kspace, frames, out):
+        for fo in range(frames):
+            self._frame(kspace, self.frame, out, fo)
+        return out
+
+
+class RowShardedEngine(RowShardLoop):
+    """One rank (one GPU) of the row-sharded online loop (BASELINE config 4) on the device.
+
+    The rank owns k-space rows [r0, r1) of Ah; Bh is replicated. ``rows``/``counts`` give static row
+    tables, or ``rows`` is an :class:`Informative` policy (every rank draws the same rows from the same
+    Philox stream and the all-reduced row energies; the drawn set goes from phase 1 to phase 2 on the
+    device). ``allreduce`` defaults to ``torch.distributed.all_reduce`` (NCCL). ``run(graph=True)`` captures
+    the whole T-frame chain — kernels and NCCL collectives — in one CUDA graph (the first frame runs
+    eagerly to settle one-time launch attributes and communicator setup) and replays it.
     """
 
-    def __init__(self, nx, ny, rank, lam, step, rows, counts, world, rank_id, cluster=0, t0=1, allreduce=None):
-        from .sharding import row_partition
+    def __init__(self, nx, ny, rank, lam, step, rows, counts=None, world=1, rank_id=0, cluster=0, t0=1,
+                 allreduce=None):
+        from .sharding import payload_doubles, row_partition
 
         self.nx, self.ny, self.R = int(nx), int(ny), int(rank)
         self.world, self.rank_id = int(world), int(rank_id)
+        if not 0 <= self.rank_id < self.world:
+            raise ValueError("need 0 <= rank_id < world")
         self.r0, self.r1 = row_partition(self.nx, self.world, self.rank_id)
         self.lam, self.step = float(lam), step
         self.dev = L.device()
-        rows = np.asarray(rows).reshape(np.asarray(rows).shape[0], -1)
-        self.max_rows = int(rows.shape[1])
-        self.rows_tab = torch.from_numpy(np.ascontiguousarray(rows, dtype=np.int32)).to(self.dev)
-        self.rows_cnt = torch.from_numpy(np.ascontiguousarray(np.asarray(counts).reshape(-1), dtype=np.int32)).to(self.dev)
+        self.policy = rows if isinstance(rows, Informative) else None
+        self.informative = self.policy is not None
+        if self.informative:
+            pol = self.policy
+            if not 1 <= pol.k <= self.nx or not pol.replacement:
+                raise ValueError("sharded informative draws: 1 <= k <= nx, with replacement")
+            forced = np.unique(np.asarray(pol.forced, dtype=np.int64))
+            if forced.size > pol.k or (forced.size and (forced.min() < 0 or forced.max() >= self.nx)):
+                raise ValueError("bad forced rows")
+            self.forced = torch.from_numpy(forced.astype(np.int32)).to(self.dev)
+            self.max_rows = int(pol.k)
+            self.philox_pos = torch.full((1,), int(pol.pos0), dtype=torch.int64, device=self.dev)
+            self.energy = torch.zeros(self.nx, self.R, dtype=torch.float64, device=self.dev)
+            self.sraw = torch.zeros(self.nx, dtype=torch.float64, device=self.dev)
+            self.rows_tab = None
+        else:
+            rows = np.asarray(rows).reshape(np.asarray(rows).shape[0], -1)
+            self.max_rows = int(rows.shape[1])
+            self.rows_tab = torch.from_numpy(np.ascontiguousarray(rows, dtype=np.int32)).to(self.dev)
+            self.rows_cnt = torch.from_numpy(np.ascontiguousarray(np.asarray(counts).reshape(-1),
+                                                                  dtype=np.int32)).to(self.dev)
         self.scr = K.RowsScratch(1, self.nx, self.ny, self.R, self.max_rows, cluster)
         self.cluster = self.scr.cluster
         self.ah = torch.zeros(self.r1 - self.r0, self.R, dtype=torch.complex64, device=self.dev)
@@ -1155,13 +1210,14 @@ class RowShardedEngine:
         # the frame's payload in one fp64 buffer: W (ny x R complex128) then GA / ||Y||^2 / ||Ah||^2, so one
         # all-reduce per frame carries all of it
         nw = 2 * self.ny * self.R
-        self.payload = torch.zeros(nw + int(L.lib().tt_rows_shard_xg_len(self.R)), dtype=torch.float64, device=self.dev)
+        self.payload = torch.zeros(payload_doubles(self.ny, self.R), dtype=torch.float64, device=self.dev)
         self.xw = self.payload[:nw].view(torch.complex128).view(self.ny, self.R)
         self.xg = self.payload[nw:]
         self.alpha_bar = torch.zeros(1, dtype=torch.float64, device=self.dev)
         self.status = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.t = int(t0)
         self.frame = 0
+        self._keep = []
         if allreduce is None:
             import torch.distributed as dist
 
@@ -1179,11 +1235,15 @@ class RowShardedEngine:
 
     def make_outputs(self, frames):
         d = self.dev
-        return dict(gamma=torch.empty(frames, self.R, dtype=torch.complex64, device=d),
-                    cost=torch.empty(frames, dtype=torch.float64, device=d),
-                    mu=torch.empty(frames, dtype=torch.float64, device=d),
-                    ah=torch.empty(frames, self.r1 - self.r0, self.R, dtype=torch.complex64, device=d),
-                    bh=torch.empty(frames, self.ny, self.R, dtype=torch.complex64, device=d))
+        out = dict(gamma=torch.empty(frames, self.R, dtype=torch.complex64, device=d),
+                   cost=torch.empty(frames, dtype=torch.float64, device=d),
+                   mu=torch.empty(frames, dtype=torch.float64, device=d),
+                   ah=torch.empty(frames, self.r1 - self.r0, self.R, dtype=torch.complex64, device=d),
+                   bh=torch.empty(frames, self.ny, self.R, dtype=torch.complex64, device=d))
+        if self.informative:  # each frame's drawn rows (all ranks'), sorted, -1 padded
+            out["rows"] = torch.full((frames, self.max_rows), -1, dtype=torch.int32, device=d)
+            out["cnt"] = torch.zeros(frames, dtype=torch.int32, device=d)
+        return out
 
     def _args(self, kspace, f, out, fo, phase):
         mode, mu, cf, cc = _step_params(self.step)
@@ -1193,9 +1253,26 @@ class RowShardedEngine:
         a.ah_in = a.ah_out = self.ah.data_ptr()
         a.bh_in = a.bh_out = self.bh.data_ptr()
         a.alpha_bar = self.alpha_bar.data_ptr()
-        a.policy = L.TT_POLICY_STATIC
-        a.rows_tab = self.rows_tab.data_ptr() + 4 * f * self.max_rows
-        a.rows_cnt = self.rows_cnt.data_ptr() + 4 * f
+        if self.informative and phase == 1:
+            pol = self.policy
+            a.policy = L.TT_POLICY_INFORMATIVE
+            a.k_draws = int(pol.k)
+            a.forced = self.forced.data_ptr() if self.forced.numel() else None
+            a.nforced = int(self.forced.numel())
+            a.beta = float(pol.beta)
+            a.key0, a.key1 = int(pol.key0), int(pol.key1)
+            a.philox_pos = self.philox_pos.data_ptr()
+            a.sraw_in = self.sraw.data_ptr()
+            a.rows_out = out["rows"][fo].data_ptr()  # the drawn set, read back by phase 2
+            a.cnt_out = out["cnt"][fo:].data_ptr()
+        elif self.informative:
+            a.policy = L.TT_POLICY_STATIC
+            a.rows_tab = out["rows"][fo].data_ptr()
+            a.rows_cnt = out["cnt"][fo:].data_ptr()
+        else:
+            a.policy = L.TT_POLICY_STATIC
+            a.rows_tab = self.rows_tab.data_ptr() + 4 * f * self.max_rows
+            a.rows_cnt = self.rows_cnt.data_ptr() + 4 * f
         a.y_mode = L.TT_Y_GATHER
         a.ysrc = kspace[f].data_ptr()
         a.y_frame_stride, a.y_slice_stride = self.nx * self.ny, self.nx * self.ny
@@ -1210,23 +1287,93 @@ class RowShardedEngine:
         a.scratch = self.scr.buf.data_ptr()
         a.shard_rank, a.shard_world, a.shard_phase = self.rank_id, self.world, phase
         a.xw, a.xg = self.xw.data_ptr(), self.xg.data_ptr()
+        self._keep.append(a)
         return a
 
-    def partial(self, kspace, f):
-        K.track_rows(self._args(kspace, f, None, 0, 1))
+    # ---- the phases on the device
+    def _energy(self):
+        L.check(L.lib().tt_rows_shard_energy(L.stream_ptr(), self.nx, self.R, self.r0, self.r1 - self.r0,
+                                             self.ah.data_ptr(), self.energy.data_ptr()), "shard energy")
+
+    def _scores(self):
+        L.check(L.lib().tt_rows_shard_scores(L.stream_ptr(), self.nx, self.ny, self.R, self.energy.data_ptr(),
+                                             self.sraw.data_ptr(), self.status.data_ptr()), "shard scores")
+
+    def _phase1(self, kspace, f):
+        K.track_rows(self._args(kspace, f, self._out, self._fo, 1))
+
+    def _phase2(self, kspace, f, out, fo):
+        K.track_rows(self._args(kspace, f, out, fo, 2))
+
+    def _frame(self, kspace, f, out, fo):
+        self._out, self._fo = out, fo
+        super()._frame(kspace, f, out, fo)
+
+    # ---- the per-frame API of the emulation tests
+    def partial(self, kspace, f, out=None, fo=0):
+        if self.informative:
+            self._energy()
+            self.allreduce(self.energy)
+            self._scores()
+        self._out, self._fo = out, fo
+        self._phase1(kspace, f)
 
     def finish(self, kspace, f, out, fo):
-        K.track_rows(self._args(kspace, f, out, fo, 2))
+        self._phase2(kspace, f, out, fo)
         self.t += 1
         self.frame += 1
 
-    def run(self, kspace, frames, out=None):
-        """kspace: (T, nx, ny) complex64 CUDA (full frames). Frames from the current index."""
+    def save(self):
+        """A copy of the rank's state (factors, step accumulator, Philox position, status, t, frame)."""
+        return (self.ah.clone(), self.bh.clone(), self.alpha_bar.clone(),
+                self.philox_pos.clone() if self.informative else None, self.status.clone(), self.t, self.frame)
+
+    def restore(self, saved):
+        """Back to a :meth:`save`d state, into the same buffers (a captured graph stays valid)."""
+        ah, bh, ab, pp, st, t, f = saved
+        self.ah.copy_(ah)
+        self.bh.copy_(bh)
+        self.alpha_bar.copy_(ab)
+        if pp is not None:
+            self.philox_pos.copy_(pp)
+        self.status.copy_(st)
+        self.t, self.frame = t, f
+
+    def capture(self, kspace, frames, out):
+        """Capture the next ``frames`` frames — energies, scores, both phases and the NCCL collectives —
+        into one CUDA graph without running them (``replay`` runs them). One eager frame first, on the
+        state that is then restored, settles one-time launch attributes and the communicator."""
+        saved = self.save()
+        self._keep = []
+        self._frame(kspace, self.frame, out, 0)
+        self.restore(saved)
+        g = torch.cuda.CUDAGraph()
+        f0, t0 = self.frame, self.t
+        with torch.cuda.graph(g):
+            for fo in range(frames):
+                self._frame(kspace, f0 + fo, out, fo)
+        self.frame, self.t = f0, t0
+        self._graph = (g, list(self._keep), int(frames))
+        return g
+
+    def replay(self):
+        g, _, frames = self._graph
+        g.replay()
+        self.frame += frames
+        self.t += frames
+
+    def run(self, kspace, frames, out=None, graph=False):
+        """kspace: (T, nx, ny) complex64 CUDA (full frames). Frames from the current index. ``graph``:
+        capture the frames (kernels and collectives) in one CUDA graph and replay it."""
         if out is None:
             out = self.make_outputs(frames)
-        for fo in range(frames):
-            f = self.frame
-            self.partial(kspace, f)
-            self.allreduce(self.payload)  # one sum over the ranks per frame (SURVEY §8e)
-            self.finish(kspace, f, out, fo)
+        if graph and frames > 0:
+            self.capture(kspace, frames, out)
+            self.replay()
+        else:
+            self._keep = []
+            self.run_frames(kspace, frames, out)
         return out
+
+    def check_status(self):
+        L.raise_status(int(self.status.max().item()), "row-sharded engine")
