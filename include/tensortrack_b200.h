@@ -159,6 +159,10 @@ int tt_rows_shard_scores(void* stream, int nx, int ny, int rank, const double* e
 int tt_rows_plan_info(int nx, int ny, int rank, int max_rows, int cluster, int* out);
 /* doubles in the fp64 payload xg of a sharded launch */
 size_t tt_rows_shard_xg_len(int rank);
+/* 1 when tt_track_rows runs the mirrored kernel for this shape at `cluster` (every CTA holds the whole Ah;
+ * two cluster barriers per frame, exchanges through distributed shared memory; opt-in with the environment
+ * variable TT_ROWS_MIRROR=1), else 0 (the L2-exchange kernel runs); diagnostics / tests. */
+int tt_rows_mirror_fits(int nx, int ny, int rank, int max_rows, int cluster);
 /* sum the `world` payload slots of a local multi-rank phase-1 launch into slot 0 (fixed order) */
 int tt_rows_shard_reduce(void* stream, int world, int ny, int rank, double* xw, double* xg);
 

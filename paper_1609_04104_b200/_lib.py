@@ -84,6 +84,7 @@ SIGNATURES = {
     "tt_rows_scratch_bytes": (C.c_size_t, [C.c_int] * 6),
     "tt_track_rows": (C.c_int, [_p, C.POINTER(RowsArgs)]),
     "tt_rows_shard_xg_len": (C.c_size_t, [C.c_int]),
+    "tt_rows_mirror_fits": (C.c_int, [C.c_int] * 5),
     "tt_rows_plan_info": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _p]),
     "tt_rows_shard_reduce": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, _p, _p]),
     "tt_entries_scratch_bytes": (C.c_size_t, [C.c_int] * 4),

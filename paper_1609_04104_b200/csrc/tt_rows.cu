@@ -39,6 +39,7 @@
 #include <stdlib.h>
 
 #include "tt_block.cuh"
+#include "tt_mirror.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -51,7 +52,9 @@ constexpr int GTM = 4, GTN = 2;
 // register tile of the fp64-accumulating data GEMMs (zgemm_tile): F2F conversions per k step = TM + TN
 // complex operands, DFMA = 4 TM TN
 constexpr int ZTM = 2, ZTN = 4;
-constexpr int ZG = 4;  // 8-row M blocks per DMMA work item (zgemm_dmma)
+constexpr int ZG = 4;   // 8-row M blocks per DMMA work item (zgemm_dmma)
+constexpr int ZGZ = 6;  // ... for the Z GEMM (short M = sampled rows, long K: K parts instead of M groups;
+                        // profiles/tools/ubench_dmma_shapes.cu: config 3 Z 11.9k -> 9.5k cycles)
 
 struct RowsPlan {
   int CL, KT, nIm, nJm, Rp, red_cap, tight, ysr;
@@ -685,20 +688,37 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       if (!a.sraw_in) {
       // raw row scores for own rows (sampler.py:77-85, :126)
       const double cs = (double)ny, cr = (double)R, cd = 1.0 / ((double)R * (double)(nx + ny));
-      // tpr lanes per row (rank terms split, fixed-order butterfly), so the fp64 chain is R / tpr long
-      int tpr = 32;
-      while (tpr > 1 && tpr * nI > NT) tpr >>= 1;
-      const int sub = lane & (tpr - 1);
-      for (int base = 0; base < nI; base += NT / tpr) {  // uniform trip count (full-warp shuffles)
-        const int i = base + tid / tpr;
-        double e = 0.0;
-        if (i < nI)
-          for (int r = sub; r < R; r += tpr) {
-            const float2 v = ahl[i * R + r];
+      if (nI * 2 <= NT) {
+        // short row blocks (config 2): tpr lanes per row (rank terms split, fixed-order butterfly), so the
+        // fp64 chain is R / tpr long
+        int tpr = 32;
+        while (tpr > 1 && tpr * nI > NT) tpr >>= 1;
+        const int sub = lane & (tpr - 1);
+        for (int base = 0; base < nI; base += NT / tpr) {  // uniform trip count (full-warp shuffles)
+          const int i = base + tid / tpr;
+          double e = 0.0;
+          if (i < nI)
+            for (int r = sub; r < R; r += tpr) {
+              const float2 v = ahl[i * R + r];
+              e = fma((double)v.x * v.x + (double)v.y * v.y, inrm[r], e);
+            }
+          for (int o = 1; o < tpr; o <<= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+          if (sub == 0 && i < nI) __stcg(&g_sraw[i0 + i], (cs * e + cr) * cd);
+        }
+      } else {
+        // long row blocks (config 3): a row per thread, the rank terms from a row-dependent start so the
+        // lanes of a warp spread over the shared-memory banks (rows are R complex apart: one bank otherwise)
+        for (int i = tid; i < nI; i += NT) {
+          const float2* rowp = ahl + i * R;
+          double e = 0.0;
+          int r = (i0 + i) % R;
+          for (int k = 0; k < R; ++k) {
+            const float2 v = rowp[r];
             e = fma((double)v.x * v.x + (double)v.y * v.y, inrm[r], e);
+            r = r + 1 == R ? 0 : r + 1;
           }
-        for (int o = 1; o < tpr; o <<= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-        if (sub == 0 && i < nI) __stcg(&g_sraw[i0 + i], (cs * e + cr) * cd);
+          __stcg(&g_sraw[i0 + i], (cs * e + cr) * cd);
+        }
       }
       if (tid < R && nrm[tid] == 0.0) atomicOr(&sh_err, TT_ST_ZEROCOL);
       STAMP(3);
@@ -895,7 +915,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         const int ztiles = ((zM + ZTM - 1) / ZTM) * ((R + ZTN - 1) / ZTN);
         zks = max(1, min(NT / ztiles, min(ROWS_ZKS, pl.nJm / 4)));
       } else {      // DMMA items (4 M blocks x 1 r block), one per warp
-        const int items = ((((zM + 7) >> 3) + ZG - 1) / ZG) * ((R + 3) >> 2);
+        const int items = ((((zM + 7) >> 3) + ZGZ - 1) / ZGZ) * ((R + 3) >> 2);
         zks = max(1, min((NT / 32) / items, min(ROWS_ZKS, (pl.nJm + 3) / 4)));
       }
     }
@@ -1023,7 +1043,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
           if (TIGHT)
             zgemm_fd<ZTM, ZTN, true, true>(S, R, nJ, ys, pl.ysr, 1, bhl, R, 1, zks, red2d, epi);
           else
-            zgemm_dmma<ZG>(S, R, nJ, ys, pl.ysr, 1, bh64, R, zks, epi);
+            zgemm_dmma<ZGZ>(S, R, nJ, ys, pl.ysr, 1, bh64, R, zks, epi);
         } else {
           const RowsEpiD epi{EPI_W_ACC, R, wacc, nullptr, 0};
           if (TIGHT)
@@ -1096,7 +1116,7 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
           if (TIGHT)
             zgemm_fd<ZTM, ZTN, true, true>(kt, R, nJ, ys, pl.ysr, 1, bhl, R, 1, zks, red2d, epi);
           else
-            zgemm_dmma<ZG>(kt, R, nJ, ys, pl.ysr, 1, bh64, R, zks, epi);
+            zgemm_dmma<ZGZ>(kt, R, nJ, ys, pl.ysr, 1, bh64, R, zks, epi);
         }
         if (w) __syncthreads();  // the K-split buffer is reused
       }
@@ -1635,6 +1655,18 @@ extern "C" int tt_track_rows(void* stream, const tt_rows_args* a) {
   }
   if (a->t0 < 1) return tt_fail(TT_EINVAL, "t must be >= 1");
   if (a->frames == 0) return TT_OK;
+  {
+    // the mirrored kernel (tt_rows2.cu) when the whole Ah fits every CTA at the requested cluster size
+    const int cands[5] = {16, 8, 4, 2, 1};
+    MirrorPlan mp;
+    if (a->cluster > 0) {
+      if (tt_rows_mirror_plan(a, a->cluster, &mp)) return tt_rows_mirror_launch(stream, a, mp);
+    } else {
+      for (int i = 0; i < 5; ++i)
+        if (a->nslices * cands[i] <= 148 && tt_rows_mirror_plan(a, cands[i], &mp))
+          return tt_rows_mirror_launch(stream, a, mp);
+    }
+  }
   RowsPlan pl;
   int rc = rows_choose_cluster(a->nx, a->ny, a->rank, a->max_rows, a->cluster, &pl);
   if (rc) return rc;

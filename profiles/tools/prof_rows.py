@@ -41,6 +41,13 @@ names = {0: "frame start", 26: "a:colnorm", 1: "a-partials", 2: "B1", 24: "s:nrm
          6: "publishAhS", 7: "B3 complete", 16: "h:tile landed", 17: "h:Z (one tile) / W", 18: "h:Ah_S + GA",
          19: "h:W (one tile) / Z", 8: "heavy-rest", 9: "h/ga/yn", 10: "B4", 11: "Gbuild", 12: "solve", 13: "cost/mu",
          21: "u:mark", 22: "u:P", 23: "u:Q", 14: "update", 15: "outputs"}
+from paper_1609_04104_b200 import _lib as L
+Smax = eng.max_rows
+if L.lib().tt_rows_mirror_fits(cfg["n"], cfg["n"], cfg["R"], Smax, eng.cluster):
+    print("mirrored kernel (tt_rows2.cu)")
+    names = {0: "frame start", 1: "GB bcast + norms", 2: "scores", 3: "draw / rows", 4: "marks + AhS + GA",
+             5: "Y landed", 6: "W + Z GEMMs", 7: "h / yn partials", 8: "B1", 9: "Gram", 10: "solve", 11: "cost/mu",
+             12: "Z sums + aown", 16: "P GEMM", 13: "Q GEMM", 17: "apply", 14: "GB scatter", 15: "outputs + B2"}
 cc = c[5:]
 # stamps present in every frame, ordered by their median offset from the frame start (the one-tile and the
 # k-tiled heavy phases stamp 16-19 on different sides of B3)
