@@ -1093,6 +1093,13 @@ def run_ours(args, cfg):
                    "sample": f"first {fr} frames of slice 0 ({dt:.1f} s), oracle port of the reference algorithm "
                              f"(numpy SVD ridge, pocketfft), all host threads; reference unavailable: {e!r}"}
 
+    api_fps = None
+    if rank == 0 and not args.no_e2e:
+        try:
+            api_fps = api_loop_rate(cfg, ks_np[:, 0], A0[0], B0[0])
+        except Exception as e:  # reported, never fatal to the bench line
+            api_fps = f"failed: {e!r}"
+
     # ---- parity of this run (rank 0's first slice) against the oracle on the same masks: the device's
     # own rows fed to the oracle restatement, every frame's gamma and NRMSE compared (north_star tolerances)
     parity = None
@@ -1120,7 +1127,10 @@ def run_ours(args, cfg):
                   "step_hbm_frac": (b_upd + b_rec) * value / 1e9 / hbm_peak / (1 if cfg["slices"] == 1 else 1),
                   "fp32_frac_tracking": f_sep * T * ns / track_s / 1e12 / fp32_peak,
                   "mean_nrmse": float(nmse.sqrt().mean()), "last_nrmse": float(nmse[-1].sqrt().mean()),
-                  "rows_per_frame_avg": S_avg},
+                  "rows_per_frame_avg": S_avg,
+                  "per_call_api_frames_per_s": api_fps,
+                  "per_call_api": "row_scores -> draw_samples -> track_step(FourierMask rows, host y) -> "
+                                  "reconstruct_frame (host k-space + image), one slice, synchronous"},
         "clocks": clk.summary(),
         "e2e": e2e,
         "cpu_baseline": cpu,
@@ -1128,6 +1138,38 @@ def run_ours(args, cfg):
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def api_loop_rate(cfg, ks_host, A0, B0, frames=24):
+    """The per-call drop-in loop a reference caller gets after switching imports (experiment.py:498-525 on
+    the per-call API): row_scores -> draw_samples (Philox generator) -> FourierMask batch from host k-space
+    rows -> track_step -> reconstruct_frame (host k-space and magnitude image back), image-domain factors,
+    one frame at a time. Frames/s over `frames` frames after two warm-up frames (wall clock, synchronous
+    API: every call returns host data)."""
+    import torch
+
+    import paper_1609_04104_b200 as tt
+
+    n, R = cfg["n"], cfg["R"]
+    k = int(cfg["K"]) if "K" in cfg else int(np.ceil(cfg["vd"] * n))
+    forced = list(cfg.get("forced", (0,)))
+    state = tt.TrackerState(tt.TensorSubspace((np.asarray(A0, np.complex128), np.asarray(B0, np.complex128))),
+                            tt.StepConfig(cfg["lam"], R, tt.Fixed(cfg["mu"])))
+    gen = np.random.Generator(np.random.Philox(key=11))
+    t_start = None
+    for f in range(frames + 2):
+        if f == 2:
+            torch.cuda.synchronize()
+            t_start = time.perf_counter()
+        dist = tt.row_scores(state.subspace, cfg.get("beta", 0.1))
+        plan = tt.draw_samples(dist, k, True, gen, forced=forced)
+        rows = plan.omega
+        y = ks_host[f % ks_host.shape[0]][rows, :].ravel()
+        batch = tt.MeasurementBatch(y, tt.FourierMask((n, n), tt.rows_to_entries(rows, n)), t=f)
+        state, rep = tt.track_step(state, batch)
+        tt.reconstruct_frame(state.subspace, rep.gamma)
+    torch.cuda.synchronize()
+    return frames / (time.perf_counter() - t_start)
 
 
 PARITY_FRAMES = {"c4": 12}  # the oracle's numpy SVD at 1024^2 takes ~1 s per frame

@@ -318,6 +318,9 @@ int tt_reconstruct(void* stream, int frames, int nx, int ny, int rank, const flo
  * summation order: repeat calls are bit-identical. */
 int tt_nmse(void* stream, int frames, size_t n, const float* truth, const float* est, double* work, double* out);
 size_t tt_nmse_work_doubles(int frames);
+/* Squared Frobenius norms (fp64, fixed order) of `batch` complex64 matrices of n elements each -> out[batch]:
+ * the post-update factor norms a factor history needs for StepConfig.norm_cap (tracker.py:406-408). */
+int tt_factor_norms2(void* stream, int batch, size_t n, const float* x, double* out);
 /* rebalance (core.py:138-166) in place on [nslices][n][rank] factor pairs. */
 int tt_rebalance(void* stream, int nslices, int nx, int ny, int rank, float* a, float* b, int32_t* status);
 

@@ -98,6 +98,7 @@ SIGNATURES = {
                                                  _p, _p, _p]),
     "tt_rows_shard_energy": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, C.c_int, _p, _p]),
     "tt_rows_shard_scores": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, _p, _p, _p]),
+    "tt_factor_norms2": (C.c_int, [_p, C.c_int, C.c_size_t, _p, _p]),
     "tt_vd_rows_batch": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, _p, C.c_int, C.c_uint64, C.c_uint64, _p, _p]),
     "tt_terms_scratch_bytes": (C.c_size_t, [C.c_int, C.c_int, C.c_int]),
     "tt_residual": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, C.c_int, _p, _p, _p, _p, _p, _p]),

@@ -124,3 +124,23 @@ extern "C" int tt_solve_gamma(void* stream, int L, int R, const double* phi, con
   TT_CUDA_TRY(cudaGetLastError());
   return TT_OK;
 }
+
+// ---------------------------------------------------------------- norm_cap flags (tracker.py:406-408)
+// Squared Frobenius norms of `batch` complex64 matrices of `n` elements each (fp64, fixed order: one CTA
+// per matrix, block-strided partials then a fixed tree): the post-update factor norms of a factor history.
+__global__ void __launch_bounds__(256) factor_norms2_kernel(size_t n, const float2* __restrict__ x, double* out) {
+  __shared__ double red[8];
+  const float2* p = x + (size_t)blockIdx.x * n;
+  double acc = 0.0;
+  for (size_t i = threadIdx.x; i < n; i += blockDim.x) acc += (double)p[i].x * p[i].x + (double)p[i].y * p[i].y;
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) out[blockIdx.x] = acc;
+}
+
+extern "C" int tt_factor_norms2(void* stream, int batch, size_t n, const float* x, double* out) {
+  if (batch < 0 || (batch > 0 && (!x || !out))) return tt_fail(TT_EINVAL, "tt_factor_norms2: bad args");
+  if (batch == 0) return TT_OK;
+  factor_norms2_kernel<<<batch, 256, 0, (cudaStream_t)stream>>>(n, (const float2*)x, out);
+  TT_CUDA_TRY(cudaGetLastError());
+  return TT_OK;
+}

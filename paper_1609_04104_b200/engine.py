@@ -35,7 +35,8 @@ from . import _ops as K
 from .tracker import Fixed, HessianBound
 
 __all__ = ["StaticRows", "Informative", "AdaptiveSchedule", "OnlineEngine", "run_online", "OnlineResult", "warm_up", "RowShardedEngine",
-           "InformativeEntries", "StaticEntries", "EntryEngine", "run_batch", "BatchResult", "LocalShardedEngine"]
+           "InformativeEntries", "StaticEntries", "EntryEngine", "run_batch", "BatchResult", "LocalShardedEngine",
+           "RowShardLoop", "history_norm_flags"]
 
 
 @dataclass(frozen=True)
@@ -664,9 +665,7 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
     A0 = np.asarray(A0).reshape(ns, nx, -1)
     R = A0.shape[-1]
     if isinstance(policy, (InformativeEntries, StaticEntries)):
-        if norm_cap is not None:
-            raise ValueError("norm_cap is reported by the row-mask engines")
-        return _run_online_entries(src, on_dev, A0, B0, lam, step, policy, clean, t0, warm_frames)
+        return _run_online_entries(src, on_dev, A0, B0, lam, step, policy, clean, t0, warm_frames, norm_cap)
     sched = policy if isinstance(policy, AdaptiveSchedule) else None
     dev = L.device()
     comp = torch.cuda.current_stream(dev)
@@ -948,7 +947,25 @@ class LocalShardedEngine:
 _ENTRY_PLANS: dict = {}  # (shape, policy, length) -> (EntryEngine with a captured graph, resident truth)
 
 
-def _run_online_entries(src, on_dev, A0, B0, lam, step, policy, clean, t0, warm_frames) -> OnlineResult:
+def history_norm_flags(out: dict, norm_cap: float) -> torch.Tensor:
+    """StepReport.norm_exceeded (tracker.py:406-408) per frame of an engine's outputs from its factor history:
+    the frame updated (count > 0) and a post-update factor's Frobenius norm exceeds ``norm_cap`` (the DFT is
+    unitary, so the k-space history has the image factors' norms). (F, nslices) bool on the device."""
+    ah, bh = out["ah"], out["bh"]
+    F = ah.shape[0] * ah.shape[1]
+    na = torch.empty(F, dtype=torch.float64, device=ah.device)
+    nb = torch.empty(F, dtype=torch.float64, device=ah.device)
+    L.check(L.lib().tt_factor_norms2(L.stream_ptr(), F, ah.shape[-2] * ah.shape[-1], ah.data_ptr(), na.data_ptr()),
+            "factor norms")
+    L.check(L.lib().tt_factor_norms2(L.stream_ptr(), F, bh.shape[-2] * bh.shape[-1], bh.data_ptr(), nb.data_ptr()),
+            "factor norms")
+    cap2 = float(norm_cap) ** 2
+    over = (na > cap2) | (nb > cap2)
+    return (over.reshape(ah.shape[:2]) & (out["cnt"] > 0))
+
+
+def _run_online_entries(src, on_dev, A0, B0, lam, step, policy, clean, t0, warm_frames,
+                        norm_cap=None) -> OnlineResult:
     """run_online for the entry policies (one slice): upload, the graph-replayed frame chain,
     reconstruction, download. The entry lists are reported in ``rows`` (flat indices i*ny + j)."""
     T, ns, nx, ny = src.shape
@@ -1034,6 +1051,8 @@ def _run_online_entries(src, on_dev, A0, B0, lam, step, policy, clean, t0, warm_
     Ad, Bd = eng.image_factors()
     small = (("gamma", out["gamma"]), ("cost", out["cost"]), ("mu", out["mu"]), ("cnt", out["cnt"]),
              ("rows", out["rows"]), ("A", Ad), ("B", Bd), ("st", eng.status))
+    if norm_cap is not None:
+        small = small + (("norm", history_norm_flags(out, norm_cap).to(torch.int32)),)
     host = {k: pinned(tuple(v.shape), v.dtype) for k, v in small}
     for k, v in small:
         host[k].copy_(v, non_blocking=True)
@@ -1046,7 +1065,8 @@ def _run_online_entries(src, on_dev, A0, B0, lam, step, policy, clean, t0, warm_
     rows = [[rows_np[f, 0, :cnt[f, 0]].astype(np.int64)] for f in range(T)]
     return OnlineResult(recon=host["recon"].numpy(), gamma=host["gamma"].numpy(), cost=host["cost"].numpy(),
                         mu=host["mu"].numpy(), rows=rows, nmse=nm, final_A=host["A"].numpy(),
-                        final_B=host["B"].numpy())
+                        final_B=host["B"].numpy(),
+                        norm_exceeded=host["norm"].numpy().astype(bool) if norm_cap is not None else None)
 
 
 @dataclass
@@ -1060,17 +1080,19 @@ class BatchResult:
     final_A: np.ndarray
     final_B: np.ndarray
     t: int
+    step_norm_exceeded: np.ndarray | None = None  # (epochs * T,) bool, processing order (norm_cap set)
 
 
 def run_batch(kspace, A0, B0, lam, step, rows, counts, epochs=1, rng=None, reshuffle=False,
-              rebalance_epochs=True, t0=1, cluster=0) -> BatchResult:
+              rebalance_epochs=True, t0=1, cluster=0, norm_cap=None) -> BatchResult:
     """Multi-epoch batch mode on the device (tracker.run tracker.py:456-500,
     experiment.run_tracking experiment.py:284-313): the frames' row-mask data
     (``rows`` (T, Smax) table, ``counts`` (T,)) is revisited for ``epochs`` passes of the rows
     kernel, the factors rebalanced between passes, the order re-drawn with ``rng.permutation`` when
     ``reshuffle`` (the caller's generator, consumed as the reference does), t growing globally.
     With epochs > 1 every frame's gamma is then re-solved against the final subspace (a pass of the
-    same kernel with a zero step) and the images synthesised from it. One slice."""
+    same kernel with a zero step) and the images synthesised from it. One slice. ``norm_cap`` flags every
+    step whose post-update factors exceed it (StepReport.norm_exceeded, tracker.py:406-408)."""
     if epochs < 1:
         raise ValueError("epochs must be at least 1")
     if reshuffle and epochs > 1 and rng is None:
@@ -1087,7 +1109,7 @@ def run_batch(kspace, A0, B0, lam, step, rows, counts, epochs=1, rng=None, reshu
     base = OnlineEngine(nx, ny, R, 1, lam, step, StaticRows(tab, cnt), cluster, t0)
     base.set_image_factors(np.asarray(A0).reshape(1, nx, R), np.asarray(B0).reshape(1, ny, R))
     st = torch.zeros(1, dtype=torch.int32, device=dev)
-    g_steps, c_steps, m_steps, orders = [], [], [], []
+    g_steps, c_steps, m_steps, n_steps, orders = [], [], [], [], []
     ah, bh, ab, t = base.ah, base.bh, base.alpha_bar, base.t
     for epoch in range(epochs):
         if rebalance_epochs and epoch > 0:
@@ -1096,13 +1118,15 @@ def run_batch(kspace, A0, B0, lam, step, rows, counts, epochs=1, rng=None, reshu
         if reshuffle and epoch > 0:
             order = np.asarray(rng.permutation(T))
         orders.append(order)
-        eng = OnlineEngine(nx, ny, R, 1, lam, step, StaticRows(tab[order], cnt[order]), base.cluster, t)
+        eng = OnlineEngine(nx, ny, R, 1, lam, step, StaticRows(tab[order], cnt[order]), base.cluster, t, norm_cap)
         eng.ah, eng.bh, eng.alpha_bar = ah, bh, ab
         sel = torch.from_numpy(order.astype(np.int64)).to(dev)
         out = eng.run(kd.index_select(0, sel).contiguous(), T, history=False)
         g_steps.append(out["gamma"][:, 0])
         c_steps.append(out["cost"][:, 0])
         m_steps.append(out["mu"][:, 0])
+        if norm_cap is not None:
+            n_steps.append(out["norm"][:, 0])
         ah, bh, ab, t = eng.ah, eng.bh, eng.alpha_bar, eng.t
     L.raise_status(int(st.max().item()) & L.TT_ST_ZEROCOL, "batch rebalance")
     if epochs > 1:  # re-projection onto the final subspace
@@ -1117,13 +1141,16 @@ def run_batch(kspace, A0, B0, lam, step, rows, counts, epochs=1, rng=None, reshu
     # asynchronous downloads into pinned memory, one synchronisation
     dl = {"recon": X, "gamma": gam, "sg": torch.cat(g_steps), "sc": torch.cat(c_steps), "sm": torch.cat(m_steps),
           "A": A, "B": B}
+    if norm_cap is not None:
+        dl["sn"] = torch.cat(n_steps)
     host = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in dl.items()}
     for k, v in dl.items():
         host[k].copy_(v, non_blocking=True)
     torch.cuda.current_stream().synchronize()
     h = {k: v.numpy() for k, v in host.items()}
     return BatchResult(recon=h["recon"], gamma=h["gamma"], step_gamma=h["sg"], step_cost=h["sc"], step_mu=h["sm"],
-                       orders=orders, final_A=h["A"], final_B=h["B"], t=t)
+                       orders=orders, final_A=h["A"], final_B=h["B"], t=t,
+                       step_norm_exceeded=h["sn"].astype(bool) if norm_cap is not None else None)
 
 
 class RowShardLoop:

@@ -91,3 +91,39 @@ def test_norm_cap_flags_match_oracle_norms(nslices, chunk):
     assert 0 < want.sum() < T
     for s in range(nslices):
         np.testing.assert_array_equal(res.norm_exceeded[:, s], want)
+
+
+def test_norm_cap_flags_entries_and_batch():
+    """norm_cap on the entry-mask engine (flags from the factor history) against the oracle's post-update
+    norms, and on batch mode (epochs = 1 equals the online run's flags)."""
+    import paper_1609_04104_b200 as tt
+    from paper_1609_04104_b200.phantom import cine_phantom
+
+    n, R, T = 32, 4, 7
+    ph = cine_phantom(n, n, T, period=8.0, seed=61)
+    A0, B0 = O.random_subspace(n, n, R, seed=62)
+    rng = np.random.default_rng(63)
+    lists = [rng.permutation(rng.choice(n * n, int(0.3 * n * n), replace=False)) for _ in range(T)]
+    lists[3] = np.empty(0, np.int64)
+    ref = O.online_run_entries(ph.kspace, O.fft_cols(A0), O.fft_cols(B0), 0.1, ("fixed", 0.5),
+                               {"kind": "static", "entries": lists}, record_factors=True)
+    top = np.array([max(np.linalg.norm(a), np.linalg.norm(b)) for a, b in zip(ref["A"], ref["B"])])
+    u = np.unique(np.round(top, 6))
+    cap = float(0.5 * (u[len(u) // 2 - 1] + u[len(u) // 2]))
+    want = top > cap
+    want[3] = False
+    S = max(len(x) for x in lists)
+    tab = np.full((T, S), -1, np.int64)
+    for f, x in enumerate(lists):
+        tab[f, :len(x)] = x
+    res = tt.run_online(ph.kspace, A0[None], B0[None], 0.1, tt.Fixed(0.5),
+                        tt.StaticEntries(tab, np.array([len(x) for x in lists])), norm_cap=cap)
+    assert 0 < want.sum() < T
+    np.testing.assert_array_equal(res.norm_exceeded[:, 0], want)
+    # batch mode, one epoch: the same flags as the online run
+    rows = [O.vd_rows(n, -1.0, 0.25, np.random.default_rng(f).random) for f in range(T)]
+    rt = np.stack(rows)
+    on = tt.run_online(ph.kspace, A0[None], B0[None], 0.1, tt.Fixed(0.5), tt.StaticRows(rt[:, None, :],
+                       np.full((T, 1), rt.shape[1])), norm_cap=cap)
+    bt = tt.run_batch(ph.kspace, A0, B0, 0.1, tt.Fixed(0.5), rt, np.full(T, rt.shape[1]), norm_cap=cap)
+    np.testing.assert_array_equal(bt.step_norm_exceeded, on.norm_exceeded[:, 0])
