@@ -992,8 +992,8 @@ TT_DEV void dmma_m8n8k4(double& d0, double& d1, double a, double b) {
       : "d"(a), "d"(b));
 }
 template <int G, typename AT, typename Out>
-TT_DEV void zgemm_dmma(int M, int R, int K, const AT* A, int a_m, int a_k, const double2* B, int b_k, int KS,
-                       Out out) {
+TT_DEV void zgemm_dmma_v1(int M, int R, int K, const AT* A, int a_m, int a_k, const double2* B, int b_k, int KS,
+                          Out out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int row = lane >> 2, kq = lane & 3;
   const int MB = (M + 7) >> 3, NB = (R + 3) >> 2, MG = (MB + G - 1) / G;
@@ -1040,6 +1040,82 @@ TT_DEV void zgemm_dmma(int M, int R, int K, const AT* A, int a_m, int a_k, const
 #pragma unroll
       for (int g = 0; g < G; ++g)
         if (g < gcount) dmma_m8n8k4(acc[g][0], acc[g][1], ai[g], b1);
+    }
+    const int r = nb * 4 + kq;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int m = ((mg * G + g) << 3) + row;
+      if (g < gcount && m < M && r < R) out(m, r, ks, make_double2(acc[g][0], acc[g][1]));
+    }
+  }
+}
+
+// zgemm_dmma (the round-2 form; zgemm_dmma_v1 above is the round-1 loop, kept for
+// profiles/tools/ubench_dmma_shapes.cu): fewer issue slots per DMMA (the loop is issue-bound: a DMMA every ~16 SMSP cycles leaves
+// ~8 slots per DMMA per warp at two warps per SMSP): every one of the G blocks of an item issues its DMMAs
+// unpredicated (blocks past the item's last one, rows past M and columns past R compute on clamped, finite
+// operands into accumulators that are never stored: a row of A only reaches its own output row, a column
+// of B its own output column), the operand pointers advance by increments, and only the K tail step (K not a
+// multiple of 4) selects zeros. Same products and K order per output as zgemm_dmma.
+template <int G, typename AT, typename Out>
+TT_DEV void zgemm_dmma(int M, int R, int K, const AT* A, int a_m, int a_k, const double2* B, int b_k, int KS,
+                       Out out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int row = lane >> 2, kq = lane & 3;
+  const int MB = (M + 7) >> 3, NB = (R + 3) >> 2, MG = (MB + G - 1) / G;
+  const int kfull = K >> 2;                 // steps with all 4 k valid
+  const int kpairs = (K + 3) >> 2;
+  const int items = MG * NB * KS;
+  for (int it = warp; it < items; it += nw) {
+    const int ks = idiv(it, MG * NB), rest = it - ks * MG * NB;
+    const int mg = idiv(rest, NB), nb = rest - mg * NB;
+    const int gcount = min(G, MB - mg * G);
+    const int t0 = idiv(kpairs * ks, KS), t1 = idiv(kpairs * (ks + 1), KS);
+    const int rb = nb * 4 + (row >> 1), q = row & 1;
+    const AT* ap[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int m = ((mg * G + g) << 3) + row;
+      ap[g] = A + (size_t)min(m, M - 1) * a_m + (size_t)(4 * t0 + kq) * a_k;
+    }
+    const double2* bp = B + min(rb, R - 1) + (size_t)(4 * t0 + kq) * b_k;
+    const size_t astep = (size_t)4 * a_k, bstep = (size_t)4 * b_k;
+    double acc[G][2];
+#pragma unroll
+    for (int g = 0; g < G; ++g) acc[g][0] = acc[g][1] = 0.0;
+    const int tf = min(t1, kfull);
+    for (int t = t0; t < tf; ++t) {
+      const double2 b = *bp;
+      bp += bstep;
+      const double b0 = q == 0 ? b.x : -b.y, b1 = q == 0 ? b.y : b.x;
+      double ar[G], ai[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const AT a = *ap[g];
+        ap[g] += astep;
+        ar[g] = (double)a.x;
+        ai[g] = (double)a.y;
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) dmma_m8n8k4(acc[g][0], acc[g][1], ar[g], b0);
+#pragma unroll
+      for (int g = 0; g < G; ++g) dmma_m8n8k4(acc[g][0], acc[g][1], ai[g], b1);
+    }
+    if (tf < t1) {  // the K tail: k >= K contributes zero
+      const bool kok = 4 * tf + kq < K;
+      const double2 b = kok ? *bp : make_double2(0.0, 0.0);
+      const double b0 = q == 0 ? b.x : -b.y, b1 = q == 0 ? b.y : b.x;
+      double ar[G], ai[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const AT a = kok ? *ap[g] : AT{0, 0};
+        ar[g] = (double)a.x;
+        ai[g] = (double)a.y;
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) dmma_m8n8k4(acc[g][0], acc[g][1], ar[g], b0);
+#pragma unroll
+      for (int g = 0; g < G; ++g) dmma_m8n8k4(acc[g][0], acc[g][1], ai[g], b1);
     }
     const int r = nb * 4 + kq;
 #pragma unroll

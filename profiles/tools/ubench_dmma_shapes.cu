@@ -223,13 +223,13 @@ __global__ void __launch_bounds__(256, 1) kb(int S, int NJ, int R, int RS, int Y
     __syncthreads();
     long long t0 = clock64();
     if (WHICH == 0) {
-if (PIPE == 0) zgemm_dmma<G>(S, R, NJ, ys, YSR, 1, b64, RS, KS, snk); else if (PIPE == 1) zgemm_dmma_p<G>(S, R, NJ, ys, YSR, 1, b64, RS, KS, snk); else if (PIPE == 2) zgemm_dmma_u<G, 4>(S, R, NJ, ys, YSR, 1, b64, RS, KS, snk); else if (PIPE == 3) zgemm_dmma_i<G, 4>(S, R, NJ, ys, YSR, 1, b64, RS, KS, snk); else zgemm_dmma_i<G, 8>(S, R, NJ, ys, YSR, 1, b64, RS, KS, snk);
+if (PIPE == 0) zgemm_dmma_v1<G>(S, R, NJ, ys, YSR, 1, b64, RS, KS, snk); else if (PIPE == 1) zgemm_dmma_p<G>(S, R, NJ, ys, YSR, 1, b64, RS, KS, snk); else if (PIPE == 2) zgemm_dmma_u<G, 4>(S, R, NJ, ys, YSR, 1, b64, RS, KS, snk); else if (PIPE == 5) zgemm_dmma<G>(S, R, NJ, ys, YSR, 1, b64, RS, KS, snk); else if (PIPE == 3) zgemm_dmma_i<G, 4>(S, R, NJ, ys, YSR, 1, b64, RS, KS, snk); else zgemm_dmma_i<G, 8>(S, R, NJ, ys, YSR, 1, b64, RS, KS, snk);
     } else if (WHICH == 1) {
-if (PIPE == 0) zgemm_dmma<G>(NJ, R, S, ys, 1, YSR, b64, RS, KS, snk); else if (PIPE == 1) zgemm_dmma_p<G>(NJ, R, S, ys, 1, YSR, b64, RS, KS, snk); else if (PIPE == 2) zgemm_dmma_u<G, 4>(NJ, R, S, ys, 1, YSR, b64, RS, KS, snk); else if (PIPE == 3) zgemm_dmma_i<G, 4>(NJ, R, S, ys, 1, YSR, b64, RS, KS, snk); else zgemm_dmma_i<G, 8>(NJ, R, S, ys, 1, YSR, b64, RS, KS, snk);
+if (PIPE == 0) zgemm_dmma_v1<G>(NJ, R, S, ys, 1, YSR, b64, RS, KS, snk); else if (PIPE == 1) zgemm_dmma_p<G>(NJ, R, S, ys, 1, YSR, b64, RS, KS, snk); else if (PIPE == 2) zgemm_dmma_u<G, 4>(NJ, R, S, ys, 1, YSR, b64, RS, KS, snk); else if (PIPE == 5) zgemm_dmma<G>(NJ, R, S, ys, 1, YSR, b64, RS, KS, snk); else if (PIPE == 3) zgemm_dmma_i<G, 4>(NJ, R, S, ys, 1, YSR, b64, RS, KS, snk); else zgemm_dmma_i<G, 8>(NJ, R, S, ys, 1, YSR, b64, RS, KS, snk);
     } else if (WHICH == 2) {
-if (PIPE == 0) zgemm_dmma<G>(R, R, NJ, b64, 1, RS, b64, RS, KS, snk); else if (PIPE == 1) zgemm_dmma_p<G>(R, R, NJ, b64, 1, RS, b64, RS, KS, snk); else if (PIPE == 2) zgemm_dmma_u<G, 4>(R, R, NJ, b64, 1, RS, b64, RS, KS, snk); else if (PIPE == 3) zgemm_dmma_i<G, 4>(R, R, NJ, b64, 1, RS, b64, RS, KS, snk); else zgemm_dmma_i<G, 8>(R, R, NJ, b64, 1, RS, b64, RS, KS, snk);
+if (PIPE == 0) zgemm_dmma_v1<G>(R, R, NJ, b64, 1, RS, b64, RS, KS, snk); else if (PIPE == 1) zgemm_dmma_p<G>(R, R, NJ, b64, 1, RS, b64, RS, KS, snk); else if (PIPE == 2) zgemm_dmma_u<G, 4>(R, R, NJ, b64, 1, RS, b64, RS, KS, snk); else if (PIPE == 5) zgemm_dmma<G>(R, R, NJ, b64, 1, RS, b64, RS, KS, snk); else if (PIPE == 3) zgemm_dmma_i<G, 4>(R, R, NJ, b64, 1, RS, b64, RS, KS, snk); else zgemm_dmma_i<G, 8>(R, R, NJ, b64, 1, RS, b64, RS, KS, snk);
     } else {
-if (PIPE == 0) zgemm_dmma<G>(NJ, R, R, b64, RS, 1, b64, RS, KS, snk); else if (PIPE == 1) zgemm_dmma_p<G>(NJ, R, R, b64, RS, 1, b64, RS, KS, snk); else if (PIPE == 2) zgemm_dmma_u<G, 4>(NJ, R, R, b64, RS, 1, b64, RS, KS, snk); else if (PIPE == 3) zgemm_dmma_i<G, 4>(NJ, R, R, b64, RS, 1, b64, RS, KS, snk); else zgemm_dmma_i<G, 8>(NJ, R, R, b64, RS, 1, b64, RS, KS, snk);
+if (PIPE == 0) zgemm_dmma_v1<G>(NJ, R, R, b64, RS, 1, b64, RS, KS, snk); else if (PIPE == 1) zgemm_dmma_p<G>(NJ, R, R, b64, RS, 1, b64, RS, KS, snk); else if (PIPE == 2) zgemm_dmma_u<G, 4>(NJ, R, R, b64, RS, 1, b64, RS, KS, snk); else if (PIPE == 5) zgemm_dmma<G>(NJ, R, R, b64, RS, 1, b64, RS, KS, snk); else if (PIPE == 3) zgemm_dmma_i<G, 4>(NJ, R, R, b64, RS, 1, b64, RS, KS, snk); else zgemm_dmma_i<G, 8>(NJ, R, R, b64, RS, 1, b64, RS, KS, snk);
     }
     __syncthreads();
     long long t1 = clock64();
@@ -265,15 +265,16 @@ void run(const char* name, int S, int NJ, int R, int KS) {
 }
 
 int main() {
-  for (int v = 0; v < 5; ++v) {
+  for (int v : {0, 5}) {
     printf("--- variant %d\n", v);
 #define RUNV(W, G, name, S_, NJ_, R_, KS_) \
     if (v == 0) run<W, 0, G>(name, S_, NJ_, R_, KS_); else if (v == 1) run<W, 1, G>(name, S_, NJ_, R_, KS_); \
     else if (v == 2) run<W, 2, G>(name, S_, NJ_, R_, KS_); else if (v == 3) run<W, 3, G>(name, S_, NJ_, R_, KS_); \
-    else run<W, 4, G>(name, S_, NJ_, R_, KS_);
+    else if (v == 5) run<W, 5, G>(name, S_, NJ_, R_, KS_); else run<W, 4, G>(name, S_, NJ_, R_, KS_);
     RUNV(0, 4, "c3 Z", 42, 128, 16, 1)
     RUNV(0, 3, "c3 Z", 42, 128, 16, 1)
     RUNV(0, 6, "c3 Z", 42, 128, 16, 2)
+    RUNV(0, 6, "c3 Z", 42, 128, 16, 1)
     RUNV(1, 4, "c3 W", 42, 128, 16, 1)
     RUNV(1, 2, "c3 W", 42, 128, 16, 1)
     RUNV(2, 4, "c3 GB", 42, 128, 16, 2)
