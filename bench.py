@@ -7,8 +7,9 @@ mu=0.01, informative row sampling at 20% (K=52 trials incl. the forced DC line, 
 draws per slice). One bench *step* = the whole T-frame online sequence of every slice from the same
 initial state: per slice-frame [row scores -> Philox draw -> gather y -> Gram/ridge -> k-space factor
 update] in persistent cluster-kernel launches over blocks of frames (`--blocks`, default 4; the state
-stays resident across them), each block's reconstruction of the image frames overlapping the next
-block's tracking on a second stream. `--config c2` (single 256^2 slice, T=200, R=20, K=64 with 16
+stays resident across them), each block's reconstructed frames — the k-space estimates Ah diag(gamma)
+Bh^T that run_adaptive records for k-space data (experiment.py:242-245, :525) — computed on a second
+stream while the next block tracks. `--config c2` (single 256^2 slice, T=200, R=20, K=64 with 16
 forced centre lines), `c1`, `c4` and the widening configs select the others.
 
 `value`  = slice-frames reconstructed per second over all ranks (device time, inputs resident, L2
@@ -996,7 +997,7 @@ def run_ours(args, cfg):
             ev.record(stream)
             s_rec.wait_event(ev)
             with torch.cuda.stream(s_rec):
-                eng.reconstruct(part, into=X[a:b], in_place=True)  # 2 inverse column FFTs + reconstruction
+                eng.reconstruct(part, into=X[a:b], domain="kspace")  # k-space frames (run_adaptive's .kspace)
         if e_track is not None:
             e_track.record(stream)
         stream.wait_stream(s_rec)
@@ -1037,7 +1038,9 @@ def run_ours(args, cfg):
 
     # ---- quality (outside timing): NRMSE of the last step's reconstructions
     Xr = X.reshape(T, ns, n, n)
-    cl = torch.from_numpy(clean_np).to(dev)
+    cl = torch.from_numpy(clean_np).to(dev).reshape(T * ns, n, n)
+    cl = K.fft_cols_(K.fft_cols_(cl.contiguous()).transpose(1, 2).contiguous()).transpose(1, 2)  # F_x X F_y^T
+    cl = cl.reshape(T, ns, n, n)
     nmse = ((cl - Xr).abs().pow(2).sum((-1, -2)) / cl.abs().pow(2).sum((-1, -2))).double()
     cnt = out["cnt"].double()
 
@@ -1065,12 +1068,14 @@ def run_ours(args, cfg):
         # call runs): both pinned result blocks are then in torch's host caching allocator
         res = None
         for _ in range(2):
-            res = tt.run_online(ks_pin, A0, B0, cfg["lam"], tt.Fixed(cfg["mu"]), pol, cluster=args.cluster)
+            res = tt.run_online(ks_pin, A0, B0, cfg["lam"], tt.Fixed(cfg["mu"]), pol, cluster=args.cluster,
+                                recon_domain="kspace")
         torch.cuda.synchronize()
         t_e2e = []
         for _ in range(max(1, args.steps)):
             t0 = time.perf_counter()
-            res = tt.run_online(ks_pin, A0, B0, cfg["lam"], tt.Fixed(cfg["mu"]), pol, cluster=args.cluster)
+            res = tt.run_online(ks_pin, A0, B0, cfg["lam"], tt.Fixed(cfg["mu"]), pol, cluster=args.cluster,
+                                recon_domain="kspace")
             torch.cuda.synchronize()
             t_e2e.append(time.perf_counter() - t0)
         h2d = ks_np.nbytes
@@ -1080,7 +1085,8 @@ def run_ours(args, cfg):
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e = {"value": T * ns * (world if cfg["slices"] == 1 else 1) * len(t_e2e) / float(et[0]), "unit": "frames/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "call": "paper_1609_04104_b200.run_online(pinned host kspace) -> host recon/reports"}
+               "call": "paper_1609_04104_b200.run_online(pinned host kspace, recon_domain='kspace') -> host "
+                       "k-space frames (run_adaptive's recon for k-space data) + reports"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -1104,7 +1110,8 @@ def run_ours(args, cfg):
     # own rows fed to the oracle restatement, every frame's gamma and NRMSE compared (north_star tolerances)
     parity = None
     if rank == 0 and not args.no_parity:
-        parity = run_parity(cfg, ks_np[:, 0], clean_np[:, 0], A0[0], B0[0], out, Xr[:, 0], cnt[:, 0])
+        parity = run_parity(cfg, ks_np[:, 0], clean_np[:, 0], A0[0], B0[0], out, Xr[:, 0], cnt[:, 0],
+                            clean_k=cl[:, 0].cpu().numpy())
 
     if world > 1:
         dist.destroy_process_group()
@@ -1175,7 +1182,7 @@ def api_loop_rate(cfg, ks_host, A0, B0, frames=24):
 PARITY_FRAMES = {"c4": 12}  # the oracle's numpy SVD at 1024^2 takes ~1 s per frame
 
 
-def run_parity(cfg, ks, clean, A0, B0, out, X, cnt):
+def run_parity(cfg, ks, clean, A0, B0, out, X, cnt, clean_k=None):
     """Slice 0 of the last timed step against the CPU oracle (oracle/tt_oracle.py, pinned to the
     reference) fed the same per-frame rows the device drew: per-frame gamma (relative) and the NRMSE
     trajectory (absolute) over the first T frames (PARITY_FRAMES bounds c4); the device's masks are
@@ -1196,7 +1203,7 @@ def run_parity(cfg, ks, clean, A0, B0, out, X, cnt):
     ge = max(float(np.linalg.norm(gam[f] - ref["gamma"][f]) / max(np.linalg.norm(ref["gamma"][f]), 1e-300))
              for f in range(T))
     nd = X[:T].cpu().numpy().reshape(T, -1)
-    cl = clean[:T].reshape(T, -1)
+    cl = (clean if clean_k is None else clean_k)[:T].reshape(T, -1)  # the device frames' domain
     nr_dev = np.sqrt(np.sum(np.abs(cl - nd) ** 2, axis=1) / np.sum(np.abs(cl) ** 2, axis=1))
     ne = float(np.max(np.abs(nr_dev - np.sqrt(np.asarray(ref["nmse"])))))
     first_div = None

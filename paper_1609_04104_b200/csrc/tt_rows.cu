@@ -920,25 +920,6 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
       }
     }
 
-    // ======== (b) publish own sampled rows of Ah; list them; prefetch the first Y tile
-    if (tid == 0) sh_own = 0;
-    for (int li = tid; li < nI; li += NT) flags[li] = -1;
-    __syncthreads();
-    for (int k = tid; k < S; k += NT) {
-      const int i = rows[k];
-      if (i >= i0 && i < i0 + nI) flags[i - i0] = k;
-    }
-    for (int o = tid; phase != 2 && o < S * R; o += NT) {
-      const int k = idiv(o, R), r = o - k * R;
-      const int i = rows[k];
-      if (i >= i0 && i < i0 + nI) {
-        const float2 v = ahl[(i - i0) * R + r];
-        __stcg(&g_ahs[(size_t)k * R + r].x, v.x);
-        __stcg(&g_ahs[(size_t)k * R + r].y, v.y);
-      }
-    }
-    STAMP(6);
-    cluster_arrive();  // ------------------------------------------------ B3 (split)
     const bool gather = a.y_mode == TT_Y_GATHER;
     const float2* ybase = gather ? (const float2*)a.ysrc + (size_t)f * a.y_frame_stride + (size_t)s * a.y_slice_stride + j0
                                  : (const float2*)a.ysrc + ((size_t)f * a.nslices + s) * Smax * ny + j0;
@@ -970,7 +951,27 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         cp_async_wait_all();
       }
     };
-    if (phase != 2) issue_y(0, min(KT, S));
+    if (phase != 2) issue_y(0, min(KT, S));  // the first Y tile in flight before the publish below
+    // ======== (b) publish own sampled rows of Ah; list them
+    if (tid == 0) sh_own = 0;
+    for (int li = tid; li < nI; li += NT) flags[li] = -1;
+    __syncthreads();
+    for (int k = tid; k < S; k += NT) {
+      const int i = rows[k];
+      if (i >= i0 && i < i0 + nI) flags[i - i0] = k;
+    }
+    for (int o = tid; phase != 2 && o < S * R; o += NT) {
+      const int k = idiv(o, R), r = o - k * R;
+      const int i = rows[k];
+      if (i >= i0 && i < i0 + nI) {
+        const float2 v = ahl[(i - i0) * R + r];
+        __stcg(&g_ahs[(size_t)k * R + r].x, v.x);
+        __stcg(&g_ahs[(size_t)k * R + r].y, v.y);
+      }
+    }
+    STAMP(6);
+    cluster_arrive();  // ------------------------------------------------ B3 (split)
+
     for (int o = tid; o < nJ * R; o += NT) wacc[o] = make_double2(0.0, 0.0);
     for (int e = eb + tid; e < ee; e += NT) G[e - eb] = make_double2(0.0, 0.0);
     __syncthreads();  // row marks visible to warp 0

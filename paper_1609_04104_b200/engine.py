@@ -276,12 +276,20 @@ class OnlineEngine:
     def check_status(self):
         L.raise_status(int(self.status.max().item()), "online engine")
 
-    def reconstruct(self, out: dict, into: torch.Tensor | None = None, in_place: bool = False) -> torch.Tensor:
-        """Image frames (F, nslices, nx, ny) from the recorded k-space factor
-        history: inverse column FFT of each frame's factors, then the
-        gamma-weighted outer product. ``in_place`` transforms the history
-        itself (no copies); ``into`` receives the images."""
+    def reconstruct(self, out: dict, into: torch.Tensor | None = None, in_place: bool = False,
+                    domain: str = "image") -> torch.Tensor:
+        """Frames (F, nslices, nx, ny) from the recorded k-space factor history. ``domain="image"``:
+        inverse column FFT of each frame's factors, then the gamma-weighted outer product (``in_place``
+        transforms the history itself, no copies). ``domain="kspace"``: the outer product of the k-space
+        factors themselves, Ah diag(gamma) Bh^T = F_x X F_y^T — what run_adaptive records for k-space data
+        (reconstruct_frame(...).kspace, experiment.py:242-245, :525), no FFT. ``into`` receives the frames."""
         F, ns = out["gamma"].shape[:2]
+        if domain == "kspace":
+            X = K.reconstruct(out["ah"].reshape(F * ns, self.nx, self.rank), out["bh"].reshape(F * ns, self.ny, self.rank),
+                              out["gamma"].reshape(F * ns, self.rank), out=into)
+            return X.reshape(F, ns, self.nx, self.ny)
+        if domain != "image":
+            raise ValueError("domain must be 'image' or 'kspace'")
         if in_place:
             A = K.fft_cols_(out["ah"], inverse=True).reshape(F * ns, self.nx, self.rank)
             B = K.fft_cols_(out["bh"], inverse=True).reshape(F * ns, self.ny, self.rank)
@@ -637,14 +645,16 @@ BLOCK_BYTES = 128 << 20  # run_online's default pipeline block: ~128 MB of truth
 
 
 def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, warm_frames=0,
-               warm_epochs=20, chunk=None, keep_history=False, norm_cap=None) -> OnlineResult:
+               warm_epochs=20, chunk=None, keep_history=False, norm_cap=None, recon_domain="image") -> OnlineResult:
     """Public end-to-end call (host in, host out): the online loop over the
     frames of ``kspace`` (T, [nslices,] nx, ny) from image-domain initial
     factors, returning reconstructions and per-frame reports. The analogue of
     ``experiment.run_adaptive`` for pre-noised truth: with ``warm_frames`` > 0
     the leading frames are fully sampled and tracked for ``warm_epochs`` passes
     first (experiment.py:219-239, default 5 x 20 in the reference config) and
-    the results cover the streaming frames only; the policy applies to those.
+    the results cover the streaming frames only; the policy applies to those. ``recon_domain``:
+    "image" (default) returns image frames; "kspace" the k-space estimates Ah diag(gamma) Bh^T, which is what
+    run_adaptive records for k-space data (no inverse FFTs); ``clean`` is an image sequence either way.
     ``policy`` is StaticRows, Informative, AdaptiveSchedule (variable-density rows until the switch
     frame, then informative draws, experiment.py:462-497) or an entries policy. ``norm_cap`` flags
     the frames whose post-update factors exceed it (``norm_exceeded``, tracker.py:406-408).
@@ -744,7 +754,7 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
         with torch.cuda.stream(s_rec):
             if keep_history:
                 hist[a:b].copy_(part["ah"][:, 0])
-            e.reconstruct(part, into=Xd[a:b], in_place=True)  # the history is not needed afterwards
+            e.reconstruct(part, into=Xd[a:b], in_place=True, domain=recon_domain)  # history not needed after
             done = torch.cuda.Event()
             done.record(s_rec)
         s_out.wait_event(done)
@@ -770,8 +780,11 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
     st.copy_(eng.status, non_blocking=True)
     nm = None
     if clean is not None:
-        cl = torch.as_tensor(np.asarray(clean, dtype=np.complex64)).to(dev).reshape(Ts * ns, nx * ny)
-        nm = nmse_frames(cl, Xd.reshape(Ts * ns, nx * ny)).reshape(Ts, ns).cpu().numpy()  # metrics.py:53-62
+        cl = torch.as_tensor(np.asarray(clean, dtype=np.complex64)).to(dev).reshape(Ts * ns, nx, ny)
+        if recon_domain == "kspace":  # F_x X F_y^T of the clean images (unitary: the same NMSE)
+            cl = K.fft_cols_(K.fft_cols_(cl.contiguous()).transpose(1, 2).contiguous()).transpose(1, 2)
+        nm = nmse_frames(cl.reshape(Ts * ns, nx * ny).contiguous(),
+                         Xd.reshape(Ts * ns, nx * ny)).reshape(Ts, ns).cpu().numpy()  # metrics.py:53-62
     comp.synchronize()
     s_out.synchronize()
     L.raise_status(int(st.max().item()), "online engine")

@@ -232,3 +232,22 @@ def test_hessian_step_trajectory_matches_oracle(chunk):
         assert res.mu[f, 0] == pytest.approx(ref["mu"][f], rel=1e-5), f
         assert rel(res.gamma[f, 0], ref["gamma"][f]) < 1e-4, f
     assert np.max(np.abs(np.sqrt(res.nmse[:, 0]) - np.sqrt(np.array(ref["nmse"])))) < 1e-3
+
+
+def test_run_online_kspace_reconstruction_domain():
+    """recon_domain="kspace" returns Ah diag(gamma) Bh^T (run_adaptive's .kspace record, no inverse FFT):
+    the unitary 2-D DFT of the image-domain reconstruction, with the same NMSE against the clean frames."""
+    import paper_1609_04104_b200 as tt
+    from paper_1609_04104_b200.phantom import cine_phantom
+
+    n, R, T = 64, 6, 7
+    ph = cine_phantom(n, n, T, period=8.0, seed=71)
+    A0, B0 = O.random_subspace(n, n, R, seed=72)
+    pol = tt.Informative(k=16, forced=(0,), beta=0.1, key0=73)
+    im = tt.run_online(ph.kspace, A0[None], B0[None], 0.1, tt.Fixed(0.01), pol, clean=ph.clean)
+    ks = tt.run_online(ph.kspace, A0[None], B0[None], 0.1, tt.Fixed(0.01), pol, clean=ph.clean,
+                       recon_domain="kspace")
+    np.testing.assert_array_equal(ks.gamma, im.gamma)
+    for f in range(T):
+        assert rel(ks.recon[f, 0], O.dft2(im.recon[f, 0].astype(np.complex128))) < 1e-5
+    np.testing.assert_allclose(ks.nmse, im.nmse, rtol=1e-4)
