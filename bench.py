@@ -1001,7 +1001,7 @@ def run_ours(args, cfg):
         if e_track is not None:
             e_track.record(stream)
         stream.wait_stream(s_rec)
-    launches_per_step = 4 * nblk
+    launches_per_step = 2 * nblk  # per block: the tracking launch and the reconstruction
 
     for _ in range(args.warmup):
         reset()
