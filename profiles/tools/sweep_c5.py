@@ -6,8 +6,8 @@ Nx = Ny in {128, 256, 512, 1024}, R in {4, 8, 16, 32, 64}, sampling fraction in
 both fixed (variable-density rows, alpha = -1, Philox stream per point) and
 informative (K = ceil(frac N) trials with replacement, forced DC, beta = 0.1).
 Each point runs what `bench.py` times for config 2: the fused online loop
-(`tt_rows_kernel`, T frames in one launch), the inverse column FFTs of the
-per-frame factors and the reconstruction of all T frames, device-timed with
+(`tt_rows_kernel`, T frames in one launch) and the reconstruction of all T frames in k-space
+(Ah diag(gamma) Bh^T, what run_adaptive records for k-space data), device-timed with
 CUDA events, L2 flushed between steps. Reported per point:
 
 * fps            reconstructed frames / s (device, inputs resident)
@@ -88,8 +88,7 @@ def run_point(n, R, frac, kind, ks_dev, clean_dev, T, steps, warmup, flush, hbm_
         K.track_rows(args)
         if evs:
             evs[1].record(stream)
-        K.fft_cols_(out["ah"], inverse=True)
-        K.fft_cols_(out["bh"], inverse=True)
+        # the k-space frames Ah diag(gamma) Bh^T (run_adaptive's record for k-space data, as bench.py's step)
         L.check(lib.tt_reconstruct(stream.cuda_stream, T, n, n, R, out["ah"].data_ptr(), out["bh"].data_ptr(),
                                    out["gamma"].data_ptr(), X.data_ptr()), "reconstruct")
         if evs:
