@@ -1078,7 +1078,12 @@ def run_ours(args, cfg):
                                 recon_domain="kspace")
             torch.cuda.synchronize()
             t_e2e.append(time.perf_counter() - t0)
-        h2d = ks_np.nbytes
+        # bytes that crossed the host link: the whole truth when it is uploaded, only the sampled rows when the
+        # kernels read the page-locked truth in place (run_online's zero-copy mode for truths >= 512 MB)
+        from paper_1609_04104_b200.engine import ZERO_COPY_BYTES
+
+        zc = ks_np.nbytes >= ZERO_COPY_BYTES
+        h2d = (sum(len(r) for fr in res.rows for r in fr) * n * 8) if zc else ks_np.nbytes
         d2h = res.recon.nbytes + res.gamma.nbytes + res.cost.nbytes + res.mu.nbytes + 4 * (T * ns * (eng.max_rows + 1))
         et = torch.tensor([sum(t_e2e)], dtype=torch.float64, device=dev)
         if world > 1:
@@ -1086,7 +1091,8 @@ def run_ours(args, cfg):
         e2e = {"value": T * ns * (world if cfg["slices"] == 1 else 1) * len(t_e2e) / float(et[0]), "unit": "frames/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "call": "paper_1609_04104_b200.run_online(pinned host kspace, recon_domain='kspace') -> host "
-                       "k-space frames (run_adaptive's recon for k-space data) + reports"}
+                       "k-space frames (run_adaptive's recon for k-space data) + reports",
+               "truth_transfer": "zero-copy (sampled rows read in place)" if zc else "upload"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -145,6 +145,11 @@ typedef struct tt_rows_args {
    * row set goes to rows_out / cnt_out (frame 0 slots), which the caller passes to phase 2 as its
    * static table. */
   const double* sraw_in;
+  /* Truth in host memory (appended; 0 = device memory): ysrc is a page-locked host buffer addressed through
+   * unified virtual addressing, and the kernel reads only the frame's sampled rows over the host link
+   * (zero-copy: the truth is consulted only at the sampled rows, as run_adaptive's StreamingProvider
+   * consults it, experiment.py:70-111) instead of the caller uploading every frame. */
+  int32_t y_host;
 } tt_rows_args;
 /* Row energies of a rank's owned k-space rows: energy [nx][rank] (fp64) gets E[i][r] = |Ah_ir|^2 for the owned
  * rows [r0, r0 + nrows) (ah_rows [nrows][rank] complex64) and 0 elsewhere, so a sum all-reduce over the ranks

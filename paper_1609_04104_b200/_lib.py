@@ -48,7 +48,7 @@ class RowsArgs(C.Structure):
         ("cnt_out", _p), ("resid_out", _p), ("ah_hist", _p), ("bh_hist", _p), ("status", _p), ("scratch", _p),
         ("phase_clock", _p), ("shard_rank", _i32), ("shard_world", _i32), ("shard_phase", _i32), ("xw", _p),
         ("xg", _p), ("shard_local", _i32), ("shard_fused", _i32), ("grid_sync", _p),
-        ("draw_wor", _i32), ("norm_cap", _f64), ("norm_out", _p), ("sraw_in", _p),
+        ("draw_wor", _i32), ("norm_cap", _f64), ("norm_out", _p), ("sraw_in", _p), ("y_host", _i32),
     ]
 
 

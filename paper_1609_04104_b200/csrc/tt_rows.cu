@@ -563,7 +563,9 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
   }
   ldl_table_init(tab, R);
   // Y rows by bulk copy (TMA) when every row segment is 16-byte aligned and sized, else cp.async
-  const bool y_bulk = (nJ & 1) == 0 && (j0 & 1) == 0 && (ny & 1) == 0 && ((size_t)a.ysrc & 15) == 0 &&
+  // (host truth: 8-byte cp.async reads of the sampled rows over the host link; the bulk copies take device
+  // memory)
+  const bool y_bulk = !a.y_host && (nJ & 1) == 0 && (j0 & 1) == 0 && (ny & 1) == 0 && ((size_t)a.ysrc & 15) == 0 &&
                       (size_t)KT * nJ * sizeof(float2) < (1u << 20);
   unsigned yph = 0;
   if (tid == 0) {

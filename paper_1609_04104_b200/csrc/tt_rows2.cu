@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(MR_NT, 1) tt_rows_mirror_kernel(const __grid_c
     while (q + 1 < CL && part_begin(Rp, CL, q + 1) <= e) ++q;
     eown[e] = (q << 16) | (e - part_begin(Rp, CL, q));
   }
-  const bool y_bulk = (nJ & 1) == 0 && (j0 & 1) == 0 && (ny & 1) == 0 && ((size_t)a.ysrc & 15) == 0 &&
+  const bool y_bulk = !a.y_host && (nJ & 1) == 0 && (j0 & 1) == 0 && (ny & 1) == 0 && ((size_t)a.ysrc & 15) == 0 &&
                       (size_t)Smax * nJ * sizeof(float2) < (1u << 20);
   unsigned yph = 0;
   if (tid == 0) {

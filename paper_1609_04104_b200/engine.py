@@ -212,10 +212,12 @@ class OnlineEngine:
 
     def args(self, kspace: torch.Tensor, frames: int, out: dict, ah_in=None, bh_in=None, ah_out=None,
              bh_out=None, frame0=None, t0=None) -> L.RowsArgs:
-        """Build the C argument block. ``kspace`` is the resident truth,
-        (T, nslices, nx, ny) complex64; frames [frame0, frame0+frames)."""
-        if kspace.dtype != torch.complex64 or not kspace.is_cuda or not kspace.is_contiguous():
-            raise TypeError("kspace must be a contiguous complex64 CUDA tensor (T, nslices, nx, ny)")
+        """Build the C argument block. ``kspace`` is the truth, (T, nslices, nx, ny) complex64: a CUDA
+        tensor, or a page-locked host tensor read in place (only the sampled rows cross the host link);
+        frames [frame0, frame0+frames)."""
+        host = not kspace.is_cuda
+        if kspace.dtype != torch.complex64 or not kspace.is_contiguous() or (host and not kspace.is_pinned()):
+            raise TypeError("kspace must be a contiguous complex64 CUDA or page-locked host tensor (T, nslices, nx, ny)")
         f0 = self.frame if frame0 is None else int(frame0)
         ks = kspace.reshape(kspace.shape[0], self.nslices, self.nx, self.ny)
         if f0 + frames > ks.shape[0]:
@@ -246,6 +248,7 @@ class OnlineEngine:
             a.rows_cnt = self.rows_cnt.data_ptr() + 4 * f0 * self.nslices
         a.y_mode = L.TT_Y_GATHER
         a.ysrc = ks[f0].data_ptr()
+        a.y_host = 1 if host else 0
         a.y_frame_stride = self.nslices * self.nx * self.ny
         a.y_slice_stride = self.nx * self.ny
         a.lam, a.step_mode, a.mu, a.c_floor, a.c_cap = self.lam, mode, mu, cf, cc
@@ -642,10 +645,12 @@ def _blocks(f0, f1, C):
 
 
 BLOCK_BYTES = 128 << 20  # run_online's default pipeline block: ~128 MB of truth per upload
+ZERO_COPY_BYTES = 512 << 20  # run_online(truth_transfer="auto"): page-locked truths this large are read in place
 
 
 def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, warm_frames=0,
-               warm_epochs=20, chunk=None, keep_history=False, norm_cap=None, recon_domain="image") -> OnlineResult:
+               warm_epochs=20, chunk=None, keep_history=False, norm_cap=None, recon_domain="image",
+               truth_transfer="auto") -> OnlineResult:
     """Public end-to-end call (host in, host out): the online loop over the
     frames of ``kspace`` (T, [nslices,] nx, ny) from image-domain initial
     factors, returning reconstructions and per-frame reports. The analogue of
@@ -655,6 +660,10 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
     the results cover the streaming frames only; the policy applies to those. ``recon_domain``:
     "image" (default) returns image frames; "kspace" the k-space estimates Ah diag(gamma) Bh^T, which is what
     run_adaptive records for k-space data (no inverse FFTs); ``clean`` is an image sequence either way.
+    ``truth_transfer``: "upload" copies the truth to the device block by block; "zero-copy" has the row
+    kernels read a page-locked host truth in place, only each frame's sampled rows crossing the host link;
+    "auto" takes zero-copy for page-locked truths of at least ZERO_COPY_BYTES (there the full upload
+    dominates the call; below it the per-frame host-link latency costs more than the copy saves).
     ``policy`` is StaticRows, Informative, AdaptiveSchedule (variable-density rows until the switch
     frame, then informative draws, experiment.py:462-497) or an entries policy. ``norm_cap`` flags
     the frames whose post-update factors exceed it (``norm_exceeded``, tracker.py:406-408).
@@ -672,6 +681,16 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
     if src.dim() == 3:
         src = src[:, None]
     T, ns, nx, ny = src.shape
+    # a page-locked host truth is read in place by the row kernels (zero-copy: only each frame's sampled rows
+    # cross the host link, as run_adaptive's StreamingProvider consults the truth at the sampled indices);
+    # pageable inputs are uploaded block by block
+    if truth_transfer not in ("auto", "upload", "zero-copy"):
+        raise ValueError("truth_transfer must be 'auto', 'upload' or 'zero-copy'")
+    rows_policy = not isinstance(policy, (InformativeEntries, StaticEntries))
+    if truth_transfer == "zero-copy" and not (rows_policy and not on_dev and src.is_pinned()):
+        raise ValueError("zero-copy needs a page-locked host truth and a row policy")
+    zero_copy = rows_policy and not on_dev and src.is_pinned() and (
+        truth_transfer == "zero-copy" or (truth_transfer == "auto" and src.numel() * 8 >= ZERO_COPY_BYTES))
     A0 = np.asarray(A0).reshape(ns, nx, -1)
     R = A0.shape[-1]
     if isinstance(policy, (InformativeEntries, StaticEntries)):
@@ -684,7 +703,7 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
     # small upload must not queue behind the truth uploads on the copy engine
     eng, ekey = _take_engine(nx, ny, R, ns, lam, step, sched.informative if sched else policy, cluster, t0, norm_cap)
     eng.set_image_factors(A0, np.asarray(B0).reshape(ns, ny, R))
-    kd = src.contiguous() if on_dev else torch.empty(T, ns, nx, ny, dtype=torch.complex64, device=dev)
+    kd = src.contiguous() if (on_dev or zero_copy) else torch.empty(T, ns, nx, ny, dtype=torch.complex64, device=dev)
     W = int(warm_frames)
     if W < 0 or W > T:
         raise ValueError("warm_frames must be in [0, T]")
@@ -703,7 +722,7 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
     ev_in = []
     with torch.cuda.stream(s_in):
         for f0, f1 in bounds:
-            if not on_dev:
+            if not (on_dev or zero_copy):
                 kd[f0:f1].copy_(src[f0:f1], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(s_in)
@@ -711,7 +730,8 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
     blocks = list(zip(bounds, ev_in))
     if W:
         comp.wait_event(blocks[0][1])
-        warm_up(eng, kd[:W], warm_epochs)
+        # the warm-up revisits its full frames warm_epochs times: resident on the device even in zero-copy mode
+        warm_up(eng, kd[:W].to(dev, non_blocking=True) if zero_copy else kd[:W], warm_epochs)
         blocks = blocks[1:]
         if clean is not None:
             clean = np.asarray(clean).reshape(T, ns, nx, ny)[W:]

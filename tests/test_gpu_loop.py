@@ -251,3 +251,36 @@ def test_run_online_kspace_reconstruction_domain():
     for f in range(T):
         assert rel(ks.recon[f, 0], O.dft2(im.recon[f, 0].astype(np.complex128))) < 1e-5
     np.testing.assert_allclose(ks.nmse, im.nmse, rtol=1e-4)
+
+
+@pytest.mark.parametrize("transfer", ["upload", "zero-copy"])
+def test_run_online_truth_transfer_modes_are_bit_identical(transfer):
+    """The row kernels reading a page-locked host truth in place (only the sampled rows cross the host link)
+    give the same bits as the uploaded truth and the device-resident truth."""
+    import torch
+
+    import paper_1609_04104_b200 as tt
+    from paper_1609_04104_b200.phantom import cine_phantom
+
+    n, R, T, ns = 64, 6, 9, 3
+    ks = np.stack([cine_phantom(n, n, T, period=8.0, seed=80 + s).kspace for s in range(ns)], axis=1)
+    A0 = np.stack([O.random_subspace(n, n, R, seed=90 + s)[0] for s in range(ns)])
+    B0 = np.stack([O.random_subspace(n, n, R, seed=90 + s)[1] for s in range(ns)])
+    pol = tt.Informative(k=16, forced=(0,), beta=0.1, key0=5)
+    ref = tt.run_online(torch.from_numpy(ks.astype(np.complex64)).cuda(), A0, B0, 0.1, tt.Fixed(0.01), pol)
+    pinned = torch.from_numpy(ks.astype(np.complex64)).pin_memory()
+    got = tt.run_online(pinned, A0, B0, 0.1, tt.Fixed(0.01), pol, truth_transfer=transfer, chunk=4)
+    np.testing.assert_array_equal(got.gamma, ref.gamma)
+    np.testing.assert_array_equal(got.recon, ref.recon)
+    for f in range(T):
+        for s in range(ns):
+            np.testing.assert_array_equal(got.rows[f][s], ref.rows[f][s])
+    # with the warm-up protocol (its full frames are made resident for the epochs)
+    ref_w = tt.run_online(torch.from_numpy(ks.astype(np.complex64)).cuda(), A0, B0, 0.1, tt.Fixed(0.01), pol,
+                          warm_frames=2, warm_epochs=3)
+    got_w = tt.run_online(pinned, A0, B0, 0.1, tt.Fixed(0.01), pol, truth_transfer=transfer, warm_frames=2,
+                          warm_epochs=3)
+    np.testing.assert_array_equal(got_w.gamma, ref_w.gamma)
+    np.testing.assert_array_equal(got_w.recon, ref_w.recon)
+    with pytest.raises(ValueError):
+        tt.run_online(ks, A0, B0, 0.1, tt.Fixed(0.01), pol, truth_transfer="zero-copy")  # pageable
