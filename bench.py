@@ -783,7 +783,6 @@ def run_row_sharded(args, cfg):
     e = fresh()
     r0, r1 = e.r0, e.r1
     out = e.make_outputs(T)
-    Afull = torch.empty(T, n, R, dtype=torch.complex64, device=dev)
     Xblk = torch.empty(T, r1 - r0, n, dtype=torch.complex64, device=dev)
     lib = L.lib()
     stream = torch.cuda.current_stream()
@@ -798,18 +797,9 @@ def run_row_sharded(args, cfg):
 
     def step():
         e.replay()
-        # all-gather of the owned k-space rows history, inverse FFTs, this rank's image-row block
-        if world > 1:
-            parts = [torch.empty(T, b - a, R, dtype=torch.complex64, device=dev)
-                     for a, b in [tuple((n * p) // world for p in (q, q + 1)) for q in range(world)]]
-            dist.all_gather(parts, out["ah"])
-            Afull.copy_(torch.cat(parts, dim=1))
-        else:
-            Afull.copy_(out["ah"])
-        K.fft_cols_(Afull, inverse=True)
-        K.fft_cols_(out["bh"], inverse=True)
-        Ablk = Afull[:, r0:r1].contiguous()
-        L.check(lib.tt_reconstruct(stream.cuda_stream, T, r1 - r0, n, R, Ablk.data_ptr(), out["bh"].data_ptr(),
+        # this rank's block of k-space rows of every frame, Ah_rows diag(gamma) Bh^T (row i of the k-space frame
+        # needs only row i of Ah: the reconstruction shards by rows with no collective and no FFT)
+        L.check(lib.tt_reconstruct(stream.cuda_stream, T, r1 - r0, n, R, out["ah"].data_ptr(), out["bh"].data_ptr(),
                                    out["gamma"].data_ptr(), Xblk.data_ptr()), "reconstruct")
 
     for _ in range(args.warmup):
@@ -965,7 +955,8 @@ def run_ours(args, cfg):
         pol = tt.StaticRows(tab, np.full((T, ns), Smax))
     else:
         pol = tt.Informative(k=cfg["K"], forced=cfg["forced"], beta=cfg["beta"], key0=2024, key1=slice_ids[0])
-    eng = tt.OnlineEngine(n, n, R, ns, cfg["lam"], tt.Fixed(cfg["mu"]), pol, cluster=args.cluster)
+    step_rule = tt.HessianBound(1e-3, 1e9) if args.step == "hessian" else tt.Fixed(cfg["mu"])
+    eng = tt.OnlineEngine(n, n, R, ns, cfg["lam"], step_rule, pol, cluster=args.cluster)
     eng.set_image_factors(A0, B0)
     ah0, bh0 = eng.ah.clone(), eng.bh.clone()
     ks = torch.from_numpy(ks_np).to(dev)
@@ -1068,13 +1059,13 @@ def run_ours(args, cfg):
         # call runs): both pinned result blocks are then in torch's host caching allocator
         res = None
         for _ in range(2):
-            res = tt.run_online(ks_pin, A0, B0, cfg["lam"], tt.Fixed(cfg["mu"]), pol, cluster=args.cluster,
+            res = tt.run_online(ks_pin, A0, B0, cfg["lam"], step_rule, pol, cluster=args.cluster,
                                 recon_domain="kspace")
         torch.cuda.synchronize()
         t_e2e = []
         for _ in range(max(1, args.steps)):
             t0 = time.perf_counter()
-            res = tt.run_online(ks_pin, A0, B0, cfg["lam"], tt.Fixed(cfg["mu"]), pol, cluster=args.cluster,
+            res = tt.run_online(ks_pin, A0, B0, cfg["lam"], step_rule, pol, cluster=args.cluster,
                                 recon_domain="kspace")
             torch.cuda.synchronize()
             t_e2e.append(time.perf_counter() - t0)
@@ -1117,7 +1108,8 @@ def run_ours(args, cfg):
     parity = None
     if rank == 0 and not args.no_parity:
         parity = run_parity(cfg, ks_np[:, 0], clean_np[:, 0], A0[0], B0[0], out, Xr[:, 0], cnt[:, 0],
-                            clean_k=cl[:, 0].cpu().numpy())
+                            clean_k=cl[:, 0].cpu().numpy(),
+                            ostep=("hessian", 1e-3, 1e9) if args.step == "hessian" else ("fixed", cfg["mu"]))
 
     if world > 1:
         dist.destroy_process_group()
@@ -1128,6 +1120,7 @@ def run_ours(args, cfg):
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "c64", "data": "synthetic",
         "config": dict(workload_config(args, cfg), slices_per_gpu=ns, cluster_ctas_per_slice=eng.cluster,
+                       step=("HessianBound(1e-3, 1e9)" if args.step == "hessian" else f"Fixed({cfg['mu']})"),
                        tracking_launches_per_step=nblk,
                        parallelism=f"{'replicas' if cfg['slices'] == 1 else 'slice-shard'} x{world}"),
         "gpu_launches": launches_per_step * args.steps,
@@ -1188,7 +1181,7 @@ def api_loop_rate(cfg, ks_host, A0, B0, frames=24):
 PARITY_FRAMES = {"c4": 12}  # the oracle's numpy SVD at 1024^2 takes ~1 s per frame
 
 
-def run_parity(cfg, ks, clean, A0, B0, out, X, cnt, clean_k=None):
+def run_parity(cfg, ks, clean, A0, B0, out, X, cnt, clean_k=None, ostep=None):
     """Slice 0 of the last timed step against the CPU oracle (oracle/tt_oracle.py, pinned to the
     reference) fed the same per-frame rows the device drew: per-frame gamma (relative) and the NRMSE
     trajectory (absolute) over the first T frames (PARITY_FRAMES bounds c4); the device's masks are
@@ -1203,7 +1196,8 @@ def run_parity(cfg, ks, clean, A0, B0, out, X, cnt, clean_k=None):
     A0c = np.asarray(A0).astype(np.complex64).astype(np.complex128)
     B0c = np.asarray(B0).astype(np.complex64).astype(np.complex128)
     t0 = time.perf_counter()
-    ref = O.online_run(ks[:T], A0c, B0c, cfg["lam"], ("fixed", cfg["mu"]), {"kind": "static", "rows": rows},
+    ostep = ostep or ("fixed", cfg["mu"])
+    ref = O.online_run(ks[:T], A0c, B0c, cfg["lam"], ostep, {"kind": "static", "rows": rows},
                        clean=clean[:T])
     gam = out["gamma"][:T, 0].cpu().numpy()
     ge = max(float(np.linalg.norm(gam[f] - ref["gamma"][f]) / max(np.linalg.norm(ref["gamma"][f]), 1e-300))
@@ -1214,7 +1208,7 @@ def run_parity(cfg, ks, clean, A0, B0, out, X, cnt, clean_k=None):
     ne = float(np.max(np.abs(nr_dev - np.sqrt(np.asarray(ref["nmse"])))))
     first_div = None
     if "K" in cfg:  # the oracle's own draws from its own probabilities (device masks bit-exact until a near-tie)
-        free = O.online_run(ks[:T], A0c, B0c, cfg["lam"], ("fixed", cfg["mu"]),
+        free = O.online_run(ks[:T], A0c, B0c, cfg["lam"], ostep,
                             {"kind": "informative", "k": cfg["K"], "forced": list(cfg["forced"]), "beta": cfg["beta"],
                              "key": (2024, 0)})
         for f in range(T):
@@ -1236,6 +1230,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
     ap.add_argument("--cluster", type=int, default=0)
+    ap.add_argument("--step", choices=["fixed", "hessian"], default="fixed",
+                    help="step rule of the default arms: Fixed(mu) or the Lipschitz HessianBound(1e-3, 1e9) (config.py)")
     ap.add_argument("--cpu-frames", type=int, default=100)
     ap.add_argument("--ref-frames", type=int, default=0,
                     help="frames per reference step (default: the config's T; 8 for c4, SURVEY §8d)")
