@@ -970,7 +970,14 @@ def run_ours(args, cfg):
     # FFTs + reconstruction run on a second stream as soon as its tracking is done, on the SMs the
     # tracking clusters leave free (run_online's pipeline without the host transfers)
     nblk = max(1, min(args.blocks, T))
-    bounds = [(T * i // nblk, T * (i + 1) // nblk) for i in range(nblk)]
+    # the last block's reconstruction runs after the tracking ends (the step's tail): it is made short
+    # (--tail-frac of an even block), the others share the rest evenly
+    if nblk > 1 and args.tail_frac < 1.0:
+        last = max(1, int(round(args.tail_frac * T / nblk)))
+        head = T - last
+        bounds = [(head * i // (nblk - 1), head * (i + 1) // (nblk - 1)) for i in range(nblk - 1)] + [(head, T)]
+    else:
+        bounds = [(T * i // nblk, T * (i + 1) // nblk) for i in range(nblk)]
     parts = [{k: v[a:b] for k, v in out.items()} for a, b in bounds]
     tracked = [torch.cuda.Event() for _ in bounds]
 
@@ -1240,6 +1247,8 @@ def main():
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--row-shard", action="store_true", help="config c4: use the row-sharded two-phase path")
     ap.add_argument("--blocks", type=int, default=4, help="tracking launches per step (reconstruction overlaps)")
+    ap.add_argument("--tail-frac", type=float, default=1.0,
+                    help="size of the last tracking block relative to an even split (its reconstruction is the tail)")
     ap.add_argument("--local-ranks", type=int, default=0,
                     help="config c4 on one GPU: row-shard over this many thread-block clusters (fused launch)")
     args = ap.parse_args()
