@@ -191,6 +191,16 @@ static bool rows_make_plan_cap(int nx, int ny, int R, int Smax, int CL, int red_
 // (K = R, fp32 operands: cgemm_tile) deliver float2 and are subtracted from the fp64 W / Z in fp64, so the
 // update keeps the digits the cancellation would cost in fp32.
 enum { EPI_W_ACC = 0, EPI_Z_STORE = 1, EPI_Q_UPDATE = 2, EPI_P_UPDATE = 3, EPI_P_MAPPED = 4 };
+struct RowsEpiGB {    // GB partial on the fp64 tensor cores: C = Bh_J^T conj(Bh_J), C[m][n] = GB[n][m]
+  double2* dst;       // this CTA's packed partial slots (L2)
+  TT_DEV void operator()(int m, int n, int ks, double2 v) const {
+    (void)ks;
+    if (n < m) return;
+    double2* d = dst + tri_idx(n, m);
+    __stcg(&d->x, v.x);
+    __stcg(&d->y, v.y);
+  }
+};
 struct RowsEpiD {     // W / Z: fp64 values
   int mode, R;
   double2* acc;       // W: wacc
@@ -631,6 +641,10 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     // packed entry per thread
     if (gb_tiled) {
       gb_partials_tiled<TIGHT>(bhl, bh64, R, nJ, Rp, gb_nt, gb_parts, tab, gbt, g_gbp + (size_t)c * Rp, gb_jo, gb_js);
+    } else if (!TIGHT && Rp > NT && gb_js == 1) {
+      // large ranks (config 4: R = 32, 528 packed entries over 256 threads) on the fp64 tensor cores: the full
+      // R x R product over the own rows, the lower triangle kept (the same exact products, another K order)
+      zgemm_dmma<ZG>(R, R, nJ, bh64, 1, R, bh64, R, 1, RowsEpiGB{g_gbp + (size_t)c * Rp});
     } else {
       for (int e = tid; e < Rp; e += NT) {
         const int ij = tab[e];
@@ -1253,11 +1267,35 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
         }
       }
     }
-    for (int e = tid; e < Rp; e += NT) {
+    // the entries past the first: every load of the thread issued before the first use (R = 32: 3 entries)
+    constexpr int GPF = 3;
+    double2 gap[GPF], gbp[GPF];
+#pragma unroll
+    for (int u = 1; u < GPF; ++u) {
+      const int e = tid + u * NT;
+      gap[u] = gbp[u] = make_double2(0.0, 0.0);
+      if (e < Rp) {
+        gap[u] = phase == 2 ? make_double2(xg_at(2 * e), xg_at(2 * e + 1)) : __ldcg(&g_ga[e]);
+        gbp[u] = fused ? make_double2(__ldcg(xgp + 2 * Rp + 2 + 2 * e), __ldcg(xgp + 2 * Rp + 3 + 2 * e))
+                       : __ldcg(&g_gb[e]);
+      }
+    }
+    gap[0] = gae0;
+    gbp[0] = gbe0;
+    for (int e = tid, u = 0; e < Rp; e += NT, ++u) {
       const int ij = tab[e];
       const int r = ij >> 8, q = ij & 255;
-      double2 gae = gae0, gbe = gbe0;
-      if (e != tid) {
+      double2 gae, gbe;
+      if (u < GPF) {
+        gae = gap[0];
+        gbe = gbp[0];
+#pragma unroll
+        for (int w = 1; w < GPF; ++w)
+          if (u == w) {
+            gae = gap[w];
+            gbe = gbp[w];
+          }
+      } else {
         gae = phase == 2 ? make_double2(xg_at(2 * e), xg_at(2 * e + 1)) : __ldcg(&g_ga[e]);
         gbe = fused ? make_double2(__ldcg(xgp + 2 * Rp + 2 + 2 * e), __ldcg(xgp + 2 * Rp + 3 + 2 * e))
                     : __ldcg(&g_gb[e]);
