@@ -201,6 +201,118 @@ __global__ void __launch_bounds__(RC_NT, 3) recon3_kernel(int nx, int ny, int R,
   }
 }
 
+
+// Gauss form with full-sector stores: a thread's 4 columns are 2 tj, 2 tj + 1, 2 tj + 32, 2 tj + 33 (one 16 B
+// store per pair: a warp's store covers 256 contiguous bytes of a row), its 4 rows 4 ti .. 4 ti + 3 (LDS.128);
+// the three planes are consumed one after the other so only 8 operands are live.
+__global__ void __launch_bounds__(RC_NT, 3) recon3b_kernel(int nx, int ny, int R, const float2* __restrict__ A,
+                                                           const float2* __restrict__ B, const float2* __restrict__ gamma,
+                                                           float2* __restrict__ X) {
+  extern __shared__ __align__(16) float rgs[];
+  const int PL = R * RG_TP;
+  float* p_ar = rgs;
+  float* p_ai = rgs + PL;
+  float* p_sa = rgs + 2 * PL;
+  float* p_br = rgs + 3 * PL;
+  float* p_db = rgs + 4 * PL;
+  float* p_sb = rgs + 5 * PL;
+  const int tid = threadIdx.x;
+  const int f = blockIdx.z;
+  const int i0 = blockIdx.y * RC_T, j0 = blockIdx.x * RC_T;
+  const float2* Af = A + (size_t)f * nx * R;
+  const float2* Bf = B + (size_t)f * ny * R;
+  const float2* gf = gamma + (size_t)f * R;
+  for (int base = 0; base < RC_T * R; base += 4 * RC_NT) {
+    float2 va[4], vb[4], vg[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int o = base + u * RC_NT + tid;
+      va[u] = vb[u] = vg[u] = make_float2(0.f, 0.f);
+      if (o < RC_T * R) {
+        const int ii = idiv(o, R), r = o - ii * R;
+        const int i = i0 + ii, j = j0 + ii;
+        vg[u] = gf[r];
+        if (i < nx) va[u] = Af[(size_t)i * R + r];
+        if (j < ny) vb[u] = Bf[(size_t)j * R + r];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int o = base + u * RC_NT + tid;
+      if (o < RC_T * R) {
+        const int ii = idiv(o, R), r = o - ii * R;
+        const float2 a = cmul(va[u], vg[u]), b = vb[u];
+        const int at = r * RG_TP + ii;
+        p_ar[at] = a.x;
+        p_ai[at] = a.y;
+        p_sa[at] = a.x + a.y;
+        p_br[at] = b.x;
+        p_db[at] = b.y - b.x;
+        p_sb[at] = b.x + b.y;
+      }
+    }
+  }
+  __syncthreads();
+  const int tj = tid & 15, ti = tid >> 4;
+  float k1[4][4], k2[4][4], k3[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) k1[u][v] = k2[u][v] = k3[u][v] = 0.f;
+  const int ca = 4 * ti, cb = 2 * tj;
+#pragma unroll 2
+  for (int r = 0; r < R; ++r) {
+    const int ro = r * RG_TP;
+    {
+      const float4 a = *(const float4*)(p_sa + ro + ca);
+      const float2 b0 = *(const float2*)(p_br + ro + cb), b1 = *(const float2*)(p_br + ro + cb + 32);
+      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b0.x, b0.y, b1.x, b1.y};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) k1[u][v] = fmaf(bv[v], av[u], k1[u][v]);
+    }
+    {
+      const float4 a = *(const float4*)(p_ar + ro + ca);
+      const float2 b0 = *(const float2*)(p_db + ro + cb), b1 = *(const float2*)(p_db + ro + cb + 32);
+      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b0.x, b0.y, b1.x, b1.y};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) k2[u][v] = fmaf(av[u], bv[v], k2[u][v]);
+    }
+    {
+      const float4 a = *(const float4*)(p_ai + ro + ca);
+      const float2 b0 = *(const float2*)(p_sb + ro + cb), b1 = *(const float2*)(p_sb + ro + cb + 32);
+      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b0.x, b0.y, b1.x, b1.y};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) k3[u][v] = fmaf(av[u], bv[v], k3[u][v]);
+    }
+  }
+  float2* Xf = X + (size_t)f * nx * ny;
+  const bool vec = (ny & 1) == 0;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int i = i0 + ca + u;
+    if (i >= nx) continue;
+    float2* xr = Xf + (size_t)i * ny;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = j0 + cb + 32 * h;
+      const float2 o0 = make_float2(k1[u][2 * h] - k3[u][2 * h], k1[u][2 * h] + k2[u][2 * h]);
+      const float2 o1 = make_float2(k1[u][2 * h + 1] - k3[u][2 * h + 1], k1[u][2 * h + 1] + k2[u][2 * h + 1]);
+      if (vec && j + 1 < ny) {
+        *(float4*)(xr + j) = make_float4(o0.x, o0.y, o1.x, o1.y);
+      } else {
+        if (j < ny) xr[j] = o0;
+        if (j + 1 < ny) xr[j + 1] = o1;
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- split-BF16 tensor-core form
 // The same X_f = A_f diag(gamma_f) B_f^T on the tensor cores at fp32 accuracy. As real products over
 // K = 2 RP (RP = R padded to 8):
@@ -446,6 +558,10 @@ static void run(int form, int F, int nx, int ny, int R, const float2* a, const f
     const size_t sm = sizeof(float) * 6 * RG_TP * (size_t)R;
     CK(cudaFuncSetAttribute(recon3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     recon3_kernel<<<grid, RC_NT, sm>>>(nx, ny, R, a, b, g, x);
+  } else if (form == 3) {
+    const size_t sm = sizeof(float) * 6 * RG_TP * (size_t)R;
+    CK(cudaFuncSetAttribute(recon3b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    recon3b_kernel<<<grid, RC_NT, sm>>>(nx, ny, R, a, b, g, x);
   } else {
     switch ((R + 7) / 8) {
       case 1: launch_tc<1>(F, nx, ny, R, a, b, g, x); break;
@@ -476,11 +592,11 @@ int main(int argc, char** argv) {
   run(0, F, nx, ny, R, a, b, g, x0);
   std::vector<float2> r0(nxo), r1(nxo);
   CK(cudaMemcpy(r0.data(), x0, nxo * sizeof(float2), cudaMemcpyDeviceToHost));
-  const char* names[3] = {"four-product fp32", "three-product fp32", "split-BF16 mma.sync"};
+  const char* names[4] = {"four-product fp32", "three-product fp32", "split-BF16 mma.sync", "three-product, 16B st"};
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int form = 0; form < 3; ++form) {
+  for (int form = 0; form < 4; ++form) {
     if (form == 2 && R > 32) continue;
     for (int w = 0; w < 3; ++w) run(form, F, nx, ny, R, a, b, g, x1);
     cudaEventRecord(e0);
