@@ -5,6 +5,7 @@
 // transpose). In run_adaptive it is called once per frame with the
 // post-update factors and that frame's gamma (experiment.py:525).
 //
+// R <= 32 runs on the tensor cores (tt_recon_tc.cu); this CUDA-core form covers R up to 64.
 // Each CTA produces a 64 x 64 output tile: the gamma-scaled A tile and the B
 // tile are staged transposed ([r][64]) in shared memory and every thread
 // accumulates a 4 x 4 register block over r (complex fp32 FMAs), then writes
@@ -86,6 +87,9 @@ __global__ void __launch_bounds__(RC_NT) recon_kernel(int nx, int ny, int R, con
   }
 }
 
+int tt_recon_tc(cudaStream_t st, int frames, int nx, int ny, int rank, const float2* a, const float2* b,
+                const float2* g, float2* x, int vec);  // tt_recon_tc.cu
+
 extern "C" int tt_reconstruct(void* stream, int frames, int nx, int ny, int rank, const float* a, const float* b,
                               const float* gamma, float* x_out) {
   if (frames < 0 || nx < 1 || ny < 1 || rank < 1 || !a || !b || !gamma || !x_out)
@@ -93,6 +97,12 @@ extern "C" int tt_reconstruct(void* stream, int frames, int nx, int ny, int rank
   if (rank > RC_RMAX) return tt_fail(TT_EUNSUPPORTED, "tt_reconstruct: rank > %d", RC_RMAX);
   if (frames == 0) return TT_OK;
   if (frames > 65535) return tt_fail(TT_EINVAL, "tt_reconstruct: frames > 65535 per call");
+  // R <= 32: the tensor-core form (3xTF32 on tcgen05, tt_recon_tc.cu); TT_RECON_FFMA=1 selects the
+  // CUDA-core form below at any rank (tests compare the two)
+  const char* env = getenv("TT_RECON_FFMA");
+  if (rank <= 32 && !(env && env[0] == '1'))
+    return tt_recon_tc((cudaStream_t)stream, frames, nx, ny, rank, (const float2*)a, (const float2*)b,
+                       (const float2*)gamma, (float2*)x_out, (ny % 2 == 0 && ((size_t)x_out & 15) == 0) ? 1 : 0);
   const size_t sm = sizeof(float2) * 2 * RC_TP * (size_t)rank;
   static size_t cfg[TT_MAXDEV] = {0};
   TT_CUDA_TRY(tt_smem_attr((const void*)recon_kernel, sm, cfg));

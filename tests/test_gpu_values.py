@@ -69,6 +69,34 @@ def test_batched_reconstruct_matches_outer_product(shape):
         assert rel(X[f], O.synth(A[f], B[f], gm[f])) < 1e-5
 
 
+@pytest.mark.parametrize("shape", [(256, 256, 16, 5), (128, 128, 8, 3), (130, 77, 5, 2), (33, 300, 32, 2),
+                                   (512, 384, 24, 2), (256, 256, 20, 3), (1, 1, 1, 1), (200, 129, 9, 2)])
+def test_reconstruct_tensor_core_form(shape, monkeypatch):
+    """R <= 32 runs on tcgen05 (3xTF32, tt_recon_tc.cu): against the complex128 outer product element by
+    element, scaled by sum_r |a'_ir| |b_jr| (the bound both fp32 forms share), and against the CUDA-core
+    form (TT_RECON_FFMA=1); ragged tiles, odd ny, R not a multiple of 4, several frames per launch."""
+    import torch
+
+    from paper_1609_04104_b200 import _ops as K
+
+    nx, ny, R, F = shape
+    rng = np.random.default_rng(nx * 7 + R)
+    A = (rng.standard_normal((F, nx, R)) + 1j * rng.standard_normal((F, nx, R))).astype(np.complex64)
+    B = (rng.standard_normal((F, ny, R)) + 1j * rng.standard_normal((F, ny, R))).astype(np.complex64)
+    gm = (rng.standard_normal((F, R)) + 1j * rng.standard_normal((F, R))).astype(np.complex64)
+    a, b, g = (torch.from_numpy(v).cuda() for v in (A, B, gm))
+    Xt = K.reconstruct(a, b, g).cpu().numpy()
+    monkeypatch.setenv("TT_RECON_FFMA", "1")
+    Xf = K.reconstruct(a, b, g).cpu().numpy()
+    for f in range(F):
+        a2 = A[f].astype(np.complex128) * gm[f].astype(np.complex128)
+        ex = a2 @ B[f].astype(np.complex128).T
+        bound = np.abs(a2) @ np.abs(B[f].astype(np.complex128)).T
+        assert np.max(np.abs(Xt[f] - ex) / bound) < 4e-6
+        assert np.max(np.abs(Xf[f] - ex) / bound) < 4e-6
+        assert rel(Xt[f], ex) < 2e-6
+
+
 @pytest.mark.parametrize("n,ncols", [(256, 1), (256, 20), (256, 33), (1024, 64), (2048, 5), (8, 70)])
 def test_fft_cols_column_blocking(n, ncols):
     """Column counts that split over several CTAs (up to 32 whole columns per CTA, fewer at large n)
