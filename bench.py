@@ -964,6 +964,13 @@ def run_ours(args, cfg):
     X = torch.empty(T, ns, n, n, dtype=torch.complex64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
+    if args.track_priority:
+        # tracking on a high-priority stream: at a block boundary the next tracking launch's clusters go
+        # ahead of the reconstruction CTAs still pending (those take what is left of their block later)
+        hp = torch.cuda.Stream(dev, priority=-1)
+        hp.wait_stream(stream)
+        torch.cuda.set_stream(hp)
+        stream = hp
     s_rec = torch.cuda.Stream(dev)
     # one step = the T-frame sequence in `nblk` tracking launches on the compute stream (the resident
     # state carries across launches; results are launch-boundary invariant); each block's inverse column
@@ -995,6 +1002,11 @@ def run_ours(args, cfg):
             ev.record(stream)
             s_rec.wait_event(ev)
             with torch.cuda.stream(s_rec):
+                if args.recon_ctas:
+                    if b < T:
+                        os.environ["TT_RECON_MAXCTAS"] = str(args.recon_ctas)
+                    else:
+                        os.environ.pop("TT_RECON_MAXCTAS", None)
                 eng.reconstruct(part, into=X[a:b], domain="kspace")  # k-space frames (run_adaptive's .kspace)
         if e_track is not None:
             e_track.record(stream)
@@ -1247,6 +1259,10 @@ def main():
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--row-shard", action="store_true", help="config c4: use the row-sharded two-phase path")
     ap.add_argument("--blocks", type=int, default=4, help="tracking launches per step (reconstruction overlaps)")
+    ap.add_argument("--track-priority", type=int, default=0,
+                    help="1: the tracking launches run on a high-priority stream (measured: no effect)")
+    ap.add_argument("--recon-ctas", type=int, default=0,
+                    help="experiment: persistent reconstruction CTAs of every block but the last (0: one per SM)")
     ap.add_argument("--tail-frac", type=float, default=1.0,
                     help="size of the last tracking block relative to an even split (its reconstruction is the tail)")
     ap.add_argument("--local-ranks", type=int, default=0,

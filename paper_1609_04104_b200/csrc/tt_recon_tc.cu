@@ -11,13 +11,18 @@
 // accumulates lo*hi + hi*lo + hi*hi in fp32 (the dropped lo*lo term and lo's own rounding are ~2^-22 of
 // |x|; the four-product CUDA-core form stays in tt_recon.cu for R > 32 and as the check).
 //
-// One persistent CTA per SM (512 TMEM columns: two 128 x 256 fp32 accumulators). Warps 0-3 stage a tile's
+// One persistent CTA per SM (512 TMEM columns: two 128 x 256 fp32 accumulators); tiles are handed out by a
+// global counter (the first tile of a CTA is its block index), so CTAs that become resident late - the
+// reconstruction of a block of frames overlaps the tracking of the next one, which holds most SMs - take
+// only what is left, and the CTAs on the free SMs keep working meanwhile. Warps 0-3 stage a tile's
 // operands (fp32 loads, gamma scaling, the TF32 split) into shared memory in the no-swizzle K-major core-
 // matrix layout, thread 0 then issues the tile's 3 Kp/8 tcgen05.mma (M 128, N 256, K 8) into accumulator
 // n % 2 and commits them to an mbarrier; warps 4-7 drain the other accumulator with tcgen05.ld (one output
 // row per thread, 128 contiguous bytes per 32 columns) while the next tile is staged and multiplied. The
 // kernel is bound by the HBM writes of the frames.
+#include <cuda.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include "tt_block.cuh"
 #include "tt_common.cuh"
@@ -82,20 +87,29 @@ template <int KC>
 __global__ void __launch_bounds__(RT_NT, 1) recon_tc_kernel(int frames, int nx, int ny, int R,
                                                             const float2* __restrict__ A, const float2* __restrict__ B,
                                                             const float2* __restrict__ gamma, float2* __restrict__ X,
-                                                            int vec) {
+                                                            int vec, unsigned* __restrict__ tile_ctr,
+                                                            const __grid_constant__ CUtensorMap xmap) {
   constexpr int Kp = 4 * KC, HC = KC / 2;  // HC: chunks per half (re | im), 4 complex per chunk
   constexpr unsigned SBO = KC * 128;        // bytes per 8-row group (all its K chunks, 128 B each)
   constexpr unsigned A_BYTES = RT_M * Kp * 4, B_BYTES = 2 * RT_NC * Kp * 4;
+  constexpr int NOB = KC <= 12 ? 4 : 2;  // output boxes in flight per drain warp
+  constexpr unsigned OB_BYTES = 4 * NOB * 4096 > 4 * 32 * 36 * 4 ? 4 * NOB * 4096 : 4 * 32 * 36 * 4;
   extern __shared__ __align__(1024) unsigned char sm[];
   unsigned char* a_hi = sm;
   unsigned char* a_lo = sm + A_BYTES;
   unsigned char* b_hi = sm + 2 * A_BYTES;
   unsigned char* b_lo = b_hi + B_BYTES;
-  unsigned long long* mma_done = (unsigned long long*)(b_lo + B_BYTES);  // [2], one arrival (the commit)
+  // drain staging: with a tensor map (vec) NOB 4 KB boxes per drain warp, 1024-byte aligned (128-byte swizzle);
+  // without one, one padded transpose buffer per warp in the same space
+  unsigned char* obuf = b_lo + B_BYTES;
+  float* tbuf = (float*)obuf;  // 4 warps x 32 rows x 36 floats
+  unsigned long long* mma_done = (unsigned long long*)(obuf + OB_BYTES);  // [2], one arrival (the commit)
   unsigned long long* acc_free = mma_done + 2;                             // [2], 128 arrivals (the drain)
   unsigned* tmem_slot = (unsigned*)(acc_free + 2);
-  float2* gs = (float2*)(acc_free + 4);          // the tile's gamma (2 KC values)
-  float* tbuf = (float*)(gs + 2 * KC);            // drain transpose: 4 warps x 32 rows x 36 floats
+  unsigned long long* tq_full = acc_free + 4;      // [4], one arrival: tile-queue entry n is in tq[n % 4]
+  volatile int* tq = (volatile int*)(tq_full + 4);  // [4] tile of entry n (-1: no more tiles)
+  volatile int* bc = tq + 4;                       // [2] the staging warps' next tile (written by thread 0)
+  float2* gs = (float2*)(bc + 4);                  // the tile's gamma (2 KC values)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   if (tid == 0) {
@@ -103,6 +117,7 @@ __global__ void __launch_bounds__(RT_NT, 1) recon_tc_kernel(int frames, int nx, 
     mbar_init(&mma_done[1], 1);
     mbar_init(&acc_free[0], 128);
     mbar_init(&acc_free[1], 128);
+    for (int i = 0; i < 4; ++i) mbar_init(&tq_full[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 0) {
@@ -117,10 +132,10 @@ __global__ void __launch_bounds__(RT_NT, 1) recon_tc_kernel(int frames, int nx, 
 
   const int tiles_i = (nx + RT_M - 1) / RT_M, tiles_j = (ny + RT_NC - 1) / RT_NC;
   const int per_frame = tiles_i * tiles_j;
-  const long long ntiles = (long long)frames * per_frame;
-  auto tile_origin = [&](long long t, int& f, int& i0, int& j0) {
-    f = (int)(t / per_frame);
-    const int rem = (int)(t - (long long)f * per_frame);
+  const int ntiles = frames * per_frame;  // < 2^31 (checked at the launch)
+  auto tile_origin = [&](int t, int& f, int& i0, int& j0) {
+    f = t / per_frame;
+    const int rem = t - f * per_frame;
     i0 = (rem / tiles_j) * RT_M;
     j0 = (rem % tiles_j) * RT_NC;
   };
@@ -130,66 +145,99 @@ __global__ void __launch_bounds__(RT_NT, 1) recon_tc_kernel(int frames, int nx, 
   };
 
   if (warp < 4) {
-    // ---------------- staging + MMA issue. The next tile's raw operands are loaded into registers right
+    // ---------------- staging + MMA issue. Thread = one operand row (A row tid, B row tid of the tile), its
+    // HC chunks of 4 complex in turn: a quarter warp's 16-byte stores of one chunk fill one 128-byte core-
+    // matrix row group (no bank conflicts). The next tile's raw operands are loaded into registers right
     // after a tile's MMAs are issued (they land while the tensor cores run); the split waits only for the
     // MMAs that still read shared memory.
     float2 ra[HC][4], rb[HC][4], rg = make_float2(0.f, 0.f);
-    auto fetch = [&](long long t) {
+    const bool ldvec = (R % 4 == 0) && (((size_t)A | (size_t)B) & 15) == 0;
+    auto fetch = [&](int t) {
       int f, i0, j0;
       tile_origin(t, f, i0, j0);
-      const float2* Af = A + (size_t)f * nx * R;
-      const float2* Bf = B + (size_t)f * ny * R;
+      const int i = i0 + tid, j = j0 + tid;
+      const float2* Ar = A + ((size_t)f * nx + (i < nx ? i : 0)) * R;
+      const float2* Br = B + ((size_t)f * ny + (j < ny ? j : 0)) * R;
 #pragma unroll
       for (int u = 0; u < HC; ++u) {
-        const int it = tid + 128 * u;  // RT_M * HC items, HC per thread
-        const int row = it / HC, c = it - row * HC, i = i0 + row, j = j0 + row;
+        if (ldvec) {
+          float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f), p1 = p0, q0 = p0, q1 = p0;
+          if (4 * u < R) {
+            if (i < nx) {
+              p0 = __ldg((const float4*)(Ar + 4 * u));
+              p1 = __ldg((const float4*)(Ar + 4 * u) + 1);
+            }
+            if (j < ny) {
+              q0 = __ldg((const float4*)(Br + 4 * u));
+              q1 = __ldg((const float4*)(Br + 4 * u) + 1);
+            }
+          }
+          ra[u][0] = make_float2(p0.x, p0.y), ra[u][1] = make_float2(p0.z, p0.w);
+          ra[u][2] = make_float2(p1.x, p1.y), ra[u][3] = make_float2(p1.z, p1.w);
+          rb[u][0] = make_float2(q0.x, q0.y), rb[u][1] = make_float2(q0.z, q0.w);
+          rb[u][2] = make_float2(q1.x, q1.y), rb[u][3] = make_float2(q1.z, q1.w);
+        } else {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int r = 4 * c + e;
-          ra[u][e] = (i < nx && r < R) ? __ldg(Af + (size_t)i * R + r) : make_float2(0.f, 0.f);
-          rb[u][e] = (j < ny && r < R) ? __ldg(Bf + (size_t)j * R + r) : make_float2(0.f, 0.f);
+          for (int e = 0; e < 4; ++e) {
+            const int r = 4 * u + e;
+            ra[u][e] = (i < nx && r < R) ? __ldg(Ar + r) : make_float2(0.f, 0.f);
+            rb[u][e] = (j < ny && r < R) ? __ldg(Br + r) : make_float2(0.f, 0.f);
+          }
         }
       }
       if (tid < R) rg = __ldg(gamma + (size_t)f * R + tid);
     };
+    // B2 rows 2 jj = [Br | -Bi] and 2 jj + 1 = [Bi | Br]: a value goes to an even row (16-byte slots 0, 2, 4, 6
+    // of a row group) and to an odd one (slots 1, 3, 5, 7). In each store instruction the lanes with jj % 8 < 4
+    // write the even row and the others the odd one, so a quarter warp covers all eight slots.
+    const int jj = tid;
+    const bool ev = (jj & 4) == 0;
     int n = 0;
-    if ((long long)blockIdx.x < ntiles) fetch(blockIdx.x);
-    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++n) {
+    // thread 0 draws the tiles two ahead (tile n + 1 is fetched during tile n's MMAs): grid <= ntiles
+    int tnext = 0;
+    if (tid == 0) tnext = (int)gridDim.x + (int)atomicAdd(tile_ctr, 1u);
+    fetch(blockIdx.x);
+    for (int t = blockIdx.x; t < ntiles; ++n) {
       if (n >= 1) mbar_wait(&mma_done[(n - 1) & 1], ((n - 1) >> 1) & 1);  // the previous tile's MMAs read smem
       if (tid < 2 * KC) gs[tid] = rg;  // RP = 2 KC gamma values (zeros past R)
+      if (tid == 0) {
+        bc[n & 1] = tnext;
+        tq[n & 3] = t;  // the drain warps are at most two tiles behind: slot (n - 4) % 4 is free
+        mbar_arrive(&tq_full[n & 3]);
+      }
       asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      const int tn = bc[n & 1];
 #pragma unroll
-      for (int u = 0; u < HC; ++u) {
-        const int it = tid + 128 * u;
-        const int row = it / HC, c = it - row * HC;
+      for (int c = 0; c < HC; ++c) {
         float4 hi, lo;
-        {  // A' = A diag(gamma): row `row`, re chunk c and im chunk HC + c
+        {  // A' = A diag(gamma): row tid, re chunk c and im chunk HC + c
           float2 v[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) v[e] = cmul(ra[u][e], gs[4 * c + e]);
+          for (int e = 0; e < 4; ++e) v[e] = cmul(ra[c][e], gs[4 * c + e]);
           split4(make_float4(v[0].x, v[1].x, v[2].x, v[3].x), hi, lo);
-          *(float4*)(a_hi + cm(row, c)) = hi;
-          *(float4*)(a_lo + cm(row, c)) = lo;
+          *(float4*)(a_hi + cm(tid, c)) = hi;
+          *(float4*)(a_lo + cm(tid, c)) = lo;
           split4(make_float4(v[0].y, v[1].y, v[2].y, v[3].y), hi, lo);
-          *(float4*)(a_hi + cm(row, HC + c)) = hi;
-          *(float4*)(a_lo + cm(row, HC + c)) = lo;
+          *(float4*)(a_hi + cm(tid, HC + c)) = hi;
+          *(float4*)(a_lo + cm(tid, HC + c)) = lo;
         }
-        {  // B rows 2 jj = [Br | -Bi], 2 jj + 1 = [Bi | Br]
-          const int jj = row;
-          const float4 vr = make_float4(rb[u][0].x, rb[u][1].x, rb[u][2].x, rb[u][3].x);
-          const float4 vi = make_float4(rb[u][0].y, rb[u][1].y, rb[u][2].y, rb[u][3].y);
+        {
+          const float4 vr = make_float4(rb[c][0].x, rb[c][1].x, rb[c][2].x, rb[c][3].x);
+          const float4 vi = make_float4(rb[c][0].y, rb[c][1].y, rb[c][2].y, rb[c][3].y);
+          const unsigned e_re = cm(2 * jj, c), o_re = cm(2 * jj + 1, HC + c);  // Br: even row re half, odd row im half
+          const unsigned o_im = cm(2 * jj + 1, c), e_im = cm(2 * jj, HC + c);  // Bi: odd row re half, -Bi: even row im half
           split4(vr, hi, lo);
-          *(float4*)(b_hi + cm(2 * jj, c)) = hi;
-          *(float4*)(b_lo + cm(2 * jj, c)) = lo;
-          *(float4*)(b_hi + cm(2 * jj + 1, HC + c)) = hi;
-          *(float4*)(b_lo + cm(2 * jj + 1, HC + c)) = lo;
+          *(float4*)(b_hi + (ev ? e_re : o_re)) = hi;
+          *(float4*)(b_lo + (ev ? e_re : o_re)) = lo;
+          *(float4*)(b_hi + (ev ? o_re : e_re)) = hi;
+          *(float4*)(b_lo + (ev ? o_re : e_re)) = lo;
           split4(vi, hi, lo);
-          *(float4*)(b_hi + cm(2 * jj + 1, c)) = hi;
-          *(float4*)(b_lo + cm(2 * jj + 1, c)) = lo;
-          hi = make_float4(-hi.x, -hi.y, -hi.z, -hi.w);  // the split of -x is -(split of x)
-          lo = make_float4(-lo.x, -lo.y, -lo.z, -lo.w);
-          *(float4*)(b_hi + cm(2 * jj, HC + c)) = hi;
-          *(float4*)(b_lo + cm(2 * jj, HC + c)) = lo;
+          // the split of -x is -(split of x)
+          const float4 nhi = make_float4(-hi.x, -hi.y, -hi.z, -hi.w), nlo = make_float4(-lo.x, -lo.y, -lo.z, -lo.w);
+          *(float4*)(b_hi + (ev ? e_im : o_im)) = ev ? nhi : hi;
+          *(float4*)(b_lo + (ev ? e_im : o_im)) = ev ? nlo : lo;
+          *(float4*)(b_hi + (ev ? o_im : e_im)) = ev ? hi : nhi;
+          *(float4*)(b_lo + (ev ? o_im : e_im)) = ev ? lo : nlo;
         }
       }
       fence_proxy_async_smem();  // the operand stores, before the tensor cores read them
@@ -208,18 +256,31 @@ __global__ void __launch_bounds__(RT_NT, 1) recon_tc_kernel(int frames, int nx, 
           umma_tf32(d, umma_desc(sa_hi + ko, 128, SBO), umma_desc(sb_hi + ko, 128, SBO), 1);
         }
         umma_commit(&mma_done[b]);
+        tnext = tn < ntiles ? (int)gridDim.x + (int)atomicAdd(tile_ctr, 1u) : ntiles;
       }
       __syncwarp();
-      if (t + gridDim.x < ntiles) fetch(t + gridDim.x);
+      if (tn < ntiles) fetch(tn);
+      t = tn;
+    }
+    if (tid == 0) {
+      tq[n & 3] = -1;
+      mbar_arrive(&tq_full[n & 3]);
     }
   } else {
-    // ---------------- TMEM drain: a warp owns the 32 accumulator lanes (rows) of its quarter (warp % 4);
-    // each 32-column chunk goes through a padded shared-memory transpose so every store instruction writes
-    // four full 128-byte row segments
+    // ---------------- TMEM drain: a warp owns the 32 accumulator lanes (rows) of its quarter (warp % 4).
+    // A 32-column chunk (one output row segment of 128 bytes per lane) is written to a 4 KB shared-memory box
+    // in the 128-byte swizzle (16-byte slot e of row r at slot e ^ (r % 8): conflict-free) and leaves as ONE
+    // bulk tensor store (TMA; rows and columns past the frame are clipped by the tensor map), NOB boxes in
+    // flight per warp; the next two chunks leave TMEM while the current ones are stored. Without a tensor map
+    // (odd ny or an unaligned output) the chunks go through a padded transpose and plain stores.
     const int q = warp & 3;
     float* tb = tbuf + q * (32 * 36);
-    int n = 0;
-    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++n) {
+    unsigned char* ob = obuf + q * (NOB * 4096);
+    unsigned box = 0;  // boxes issued by this warp
+    for (int n = 0;; ++n) {
+      mbar_wait(&tq_full[n & 3], (n >> 2) & 1);
+      const int t = tq[n & 3];
+      if (t < 0) break;
       int f, i0, j0;
       tile_origin(t, f, i0, j0);
       const int b = n & 1;
@@ -227,40 +288,71 @@ __global__ void __launch_bounds__(RT_NT, 1) recon_tc_kernel(int frames, int nx, 
       tc_fence_after();
       const unsigned taddr = tmem + ((unsigned)(32 * q) << 16) + (unsigned)b * (2 * RT_NC);
       float2* Xf = X + (size_t)f * nx * ny;
-#pragma unroll 1
+      unsigned v[2][2][32];  // [ping-pong][chunk of the pair][column]
+      RT_LD32(taddr, v[0][0]);
+      RT_LD32(taddr + 32, v[0][1]);
+#pragma unroll
       for (int c = 0; c < 2 * RT_NC / 32; c += 2) {
-        unsigned v[2][32];
-        RT_LD32(taddr + 32 * c, v[0]);
-        RT_LD32(taddr + 32 * (c + 1), v[1]);
+        const int pp = (c >> 1) & 1;
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            *(float4*)(tb + lane * 36 + 4 * e) = make_float4(__uint_as_float(v[h][4 * e]), __uint_as_float(v[h][4 * e + 1]),
-                                                              __uint_as_float(v[h][4 * e + 2]), __uint_as_float(v[h][4 * e + 3]));
+        if (c + 2 < 2 * RT_NC / 32) {
+          RT_LD32(taddr + 32 * (c + 2), v[pp ^ 1][0]);
+          RT_LD32(taddr + 32 * (c + 3), v[pp ^ 1][1]);
+        }
+        if (vec) {
+          // the pair's two boxes: the bulk stores that last read them are done reading (lane 0 owns the
+          // warp's bulk groups, one group per pair)
+          unsigned char* o = ob + (box % NOB) * 4096;  // NOB is even: the pair is contiguous
+          box += 2;
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(NOB / 2 - 1) : "memory");
           __syncwarp();
-          const int jc = j0 + 16 * (c + h) + 2 * (lane & 7);  // this lane's two complex columns
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int rr = 4 * k + (lane >> 3), i = i0 + 32 * q + rr;
-            const float4 w = *(const float4*)(tb + rr * 36 + 4 * (lane & 7));
-            if (i < nx) {
-              float2* xr = Xf + (size_t)i * ny;
-              if (vec && jc + 1 < ny) {
-                *(float4*)(xr + jc) = w;
-              } else {
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              *(float4*)(o + h * 4096 + lane * 128 + ((e ^ (lane & 7)) << 4)) =
+                  make_float4(__uint_as_float(v[pp][h][4 * e]), __uint_as_float(v[pp][h][4 * e + 1]),
+                              __uint_as_float(v[pp][h][4 * e + 2]), __uint_as_float(v[pp][h][4 * e + 3]));
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              if (j0 + 16 * (c + h) < ny)
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(&xmap),
+                    "r"(2 * (j0 + 16 * (c + h))), "r"(i0 + 32 * q), "r"(f), "r"(smem_u32(o + h * 4096))
+                    : "memory");
+            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+          }
+        } else {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              *(float4*)(tb + lane * 36 + 4 * e) =
+                  make_float4(__uint_as_float(v[pp][h][4 * e]), __uint_as_float(v[pp][h][4 * e + 1]),
+                              __uint_as_float(v[pp][h][4 * e + 2]), __uint_as_float(v[pp][h][4 * e + 3]));
+            __syncwarp();
+            const int jc = j0 + 16 * (c + h) + 2 * (lane & 7);  // this lane's two complex columns
+#pragma unroll 1
+            for (int k = 0; k < 8; ++k) {
+              const int rr = 4 * k + (lane >> 3), i = i0 + 32 * q + rr;
+              const float4 w = *(const float4*)(tb + rr * 36 + 4 * (lane & 7));
+              if (i < nx) {
+                float2* xr = Xf + (size_t)i * ny;
                 if (jc < ny) xr[jc] = make_float2(w.x, w.y);
                 if (jc + 1 < ny) xr[jc + 1] = make_float2(w.z, w.w);
               }
             }
+            __syncwarp();
           }
-          __syncwarp();
         }
       }
       tc_fence_before();
       mbar_arrive(&acc_free[b]);
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");  // the warp's stores are complete
   }
   tc_fence_before();
   __syncthreads();
@@ -270,21 +362,77 @@ __global__ void __launch_bounds__(RT_NT, 1) recon_tc_kernel(int frames, int nx, 
   }
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (the library links cudart only)
+typedef CUresult (*tensormap_encode_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                        const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                        CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static tensormap_encode_fn tensormap_encoder() {
+  static tensormap_encode_fn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (tensormap_encode_fn)p;
+  }
+  return fn;
+}
+
+// The tile counter of one launch: a slot of a per-device ring, zeroed on the launch's stream ahead of the
+// kernel (a memset node under graph capture). RT_CTRS launches can be in flight per device.
+#define RT_CTRS 1024
+static cudaError_t recon_tile_counter(int d, cudaStream_t st, unsigned** out) {
+  static unsigned* ring[TT_MAXDEV] = {nullptr};
+  static unsigned next[TT_MAXDEV] = {0};
+  if (!ring[d]) {
+    cudaError_t e = cudaMalloc((void**)&ring[d], RT_CTRS * sizeof(unsigned));
+    if (e != cudaSuccess) return e;
+  }
+  unsigned* c = ring[d] + (__sync_fetch_and_add(&next[d], 1u) % RT_CTRS);
+  *out = c;
+  return cudaMemsetAsync(c, 0, sizeof(unsigned), st);
+}
+
 template <int KC>
 static int recon_tc_launch(cudaStream_t st, int frames, int nx, int ny, int R, const float2* a, const float2* b,
                            const float2* g, float2* x, int vec) {
-  const size_t smb = (size_t)(RT_M + 2 * RT_NC) * 4 * KC * 4 * 2 + 64 + 8 * 2 * KC + 4 * 32 * 36 * 4;
+  const size_t ob = (KC <= 12 ? 4 : 2) * 4 * 4096;
+  const size_t smb = (size_t)(RT_M + 2 * RT_NC) * 4 * KC * 4 * 2 + (ob > 4 * 32 * 36 * 4 ? ob : 4 * 32 * 36 * 4) + 128 +
+                     8 * 2 * KC;
   static size_t cfg[TT_MAXDEV] = {0};
   static int sms[TT_MAXDEV] = {0};
   int dev = 0;
   TT_CUDA_TRY(cudaGetDevice(&dev));
-  const int d = dev < TT_MAXDEV ? dev : 0;
+  if (dev >= TT_MAXDEV) return tt_fail(TT_EUNSUPPORTED, "tt_reconstruct: device index %d", dev);
+  const int d = dev;
   TT_CUDA_TRY(tt_smem_attr((const void*)recon_tc_kernel<KC>, smb, cfg));
   if (sms[d] == 0) TT_CUDA_TRY(cudaDeviceGetAttribute(&sms[d], cudaDevAttrMultiProcessorCount, dev));
   const long long tiles = (long long)frames * ((nx + RT_M - 1) / RT_M) * ((ny + RT_NC - 1) / RT_NC);
   if (tiles == 0) return TT_OK;
-  const int grid = (int)(tiles < sms[d] ? tiles : sms[d]);
-  recon_tc_kernel<KC><<<grid, RT_NT, smb, st>>>(frames, nx, ny, R, a, b, g, x, vec);
+  if (tiles > 0x7fffffffLL - 4096) return tt_fail(TT_EUNSUPPORTED, "tt_reconstruct: more than 2^31 output tiles");
+  int grid = (int)(tiles < sms[d] ? tiles : sms[d]);
+  if (const char* e = getenv("TT_RECON_MAXCTAS")) {  // experiment hook: fewer persistent CTAs
+    const int m = atoi(e);
+    if (m > 0 && m < grid) grid = m;
+  }
+  unsigned* ctr = nullptr;
+  TT_CUDA_TRY(recon_tile_counter(d, st, &ctr));
+  // the output as a 3-D fp32 tensor (2 ny, nx, frames) for the drain's bulk tensor stores: 32 x 32 boxes,
+  // 128-byte swizzle. Needs 16-byte row strides (even ny) and base; otherwise the plain-store drain runs.
+  CUtensorMap xmap;
+  memset(&xmap, 0, sizeof(xmap));
+  if (vec) {
+    tensormap_encode_fn enc = tensormap_encoder();
+    if (!enc) return tt_fail(TT_EUNSUPPORTED, "tt_reconstruct: cuTensorMapEncodeTiled is not available from this driver");
+    const cuuint64_t gdim[3] = {(cuuint64_t)2 * ny, (cuuint64_t)nx, (cuuint64_t)frames};
+    const cuuint64_t gstr[2] = {(cuuint64_t)ny * 8, (cuuint64_t)nx * ny * 8};
+    const cuuint32_t box[3] = {32, 32, 1}, estr[3] = {1, 1, 1};
+    const CUresult r = enc(&xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)x, gdim, gstr, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return tt_fail(TT_ECUDA, "tt_reconstruct: cuTensorMapEncodeTiled failed (%d)", (int)r);
+  }
+  recon_tc_kernel<KC><<<grid, RT_NT, smb, st>>>(frames, nx, ny, R, a, b, g, x, vec, ctr, xmap);
   TT_CUDA_TRY(cudaGetLastError());
   return TT_OK;
 }
