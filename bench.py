@@ -1093,7 +1093,7 @@ def run_ours(args, cfg):
         from paper_1609_04104_b200.engine import ZERO_COPY_BYTES
 
         zc = ks_np.nbytes >= ZERO_COPY_BYTES
-        h2d = (sum(len(r) for fr in res.rows for r in fr) * n * 8) if zc else ks_np.nbytes
+        h2d = (res.rows.total() * n * 8) if zc else ks_np.nbytes
         d2h = res.recon.nbytes + res.gamma.nbytes + res.cost.nbytes + res.mu.nbytes + 4 * (T * ns * (eng.max_rows + 1))
         et = torch.tensor([sum(t_e2e)], dtype=torch.float64, device=dev)
         if world > 1:

@@ -23,6 +23,7 @@ Semantics kept from the reference loop:
 
 from __future__ import annotations
 
+from collections.abc import Sequence
 from dataclasses import dataclass
 import ctypes as C
 
@@ -303,13 +304,44 @@ class OnlineEngine:
         return X.reshape(F, ns, self.nx, self.ny)
 
 
+class FrameRows(Sequence):
+    """The sampled rows of a run as a read-only sequence: ``rows[f][s]`` is the int64 row array of
+    frame f and slice s (the kernel's order: sorted and unique for draws with replacement, draw order
+    without). Backed by the run's (frames, nslices, Smax) row tables and counts; the per-frame lists
+    are built on access (a C3 run has 6400 of them), not inside the timed call."""
+
+    def __init__(self, segments):
+        self._seg = [(np.asarray(r), np.asarray(c)) for r, c in segments]  # (rows table, counts) per run segment
+        self._off = np.cumsum([0] + [c.shape[0] for _, c in self._seg])
+
+    def __len__(self):
+        return int(self._off[-1])
+
+    def __getitem__(self, f):
+        if isinstance(f, slice):
+            return [self[i] for i in range(*f.indices(len(self)))]
+        f = int(f)
+        if f < 0:
+            f += len(self)
+        if not 0 <= f < len(self):
+            raise IndexError("frame index out of range")
+        k = int(np.searchsorted(self._off, f, side="right")) - 1
+        rows, cnt = self._seg[k]
+        g = f - int(self._off[k])
+        return [rows[g, s, :cnt[g, s]].astype(np.int64) for s in range(cnt.shape[1])]
+
+    def total(self) -> int:
+        """Number of sampled rows over all frames and slices."""
+        return int(sum(int(c.sum()) for _, c in self._seg))
+
+
 @dataclass
 class OnlineResult:
     recon: np.ndarray     # (T, nslices, nx, ny) complex64 image frames
     gamma: np.ndarray     # (T, nslices, R)
     cost: np.ndarray      # (T, nslices)
     mu: np.ndarray
-    rows: list            # per frame per slice row arrays
+    rows: Sequence        # rows[f][s]: row array of frame f, slice s (FrameRows, or a list of lists)
     nmse: np.ndarray | None
     final_A: np.ndarray
     final_B: np.ndarray
@@ -810,10 +842,7 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
     L.raise_status(int(st.max().item()), "online engine")
     _give_engine(ekey, eng)
     cat = lambda k: np.concatenate([sm[k].numpy() for sm in small], axis=0)  # noqa: E731
-    rows = []
-    for sm in small:
-        cnt, rows_np = sm["cnt"].numpy(), sm["rows"].numpy()
-        rows += [[rows_np[f, s, :cnt[f, s]].astype(np.int64) for s in range(ns)] for f in range(cnt.shape[0])]
+    rows = FrameRows([(sm["rows"].numpy(), sm["cnt"].numpy()) for sm in small])
     return OnlineResult(recon=recon.numpy(), gamma=cat("gamma"), cost=cat("cost"), mu=cat("mu"), rows=rows, nmse=nm,
                         final_A=A.numpy(), final_B=B.numpy(), factor_history=hist,
                         norm_exceeded=cat("norm").astype(bool) if norm_cap is not None else None)
@@ -1095,7 +1124,7 @@ def _run_online_entries(src, on_dev, A0, B0, lam, step, policy, clean, t0, warm_
     cnt = host["cnt"].numpy()
     rows_np = host["rows"].numpy()
     # entry lists as measured: sorted for informative draws (np.union1d), the given order for static ones
-    rows = [[rows_np[f, 0, :cnt[f, 0]].astype(np.int64)] for f in range(T)]
+    rows = FrameRows([(rows_np, cnt)])
     return OnlineResult(recon=host["recon"].numpy(), gamma=host["gamma"].numpy(), cost=host["cost"].numpy(),
                         mu=host["mu"].numpy(), rows=rows, nmse=nm, final_A=host["A"].numpy(),
                         final_B=host["B"].numpy(),
