@@ -277,6 +277,10 @@ __global__ void __launch_bounds__(RT_NT, 1) recon_tc_kernel(int frames, int nx, 
     float* tb = tbuf + q * (32 * 36);
     unsigned char* ob = obuf + q * (NOB * 4096);
     unsigned box = 0;  // boxes issued by this warp
+    // the frames are written once and read by nobody on the device soon: evict-first in L2, so the stream of
+    // output lines does not displace the tracking clusters' exchange buffers and factor history
+    unsigned long long l2_first;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(l2_first));
     for (int n = 0;; ++n) {
       mbar_wait(&tq_full[n & 3], (n >> 2) & 1);
       const int t = tq[n & 3];
@@ -320,8 +324,9 @@ __global__ void __launch_bounds__(RT_NT, 1) recon_tc_kernel(int frames, int nx, 
             for (int h = 0; h < 2; ++h)
               if (j0 + 16 * (c + h) < ny)
                 asm volatile(
-                    "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(&xmap),
-                    "r"(2 * (j0 + 16 * (c + h))), "r"(i0 + 32 * q), "r"(f), "r"(smem_u32(o + h * 4096))
+                    "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2, %3}], [%4], %5;\n" ::
+                        "l"(&xmap),
+                    "r"(2 * (j0 + 16 * (c + h))), "r"(i0 + 32 * q), "r"(f), "r"(smem_u32(o + h * 4096)), "l"(l2_first)
                     : "memory");
             asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
           }
