@@ -97,6 +97,48 @@ def test_reconstruct_tensor_core_form(shape, monkeypatch):
         assert rel(Xt[f], ex) < 2e-6
 
 
+@pytest.mark.parametrize("shape,offset", [((200, 136, 12, 3), 0), ((200, 136, 12, 3), 1), ((130, 258, 16, 2), 2),
+                                          ((128, 128, 4, 2), 3)])
+def test_reconstruct_writes_only_its_frames(shape, offset):
+    """The tensor-core reconstruction's bulk tensor stores are clipped to the frames (ragged tiles in
+    both dimensions); an output at an 8-byte-only aligned address and factors at one take the plain-store
+    and scalar-load paths. Guard elements around the output stay untouched; repeated launches (the
+    per-launch tile counters) agree bit for bit."""
+    import torch
+
+    from paper_1609_04104_b200 import _ops as K
+
+    nx, ny, R, F = shape
+    rng = np.random.default_rng(nx + ny + offset)
+    A = (rng.standard_normal((F, nx, R)) + 1j * rng.standard_normal((F, nx, R))).astype(np.complex64)
+    B = (rng.standard_normal((F, ny, R)) + 1j * rng.standard_normal((F, ny, R))).astype(np.complex64)
+    gm = (rng.standard_normal((F, R)) + 1j * rng.standard_normal((F, R))).astype(np.complex64)
+
+    def shifted(x):  # a contiguous copy whose address is offset complex64 elements past an aligned base
+        buf = torch.empty(x.size + offset, dtype=torch.complex64, device="cuda")
+        v = buf[offset:].view(x.shape)
+        v.copy_(torch.from_numpy(x))
+        return v
+
+    a, b, g = shifted(A), shifted(B), shifted(gm)
+    guard = 4096
+    sentinel = complex(-7.5, 3.25)
+    buf = torch.full((guard + offset + F * nx * ny + guard,), sentinel, dtype=torch.complex64, device="cuda")
+    out = buf[guard + offset:guard + offset + F * nx * ny].view(F, nx, ny)
+    K.reconstruct(a, b, g, out)
+    first = out.clone()
+    for _ in range(3):
+        K.reconstruct(a, b, g, out)
+    torch.cuda.synchronize()
+    assert torch.equal(first, out)
+    host = buf.cpu().numpy()
+    assert np.all(host[:guard + offset] == np.complex64(sentinel))
+    assert np.all(host[guard + offset + F * nx * ny:] == np.complex64(sentinel))
+    X = out.cpu().numpy()
+    for f in range(F):
+        assert rel(X[f], O.synth(A[f], B[f], gm[f])) < 1e-5
+
+
 @pytest.mark.parametrize("n,ncols", [(256, 1), (256, 20), (256, 33), (1024, 64), (2048, 5), (8, 70)])
 def test_fft_cols_column_blocking(n, ncols):
     """Column counts that split over several CTAs (up to 32 whole columns per CTA, fewer at large n)
