@@ -42,6 +42,7 @@ sys.path.insert(0, ROOT)
 import bench  # noqa: E402  (helpers: ClockSampler, measured_peaks, init_factors)
 
 CPU_FRAMES = {128: 16, 256: 8, 512: 3, 1024: 2}
+CLUSTER = 0  # --cluster: CTAs per slice (0: the library's choice)
 
 
 def byte_model(n, R, S, informative):
@@ -71,7 +72,7 @@ def run_point(n, R, frac, kind, ks_dev, clean_dev, T, steps, warmup, flush, hbm_
     else:
         pol = tt.Informative(k=S_max, forced=(0,), beta=0.1, key0=2024, key1=n * 1000 + R)
     lam = 0.05
-    eng = tt.OnlineEngine(n, n, R, 1, lam, tt.Fixed(0.01), pol)
+    eng = tt.OnlineEngine(n, n, R, 1, lam, tt.Fixed(0.01), pol, cluster=CLUSTER)
     eng.set_image_factors(A0, B0)
     ah0, bh0 = eng.ah.clone(), eng.bh.clone()
     ahf, bhf = torch.empty_like(ah0), torch.empty_like(bh0)
@@ -146,8 +147,11 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cluster", type=int, default=0, help="CTAs per slice (0: the library's choice)")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweep_c5.jsonl"))
     args = ap.parse_args()
+    global CLUSTER
+    CLUSTER = args.cluster
 
     import torch
 

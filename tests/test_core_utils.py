@@ -48,3 +48,21 @@ def test_config_error_and_metric_exports():
     assert issubclass(tt.ConfigError, ValueError)
     for name in ("ConfigError", "nmse", "nmse_frames"):
         assert name in tt.__all__ and hasattr(tt, name)
+
+
+def test_frame_rows_sequence():
+    """OnlineResult.rows: a lazy per-frame / per-slice view over the run's row tables (several run
+    segments concatenated), list-of-lists semantics."""
+    from paper_1609_04104_b200.engine import FrameRows
+
+    r = np.arange(2 * 3 * 5).reshape(2, 3, 5).astype(np.int32)
+    c = np.array([[1, 2, 3], [5, 0, 4]], np.int32)
+    fr = FrameRows([(r, c), (r + 100, c)])
+    assert len(fr) == 4 and fr.total() == 30
+    assert fr[1][0].dtype == np.int64 and fr[1][0].tolist() == [15, 16, 17, 18, 19]
+    assert fr[3][2].tolist() == [125, 126, 127, 128] and fr[-1][1].size == 0
+    assert [len(x) for x in fr] == [3, 3, 3, 3]
+    assert sum(len(s) for f in fr for s in f) == 30
+    assert [a.tolist() for a in fr[1:3][1]] == [a.tolist() for a in fr[2]]
+    with pytest.raises(IndexError):
+        fr[4]
