@@ -944,13 +944,15 @@ __global__ void __launch_bounds__(ROWS_NT, 1) tt_rows_kernel(const __grid_consta
     auto issue_y = [&](int k0, int kt) {
       if (kt <= 0 || nJ <= 0) return;
       if (y_bulk) {
-        if (warp == 0) {
-          if (lane == 0) mbar_arrive_expect_tx(&ybar, (unsigned)(kt * nJ * sizeof(float2)));
-          __syncwarp();
-          for (int kk = lane; kk < kt; kk += 32)
-            bulk_g2s(&ys[(size_t)kk * pl.ysr], ybase + (size_t)(gather ? rows[k0 + kk] : k0 + kk) * ny,
-                     (unsigned)(nJ * sizeof(float2)), &ybar);
-        }
+        // the rows dealt round robin to the warps: a warp issues its bulk copies one lane after the other
+        // (~90 cycles each), so one issuing warp held the block at the next barrier for ~2k cycles per frame.
+        // The one arrival carries the tile's byte count; copies of other warps may complete before it (the
+        // transaction count goes negative until then, the phase still needs the arrival).
+        if (tid == 0) mbar_arrive_expect_tx(&ybar, (unsigned)(kt * nJ * sizeof(float2)));
+        const int nwarps = NT >> 5;
+        for (int kk = warp + nwarps * lane; kk < kt; kk += NT)
+          bulk_g2s(&ys[(size_t)kk * pl.ysr], ybase + (size_t)(gather ? rows[k0 + kk] : k0 + kk) * ny,
+                   (unsigned)(nJ * sizeof(float2)), &ybar);
       } else {
         for (int o = tid; o < kt * nJ; o += NT) {
           const int kk = idiv(o, nJ), jj = o - kk * nJ;
