@@ -939,6 +939,10 @@ def run_ours(args, cfg):
     else:
         slice_ids = slice_partition(cfg["slices"], world, rank)
         scaling = "strong"
+        if args.shard_of > 1:
+            if world != 1:
+                raise SystemExit("bench.py: --shard-of is a one-GPU measurement")
+            slice_ids = slice_partition(cfg["slices"], args.shard_of, 0)
     ns = len(slice_ids)
     n, R, T = cfg["n"], cfg["R"], cfg["T"]
     ks_np, clean_np = make_data(cfg, slice_ids)
@@ -1044,6 +1048,8 @@ def run_ours(args, cfg):
     total_ms, track_total = float(tot[0]), float(tot[1])
     eng.check_status()
     frames_all = T * cfg["slices"] * (world if cfg["slices"] == 1 else 1) * args.steps
+    if args.shard_of > 1:
+        frames_all = T * ns * args.steps  # this GPU's shard only
     value = frames_all / (total_ms / 1e3)
 
     # ---- quality (outside timing): NRMSE of the last step's reconstructions
@@ -1098,7 +1104,9 @@ def run_ours(args, cfg):
         et = torch.tensor([sum(t_e2e)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e2e = {"value": T * ns * (world if cfg["slices"] == 1 else 1) * len(t_e2e) / float(et[0]), "unit": "frames/s",
+        # whole-job frames: replicas (one slice per rank) or all the job's slices sharded over the ranks
+        job_slices = world if cfg["slices"] == 1 else (ns if args.shard_of > 1 else cfg["slices"])
+        e2e = {"value": T * job_slices * len(t_e2e) / float(et[0]), "unit": "frames/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "call": "paper_1609_04104_b200.run_online(pinned host kspace, recon_domain='kspace') -> host "
                        "k-space frames (run_adaptive's recon for k-space data) + reports",
@@ -1141,6 +1149,8 @@ def run_ours(args, cfg):
         "config": dict(workload_config(args, cfg), slices_per_gpu=ns, cluster_ctas_per_slice=eng.cluster,
                        step=("HessianBound(1e-3, 1e9)" if args.step == "hessian" else f"Fixed({cfg['mu']})"),
                        tracking_launches_per_step=nblk,
+                       **({"shard_of": f"rank 0's shard of a {args.shard_of}-GPU run, alone on one GPU"}
+                          if args.shard_of > 1 else {}),
                        parallelism=f"{'replicas' if cfg['slices'] == 1 else 'slice-shard'} x{world}"),
         "gpu_launches": launches_per_step * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
@@ -1265,6 +1275,9 @@ def main():
                     help="experiment: persistent reconstruction CTAs of every block but the last (0: one per SM)")
     ap.add_argument("--tail-frac", type=float, default=1.0,
                     help="size of the last tracking block relative to an even split (its reconstruction is the tail)")
+    ap.add_argument("--shard-of", type=int, default=0,
+                    help="config c3 on one GPU: run only rank 0's slice shard of an N-GPU run (the per-rank "
+                         "workload of --gpus N measured alone; value counts this GPU's frames only)")
     ap.add_argument("--local-ranks", type=int, default=0,
                     help="config c4 on one GPU: row-shard over this many thread-block clusters (fused launch)")
     args = ap.parse_args()
