@@ -162,6 +162,11 @@ int tt_rows_shard_scores(void* stream, int nx, int ny, int rank, const double* e
 /* plan of a row-mask launch at `cluster` (0: smallest that fits): out[6] = cluster, rows per k tile,
  * shared-memory bytes, tight plan (0/1), padded Y row stride, K-split buffer entries (diagnostics) */
 int tt_rows_plan_info(int nx, int ny, int rank, int max_rows, int cluster, int* out);
+/* how many clusters of `cluster` CTAs of the row-mask kernel (this shape's shared-memory plan) the current
+ * device holds at once (cudaOccupancyMaxActiveClusters): a launch with more slices than this runs in waves, so
+ * the host picks the widest cluster whose count covers the slices (the reference has no counterpart: its
+ * slices are a Python loop, experiment.py:332-441) */
+int tt_rows_max_clusters(int nx, int ny, int rank, int max_rows, int cluster, int* nclusters);
 /* doubles in the fp64 payload xg of a sharded launch */
 size_t tt_rows_shard_xg_len(int rank);
 /* 1 when tt_track_rows runs the mirrored kernel for this shape at `cluster` (every CTA holds the whole Ah;

@@ -86,6 +86,7 @@ SIGNATURES = {
     "tt_rows_shard_xg_len": (C.c_size_t, [C.c_int]),
     "tt_rows_mirror_fits": (C.c_int, [C.c_int] * 5),
     "tt_rows_plan_info": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _p]),
+    "tt_rows_max_clusters": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _p]),
     "tt_rows_shard_reduce": (C.c_int, [_p, C.c_int, C.c_int, C.c_int, _p, _p]),
     "tt_entries_scratch_bytes": (C.c_size_t, [C.c_int] * 4),
     "tt_track_entries": (C.c_int, [_p, C.POINTER(EntriesArgs)]),

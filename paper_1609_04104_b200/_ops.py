@@ -51,16 +51,25 @@ class RowsScratch:
     def __init__(self, nslices, nx, ny, rank, max_rows, cluster=0, policy=0, dev=None):
         sm = C.c_size_t(0)
         if int(cluster) <= 0:
-            # widest cluster that keeps every slice's cluster co-resident on the
-            # 148 SMs: 16 CTAs for one slice (latency), 2 for 64 slices
+            # widest cluster that keeps every slice's cluster resident at once: 16 CTAs for one
+            # slice (latency), 2 for 64 slices. The device holds fewer than 148 / c clusters of 8
+            # or 16 CTAs (8 GPCs of 16-20 SMs: tt_rows_max_clusters asks the occupancy
+            # calculator), and a launch with more slices than that runs in two waves.
             cl = None
             for c in (16, 8, 4, 2, 1):
                 if c > 1 and nslices * c > 148:
                     continue
                 t = C.c_int(c)
-                if L.lib().tt_rows_plan(nx, ny, rank, max_rows, policy, C.byref(t), C.byref(sm)) == 0:
-                    cl = t
-                    break
+                if L.lib().tt_rows_plan(nx, ny, rank, max_rows, policy, C.byref(t), C.byref(sm)) != 0:
+                    continue
+                if c > 1:
+                    nmax = C.c_int(0)
+                    L.check(L.lib().tt_rows_max_clusters(nx, ny, rank, max_rows, c, C.byref(nmax)),
+                            "rows cluster occupancy")
+                    if nslices > nmax.value:
+                        continue
+                cl = t
+                break
             if cl is None:
                 cl = C.c_int(0)
                 L.check(L.lib().tt_rows_plan(nx, ny, rank, max_rows, policy, C.byref(cl), C.byref(sm)),

@@ -1536,6 +1536,55 @@ static int rows_choose_cluster(int nx, int ny, int R, int Smax, int want, RowsPl
   return tt_fail(TT_EUNSUPPORTED, "row-mask step (nx=%d ny=%d R=%d rows=%d) does not fit", nx, ny, R, Smax);
 }
 
+// the instantiation: solver by Gauss-Jordan entries per thread, sharding phases only when sharded
+typedef void (*RowsFn)(const tt_rows_args, const RowsPlan);
+static const RowsFn rows_fns[10] = {tt_rows_kernel<1, false>, tt_rows_kernel<2, false>, tt_rows_kernel<5, false>,
+                                    tt_rows_kernel<9, false>, tt_rows_kernel<1, true>,  tt_rows_kernel<2, true>,
+                                    tt_rows_kernel<5, true>,  tt_rows_kernel<9, true>,
+                                    tt_rows_kernel<5, false, true>, tt_rows_kernel<9, false, true>};
+static int rows_which(int rank, bool sharded, bool tight) {
+  const int ept = gj_ept(rank, ROWS_NT);
+  const int solv = ept <= 1 ? 0 : ept <= 2 ? 1 : ept <= 5 ? 2 : 3;
+  if (!tight) return solv + (sharded ? 4 : 0);
+  // the tight plan is needed only at large N x R (R = 64 at 1024^2); compiled for the two wide solvers
+  if (sharded || solv < 2) return -1;
+  return 8 + (solv - 2);
+}
+
+// How many clusters of `cluster` CTAs of the row-mask kernel the device holds at once
+// (cudaOccupancyMaxActiveClusters): on the B200's 8 GPCs of 16-20 SMs fewer than 148 / cluster for
+// clusters of 8 and 16, so a launch with more slices than this runs in waves.
+extern "C" int tt_rows_max_clusters(int nx, int ny, int rank, int max_rows, int cluster, int* nclusters) {
+  if (!nclusters || nx < 1 || ny < 1 || rank < 1 || max_rows < 1 || cluster < 1)
+    return tt_fail(TT_EINVAL, "tt_rows_max_clusters: bad args");
+  RowsPlan pl;
+  int rc = rows_choose_cluster(nx, ny, rank, max_rows, cluster, &pl);
+  if (rc) return rc;
+  const int which = rows_which(rank, false, pl.tight);
+  if (which < 0) return tt_fail(TT_EUNSUPPORTED, "tt_rows_max_clusters: no kernel for this shape");
+  const RowsFn fn = rows_fns[which];
+  TT_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaFuncAttributes fa;
+  TT_CUDA_TRY(cudaFuncGetAttributes(&fa, fn));
+  if (fa.maxDynamicSharedSizeBytes < (int)pl.smem)  // only ever raised (the launch path caches the size it set)
+    TT_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(148 * pl.CL), 1, 1);
+  cfg.blockDim = dim3(ROWS_NT, 1, 1);
+  cfg.dynamicSmemBytes = (size_t)pl.smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)pl.CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  TT_CUDA_TRY(cudaOccupancyMaxActiveClusters(&n, fn, &cfg));
+  *nclusters = n;
+  return TT_OK;
+}
+
 extern "C" int tt_rows_plan(int nx, int ny, int rank, int max_rows, int policy, int* cluster, size_t* smem_bytes) {
   (void)policy;
   if (nx < 1 || ny < 1 || rank < 1 || max_rows < 1 || !cluster)
@@ -1715,23 +1764,12 @@ extern "C" int tt_track_rows(void* stream, const tt_rows_args* a) {
   if (rc) return rc;
   if (a->cluster > 0 && a->cluster != pl.CL) return tt_fail(TT_EINVAL, "cluster mismatch");
   // the instantiation: solver by Gauss-Jordan entries per thread, sharding phases only when sharded
-  typedef void (*RowsFn)(const tt_rows_args, const RowsPlan);
-  static const RowsFn fns[10] = {tt_rows_kernel<1, false>, tt_rows_kernel<2, false>, tt_rows_kernel<5, false>,
-                                 tt_rows_kernel<9, false>, tt_rows_kernel<1, true>,  tt_rows_kernel<2, true>,
-                                 tt_rows_kernel<5, true>,  tt_rows_kernel<9, true>,
-                                 tt_rows_kernel<5, false, true>, tt_rows_kernel<9, false, true>};
   static size_t configured_smem[10][TT_MAXDEV] = {{0}};
-  const int ept = gj_ept(a->rank, ROWS_NT);
-  const int solv = ept <= 1 ? 0 : ept <= 2 ? 1 : ept <= 5 ? 2 : 3;
-  int which = solv + (a->shard_world > 0 ? 4 : 0);
-  if (pl.tight) {
-    // the tight plan is needed only at large N x R (R = 64 at 1024^2); compiled for the two wide solvers
-    if (a->shard_world > 0 || solv < 2)
-      return tt_fail(TT_EUNSUPPORTED, "row-mask step (nx=%d R=%d rows=%d) needs the tight shared-memory plan, "
-                                      "which is not built for this solver / sharding", a->nx, a->rank, a->max_rows);
-    which = 8 + (solv - 2);
-  }
-  const RowsFn fn = fns[which];
+  const int which = rows_which(a->rank, a->shard_world > 0, pl.tight);
+  if (which < 0)
+    return tt_fail(TT_EUNSUPPORTED, "row-mask step (nx=%d R=%d rows=%d) needs the tight shared-memory plan, "
+                                    "which is not built for this solver / sharding", a->nx, a->rank, a->max_rows);
+  const RowsFn fn = rows_fns[which];
   {
     int dev = 0;
     TT_CUDA_TRY(cudaGetDevice(&dev));
