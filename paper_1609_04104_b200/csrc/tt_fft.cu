@@ -13,6 +13,9 @@
 // sign/normalisation convention.
 
 #include <math.h>
+#include <stdlib.h>
+
+#include <mutex>
 
 #include "tt_common.cuh"
 
@@ -24,7 +27,7 @@
 // conflicts). All of a thread's global loads are issued before the first shared-memory store.
 #define FFT_LU 8
 __global__ void __launch_bounds__(FFT_NT) fft_pow2_kernel(float2* __restrict__ data, int n, int logn, int ncols,
-                                                          int CB, int inverse) {
+                                                          int CB, int inverse, const float2* __restrict__ twg) {
   extern __shared__ __align__(16) unsigned char smem[];
   float2* buf0 = (float2*)smem;               // [n][CB]
   float2* buf1 = buf0 + (size_t)CB * n;       // [n][CB]
@@ -54,10 +57,14 @@ __global__ void __launch_bounds__(FFT_NT) fft_pow2_kernel(float2* __restrict__ d
       }
     }
   }
-  for (int m = tid; m < n; m += NT) {  // tw[m] = exp(+-2 pi i m / n); overlaps the loads in flight
-    double sv, cv;
-    sincospi(sgn * (double)m / (double)n, &sv, &cv);
-    tw[m] = make_float2((float)cv, (float)sv);
+  if (twg) {  // the cached table of this (n, direction): the same values, one 8-byte load per entry
+    for (int m = tid; m < n; m += NT) tw[m] = twg[m];
+  } else {
+    for (int m = tid; m < n; m += NT) {  // tw[m] = exp(+-2 pi i m / n); overlaps the loads in flight
+      double sv, cv;
+      sincospi(sgn * (double)m / (double)n, &sv, &cv);
+      tw[m] = make_float2((float)cv, (float)sv);
+    }
   }
   __syncthreads();
   float2* in = buf0;
@@ -112,6 +119,147 @@ __global__ void __launch_bounds__(FFT_NT) fft_pow2_kernel(float2* __restrict__ d
   }
 }
 
+// ---------------------------------------------------------------- two-level register FFT
+// n = N1 * N2 with N1, N2 in {8, 16, 32}: every thread transforms N1 (then N2) points in registers, so the
+// CTA's columns cross shared memory once (one barrier) instead of once per radix-4 pass, and the global
+// loads / stores go straight from / to registers as full row segments of CB columns:
+//   Y[j][k1] = sum_q x[j + N2 q] w_N1^(q k1)                (stage 1: N1 points over q, per j)
+//   X[k1 + N1 k2] = sum_j (w_n^(j k1) Y[j][k1]) w_N2^(j k2)  (stage 2: N2 points over j, per k1)
+__constant__ float2 c_w32[32];  // exp(-2 pi i k / 32), rounded from fp64
+
+template <int N>
+struct RegFFT {
+  // in-place natural-order DFT of x[0..N) (decimation in time, radix 2), forward sign; INV conjugates
+  template <bool INV>
+  static TT_DEV void run(float2 (&x)[N]) {
+    float2 e[N / 2], o[N / 2];
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) {
+      e[i] = x[2 * i];
+      o[i] = x[2 * i + 1];
+    }
+    RegFFT<N / 2>::template run<INV>(e);
+    RegFFT<N / 2>::template run<INV>(o);
+#pragma unroll
+    for (int k = 0; k < N / 2; ++k) {
+      float2 t;
+      if (k == 0) {
+        t = o[k];
+      } else if (4 * k == N) {  // w = -i (forward), +i (inverse)
+        t = INV ? make_float2(-o[k].y, o[k].x) : make_float2(o[k].y, -o[k].x);
+      } else {
+        float2 w = c_w32[k * (32 / N)];
+        if (INV) w.y = -w.y;
+        t = cmul(o[k], w);
+      }
+      x[k] = cadd(e[k], t);
+      x[k + N / 2] = csub(e[k], t);
+    }
+  }
+};
+template <>
+struct RegFFT<1> {
+  template <bool INV>
+  static TT_DEV void run(float2 (&)[1]) {}
+};
+
+template <int N1, int N2, int CB, bool INV>
+__global__ void __launch_bounds__(FFT_NT) fft_reg2_kernel(float2* __restrict__ data, int ncols,
+                                                          const float2* __restrict__ twg) {
+  constexpr int n = N1 * N2;
+  constexpr int KS = N2 * CB + CB;  // k1 stride: a warp's k1 groups land on distinct banks
+  extern __shared__ __align__(16) unsigned char smem[];
+  float2* ybuf = (float2*)smem;         // [N1][KS]
+  float2* tw = ybuf + (size_t)N1 * KS;  // [n]
+  const int tid = threadIdx.x;
+  const int col0 = blockIdx.x * CB;
+  const int cb = min(CB, ncols - col0);
+  float2* mat = data + (size_t)blockIdx.y * n * ncols + col0;
+  for (int m = tid; m < n; m += FFT_NT) tw[m] = twg[m];
+  // stage 1, item (j, c): N1 points over q from global memory, twiddled into the exchange buffer
+  auto load1 = [&](int it, float2 (&x)[N1]) {
+    const int j = it / CB, c = it % CB;
+    if (it < N2 * CB && c < cb) {
+#pragma unroll
+      for (int q = 0; q < N1; ++q) x[q] = mat[(size_t)(j + N2 * q) * ncols + c];
+      RegFFT<N1>::template run<INV>(x);
+    }
+  };
+  auto store1 = [&](int it, const float2 (&x)[N1]) {
+    const int j = it / CB, c = it % CB;
+    if (it < N2 * CB && c < cb) {
+#pragma unroll
+      for (int k1 = 0; k1 < N1; ++k1) ybuf[k1 * KS + j * CB + c] = k1 == 0 ? x[0] : cmul(x[k1], tw[j * k1]);
+    }
+  };
+  {
+    float2 x[N1];
+    load1(tid, x);
+    __syncthreads();  // the twiddle table; the first trip's loads and butterflies are ahead of it
+    store1(tid, x);
+    for (int it = tid + FFT_NT; it < N2 * CB; it += FFT_NT) {
+      load1(it, x);
+      store1(it, x);
+    }
+  }
+  __syncthreads();
+  const float scale = (float)(1.0 / sqrt((double)n));
+  // stage 2, item (k1, c): N2 points over j, rows k1 + N1 k2 back to global memory
+  for (int it = tid; it < N1 * CB; it += FFT_NT) {
+    const int k1 = it / CB, c = it % CB;
+    if (c >= cb) continue;
+    float2 y[N2];
+#pragma unroll
+    for (int j = 0; j < N2; ++j) y[j] = ybuf[k1 * KS + j * CB + c];
+    RegFFT<N2>::template run<INV>(y);
+#pragma unroll
+    for (int k2 = 0; k2 < N2; ++k2) mat[(size_t)(k1 + N1 * k2) * ncols + c] = cscale(y[k2], scale);
+  }
+}
+
+template <int N1, int N2, int CB>
+static cudaError_t fft_reg2_launch(cudaStream_t st, float2* data, int ncols, int batch, int inverse,
+                                   const float2* twg) {
+  constexpr size_t sm = ((size_t)N1 * (N2 * CB + CB) + (size_t)N1 * N2) * sizeof(float2);
+  static size_t cfg[2][TT_MAXDEV] = {{0}};
+  dim3 grid((ncols + CB - 1) / CB, batch);
+  if (inverse) {
+    cudaError_t e = tt_smem_attr((const void*)fft_reg2_kernel<N1, N2, CB, true>, sm, cfg[1]);
+    if (e != cudaSuccess) return e;
+    fft_reg2_kernel<N1, N2, CB, true><<<grid, FFT_NT, sm, st>>>(data, ncols, twg);
+  } else {
+    cudaError_t e = tt_smem_attr((const void*)fft_reg2_kernel<N1, N2, CB, false>, sm, cfg[0]);
+    if (e != cudaSuccess) return e;
+    fft_reg2_kernel<N1, N2, CB, false><<<grid, FFT_NT, sm, st>>>(data, ncols, twg);
+  }
+  return cudaGetLastError();
+}
+
+// exp(-2 pi i k / 32) into constant memory, once per device
+static bool fft_w32_ready() {
+  static bool done[TT_MAXDEV] = {false};
+  static std::mutex mu;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= TT_MAXDEV) return false;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done[dev]) return true;
+  float2 h[32];
+  for (int k = 0; k < 32; ++k) {
+    const double a = -2.0 * 3.14159265358979323846 * (double)k / 32.0;
+    h[k] = make_float2((float)cos(a), (float)sin(a));
+  }
+  h[0] = make_float2(1.f, 0.f);
+  h[8] = make_float2(0.f, -1.f);
+  h[16] = make_float2(-1.f, 0.f);
+  h[24] = make_float2(0.f, 1.f);
+  if (cudaMemcpyToSymbol(c_w32, h, sizeof(h)) != cudaSuccess) {  // synchronous; fails inside a stream capture
+    (void)cudaGetLastError();
+    return false;
+  }
+  done[dev] = true;
+  return true;
+}
+
 // Direct DFT for any n: each CTA handles CB columns of one matrix.
 __global__ void __launch_bounds__(FFT_NT) dft_direct_kernel(float2* __restrict__ data, int n, int ncols, int CB,
                                                             int inverse) {
@@ -149,6 +297,47 @@ __global__ void __launch_bounds__(FFT_NT) dft_direct_kernel(float2* __restrict__
   }
 }
 
+// exp(+-2 pi i m / n), m < n, rounded from fp64 (the values the kernel computes itself without a table)
+__global__ void fft_twiddle_kernel(float2* __restrict__ tw, int n, int inverse) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n) return;
+  double sv, cv;
+  sincospi((inverse ? 2.0 : -2.0) * (double)m / (double)n, &sv, &cv);
+  tw[m] = make_float2((float)cv, (float)sv);
+}
+
+// Twiddle table of (device, log2 n, direction), built once: the per-CTA fp64 sincospi of n values cost
+// more than the CTA's butterflies (each CTA transforms only CB <= 32 columns). Returns nullptr while the
+// stream is being captured into a graph and the table does not exist yet (the kernel then computes its own).
+static const float2* fft_twiddles(cudaStream_t st, int n, int logn, int inverse) {
+  static float2* tab[TT_MAXDEV][13][2] = {};
+  static std::mutex mu;
+  if (getenv("TT_FFT_NO_TABLE")) return nullptr;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= TT_MAXDEV || logn > 12) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  float2*& t = tab[dev][logn][inverse ? 1 : 0];
+  if (t) return t;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  float2* p = nullptr;
+  if (cudaMalloc(&p, (size_t)n * sizeof(float2)) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  fft_twiddle_kernel<<<(n + 255) / 256, 256, 0, st>>>(p, n, inverse);
+  if (cudaStreamSynchronize(st) != cudaSuccess) {  // complete before any other stream reads it
+    (void)cudaGetLastError();
+    cudaFree(p);
+    return nullptr;
+  }
+  t = p;
+  return t;
+}
+
 extern "C" int tt_fft_cols(void* stream, float* data, int n, int ncols, int batch, int inverse) {
   if (n < 1 || ncols < 1 || batch < 0 || !data) return tt_fail(TT_EINVAL, "tt_fft_cols: bad arguments");
   if (batch == 0) return TT_OK;
@@ -158,6 +347,19 @@ extern "C" int tt_fft_cols(void* stream, float* data, int n, int ncols, int batc
   if (pow2 && n >= 2 && n <= 4096) {
     int logn = 0;
     while ((1 << logn) < n) ++logn;
+    const float2* twg = fft_twiddles(st, n, logn, inverse);
+    if (twg && n >= 64 && n <= 1024 && !getenv("TT_FFT_STOCKHAM") && fft_w32_ready()) {
+      cudaError_t e = cudaSuccess;
+      switch (n) {
+        case 64: e = fft_reg2_launch<8, 8, 16>(st, (float2*)data, ncols, batch, inverse, twg); break;
+        case 128: e = fft_reg2_launch<8, 16, 16>(st, (float2*)data, ncols, batch, inverse, twg); break;
+        case 256: e = fft_reg2_launch<16, 16, 16>(st, (float2*)data, ncols, batch, inverse, twg); break;
+        case 512: e = fft_reg2_launch<16, 32, 16>(st, (float2*)data, ncols, batch, inverse, twg); break;
+        default: e = fft_reg2_launch<32, 32, 8>(st, (float2*)data, ncols, batch, inverse, twg); break;
+      }
+      TT_CUDA_TRY(e);
+      return TT_OK;
+    }
     // whole rows of up to 32 columns per CTA, at most ~96 KB so that two CTAs share an SM
     int CB = ncols < 32 ? ncols : 32;
     while (CB > 1 && (size_t)(2 * CB * n + n) * sizeof(float2) > 96 * 1024) CB = (CB + 1) / 2;
@@ -165,7 +367,7 @@ extern "C" int tt_fft_cols(void* stream, float* data, int n, int ncols, int batc
     static size_t cfg[TT_MAXDEV] = {0};
     TT_CUDA_TRY(tt_smem_attr((const void*)fft_pow2_kernel, sm, cfg));
     dim3 grid((ncols + CB - 1) / CB, batch);
-    fft_pow2_kernel<<<grid, FFT_NT, sm, st>>>((float2*)data, n, logn, ncols, CB, inverse);
+    fft_pow2_kernel<<<grid, FFT_NT, sm, st>>>((float2*)data, n, logn, ncols, CB, inverse, twg);
   } else if (n == 1) {
     return TT_OK;  // a length-1 ortho DFT is the identity
   } else {
