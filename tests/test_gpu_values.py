@@ -24,6 +24,31 @@ def test_fft_cols_matches_numpy(n, inverse):
     assert rel(got, want) < 2e-6
 
 
+@pytest.mark.parametrize("n", [64, 128, 256, 512, 1024])
+@pytest.mark.parametrize("ncols", [1, 16, 20, 37])
+def test_fft_register_kernel_matches_numpy_and_the_stockham_kernel(monkeypatch, n, ncols):
+    """The two-level register kernel (n = 64 ... 1024) on whole and ragged column blocks, both directions,
+    against numpy and against the shared-memory Stockham kernel it replaced (TT_FFT_STOCKHAM=1)."""
+    import torch
+
+    from paper_1609_04104_b200 import _ops as K
+
+    rng = np.random.default_rng(n + ncols)
+    x = (rng.standard_normal((2, n, ncols)) + 1j * rng.standard_normal((2, n, ncols))).astype(np.complex64)
+    xd = torch.from_numpy(x).cuda()
+    for inverse in (False, True):
+        monkeypatch.delenv("TT_FFT_STOCKHAM", raising=False)
+        got = K.fft_cols(xd, inverse).cpu().numpy()
+        monkeypatch.setenv("TT_FFT_STOCKHAM", "1")
+        old = K.fft_cols(xd, inverse).cpu().numpy()
+        want = np.stack([O.fft_cols(x[b], inverse) for b in range(2)])
+        assert rel(got, want) < 2e-6
+        assert rel(got, old) < 2e-6
+    monkeypatch.delenv("TT_FFT_STOCKHAM", raising=False)
+    back = K.fft_cols(K.fft_cols(xd, False), True).cpu().numpy()  # unitary round trip
+    assert rel(back, x) < 2e-6
+
+
 def test_dft2_delta_roundtrip_and_golden():
     import paper_1609_04104_b200 as tt
 
