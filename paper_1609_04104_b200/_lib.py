@@ -79,6 +79,7 @@ SIGNATURES = {
     "tt_version": (C.c_char_p, []),
     "tt_last_error": (C.c_char_p, []),
     "tt_fft_cols": (C.c_int, [_p, _p, C.c_int, C.c_int, C.c_int, C.c_int]),
+    "tt_fft_rows": (C.c_int, [_p, _p, C.c_longlong, C.c_int, C.c_int]),
     "tt_rows_plan": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int),
                                C.POINTER(C.c_size_t)]),
     "tt_rows_scratch_bytes": (C.c_size_t, [C.c_int] * 6),

@@ -45,6 +45,36 @@ def fft_cols(x: torch.Tensor, inverse: bool = False) -> torch.Tensor:
     return fft_cols_(x.clone(), inverse)
 
 
+FFT_ROWS_N = (64, 128, 256, 512, 1024)  # row lengths tt_fft_rows transforms (the register kernel's sizes)
+
+
+def fft_rows_(x: torch.Tensor, inverse: bool = False) -> torch.Tensor:
+    """In-place ortho DFT along the last axis of (..., n) complex64, n in FFT_ROWS_N."""
+    _need(x, C64, "x")
+    n = x.shape[-1]
+    if x.numel() == 0:
+        return x
+    L.check(L.lib().tt_fft_rows(L.stream_ptr(), x.data_ptr(), x.numel() // n, n, 1 if inverse else 0), "fft_rows")
+    return x
+
+
+def fft2_(x: torch.Tensor, inverse: bool = False) -> torch.Tensor:
+    """In-place unshifted ortho 2-D DFT of (..., nx, ny) complex64 frames (observation.py:171-183): a column
+    pass and a row pass over the same buffer; row lengths the row kernel does not take go through a
+    transposed copy and a second column pass."""
+    _need(x, C64, "x")
+    fft_cols_(x, inverse)
+    if x.shape[-1] in FFT_ROWS_N:
+        return fft_rows_(x, inverse)
+    xt = fft_cols_(x.transpose(-1, -2).contiguous(), inverse)
+    x.copy_(xt.transpose(-1, -2))
+    return x
+
+
+def fft2(x: torch.Tensor, inverse: bool = False) -> torch.Tensor:
+    return fft2_(x.clone(), inverse)
+
+
 class RowsScratch:
     """Cached scratch / plan for one (nslices, nx, ny, R, max_rows) shape."""
 

@@ -102,9 +102,8 @@ def project(frame, descriptor) -> np.ndarray:
     if isinstance(descriptor, EntryMask):
         y = _gather(x, descriptor.indices)
     elif isinstance(descriptor, FourierMask):
-        k = K.fft_cols(x.contiguous())                                   # F1 X
-        k = K.fft_cols(k.transpose(0, 1).contiguous()).transpose(0, 1)   # (F1 X) F2^T
-        y = _gather(k.contiguous(), descriptor.indices)
+        k = K.fft2(x.contiguous())                                       # F1 X F2^T
+        y = _gather(k, descriptor.indices)
     else:
         raise TypeError(f"unknown descriptor type {type(descriptor).__name__}")
     return y.cpu().numpy().astype(np.complex128)

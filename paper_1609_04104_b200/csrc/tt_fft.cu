@@ -235,6 +235,86 @@ static cudaError_t fft_reg2_launch(cudaStream_t st, float2* data, int ncols, int
   return cudaGetLastError();
 }
 
+// The same two-level transform along the LAST axis (rows of length n, in place): a CTA takes RB whole
+// rows; lanes run over j (stage 1 loads x[r][j + N2 q]) and over k1 (stage 2 stores X[r][k1 + N1 k2]), so
+// global accesses are contiguous runs of N2 / N1 elements. The exchange buffer is [r][j][k1] with an odd
+// j stride (N1 + 1): stage 1 writes it down the j of a half-warp, stage 2 reads it along k1, both
+// conflict-free for 8-byte elements. With tt_fft_cols this gives the 2-D transform without transposes.
+template <int N1, int N2, int RB, bool INV>
+__global__ void __launch_bounds__(FFT_NT) fft_reg2_rows_kernel(float2* __restrict__ data, long long nrows,
+                                                               const float2* __restrict__ twg) {
+  constexpr int n = N1 * N2;
+  constexpr int JS = N1 + 1;
+  constexpr int RS = N2 * JS + ((N1 == 8 && (N2 * JS) % 16 == 0) ? 8 : 0);
+  extern __shared__ __align__(16) unsigned char smem[];
+  float2* ybuf = (float2*)smem;         // [RB][RS]
+  float2* tw = ybuf + (size_t)RB * RS;  // [n]
+  const int tid = threadIdx.x;
+  const long long row0 = (long long)blockIdx.x * RB;
+  const int rb = (int)min((long long)RB, nrows - row0);
+  float2* mat = data + (size_t)row0 * n;
+  for (int m = tid; m < n; m += FFT_NT) tw[m] = twg[m];
+  auto load1 = [&](int it, float2 (&x)[N1]) {
+    const int r = it / N2, j = it % N2;
+    if (it < RB * N2 && r < rb) {
+#pragma unroll
+      for (int q = 0; q < N1; ++q) x[q] = mat[(size_t)r * n + j + N2 * q];
+      RegFFT<N1>::template run<INV>(x);
+    }
+  };
+  auto store1 = [&](int it, const float2 (&x)[N1]) {
+    const int r = it / N2, j = it % N2;
+    if (it < RB * N2 && r < rb) {
+#pragma unroll
+      for (int k1 = 0; k1 < N1; ++k1) ybuf[r * RS + j * JS + k1] = k1 == 0 ? x[0] : cmul(x[k1], tw[j * k1]);
+    }
+  };
+  {
+    float2 x[N1];
+    load1(tid, x);
+    __syncthreads();  // the twiddle table
+    store1(tid, x);
+    for (int it = tid + FFT_NT; it < RB * N2; it += FFT_NT) {
+      load1(it, x);
+      store1(it, x);
+    }
+  }
+  __syncthreads();
+  const float scale = (float)(1.0 / sqrt((double)n));
+  for (int it = tid; it < RB * N1; it += FFT_NT) {
+    const int r = it / N1, k1 = it % N1;
+    if (r >= rb) continue;
+    float2 y[N2];
+#pragma unroll
+    for (int j = 0; j < N2; ++j) y[j] = ybuf[r * RS + j * JS + k1];
+    RegFFT<N2>::template run<INV>(y);
+#pragma unroll
+    for (int k2 = 0; k2 < N2; ++k2) mat[(size_t)r * n + k1 + N1 * k2] = cscale(y[k2], scale);
+  }
+}
+
+template <int N1, int N2, int RB>
+static cudaError_t fft_reg2_rows_launch(cudaStream_t st, float2* data, long long nrows, int inverse,
+                                        const float2* twg) {
+  constexpr int JS = N1 + 1;
+  constexpr int RS = N2 * JS + ((N1 == 8 && (N2 * JS) % 16 == 0) ? 8 : 0);
+  constexpr size_t sm = ((size_t)RB * RS + (size_t)N1 * N2) * sizeof(float2);
+  static size_t cfg[2][TT_MAXDEV] = {{0}};
+  const long long nblk = (nrows + RB - 1) / RB;
+  if (nblk > 2147483647LL) return cudaErrorInvalidValue;
+  dim3 grid((unsigned)nblk, 1);
+  if (inverse) {
+    cudaError_t e = tt_smem_attr((const void*)fft_reg2_rows_kernel<N1, N2, RB, true>, sm, cfg[1]);
+    if (e != cudaSuccess) return e;
+    fft_reg2_rows_kernel<N1, N2, RB, true><<<grid, FFT_NT, sm, st>>>(data, nrows, twg);
+  } else {
+    cudaError_t e = tt_smem_attr((const void*)fft_reg2_rows_kernel<N1, N2, RB, false>, sm, cfg[0]);
+    if (e != cudaSuccess) return e;
+    fft_reg2_rows_kernel<N1, N2, RB, false><<<grid, FFT_NT, sm, st>>>(data, nrows, twg);
+  }
+  return cudaGetLastError();
+}
+
 // exp(-2 pi i k / 32) into constant memory, once per device
 static bool fft_w32_ready() {
   static bool done[TT_MAXDEV] = {false};
@@ -382,5 +462,30 @@ extern "C" int tt_fft_cols(void* stream, float* data, int n, int ncols, int batc
     dft_direct_kernel<<<grid, FFT_NT, sm, st>>>((float2*)data, n, ncols, CB, inverse);
   }
   TT_CUDA_TRY(cudaGetLastError());
+  return TT_OK;
+}
+
+// In-place ortho DFT along the last axis of nrows contiguous rows of n complex64 (n = 64, 128, 256, 512 or
+// 1024; other lengths: TT_EUNSUPPORTED, the host then transposes and uses tt_fft_cols).
+extern "C" int tt_fft_rows(void* stream, float* data, long long nrows, int n, int inverse) {
+  if (n < 1 || nrows < 0 || !data) return tt_fail(TT_EINVAL, "tt_fft_rows: bad arguments");
+  if (nrows == 0) return TT_OK;
+  if (n != 64 && n != 128 && n != 256 && n != 512 && n != 1024)
+    return tt_fail(TT_EUNSUPPORTED, "tt_fft_rows: n=%d (supported: 64, 128, 256, 512, 1024)", n);
+  cudaStream_t st = (cudaStream_t)stream;
+  int logn = 0;
+  while ((1 << logn) < n) ++logn;
+  const float2* twg = fft_twiddles(st, n, logn, inverse);
+  if (!twg || !fft_w32_ready())
+    return tt_fail(TT_EUNSUPPORTED, "tt_fft_rows: twiddle tables unavailable (first call inside a stream capture?)");
+  cudaError_t e = cudaSuccess;
+  switch (n) {
+    case 64: e = fft_reg2_rows_launch<8, 8, 32>(st, (float2*)data, nrows, inverse, twg); break;
+    case 128: e = fft_reg2_rows_launch<8, 16, 16>(st, (float2*)data, nrows, inverse, twg); break;
+    case 256: e = fft_reg2_rows_launch<16, 16, 16>(st, (float2*)data, nrows, inverse, twg); break;
+    case 512: e = fft_reg2_rows_launch<16, 32, 16>(st, (float2*)data, nrows, inverse, twg); break;
+    default: e = fft_reg2_rows_launch<32, 32, 8>(st, (float2*)data, nrows, inverse, twg); break;
+  }
+  TT_CUDA_TRY(e);
   return TT_OK;
 }

@@ -834,7 +834,7 @@ def run_online(kspace, A0, B0, lam, step, policy, clean=None, cluster=0, t0=1, w
     if clean is not None:
         cl = torch.as_tensor(np.asarray(clean, dtype=np.complex64)).to(dev).reshape(Ts * ns, nx, ny)
         if recon_domain == "kspace":  # F_x X F_y^T of the clean images (unitary: the same NMSE)
-            cl = K.fft_cols_(K.fft_cols_(cl.contiguous()).transpose(1, 2).contiguous()).transpose(1, 2)
+            cl = K.fft2_(cl.contiguous())
         nm = nmse_frames(cl.reshape(Ts * ns, nx * ny).contiguous(),
                          Xd.reshape(Ts * ns, nx * ny)).reshape(Ts, ns).cpu().numpy()  # metrics.py:53-62
     comp.synchronize()

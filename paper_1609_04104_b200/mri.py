@@ -39,8 +39,7 @@ def reconstruct_frame(subspace, gamma) -> FrameEstimate:
     if (g.size if isinstance(g, np.ndarray) else g.numel()) != subspace.rank:
         raise ValueError("gamma length does not match subspace rank")
     ks = synthesize_device(subspace, gamma)
-    img = K.fft_cols(ks, inverse=True)
-    img = K.fft_cols(img.transpose(0, 1).contiguous(), inverse=True).transpose(0, 1)
+    img = K.fft2(ks, inverse=True)
     return FrameEstimate(kspace=ks.cpu().numpy().astype(np.complex128),
                          image=img.abs().cpu().numpy().astype(np.float64))
 

@@ -161,15 +161,14 @@ class MeasurementBatch:
 
 # ------------------------------------------------------------------ DFT
 def unitary_dft2(image, inverse: bool = False) -> np.ndarray:
-    """Unitary 2-D DFT as two passes of the column FFT kernel (F1 X F2)."""
+    """Unitary 2-D DFT (F1 X F2^T): the column FFT kernel, then the row FFT kernel."""
     x = np.asarray(image, dtype=np.complex128) if not isinstance(image, torch.Tensor) else image
     if x.ndim != 2 or (x.size if isinstance(x, np.ndarray) else x.numel()) == 0:
         raise ValueError("unitary_dft2 expects a nonempty 2-D array")
     t = x.to(L.device(), torch.complex64) if isinstance(x, torch.Tensor) else \
         torch.from_numpy(x.astype(np.complex64)).to(L.device())
-    t = K.fft_cols(t.contiguous(), inverse)                       # F1 X
-    t = K.fft_cols(t.transpose(0, 1).contiguous(), inverse)       # (F1 X)^T F2^T ... columns of X^T
-    return t.transpose(0, 1).cpu().numpy().astype(np.complex128)
+    t = K.fft2(t.contiguous(), inverse)                           # F1 X F2^T: a column and a row pass
+    return t.cpu().numpy().astype(np.complex128)
 
 
 def unitary_dft_matrix(n: int) -> np.ndarray:

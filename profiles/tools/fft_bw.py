@@ -46,3 +46,37 @@ for shape in [(1600, 256, 256), (400, 512, 512), (100, 1024, 1024), (6400, 128, 
     ei = float((K.fft_cols(xi, inverse=True) - torch.fft.ifft(xi, dim=-2, norm="ortho")).abs().max())
     print(f"{shape}: register two-level {ms1:.3f} ms {bw1:.0f} GB/s (err {err1:.1e}) | Stockham radix-4 in smem "
           f"{ms0:.3f} ms {bw0:.0f} GB/s (err {err0:.1e}) | inverse, 37 columns: err {ei:.1e}")
+
+
+def timed(fn, x, reps=10):
+    for _ in range(3):
+        fn(x.clone())
+    ts = []
+    for _ in range(reps):
+        y = x.clone()
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn(y)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return sorted(ts)[len(ts) // 2], y
+
+
+def fft2_transposed(y):  # the 2-D transform before the row kernel: column pass, transposed copy, column pass
+    return K.fft_cols_(K.fft_cols_(y).transpose(1, 2).contiguous()).transpose(1, 2)
+
+
+print("rows / 2-D (in place; GB/s = one read + one write of the data per pass)")
+for shape in [(1600, 256, 256), (400, 512, 512), (100, 1024, 1024), (6400, 128, 128), (6400, 64, 64)]:
+    torch.manual_seed(2)
+    x = torch.randn(*shape, dtype=torch.complex64, device=dev)
+    nb = 2 * x.numel() * 8
+    ms_r, yr = timed(K.fft_rows_, x)
+    er = float((yr - torch.fft.fft(x, dim=-1, norm="ortho")).abs().max())
+    ms_2, y2 = timed(K.fft2_, x)
+    e2 = float((y2 - torch.fft.fft2(x, norm="ortho")).abs().max())
+    ms_t, _ = timed(fft2_transposed, x)
+    print(f"{shape}: rows {ms_r:.3f} ms {nb / ms_r / 1e6:.0f} GB/s (err {er:.1e}) | 2-D cols+rows {ms_2:.3f} ms "
+          f"{2 * nb / ms_2 / 1e6:.0f} GB/s (err {e2:.1e}) | 2-D by transposed copy {ms_t:.3f} ms")

@@ -49,6 +49,41 @@ def test_fft_register_kernel_matches_numpy_and_the_stockham_kernel(monkeypatch, 
     assert rel(back, x) < 2e-6
 
 
+@pytest.mark.parametrize("n", [64, 128, 256, 512, 1024])
+@pytest.mark.parametrize("lead", [(1,), (5,), (3, 37)])
+def test_fft_rows_matches_numpy(n, lead):
+    """The row transform (last axis, in place) on whole and ragged row blocks, both directions."""
+    import torch
+
+    from paper_1609_04104_b200 import _ops as K
+
+    rng = np.random.default_rng(n + len(lead))
+    x = (rng.standard_normal(lead + (n,)) + 1j * rng.standard_normal(lead + (n,))).astype(np.complex64)
+    for inverse in (False, True):
+        got = K.fft_rows_(torch.from_numpy(x).cuda(), inverse).cpu().numpy()
+        f = np.fft.ifft if inverse else np.fft.fft
+        assert rel(got, f(x.astype(np.complex128), axis=-1, norm="ortho")) < 2e-6
+    with pytest.raises(Exception):
+        K.fft_rows_(torch.zeros(4, 100, dtype=torch.complex64, device="cuda"))  # not a register-kernel length
+
+
+@pytest.mark.parametrize("shape", [(2, 256, 256), (3, 64, 128), (2, 100, 256), (2, 256, 100), (1, 1024, 512)])
+def test_fft2_matches_numpy(shape):
+    """2-D ortho DFT as a column pass and a row pass (no transposes when the row length is one of the row
+    kernel's; the transposed fallback otherwise), both directions and the round trip."""
+    import torch
+
+    from paper_1609_04104_b200 import _ops as K
+
+    rng = np.random.default_rng(sum(shape))
+    x = (rng.standard_normal(shape) + 1j * rng.standard_normal(shape)).astype(np.complex64)
+    xd = torch.from_numpy(x).cuda()
+    for inverse in (False, True):
+        f = np.fft.ifft2 if inverse else np.fft.fft2
+        assert rel(K.fft2(xd, inverse).cpu().numpy(), f(x.astype(np.complex128), norm="ortho")) < 3e-6
+    assert rel(K.fft2_(K.fft2(xd), inverse=True).cpu().numpy(), x) < 3e-6
+
+
 def test_dft2_delta_roundtrip_and_golden():
     import paper_1609_04104_b200 as tt
 
