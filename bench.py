@@ -1055,7 +1055,7 @@ def run_ours(args, cfg):
     # ---- quality (outside timing): NRMSE of the last step's reconstructions
     Xr = X.reshape(T, ns, n, n)
     cl = torch.from_numpy(clean_np).to(dev).reshape(T * ns, n, n)
-    cl = K.fft_cols_(K.fft_cols_(cl.contiguous()).transpose(1, 2).contiguous()).transpose(1, 2)  # F_x X F_y^T
+    cl = K.fft2_(cl.contiguous())  # F_x X F_y^T
     cl = cl.reshape(T, ns, n, n)
     nmse = ((cl - Xr).abs().pow(2).sum((-1, -2)) / cl.abs().pow(2).sum((-1, -2))).double()
     cnt = out["cnt"].double()
