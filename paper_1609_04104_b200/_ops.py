@@ -75,6 +75,19 @@ def fft2(x: torch.Tensor, inverse: bool = False) -> torch.Tensor:
     return fft2_(x.clone(), inverse)
 
 
+_MAX_CLUSTERS: dict = {}  # (device, nx, ny, rank, max_rows, cluster) -> resident clusters (the query takes ~1 ms)
+
+
+def _max_clusters(nx, ny, rank, max_rows, cluster) -> int:
+    key = (torch.cuda.current_device(), nx, ny, rank, max_rows, cluster)
+    n = _MAX_CLUSTERS.get(key)
+    if n is None:
+        out = C.c_int(0)
+        L.check(L.lib().tt_rows_max_clusters(nx, ny, rank, max_rows, cluster, C.byref(out)), "rows cluster occupancy")
+        n = _MAX_CLUSTERS[key] = out.value
+    return n
+
+
 class RowsScratch:
     """Cached scratch / plan for one (nslices, nx, ny, R, max_rows) shape."""
 
@@ -92,12 +105,8 @@ class RowsScratch:
                 t = C.c_int(c)
                 if L.lib().tt_rows_plan(nx, ny, rank, max_rows, policy, C.byref(t), C.byref(sm)) != 0:
                     continue
-                if c > 1:
-                    nmax = C.c_int(0)
-                    L.check(L.lib().tt_rows_max_clusters(nx, ny, rank, max_rows, c, C.byref(nmax)),
-                            "rows cluster occupancy")
-                    if nslices > nmax.value:
-                        continue
+                if c > 1 and nslices > _max_clusters(nx, ny, rank, max_rows, c):
+                    continue
                 cl = t
                 break
             if cl is None:
