@@ -6,11 +6,15 @@
 // ifft2(Xi) conj(B) = ifft_x(Xi conj(F_y B)), the 2-D inverse transform of
 // _scatter_theta (tracker.py:186-188): no 2-D FFT is ever formed.
 //
-// Power-of-two n: one CTA transforms CB columns of one matrix entirely in
-// shared memory with Stockham autosort passes (ping-pong buffers,
-// twiddles from an fp64 sincospi table; radix-4 passes plus one radix-2 pass for odd
-// log2 n). Other n: a direct DFT with the same
-// sign/normalisation convention.
+// n = 64 ... 1024 (powers of two): a two-level transform n = N1 * N2 with every
+// thread's N1 (then N2) points in registers and one exchange through shared
+// memory (fft_reg2_kernel down the columns, fft_reg2_rows_kernel along the
+// rows; HBM-bound). Other powers of two (and
+// TT_FFT_STOCKHAM=1): one CTA transforms CB columns of one matrix entirely in
+// shared memory with Stockham autosort passes (ping-pong buffers, radix-4
+// passes plus one radix-2 pass for odd log2 n). Other n: a direct DFT with the
+// same sign/normalisation convention. Twiddles are rounded from fp64 sincospi,
+// cached per (device, n, direction) (TT_FFT_NO_TABLE=1: computed in the kernel).
 
 #include <math.h>
 #include <stdlib.h>
