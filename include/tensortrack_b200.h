@@ -55,12 +55,12 @@ const char* tt_last_error(void);
  * norm="ortho")); inverse=1: F^-1. Replaces observation.py:225-226 (build_phi
  * Fourier branch) and the x/y inverse transforms inside _scatter_theta
  * (tracker.py:186-188) by the separable identity F(a b^T) = (F a)(F b)^T.
- * n = 64 ... 1024 (powers of two) use a two-level register transform (one
+ * n = 16 ... 1024 (powers of two) use a two-level register transform (one
  * shared-memory exchange), other powers of two <= 4096 shared-memory Stockham
  * passes; other n use a direct DFT (exact same convention). */
 int tt_fft_cols(void* stream, float* data, int n, int ncols, int batch, int inverse);
-/* The same ortho DFT along the LAST axis: `nrows` contiguous rows of n complex64, in place (n = 64, 128, 256,
- * 512 or 1024; other n: TT_EUNSUPPORTED). tt_fft_cols then tt_fft_rows over a batch of (nx x ny) frames is the
+/* The same ortho DFT along the LAST axis: `nrows` contiguous rows of n complex64, in place (n a power of two
+ * from 16 to 1024; other n: TT_EUNSUPPORTED). tt_fft_cols then tt_fft_rows over a batch of (nx x ny) frames is the
  * unshifted ortho 2-D DFT of observation.py:171-183 (np.fft.fft2(.., norm="ortho")) without transposes. */
 int tt_fft_rows(void* stream, float* data, long long nrows, int n, int inverse);
 

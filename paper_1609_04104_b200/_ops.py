@@ -45,7 +45,7 @@ def fft_cols(x: torch.Tensor, inverse: bool = False) -> torch.Tensor:
     return fft_cols_(x.clone(), inverse)
 
 
-FFT_ROWS_N = (64, 128, 256, 512, 1024)  # row lengths tt_fft_rows transforms (the register kernel's sizes)
+FFT_ROWS_N = (16, 32, 64, 128, 256, 512, 1024)  # row lengths tt_fft_rows transforms (the register kernel's sizes)
 
 
 def fft_rows_(x: torch.Tensor, inverse: bool = False) -> torch.Tensor:

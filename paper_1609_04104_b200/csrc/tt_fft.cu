@@ -6,7 +6,7 @@
 // ifft2(Xi) conj(B) = ifft_x(Xi conj(F_y B)), the 2-D inverse transform of
 // _scatter_theta (tracker.py:186-188): no 2-D FFT is ever formed.
 //
-// n = 64 ... 1024 (powers of two): a two-level transform n = N1 * N2 with every
+// n = 16 ... 1024 (powers of two): a two-level transform n = N1 * N2 with every
 // thread's N1 (then N2) points in registers and one exchange through shared
 // memory (fft_reg2_kernel down the columns, fft_reg2_rows_kernel along the
 // rows; HBM-bound). Other powers of two (and
@@ -432,9 +432,11 @@ extern "C" int tt_fft_cols(void* stream, float* data, int n, int ncols, int batc
     int logn = 0;
     while ((1 << logn) < n) ++logn;
     const float2* twg = fft_twiddles(st, n, logn, inverse);
-    if (twg && n >= 64 && n <= 1024 && !getenv("TT_FFT_STOCKHAM") && fft_w32_ready()) {
+    if (twg && n >= 16 && n <= 1024 && !getenv("TT_FFT_STOCKHAM") && fft_w32_ready()) {
       cudaError_t e = cudaSuccess;
       switch (n) {
+        case 16: e = fft_reg2_launch<4, 4, 16>(st, (float2*)data, ncols, batch, inverse, twg); break;
+        case 32: e = fft_reg2_launch<4, 8, 16>(st, (float2*)data, ncols, batch, inverse, twg); break;
         case 64: e = fft_reg2_launch<8, 8, 16>(st, (float2*)data, ncols, batch, inverse, twg); break;
         case 128: e = fft_reg2_launch<8, 16, 16>(st, (float2*)data, ncols, batch, inverse, twg); break;
         case 256: e = fft_reg2_launch<16, 16, 16>(st, (float2*)data, ncols, batch, inverse, twg); break;
@@ -474,8 +476,8 @@ extern "C" int tt_fft_cols(void* stream, float* data, int n, int ncols, int batc
 extern "C" int tt_fft_rows(void* stream, float* data, long long nrows, int n, int inverse) {
   if (n < 1 || nrows < 0 || !data) return tt_fail(TT_EINVAL, "tt_fft_rows: bad arguments");
   if (nrows == 0) return TT_OK;
-  if (n != 64 && n != 128 && n != 256 && n != 512 && n != 1024)
-    return tt_fail(TT_EUNSUPPORTED, "tt_fft_rows: n=%d (supported: 64, 128, 256, 512, 1024)", n);
+  if (n != 16 && n != 32 && n != 64 && n != 128 && n != 256 && n != 512 && n != 1024)
+    return tt_fail(TT_EUNSUPPORTED, "tt_fft_rows: n=%d (supported: powers of two from 16 to 1024)", n);
   cudaStream_t st = (cudaStream_t)stream;
   int logn = 0;
   while ((1 << logn) < n) ++logn;
@@ -484,6 +486,8 @@ extern "C" int tt_fft_rows(void* stream, float* data, long long nrows, int n, in
     return tt_fail(TT_EUNSUPPORTED, "tt_fft_rows: twiddle tables unavailable (first call inside a stream capture?)");
   cudaError_t e = cudaSuccess;
   switch (n) {
+    case 16: e = fft_reg2_rows_launch<4, 4, 64>(st, (float2*)data, nrows, inverse, twg); break;
+    case 32: e = fft_reg2_rows_launch<4, 8, 32>(st, (float2*)data, nrows, inverse, twg); break;
     case 64: e = fft_reg2_rows_launch<8, 8, 32>(st, (float2*)data, nrows, inverse, twg); break;
     case 128: e = fft_reg2_rows_launch<8, 16, 16>(st, (float2*)data, nrows, inverse, twg); break;
     case 256: e = fft_reg2_rows_launch<16, 16, 16>(st, (float2*)data, nrows, inverse, twg); break;

@@ -24,7 +24,7 @@ def test_fft_cols_matches_numpy(n, inverse):
     assert rel(got, want) < 2e-6
 
 
-@pytest.mark.parametrize("n", [64, 128, 256, 512, 1024])
+@pytest.mark.parametrize("n", [16, 32, 64, 128, 256, 512, 1024])
 @pytest.mark.parametrize("ncols", [1, 16, 20, 37])
 def test_fft_register_kernel_matches_numpy_and_the_stockham_kernel(monkeypatch, n, ncols):
     """The two-level register kernel (n = 64 ... 1024) on whole and ragged column blocks, both directions,
@@ -49,8 +49,8 @@ def test_fft_register_kernel_matches_numpy_and_the_stockham_kernel(monkeypatch, 
     assert rel(back, x) < 2e-6
 
 
-@pytest.mark.parametrize("n", [64, 128, 256, 512, 1024])
-@pytest.mark.parametrize("lead", [(1,), (5,), (3, 37)])
+@pytest.mark.parametrize("n", [16, 32, 64, 128, 256, 512, 1024])
+@pytest.mark.parametrize("lead", [(1,), (5,), (3, 37), (2, 70)])
 def test_fft_rows_matches_numpy(n, lead):
     """The row transform (last axis, in place) on whole and ragged row blocks, both directions."""
     import torch
@@ -67,7 +67,8 @@ def test_fft_rows_matches_numpy(n, lead):
         K.fft_rows_(torch.zeros(4, 100, dtype=torch.complex64, device="cuda"))  # not a register-kernel length
 
 
-@pytest.mark.parametrize("shape", [(2, 256, 256), (3, 64, 128), (2, 100, 256), (2, 256, 100), (1, 1024, 512)])
+@pytest.mark.parametrize("shape", [(2, 256, 256), (3, 64, 128), (2, 100, 256), (2, 256, 100), (1, 1024, 512),
+                                   (5, 32, 32), (4, 16, 32)])
 def test_fft2_matches_numpy(shape):
     """2-D ortho DFT as a column pass and a row pass (no transposes when the row length is one of the row
     kernel's; the transposed fallback otherwise), both directions and the round trip."""
